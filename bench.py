@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""Benchmark of the NAO grid pass (rho build + V_eff matrix elements H_ij).
+
+Metric (BASELINE.json): ms per SCF-iteration grid pass (rho + H_ij) on
+synthetic Fe3O4, plus the FP64 roofline fraction of the dominant kernel.
+A "step" = one density pass (DM -> rho) + one Hamiltonian pass (V_eff -> H,
+incl. the mirror and, for N > 1, the NCCL allreduce of H) over the whole
+grid. Default workload: the 56-atom conventional cell at 200 Ry (configs[1]).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl ours|reference]
+
+N > 1: launched by torch.distributed.run; the grid is split into contiguous
+cost-balanced block ranges (strong scaling); H partials are summed with
+torch.distributed.all_reduce (NCCL); time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "Fe3O4 grid pass (rho+H_ij) ms/SCF iter at 1/2/4/8 B200; % FP64/HBM roofline"
+L2_FLUSH_BYTES = 512 << 20  # > 126 MB L2
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--config", default="cubic56_200Ry")
+    p.add_argument("--nspin", type=int, default=1)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--warps", type=int, default=8)
+    p.add_argument("--profile", action="store_true", help="one warm pass only (for ncu)")
+    return p.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dgemm_peak_tflops(torch, dev):
+    """cuBLAS DGEMM 8192^3 (MEASURED_PEAKS.json has no FP64 entry)."""
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    torch.matmul(a, b)
+    torch.cuda.synchronize()
+    best = 1e30
+    for _ in range(3):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        torch.matmul(a, b)
+        e.record()
+        e.synchronize()
+        best = min(best, s.elapsed_time(e))
+    del a, b
+    return 2.0 * n ** 3 / (best * 1e-3) / 1e12
+
+
+def cpu_oracle_pass(f, oracle, dm, veff, threads, budget_s=20.0):
+    """Time the oracle on a bounded, cost-weighted sample of grid blocks and
+    extrapolate to ms per full pass. Returns (ms_per_pass, sample_desc)."""
+    ix = oracle.index
+    nblock = ix["nblock"]
+    cover = np.diff(ix["blk_ptr"]).astype(np.float64)
+    # probe: 2% of blocks from the middle of the grid
+    w = cover ** 2 + 1.0
+    pre = np.concatenate([[0.0], np.cumsum(w)])
+    total = pre[-1]
+
+    def run(b0, b1):
+        t = time.perf_counter()
+        oracle.density(dm, threads=threads, blocks=(b0, b1))
+        oracle.hamiltonian(veff, f.dV, threads=threads, blocks=(b0, b1))
+        return time.perf_counter() - t
+
+    mid = nblock // 2
+    b0 = mid
+    b1 = min(nblock, int(np.searchsorted(pre, pre[mid] + 0.02 * total)) + 1)
+    t = run(b0, b1)
+    frac = (pre[b1] - pre[b0]) / total
+    est_full = t / frac
+    if est_full <= budget_s:
+        t_full = run(0, nblock)
+        return t_full * 1e3, f"full pass, all {nblock} blocks"
+    # bounded sample sized to ~budget
+    want = budget_s / est_full
+    b0 = max(0, int(np.searchsorted(pre, pre[mid] - 0.5 * want * total)))
+    b1 = min(nblock, int(np.searchsorted(pre, pre[mid] + 0.5 * want * total)) + 1)
+    t = run(b0, b1)
+    frac = (pre[b1] - pre[b0]) / total
+    return t / frac * 1e3, (f"blocks [{b0},{b1}) of {nblock} (cost fraction {frac:.3f} by sum ncover^2), "
+                            f"extrapolated to the full pass")
+
+
+def run_reference(args):
+    """--impl reference: the CPU implementation of the path (oracle port; the
+    reference ships none) on all host threads, same metric/config."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle.oracle import Oracle
+    from paper_1402_4247_b200.system import Fe3O4
+
+    f = Fe3O4.config(args.config)
+    o = Oracle(f.system)
+    ix = o.build_index()
+    dm = f.dm(ix, nspin=args.nspin)
+    veff = f.veff(nspin=args.nspin)
+    threads = os.cpu_count() or 1
+    per = max(1.0, 150.0 / max(1, args.steps + args.warmup))
+    ms, sample = cpu_oracle_pass(f, o, dm, veff, threads, budget_s=per)
+    times = []
+    for _ in range(args.warmup):
+        cpu_oracle_pass(f, o, dm, veff, threads, budget_s=per)
+    for _ in range(args.steps):
+        m, sample = cpu_oracle_pass(f, o, dm, veff, threads, budget_s=per)
+        times.append(m)
+    v = float(np.mean(times)) if times else ms
+    line = {"metric": METRIC, "value": round(v, 4), "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(v, 4), "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic Fe3O4 (libkbgsynth, seed 1402)",
+            "config": {"workload": args.config, "nspin": args.nspin, "parallelism": "host threads"},
+            "impl": "reference",
+            "cpu_baseline": {"value": round(v, 4), "unit": "ms", "cores": threads, "kind": "port",
+                             "sample": sample + "; oracle/ C++ port (no reference implementation exists)"},
+            "e2e": {"value": round(v, 4), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1402_4247_b200.grid import GridPass
+    from paper_1402_4247_b200.system import Fe3O4
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    f = Fe3O4.config(args.config)
+    sysm = f.system
+    gp = GridPass(sysm, device=local, rank=rank, nranks=world)
+    gp.set_option(1, args.warps)
+    t_idx = time.perf_counter()
+    ix = gp.build_index()
+    t_idx = time.perf_counter() - t_idx
+    nspin = args.nspin
+    dm_h = f.dm(ix, nspin=nspin)
+    veff_h = f.veff(nspin=nspin)
+    nnz, npts = ix["nnz"], sysm.npts
+
+    stream = torch.cuda.current_stream()
+    d_dm = torch.from_numpy(dm_h).to(dev)
+    d_veff = torch.from_numpy(veff_h).to(dev)
+    d_rho = torch.empty((nspin, npts), dtype=torch.float64, device=dev)
+    d_h = torch.empty((nspin, nnz), dtype=torch.float64, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        gp.density_dev(d_dm, d_rho, stream)
+        if ev:
+            ev[1].record(stream)
+        gp.hamiltonian_accumulate_dev(d_veff, f.dV, d_h, stream)
+        if ev:
+            ev[2].record(stream)
+        gp.hamiltonian_mirror_dev(d_h, stream)
+        if ev:
+            ev[3].record(stream)
+        if world > 1:
+            dist.all_reduce(d_h)
+        if ev:
+            ev[4].record(stream)
+
+    if args.profile:
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        print(json.dumps({"profile": "done", "config": args.config}))
+        return
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    launches = 0
+    seg = np.zeros(4)
+    tot = []
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()  # L2 flush between timed iterations (outside the events)
+            step(evs[k])
+            launches += 3
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    for e in evs:
+        t = [e[i].elapsed_time(e[i + 1]) for i in range(4)]
+        seg += np.array(t)
+        tot.append(sum(t))
+    ms_local = float(np.mean(tot))
+    seg /= args.steps
+    if world > 1:
+        t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    else:
+        ms = ms_local
+
+    # e2e through the host-pointer C-ABI (kbg_density / kbg_hamiltonian), pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        p_dm = torch.from_numpy(dm_h).pin_memory()
+        p_veff = torch.from_numpy(veff_h).pin_memory()
+        p_rho = torch.empty((nspin, npts), dtype=torch.float64).pin_memory()
+        p_h = torch.empty((nspin, nnz), dtype=torch.float64).pin_memory()
+        lib = gp._lib
+        import ctypes as C
+
+        dp = C.POINTER(C.c_double)
+
+        def e2e_step():
+            st = lib.kbg_density(gp.handle, nspin, C.cast(p_dm.data_ptr(), dp), C.cast(p_rho.data_ptr(), dp))
+            st |= lib.kbg_hamiltonian(gp.handle, nspin, C.cast(p_veff.data_ptr(), dp), f.dV,
+                                      C.cast(p_h.data_ptr(), dp))
+            if world > 1:
+                t = p_h.to(dev, non_blocking=False)
+                dist.all_reduce(t)
+                p_h.copy_(t)
+            assert st == 0, gp._lib.kbg_last_error(gp.handle)
+
+        for _ in range(2):
+            e2e_step()
+        if world > 1:
+            dist.barrier()
+        tt = []
+        for _ in range(max(3, min(args.steps, 10))):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            e2e_step()
+            tt.append((time.perf_counter() - t0) * 1e3)
+        e_ms = float(np.mean(tt))
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        h2d = 8 * nspin * (nnz + npts) + (8 * nspin * nnz if world > 1 else 0)
+        d2h = 8 * nspin * (npts + nnz) + (8 * nspin * nnz if world > 1 else 0)
+        e2e = {"value": round(e_ms, 4), "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "api": "kbg_density + kbg_hamiltonian (host pointers, pinned)"}
+
+    # roofline of the dominant kernel (FP64 DMMA pipe)
+    peak = dgemm_peak_tflops(torch, dev) if rank == 0 else None
+    f_rho = nspin * (2.0 * ix["sum_m2"] + 2.0 * ix["sum_m"])
+    f_h = nspin * 2.0 * ix["sum_m2"]
+    if world > 1:
+        f_rho /= world  # per-rank share of the algorithmic work (cost-balanced shards)
+        f_h /= world
+    kern = {"density": (seg[0], f_rho), "hamiltonian_accumulate": (seg[1], f_h)}
+    dom = max(kern, key=lambda k: kern[k][0])
+    achieved = kern[dom][1] / (kern[dom][0] * 1e-3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(args.config, {}).get(dom)
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle.oracle import Oracle
+
+        o = Oracle(sysm)
+        o.build_index()
+        threads = os.cpu_count() or 1
+        cms, sample = cpu_oracle_pass(f, o, dm_h, veff_h, threads, budget_s=20.0)
+        cpu = {"value": round(cms, 3), "unit": "ms", "cores": threads, "kind": "port",
+               "sample": sample + f"; oracle/ C++ port, {threads} threads"}
+
+    if rank == 0:
+        total_f = nspin * (4.0 * ix["sum_m2"] + 2.0 * ix["sum_m"])
+        line = {
+            "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": round(ms, 4), "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic Fe3O4 (libkbgsynth, seed 1402; random DM / V_eff of the stated shape)",
+            "config": {"workload": args.config, "atoms": sysm.natom, "grid": list(sysm.grid), "nbasis": sysm.nbasis,
+                       "nspin": nspin, "pairs": int(len(ix["pair_a"])), "nnz": int(nnz),
+                       "parallelism": f"grid-sharded x{world}" if world > 1 else "1 GPU",
+                       "l2": "flushed (512 MB write) between timed steps, outside the events",
+                       "pass_gflop": round(total_f / 1e9, 3),
+                       "achieved_pass_tflops": round(total_f / (ms * 1e-3) / 1e12, 3)},
+            "segments_ms": {"density": round(seg[0], 4), "hamiltonian_accumulate": round(seg[1], 4),
+                            "mirror": round(seg[2], 4), "allreduce": round(seg[3], 4)},
+            "index_build_s": round(t_idx, 3),
+            "roofline": {"bound": "tensor", "kernel": dom, "achieved": round(achieved, 3),
+                         "peak": round(peak, 3) if peak else None, "unit": "TFLOP/s (FP64)",
+                         "frac": round(achieved / peak, 4) if peak else None, "traffic": traffic,
+                         "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (MEASURED_PEAKS.json has no "
+                                        "FP64 entry)",
+                         "flops_per_launch": kern[dom][1]},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

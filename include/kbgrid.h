@@ -1,0 +1,191 @@
+/*
+ * kbgrid.h -- C-ABI of the B200 NAO real-space grid pass (libkbgrid.so).
+ *
+ * The grid pass of an NAO-DFT SCF iteration:
+ *   (G1) index      : which (atom, lattice image) spheres cover which grid points,
+ *                     and the sparse atom-pair list (a, b, R) that carries DM and H;
+ *   (G2) orbitals   : phi_{a,l zeta m}(r) = u_{l zeta}(|r - t_a|) * P_lm(r - t_a)
+ *                     (u = radial table R(r)/r^l, P_lm = real solid harmonic);
+ *   (G3) density    : rho(r)  = sum_{ab} sum_ij phi_ai(r) DM_ab(R)_ij phi_bj(r);
+ *   (G4) hamiltonian: H_ab(R)_ij += sum_r phi_ai(r) V(r) dV phi_bj(r).
+ *
+ * Reference anchor.  arxiv/paper_1402_4247 ships no code for this path
+ * (/root/reference/SPEC.md:9 and :318 put it out of scope).
+ * The entry points below are what the reference's Band_DFT_Col pipeline would
+ * bind between Part 6 (density_matrices, producing
+ * DensityMatrices) and Part 1 (bloch_transform, SPEC.md:235-243,
+ * consuming RealSpaceOperator).  They follow the reference's
+ * conventions:
+ *   - status codes mirror the kband::Error taxonomy
+ *     (/root/reference/proj/include/kband/common.hpp:21-38);
+ *   - an optional work tally mirrors kband::WorkTally (common.hpp:43-56);
+ *   - errors carry a message naming the failing index, like
+ *     householder.cpp:119-123 / :312-316 (kbg_last_error).
+ *   - pure, reentrant operations on caller-owned buffers; one
+ *     host thread per context (ThreadTeam single-job rule, common.hpp:84-93).
+ *
+ * Conventions (shared bit-for-bit with the CPU oracle in oracle/):
+ *   lattice[3*i + c]  = Cartesian component c of lattice vector a_i (bohr).
+ *   grid point (i,j,k), 0 <= i < N0 ...; linear index p = (i*N1 + j)*N2 + k.
+ *   position r_c = (fi*A[0][c] + fj*A[1][c]) + fk*A[2][c], fi = (double)i/N0,
+ *   image centre t_c = tau_c + ((R0*A[0][c] + R1*A[1][c]) + R2*A[2][c]),
+ *   d = r - t,  d2 = (d0*d0 + d1*d1) + d2*d2 (no fused multiply-add),
+ *   sphere membership  d2 < rc*rc  (strict).
+ *   Pair (a, b, R) exists iff |t_b(R) - tau_a|^2 < (rc_a + rc_b)^2, same
+ *   expression order.  Pairs sorted lexicographically by (a, b, R0, R1, R2);
+ *   the block of pair p is n_a x n_b doubles, row-major, at pair_off[p].
+ *   Grid blocks are 4x4x4 points, block id = (bi*nb1 + bj)*nb2 + bk; within
+ *   a block point (li,lj,lk) has slot
+ *     ((((li>>1)*2 + (lj>>1))*2 + (lk>>1)) * 8) + ((li&1)*2 + (lj&1))*2 + (lk&1)
+ *   and bit `slot` of a cover mask is set iff that point lies in the sphere.
+ *   Orbital order inside an atom: species radial list order; within l:
+ *     s; p_x p_y p_z; d_z2, d_x2-y2, d_xy, d_xz, d_yz.
+ *   Radial table of (species, radial fn r): table[(r*ntab + k)*2 + {0,1}] =
+ *     (u(r_k), du/dr(r_k)), r_k = k*rc/(ntab-1), u = R(r)/r^l; cubic Hermite.
+ *   Spin-major arrays: dm/h [nspin][nnz], rho/veff [nspin][npts].
+ */
+#ifndef KBGRID_H
+#define KBGRID_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KBG_OK 0
+#define KBG_ERR_CONFIG 1      /* kband::ConfigError      */
+#define KBG_ERR_DIMENSION 2   /* kband::DimensionError   */
+#define KBG_ERR_CONSISTENCY 3 /* kband::ConsistencyError */
+#define KBG_ERR_NONFINITE 4   /* kband::ConvergenceError (non-finite values) */
+#define KBG_ERR_CUDA 5        /* CUDA runtime failure / no device */
+#define KBG_ERR_NCCL 6        /* collective failure (host-side reduction) */
+
+#define KBG_BLOCK_EDGE 4      /* grid block = 4x4x4 points = 64 slots */
+#define KBG_MAX_L 2           /* s, p, d */
+#define KBG_MAX_ORB_PER_ATOM 32
+
+typedef struct kbg_species {
+    int nrad;            /* number of radial functions                       */
+    const int* l;        /* [nrad] angular momentum, 0..KBG_MAX_L            */
+    double rc;           /* cutoff radius (bohr), > 0                        */
+    int ntab;            /* radial table points, >= 4                        */
+    const double* table; /* [nrad][ntab][2] (u, du/dr)                       */
+} kbg_species;
+
+typedef struct kbg_system {
+    double lattice[9];        /* rows = lattice vectors (bohr)                */
+    int grid[3];              /* N0, N1, N2                                   */
+    int natom;
+    const int* species;       /* [natom] species id                           */
+    const double* tau;        /* [natom*3] Cartesian positions (bohr)         */
+    int nspecies;
+    const kbg_species* spec;  /* [nspecies]                                   */
+} kbg_system;
+
+/* Host view of the integer index (bit-exact parity surface). Pointers are
+ * owned by the context and stay valid until the next kbg_build_index or
+ * kbg_destroy. */
+typedef struct kbg_index {
+    int64_t npts;
+    int nblk[3];
+    int64_t nblock;
+    int64_t ncover;
+    const int32_t* blk_ptr;   /* [nblock+1] CSR into the cover arrays         */
+    const int32_t* cov_atom;  /* [ncover]                                     */
+    const int32_t* cov_R;     /* [ncover*3] lattice image of the atom         */
+    const uint64_t* cov_mask; /* [ncover] slot mask                           */
+    int64_t npair;
+    const int32_t* pair_a;    /* [npair]                                      */
+    const int32_t* pair_b;    /* [npair]                                      */
+    const int32_t* pair_R;    /* [npair*3]                                    */
+    const int64_t* pair_off;  /* [npair+1] value offsets                      */
+    const int32_t* pair_mirror; /* [npair] index of (b, a, -R)                */
+    int64_t nnz;              /* pair_off[npair]                              */
+    int64_t nbpair;           /* canonical (block, cover-pair) work items     */
+    int64_t natompt;          /* sum of popcount(cov_mask)                    */
+    double sum_m;             /* sum_r m(r)   (m = nonzero orbitals at r)     */
+    double sum_m2;            /* sum_r m(r)^2                                 */
+} kbg_index;
+
+/* Work accounting (kband::WorkTally analogue): algorithmic flops and
+ * compulsory bytes of the last call, SURVEY.md section 8(d) formulas. */
+typedef struct kbg_tally {
+    double flops;
+    double bytes;
+} kbg_tally;
+
+typedef struct kbg_ctx kbg_ctx;
+
+/* Create a context on CUDA device `device`; copies the system (the caller's
+ * arrays may be freed afterwards). Validates the system (ConfigError /
+ * DimensionError with a message naming the bad field). */
+int kbg_create(const kbg_system* sys, int device, kbg_ctx** out);
+
+/* Sharded context for multi-GPU: this rank owns a contiguous, cost-balanced
+ * range of grid blocks. rho is produced for owned points only; H holds this
+ * rank's partial sums -- the caller sums it across ranks (ncclAllReduce,
+ * see INTEGRATION.md). */
+int kbg_create_sharded(const kbg_system* sys, int device, int rank, int nranks, kbg_ctx** out);
+
+/* Build the integer index on the device (once per geometry). */
+int kbg_build_index(kbg_ctx* ctx);
+
+/* Host copies of the index lists (for bit-exact parity and for callers that
+ * lay out DM / H in pair order). */
+int kbg_index_view(kbg_ctx* ctx, kbg_index* out);
+
+/* Owned block range [blk_begin, blk_end) of this context (sharded or not). */
+int kbg_shard_range(const kbg_ctx* ctx, int64_t* blk_begin, int64_t* blk_end);
+
+/* Host-pointer drop-in entry points: copies in, computes, copies out.
+ * dm: [nspin][nnz]; rho: [nspin][npts] (every point written; points outside
+ * this shard are written as 0 in a sharded context). DM must satisfy
+ * DM_ba(-R) = DM_ab(R)^T (DensityMatrices invariant); violations
+ * above 1e-13 * max|DM| return KBG_ERR_CONSISTENCY. */
+int kbg_density(kbg_ctx* ctx, int nspin, const double* dm, double* rho);
+/* veff: [nspin][npts]; h: [nspin][nnz], overwritten with sum_r phi V dV phi. */
+int kbg_hamiltonian(kbg_ctx* ctx, int nspin, const double* veff, double dV, double* h);
+
+/* Device-pointer variants (timing path). `stream` is a cudaStream_t (0 =
+ * legacy default). No host synchronisation, no validation. */
+int kbg_density_dev(kbg_ctx* ctx, int nspin, const double* d_dm, double* d_rho, void* stream);
+int kbg_hamiltonian_dev(kbg_ctx* ctx, int nspin, const double* d_veff, double dV, double* d_h,
+                        void* stream);
+
+/* Phase split of kbg_hamiltonian_dev for timing: accumulate canonical pair
+ * blocks (hot kernel), then mirror H_ba(-R) = H_ab(R)^T. */
+int kbg_hamiltonian_accumulate_dev(kbg_ctx* ctx, int nspin, const double* d_veff, double dV,
+                                   double* d_h, void* stream);
+int kbg_hamiltonian_mirror_dev(kbg_ctx* ctx, int nspin, double* d_h, void* stream);
+
+/* Orbital values phi on all grid points of one block, [ncover_blk][64] rows
+ * in cover order (testing surface for G2). out must hold M*64 doubles where
+ * M = total orbitals of the block's covers; *m_out receives M. */
+int kbg_block_orbitals(kbg_ctx* ctx, int64_t block, double* out, int64_t cap, int* m_out);
+
+/* Number of kernel launches made by the last kbg_density_dev /
+ * kbg_hamiltonian_dev call (evidence for gpu_launches). */
+int kbg_last_launches(const kbg_ctx* ctx);
+
+/* Work tally of the last density / hamiltonian call. */
+int kbg_last_tally(const kbg_ctx* ctx, kbg_tally* out);
+
+/* Options. KBG_OPT_WARPS: warps per CTA of the grid kernels (4 or 8). */
+#define KBG_OPT_WARPS 1
+#define KBG_OPT_FAULT_SIGN 2 /* test hook: flip the sign of the H accumulate (kband fault_proc6_sign analogue) */
+int kbg_set_option(kbg_ctx* ctx, int option, int64_t value);
+
+const char* kbg_last_error(const kbg_ctx* ctx);
+const char* kbg_status_string(int status);
+void kbg_destroy(kbg_ctx* ctx);
+
+/* Library identification: "kbgrid <version> sm_100a". */
+const char* kbg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KBGRID_H */

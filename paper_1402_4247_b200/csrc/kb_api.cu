@@ -1,0 +1,474 @@
+// C-ABI of libkbgrid (include/kbgrid.h): context, validation, host/device
+// entry points. Errors follow the kband taxonomy (common.hpp:21-38) as status
+// codes with a message naming the failing field (kbg_last_error).
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kb_device.cuh"
+
+struct kbg_ctx {
+    int device = 0;
+    int rank = 0, nranks = 1;
+    kbg::SysParams P{};
+    double* d_tau = nullptr;
+    int* d_spc = nullptr;
+    double* d_tables = nullptr;
+    kbg::DevIndex ix;
+    kbg::HostIndex hix;
+    bool built = false;
+    int64_t blk_begin = 0, blk_end = 0;
+    int nwarps = 8;
+    double sign = 1.0;
+    cudaStream_t stream = nullptr;
+    double* d_in = nullptr;
+    size_t cap_in = 0;
+    double* d_out = nullptr;
+    size_t cap_out = 0;
+    unsigned long long* d_check = nullptr;
+    int last_launches = 0;
+    kbg_tally tally{0, 0};
+    std::string err;
+    int64_t npts = 0;
+    std::vector<int> h_spc;
+};
+
+namespace {
+
+using kbg::Error;
+
+template <class F>
+int guard(kbg_ctx* ctx, F&& fn) {
+    try {
+        fn();
+        if (ctx) ctx->err.clear();
+        return KBG_OK;
+    } catch (const Error& e) {
+        if (ctx) ctx->err = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        if (ctx) ctx->err = e.what();
+        return KBG_ERR_CONSISTENCY;
+    }
+}
+
+void validate_and_load(kbg_ctx* c, const kbg_system& s) {
+    if (s.natom < 1) throw Error(KBG_ERR_CONFIG, "system: natom must be >= 1");
+    if (s.nspecies < 1 || !s.spec) throw Error(KBG_ERR_CONFIG, "system: no species");
+    if (s.nspecies > kbg::kMaxSpecies) throw Error(KBG_ERR_CONFIG, "system: too many species (max 8)");
+    if (!s.species || !s.tau) throw Error(KBG_ERR_CONFIG, "system: null species/tau");
+    for (int i = 0; i < 3; ++i)
+        if (s.grid[i] < 1) throw Error(KBG_ERR_DIMENSION, "system: grid[" + std::to_string(i) + "] < 1");
+    kbg::SysParams& P = c->P;
+    std::memcpy(P.A, s.lattice, sizeof(P.A));
+    const double* A = P.A;
+    const double det = A[0] * (A[4] * A[8] - A[5] * A[7]) - A[1] * (A[3] * A[8] - A[5] * A[6]) +
+                       A[2] * (A[3] * A[7] - A[4] * A[6]);
+    if (!(std::fabs(det) > 1e-12)) throw Error(KBG_ERR_CONFIG, "system: singular lattice");
+    P.Ainv[0] = (A[4] * A[8] - A[5] * A[7]) / det;
+    P.Ainv[1] = (A[2] * A[7] - A[1] * A[8]) / det;
+    P.Ainv[2] = (A[1] * A[5] - A[2] * A[4]) / det;
+    P.Ainv[3] = (A[5] * A[6] - A[3] * A[8]) / det;
+    P.Ainv[4] = (A[0] * A[8] - A[2] * A[6]) / det;
+    P.Ainv[5] = (A[2] * A[3] - A[0] * A[5]) / det;
+    P.Ainv[6] = (A[3] * A[7] - A[4] * A[6]) / det;
+    P.Ainv[7] = (A[1] * A[6] - A[0] * A[7]) / det;
+    P.Ainv[8] = (A[0] * A[4] - A[1] * A[3]) / det;
+    for (int i = 0; i < 3; ++i) {
+        P.N[i] = s.grid[i];
+        P.nblk[i] = (s.grid[i] + KBG_BLOCK_EDGE - 1) / KBG_BLOCK_EDGE;
+    }
+    P.natom = s.natom;
+    P.nspecies = s.nspecies;
+    std::vector<double> tables;
+    for (int t = 0; t < s.nspecies; ++t) {
+        const kbg_species& in = s.spec[t];
+        const std::string who = "species " + std::to_string(t);
+        if (in.nrad < 1 || !in.l || !in.table) throw Error(KBG_ERR_CONFIG, who + ": empty radial list");
+        if (in.nrad > kbg::kMaxRad) throw Error(KBG_ERR_CONFIG, who + ": too many radial functions");
+        if (!(in.rc > 0)) throw Error(KBG_ERR_CONFIG, who + ": rc <= 0");
+        if (in.ntab < 4) throw Error(KBG_ERR_CONFIG, who + ": ntab < 4");
+        kbg::DevSpecies& d = P.sp[t];
+        d.nrad = in.nrad;
+        d.ntab = in.ntab;
+        d.rc = in.rc;
+        d.rc2 = in.rc * in.rc;
+        d.h = in.rc / (in.ntab - 1);
+        d.inv_h = 1.0 / d.h;
+        d.norb = 0;
+        for (int r = 0; r < in.nrad; ++r) {
+            if (in.l[r] < 0 || in.l[r] > KBG_MAX_L) throw Error(KBG_ERR_CONFIG, who + ": l out of range");
+            d.l[r] = in.l[r];
+            d.norb += 2 * in.l[r] + 1;
+        }
+        if (d.norb > KBG_MAX_ORB_PER_ATOM) throw Error(KBG_ERR_CONFIG, who + ": too many orbitals");
+        d.tab_off = static_cast<long long>(tables.size());
+        const size_t n = static_cast<size_t>(in.nrad) * in.ntab * 2;
+        for (size_t i = 0; i < n; ++i) {
+            if (!std::isfinite(in.table[i])) throw Error(KBG_ERR_NONFINITE, who + ": non-finite radial table");
+            tables.push_back(in.table[i]);
+        }
+    }
+    for (int a = 0; a < s.natom; ++a) {
+        if (s.species[a] < 0 || s.species[a] >= s.nspecies)
+            throw Error(KBG_ERR_CONFIG, "atom " + std::to_string(a) + ": bad species id");
+        for (int q = 0; q < 3; ++q)
+            if (!std::isfinite(s.tau[3 * a + q]))
+                throw Error(KBG_ERR_NONFINITE, "atom " + std::to_string(a) + ": non-finite position");
+    }
+    c->npts = static_cast<int64_t>(s.grid[0]) * s.grid[1] * s.grid[2];
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        throw Error(KBG_ERR_CUDA, "no CUDA device available (libkbgrid has no CPU fallback)");
+    if (c->device < 0 || c->device >= ndev) throw Error(KBG_ERR_CUDA, "device index out of range");
+    KBG_CUDA(cudaSetDevice(c->device));
+    KBG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    KBG_CUDA(cudaMalloc(&c->d_tau, sizeof(double) * 3 * s.natom));
+    KBG_CUDA(cudaMalloc(&c->d_spc, sizeof(int) * s.natom));
+    KBG_CUDA(cudaMalloc(&c->d_tables, sizeof(double) * tables.size()));
+    KBG_CUDA(cudaMalloc(&c->d_check, sizeof(unsigned long long) * 4));
+    KBG_CUDA(cudaMemcpy(c->d_tau, s.tau, sizeof(double) * 3 * s.natom, cudaMemcpyHostToDevice));
+    KBG_CUDA(cudaMemcpy(c->d_spc, s.species, sizeof(int) * s.natom, cudaMemcpyHostToDevice));
+    KBG_CUDA(cudaMemcpy(c->d_tables, tables.data(), sizeof(double) * tables.size(), cudaMemcpyHostToDevice));
+    c->h_spc.assign(s.species, s.species + s.natom);
+    P.tau = c->d_tau;
+    P.spc = c->d_spc;
+    P.tables = c->d_tables;
+}
+
+void ensure(double*& buf, size_t& cap, size_t n) {
+    if (cap >= n) return;
+    if (buf) cudaFree(buf);
+    buf = nullptr;
+    KBG_CUDA(cudaMalloc(&buf, n * sizeof(double)));
+    cap = n;
+}
+
+void require_index(kbg_ctx* c) {
+    if (!c->built) throw Error(KBG_ERR_CONFIG, "index not built (call kbg_build_index first)");
+}
+
+void check_nspin(int nspin) {
+    if (nspin < 1 || nspin > 2) throw Error(KBG_ERR_CONFIG, "nspin must be 1 or 2");
+}
+
+kbg::GridArgs grid_args(kbg_ctx* c, int nspin, double dV, const double* in, double* out) {
+    kbg::GridArgs g{};
+    g.sys = c->P;
+    g.blk_ptr = c->ix.blk_ptr;
+    g.cov_atom = c->ix.cov_atom;
+    g.cov_R = c->ix.cov_R;
+    g.cov_mask = c->ix.cov_mask;
+    g.bp_ptr = c->ix.bp_ptr;
+    g.bp = c->ix.bp;
+    g.blk_begin = c->blk_begin;
+    g.max_rows = ((c->ix.max_rows + kbg::kRowPad + 7) / 8) * 8;
+    g.max_cover = c->ix.max_cover > 0 ? c->ix.max_cover : 1;
+    g.nspin = nspin;
+    g.nnz = c->ix.nnz;
+    g.npts = c->npts;
+    g.dV = dV;
+    g.sign = c->sign;
+    g.in = in;
+    g.out = out;
+    if (g.max_cover > 32 * c->nwarps)
+        throw Error(KBG_ERR_DIMENSION, "a grid block is covered by more atoms than threads per CTA");
+    const size_t smem = kbg::grid_smem_bytes(g.max_rows, g.max_cover, c->nwarps, true);
+    if (smem > 227 * 1024)
+        throw Error(KBG_ERR_DIMENSION, "grid block needs " + std::to_string(smem) +
+                                           " B of shared memory (> 227 KB): too many orbitals per block");
+    return g;
+}
+
+void shard(kbg_ctx* c) {
+    const int64_t nb = c->ix.nblock;
+    if (c->nranks == 1) {
+        c->blk_begin = 0;
+        c->blk_end = nb;
+        return;
+    }
+    std::vector<int64_t> cost(nb);
+    KBG_CUDA(cudaMemcpy(cost.data(), c->ix.blk_cost, nb * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    // Contiguous cost-balanced split; mirrors
+    // paper_1402_4247_b200/shard.py:partition (+1 per block so empty blocks count).
+    std::vector<long double> pre(nb + 1, 0);
+    for (int64_t b = 0; b < nb; ++b) pre[b + 1] = pre[b] + static_cast<long double>(cost[b] + 1);
+    auto bound = [&](int r) -> int64_t {
+        if (r <= 0) return 0;
+        if (r >= c->nranks) return nb;
+        const long double target = pre[nb] * r / c->nranks;
+        int64_t lo = 0, hi = nb;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) / 2;
+            if (pre[mid] < target)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        return lo;
+    };
+    c->blk_begin = bound(c->rank);
+    c->blk_end = bound(c->rank + 1);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* kbg_version(void) { return "kbgrid 0.1 sm_100a"; }
+
+const char* kbg_status_string(int status) {
+    switch (status) {
+        case KBG_OK: return "ok";
+        case KBG_ERR_CONFIG: return "config error";
+        case KBG_ERR_DIMENSION: return "dimension error";
+        case KBG_ERR_CONSISTENCY: return "consistency error";
+        case KBG_ERR_NONFINITE: return "non-finite value";
+        case KBG_ERR_CUDA: return "cuda error";
+        case KBG_ERR_NCCL: return "collective error";
+        default: return "unknown status";
+    }
+}
+
+int kbg_create_sharded(const kbg_system* sys, int device, int rank, int nranks, kbg_ctx** out) {
+    if (!out) return KBG_ERR_CONFIG;
+    *out = nullptr;
+    if (!sys) return KBG_ERR_CONFIG;
+    if (nranks < 1 || rank < 0 || rank >= nranks) return KBG_ERR_CONFIG;
+    auto* c = new kbg_ctx();
+    c->device = device;
+    c->rank = rank;
+    c->nranks = nranks;
+    const int st = guard(c, [&] { validate_and_load(c, *sys); });
+    if (st != KBG_OK) {
+        std::fprintf(stderr, "kbg_create: %s\n", c->err.c_str());
+        kbg_destroy(c);
+        return st;
+    }
+    *out = c;
+    return KBG_OK;
+}
+
+int kbg_create(const kbg_system* sys, int device, kbg_ctx** out) { return kbg_create_sharded(sys, device, 0, 1, out); }
+
+int kbg_build_index(kbg_ctx* c) {
+    if (!c) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        KBG_CUDA(cudaSetDevice(c->device));
+        c->built = false;
+        c->hix = kbg::HostIndex();
+        kbg::build_index_device(c->P, c->ix, c->stream);
+        shard(c);
+        c->built = true;
+    });
+}
+
+int kbg_index_view(kbg_ctx* c, kbg_index* out) {
+    if (!c || !out) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        require_index(c);
+        KBG_CUDA(cudaSetDevice(c->device));
+        if (!c->hix.valid) kbg::copy_index_to_host(c->ix, c->hix, c->stream);
+        std::memset(out, 0, sizeof(*out));
+        out->npts = c->npts;
+        for (int i = 0; i < 3; ++i) out->nblk[i] = c->P.nblk[i];
+        out->nblock = c->ix.nblock;
+        out->ncover = c->ix.ncover;
+        out->blk_ptr = c->hix.blk_ptr.data();
+        out->cov_atom = c->hix.cov_atom.data();
+        out->cov_R = c->hix.cov_R.data();
+        out->cov_mask = c->hix.cov_mask.data();
+        out->npair = c->ix.npair;
+        out->pair_a = c->hix.pair_a.data();
+        out->pair_b = c->hix.pair_b.data();
+        out->pair_R = c->hix.pair_R.data();
+        out->pair_off = c->hix.pair_off.data();
+        out->pair_mirror = c->hix.pair_mirror.data();
+        out->nnz = c->ix.nnz;
+        out->nbpair = c->ix.nbpair;
+        out->natompt = c->ix.natompt;
+        out->sum_m = c->ix.sum_m;
+        out->sum_m2 = c->ix.sum_m2;
+    });
+}
+
+int kbg_shard_range(const kbg_ctx* c, int64_t* b0, int64_t* b1) {
+    if (!c || !b0 || !b1) return KBG_ERR_CONFIG;
+    if (!c->built) return KBG_ERR_CONFIG;
+    *b0 = c->blk_begin;
+    *b1 = c->blk_end;
+    return KBG_OK;
+}
+
+int kbg_density_dev(kbg_ctx* c, int nspin, const double* d_dm, double* d_rho, void* stream) {
+    if (!c || !d_dm || !d_rho) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        check_nspin(nspin);
+        require_index(c);
+        KBG_CUDA(cudaSetDevice(c->device));
+        const kbg::GridArgs g = grid_args(c, nspin, 0.0, d_dm, d_rho);
+        c->last_launches = kbg::launch_density(g, c->blk_end - c->blk_begin, c->nwarps,
+                                               static_cast<cudaStream_t>(stream));
+        c->tally.flops = nspin * (2.0 * c->ix.sum_m2 + 2.0 * c->ix.sum_m);
+        c->tally.bytes = 8.0 * nspin * (c->ix.nnz + c->npts);
+    });
+}
+
+int kbg_hamiltonian_accumulate_dev(kbg_ctx* c, int nspin, const double* d_veff, double dV, double* d_h,
+                                   void* stream) {
+    if (!c || !d_veff || !d_h) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        check_nspin(nspin);
+        require_index(c);
+        KBG_CUDA(cudaSetDevice(c->device));
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        KBG_CUDA(cudaMemsetAsync(d_h, 0, sizeof(double) * nspin * c->ix.nnz, st));
+        const kbg::GridArgs g = grid_args(c, nspin, dV, d_veff, d_h);
+        c->last_launches = kbg::launch_hamiltonian(g, c->blk_end - c->blk_begin, c->nwarps, st);
+        c->tally.flops = nspin * 2.0 * c->ix.sum_m2;
+        c->tally.bytes = 8.0 * nspin * (c->ix.nnz + c->npts);
+    });
+}
+
+int kbg_hamiltonian_mirror_dev(kbg_ctx* c, int nspin, double* d_h, void* stream) {
+    if (!c || !d_h) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        check_nspin(nspin);
+        require_index(c);
+        KBG_CUDA(cudaSetDevice(c->device));
+        c->last_launches = kbg::launch_mirror(c->ix, c->P, nspin, d_h, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int kbg_hamiltonian_dev(kbg_ctx* c, int nspin, const double* d_veff, double dV, double* d_h, void* stream) {
+    int st = kbg_hamiltonian_accumulate_dev(c, nspin, d_veff, dV, d_h, stream);
+    if (st != KBG_OK) return st;
+    const int n1 = c->last_launches;
+    const kbg_tally t = c->tally;
+    st = kbg_hamiltonian_mirror_dev(c, nspin, d_h, stream);
+    if (st != KBG_OK) return st;
+    c->last_launches += n1;
+    c->tally = t;
+    return KBG_OK;
+}
+
+int kbg_density(kbg_ctx* c, int nspin, const double* dm, double* rho) {
+    if (!c || !dm || !rho) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        check_nspin(nspin);
+        require_index(c);
+        KBG_CUDA(cudaSetDevice(c->device));
+        const size_t nin = static_cast<size_t>(nspin) * c->ix.nnz, nout = static_cast<size_t>(nspin) * c->npts;
+        ensure(c->d_in, c->cap_in, nin);
+        ensure(c->d_out, c->cap_out, nout);
+        KBG_CUDA(cudaMemcpyAsync(c->d_in, dm, nin * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        KBG_CUDA(cudaMemsetAsync(c->d_check, 0, 4 * sizeof(unsigned long long), c->stream));
+        kbg::launch_dm_check(c->ix, c->P, nspin, c->d_in, c->d_check, c->stream);
+        unsigned long long chk[4];
+        KBG_CUDA(cudaMemcpyAsync(chk, c->d_check, sizeof(chk), cudaMemcpyDeviceToHost, c->stream));
+        KBG_CUDA(cudaStreamSynchronize(c->stream));
+        double dmax, amax;
+        std::memcpy(&dmax, &chk[0], 8);
+        std::memcpy(&amax, &chk[1], 8);
+        if (chk[2]) throw Error(KBG_ERR_NONFINITE, "density: non-finite density-matrix entry");
+        if (dmax > 1e-13 * amax)
+            throw Error(KBG_ERR_CONSISTENCY, "density: DM violates DM_ba(-R) = DM_ab(R)^T by " + std::to_string(dmax));
+        if (c->nranks > 1) KBG_CUDA(cudaMemsetAsync(c->d_out, 0, nout * sizeof(double), c->stream));
+        const kbg::GridArgs g = grid_args(c, nspin, 0.0, c->d_in, c->d_out);
+        c->last_launches = 1 + kbg::launch_density(g, c->blk_end - c->blk_begin, c->nwarps, c->stream);
+        KBG_CUDA(cudaMemcpyAsync(rho, c->d_out, nout * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        KBG_CUDA(cudaStreamSynchronize(c->stream));
+        c->tally.flops = nspin * (2.0 * c->ix.sum_m2 + 2.0 * c->ix.sum_m);
+        c->tally.bytes = 8.0 * nspin * (c->ix.nnz + c->npts);
+    });
+}
+
+int kbg_hamiltonian(kbg_ctx* c, int nspin, const double* veff, double dV, double* h) {
+    if (!c || !veff || !h) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        check_nspin(nspin);
+        require_index(c);
+        if (!std::isfinite(dV)) throw Error(KBG_ERR_NONFINITE, "hamiltonian: non-finite dV");
+        KBG_CUDA(cudaSetDevice(c->device));
+        const size_t nin = static_cast<size_t>(nspin) * c->npts, nout = static_cast<size_t>(nspin) * c->ix.nnz;
+        ensure(c->d_in, c->cap_in, nin);
+        ensure(c->d_out, c->cap_out, nout);
+        KBG_CUDA(cudaMemcpyAsync(c->d_in, veff, nin * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        KBG_CUDA(cudaMemsetAsync(c->d_out, 0, nout * sizeof(double), c->stream));
+        const kbg::GridArgs g = grid_args(c, nspin, dV, c->d_in, c->d_out);
+        int n = kbg::launch_hamiltonian(g, c->blk_end - c->blk_begin, c->nwarps, c->stream);
+        n += kbg::launch_mirror(c->ix, c->P, nspin, c->d_out, c->stream);
+        c->last_launches = n;
+        KBG_CUDA(cudaMemcpyAsync(h, c->d_out, nout * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        KBG_CUDA(cudaStreamSynchronize(c->stream));
+        c->tally.flops = nspin * 2.0 * c->ix.sum_m2;
+        c->tally.bytes = 8.0 * nspin * (c->ix.nnz + c->npts);
+    });
+}
+
+int kbg_block_orbitals(kbg_ctx* c, int64_t block, double* out, int64_t cap, int* m_out) {
+    if (!c || !out || !m_out) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        require_index(c);
+        if (block < 0 || block >= c->ix.nblock) throw Error(KBG_ERR_DIMENSION, "block_orbitals: bad block");
+        KBG_CUDA(cudaSetDevice(c->device));
+        if (!c->hix.valid) kbg::copy_index_to_host(c->ix, c->hix, c->stream);
+        int M = 0;
+        for (int e = c->hix.blk_ptr[block]; e < c->hix.blk_ptr[block + 1]; ++e)
+            M += c->P.sp[c->h_spc[c->hix.cov_atom[e]]].norb;
+        *m_out = M;
+        if (static_cast<int64_t>(M) * 64 > cap) throw Error(KBG_ERR_DIMENSION, "block_orbitals: cap too small");
+        if (M == 0) return;
+        ensure(c->d_out, c->cap_out, static_cast<size_t>(M) * 64);
+        const kbg::GridArgs g = grid_args(c, 1, 0.0, nullptr, nullptr);
+        kbg::launch_block_orbitals(g, block, c->d_out, c->stream);
+        KBG_CUDA(cudaMemcpyAsync(out, c->d_out, sizeof(double) * M * 64, cudaMemcpyDeviceToHost, c->stream));
+        KBG_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int kbg_last_launches(const kbg_ctx* c) { return c ? c->last_launches : 0; }
+
+int kbg_last_tally(const kbg_ctx* c, kbg_tally* out) {
+    if (!c || !out) return KBG_ERR_CONFIG;
+    *out = c->tally;
+    return KBG_OK;
+}
+
+int kbg_set_option(kbg_ctx* c, int option, int64_t value) {
+    if (!c) return KBG_ERR_CONFIG;
+    switch (option) {
+        case KBG_OPT_WARPS:
+            if (value != 4 && value != 8) {
+                c->err = "set_option: warps must be 4 or 8";
+                return KBG_ERR_CONFIG;
+            }
+            c->nwarps = static_cast<int>(value);
+            return KBG_OK;
+        case KBG_OPT_FAULT_SIGN:
+            c->sign = value ? -1.0 : 1.0;
+            return KBG_OK;
+        default:
+            c->err = "set_option: unknown option";
+            return KBG_ERR_CONFIG;
+    }
+}
+
+const char* kbg_last_error(const kbg_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+void kbg_destroy(kbg_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    kbg::free_index(c->ix);
+    if (c->d_tau) cudaFree(c->d_tau);
+    if (c->d_spc) cudaFree(c->d_spc);
+    if (c->d_tables) cudaFree(c->d_tables);
+    if (c->d_in) cudaFree(c->d_in);
+    if (c->d_out) cudaFree(c->d_out);
+    if (c->d_check) cudaFree(c->d_check);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,116 @@
+// Device helpers shared by the index build and the grid kernels.
+#pragma once
+
+#include "kb_internal.cuh"
+
+namespace kbg {
+
+// Real-solid-harmonic constants (same literals as the oracle).
+constexpr double kC00 = 0.28209479177387814;  // 1/(2 sqrt(pi))
+constexpr double kC1 = 0.4886025119029199;    // sqrt(3/(4 pi))
+constexpr double kC20 = 0.31539156525252005;  // sqrt(5/(16 pi))
+constexpr double kC22 = 0.5462742152960396;   // sqrt(15/(16 pi))
+constexpr double kC2 = 1.0925484305920792;    // sqrt(15/(4 pi))
+
+// Slot (0..63) -> block-local (li, lj, lk). Octet o = slot>>3 is a 2x2x2 cube,
+// quad q = slot>>2 a 1x2x2 square (include/kbgrid.h).
+__device__ __forceinline__ void slot_decode(int s, int& li, int& lj, int& lk) {
+    const int o = s >> 3, w = s & 7;
+    li = ((o >> 2) & 1) * 2 + ((w >> 2) & 1);
+    lj = ((o >> 1) & 1) * 2 + ((w >> 1) & 1);
+    lk = (o & 1) * 2 + (w & 1);
+}
+
+// Exact-rounding expressions of include/kbgrid.h (no contraction).
+__device__ __forceinline__ void point_pos_exact(const SysParams& P, int i, int j, int k, double r[3]) {
+    const double fi = __ddiv_rn(static_cast<double>(i), static_cast<double>(P.N[0]));
+    const double fj = __ddiv_rn(static_cast<double>(j), static_cast<double>(P.N[1]));
+    const double fk = __ddiv_rn(static_cast<double>(k), static_cast<double>(P.N[2]));
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        r[c] = __dadd_rn(__dadd_rn(__dmul_rn(fi, P.A[c]), __dmul_rn(fj, P.A[3 + c])), __dmul_rn(fk, P.A[6 + c]));
+}
+
+__device__ __forceinline__ void image_pos_exact(const SysParams& P, const double* tau, int R0, int R1, int R2,
+                                                double t[3]) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        t[c] = __dadd_rn(tau[c], __dadd_rn(__dadd_rn(__dmul_rn(static_cast<double>(R0), P.A[c]),
+                                                     __dmul_rn(static_cast<double>(R1), P.A[3 + c])),
+                                           __dmul_rn(static_cast<double>(R2), P.A[6 + c])));
+}
+
+__device__ __forceinline__ double dist2_exact(const double d[3]) {
+    return __dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])), __dmul_rn(d[2], d[2]));
+}
+
+// Orbitals of one atom at displacement d (inside the sphere): out[norb].
+// Cubic Hermite on the uniform radial table times real solid harmonics.
+template <class Sink>
+__device__ __forceinline__ void eval_orbitals(const DevSpecies& sp, const double* __restrict__ tables, double dx,
+                                              double dy, double dz, double d2, Sink&& sink) {
+    const double r = sqrt(d2);
+    const double x = r * sp.inv_h;
+    int k = static_cast<int>(x);
+    if (k > sp.ntab - 2) k = sp.ntab - 2;
+    const double t = x - k;
+    const double omt = 1.0 - t;
+    const double h00 = (1.0 + 2.0 * t) * omt * omt;
+    const double h10 = t * omt * omt * sp.h;
+    const double h01 = t * t * (3.0 - 2.0 * t);
+    const double h11 = t * t * (t - 1.0) * sp.h;
+    const double* tab = tables + sp.tab_off + 2 * k;
+    int o = 0;
+    for (int rad = 0; rad < sp.nrad; ++rad) {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(tab + static_cast<long long>(rad) * sp.ntab * 2));
+        const double2 b = __ldg(reinterpret_cast<const double2*>(tab + static_cast<long long>(rad) * sp.ntab * 2 + 2));
+        const double u = h00 * a.x + h10 * a.y + h01 * b.x + h11 * b.y;
+        const int l = sp.l[rad];
+        if (l == 0) {
+            sink(o++, kC00 * u);
+        } else if (l == 1) {
+            const double cu = kC1 * u;
+            sink(o++, cu * dx);
+            sink(o++, cu * dy);
+            sink(o++, cu * dz);
+        } else {
+            sink(o++, kC20 * (2.0 * dz * dz - dx * dx - dy * dy) * u);
+            sink(o++, kC22 * (dx * dx - dy * dy) * u);
+            const double cu = kC2 * u;
+            sink(o++, cu * dx * dy);
+            sink(o++, cu * dx * dz);
+            sink(o++, cu * dy * dz);
+        }
+    }
+}
+
+__device__ __forceinline__ int64_t block_id(const SysParams& P, int bi, int bj, int bk) {
+    return (static_cast<int64_t>(bi) * P.nblk[1] + bj) * P.nblk[2] + bk;
+}
+
+__device__ __forceinline__ void block_decode(const SysParams& P, int64_t b, int& bi, int& bj, int& bk) {
+    bk = static_cast<int>(b % P.nblk[2]);
+    const int64_t t = b / P.nblk[2];
+    bj = static_cast<int>(t % P.nblk[1]);
+    bi = static_cast<int>(t / P.nblk[1]);
+}
+
+// Lexicographic pair key (a, b, R0, R1, R2); |R_c| < 512, natom^2 < 2^33.
+__host__ __device__ __forceinline__ int64_t pair_key(int a, int b, int R0, int R1, int R2, int natom) {
+    return ((static_cast<int64_t>(a) * natom + b) << 30) | (static_cast<int64_t>(R0 + 512) << 20) |
+           (static_cast<int64_t>(R1 + 512) << 10) | static_cast<int64_t>(R2 + 512);
+}
+
+__device__ __forceinline__ int64_t find_pair(const int64_t* __restrict__ keys, int64_t n, int64_t key) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (keys[mid] < key)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return (lo < n && keys[lo] == key) ? lo : -1;
+}
+
+}  // namespace kbg

@@ -1,0 +1,138 @@
+// Internal declarations of libkbgrid (not part of the C-ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kbgrid.h"
+
+namespace kbg {
+
+constexpr int kMaxSpecies = 8;
+constexpr int kMaxRad = 16;
+constexpr int kPhiStride = 68;  // doubles per Phi row: 64 slots + 4 pad (bank-conflict-free DMMA fragments)
+constexpr int kRowPad = 16;     // zeroed rows after the last orbital (tile overrun)
+
+// Error taxonomy of kband (common.hpp:21-38) carried as a status code.
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define KBG_CUDA(call)                                                                        \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            throw ::kbg::Error(KBG_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+struct DevSpecies {
+    int nrad;
+    int norb;
+    int ntab;
+    int pad_;
+    double rc;
+    double rc2;     // rc*rc (host-rounded, identical to the oracle's)
+    double h;       // rc / (ntab-1)
+    double inv_h;
+    int l[kMaxRad];
+    long long tab_off;  // offset (doubles) of this species' table in the table array
+};
+
+struct SysParams {
+    double A[9];
+    double Ainv[9];
+    int N[3];
+    int nblk[3];
+    int natom;
+    int nspecies;
+    const double* tau;    // [natom*3]
+    const int* spc;       // [natom]
+    const double* tables; // concatenated radial tables
+    DevSpecies sp[kMaxSpecies];
+};
+
+// One canonical work item of a grid block: covers (ci <= cj, block-local),
+// value offset of the pair block (a_ci, a_cj, R_cj - R_ci).
+struct BPair {
+    int32_t cicj;  // ci | (cj << 16)
+    int32_t cost;  // n_a * n_b * |mask_ci & mask_cj|
+    int64_t off;
+};
+
+struct Candidate {
+    int32_t atom;
+    int32_t R[3];
+    int32_t lo[3];
+    int32_t hi[3];
+};
+
+// Device-resident index.
+struct DevIndex {
+    int64_t nblock = 0, ncover = 0, npair = 0, nnz = 0, nbpair = 0;
+    int32_t* blk_ptr = nullptr;
+    int32_t* cov_atom = nullptr;
+    int32_t* cov_R = nullptr;
+    uint64_t* cov_mask = nullptr;
+    int32_t* pair_a = nullptr;
+    int32_t* pair_b = nullptr;
+    int32_t* pair_R = nullptr;
+    int64_t* pair_off = nullptr;
+    int64_t* pair_key = nullptr;
+    int32_t* pair_mirror = nullptr;
+    int64_t* bp_ptr = nullptr;
+    BPair* bp = nullptr;
+    int64_t* blk_cost = nullptr;
+    int max_rows = 0;    // max orbitals covering one block
+    int max_cover = 0;   // max covers per block
+    int64_t natompt = 0;
+    double sum_m = 0, sum_m2 = 0;
+};
+
+// Host copies for kbg_index_view.
+struct HostIndex {
+    std::vector<int32_t> blk_ptr, cov_atom, cov_R, pair_a, pair_b, pair_R, pair_mirror;
+    std::vector<uint64_t> cov_mask;
+    std::vector<int64_t> pair_off;
+    bool valid = false;
+};
+
+struct GridArgs {
+    SysParams sys;
+    const int32_t* blk_ptr;
+    const int32_t* cov_atom;
+    const int32_t* cov_R;
+    const uint64_t* cov_mask;
+    const int64_t* bp_ptr;
+    const BPair* bp;
+    int64_t blk_begin;  // first owned block
+    int max_rows;       // Phi rows allocated (incl. pad)
+    int max_cover;
+    int nspin;
+    int64_t nnz;
+    int64_t npts;
+    double dV;
+    double sign;        // +1, or -1 under the fault hook
+    const double* in;   // dm [nspin][nnz] or veff [nspin][npts]
+    double* out;        // rho [nspin][npts] or h [nspin][nnz]
+};
+
+// Index build (kb_index.cu). Fills `ix` (device) and returns host stats.
+void build_index_device(const SysParams& sys, DevIndex& ix, cudaStream_t st);
+void free_index(DevIndex& ix);
+void copy_index_to_host(const DevIndex& ix, HostIndex& h, cudaStream_t st);
+
+// Grid kernels (kb_grid.cu). Return number of kernel launches.
+size_t grid_smem_bytes(int max_rows, int max_cover, int nwarps, bool density);
+int launch_density(const GridArgs& g, int64_t nblk_owned, int nwarps, cudaStream_t st);
+int launch_hamiltonian(const GridArgs& g, int64_t nblk_owned, int nwarps, cudaStream_t st);
+int launch_mirror(const DevIndex& ix, const SysParams& sys, int nspin, double* h, cudaStream_t st);
+int launch_dm_check(const DevIndex& ix, const SysParams& sys, int nspin, const double* dm,
+                    unsigned long long* d_maxdiff_maxabs, cudaStream_t st);
+int launch_block_orbitals(const GridArgs& g, int64_t block, double* d_out, cudaStream_t st);
+
+}  // namespace kbg
