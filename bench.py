@@ -263,6 +263,14 @@ def main():
             step(evs[k])
             launches += 3
         torch.cuda.synchronize()
+        # the timed region is shorter than nvidia-smi's sampling period: keep the
+        # same workload running (untimed) until 3 samples exist
+        extra, t_end = 0, time.time() + 5.0
+        while len(clk.rows) < 3 and time.time() < t_end:
+            for _ in range(20):
+                step()
+            torch.cuda.synchronize()
+            extra += 20
     if world > 1:
         dist.barrier()
     for e in evs:
@@ -375,7 +383,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
-            "clocks": clk.summary(),
+            "clocks": dict(clk.summary(), extra_untimed_passes=extra),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -175,6 +175,7 @@ int kbg_last_tally(const kbg_ctx* ctx, kbg_tally* out);
 /* Options. KBG_OPT_WARPS: warps per CTA of the grid kernels (4 or 8). */
 #define KBG_OPT_WARPS 1
 #define KBG_OPT_FAULT_SIGN 2 /* test hook: flip the sign of the H accumulate (kband fault_proc6_sign analogue) */
+#define KBG_OPT_SCATTER_STORE 3 /* timing experiment: plain stores instead of atomics (H is WRONG) */
 int kbg_set_option(kbg_ctx* ctx, int option, int64_t value);
 
 const char* kbg_last_error(const kbg_ctx* ctx);

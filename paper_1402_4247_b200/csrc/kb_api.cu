@@ -21,6 +21,7 @@ struct kbg_ctx {
     int64_t blk_begin = 0, blk_end = 0;
     int nwarps = 8;
     double sign = 1.0;
+    int scatter = 0;
     cudaStream_t stream = nullptr;
     double* d_in = nullptr;
     size_t cap_in = 0;
@@ -170,6 +171,7 @@ kbg::GridArgs grid_args(kbg_ctx* c, int nspin, double dV, const double* in, doub
     g.npts = c->npts;
     g.dV = dV;
     g.sign = c->sign;
+    g.scatter = c->scatter;
     g.in = in;
     g.out = out;
     if (g.max_cover > 32 * c->nwarps)
@@ -448,6 +450,9 @@ int kbg_set_option(kbg_ctx* c, int option, int64_t value) {
             return KBG_OK;
         case KBG_OPT_FAULT_SIGN:
             c->sign = value ? -1.0 : 1.0;
+            return KBG_OK;
+        case KBG_OPT_SCATTER_STORE:
+            c->scatter = value ? 1 : 0;
             return KBG_OK;
         default:
             c->err = "set_option: unknown option";

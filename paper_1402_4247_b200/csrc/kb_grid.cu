@@ -46,6 +46,14 @@ __device__ __forceinline__ uint32_t octet_mask(uint64_t m) {
     return q;
 }
 
+// Shared-memory address of Phi[row][slot]: rows of 64 doubles with the slot
+// index XOR-swizzled by 4*(row & 3), so the 4-row x 4-slot half-warp footprint
+// of every DMMA fragment load hits 32 distinct banks.
+__device__ __forceinline__ int phi_swz(int row) { return (row & 3) << 2; }
+__device__ __forceinline__ size_t phi_at(int row, int slot) {
+    return static_cast<size_t>(row) * kPhiStride + (slot ^ phi_swz(row));
+}
+
 struct Smem {
     double* phi;
     double* acc;  // w[64] (H) or racc[NW][64] (rho)
@@ -94,7 +102,8 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm) {
     for (int task = tid; task < ncov * 64; task += nt) {
         const int c = task >> 6, s = task & 63;
         const CoverS& cv = sm.cov[c];
-        double* dst = sm.phi + static_cast<size_t>(cv.row0) * kPhiStride + s;
+        double* dst = sm.phi;
+        const int row0 = cv.row0;
         if ((cv.mask >> s) & 1) {
             int li, lj, lk;
             slot_decode(s, li, lj, lk);
@@ -106,9 +115,9 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm) {
             const double dz = (fi * P.A[2] + fj * P.A[5] + fk * P.A[8]) - cv.t[2];
             const double d2 = dx * dx + dy * dy + dz * dz;
             eval_orbitals(P.sp[cv.sp], P.tables, dx, dy, dz, d2,
-                          [&](int o, double v) { dst[static_cast<size_t>(o) * kPhiStride] = v; });
+                          [&](int o, double v) { dst[phi_at(row0 + o, s)] = v; });
         } else {
-            for (int o = 0; o < cv.norb; ++o) dst[static_cast<size_t>(o) * kPhiStride] = 0.0;
+            for (int o = 0; o < cv.norb; ++o) dst[phi_at(row0 + o, s)] = 0.0;
         }
     }
     __syncthreads();
@@ -126,24 +135,28 @@ __device__ __forceinline__ int64_t slot_point(const SysParams& P, int bi, int bj
 // ---- H pair task ---------------------------------------------------------------
 template <int TM, int TN>
 __device__ __forceinline__ void h_pair(const double* __restrict__ phi, const double* __restrict__ w, const CoverS& A,
-                                       const CoverS& B, uint32_t qm, double* __restrict__ H, double sign, int lane) {
+                                       const CoverS& B, uint32_t qm, double* __restrict__ H, double sign, int scatter,
+                                       int lane) {
     double c[TM][TN][2];
 #pragma unroll
     for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < TN; ++j) c[i][j][0] = c[i][j][1] = 0.0;
-    const double* pa = phi + static_cast<size_t>(A.row0 + (lane >> 2)) * kPhiStride + (lane & 3);
-    const double* pb = phi + static_cast<size_t>(B.row0 + (lane >> 2)) * kPhiStride + (lane & 3);
+    const int ra = A.row0 + (lane >> 2), rb = B.row0 + (lane >> 2);
+    const double* pa = phi + static_cast<size_t>(ra) * kPhiStride + (lane & 3);
+    const double* pb = phi + static_cast<size_t>(rb) * kPhiStride + (lane & 3);
+    const int sa = ra & 3, sb = rb & 3;
     const double* pw = w + (lane & 3);
     while (qm) {
-        const int col = (__ffs(qm) - 1) * 4;
+        const int q = __ffs(qm) - 1;
         qm &= qm - 1;
-        const double wv = pw[col];
+        const double wv = pw[4 * q];
+        const int ca = 4 * (q ^ sa), cb = 4 * (q ^ sb);
         double a[TM], b[TN];
 #pragma unroll
-        for (int i = 0; i < TM; ++i) a[i] = pa[i * 8 * kPhiStride + col] * wv;
+        for (int i = 0; i < TM; ++i) a[i] = pa[i * 8 * kPhiStride + ca] * wv;
 #pragma unroll
-        for (int j = 0; j < TN; ++j) b[j] = pb[j * 8 * kPhiStride + col];
+        for (int j = 0; j < TN; ++j) b[j] = pb[j * 8 * kPhiStride + cb];
 #pragma unroll
         for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -157,18 +170,24 @@ __device__ __forceinline__ void h_pair(const double* __restrict__ phi, const dou
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int r = i * 8 + (lane >> 2), col = j * 8 + (lane & 3) * 2 + e;
-                if (r < na && col < nb) atomicAdd(H + r * nb + col, sign * c[i][j][e]);
+                if (r < na && col < nb) {
+                    if (scatter == 0)
+                        atomicAdd(H + r * nb + col, sign * c[i][j][e]);
+                    else
+                        H[r * nb + col] = sign * c[i][j][e];
+                }
             }
 }
 
 template <int TM>
 __device__ __forceinline__ void h_pair_tn(int tn, const double* phi, const double* w, const CoverS& A,
-                                          const CoverS& B, uint32_t qm, double* H, double sign, int lane) {
+                                          const CoverS& B, uint32_t qm, double* H, double sign, int scatter,
+                                          int lane) {
     switch (tn) {
-        case 1: h_pair<TM, 1>(phi, w, A, B, qm, H, sign, lane); break;
-        case 2: h_pair<TM, 2>(phi, w, A, B, qm, H, sign, lane); break;
-        case 3: h_pair<TM, 3>(phi, w, A, B, qm, H, sign, lane); break;
-        default: h_pair<TM, 4>(phi, w, A, B, qm, H, sign, lane); break;
+        case 1: h_pair<TM, 1>(phi, w, A, B, qm, H, sign, scatter, lane); break;
+        case 2: h_pair<TM, 2>(phi, w, A, B, qm, H, sign, scatter, lane); break;
+        case 3: h_pair<TM, 3>(phi, w, A, B, qm, H, sign, scatter, lane); break;
+        default: h_pair<TM, 4>(phi, w, A, B, qm, H, sign, scatter, lane); break;
     }
 }
 
@@ -199,10 +218,10 @@ __global__ void __launch_bounds__(NW * 32) k_hamiltonian(GridArgs g) {
             const int tm = (A.norb + 7) >> 3, tn = (B.norb + 7) >> 3;
             double* H = Hs + bp.off;
             switch (tm) {
-                case 1: h_pair_tn<1>(tn, sm.phi, sm.acc, A, B, qm, H, g.sign, lane); break;
-                case 2: h_pair_tn<2>(tn, sm.phi, sm.acc, A, B, qm, H, g.sign, lane); break;
-                case 3: h_pair_tn<3>(tn, sm.phi, sm.acc, A, B, qm, H, g.sign, lane); break;
-                default: h_pair_tn<4>(tn, sm.phi, sm.acc, A, B, qm, H, g.sign, lane); break;
+                case 1: h_pair_tn<1>(tn, sm.phi, sm.acc, A, B, qm, H, g.sign, g.scatter, lane); break;
+                case 2: h_pair_tn<2>(tn, sm.phi, sm.acc, A, B, qm, H, g.sign, g.scatter, lane); break;
+                case 3: h_pair_tn<3>(tn, sm.phi, sm.acc, A, B, qm, H, g.sign, g.scatter, lane); break;
+                default: h_pair_tn<4>(tn, sm.phi, sm.acc, A, B, qm, H, g.sign, g.scatter, lane); break;
             }
         }
         __syncthreads();
@@ -223,28 +242,31 @@ __device__ __forceinline__ void rho_pair(const double* __restrict__ phi, const C
             const int k = 4 * s + (lane & 3), n = 8 * t + (lane >> 2);
             bfr[s][t] = (k < na && n < nb) ? __ldg(D + k * nb + n) : 0.0;
         }
-    const double* pa = phi + static_cast<size_t>(A.row0 + (lane & 3)) * kPhiStride + (lane >> 2);
-    const double* pbr = phi + static_cast<size_t>(B.row0 + (lane & 3) * 2) * kPhiStride + (lane >> 2);
+    const int ra = A.row0 + (lane & 3), rb = B.row0 + (lane & 3) * 2;
+    const double* pa = phi + static_cast<size_t>(ra) * kPhiStride;
+    const double* pbr = phi + static_cast<size_t>(rb) * kPhiStride;
+    const int sa = phi_swz(ra), sb0 = phi_swz(rb), sb1 = phi_swz(rb + 1);
     while (om) {
-        const int col = (__ffs(om) - 1) * 8;
+        const int col = (__ffs(om) - 1) * 8 + (lane >> 2);
         om &= om - 1;
         double x[TN][2];
 #pragma unroll
         for (int t = 0; t < TN; ++t) x[t][0] = x[t][1] = 0.0;
 #pragma unroll
         for (int s = 0; s < KS; ++s) {
-            const double a = pa[4 * s * kPhiStride + col];
+            const double a = pa[4 * s * kPhiStride + (col ^ sa)];
 #pragma unroll
             for (int t = 0; t < TN; ++t) dmma(x[t], a, bfr[s][t]);
         }
         double part = 0.0;
 #pragma unroll
-        for (int t = 0; t < TN; ++t)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) part += x[t][e] * pbr[(8 * t + e) * kPhiStride + col];
+        for (int t = 0; t < TN; ++t) {
+            part += x[t][0] * pbr[(8 * t) * kPhiStride + (col ^ sb0)];
+            part += x[t][1] * pbr[(8 * t + 1) * kPhiStride + (col ^ sb1)];
+        }
         part += __shfl_xor_sync(0xffffffffu, part, 1);
         part += __shfl_xor_sync(0xffffffffu, part, 2);
-        if ((lane & 3) == 0) racc[col + (lane >> 2)] += f * part;
+        if ((lane & 3) == 0) racc[col] += f * part;
     }
 }
 
@@ -326,9 +348,24 @@ __global__ void k_mirror(SysParams P, int64_t npair, int nspin, int64_t nnz, con
     const int a = pa[p], b = pb[p];
     const int R0 = pR[3 * p], R1 = pR[3 * p + 1], R2 = pR[3 * p + 2];
     const bool canon = (a != b) ? a < b : (R0 != 0 ? R0 > 0 : (R1 != 0 ? R1 > 0 : R2 >= 0));
-    if (canon) return;
     const int na = P.sp[P.spc[a]].norb, nb = P.sp[P.spc[b]].norb;
     const int64_t q = mirror[p];
+    if (q == p) {
+        // (a, a, 0): re-symmetrise (H + H^T)/2, like kband triple_product (linalg.cpp:120-128)
+        for (int s = 0; s < nspin; ++s) {
+            double* x = h + s * nnz + poff[p];
+            for (int e = lane; e < na * na; e += 32) {
+                const int i = e / na, j = e % na;
+                if (i < j) {
+                    const double v = 0.5 * (x[i * na + j] + x[j * na + i]);
+                    x[i * na + j] = v;
+                    x[j * na + i] = v;
+                }
+            }
+        }
+        return;
+    }
+    if (canon) return;
     for (int s = 0; s < nspin; ++s) {
         const double* src = h + s * nnz + poff[q];  // nb x na
         double* dst = h + s * nnz + poff[p];        // na x nb
@@ -382,7 +419,7 @@ __global__ void k_block_orbitals(GridArgs g, int64_t b, double* out) {
     if (ncov == 0) return;
     const int M = sm.cov[ncov - 1].row0 + sm.cov[ncov - 1].norb;
     for (int i = threadIdx.x; i < M * 64; i += blockDim.x)
-        out[i] = sm.phi[static_cast<size_t>(i >> 6) * kPhiStride + (i & 63)];
+        out[i] = sm.phi[phi_at(i >> 6, i & 63)];
 }
 
 template <class K>

@@ -14,8 +14,8 @@ namespace kbg {
 
 constexpr int kMaxSpecies = 8;
 constexpr int kMaxRad = 16;
-constexpr int kPhiStride = 68;  // doubles per Phi row: 64 slots + 4 pad (bank-conflict-free DMMA fragments)
-constexpr int kRowPad = 16;     // zeroed rows after the last orbital (tile overrun)
+constexpr int kPhiStride = 64;  // doubles per Phi row (one per slot); columns XOR-swizzled by row, see phi_col
+constexpr int kRowPad = 8;      // zeroed rows after the last orbital (tile overrun of the 8-row DMMA tiles)
 
 // Error taxonomy of kband (common.hpp:21-38) carried as a status code.
 struct Error : std::runtime_error {
@@ -117,6 +117,7 @@ struct GridArgs {
     int64_t npts;
     double dV;
     double sign;        // +1, or -1 under the fault hook
+    int scatter;        // 0: atomic scatter (product); 1: plain stores (timing experiment only, wrong H)
     const double* in;   // dm [nspin][nnz] or veff [nspin][npts]
     double* out;        // rho [nspin][npts] or h [nspin][nnz]
 };

@@ -1,0 +1,73 @@
+"""Per-kernel timing experiments (CUDA events, L2 flushed between reps).
+
+python tools/kernel_times.py [--config cubic56_200Ry] [--reps 20]
+Prints one JSON line per variant: density / hamiltonian accumulate with
+atomic scatter vs plain-store scatter (timing experiment only), 4 vs 8 warps.
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_1402_4247_b200 import _abi  # noqa: E402
+from paper_1402_4247_b200.grid import GridPass  # noqa: E402
+from paper_1402_4247_b200.system import Fe3O4  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="cubic56_200Ry")
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--nspin", type=int, default=1)
+    a = ap.parse_args()
+    f = Fe3O4.config(a.config)
+    gp = GridPass(f.system)
+    ix = gp.build_index()
+    dev = torch.device("cuda", 0)
+    d_dm = torch.from_numpy(f.dm(ix, nspin=a.nspin)).to(dev)
+    d_v = torch.from_numpy(f.veff(nspin=a.nspin)).to(dev)
+    rho = torch.empty((a.nspin, f.system.npts), dtype=torch.float64, device=dev)
+    h = torch.empty((a.nspin, ix["nnz"]), dtype=torch.float64, device=dev)
+    flush = torch.empty(512 << 18, dtype=torch.float32, device=dev)
+    st = torch.cuda.current_stream()
+
+    def timeit(fn):
+        for _ in range(3):
+            fn()
+        ts = []
+        for _ in range(a.reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            fn()
+            e1.record(st)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return float(np.median(ts)), float(np.min(ts))
+
+    f_rho = a.nspin * (2 * ix["sum_m2"] + 2 * ix["sum_m"])
+    f_h = a.nspin * 2 * ix["sum_m2"]
+    for warps in (8, 4):
+        gp.set_option(_abi.KBG_OPT_WARPS, warps)
+        for name, fn, fl in (
+            ("density", lambda: gp.density_dev(d_dm, rho, st), f_rho),
+            ("h_accumulate", lambda: gp.hamiltonian_accumulate_dev(d_v, f.dV, h, st), f_h),
+        ):
+            med, mn = timeit(fn)
+            print(json.dumps({"config": a.config, "kernel": name, "warps": warps, "median_ms": round(med, 4),
+                              "min_ms": round(mn, 4), "alg_tflops": round(fl / (med * 1e-3) / 1e12, 3)}))
+        gp.set_option(_abi.KBG_OPT_SCATTER_STORE, 1)
+        med, mn = timeit(lambda: gp.hamiltonian_accumulate_dev(d_v, f.dV, h, st))
+        gp.set_option(_abi.KBG_OPT_SCATTER_STORE, 0)
+        print(json.dumps({"config": a.config, "kernel": "h_accumulate_store_scatter(experiment)", "warps": warps,
+                          "median_ms": round(med, 4), "min_ms": round(mn, 4)}))
+
+
+if __name__ == "__main__":
+    main()
