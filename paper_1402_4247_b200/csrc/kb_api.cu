@@ -193,17 +193,19 @@ void shard(kbg_ctx* c) {
     std::vector<int64_t> cost(nb);
     KBG_CUDA(cudaMemcpy(cost.data(), c->ix.blk_cost, nb * sizeof(int64_t), cudaMemcpyDeviceToHost));
     // Contiguous cost-balanced split; mirrors
-    // paper_1402_4247_b200/shard.py:partition (+1 per block so empty blocks count).
-    std::vector<long double> pre(nb + 1, 0);
-    for (int64_t b = 0; b < nb; ++b) pre[b + 1] = pre[b] + static_cast<long double>(cost[b] + 1);
+    // paper_1402_4247_b200/shard.py:partition: weights cost+1 (empty blocks
+    // count), bound(r) = first b with prefix(b) * nranks >= total * r (exact
+    // integer arithmetic).
+    std::vector<int64_t> pre(nb + 1, 0);
+    for (int64_t b = 0; b < nb; ++b) pre[b + 1] = pre[b] + cost[b] + 1;
     auto bound = [&](int r) -> int64_t {
         if (r <= 0) return 0;
         if (r >= c->nranks) return nb;
-        const long double target = pre[nb] * r / c->nranks;
+        const __int128 target = static_cast<__int128>(pre[nb]) * r;
         int64_t lo = 0, hi = nb;
         while (lo < hi) {
             const int64_t mid = (lo + hi) / 2;
-            if (pre[mid] < target)
+            if (static_cast<__int128>(pre[mid]) * c->nranks < target)
                 lo = mid + 1;
             else
                 hi = mid;
