@@ -46,34 +46,42 @@ __device__ __forceinline__ uint32_t octet_mask(uint64_t m) {
     return q;
 }
 
-// Shared-memory address of Phi[row][slot]: rows of 64 doubles with the slot
-// index XOR-swizzled by 4*(row & 3), so the 4-row x 4-slot half-warp footprint
-// of every DMMA fragment load hits 32 distinct banks.
-__device__ __forceinline__ int phi_swz(int row) { return (row & 3) << 2; }
+// Shared-memory address of Phi[row][slot]. Every cover's rows start at a
+// multiple of 4 (pad rows zeroed); slots are XOR-swizzled by 4*f(row),
+// f(row) = (row ^ (row >> 2)) & 3, which is a permutation both on any 4
+// consecutive aligned rows (DMMA A/B fragments) and on rows {r, r+2, r+4, r+6}
+// (density epilogue), so every half-warp LDS.64 touches 32 distinct banks.
+__device__ __forceinline__ int phi_swz(int row) { return ((row ^ (row >> 2)) & 3) << 2; }
 __device__ __forceinline__ size_t phi_at(int row, int slot) {
     return static_cast<size_t>(row) * kPhiStride + (slot ^ phi_swz(row));
 }
 
+__host__ __device__ __forceinline__ int align4(int n) { return (n + 3) & ~3; }
+
 struct Smem {
     double* phi;
     double* acc;  // w[64] (H) or racc[NW][64] (rho)
+    BPair* bp;    // this block's work items
     CoverS* cov;
 };
 
-__device__ __forceinline__ Smem carve(unsigned char* base, int rows_alloc, int acc_doubles) {
+__device__ __forceinline__ Smem carve(unsigned char* base, int rows_alloc, int acc_doubles, int max_bpairs) {
     Smem s;
     s.phi = reinterpret_cast<double*>(base);
     s.acc = s.phi + static_cast<size_t>(rows_alloc) * kPhiStride;
-    s.cov = reinterpret_cast<CoverS*>(s.acc + acc_doubles);
+    s.bp = reinterpret_cast<BPair*>(s.acc + acc_doubles);
+    s.cov = reinterpret_cast<CoverS*>(s.bp + max_bpairs);
     return s;
 }
 
-// Loads the covers of block b and evaluates Phi into shared memory.
-// Returns the number of covers (uniform across the CTA).
-__device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm) {
+// Loads the covers and work items of block b into shared memory and evaluates
+// Phi. Returns the number of covers (uniform across the CTA).
+__device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int& nbp) {
     const int tid = threadIdx.x, nt = blockDim.x;
     const int c0 = g.blk_ptr[b], c1 = g.blk_ptr[b + 1];
     const int ncov = c1 - c0;
+    const int64_t p0 = g.bp_ptr[b];
+    nbp = static_cast<int>(g.bp_ptr[b + 1] - p0);
     if (ncov == 0) return 0;
     const SysParams& P = g.sys;
     if (tid < ncov) {
@@ -87,15 +95,15 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) cv.t[c] = P.tau[3 * a + c] + ((R0 * P.A[c] + R1 * P.A[3 + c]) + R2 * P.A[6 + c]);
     }
+    for (int i = tid; i < nbp; i += nt) sm.bp[i] = g.bp[p0 + i];
     __syncthreads();
     if (tid < ncov) {
         int r0 = 0;
-        for (int c = 0; c < tid; ++c) r0 += sm.cov[c].norb;
+        for (int c = 0; c < tid; ++c) r0 += align4(sm.cov[c].norb);
         sm.cov[tid].row0 = r0;
     }
     __syncthreads();
-    const int M = sm.cov[ncov - 1].row0 + sm.cov[ncov - 1].norb;
-    // zero the pad rows read by tile overrun
+    const int M = sm.cov[ncov - 1].row0 + align4(sm.cov[ncov - 1].norb);
     for (int i = tid; i < kRowPad * kPhiStride; i += nt) sm.phi[static_cast<size_t>(M) * kPhiStride + i] = 0.0;
     int bi, bj, bk;
     block_decode(P, b, bi, bj, bk);
@@ -119,6 +127,7 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm) {
         } else {
             for (int o = 0; o < cv.norb; ++o) dst[phi_at(row0 + o, s)] = 0.0;
         }
+        for (int o = cv.norb; o < align4(cv.norb); ++o) dst[phi_at(row0 + o, s)] = 0.0;
     }
     __syncthreads();
     return ncov;
@@ -133,34 +142,52 @@ __device__ __forceinline__ int64_t slot_point(const SysParams& P, int bi, int bj
 }
 
 // ---- H pair task ---------------------------------------------------------------
+// C(na x nb) = sum over active quads q of A(na x 4) B(4 x nb), A = Phi_ci * w,
+// B = Phi_cj^T. Pairs with <= 2 output tiles alternate two accumulator sets
+// over the quads so that two independent DMMA chains are in flight.
 template <int TM, int TN>
 __device__ __forceinline__ void h_pair(const double* __restrict__ phi, const double* __restrict__ w, const CoverS& A,
                                        const CoverS& B, uint32_t qm, double* __restrict__ H, double sign, int scatter,
                                        int lane) {
-    double c[TM][TN][2];
+    constexpr int NACC = (TM * TN <= 2) ? 2 : 1;
+    double c[NACC][TM][TN][2];
 #pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) c[i][j][0] = c[i][j][1] = 0.0;
-    const int ra = A.row0 + (lane >> 2), rb = B.row0 + (lane >> 2);
-    const double* pa = phi + static_cast<size_t>(ra) * kPhiStride + (lane & 3);
-    const double* pb = phi + static_cast<size_t>(rb) * kPhiStride + (lane & 3);
-    const int sa = ra & 3, sb = rb & 3;
-    const double* pw = w + (lane & 3);
-    while (qm) {
-        const int q = __ffs(qm) - 1;
-        qm &= qm - 1;
-        const double wv = pw[4 * q];
-        const int ca = 4 * (q ^ sa), cb = 4 * (q ^ sb);
-        double a[TM], b[TN];
-#pragma unroll
-        for (int i = 0; i < TM; ++i) a[i] = pa[i * 8 * kPhiStride + ca] * wv;
-#pragma unroll
-        for (int j = 0; j < TN; ++j) b[j] = pb[j * 8 * kPhiStride + cb];
+    for (int u = 0; u < NACC; ++u)
 #pragma unroll
         for (int i = 0; i < TM; ++i)
 #pragma unroll
-            for (int j = 0; j < TN; ++j) dmma(c[i][j], a[i], b[j]);
+            for (int j = 0; j < TN; ++j) c[u][i][j][0] = c[u][i][j][1] = 0.0;
+    const int ra = A.row0 + (lane >> 2), rb = B.row0 + (lane >> 2);
+    const double* pa = phi + static_cast<size_t>(ra) * kPhiStride + (lane & 3);
+    const double* pb = phi + static_cast<size_t>(rb) * kPhiStride + (lane & 3);
+    const int sa = phi_swz(ra), sb = phi_swz(rb);  // same for every 8-row tile (8 = 0 mod 4, f(r+8) = f(r) ^ 2)
+    const double* pw = w + (lane & 3);
+    auto step = [&](int u, int q) {
+        const int col = 4 * q;
+        const double wv = pw[col];
+        double a[TM], b[TN];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) a[i] = pa[i * 8 * kPhiStride + (col ^ phi_swz(ra + 8 * i) ^ 0)] * wv;
+#pragma unroll
+        for (int j = 0; j < TN; ++j) b[j] = pb[j * 8 * kPhiStride + (col ^ phi_swz(rb + 8 * j))];
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) dmma(c[u][i][j], a[i], b[j]);
+    };
+    (void)sa;
+    (void)sb;
+    while (qm) {
+        const int q0 = __ffs(qm) - 1;
+        qm &= qm - 1;
+        if (NACC == 2 && qm) {
+            const int q1 = __ffs(qm) - 1;
+            qm &= qm - 1;
+            step(0, q0);
+            step(NACC - 1, q1);
+        } else {
+            step(0, q0);
+        }
     }
     const int na = A.norb, nb = B.norb;
 #pragma unroll
@@ -170,11 +197,13 @@ __device__ __forceinline__ void h_pair(const double* __restrict__ phi, const dou
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int r = i * 8 + (lane >> 2), col = j * 8 + (lane & 3) * 2 + e;
+                double v = c[0][i][j][e];
+                if (NACC == 2) v += c[NACC - 1][i][j][e];
                 if (r < na && col < nb) {
                     if (scatter == 0)
-                        atomicAdd(H + r * nb + col, sign * c[i][j][e]);
+                        atomicAdd(H + r * nb + col, sign * v);
                     else
-                        H[r * nb + col] = sign * c[i][j][e];
+                        H[r * nb + col] = sign * v;
                 }
             }
 }
@@ -194,14 +223,14 @@ __device__ __forceinline__ void h_pair_tn(int tn, const double* phi, const doubl
 template <int NW>
 __global__ void __launch_bounds__(NW * 32) k_hamiltonian(GridArgs g) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const Smem sm = carve(smem_raw, g.max_rows, 64);
+    const Smem sm = carve(smem_raw, g.max_rows, 64, g.max_bpairs);
     const int64_t b = g.blk_begin + blockIdx.x;
-    const int ncov = stage_block(g, b, sm);
+    int nbp;
+    const int ncov = stage_block(g, b, sm, nbp);
     if (ncov == 0) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int bi, bj, bk;
     block_decode(g.sys, b, bi, bj, bk);
-    const int64_t p0 = g.bp_ptr[b], p1 = g.bp_ptr[b + 1];
     for (int spin = 0; spin < g.nspin; ++spin) {
         if (tid < 64) {
             bool valid;
@@ -210,8 +239,8 @@ __global__ void __launch_bounds__(NW * 32) k_hamiltonian(GridArgs g) {
         }
         __syncthreads();
         double* Hs = g.out + spin * g.nnz;
-        for (int64_t e = p0 + warp; e < p1; e += NW) {
-            const BPair bp = g.bp[e];
+        for (int e = warp; e < nbp; e += NW) {
+            const BPair bp = sm.bp[e];
             const CoverS& A = sm.cov[bp.cicj & 0xffff];
             const CoverS& B = sm.cov[bp.cicj >> 16];
             const uint32_t qm = quad_mask(A.mask & B.mask);
@@ -229,40 +258,101 @@ __global__ void __launch_bounds__(NW * 32) k_hamiltonian(GridArgs g) {
 }
 
 // ---- rho pair task -------------------------------------------------------------
+// Fast path (na, nb <= 16): DM fragments arrive in registers (prefetched one
+// pair ahead); two octets are processed per iteration for DMMA ILP.
+constexpr int kFrag = 8;  // B fragments per lane for na, nb <= 16: (4 K-steps) x (2 N-tiles)
+
+__device__ __forceinline__ void load_dfrag(const double* __restrict__ D, int na, int nb, int lane,
+                                           double (&out)[kFrag]) {
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const int k = 4 * s + (lane & 3), n = 8 * t + (lane >> 2);
+            out[s * 2 + t] = (k < na && n < nb) ? __ldg(D + k * nb + n) : 0.0;
+        }
+}
+
+template <int KS, int TN, int NO>
+__device__ __forceinline__ void rho_octets(const double* __restrict__ pa, const double* __restrict__ pbr, int ra,
+                                           int rb, const int (&col)[2], const double (&bf)[kFrag], double f,
+                                           double* __restrict__ racc, int lane) {
+    double x[NO][TN][2];
+#pragma unroll
+    for (int o = 0; o < NO; ++o)
+#pragma unroll
+        for (int t = 0; t < TN; ++t) x[o][t][0] = x[o][t][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+        const int sw = phi_swz(ra + 4 * s);
+        double a[NO];
+#pragma unroll
+        for (int o = 0; o < NO; ++o) a[o] = pa[4 * s * kPhiStride + (col[o] ^ sw)];
+#pragma unroll
+        for (int o = 0; o < NO; ++o)
+#pragma unroll
+            for (int t = 0; t < TN; ++t) dmma(x[o][t], a[o], bf[s * 2 + t]);
+    }
+#pragma unroll
+    for (int o = 0; o < NO; ++o) {
+        double part = 0.0;
+#pragma unroll
+        for (int t = 0; t < TN; ++t)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int row = rb + 8 * t + e;
+                part += x[o][t][e] * pbr[(8 * t + e) * kPhiStride + (col[o] ^ phi_swz(row))];
+            }
+        part += __shfl_xor_sync(0xffffffffu, part, 1);
+        part += __shfl_xor_sync(0xffffffffu, part, 2);
+        if ((lane & 3) == 0) racc[col[o]] += f * part;
+    }
+}
+
 template <int KS, int TN>
 __device__ __forceinline__ void rho_pair(const double* __restrict__ phi, const CoverS& A, const CoverS& B,
-                                         uint32_t om, const double* __restrict__ D, double f, double* __restrict__ racc,
+                                         uint32_t om, const double (&bf)[kFrag], double f, double* __restrict__ racc,
                                          int lane) {
-    const int na = A.norb, nb = B.norb;
-    double bfr[KS][TN];
-#pragma unroll
-    for (int s = 0; s < KS; ++s)
-#pragma unroll
-        for (int t = 0; t < TN; ++t) {
-            const int k = 4 * s + (lane & 3), n = 8 * t + (lane >> 2);
-            bfr[s][t] = (k < na && n < nb) ? __ldg(D + k * nb + n) : 0.0;
-        }
     const int ra = A.row0 + (lane & 3), rb = B.row0 + (lane & 3) * 2;
     const double* pa = phi + static_cast<size_t>(ra) * kPhiStride;
     const double* pbr = phi + static_cast<size_t>(rb) * kPhiStride;
-    const int sa = phi_swz(ra), sb0 = phi_swz(rb), sb1 = phi_swz(rb + 1);
+    while (om) {
+        int col[2];
+        col[0] = (__ffs(om) - 1) * 8 + (lane >> 2);
+        om &= om - 1;
+        if (om) {
+            col[1] = (__ffs(om) - 1) * 8 + (lane >> 2);
+            om &= om - 1;
+            rho_octets<KS, TN, 2>(pa, pbr, ra, rb, col, bf, f, racc, lane);
+        } else {
+            col[1] = col[0];
+            rho_octets<KS, TN, 1>(pa, pbr, ra, rb, col, bf, f, racc, lane);
+        }
+    }
+}
+
+// General path for atoms with more than 16 orbitals (not used by Fe3O4).
+__device__ void rho_pair_big(const double* __restrict__ phi, const CoverS& A, const CoverS& B, uint32_t om,
+                             const double* __restrict__ D, double f, double* __restrict__ racc, int lane) {
+    const int na = A.norb, nb = B.norb;
+    const int ks = (na + 3) >> 2, tn = (nb + 7) >> 3;
     while (om) {
         const int col = (__ffs(om) - 1) * 8 + (lane >> 2);
         om &= om - 1;
-        double x[TN][2];
-#pragma unroll
-        for (int t = 0; t < TN; ++t) x[t][0] = x[t][1] = 0.0;
-#pragma unroll
-        for (int s = 0; s < KS; ++s) {
-            const double a = pa[4 * s * kPhiStride + (col ^ sa)];
-#pragma unroll
-            for (int t = 0; t < TN; ++t) dmma(x[t], a, bfr[s][t]);
-        }
         double part = 0.0;
+        for (int t = 0; t < tn; ++t) {
+            double x[2] = {0.0, 0.0};
+            for (int s = 0; s < ks; ++s) {
+                const int k = 4 * s + (lane & 3), n = 8 * t + (lane >> 2);
+                const double bv = (k < na && n < nb) ? __ldg(D + k * nb + n) : 0.0;
+                const int ra = A.row0 + 4 * s + (lane & 3);
+                dmma(x, phi[phi_at(ra, col)], bv);
+            }
 #pragma unroll
-        for (int t = 0; t < TN; ++t) {
-            part += x[t][0] * pbr[(8 * t) * kPhiStride + (col ^ sb0)];
-            part += x[t][1] * pbr[(8 * t + 1) * kPhiStride + (col ^ sb1)];
+            for (int e = 0; e < 2; ++e) {
+                const int row = B.row0 + 8 * t + (lane & 3) * 2 + e;
+                part += x[e] * phi[phi_at(row, col)];
+            }
         }
         part += __shfl_xor_sync(0xffffffffu, part, 1);
         part += __shfl_xor_sync(0xffffffffu, part, 2);
@@ -272,24 +362,23 @@ __device__ __forceinline__ void rho_pair(const double* __restrict__ phi, const C
 
 template <int KS>
 __device__ __forceinline__ void rho_pair_tn(int tn, const double* phi, const CoverS& A, const CoverS& B, uint32_t om,
-                                            const double* D, double f, double* racc, int lane) {
-    switch (tn) {
-        case 1: rho_pair<KS, 1>(phi, A, B, om, D, f, racc, lane); break;
-        case 2: rho_pair<KS, 2>(phi, A, B, om, D, f, racc, lane); break;
-        case 3: rho_pair<KS, 3>(phi, A, B, om, D, f, racc, lane); break;
-        default: rho_pair<KS, 4>(phi, A, B, om, D, f, racc, lane); break;
-    }
+                                            const double (&bf)[kFrag], double f, double* racc, int lane) {
+    if (tn == 1)
+        rho_pair<KS, 1>(phi, A, B, om, bf, f, racc, lane);
+    else
+        rho_pair<KS, 2>(phi, A, B, om, bf, f, racc, lane);
 }
 
 template <int NW>
 __global__ void __launch_bounds__(NW * 32) k_density(GridArgs g) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const Smem sm = carve(smem_raw, g.max_rows, NW * 64);
+    const Smem sm = carve(smem_raw, g.max_rows, NW * 64, g.max_bpairs);
     const int64_t b = g.blk_begin + blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int bi, bj, bk;
     block_decode(g.sys, b, bi, bj, bk);
-    const int ncov = stage_block(g, b, sm);
+    int nbp;
+    const int ncov = stage_block(g, b, sm, nbp);
     if (ncov == 0) {
         if (tid < 64) {
             bool valid;
@@ -299,30 +388,39 @@ __global__ void __launch_bounds__(NW * 32) k_density(GridArgs g) {
         }
         return;
     }
-    const int64_t p0 = g.bp_ptr[b], p1 = g.bp_ptr[b + 1];
     double* racc = sm.acc + warp * 64;
     for (int spin = 0; spin < g.nspin; ++spin) {
         for (int i = lane; i < 64; i += 32) racc[i] = 0.0;
         __syncwarp();
         const double* Ds = g.in + spin * g.nnz;
-        for (int64_t e = p0 + warp; e < p1; e += NW) {
-            const BPair bp = g.bp[e];
+        double nxt[kFrag];
+        auto prefetch = [&](int e) {
+            const BPair bp = sm.bp[e];
+            const int na = sm.cov[bp.cicj & 0xffff].norb, nb = sm.cov[bp.cicj >> 16].norb;
+            if (na <= 16 && nb <= 16) load_dfrag(Ds + bp.off, na, nb, lane, nxt);
+        };
+        if (warp < nbp) prefetch(warp);
+        for (int e = warp; e < nbp; e += NW) {
+            double cur[kFrag];
+#pragma unroll
+            for (int i = 0; i < kFrag; ++i) cur[i] = nxt[i];
+            if (e + NW < nbp) prefetch(e + NW);
+            const BPair bp = sm.bp[e];
             const int ci = bp.cicj & 0xffff, cj = bp.cicj >> 16;
             const CoverS& A = sm.cov[ci];
             const CoverS& B = sm.cov[cj];
             const uint32_t om = octet_mask(A.mask & B.mask);
-            const int ks = (A.norb + 3) >> 2, tn = (B.norb + 7) >> 3;
             const double f = ci == cj ? 1.0 : 2.0;
-            const double* D = Ds + bp.off;
+            if (A.norb > 16 || B.norb > 16) {
+                rho_pair_big(sm.phi, A, B, om, Ds + bp.off, f, racc, lane);
+                continue;
+            }
+            const int ks = (A.norb + 3) >> 2, tn = (B.norb + 7) >> 3;
             switch (ks) {
-                case 1: rho_pair_tn<1>(tn, sm.phi, A, B, om, D, f, racc, lane); break;
-                case 2: rho_pair_tn<2>(tn, sm.phi, A, B, om, D, f, racc, lane); break;
-                case 3: rho_pair_tn<3>(tn, sm.phi, A, B, om, D, f, racc, lane); break;
-                case 4: rho_pair_tn<4>(tn, sm.phi, A, B, om, D, f, racc, lane); break;
-                case 5: rho_pair_tn<5>(tn, sm.phi, A, B, om, D, f, racc, lane); break;
-                case 6: rho_pair_tn<6>(tn, sm.phi, A, B, om, D, f, racc, lane); break;
-                case 7: rho_pair_tn<7>(tn, sm.phi, A, B, om, D, f, racc, lane); break;
-                default: rho_pair_tn<8>(tn, sm.phi, A, B, om, D, f, racc, lane); break;
+                case 1: rho_pair_tn<1>(tn, sm.phi, A, B, om, cur, f, racc, lane); break;
+                case 2: rho_pair_tn<2>(tn, sm.phi, A, B, om, cur, f, racc, lane); break;
+                case 3: rho_pair_tn<3>(tn, sm.phi, A, B, om, cur, f, racc, lane); break;
+                default: rho_pair_tn<4>(tn, sm.phi, A, B, om, cur, f, racc, lane); break;
             }
         }
         __syncthreads();
@@ -414,12 +512,17 @@ __global__ void k_dm_check(SysParams P, int64_t npair, int nspin, int64_t nnz, c
 
 __global__ void k_block_orbitals(GridArgs g, int64_t b, double* out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const Smem sm = carve(smem_raw, g.max_rows, 64);
-    const int ncov = stage_block(g, b, sm);
+    const Smem sm = carve(smem_raw, g.max_rows, 64, g.max_bpairs);
+    int nbp;
+    const int ncov = stage_block(g, b, sm, nbp);
     if (ncov == 0) return;
-    const int M = sm.cov[ncov - 1].row0 + sm.cov[ncov - 1].norb;
-    for (int i = threadIdx.x; i < M * 64; i += blockDim.x)
-        out[i] = sm.phi[phi_at(i >> 6, i & 63)];
+    // compact rows (drop the 4-alignment pad) in cover order
+    for (int c = 0; c < ncov; ++c) {
+        int r0 = 0;
+        for (int q = 0; q < c; ++q) r0 += sm.cov[q].norb;
+        for (int i = threadIdx.x; i < sm.cov[c].norb * 64; i += blockDim.x)
+            out[static_cast<size_t>(r0) * 64 + i] = sm.phi[phi_at(sm.cov[c].row0 + (i >> 6), i & 63)];
+    }
 }
 
 template <class K>
@@ -429,15 +532,15 @@ void set_smem(K kernel, size_t bytes) {
 
 }  // namespace
 
-size_t grid_smem_bytes(int max_rows, int max_cover, int nwarps, bool density) {
+size_t grid_smem_bytes(int max_rows, int max_cover, int max_bpairs, int nwarps, bool density) {
     return static_cast<size_t>(max_rows) * kPhiStride * sizeof(double) +
            static_cast<size_t>(density ? nwarps * 64 : 64) * sizeof(double) +
-           static_cast<size_t>(max_cover) * sizeof(CoverS);
+           static_cast<size_t>(max_bpairs) * sizeof(BPair) + static_cast<size_t>(max_cover) * sizeof(CoverS);
 }
 
 int launch_density(const GridArgs& g, int64_t nblk, int nwarps, cudaStream_t st) {
     if (nblk <= 0) return 0;
-    const size_t smem = grid_smem_bytes(g.max_rows, g.max_cover, nwarps, true);
+    const size_t smem = grid_smem_bytes(g.max_rows, g.max_cover, g.max_bpairs, nwarps, true);
     if (nwarps == 4) {
         set_smem(k_density<4>, smem);
         k_density<4><<<static_cast<unsigned>(nblk), 128, smem, st>>>(g);
@@ -451,7 +554,7 @@ int launch_density(const GridArgs& g, int64_t nblk, int nwarps, cudaStream_t st)
 
 int launch_hamiltonian(const GridArgs& g, int64_t nblk, int nwarps, cudaStream_t st) {
     if (nblk <= 0) return 0;
-    const size_t smem = grid_smem_bytes(g.max_rows, g.max_cover, nwarps, false);
+    const size_t smem = grid_smem_bytes(g.max_rows, g.max_cover, g.max_bpairs, nwarps, false);
     if (nwarps == 4) {
         set_smem(k_hamiltonian<4>, smem);
         k_hamiltonian<4><<<static_cast<unsigned>(nblk), 128, smem, st>>>(g);
@@ -483,7 +586,7 @@ int launch_dm_check(const DevIndex& ix, const SysParams& sys, int nspin, const d
 }
 
 int launch_block_orbitals(const GridArgs& g, int64_t block, double* d_out, cudaStream_t st) {
-    const size_t smem = grid_smem_bytes(g.max_rows, g.max_cover, 1, false);
+    const size_t smem = grid_smem_bytes(g.max_rows, g.max_cover, g.max_bpairs, 1, false);
     set_smem(k_block_orbitals, smem);
     k_block_orbitals<<<1, 256, smem, st>>>(g, block, d_out);
     KBG_CUDA(cudaGetLastError());

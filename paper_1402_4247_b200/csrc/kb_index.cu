@@ -240,7 +240,7 @@ __global__ void k_pair_mirror(SysParams P, int64_t npair, const int32_t* pa, con
 // ---- block work items -------------------------------------------------------
 struct Stats {
     unsigned long long sum_m, sum_m2, natompt;
-    int max_rows, max_cover;
+    int max_rows, max_cover, max_bpairs;
 };
 
 __global__ void k_bp_count(SysParams P, int64_t nblock, const int32_t* __restrict__ blk_ptr,
@@ -274,7 +274,7 @@ __global__ void k_bp_count(SysParams P, int64_t nblock, const int32_t* __restric
     }
     for (int c = c0 + lane; c < c1; c += 32) {
         nap += __popcll(cov_mask[c]);
-        rows += P.sp[P.spc[cov_atom[c]]].norb;
+        rows += (P.sp[P.spc[cov_atom[c]]].norb + 3) & ~3;  // Phi rows are 4-aligned per cover
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -293,6 +293,7 @@ __global__ void k_bp_count(SysParams P, int64_t nblock, const int32_t* __restric
         atomicAdd(&stats->natompt, nap);
         atomicMax(&stats->max_rows, rows);
         atomicMax(&stats->max_cover, c1 - c0);
+        atomicMax(&stats->max_bpairs, static_cast<int>(cnt));
     }
 }
 
@@ -329,6 +330,25 @@ __global__ void k_bp_fill(SysParams P, int64_t nblock, const int32_t* __restrict
             }
             pos += __popc(bal);
         }
+    }
+}
+
+// Orders each block's work items by cost, descending (ties: original order),
+// so the static round-robin warp assignment approximates LPT scheduling.
+__global__ void k_bp_sort(int64_t nblock, const int64_t* __restrict__ bp_ptr, const BPair* __restrict__ in,
+                          BPair* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t b = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    if (b >= nblock) return;
+    const int64_t p0 = bp_ptr[b], n = bp_ptr[b + 1] - p0;
+    for (int64_t i = lane; i < n; i += 32) {
+        const BPair e = in[p0 + i];
+        int64_t rank = 0;
+        for (int64_t j = 0; j < n; ++j) {
+            const int cj = in[p0 + j].cost;
+            rank += (cj > e.cost) || (cj == e.cost && j < i);
+        }
+        out[p0 + rank] = e;
     }
 }
 
@@ -473,8 +493,11 @@ void build_index_device(const SysParams& P, DevIndex& ix, cudaStream_t st) {
     ix.nbpair = exclusive_scan(bpc, ix.bp_ptr, nblock, st);
     cudaFree(bpc);
     ix.bp = dalloc<BPair>(ix.nbpair);
+    BPair* bp_unsorted = dalloc<BPair>(ix.nbpair);
     k_bp_fill<<<wgrid, T, 0, st>>>(P, nblock, ix.blk_ptr, ix.cov_atom, ix.cov_R, ix.cov_mask, ix.bp_ptr, ix.pair_key,
-                                   ix.pair_off, ix.npair, ix.bp, d_err);
+                                   ix.pair_off, ix.npair, bp_unsorted, d_err);
+    KBG_CUDA(cudaGetLastError());
+    k_bp_sort<<<wgrid, T, 0, st>>>(nblock, ix.bp_ptr, bp_unsorted, ix.bp);
     KBG_CUDA(cudaGetLastError());
     Stats hs;
     KBG_CUDA(cudaMemcpyAsync(&hs, d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, st));
@@ -482,6 +505,7 @@ void build_index_device(const SysParams& P, DevIndex& ix, cudaStream_t st) {
     KBG_CUDA(cudaStreamSynchronize(st));
     cudaFree(d_stats);
     cudaFree(d_err);
+    cudaFree(bp_unsorted);
     if (herr)
         throw Error(KBG_ERR_CONSISTENCY, "build_index: block " + std::to_string(herr - 1) +
                                              " has covers that share points but form no pair");
@@ -490,6 +514,7 @@ void build_index_device(const SysParams& P, DevIndex& ix, cudaStream_t st) {
     ix.natompt = static_cast<int64_t>(hs.natompt);
     ix.max_rows = hs.max_rows;
     ix.max_cover = hs.max_cover;
+    ix.max_bpairs = hs.max_bpairs;
 }
 
 void copy_index_to_host(const DevIndex& ix, HostIndex& h, cudaStream_t st) {

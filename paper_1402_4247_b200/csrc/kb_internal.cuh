@@ -87,8 +87,9 @@ struct DevIndex {
     int64_t* bp_ptr = nullptr;
     BPair* bp = nullptr;
     int64_t* blk_cost = nullptr;
-    int max_rows = 0;    // max orbitals covering one block
+    int max_rows = 0;    // max Phi rows of one block (orbitals, 4-aligned per cover)
     int max_cover = 0;   // max covers per block
+    int max_bpairs = 0;  // max work items per block
     int64_t natompt = 0;
     double sum_m = 0, sum_m2 = 0;
 };
@@ -112,6 +113,7 @@ struct GridArgs {
     int64_t blk_begin;  // first owned block
     int max_rows;       // Phi rows allocated (incl. pad)
     int max_cover;
+    int max_bpairs;
     int nspin;
     int64_t nnz;
     int64_t npts;
@@ -128,7 +130,7 @@ void free_index(DevIndex& ix);
 void copy_index_to_host(const DevIndex& ix, HostIndex& h, cudaStream_t st);
 
 // Grid kernels (kb_grid.cu). Return number of kernel launches.
-size_t grid_smem_bytes(int max_rows, int max_cover, int nwarps, bool density);
+size_t grid_smem_bytes(int max_rows, int max_cover, int max_bpairs, int nwarps, bool density);
 int launch_density(const GridArgs& g, int64_t nblk_owned, int nwarps, cudaStream_t st);
 int launch_hamiltonian(const GridArgs& g, int64_t nblk_owned, int nwarps, cudaStream_t st);
 int launch_mirror(const DevIndex& ix, const SysParams& sys, int nspin, double* h, cudaStream_t st);
