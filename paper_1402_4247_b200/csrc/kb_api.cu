@@ -164,7 +164,7 @@ kbg::GridArgs grid_args(kbg_ctx* c, int nspin, double dV, const double* in, doub
     g.bp_ptr = c->ix.bp_ptr;
     g.bp = c->ix.bp;
     g.blk_begin = c->blk_begin;
-    g.max_rows = ((c->ix.max_rows + kbg::kRowPad + 7) / 8) * 8;
+    g.max_phi = kbg::kZero + c->ix.max_phi + kbg::kTilePad;
     g.max_cover = c->ix.max_cover > 0 ? c->ix.max_cover : 1;
     g.max_bpairs = c->ix.max_bpairs > 0 ? c->ix.max_bpairs : 1;
     g.nspin = nspin;
@@ -177,7 +177,7 @@ kbg::GridArgs grid_args(kbg_ctx* c, int nspin, double dV, const double* in, doub
     g.out = out;
     if (g.max_cover > 32 * c->nwarps)
         throw Error(KBG_ERR_DIMENSION, "a grid block is covered by more atoms than threads per CTA");
-    const size_t smem = kbg::grid_smem_bytes(g.max_rows, g.max_cover, g.max_bpairs, c->nwarps, true);
+    const size_t smem = kbg::grid_smem_bytes(g.max_phi, g.max_cover, g.max_bpairs, c->nwarps, true);
     if (smem > 227 * 1024)
         throw Error(KBG_ERR_DIMENSION, "grid block needs " + std::to_string(smem) +
                                            " B of shared memory (> 227 KB): too many orbitals per block");

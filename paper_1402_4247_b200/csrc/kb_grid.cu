@@ -1,7 +1,8 @@
 // G2+G3 / G2+G4: fused orbital evaluation + density / Hamiltonian contraction.
 //
-// One CTA per 4x4x4 grid block (64 slots). The block's orbitals Phi
-// (M rows x 64 slots, FP64) are evaluated once into shared memory; every
+// One CTA per 4x4x4 grid block (64 slots). The block's orbitals Phi (FP64,
+// one norb x 4 tile per cover and active quad) are evaluated once into shared
+// memory; every
 // canonical cover pair (ci <= cj) sharing points is then one warp task:
 //   H : C(na x nb) += Phi_ci^T diag(V dV) Phi_cj  over active 1x2x2 quads
 //       -> mma.sync.m8n8k4.f64 (SASS DMMA), M = orbitals of ci, N = orbitals
@@ -20,10 +21,10 @@ namespace {
 struct CoverS {
     double t[3];
     uint64_t mask;
-    int row0;
+    uint32_t qmask;  // active 1x2x2 quads
+    int tbase;       // offset (doubles) of this cover's first quad tile
     int norb;
     int sp;
-    int atom;
 };
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
@@ -39,43 +40,40 @@ __device__ __forceinline__ uint32_t quad_mask(uint64_t m) {
     return q;
 }
 
-__device__ __forceinline__ uint32_t octet_mask(uint64_t m) {
-    uint32_t q = 0;
+__device__ __forceinline__ uint32_t octet_of_quads(uint32_t qm) {
+    uint32_t o = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) q |= static_cast<uint32_t>(((m >> (8 * i)) & 0xFFull) != 0) << i;
-    return q;
+    for (int i = 0; i < 8; ++i) o |= static_cast<uint32_t>(((qm >> (2 * i)) & 3u) != 0) << i;
+    return o;
 }
 
-// Shared-memory address of Phi[row][slot]. Every cover's rows start at a
-// multiple of 4 (pad rows zeroed); slots are XOR-swizzled by 4*f(row),
-// f(row) = (row ^ (row >> 2)) & 3, which is a permutation both on any 4
-// consecutive aligned rows (DMMA A/B fragments) and on rows {r, r+2, r+4, r+6}
-// (density epilogue), so every half-warp LDS.64 touches 32 distinct banks.
-__device__ __forceinline__ int phi_swz(int row) { return ((row ^ (row >> 2)) & 3) << 2; }
-__device__ __forceinline__ size_t phi_at(int row, int slot) {
-    return static_cast<size_t>(row) * kPhiStride + (slot ^ phi_swz(row));
+// Offset of the norb x 4 tile of quad q of cover cv (q must be active).
+__device__ __forceinline__ int tile_of(const CoverS& cv, int q) {
+    return cv.tbase + __popc(cv.qmask & ((1u << q) - 1u)) * cv.norb * 4;
 }
-
-__host__ __device__ __forceinline__ int align4(int n) { return (n + 3) & ~3; }
+// As tile_of, or the zero tile (offset 0) when q is inactive.
+__device__ __forceinline__ int tile_or_zero(const CoverS& cv, int q) {
+    return ((cv.qmask >> q) & 1u) ? tile_of(cv, q) : 0;
+}
 
 struct Smem {
-    double* phi;
+    double* phi;  // [kZero zeros][tiles...][kTilePad zeros]
     double* acc;  // w[64] (H) or racc[NW][64] (rho)
     BPair* bp;    // this block's work items
     CoverS* cov;
 };
 
-__device__ __forceinline__ Smem carve(unsigned char* base, int rows_alloc, int acc_doubles, int max_bpairs) {
+__device__ __forceinline__ Smem carve(unsigned char* base, int max_phi, int acc_doubles, int max_bpairs) {
     Smem s;
     s.phi = reinterpret_cast<double*>(base);
-    s.acc = s.phi + static_cast<size_t>(rows_alloc) * kPhiStride;
+    s.acc = s.phi + max_phi;
     s.bp = reinterpret_cast<BPair*>(s.acc + acc_doubles);
     s.cov = reinterpret_cast<CoverS*>(s.bp + max_bpairs);
     return s;
 }
 
 // Loads the covers and work items of block b into shared memory and evaluates
-// Phi. Returns the number of covers (uniform across the CTA).
+// Phi on the active quads. Returns the number of covers (uniform per CTA).
 __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int& nbp) {
     const int tid = threadIdx.x, nt = blockDim.x;
     const int c0 = g.blk_ptr[b], c1 = g.blk_ptr[b + 1];
@@ -87,31 +85,33 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int& nb
     if (tid < ncov) {
         CoverS& cv = sm.cov[tid];
         const int a = g.cov_atom[c0 + tid];
-        cv.atom = a;
         cv.sp = P.spc[a];
         cv.norb = P.sp[cv.sp].norb;
         cv.mask = g.cov_mask[c0 + tid];
+        cv.qmask = quad_mask(cv.mask);
         const int R0 = g.cov_R[3 * (c0 + tid)], R1 = g.cov_R[3 * (c0 + tid) + 1], R2 = g.cov_R[3 * (c0 + tid) + 2];
 #pragma unroll
         for (int c = 0; c < 3; ++c) cv.t[c] = P.tau[3 * a + c] + ((R0 * P.A[c] + R1 * P.A[3 + c]) + R2 * P.A[6 + c]);
     }
     for (int i = tid; i < nbp; i += nt) sm.bp[i] = g.bp[p0 + i];
+    for (int i = tid; i < kZero; i += nt) sm.phi[i] = 0.0;
     __syncthreads();
     if (tid < ncov) {
-        int r0 = 0;
-        for (int c = 0; c < tid; ++c) r0 += align4(sm.cov[c].norb);
-        sm.cov[tid].row0 = r0;
+        int base = kZero;
+        for (int c = 0; c < tid; ++c) base += __popc(sm.cov[c].qmask) * sm.cov[c].norb * 4;
+        sm.cov[tid].tbase = base;
     }
     __syncthreads();
-    const int M = sm.cov[ncov - 1].row0 + align4(sm.cov[ncov - 1].norb);
-    for (int i = tid; i < kRowPad * kPhiStride; i += nt) sm.phi[static_cast<size_t>(M) * kPhiStride + i] = 0.0;
+    const CoverS& last = sm.cov[ncov - 1];
+    const int end = last.tbase + __popc(last.qmask) * last.norb * 4;
+    for (int i = tid; i < kTilePad; i += nt) sm.phi[end + i] = 0.0;
     int bi, bj, bk;
     block_decode(P, b, bi, bj, bk);
     for (int task = tid; task < ncov * 64; task += nt) {
         const int c = task >> 6, s = task & 63;
         const CoverS& cv = sm.cov[c];
-        double* dst = sm.phi;
-        const int row0 = cv.row0;
+        if (!((cv.qmask >> (s >> 2)) & 1u)) continue;  // no tile for an inactive quad
+        double* dst = sm.phi + tile_of(cv, s >> 2) + (s & 3);
         if ((cv.mask >> s) & 1) {
             int li, lj, lk;
             slot_decode(s, li, lj, lk);
@@ -122,12 +122,10 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int& nb
             const double dy = (fi * P.A[1] + fj * P.A[4] + fk * P.A[7]) - cv.t[1];
             const double dz = (fi * P.A[2] + fj * P.A[5] + fk * P.A[8]) - cv.t[2];
             const double d2 = dx * dx + dy * dy + dz * dz;
-            eval_orbitals(P.sp[cv.sp], P.tables, dx, dy, dz, d2,
-                          [&](int o, double v) { dst[phi_at(row0 + o, s)] = v; });
+            eval_orbitals(P.sp[cv.sp], P.tables, dx, dy, dz, d2, [&](int o, double v) { dst[4 * o] = v; });
         } else {
-            for (int o = 0; o < cv.norb; ++o) dst[phi_at(row0 + o, s)] = 0.0;
+            for (int o = 0; o < cv.norb; ++o) dst[4 * o] = 0.0;
         }
-        for (int o = cv.norb; o < align4(cv.norb); ++o) dst[phi_at(row0 + o, s)] = 0.0;
     }
     __syncthreads();
     return ncov;
@@ -142,9 +140,10 @@ __device__ __forceinline__ int64_t slot_point(const SysParams& P, int bi, int bj
 }
 
 // ---- H pair task ---------------------------------------------------------------
-// C(na x nb) = sum over active quads q of A(na x 4) B(4 x nb), A = Phi_ci * w,
-// B = Phi_cj^T. Pairs with <= 2 output tiles alternate two accumulator sets
-// over the quads so that two independent DMMA chains are in flight.
+// C(na x nb) = sum over common quads q of A(na x 4) B(4 x nb), A = Phi_ci w,
+// B = Phi_cj^T. The DMMA A/B fragments of a quad are 32 consecutive doubles of
+// the quad tile (lane = 4*row + point). Pairs with <= 2 output tiles alternate
+// two accumulator sets so that two independent DMMA chains are in flight.
 template <int TM, int TN>
 __device__ __forceinline__ void h_pair(const double* __restrict__ phi, const double* __restrict__ w, const CoverS& A,
                                        const CoverS& B, uint32_t qm, double* __restrict__ H, double sign, int scatter,
@@ -157,26 +156,21 @@ __device__ __forceinline__ void h_pair(const double* __restrict__ phi, const dou
         for (int i = 0; i < TM; ++i)
 #pragma unroll
             for (int j = 0; j < TN; ++j) c[u][i][j][0] = c[u][i][j][1] = 0.0;
-    const int ra = A.row0 + (lane >> 2), rb = B.row0 + (lane >> 2);
-    const double* pa = phi + static_cast<size_t>(ra) * kPhiStride + (lane & 3);
-    const double* pb = phi + static_cast<size_t>(rb) * kPhiStride + (lane & 3);
-    const int sa = phi_swz(ra), sb = phi_swz(rb);  // same for every 8-row tile (8 = 0 mod 4, f(r+8) = f(r) ^ 2)
     const double* pw = w + (lane & 3);
     auto step = [&](int u, int q) {
-        const int col = 4 * q;
-        const double wv = pw[col];
+        const double wv = pw[4 * q];
+        const double* ta = phi + tile_of(A, q) + lane;
+        const double* tb = phi + tile_of(B, q) + lane;
         double a[TM], b[TN];
 #pragma unroll
-        for (int i = 0; i < TM; ++i) a[i] = pa[i * 8 * kPhiStride + (col ^ phi_swz(ra + 8 * i) ^ 0)] * wv;
+        for (int i = 0; i < TM; ++i) a[i] = ta[32 * i] * wv;
 #pragma unroll
-        for (int j = 0; j < TN; ++j) b[j] = pb[j * 8 * kPhiStride + (col ^ phi_swz(rb + 8 * j))];
+        for (int j = 0; j < TN; ++j) b[j] = tb[32 * j];
 #pragma unroll
         for (int i = 0; i < TM; ++i)
 #pragma unroll
             for (int j = 0; j < TN; ++j) dmma(c[u][i][j], a[i], b[j]);
     };
-    (void)sa;
-    (void)sb;
     while (qm) {
         const int q0 = __ffs(qm) - 1;
         qm &= qm - 1;
@@ -221,9 +215,9 @@ __device__ __forceinline__ void h_pair_tn(int tn, const double* phi, const doubl
 }
 
 template <int NW>
-__global__ void __launch_bounds__(NW * 32) k_hamiltonian(GridArgs g) {
+__global__ void __launch_bounds__(NW * 32, 2) k_hamiltonian(GridArgs g) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const Smem sm = carve(smem_raw, g.max_rows, 64, g.max_bpairs);
+    const Smem sm = carve(smem_raw, g.max_phi, 64, g.max_bpairs);
     const int64_t b = g.blk_begin + blockIdx.x;
     int nbp;
     const int ncov = stage_block(g, b, sm, nbp);
@@ -258,8 +252,11 @@ __global__ void __launch_bounds__(NW * 32) k_hamiltonian(GridArgs g) {
 }
 
 // ---- rho pair task -------------------------------------------------------------
-// Fast path (na, nb <= 16): DM fragments arrive in registers (prefetched one
-// pair ahead); two octets are processed per iteration for DMMA ILP.
+// Per active octet o (quads 2o, 2o+1): X(8 slots x nb) = Phi_ci^T DM, the A
+// fragment of lane l is Phi_ci[4s + (l&3)][slot] read from the tile of quad
+// 2o + (l>>4) (zero tile when inactive). Fast path (na, nb <= 16): DM
+// fragments in registers, prefetched one pair ahead; two octets per
+// iteration for DMMA ILP.
 constexpr int kFrag = 8;  // B fragments per lane for na, nb <= 16: (4 K-steps) x (2 N-tiles)
 
 __device__ __forceinline__ void load_dfrag(const double* __restrict__ D, int na, int nb, int lane,
@@ -274,9 +271,18 @@ __device__ __forceinline__ void load_dfrag(const double* __restrict__ D, int na,
 }
 
 template <int KS, int TN, int NO>
-__device__ __forceinline__ void rho_octets(const double* __restrict__ pa, const double* __restrict__ pbr, int ra,
-                                           int rb, const int (&col)[2], const double (&bf)[kFrag], double f,
+__device__ __forceinline__ void rho_octets(const double* __restrict__ phi, const CoverS& A, const CoverS& B,
+                                           const int (&oct)[2], const double (&bf)[kFrag], double f,
                                            double* __restrict__ racc, int lane) {
+    const int half = lane >> 4, pt = (lane >> 2) & 3;
+    const double* ta[NO];
+    const double* tb[NO];
+#pragma unroll
+    for (int o = 0; o < NO; ++o) {
+        const int q = 2 * oct[o] + half;
+        ta[o] = phi + tile_or_zero(A, q) + 4 * (lane & 3) + pt;
+        tb[o] = phi + tile_or_zero(B, q) + 8 * (lane & 3) + pt;
+    }
     double x[NO][TN][2];
 #pragma unroll
     for (int o = 0; o < NO; ++o)
@@ -284,10 +290,9 @@ __device__ __forceinline__ void rho_octets(const double* __restrict__ pa, const 
         for (int t = 0; t < TN; ++t) x[o][t][0] = x[o][t][1] = 0.0;
 #pragma unroll
     for (int s = 0; s < KS; ++s) {
-        const int sw = phi_swz(ra + 4 * s);
         double a[NO];
 #pragma unroll
-        for (int o = 0; o < NO; ++o) a[o] = pa[4 * s * kPhiStride + (col[o] ^ sw)];
+        for (int o = 0; o < NO; ++o) a[o] = ta[o][16 * s];
 #pragma unroll
         for (int o = 0; o < NO; ++o)
 #pragma unroll
@@ -299,13 +304,10 @@ __device__ __forceinline__ void rho_octets(const double* __restrict__ pa, const 
 #pragma unroll
         for (int t = 0; t < TN; ++t)
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int row = rb + 8 * t + e;
-                part += x[o][t][e] * pbr[(8 * t + e) * kPhiStride + (col[o] ^ phi_swz(row))];
-            }
+            for (int e = 0; e < 2; ++e) part += x[o][t][e] * tb[o][32 * t + 4 * e];
         part += __shfl_xor_sync(0xffffffffu, part, 1);
         part += __shfl_xor_sync(0xffffffffu, part, 2);
-        if ((lane & 3) == 0) racc[col[o]] += f * part;
+        if ((lane & 3) == 0) racc[8 * oct[o] + (lane >> 2)] += f * part;
     }
 }
 
@@ -313,50 +315,46 @@ template <int KS, int TN>
 __device__ __forceinline__ void rho_pair(const double* __restrict__ phi, const CoverS& A, const CoverS& B,
                                          uint32_t om, const double (&bf)[kFrag], double f, double* __restrict__ racc,
                                          int lane) {
-    const int ra = A.row0 + (lane & 3), rb = B.row0 + (lane & 3) * 2;
-    const double* pa = phi + static_cast<size_t>(ra) * kPhiStride;
-    const double* pbr = phi + static_cast<size_t>(rb) * kPhiStride;
     while (om) {
-        int col[2];
-        col[0] = (__ffs(om) - 1) * 8 + (lane >> 2);
+        int oct[2];
+        oct[0] = __ffs(om) - 1;
         om &= om - 1;
         if (om) {
-            col[1] = (__ffs(om) - 1) * 8 + (lane >> 2);
+            oct[1] = __ffs(om) - 1;
             om &= om - 1;
-            rho_octets<KS, TN, 2>(pa, pbr, ra, rb, col, bf, f, racc, lane);
+            rho_octets<KS, TN, 2>(phi, A, B, oct, bf, f, racc, lane);
         } else {
-            col[1] = col[0];
-            rho_octets<KS, TN, 1>(pa, pbr, ra, rb, col, bf, f, racc, lane);
+            oct[1] = oct[0];
+            rho_octets<KS, TN, 1>(phi, A, B, oct, bf, f, racc, lane);
         }
     }
 }
 
 // General path for atoms with more than 16 orbitals (not used by Fe3O4).
-__device__ void rho_pair_big(const double* __restrict__ phi, const CoverS& A, const CoverS& B, uint32_t om,
+__device__ __noinline__ void rho_pair_big(const double* __restrict__ phi, const CoverS& A, const CoverS& B, uint32_t om,
                              const double* __restrict__ D, double f, double* __restrict__ racc, int lane) {
     const int na = A.norb, nb = B.norb;
     const int ks = (na + 3) >> 2, tn = (nb + 7) >> 3;
+    const int half = lane >> 4, pt = (lane >> 2) & 3;
     while (om) {
-        const int col = (__ffs(om) - 1) * 8 + (lane >> 2);
+        const int o = __ffs(om) - 1;
         om &= om - 1;
+        const int q = 2 * o + half;
+        const double* ta = phi + tile_or_zero(A, q) + 4 * (lane & 3) + pt;
+        const double* tb = phi + tile_or_zero(B, q) + 8 * (lane & 3) + pt;
         double part = 0.0;
         for (int t = 0; t < tn; ++t) {
             double x[2] = {0.0, 0.0};
             for (int s = 0; s < ks; ++s) {
                 const int k = 4 * s + (lane & 3), n = 8 * t + (lane >> 2);
                 const double bv = (k < na && n < nb) ? __ldg(D + k * nb + n) : 0.0;
-                const int ra = A.row0 + 4 * s + (lane & 3);
-                dmma(x, phi[phi_at(ra, col)], bv);
+                dmma(x, ta[16 * s], bv);
             }
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int row = B.row0 + 8 * t + (lane & 3) * 2 + e;
-                part += x[e] * phi[phi_at(row, col)];
-            }
+            part += x[0] * tb[32 * t] + x[1] * tb[32 * t + 4];
         }
         part += __shfl_xor_sync(0xffffffffu, part, 1);
         part += __shfl_xor_sync(0xffffffffu, part, 2);
-        if ((lane & 3) == 0) racc[col] += f * part;
+        if ((lane & 3) == 0) racc[8 * o + (lane >> 2)] += f * part;
     }
 }
 
@@ -370,9 +368,9 @@ __device__ __forceinline__ void rho_pair_tn(int tn, const double* phi, const Cov
 }
 
 template <int NW>
-__global__ void __launch_bounds__(NW * 32) k_density(GridArgs g) {
+__global__ void __launch_bounds__(NW * 32, 2) k_density(GridArgs g) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const Smem sm = carve(smem_raw, g.max_rows, NW * 64, g.max_bpairs);
+    const Smem sm = carve(smem_raw, g.max_phi, NW * 64, g.max_bpairs);
     const int64_t b = g.blk_begin + blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int bi, bj, bk;
@@ -409,7 +407,7 @@ __global__ void __launch_bounds__(NW * 32) k_density(GridArgs g) {
             const int ci = bp.cicj & 0xffff, cj = bp.cicj >> 16;
             const CoverS& A = sm.cov[ci];
             const CoverS& B = sm.cov[cj];
-            const uint32_t om = octet_mask(A.mask & B.mask);
+            const uint32_t om = octet_of_quads(quad_mask(A.mask & B.mask));
             const double f = ci == cj ? 1.0 : 2.0;
             if (A.norb > 16 || B.norb > 16) {
                 rho_pair_big(sm.phi, A, B, om, Ds + bp.off, f, racc, lane);
@@ -512,16 +510,19 @@ __global__ void k_dm_check(SysParams P, int64_t npair, int nspin, int64_t nnz, c
 
 __global__ void k_block_orbitals(GridArgs g, int64_t b, double* out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const Smem sm = carve(smem_raw, g.max_rows, 64, g.max_bpairs);
+    const Smem sm = carve(smem_raw, g.max_phi, 64, g.max_bpairs);
     int nbp;
     const int ncov = stage_block(g, b, sm, nbp);
     if (ncov == 0) return;
-    // compact rows (drop the 4-alignment pad) in cover order
+    // unpack the quad tiles to [orbital][slot] rows in cover order
+    int r0 = 0;
     for (int c = 0; c < ncov; ++c) {
-        int r0 = 0;
-        for (int q = 0; q < c; ++q) r0 += sm.cov[q].norb;
-        for (int i = threadIdx.x; i < sm.cov[c].norb * 64; i += blockDim.x)
-            out[static_cast<size_t>(r0) * 64 + i] = sm.phi[phi_at(sm.cov[c].row0 + (i >> 6), i & 63)];
+        const CoverS& cv = sm.cov[c];
+        for (int i = threadIdx.x; i < cv.norb * 64; i += blockDim.x) {
+            const int o = i >> 6, s = i & 63;
+            out[static_cast<size_t>(r0) * 64 + i] = sm.phi[tile_or_zero(cv, s >> 2) + 4 * o + (s & 3)];
+        }
+        r0 += cv.norb;
     }
 }
 
@@ -532,15 +533,15 @@ void set_smem(K kernel, size_t bytes) {
 
 }  // namespace
 
-size_t grid_smem_bytes(int max_rows, int max_cover, int max_bpairs, int nwarps, bool density) {
-    return static_cast<size_t>(max_rows) * kPhiStride * sizeof(double) +
+size_t grid_smem_bytes(int max_phi, int max_cover, int max_bpairs, int nwarps, bool density) {
+    return static_cast<size_t>(max_phi) * sizeof(double) +
            static_cast<size_t>(density ? nwarps * 64 : 64) * sizeof(double) +
            static_cast<size_t>(max_bpairs) * sizeof(BPair) + static_cast<size_t>(max_cover) * sizeof(CoverS);
 }
 
 int launch_density(const GridArgs& g, int64_t nblk, int nwarps, cudaStream_t st) {
     if (nblk <= 0) return 0;
-    const size_t smem = grid_smem_bytes(g.max_rows, g.max_cover, g.max_bpairs, nwarps, true);
+    const size_t smem = grid_smem_bytes(g.max_phi, g.max_cover, g.max_bpairs, nwarps, true);
     if (nwarps == 4) {
         set_smem(k_density<4>, smem);
         k_density<4><<<static_cast<unsigned>(nblk), 128, smem, st>>>(g);
@@ -554,7 +555,7 @@ int launch_density(const GridArgs& g, int64_t nblk, int nwarps, cudaStream_t st)
 
 int launch_hamiltonian(const GridArgs& g, int64_t nblk, int nwarps, cudaStream_t st) {
     if (nblk <= 0) return 0;
-    const size_t smem = grid_smem_bytes(g.max_rows, g.max_cover, g.max_bpairs, nwarps, false);
+    const size_t smem = grid_smem_bytes(g.max_phi, g.max_cover, g.max_bpairs, nwarps, false);
     if (nwarps == 4) {
         set_smem(k_hamiltonian<4>, smem);
         k_hamiltonian<4><<<static_cast<unsigned>(nblk), 128, smem, st>>>(g);
@@ -586,7 +587,7 @@ int launch_dm_check(const DevIndex& ix, const SysParams& sys, int nspin, const d
 }
 
 int launch_block_orbitals(const GridArgs& g, int64_t block, double* d_out, cudaStream_t st) {
-    const size_t smem = grid_smem_bytes(g.max_rows, g.max_cover, g.max_bpairs, 1, false);
+    const size_t smem = grid_smem_bytes(g.max_phi, g.max_cover, g.max_bpairs, 1, false);
     set_smem(k_block_orbitals, smem);
     k_block_orbitals<<<1, 256, smem, st>>>(g, block, d_out);
     KBG_CUDA(cudaGetLastError());

@@ -240,7 +240,7 @@ __global__ void k_pair_mirror(SysParams P, int64_t npair, const int32_t* pa, con
 // ---- block work items -------------------------------------------------------
 struct Stats {
     unsigned long long sum_m, sum_m2, natompt;
-    int max_rows, max_cover, max_bpairs;
+    int max_phi, max_cover, max_bpairs;
 };
 
 __global__ void k_bp_count(SysParams P, int64_t nblock, const int32_t* __restrict__ blk_ptr,
@@ -274,7 +274,9 @@ __global__ void k_bp_count(SysParams P, int64_t nblock, const int32_t* __restric
     }
     for (int c = c0 + lane; c < c1; c += 32) {
         nap += __popcll(cov_mask[c]);
-        rows += (P.sp[P.spc[cov_atom[c]]].norb + 3) & ~3;  // Phi rows are 4-aligned per cover
+        uint32_t qm = 0;  // active 1x2x2 quads -> one norb x 4 tile each
+        for (int q = 0; q < 16; ++q) qm |= static_cast<uint32_t>(((cov_mask[c] >> (4 * q)) & 0xFull) != 0) << q;
+        rows += __popc(qm) * P.sp[P.spc[cov_atom[c]]].norb * 4;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -291,7 +293,7 @@ __global__ void k_bp_count(SysParams P, int64_t nblock, const int32_t* __restric
         atomicAdd(&stats->sum_m, sm);
         atomicAdd(&stats->sum_m2, sm2);
         atomicAdd(&stats->natompt, nap);
-        atomicMax(&stats->max_rows, rows);
+        atomicMax(&stats->max_phi, rows);
         atomicMax(&stats->max_cover, c1 - c0);
         atomicMax(&stats->max_bpairs, static_cast<int>(cnt));
     }
@@ -512,7 +514,7 @@ void build_index_device(const SysParams& P, DevIndex& ix, cudaStream_t st) {
     ix.sum_m = static_cast<double>(hs.sum_m);
     ix.sum_m2 = static_cast<double>(hs.sum_m2);
     ix.natompt = static_cast<int64_t>(hs.natompt);
-    ix.max_rows = hs.max_rows;
+    ix.max_phi = hs.max_phi;
     ix.max_cover = hs.max_cover;
     ix.max_bpairs = hs.max_bpairs;
 }

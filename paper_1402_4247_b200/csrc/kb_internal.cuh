@@ -14,8 +14,12 @@ namespace kbg {
 
 constexpr int kMaxSpecies = 8;
 constexpr int kMaxRad = 16;
-constexpr int kPhiStride = 64;  // doubles per Phi row (one per slot); columns XOR-swizzled by row, see phi_col
-constexpr int kRowPad = 8;      // zeroed rows after the last orbital (tile overrun of the 8-row DMMA tiles)
+// Phi of a block is stored as quad tiles: for every cover and every active
+// 1x2x2 quad of its mask, norb x 4 doubles (orbital-major). kZero doubles of
+// zeros sit in front (the tile of an inactive quad) and kTilePad behind (tile
+// overrun of the 8-row DMMA fragments).
+constexpr int kZero = (KBG_MAX_ORB_PER_ATOM + 8) * 4;
+constexpr int kTilePad = 8 * 4;
 
 // Error taxonomy of kband (common.hpp:21-38) carried as a status code.
 struct Error : std::runtime_error {
@@ -87,7 +91,7 @@ struct DevIndex {
     int64_t* bp_ptr = nullptr;
     BPair* bp = nullptr;
     int64_t* blk_cost = nullptr;
-    int max_rows = 0;    // max Phi rows of one block (orbitals, 4-aligned per cover)
+    int max_phi = 0;     // max Phi quad-tile doubles of one block
     int max_cover = 0;   // max covers per block
     int max_bpairs = 0;  // max work items per block
     int64_t natompt = 0;
@@ -111,7 +115,7 @@ struct GridArgs {
     const int64_t* bp_ptr;
     const BPair* bp;
     int64_t blk_begin;  // first owned block
-    int max_rows;       // Phi rows allocated (incl. pad)
+    int max_phi;        // Phi doubles allocated (tiles + zero + pad)
     int max_cover;
     int max_bpairs;
     int nspin;
@@ -130,7 +134,7 @@ void free_index(DevIndex& ix);
 void copy_index_to_host(const DevIndex& ix, HostIndex& h, cudaStream_t st);
 
 // Grid kernels (kb_grid.cu). Return number of kernel launches.
-size_t grid_smem_bytes(int max_rows, int max_cover, int max_bpairs, int nwarps, bool density);
+size_t grid_smem_bytes(int max_phi, int max_cover, int max_bpairs, int nwarps, bool density);
 int launch_density(const GridArgs& g, int64_t nblk_owned, int nwarps, cudaStream_t st);
 int launch_hamiltonian(const GridArgs& g, int64_t nblk_owned, int nwarps, cudaStream_t st);
 int launch_mirror(const DevIndex& ix, const SysParams& sys, int nspin, double* h, cudaStream_t st);
