@@ -1,6 +1,7 @@
 // C-ABI of libkbgrid (include/kbgrid.h): context, validation, host/device
 // entry points. Errors follow the kband taxonomy (common.hpp:21-38) as status
 // codes with a message naming the failing field (kbg_last_error).
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -154,7 +155,7 @@ void check_nspin(int nspin) {
     if (nspin < 1 || nspin > 2) throw Error(KBG_ERR_CONFIG, "nspin must be 1 or 2");
 }
 
-kbg::GridArgs grid_args(kbg_ctx* c, int nspin, double dV, const double* in, double* out) {
+kbg::GridArgs grid_args(kbg_ctx* c, int nspin, double dV, const double* in, double* out, bool density) {
     kbg::GridArgs g{};
     g.sys = c->P;
     g.blk_ptr = c->ix.blk_ptr;
@@ -164,9 +165,13 @@ kbg::GridArgs grid_args(kbg_ctx* c, int nspin, double dV, const double* in, doub
     g.bp_ptr = c->ix.bp_ptr;
     g.bp = c->ix.bp;
     g.blk_begin = c->blk_begin;
-    g.max_phi = kbg::kZero + c->ix.max_phi + kbg::kTilePad;
+    g.max_rows = c->ix.max_rows_padded + 8;
     g.max_cover = c->ix.max_cover > 0 ? c->ix.max_cover : 1;
     g.max_bpairs = c->ix.max_bpairs > 0 ? c->ix.max_bpairs : 1;
+    g.t_ptr = density ? c->ix.rt_ptr : c->ix.ht_ptr;
+    g.tasks = density ? c->ix.rt : c->ix.ht;
+    g.t_wptr = density ? c->ix.rt_wptr : c->ix.ht_wptr;
+    g.max_tasks = std::max(1, density ? c->ix.max_rtask : c->ix.max_htask);
     g.nspin = nspin;
     g.nnz = c->ix.nnz;
     g.npts = c->npts;
@@ -175,9 +180,9 @@ kbg::GridArgs grid_args(kbg_ctx* c, int nspin, double dV, const double* in, doub
     g.scatter = c->scatter;
     g.in = in;
     g.out = out;
-    if (g.max_cover > 32 * c->nwarps)
-        throw Error(KBG_ERR_DIMENSION, "a grid block is covered by more atoms than threads per CTA");
-    const size_t smem = kbg::grid_smem_bytes(g.max_phi, g.max_cover, g.max_bpairs, c->nwarps, true);
+    if (g.max_cover > 32 * c->nwarps || g.max_cover > kbg::kMaxCoverPerBlock)
+        throw Error(KBG_ERR_DIMENSION, "a grid block is covered by too many atom images");
+    const size_t smem = kbg::grid_smem_bytes(g, c->nwarps, density);
     if (smem > 227 * 1024)
         throw Error(KBG_ERR_DIMENSION, "grid block needs " + std::to_string(smem) +
                                            " B of shared memory (> 227 KB): too many orbitals per block");
@@ -264,6 +269,7 @@ int kbg_build_index(kbg_ctx* c) {
         c->built = false;
         c->hix = kbg::HostIndex();
         kbg::build_index_device(c->P, c->ix, c->stream);
+        kbg::build_tasks_device(c->P, c->ix, c->stream);
         shard(c);
         c->built = true;
     });
@@ -312,7 +318,7 @@ int kbg_density_dev(kbg_ctx* c, int nspin, const double* d_dm, double* d_rho, vo
         check_nspin(nspin);
         require_index(c);
         KBG_CUDA(cudaSetDevice(c->device));
-        const kbg::GridArgs g = grid_args(c, nspin, 0.0, d_dm, d_rho);
+        const kbg::GridArgs g = grid_args(c, nspin, 0.0, d_dm, d_rho, true);
         c->last_launches = kbg::launch_density(g, c->blk_end - c->blk_begin, c->nwarps,
                                                static_cast<cudaStream_t>(stream));
         c->tally.flops = nspin * (2.0 * c->ix.sum_m2 + 2.0 * c->ix.sum_m);
@@ -329,7 +335,7 @@ int kbg_hamiltonian_accumulate_dev(kbg_ctx* c, int nspin, const double* d_veff, 
         KBG_CUDA(cudaSetDevice(c->device));
         const cudaStream_t st = static_cast<cudaStream_t>(stream);
         KBG_CUDA(cudaMemsetAsync(d_h, 0, sizeof(double) * nspin * c->ix.nnz, st));
-        const kbg::GridArgs g = grid_args(c, nspin, dV, d_veff, d_h);
+        const kbg::GridArgs g = grid_args(c, nspin, dV, d_veff, d_h, false);
         c->last_launches = kbg::launch_hamiltonian(g, c->blk_end - c->blk_begin, c->nwarps, st);
         c->tally.flops = nspin * 2.0 * c->ix.sum_m2;
         c->tally.bytes = 8.0 * nspin * (c->ix.nnz + c->npts);
@@ -380,7 +386,7 @@ int kbg_density(kbg_ctx* c, int nspin, const double* dm, double* rho) {
         if (dmax > 1e-13 * amax)
             throw Error(KBG_ERR_CONSISTENCY, "density: DM violates DM_ba(-R) = DM_ab(R)^T by " + std::to_string(dmax));
         if (c->nranks > 1) KBG_CUDA(cudaMemsetAsync(c->d_out, 0, nout * sizeof(double), c->stream));
-        const kbg::GridArgs g = grid_args(c, nspin, 0.0, c->d_in, c->d_out);
+        const kbg::GridArgs g = grid_args(c, nspin, 0.0, c->d_in, c->d_out, true);
         c->last_launches = 1 + kbg::launch_density(g, c->blk_end - c->blk_begin, c->nwarps, c->stream);
         KBG_CUDA(cudaMemcpyAsync(rho, c->d_out, nout * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         KBG_CUDA(cudaStreamSynchronize(c->stream));
@@ -401,7 +407,7 @@ int kbg_hamiltonian(kbg_ctx* c, int nspin, const double* veff, double dV, double
         ensure(c->d_out, c->cap_out, nout);
         KBG_CUDA(cudaMemcpyAsync(c->d_in, veff, nin * sizeof(double), cudaMemcpyHostToDevice, c->stream));
         KBG_CUDA(cudaMemsetAsync(c->d_out, 0, nout * sizeof(double), c->stream));
-        const kbg::GridArgs g = grid_args(c, nspin, dV, c->d_in, c->d_out);
+        const kbg::GridArgs g = grid_args(c, nspin, dV, c->d_in, c->d_out, false);
         int n = kbg::launch_hamiltonian(g, c->blk_end - c->blk_begin, c->nwarps, c->stream);
         n += kbg::launch_mirror(c->ix, c->P, nspin, c->d_out, c->stream);
         c->last_launches = n;
@@ -426,7 +432,7 @@ int kbg_block_orbitals(kbg_ctx* c, int64_t block, double* out, int64_t cap, int*
         if (static_cast<int64_t>(M) * 64 > cap) throw Error(KBG_ERR_DIMENSION, "block_orbitals: cap too small");
         if (M == 0) return;
         ensure(c->d_out, c->cap_out, static_cast<size_t>(M) * 64);
-        const kbg::GridArgs g = grid_args(c, 1, 0.0, nullptr, nullptr);
+        const kbg::GridArgs g = grid_args(c, 1, 0.0, nullptr, nullptr, false);
         kbg::launch_block_orbitals(g, block, c->d_out, c->stream);
         KBG_CUDA(cudaMemcpyAsync(out, c->d_out, sizeof(double) * M * 64, cudaMemcpyDeviceToHost, c->stream));
         KBG_CUDA(cudaStreamSynchronize(c->stream));

@@ -114,3 +114,54 @@ __device__ __forceinline__ int64_t find_pair(const int64_t* __restrict__ keys, i
 }
 
 }  // namespace kbg
+
+namespace kbg {
+
+// Row groups of a block (shared by the task builder and the grid kernels):
+// consecutive covers are packed into groups of <= kGroupRows orbitals; a cover
+// with more orbitals forms a group of its own. Group rows are padded to a
+// multiple of 8 (DMMA row tiles); covers' rows are contiguous inside a group.
+// norb(c) gives the orbital count of local cover c. Returns the group count.
+template <class NorbF>
+__host__ __device__ inline int make_groups(int ncov, NorbF norb, int* g_first, int* g_end, int* g_row0,
+                                           int* g_rows, int* c_row0, int* c_group) {
+    int ng = 0, next_row = 0, cur = 0;  // cur = rows used by the open group (0: none open)
+    for (int c = 0; c < ncov; ++c) {
+        const int n = norb(c);
+        if (cur == 0 || cur + n > kGroupRows) {
+            if (cur > 0) {
+                g_rows[ng - 1] = (cur + 7) & ~7;
+                next_row = g_row0[ng - 1] + g_rows[ng - 1];
+            }
+            g_first[ng] = c;
+            g_row0[ng] = next_row;
+            ++ng;
+            cur = 0;
+        }
+        c_row0[c] = g_row0[ng - 1] + cur;
+        c_group[c] = ng - 1;
+        cur += n;
+        g_end[ng - 1] = c + 1;
+        if (cur >= kGroupRows) {
+            g_rows[ng - 1] = (cur + 7) & ~7;
+            next_row = g_row0[ng - 1] + g_rows[ng - 1];
+            cur = 0;
+        }
+    }
+    if (cur > 0) g_rows[ng - 1] = (cur + 7) & ~7;
+    return ng;
+}
+
+__host__ __device__ __forceinline__ uint32_t quads_of(uint64_t m) {
+    uint32_t q = 0;
+    for (int i = 0; i < 16; ++i) q |= static_cast<uint32_t>(((m >> (4 * i)) & 0xFull) != 0) << i;
+    return q;
+}
+
+__host__ __device__ __forceinline__ uint32_t octets_of(uint64_t m) {
+    uint32_t q = 0;
+    for (int i = 0; i < 8; ++i) q |= static_cast<uint32_t>(((m >> (8 * i)) & 0xFFull) != 0) << i;
+    return q;
+}
+
+}  // namespace kbg

@@ -1,17 +1,20 @@
 // G2+G3 / G2+G4: fused orbital evaluation + density / Hamiltonian contraction.
 //
-// One CTA per 4x4x4 grid block (64 slots). The block's orbitals Phi (FP64,
-// one norb x 4 tile per cover and active quad) are evaluated once into shared
-// memory; every
-// canonical cover pair (ci <= cj) sharing points is then one warp task:
-//   H : C(na x nb) += Phi_ci^T diag(V dV) Phi_cj  over active 1x2x2 quads
-//       -> mma.sync.m8n8k4.f64 (SASS DMMA), M = orbitals of ci, N = orbitals
-//       of cj, K = 4 slots of a quad; FP64 atomics into the canonical pair
-//       block, mirrored afterwards.
-//   rho: X(8 slots x nb) = Phi_ci^T(8 x na) DM(na x nb) per active 2x2x2 octet
-//       -> DMMA with M = 8 slots, K = 4 orbitals of ci, N = 8 orbitals of cj;
-//       rho(slot) += f * sum_j X Phi_cj (f = 2 off-diagonal, DM symmetric),
-//       per-warp shared accumulators summed in fixed order (deterministic).
+// One CTA per 4x4x4 grid block (64 slots). Phi (FP64, M rows x 64 slots) is
+// evaluated once into shared memory; rows are the block's covers (atom
+// images) packed into row groups of <= 16 orbitals (two 8-row DMMA tiles).
+// Work is split into per-block task lists built at index time and
+// LPT-balanced over the CTA's warps (kb_tasks.cu):
+//   H  task (group g, partner cover cj >= first(g)):
+//        C(16 x 8*TN) += Phi_g^T diag(V dV) Phi_cj over the common 1x2x2 quads,
+//        mma.sync.m8n8k4.f64 (SASS DMMA), K = 4 slots of a quad; canonical rows
+//        (cover ci <= cj) are scattered with FP64 atomics, mirrored afterwards.
+//   rho task (group g, octet half h):
+//        Y(16 x 8 slots) += D'(16 x n_cj) Phi_cj(n_cj x 8) summed over all
+//        partners cj >= first(g) in registers (D' = 2 DM for ci < cj, DM for
+//        ci == cj: the symmetric half), then once per task
+//        rho(slot) += sum_rows Phi_g * Y. Per-warp shared accumulators are
+//        summed in a fixed order, so rho is bitwise deterministic.
 #include "kb_device.cuh"
 
 namespace kbg {
@@ -21,10 +24,14 @@ namespace {
 struct CoverS {
     double t[3];
     uint64_t mask;
-    uint32_t qmask;  // active 1x2x2 quads
-    int tbase;       // offset (doubles) of this cover's first quad tile
+    int row0;
     int norb;
     int sp;
+    int grp;
+};
+
+struct GroupS {
+    int first, end, row0, tm;
 };
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
@@ -33,54 +40,90 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                  : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ uint32_t quad_mask(uint64_t m) {
-    uint32_t q = 0;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) q |= static_cast<uint32_t>(((m >> (4 * i)) & 0xFull) != 0) << i;
-    return q;
+// Octets (2x2x2 cubes, 8 consecutive slots) with any bit set: OR-fold each
+// byte into its low bit, then gather the 8 low bits with one multiply.
+__device__ __forceinline__ uint32_t octet_bits(uint64_t m) {
+    m |= m >> 4;
+    m |= m >> 2;
+    m |= m >> 1;
+    return static_cast<uint32_t>(((m & 0x0101010101010101ull) * 0x0102040810204080ull) >> 56);
 }
 
-__device__ __forceinline__ uint32_t octet_of_quads(uint32_t qm) {
-    uint32_t o = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) o |= static_cast<uint32_t>(((qm >> (2 * i)) & 3u) != 0) << i;
+// Phi[row][slot] lives at row*64 + (slot ^ 4*(row & 3)): any 4 consecutive
+// rows x 4 consecutive slots (a half-warp DMMA fragment) hit 32 banks.
+__device__ __forceinline__ int swz(int row) { return (row & 3) << 2; }
+__device__ __forceinline__ int phi_idx(int row, int slot) { return row * 64 + (slot ^ swz(row)); }
+
+constexpr uint8_t kNoCover = 0xFF;
+
+struct Smem {
+    double* phi;
+    double* acc;  // w[64] (H) or racc[NW][64] (rho)
+    CoverS* cov;
+    GroupS* grp;
+    int32_t* off2d;  // [ncov][ncov] value offset of canonical pair (ci <= cj) with common points, else -1
+    uint8_t* rcov;   // [rows] cover of each Phi row (kNoCover for pad rows)
+    uint8_t* rorb;   // [rows] orbital index inside that cover
+    Task* task;
+    int32_t* wptr;   // [kTaskWarps + 1]
+};
+
+__host__ __device__ __forceinline__ size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
+
+__host__ __device__ inline size_t smem_layout(const GridArgs& g, int acc_doubles, size_t* off) {
+    size_t o = 0;
+    off[0] = o;
+    o += align16(static_cast<size_t>(g.max_rows) * 64 * sizeof(double));
+    off[1] = o;
+    o += align16(static_cast<size_t>(acc_doubles) * sizeof(double));
+    off[2] = o;
+    o += align16(static_cast<size_t>(g.max_cover) * sizeof(CoverS));
+    off[3] = o;
+    o += align16(static_cast<size_t>(g.max_cover) * sizeof(GroupS));
+    off[4] = o;
+    o += align16(static_cast<size_t>(g.max_cover) * g.max_cover * sizeof(int32_t));
+    off[5] = o;
+    o += align16(static_cast<size_t>(g.max_rows));
+    off[6] = o;
+    o += align16(static_cast<size_t>(g.max_rows));
+    off[7] = o;
+    o += align16(static_cast<size_t>(g.max_tasks) * sizeof(Task));
+    off[8] = o;
+    o += align16((kTaskWarps + 1) * sizeof(int32_t));
     return o;
 }
 
-// Offset of the norb x 4 tile of quad q of cover cv (q must be active).
-__device__ __forceinline__ int tile_of(const CoverS& cv, int q) {
-    return cv.tbase + __popc(cv.qmask & ((1u << q) - 1u)) * cv.norb * 4;
-}
-// As tile_of, or the zero tile (offset 0) when q is inactive.
-__device__ __forceinline__ int tile_or_zero(const CoverS& cv, int q) {
-    return ((cv.qmask >> q) & 1u) ? tile_of(cv, q) : 0;
-}
-
-struct Smem {
-    double* phi;  // [kZero zeros][tiles...][kTilePad zeros]
-    double* acc;  // w[64] (H) or racc[NW][64] (rho)
-    BPair* bp;    // this block's work items
-    CoverS* cov;
-};
-
-__device__ __forceinline__ Smem carve(unsigned char* base, int max_phi, int acc_doubles, int max_bpairs) {
+__device__ __forceinline__ Smem carve(unsigned char* base, const GridArgs& g, int acc_doubles) {
+    size_t off[9];
+    smem_layout(g, acc_doubles, off);
     Smem s;
-    s.phi = reinterpret_cast<double*>(base);
-    s.acc = s.phi + max_phi;
-    s.bp = reinterpret_cast<BPair*>(s.acc + acc_doubles);
-    s.cov = reinterpret_cast<CoverS*>(s.bp + max_bpairs);
+    s.phi = reinterpret_cast<double*>(base + off[0]);
+    s.acc = reinterpret_cast<double*>(base + off[1]);
+    s.cov = reinterpret_cast<CoverS*>(base + off[2]);
+    s.grp = reinterpret_cast<GroupS*>(base + off[3]);
+    s.off2d = reinterpret_cast<int32_t*>(base + off[4]);
+    s.rcov = base + off[5];
+    s.rorb = base + off[6];
+    s.task = reinterpret_cast<Task*>(base + off[7]);
+    s.wptr = reinterpret_cast<int32_t*>(base + off[8]);
     return s;
 }
 
-// Loads the covers and work items of block b into shared memory and evaluates
-// Phi on the active quads. Returns the number of covers (uniform per CTA).
-__device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int& nbp) {
+struct Block {
+    int ncov, ngrp, rows;  // rows: padded Phi rows in use (without the 8 tail rows)
+};
+
+// Stages block b: covers, row groups, row tables, pair-offset table, this
+// kernel's task list, and Phi (zeros outside spheres and in pad rows).
+__device__ Block stage_block(const GridArgs& g, int64_t b, const Smem& sm) {
     const int tid = threadIdx.x, nt = blockDim.x;
-    const int c0 = g.blk_ptr[b], c1 = g.blk_ptr[b + 1];
-    const int ncov = c1 - c0;
-    const int64_t p0 = g.bp_ptr[b];
-    nbp = static_cast<int>(g.bp_ptr[b + 1] - p0);
-    if (ncov == 0) return 0;
+    const int c0 = g.blk_ptr[b];
+    Block blk;
+    blk.ncov = g.blk_ptr[b + 1] - c0;
+    blk.ngrp = 0;
+    blk.rows = 0;
+    if (blk.ncov == 0) return blk;
+    const int ncov = blk.ncov;
     const SysParams& P = g.sys;
     if (tid < ncov) {
         CoverS& cv = sm.cov[tid];
@@ -88,30 +131,57 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int& nb
         cv.sp = P.spc[a];
         cv.norb = P.sp[cv.sp].norb;
         cv.mask = g.cov_mask[c0 + tid];
-        cv.qmask = quad_mask(cv.mask);
         const int R0 = g.cov_R[3 * (c0 + tid)], R1 = g.cov_R[3 * (c0 + tid) + 1], R2 = g.cov_R[3 * (c0 + tid) + 2];
 #pragma unroll
         for (int c = 0; c < 3; ++c) cv.t[c] = P.tau[3 * a + c] + ((R0 * P.A[c] + R1 * P.A[3 + c]) + R2 * P.A[6 + c]);
     }
-    for (int i = tid; i < nbp; i += nt) sm.bp[i] = g.bp[p0 + i];
-    for (int i = tid; i < kZero; i += nt) sm.phi[i] = 0.0;
+    const int64_t tp0 = g.t_ptr[b];
+    const int ntask = static_cast<int>(g.t_ptr[b + 1] - tp0);
+    for (int i = tid; i < ntask; i += nt) sm.task[i] = g.tasks[tp0 + i];
+    if (tid <= kTaskWarps) sm.wptr[tid] = g.t_wptr[b * (kTaskWarps + 1) + tid];
+    for (int i = tid; i < ncov * ncov; i += nt) sm.off2d[i] = -1;
+    for (int i = tid; i < g.max_rows; i += nt) sm.rcov[i] = kNoCover;
     __syncthreads();
-    if (tid < ncov) {
-        int base = kZero;
-        for (int c = 0; c < tid; ++c) base += __popc(sm.cov[c].qmask) * sm.cov[c].norb * 4;
-        sm.cov[tid].tbase = base;
+    if (tid == 0) {
+        int gf[kMaxCoverPerBlock], ge[kMaxCoverPerBlock], gr0[kMaxCoverPerBlock], grs[kMaxCoverPerBlock],
+            cr0[kMaxCoverPerBlock], cg[kMaxCoverPerBlock];
+        const int ng = make_groups(ncov, [&](int c) { return sm.cov[c].norb; }, gf, ge, gr0, grs, cr0, cg);
+        for (int q = 0; q < ng; ++q) sm.grp[q] = GroupS{gf[q], ge[q], gr0[q], grs[q] >> 3};
+        for (int c = 0; c < ncov; ++c) {
+            sm.cov[c].row0 = cr0[c];
+            sm.cov[c].grp = cg[c];
+        }
+        sm.cov[0].grp |= ng << 16;  // broadcast the group count
+    }
+    {
+        const int64_t p0 = g.bp_ptr[b], p1 = g.bp_ptr[b + 1];
+        for (int64_t e = p0 + tid; e < p1; e += nt) {
+            const BPair bp = g.bp[e];
+            sm.off2d[(bp.cicj & 0xffff) * ncov + (bp.cicj >> 16)] = static_cast<int32_t>(bp.off);
+        }
     }
     __syncthreads();
-    const CoverS& last = sm.cov[ncov - 1];
-    const int end = last.tbase + __popc(last.qmask) * last.norb * 4;
-    for (int i = tid; i < kTilePad; i += nt) sm.phi[end + i] = 0.0;
+    blk.ngrp = sm.cov[0].grp >> 16;
+    const GroupS& lg = sm.grp[blk.ngrp - 1];
+    blk.rows = lg.row0 + 8 * lg.tm;
+    if (tid < ncov) {
+        const CoverS& cv = sm.cov[tid];
+        for (int o = 0; o < cv.norb; ++o) {
+            sm.rcov[cv.row0 + o] = static_cast<uint8_t>(tid);
+            sm.rorb[cv.row0 + o] = static_cast<uint8_t>(o);
+        }
+    }
+    __syncthreads();
+    // zero the pad rows (group padding + 8 tail rows for tile overrun)
+    for (int i = tid; i < (blk.rows + 8) * 64; i += nt)
+        if (sm.rcov[i >> 6] == kNoCover) sm.phi[i] = 0.0;
     int bi, bj, bk;
     block_decode(P, b, bi, bj, bk);
     for (int task = tid; task < ncov * 64; task += nt) {
         const int c = task >> 6, s = task & 63;
         const CoverS& cv = sm.cov[c];
-        if (!((cv.qmask >> (s >> 2)) & 1u)) continue;  // no tile for an inactive quad
-        double* dst = sm.phi + tile_of(cv, s >> 2) + (s & 3);
+        double* dst = sm.phi;
+        const int row0 = cv.row0;
         if ((cv.mask >> s) & 1) {
             int li, lj, lk;
             slot_decode(s, li, lj, lk);
@@ -122,13 +192,14 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int& nb
             const double dy = (fi * P.A[1] + fj * P.A[4] + fk * P.A[7]) - cv.t[1];
             const double dz = (fi * P.A[2] + fj * P.A[5] + fk * P.A[8]) - cv.t[2];
             const double d2 = dx * dx + dy * dy + dz * dz;
-            eval_orbitals(P.sp[cv.sp], P.tables, dx, dy, dz, d2, [&](int o, double v) { dst[4 * o] = v; });
+            eval_orbitals(P.sp[cv.sp], P.tables, dx, dy, dz, d2,
+                          [&](int o, double v) { dst[phi_idx(row0 + o, s)] = v; });
         } else {
-            for (int o = 0; o < cv.norb; ++o) dst[4 * o] = 0.0;
+            for (int o = 0; o < cv.norb; ++o) dst[phi_idx(row0 + o, s)] = 0.0;
         }
     }
     __syncthreads();
-    return ncov;
+    return blk;
 }
 
 __device__ __forceinline__ int64_t slot_point(const SysParams& P, int bi, int bj, int bk, int s, bool& valid) {
@@ -139,15 +210,12 @@ __device__ __forceinline__ int64_t slot_point(const SysParams& P, int bi, int bj
     return (static_cast<int64_t>(i) * P.N[1] + j) * P.N[2] + k;
 }
 
-// ---- H pair task ---------------------------------------------------------------
-// C(na x nb) = sum over common quads q of A(na x 4) B(4 x nb), A = Phi_ci w,
-// B = Phi_cj^T. The DMMA A/B fragments of a quad are 32 consecutive doubles of
-// the quad tile (lane = 4*row + point). Pairs with <= 2 output tiles alternate
-// two accumulator sets so that two independent DMMA chains are in flight.
+// ---- H task ---------------------------------------------------------------------
+// Output tile rows ra0 + [0, 8*TM) (inside group g) x columns cb0 + [0, 8*TN)
+// of cover cj. Tiles with <= 2 DMMAs per quad alternate two accumulator sets.
 template <int TM, int TN>
-__device__ __forceinline__ void h_pair(const double* __restrict__ phi, const double* __restrict__ w, const CoverS& A,
-                                       const CoverS& B, uint32_t qm, double* __restrict__ H, double sign, int scatter,
-                                       int lane) {
+__device__ __forceinline__ void h_tile(const Smem& sm, int ncov, int cj, int ra0, int cb0, uint32_t qm,
+                                       double* __restrict__ H, double sign, int scatter, int lane) {
     constexpr int NACC = (TM * TN <= 2) ? 2 : 1;
     double c[NACC][TM][TN][2];
 #pragma unroll
@@ -156,20 +224,24 @@ __device__ __forceinline__ void h_pair(const double* __restrict__ phi, const dou
         for (int i = 0; i < TM; ++i)
 #pragma unroll
             for (int j = 0; j < TN; ++j) c[u][i][j][0] = c[u][i][j][1] = 0.0;
-    const double* pw = w + (lane & 3);
+    const CoverS& B = sm.cov[cj];
+    const int ra = ra0 + (lane >> 2), rb = B.row0 + cb0 + (lane >> 2);
+    const double* pa = sm.phi + ra * 64 + (lane & 3);
+    const double* pb = sm.phi + rb * 64 + (lane & 3);
+    const int sa = swz(ra), sb = swz(rb);  // 8-row steps keep row & 3
+    const double* pw = sm.acc + (lane & 3);
     auto step = [&](int u, int q) {
-        const double wv = pw[4 * q];
-        const double* ta = phi + tile_of(A, q) + lane;
-        const double* tb = phi + tile_of(B, q) + lane;
-        double a[TM], b[TN];
+        const int col = 4 * q;
+        const double wv = pw[col];
+        double a[TM], bb[TN];
 #pragma unroll
-        for (int i = 0; i < TM; ++i) a[i] = ta[32 * i] * wv;
+        for (int i = 0; i < TM; ++i) a[i] = pa[i * 512 + (col ^ sa)] * wv;
 #pragma unroll
-        for (int j = 0; j < TN; ++j) b[j] = tb[32 * j];
+        for (int j = 0; j < TN; ++j) bb[j] = pb[j * 512 + (col ^ sb)];
 #pragma unroll
         for (int i = 0; i < TM; ++i)
 #pragma unroll
-            for (int j = 0; j < TN; ++j) dmma(c[u][i][j], a[i], b[j]);
+            for (int j = 0; j < TN; ++j) dmma(c[u][i][j], a[i], bb[j]);
     };
     while (qm) {
         const int q0 = __ffs(qm) - 1;
@@ -183,45 +255,59 @@ __device__ __forceinline__ void h_pair(const double* __restrict__ phi, const dou
             step(0, q0);
         }
     }
-    const int na = A.norb, nb = B.norb;
+    const int nb = B.norb;
 #pragma unroll
-    for (int i = 0; i < TM; ++i)
+    for (int i = 0; i < TM; ++i) {
+        const int r = ra0 + 8 * i + (lane >> 2);
+        const int ci = sm.rcov[r];
+        const int off = (ci != kNoCover && ci <= cj) ? sm.off2d[ci * ncov + cj] : -1;
+        const int ri = sm.rorb[r];
 #pragma unroll
         for (int j = 0; j < TN; ++j)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const int r = i * 8 + (lane >> 2), col = j * 8 + (lane & 3) * 2 + e;
+                const int col = cb0 + 8 * j + (lane & 3) * 2 + e;
                 double v = c[0][i][j][e];
                 if (NACC == 2) v += c[NACC - 1][i][j][e];
-                if (r < na && col < nb) {
+                if (off >= 0 && col < nb) {
                     if (scatter == 0)
-                        atomicAdd(H + r * nb + col, sign * v);
+                        atomicAdd(H + off + ri * nb + col, sign * v);
                     else
-                        H[r * nb + col] = sign * v;
+                        H[off + ri * nb + col] = sign * v;
                 }
             }
+    }
 }
 
-template <int TM>
-__device__ __forceinline__ void h_pair_tn(int tn, const double* phi, const double* w, const CoverS& A,
-                                          const CoverS& B, uint32_t qm, double* H, double sign, int scatter,
-                                          int lane) {
-    switch (tn) {
-        case 1: h_pair<TM, 1>(phi, w, A, B, qm, H, sign, scatter, lane); break;
-        case 2: h_pair<TM, 2>(phi, w, A, B, qm, H, sign, scatter, lane); break;
-        case 3: h_pair<TM, 3>(phi, w, A, B, qm, H, sign, scatter, lane); break;
-        default: h_pair<TM, 4>(phi, w, A, B, qm, H, sign, scatter, lane); break;
+__device__ __forceinline__ void h_task(const Smem& sm, int ncov, const Task& t, double* H, double sign, int scatter,
+                                       int lane) {
+    const GroupS& G = sm.grp[t.g];
+    const int nb = sm.cov[t.cj].norb;
+    const uint32_t qm = t.qmask;
+    for (int i0 = 0; i0 < G.tm; i0 += 2) {
+        const int tm = min(2, G.tm - i0);
+        for (int j0 = 0; j0 < (nb + 7) >> 3; j0 += 2) {
+            const int tn = min(2, ((nb + 7) >> 3) - j0);
+            const int ra0 = G.row0 + 8 * i0, cb0 = 8 * j0;
+            if (tm == 2 && tn == 2)
+                h_tile<2, 2>(sm, ncov, t.cj, ra0, cb0, qm, H, sign, scatter, lane);
+            else if (tm == 2)
+                h_tile<2, 1>(sm, ncov, t.cj, ra0, cb0, qm, H, sign, scatter, lane);
+            else if (tn == 2)
+                h_tile<1, 2>(sm, ncov, t.cj, ra0, cb0, qm, H, sign, scatter, lane);
+            else
+                h_tile<1, 1>(sm, ncov, t.cj, ra0, cb0, qm, H, sign, scatter, lane);
+        }
     }
 }
 
 template <int NW>
 __global__ void __launch_bounds__(NW * 32, 2) k_hamiltonian(GridArgs g) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const Smem sm = carve(smem_raw, g.max_phi, 64, g.max_bpairs);
+    const Smem sm = carve(smem_raw, g, 64);
     const int64_t b = g.blk_begin + blockIdx.x;
-    int nbp;
-    const int ncov = stage_block(g, b, sm, nbp);
-    if (ncov == 0) return;
+    const Block blk = stage_block(g, b, sm);
+    if (blk.ncov == 0) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int bi, bj, bk;
     block_decode(g.sys, b, bi, bj, bk);
@@ -233,151 +319,155 @@ __global__ void __launch_bounds__(NW * 32, 2) k_hamiltonian(GridArgs g) {
         }
         __syncthreads();
         double* Hs = g.out + spin * g.nnz;
-        for (int e = warp; e < nbp; e += NW) {
-            const BPair bp = sm.bp[e];
-            const CoverS& A = sm.cov[bp.cicj & 0xffff];
-            const CoverS& B = sm.cov[bp.cicj >> 16];
-            const uint32_t qm = quad_mask(A.mask & B.mask);
-            const int tm = (A.norb + 7) >> 3, tn = (B.norb + 7) >> 3;
-            double* H = Hs + bp.off;
-            switch (tm) {
-                case 1: h_pair_tn<1>(tn, sm.phi, sm.acc, A, B, qm, H, g.sign, g.scatter, lane); break;
-                case 2: h_pair_tn<2>(tn, sm.phi, sm.acc, A, B, qm, H, g.sign, g.scatter, lane); break;
-                case 3: h_pair_tn<3>(tn, sm.phi, sm.acc, A, B, qm, H, g.sign, g.scatter, lane); break;
-                default: h_pair_tn<4>(tn, sm.phi, sm.acc, A, B, qm, H, g.sign, g.scatter, lane); break;
-            }
-        }
+        for (int w = warp; w < kTaskWarps; w += NW)
+            for (int e = sm.wptr[w]; e < sm.wptr[w + 1]; ++e) h_task(sm, blk.ncov, sm.task[e], Hs, g.sign, g.scatter, lane);
         __syncthreads();
     }
 }
 
-// ---- rho pair task -------------------------------------------------------------
-// Per active octet o (quads 2o, 2o+1): X(8 slots x nb) = Phi_ci^T DM, the A
-// fragment of lane l is Phi_ci[4s + (l&3)][slot] read from the tile of quad
-// 2o + (l>>4) (zero tile when inactive). Fast path (na, nb <= 16): DM
-// fragments in registers, prefetched one pair ahead; two octets per
-// iteration for DMMA ILP.
-constexpr int kFrag = 8;  // B fragments per lane for na, nb <= 16: (4 K-steps) x (2 N-tiles)
+// ---- rho task -------------------------------------------------------------------
+// Rows ra0 + [0, 8*TM) of group g; octets 4h..4h+3; partners cj >= first(g).
+// A = D'(rows x 4 cols of cj) gathered from the pair blocks (prefetched one
+// partner ahead), B = Phi_cj(4 cols x 8 slots), C = Y(rows x 8 slots).
+template <int TM>
+struct RowInfo {
+    int ci[TM];
+    int ri[TM];
+};
 
-__device__ __forceinline__ void load_dfrag(const double* __restrict__ D, int na, int nb, int lane,
-                                           double (&out)[kFrag]) {
+template <int TM>
+__device__ __forceinline__ void gather_a(const Smem& sm, int ncov, const RowInfo<TM>& ri, int cj, int kc,
+                                         const double* __restrict__ Ds, int lane, double (&a)[TM][4]) {
+    const int nb = sm.cov[cj].norb;
 #pragma unroll
-    for (int s = 0; s < 4; ++s)
+    for (int t = 0; t < TM; ++t) {
+        const int ci = ri.ci[t];
+        const int off = (ci != kNoCover && ci <= cj) ? sm.off2d[ci * ncov + cj] : -1;
+        const double fac = ci < cj ? 2.0 : 1.0;
+        const double* row = Ds + off + ri.ri[t] * nb;
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-            const int k = 4 * s + (lane & 3), n = 8 * t + (lane >> 2);
-            out[s * 2 + t] = (k < na && n < nb) ? __ldg(D + k * nb + n) : 0.0;
-        }
-}
-
-template <int KS, int TN, int NO>
-__device__ __forceinline__ void rho_octets(const double* __restrict__ phi, const CoverS& A, const CoverS& B,
-                                           const int (&oct)[2], const double (&bf)[kFrag], double f,
-                                           double* __restrict__ racc, int lane) {
-    const int half = lane >> 4, pt = (lane >> 2) & 3;
-    const double* ta[NO];
-    const double* tb[NO];
-#pragma unroll
-    for (int o = 0; o < NO; ++o) {
-        const int q = 2 * oct[o] + half;
-        ta[o] = phi + tile_or_zero(A, q) + 4 * (lane & 3) + pt;
-        tb[o] = phi + tile_or_zero(B, q) + 8 * (lane & 3) + pt;
-    }
-    double x[NO][TN][2];
-#pragma unroll
-    for (int o = 0; o < NO; ++o)
-#pragma unroll
-        for (int t = 0; t < TN; ++t) x[o][t][0] = x[o][t][1] = 0.0;
-#pragma unroll
-    for (int s = 0; s < KS; ++s) {
-        double a[NO];
-#pragma unroll
-        for (int o = 0; o < NO; ++o) a[o] = ta[o][16 * s];
-#pragma unroll
-        for (int o = 0; o < NO; ++o)
-#pragma unroll
-            for (int t = 0; t < TN; ++t) dmma(x[o][t], a[o], bf[s * 2 + t]);
-    }
-#pragma unroll
-    for (int o = 0; o < NO; ++o) {
-        double part = 0.0;
-#pragma unroll
-        for (int t = 0; t < TN; ++t)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) part += x[o][t][e] * tb[o][32 * t + 4 * e];
-        part += __shfl_xor_sync(0xffffffffu, part, 1);
-        part += __shfl_xor_sync(0xffffffffu, part, 2);
-        if ((lane & 3) == 0) racc[8 * oct[o] + (lane >> 2)] += f * part;
-    }
-}
-
-template <int KS, int TN>
-__device__ __forceinline__ void rho_pair(const double* __restrict__ phi, const CoverS& A, const CoverS& B,
-                                         uint32_t om, const double (&bf)[kFrag], double f, double* __restrict__ racc,
-                                         int lane) {
-    while (om) {
-        int oct[2];
-        oct[0] = __ffs(om) - 1;
-        om &= om - 1;
-        if (om) {
-            oct[1] = __ffs(om) - 1;
-            om &= om - 1;
-            rho_octets<KS, TN, 2>(phi, A, B, oct, bf, f, racc, lane);
-        } else {
-            oct[1] = oct[0];
-            rho_octets<KS, TN, 1>(phi, A, B, oct, bf, f, racc, lane);
+        for (int s = 0; s < 4; ++s) {
+            const int j = 16 * kc + 4 * s + (lane & 3);
+            a[t][s] = (off >= 0 && j < nb) ? fac * __ldg(row + j) : 0.0;
         }
     }
 }
 
-// General path for atoms with more than 16 orbitals (not used by Fe3O4).
-__device__ __noinline__ void rho_pair_big(const double* __restrict__ phi, const CoverS& A, const CoverS& B, uint32_t om,
-                             const double* __restrict__ D, double f, double* __restrict__ racc, int lane) {
-    const int na = A.norb, nb = B.norb;
-    const int ks = (na + 3) >> 2, tn = (nb + 7) >> 3;
-    const int half = lane >> 4, pt = (lane >> 2) & 3;
-    while (om) {
-        const int o = __ffs(om) - 1;
-        om &= om - 1;
-        const int q = 2 * o + half;
-        const double* ta = phi + tile_or_zero(A, q) + 4 * (lane & 3) + pt;
-        const double* tb = phi + tile_or_zero(B, q) + 8 * (lane & 3) + pt;
-        double part = 0.0;
-        for (int t = 0; t < tn; ++t) {
-            double x[2] = {0.0, 0.0};
-            for (int s = 0; s < ks; ++s) {
-                const int k = 4 * s + (lane & 3), n = 8 * t + (lane >> 2);
-                const double bv = (k < na && n < nb) ? __ldg(D + k * nb + n) : 0.0;
-                dmma(x, ta[16 * s], bv);
+template <int TM>
+__device__ __forceinline__ uint32_t partner_octets(const Smem& sm, const GroupS& G, int cj, uint32_t hm) {
+    const uint64_t mj = sm.cov[cj].mask;
+    uint64_t m = 0;
+    const int last = min(G.end, cj + 1);
+    for (int ci = G.first; ci < last; ++ci) m |= sm.cov[ci].mask & mj;
+    return octet_bits(m) & hm;
+}
+
+template <int TM>
+__device__ void rho_task_rows(const Smem& sm, int ncov, const GroupS& G, int ra0, int h, const double* __restrict__ Ds,
+                              double* __restrict__ racc, int lane) {
+    const uint32_t hm = 0xFu << (4 * h);
+    RowInfo<TM> ri;
+#pragma unroll
+    for (int t = 0; t < TM; ++t) {
+        const int r = ra0 + 8 * t + (lane >> 2);
+        ri.ci[t] = sm.rcov[r];
+        ri.ri[t] = sm.rorb[r];
+    }
+    double y[TM][4][2];
+#pragma unroll
+    for (int t = 0; t < TM; ++t)
+#pragma unroll
+        for (int o = 0; o < 4; ++o) y[t][o][0] = y[t][o][1] = 0.0;
+    // partner list: covers cj >= first(G) sharing an octet of this half with the group
+    auto next_partner = [&](int from, uint32_t& om) {
+        for (int c = from; c < ncov; ++c) {
+            om = partner_octets<TM>(sm, G, c, hm);
+            if (om) return c;
+        }
+        return ncov;
+    };
+    uint32_t om_n;
+    int cj = next_partner(G.first, om_n);
+    double nxt[TM][4];
+    if (cj < ncov) gather_a<TM>(sm, ncov, ri, cj, 0, Ds, lane, nxt);
+    while (cj < ncov) {
+        const uint32_t om = om_n;
+        const CoverS& B = sm.cov[cj];
+        const int nkc = (B.norb + 15) >> 4;
+        double a[TM][4];
+#pragma unroll
+        for (int t = 0; t < TM; ++t)
+#pragma unroll
+            for (int s = 0; s < 4; ++s) a[t][s] = nxt[t][s];
+        const int cn = (nkc == 1) ? next_partner(cj + 1, om_n) : cj;
+        if (nkc == 1 && cn < ncov) gather_a<TM>(sm, ncov, ri, cn, 0, Ds, lane, nxt);
+        for (int kc = 0; kc < nkc; ++kc) {
+            if (kc > 0) gather_a<TM>(sm, ncov, ri, cj, kc, Ds, lane, a);
+            const int ks = min(4, (B.norb - 16 * kc + 3) >> 2);
+            const int rb = B.row0 + 16 * kc + (lane & 3);
+            const double* pb = sm.phi + rb * 64;
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {
+                if (!((om >> (4 * h + o)) & 1u)) continue;
+                const int col = 8 * (4 * h + o) + (lane >> 2);
+#pragma unroll
+                for (int s = 0; s < 4; ++s) {
+                    if (s < ks) {
+                        const double bv = pb[s * 256 + (col ^ swz(rb))];
+#pragma unroll
+                        for (int t = 0; t < TM; ++t) dmma(y[t][o], a[t][s], bv);
+                    }
+                }
             }
-            part += x[0] * tb[32 * t] + x[1] * tb[32 * t + 4];
         }
-        part += __shfl_xor_sync(0xffffffffu, part, 1);
-        part += __shfl_xor_sync(0xffffffffu, part, 2);
-        if ((lane & 3) == 0) racc[8 * o + (lane >> 2)] += f * part;
+        if (nkc == 1) {
+            cj = cn;
+        } else {
+            cj = next_partner(cj + 1, om_n);
+            if (cj < ncov) gather_a<TM>(sm, ncov, ri, cj, 0, Ds, lane, nxt);
+        }
+    }
+    // rho(slot) += sum over rows of Phi_row(slot) * Y(row, slot)
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int p = 8 * (4 * h + o) + 2 * (lane & 3) + e;
+            double v = 0.0;
+#pragma unroll
+            for (int t = 0; t < TM; ++t) {
+                const int r = ra0 + 8 * t + (lane >> 2);
+                v += sm.phi[phi_idx(r, p)] * y[t][o][e];
+            }
+            v += __shfl_xor_sync(0xffffffffu, v, 4);
+            v += __shfl_xor_sync(0xffffffffu, v, 8);
+            v += __shfl_xor_sync(0xffffffffu, v, 16);
+            if (lane < 4) racc[p] += v;
+        }
     }
 }
 
-template <int KS>
-__device__ __forceinline__ void rho_pair_tn(int tn, const double* phi, const CoverS& A, const CoverS& B, uint32_t om,
-                                            const double (&bf)[kFrag], double f, double* racc, int lane) {
-    if (tn == 1)
-        rho_pair<KS, 1>(phi, A, B, om, bf, f, racc, lane);
-    else
-        rho_pair<KS, 2>(phi, A, B, om, bf, f, racc, lane);
+__device__ __forceinline__ void rho_task(const Smem& sm, int ncov, const Task& t, const double* Ds, double* racc,
+                                         int lane) {
+    const GroupS& G = sm.grp[t.g];
+    for (int i0 = 0; i0 < G.tm; i0 += 2) {
+        if (G.tm - i0 >= 2)
+            rho_task_rows<2>(sm, ncov, G, G.row0 + 8 * i0, t.half, Ds, racc, lane);
+        else
+            rho_task_rows<1>(sm, ncov, G, G.row0 + 8 * i0, t.half, Ds, racc, lane);
+    }
 }
 
 template <int NW>
 __global__ void __launch_bounds__(NW * 32, 2) k_density(GridArgs g) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const Smem sm = carve(smem_raw, g.max_phi, NW * 64, g.max_bpairs);
+    const Smem sm = carve(smem_raw, g, NW * 64);
     const int64_t b = g.blk_begin + blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int bi, bj, bk;
     block_decode(g.sys, b, bi, bj, bk);
-    int nbp;
-    const int ncov = stage_block(g, b, sm, nbp);
-    if (ncov == 0) {
+    const Block blk = stage_block(g, b, sm);
+    if (blk.ncov == 0) {
         if (tid < 64) {
             bool valid;
             const int64_t pt = slot_point(g.sys, bi, bj, bk, tid, valid);
@@ -391,36 +481,8 @@ __global__ void __launch_bounds__(NW * 32, 2) k_density(GridArgs g) {
         for (int i = lane; i < 64; i += 32) racc[i] = 0.0;
         __syncwarp();
         const double* Ds = g.in + spin * g.nnz;
-        double nxt[kFrag];
-        auto prefetch = [&](int e) {
-            const BPair bp = sm.bp[e];
-            const int na = sm.cov[bp.cicj & 0xffff].norb, nb = sm.cov[bp.cicj >> 16].norb;
-            if (na <= 16 && nb <= 16) load_dfrag(Ds + bp.off, na, nb, lane, nxt);
-        };
-        if (warp < nbp) prefetch(warp);
-        for (int e = warp; e < nbp; e += NW) {
-            double cur[kFrag];
-#pragma unroll
-            for (int i = 0; i < kFrag; ++i) cur[i] = nxt[i];
-            if (e + NW < nbp) prefetch(e + NW);
-            const BPair bp = sm.bp[e];
-            const int ci = bp.cicj & 0xffff, cj = bp.cicj >> 16;
-            const CoverS& A = sm.cov[ci];
-            const CoverS& B = sm.cov[cj];
-            const uint32_t om = octet_of_quads(quad_mask(A.mask & B.mask));
-            const double f = ci == cj ? 1.0 : 2.0;
-            if (A.norb > 16 || B.norb > 16) {
-                rho_pair_big(sm.phi, A, B, om, Ds + bp.off, f, racc, lane);
-                continue;
-            }
-            const int ks = (A.norb + 3) >> 2, tn = (B.norb + 7) >> 3;
-            switch (ks) {
-                case 1: rho_pair_tn<1>(tn, sm.phi, A, B, om, cur, f, racc, lane); break;
-                case 2: rho_pair_tn<2>(tn, sm.phi, A, B, om, cur, f, racc, lane); break;
-                case 3: rho_pair_tn<3>(tn, sm.phi, A, B, om, cur, f, racc, lane); break;
-                default: rho_pair_tn<4>(tn, sm.phi, A, B, om, cur, f, racc, lane); break;
-            }
-        }
+        for (int w = warp; w < kTaskWarps; w += NW)
+            for (int e = sm.wptr[w]; e < sm.wptr[w + 1]; ++e) rho_task(sm, blk.ncov, sm.task[e], Ds, racc, lane);
         __syncthreads();
         if (tid < 64) {
             double r = 0.0;
@@ -510,18 +572,14 @@ __global__ void k_dm_check(SysParams P, int64_t npair, int nspin, int64_t nnz, c
 
 __global__ void k_block_orbitals(GridArgs g, int64_t b, double* out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const Smem sm = carve(smem_raw, g.max_phi, 64, g.max_bpairs);
-    int nbp;
-    const int ncov = stage_block(g, b, sm, nbp);
-    if (ncov == 0) return;
-    // unpack the quad tiles to [orbital][slot] rows in cover order
+    const Smem sm = carve(smem_raw, g, 64);
+    const Block blk = stage_block(g, b, sm);
+    // rows in cover order, without group padding
     int r0 = 0;
-    for (int c = 0; c < ncov; ++c) {
+    for (int c = 0; c < blk.ncov; ++c) {
         const CoverS& cv = sm.cov[c];
-        for (int i = threadIdx.x; i < cv.norb * 64; i += blockDim.x) {
-            const int o = i >> 6, s = i & 63;
-            out[static_cast<size_t>(r0) * 64 + i] = sm.phi[tile_or_zero(cv, s >> 2) + 4 * o + (s & 3)];
-        }
+        for (int i = threadIdx.x; i < cv.norb * 64; i += blockDim.x)
+            out[static_cast<size_t>(r0) * 64 + i] = sm.phi[phi_idx(cv.row0 + (i >> 6), i & 63)];
         r0 += cv.norb;
     }
 }
@@ -533,15 +591,14 @@ void set_smem(K kernel, size_t bytes) {
 
 }  // namespace
 
-size_t grid_smem_bytes(int max_phi, int max_cover, int max_bpairs, int nwarps, bool density) {
-    return static_cast<size_t>(max_phi) * sizeof(double) +
-           static_cast<size_t>(density ? nwarps * 64 : 64) * sizeof(double) +
-           static_cast<size_t>(max_bpairs) * sizeof(BPair) + static_cast<size_t>(max_cover) * sizeof(CoverS);
+size_t grid_smem_bytes(const GridArgs& g, int nwarps, bool density) {
+    size_t off[9];
+    return smem_layout(g, density ? nwarps * 64 : 64, off);
 }
 
 int launch_density(const GridArgs& g, int64_t nblk, int nwarps, cudaStream_t st) {
     if (nblk <= 0) return 0;
-    const size_t smem = grid_smem_bytes(g.max_phi, g.max_cover, g.max_bpairs, nwarps, true);
+    const size_t smem = grid_smem_bytes(g, nwarps, true);
     if (nwarps == 4) {
         set_smem(k_density<4>, smem);
         k_density<4><<<static_cast<unsigned>(nblk), 128, smem, st>>>(g);
@@ -555,7 +612,7 @@ int launch_density(const GridArgs& g, int64_t nblk, int nwarps, cudaStream_t st)
 
 int launch_hamiltonian(const GridArgs& g, int64_t nblk, int nwarps, cudaStream_t st) {
     if (nblk <= 0) return 0;
-    const size_t smem = grid_smem_bytes(g.max_phi, g.max_cover, g.max_bpairs, nwarps, false);
+    const size_t smem = grid_smem_bytes(g, nwarps, false);
     if (nwarps == 4) {
         set_smem(k_hamiltonian<4>, smem);
         k_hamiltonian<4><<<static_cast<unsigned>(nblk), 128, smem, st>>>(g);
@@ -587,7 +644,7 @@ int launch_dm_check(const DevIndex& ix, const SysParams& sys, int nspin, const d
 }
 
 int launch_block_orbitals(const GridArgs& g, int64_t block, double* d_out, cudaStream_t st) {
-    const size_t smem = grid_smem_bytes(g.max_phi, g.max_cover, g.max_bpairs, 1, false);
+    const size_t smem = grid_smem_bytes(g, 1, false);
     set_smem(k_block_orbitals, smem);
     k_block_orbitals<<<1, 256, smem, st>>>(g, block, d_out);
     KBG_CUDA(cudaGetLastError());

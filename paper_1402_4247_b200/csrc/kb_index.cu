@@ -357,6 +357,7 @@ __global__ void k_bp_sort(int64_t nblock, const int64_t* __restrict__ bp_ptr, co
 }  // namespace
 
 void free_index(DevIndex& ix) {
+    free_tasks(ix);
     dfree(ix.blk_ptr);
     dfree(ix.cov_atom);
     dfree(ix.cov_R);

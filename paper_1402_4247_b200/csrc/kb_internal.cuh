@@ -14,12 +14,9 @@ namespace kbg {
 
 constexpr int kMaxSpecies = 8;
 constexpr int kMaxRad = 16;
-// Phi of a block is stored as quad tiles: for every cover and every active
-// 1x2x2 quad of its mask, norb x 4 doubles (orbital-major). kZero doubles of
-// zeros sit in front (the tile of an inactive quad) and kTilePad behind (tile
-// overrun of the 8-row DMMA fragments).
-constexpr int kZero = (KBG_MAX_ORB_PER_ATOM + 8) * 4;
-constexpr int kTilePad = 8 * 4;
+constexpr int kGroupRows = 16;  // covers are packed into row groups of <= 16 orbitals (2 DMMA row tiles)
+constexpr int kTaskWarps = 8;   // task lists are LPT-balanced over 8 warps (4-warp CTAs merge pairs)
+constexpr int kMaxCoverPerBlock = 64;
 
 // Error taxonomy of kband (common.hpp:21-38) carried as a status code.
 struct Error : std::runtime_error {
@@ -68,6 +65,18 @@ struct BPair {
     int64_t off;
 };
 
+// One warp task of a grid block. H: rows of group g x columns of cover cj over
+// the quads in qmask. rho: rows of group g, octets of half `half`, partners
+// cj >= first cover of g.
+struct Task {
+    uint8_t g;
+    uint8_t cj;
+    uint8_t half;
+    uint8_t pad_;
+    uint16_t qmask;
+    uint16_t cost;
+};
+
 struct Candidate {
     int32_t atom;
     int32_t R[3];
@@ -91,7 +100,18 @@ struct DevIndex {
     int64_t* bp_ptr = nullptr;
     BPair* bp = nullptr;
     int64_t* blk_cost = nullptr;
-    int max_phi = 0;     // max Phi quad-tile doubles of one block
+    // per-block warp task lists (kb_tasks.cu): tasks of block b are
+    // [t_ptr[b], t_ptr[b+1]), warp w's tasks start at t_ptr[b] + t_wptr[b*9+w]
+    int64_t* ht_ptr = nullptr;
+    Task* ht = nullptr;
+    int32_t* ht_wptr = nullptr;
+    int64_t* rt_ptr = nullptr;
+    Task* rt = nullptr;
+    int32_t* rt_wptr = nullptr;
+    int64_t nhtask = 0, nrtask = 0;
+    int max_rows_padded = 0;  // max Phi rows of a block (groups padded to 8-row tiles)
+    int max_htask = 0, max_rtask = 0;
+    int max_phi = 0;     // (unused)
     int max_cover = 0;   // max covers per block
     int max_bpairs = 0;  // max work items per block
     int64_t natompt = 0;
@@ -114,10 +134,14 @@ struct GridArgs {
     const uint64_t* cov_mask;
     const int64_t* bp_ptr;
     const BPair* bp;
+    const int64_t* t_ptr;   // task lists of this kernel (H or rho)
+    const Task* tasks;
+    const int32_t* t_wptr;
     int64_t blk_begin;  // first owned block
-    int max_phi;        // Phi doubles allocated (tiles + zero + pad)
+    int max_rows;       // Phi rows allocated (padded groups + 8 pad rows)
     int max_cover;
     int max_bpairs;
+    int max_tasks;
     int nspin;
     int64_t nnz;
     int64_t npts;
@@ -134,7 +158,10 @@ void free_index(DevIndex& ix);
 void copy_index_to_host(const DevIndex& ix, HostIndex& h, cudaStream_t st);
 
 // Grid kernels (kb_grid.cu). Return number of kernel launches.
-size_t grid_smem_bytes(int max_phi, int max_cover, int max_bpairs, int nwarps, bool density);
+size_t grid_smem_bytes(const GridArgs& g, int nwarps, bool density);
+// Task lists (kb_tasks.cu), built after the index.
+void build_tasks_device(const SysParams& sys, DevIndex& ix, cudaStream_t st);
+void free_tasks(DevIndex& ix);
 int launch_density(const GridArgs& g, int64_t nblk_owned, int nwarps, cudaStream_t st);
 int launch_hamiltonian(const GridArgs& g, int64_t nblk_owned, int nwarps, cudaStream_t st);
 int launch_mirror(const DevIndex& ix, const SysParams& sys, int nspin, double* h, cudaStream_t st);

@@ -1,0 +1,205 @@
+// Per-block warp task lists for the grid kernels (built once per geometry,
+// after the index). One thread per block: row groups (make_groups), the H
+// tasks (group x partner cover, common quads) and the rho tasks (group x
+// octet half), then an LPT assignment of the tasks to kTaskWarps warps so the
+// static per-warp schedule inside a CTA is balanced and deterministic.
+#include <cub/cub.cuh>
+
+#include "kb_device.cuh"
+
+namespace kbg {
+
+namespace {
+
+struct TaskStats {
+    int max_rows, max_h, max_r, too_many_covers;
+};
+
+template <class T>
+T* talloc(size_t n) {
+    T* p = nullptr;
+    if (n == 0) n = 1;
+    KBG_CUDA(cudaMalloc(&p, n * sizeof(T)));
+    return p;
+}
+
+int64_t scan_total(int64_t* cnt, int64_t* ptr, int64_t n, cudaStream_t st) {
+    size_t bytes = 0;
+    KBG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt, ptr, static_cast<int>(n + 1), st));
+    void* tmp = talloc<char>(bytes);
+    KBG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, cnt, ptr, static_cast<int>(n + 1), st));
+    int64_t total = 0;
+    KBG_CUDA(cudaMemcpyAsync(&total, ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    KBG_CUDA(cudaStreamSynchronize(st));
+    cudaFree(tmp);
+    return total;
+}
+
+__device__ __forceinline__ uint16_t sat16(int64_t c) { return static_cast<uint16_t>(c > 65535 ? 65535 : c); }
+
+__global__ void k_tasks(SysParams P, int64_t nblock, const int32_t* __restrict__ blk_ptr,
+                        const int32_t* __restrict__ cov_atom, const uint64_t* __restrict__ cov_mask, int64_t* hcnt,
+                        int64_t* rcnt, const int64_t* __restrict__ hptr, const int64_t* __restrict__ rptr, Task* hout,
+                        Task* rout, TaskStats* st) {
+    const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (b >= nblock) return;
+    const int c0 = blk_ptr[b];
+    const int ncov = blk_ptr[b + 1] - c0;
+    if (ncov > kMaxCoverPerBlock) {
+        atomicMax(&st->too_many_covers, ncov);
+        if (hcnt) hcnt[b] = rcnt[b] = 0;
+        return;
+    }
+    int norb[kMaxCoverPerBlock], g_first[kMaxCoverPerBlock], g_end[kMaxCoverPerBlock], g_row0[kMaxCoverPerBlock],
+        g_rows[kMaxCoverPerBlock], c_row0[kMaxCoverPerBlock], c_group[kMaxCoverPerBlock];
+    for (int c = 0; c < ncov; ++c) norb[c] = P.sp[P.spc[cov_atom[c0 + c]]].norb;
+    const int ng = make_groups(ncov, [&](int c) { return norb[c]; }, g_first, g_end, g_row0, g_rows, c_row0, c_group);
+    int64_t nh = 0, nr = 0;
+    for (int g = 0; g < ng; ++g) {
+        const int tm = g_rows[g] >> 3;
+        for (int cj = g_first[g]; cj < ncov; ++cj) {
+            const uint64_t mj = cov_mask[c0 + cj];
+            uint32_t qm = 0;
+            for (int ci = g_first[g]; ci < g_end[g] && ci <= cj; ++ci) qm |= quads_of(cov_mask[c0 + ci] & mj);
+            if (!qm) continue;
+            if (hout) {
+                Task t;
+                t.g = static_cast<uint8_t>(g);
+                t.cj = static_cast<uint8_t>(cj);
+                t.half = 0;
+                t.pad_ = 0;
+                t.qmask = static_cast<uint16_t>(qm);
+                t.cost = sat16(__popc(qm) * tm * ((norb[cj] + 7) >> 3) + 2);
+                hout[hptr[b] + nh] = t;
+            }
+            ++nh;
+        }
+        for (int h = 0; h < 2; ++h) {
+            int64_t cost = 0;
+            for (int cj = g_first[g]; cj < ncov; ++cj) {
+                const uint64_t mj = cov_mask[c0 + cj];
+                uint32_t om = 0;
+                for (int ci = g_first[g]; ci < g_end[g] && ci <= cj; ++ci) om |= octets_of(cov_mask[c0 + ci] & mj);
+                om &= 0xFu << (4 * h);
+                cost += __popc(om) * tm * ((norb[cj] + 3) >> 2);
+            }
+            if (!cost) continue;
+            if (rout) {
+                Task t;
+                t.g = static_cast<uint8_t>(g);
+                t.cj = 0;
+                t.half = static_cast<uint8_t>(h);
+                t.pad_ = 0;
+                t.qmask = 0;
+                t.cost = sat16(cost + 8);
+                rout[rptr[b] + nr] = t;
+            }
+            ++nr;
+        }
+    }
+    if (hcnt) {
+        hcnt[b] = nh;
+        rcnt[b] = nr;
+        atomicMax(&st->max_rows, ng ? g_row0[ng - 1] + g_rows[ng - 1] : 0);
+        atomicMax(&st->max_h, static_cast<int>(nh));
+        atomicMax(&st->max_r, static_cast<int>(nr));
+    }
+}
+
+// Sort one block's tasks by cost (descending, stable), assign each to the
+// least-loaded of kTaskWarps warps (LPT), emit warp-major into `out`.
+__global__ void k_tasks_lpt(int64_t nblock, const int64_t* __restrict__ ptr, Task* tmp, Task* out, int32_t* wptr) {
+    const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (b >= nblock) return;
+    const int64_t p0 = ptr[b];
+    const int n = static_cast<int>(ptr[b + 1] - p0);
+    Task* t = tmp + p0;
+    for (int i = 1; i < n; ++i) {  // insertion sort, stable, descending cost
+        const Task x = t[i];
+        int j = i - 1;
+        while (j >= 0 && t[j].cost < x.cost) {
+            t[j + 1] = t[j];
+            --j;
+        }
+        t[j + 1] = x;
+    }
+    int64_t load[kTaskWarps];
+    int cnt[kTaskWarps];
+    for (int w = 0; w < kTaskWarps; ++w) load[w] = cnt[w] = 0;
+    for (int i = 0; i < n; ++i) {
+        int best = 0;
+        for (int w = 1; w < kTaskWarps; ++w)
+            if (load[w] < load[best]) best = w;
+        load[best] += t[i].cost;
+        t[i].pad_ = static_cast<uint8_t>(best);
+        ++cnt[best];
+    }
+    int pos[kTaskWarps];
+    int acc = 0;
+    for (int w = 0; w < kTaskWarps; ++w) {
+        wptr[b * (kTaskWarps + 1) + w] = acc;
+        pos[w] = acc;
+        acc += cnt[w];
+    }
+    wptr[b * (kTaskWarps + 1) + kTaskWarps] = acc;
+    for (int i = 0; i < n; ++i) out[p0 + pos[t[i].pad_]++] = t[i];
+}
+
+}  // namespace
+
+void free_tasks(DevIndex& ix) {
+    for (void* p : {static_cast<void*>(ix.ht_ptr), static_cast<void*>(ix.ht), static_cast<void*>(ix.ht_wptr),
+                    static_cast<void*>(ix.rt_ptr), static_cast<void*>(ix.rt), static_cast<void*>(ix.rt_wptr)})
+        if (p) cudaFree(p);
+    ix.ht_ptr = ix.rt_ptr = nullptr;
+    ix.ht = ix.rt = nullptr;
+    ix.ht_wptr = ix.rt_wptr = nullptr;
+}
+
+void build_tasks_device(const SysParams& P, DevIndex& ix, cudaStream_t st) {
+    free_tasks(ix);
+    const int64_t nb = ix.nblock;
+    const int T = 128;
+    const unsigned grid = static_cast<unsigned>((nb + T - 1) / T);
+    int64_t* hcnt = talloc<int64_t>(nb + 1);
+    int64_t* rcnt = talloc<int64_t>(nb + 1);
+    TaskStats* d_st = talloc<TaskStats>(1);
+    KBG_CUDA(cudaMemsetAsync(hcnt, 0, (nb + 1) * sizeof(int64_t), st));
+    KBG_CUDA(cudaMemsetAsync(rcnt, 0, (nb + 1) * sizeof(int64_t), st));
+    KBG_CUDA(cudaMemsetAsync(d_st, 0, sizeof(TaskStats), st));
+    k_tasks<<<grid, T, 0, st>>>(P, nb, ix.blk_ptr, ix.cov_atom, ix.cov_mask, hcnt, rcnt, nullptr, nullptr, nullptr,
+                                nullptr, d_st);
+    KBG_CUDA(cudaGetLastError());
+    ix.ht_ptr = talloc<int64_t>(nb + 1);
+    ix.rt_ptr = talloc<int64_t>(nb + 1);
+    ix.nhtask = scan_total(hcnt, ix.ht_ptr, nb, st);
+    ix.nrtask = scan_total(rcnt, ix.rt_ptr, nb, st);
+    Task* htmp = talloc<Task>(ix.nhtask);
+    Task* rtmp = talloc<Task>(ix.nrtask);
+    k_tasks<<<grid, T, 0, st>>>(P, nb, ix.blk_ptr, ix.cov_atom, ix.cov_mask, nullptr, nullptr, ix.ht_ptr, ix.rt_ptr,
+                                htmp, rtmp, d_st);
+    KBG_CUDA(cudaGetLastError());
+    ix.ht = talloc<Task>(ix.nhtask);
+    ix.rt = talloc<Task>(ix.nrtask);
+    ix.ht_wptr = talloc<int32_t>(nb * (kTaskWarps + 1));
+    ix.rt_wptr = talloc<int32_t>(nb * (kTaskWarps + 1));
+    k_tasks_lpt<<<grid, T, 0, st>>>(nb, ix.ht_ptr, htmp, ix.ht, ix.ht_wptr);
+    k_tasks_lpt<<<grid, T, 0, st>>>(nb, ix.rt_ptr, rtmp, ix.rt, ix.rt_wptr);
+    KBG_CUDA(cudaGetLastError());
+    TaskStats hs;
+    KBG_CUDA(cudaMemcpyAsync(&hs, d_st, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    KBG_CUDA(cudaStreamSynchronize(st));
+    cudaFree(hcnt);
+    cudaFree(rcnt);
+    cudaFree(d_st);
+    cudaFree(htmp);
+    cudaFree(rtmp);
+    if (hs.too_many_covers)
+        throw Error(KBG_ERR_DIMENSION, "a grid block is covered by " + std::to_string(hs.too_many_covers) +
+                                           " atom images (max " + std::to_string(kMaxCoverPerBlock) + ")");
+    ix.max_rows_padded = hs.max_rows;
+    ix.max_htask = hs.max_h;
+    ix.max_rtask = hs.max_r;
+}
+
+}  // namespace kbg
