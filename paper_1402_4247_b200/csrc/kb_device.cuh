@@ -119,9 +119,10 @@ namespace kbg {
 
 // Row groups of a block (shared by the task builder and the grid kernels):
 // consecutive covers are packed into groups of <= kGroupRows orbitals; a cover
-// with more orbitals forms a group of its own. Group rows are padded to a
-// multiple of 8 (DMMA row tiles); covers' rows are contiguous inside a group.
-// norb(c) gives the orbital count of local cover c. Returns the group count.
+// with more orbitals forms a group of its own. Rows are not padded: a group's
+// 8-row DMMA tiles may run into the next group's rows, which the kernels mask
+// out. norb(c) gives the orbital count of local cover c; g_rows = actual rows.
+// Returns the group count.
 template <class NorbF>
 __host__ __device__ inline int make_groups(int ncov, NorbF norb, int* g_first, int* g_end, int* g_row0,
                                            int* g_rows, int* c_row0, int* c_group) {
@@ -130,7 +131,7 @@ __host__ __device__ inline int make_groups(int ncov, NorbF norb, int* g_first, i
         const int n = norb(c);
         if (cur == 0 || cur + n > kGroupRows) {
             if (cur > 0) {
-                g_rows[ng - 1] = (cur + 7) & ~7;
+                g_rows[ng - 1] = cur;
                 next_row = g_row0[ng - 1] + g_rows[ng - 1];
             }
             g_first[ng] = c;
@@ -143,12 +144,12 @@ __host__ __device__ inline int make_groups(int ncov, NorbF norb, int* g_first, i
         cur += n;
         g_end[ng - 1] = c + 1;
         if (cur >= kGroupRows) {
-            g_rows[ng - 1] = (cur + 7) & ~7;
+            g_rows[ng - 1] = cur;
             next_row = g_row0[ng - 1] + g_rows[ng - 1];
             cur = 0;
         }
     }
-    if (cur > 0) g_rows[ng - 1] = (cur + 7) & ~7;
+    if (cur > 0) g_rows[ng - 1] = cur;
     return ng;
 }
 

@@ -31,7 +31,7 @@ struct CoverS {
 };
 
 struct GroupS {
-    int first, end, row0, tm;
+    int first, end, row0, rows, tm;  // covers [first, end), Phi rows [row0, row0 + rows), tm = ceil(rows / 8)
 };
 
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
@@ -64,6 +64,8 @@ struct Smem {
     int32_t* off2d;  // [ncov][ncov] value offset of canonical pair (ci <= cj) with common points, else -1
     uint8_t* rcov;   // [rows] cover of each Phi row (kNoCover for pad rows)
     uint8_t* rorb;   // [rows] orbital index inside that cover
+    uint8_t* pom;    // [ngrp][ncov] octets shared by group g (rows ci <= cj) and cover cj
+    uint64_t* pbits; // [ngrp][2] covers cj with a shared octet in half h
     Task* task;
     int32_t* wptr;   // [kTaskWarps + 1]
 };
@@ -90,11 +92,15 @@ __host__ __device__ inline size_t smem_layout(const GridArgs& g, int acc_doubles
     o += align16(static_cast<size_t>(g.max_tasks) * sizeof(Task));
     off[8] = o;
     o += align16((kTaskWarps + 1) * sizeof(int32_t));
+    off[9] = o;
+    o += align16(static_cast<size_t>(g.max_cover) * g.max_cover);
+    off[10] = o;
+    o += align16(static_cast<size_t>(g.max_cover) * 2 * sizeof(uint64_t));
     return o;
 }
 
 __device__ __forceinline__ Smem carve(unsigned char* base, const GridArgs& g, int acc_doubles) {
-    size_t off[9];
+    size_t off[11];
     smem_layout(g, acc_doubles, off);
     Smem s;
     s.phi = reinterpret_cast<double*>(base + off[0]);
@@ -106,6 +112,8 @@ __device__ __forceinline__ Smem carve(unsigned char* base, const GridArgs& g, in
     s.rorb = base + off[6];
     s.task = reinterpret_cast<Task*>(base + off[7]);
     s.wptr = reinterpret_cast<int32_t*>(base + off[8]);
+    s.pom = base + off[9];
+    s.pbits = reinterpret_cast<uint64_t*>(base + off[10]);
     return s;
 }
 
@@ -146,7 +154,7 @@ __device__ Block stage_block(const GridArgs& g, int64_t b, const Smem& sm) {
         int gf[kMaxCoverPerBlock], ge[kMaxCoverPerBlock], gr0[kMaxCoverPerBlock], grs[kMaxCoverPerBlock],
             cr0[kMaxCoverPerBlock], cg[kMaxCoverPerBlock];
         const int ng = make_groups(ncov, [&](int c) { return sm.cov[c].norb; }, gf, ge, gr0, grs, cr0, cg);
-        for (int q = 0; q < ng; ++q) sm.grp[q] = GroupS{gf[q], ge[q], gr0[q], grs[q] >> 3};
+        for (int q = 0; q < ng; ++q) sm.grp[q] = GroupS{gf[q], ge[q], gr0[q], grs[q], (grs[q] + 7) >> 3};
         for (int c = 0; c < ncov; ++c) {
             sm.cov[c].row0 = cr0[c];
             sm.cov[c].grp = cg[c];
@@ -163,7 +171,26 @@ __device__ Block stage_block(const GridArgs& g, int64_t b, const Smem& sm) {
     __syncthreads();
     blk.ngrp = sm.cov[0].grp >> 16;
     const GroupS& lg = sm.grp[blk.ngrp - 1];
-    blk.rows = lg.row0 + 8 * lg.tm;
+    blk.rows = lg.row0 + lg.rows;
+    // partner octet table: pom[g][cj] = octets shared by cover cj and the rows
+    // ci <= cj of group g; pbits[g][h] = the covers cj with a shared octet in half h
+    for (int i = tid; i < blk.ngrp * 2; i += nt) sm.pbits[i] = 0;
+    for (int i = tid; i < blk.ngrp * ncov; i += nt) {
+        const int q = i / ncov, cj = i % ncov;
+        const GroupS& G = sm.grp[q];
+        uint64_t m = 0;
+        if (cj >= G.first)
+            for (int ci = G.first; ci < G.end && ci <= cj; ++ci) m |= sm.cov[ci].mask & sm.cov[cj].mask;
+        sm.pom[i] = static_cast<uint8_t>(octet_bits(m));
+    }
+    __syncthreads();
+    if (tid < blk.ngrp * 2) {
+        const int q = tid >> 1, h = tid & 1;
+        uint64_t bits = 0;
+        for (int cj = 0; cj < ncov; ++cj)
+            if ((sm.pom[q * ncov + cj] >> (4 * h)) & 0xF) bits |= 1ull << cj;
+        sm.pbits[tid] = bits;
+    }
     if (tid < ncov) {
         const CoverS& cv = sm.cov[tid];
         for (int o = 0; o < cv.norb; ++o) {
@@ -214,7 +241,7 @@ __device__ __forceinline__ int64_t slot_point(const SysParams& P, int bi, int bj
 // Output tile rows ra0 + [0, 8*TM) (inside group g) x columns cb0 + [0, 8*TN)
 // of cover cj. Tiles with <= 2 DMMAs per quad alternate two accumulator sets.
 template <int TM, int TN>
-__device__ __forceinline__ void h_tile(const Smem& sm, int ncov, int cj, int ra0, int cb0, uint32_t qm,
+__device__ __forceinline__ void h_tile(const Smem& sm, int ncov, int cj, int ra0, int rend, int cb0, uint32_t qm,
                                        double* __restrict__ H, double sign, int scatter, int lane) {
     constexpr int NACC = (TM * TN <= 2) ? 2 : 1;
     double c[NACC][TM][TN][2];
@@ -259,7 +286,7 @@ __device__ __forceinline__ void h_tile(const Smem& sm, int ncov, int cj, int ra0
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
         const int r = ra0 + 8 * i + (lane >> 2);
-        const int ci = sm.rcov[r];
+        const int ci = r < rend ? sm.rcov[r] : kNoCover;
         const int off = (ci != kNoCover && ci <= cj) ? sm.off2d[ci * ncov + cj] : -1;
         const int ri = sm.rorb[r];
 #pragma unroll
@@ -288,15 +315,15 @@ __device__ __forceinline__ void h_task(const Smem& sm, int ncov, const Task& t, 
         const int tm = min(2, G.tm - i0);
         for (int j0 = 0; j0 < (nb + 7) >> 3; j0 += 2) {
             const int tn = min(2, ((nb + 7) >> 3) - j0);
-            const int ra0 = G.row0 + 8 * i0, cb0 = 8 * j0;
+            const int ra0 = G.row0 + 8 * i0, cb0 = 8 * j0, rend = G.row0 + G.rows;
             if (tm == 2 && tn == 2)
-                h_tile<2, 2>(sm, ncov, t.cj, ra0, cb0, qm, H, sign, scatter, lane);
+                h_tile<2, 2>(sm, ncov, t.cj, ra0, rend, cb0, qm, H, sign, scatter, lane);
             else if (tm == 2)
-                h_tile<2, 1>(sm, ncov, t.cj, ra0, cb0, qm, H, sign, scatter, lane);
+                h_tile<2, 1>(sm, ncov, t.cj, ra0, rend, cb0, qm, H, sign, scatter, lane);
             else if (tn == 2)
-                h_tile<1, 2>(sm, ncov, t.cj, ra0, cb0, qm, H, sign, scatter, lane);
+                h_tile<1, 2>(sm, ncov, t.cj, ra0, rend, cb0, qm, H, sign, scatter, lane);
             else
-                h_tile<1, 1>(sm, ncov, t.cj, ra0, cb0, qm, H, sign, scatter, lane);
+                h_tile<1, 1>(sm, ncov, t.cj, ra0, rend, cb0, qm, H, sign, scatter, lane);
         }
     }
 }
@@ -342,35 +369,41 @@ __device__ __forceinline__ void gather_a(const Smem& sm, int ncov, const RowInfo
 #pragma unroll
     for (int t = 0; t < TM; ++t) {
         const int ci = ri.ci[t];
-        const int off = (ci != kNoCover && ci <= cj) ? sm.off2d[ci * ncov + cj] : -1;
+        const int off = (ci <= cj) ? sm.off2d[ci * ncov + cj] : -1;  // ci = kNoCover (255) fails ci <= cj
         const double fac = ci < cj ? 2.0 : 1.0;
-        const double* row = Ds + off + ri.ri[t] * nb;
+        const double* row = Ds + off + ri.ri[t] * nb + 16 * kc + (lane & 3);
+        const int jmax = nb - 16 * kc - (lane & 3);
 #pragma unroll
-        for (int s = 0; s < 4; ++s) {
-            const int j = 16 * kc + 4 * s + (lane & 3);
-            a[t][s] = (off >= 0 && j < nb) ? fac * __ldg(row + j) : 0.0;
+        for (int s = 0; s < 4; ++s) a[t][s] = (off >= 0 && 4 * s < jmax) ? fac * __ldg(row + 4 * s) : 0.0;
+    }
+}
+
+template <int TM, int KS>
+__device__ __forceinline__ void rho_partner(const double* __restrict__ pb, int swb, uint32_t om4,
+                                            const double (&a)[TM][4], double (&y)[TM][4][2], int colbase) {
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+        if (!((om4 >> o) & 1u)) continue;
+        const int col = colbase + 8 * o;
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+            const double bv = pb[s * 256 + (col ^ swb)];
+#pragma unroll
+            for (int t = 0; t < TM; ++t) dmma(y[t][o], a[t][s], bv);
         }
     }
 }
 
 template <int TM>
-__device__ __forceinline__ uint32_t partner_octets(const Smem& sm, const GroupS& G, int cj, uint32_t hm) {
-    const uint64_t mj = sm.cov[cj].mask;
-    uint64_t m = 0;
-    const int last = min(G.end, cj + 1);
-    for (int ci = G.first; ci < last; ++ci) m |= sm.cov[ci].mask & mj;
-    return octet_bits(m) & hm;
-}
-
-template <int TM>
-__device__ void rho_task_rows(const Smem& sm, int ncov, const GroupS& G, int ra0, int h, const double* __restrict__ Ds,
+__device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, const double* __restrict__ Ds,
                               double* __restrict__ racc, int lane) {
-    const uint32_t hm = 0xFu << (4 * h);
+    const GroupS& G = sm.grp[gi];
+    const int rend = G.row0 + G.rows;
     RowInfo<TM> ri;
 #pragma unroll
     for (int t = 0; t < TM; ++t) {
         const int r = ra0 + 8 * t + (lane >> 2);
-        ri.ci[t] = sm.rcov[r];
+        ri.ci[t] = r < rend ? sm.rcov[r] : kNoCover;
         ri.ri[t] = sm.rorb[r];
     }
     double y[TM][4][2];
@@ -378,54 +411,37 @@ __device__ void rho_task_rows(const Smem& sm, int ncov, const GroupS& G, int ra0
     for (int t = 0; t < TM; ++t)
 #pragma unroll
         for (int o = 0; o < 4; ++o) y[t][o][0] = y[t][o][1] = 0.0;
-    // partner list: covers cj >= first(G) sharing an octet of this half with the group
-    auto next_partner = [&](int from, uint32_t& om) {
-        for (int c = from; c < ncov; ++c) {
-            om = partner_octets<TM>(sm, G, c, hm);
-            if (om) return c;
-        }
-        return ncov;
-    };
-    uint32_t om_n;
-    int cj = next_partner(G.first, om_n);
+    const uint8_t* pom = sm.pom + gi * ncov;
+    uint64_t bits = sm.pbits[2 * gi + h];
+    const int colbase = 32 * h + (lane >> 2);
     double nxt[TM][4];
-    if (cj < ncov) gather_a<TM>(sm, ncov, ri, cj, 0, Ds, lane, nxt);
-    while (cj < ncov) {
-        const uint32_t om = om_n;
+    if (bits) gather_a<TM>(sm, ncov, ri, __ffsll(bits) - 1, 0, Ds, lane, nxt);
+    while (bits) {
+        const int cj = __ffsll(bits) - 1;
+        bits &= bits - 1;
+        const uint32_t om4 = (pom[cj] >> (4 * h)) & 0xFu;
         const CoverS& B = sm.cov[cj];
-        const int nkc = (B.norb + 15) >> 4;
         double a[TM][4];
 #pragma unroll
         for (int t = 0; t < TM; ++t)
 #pragma unroll
             for (int s = 0; s < 4; ++s) a[t][s] = nxt[t][s];
-        const int cn = (nkc == 1) ? next_partner(cj + 1, om_n) : cj;
-        if (nkc == 1 && cn < ncov) gather_a<TM>(sm, ncov, ri, cn, 0, Ds, lane, nxt);
+        const int nkc = (B.norb + 15) >> 4;
+        if (nkc == 1 && bits) gather_a<TM>(sm, ncov, ri, __ffsll(bits) - 1, 0, Ds, lane, nxt);
         for (int kc = 0; kc < nkc; ++kc) {
             if (kc > 0) gather_a<TM>(sm, ncov, ri, cj, kc, Ds, lane, a);
             const int ks = min(4, (B.norb - 16 * kc + 3) >> 2);
             const int rb = B.row0 + 16 * kc + (lane & 3);
             const double* pb = sm.phi + rb * 64;
-#pragma unroll
-            for (int o = 0; o < 4; ++o) {
-                if (!((om >> (4 * h + o)) & 1u)) continue;
-                const int col = 8 * (4 * h + o) + (lane >> 2);
-#pragma unroll
-                for (int s = 0; s < 4; ++s) {
-                    if (s < ks) {
-                        const double bv = pb[s * 256 + (col ^ swz(rb))];
-#pragma unroll
-                        for (int t = 0; t < TM; ++t) dmma(y[t][o], a[t][s], bv);
-                    }
-                }
+            const int swb = swz(rb);
+            switch (ks) {
+                case 1: rho_partner<TM, 1>(pb, swb, om4, a, y, colbase); break;
+                case 2: rho_partner<TM, 2>(pb, swb, om4, a, y, colbase); break;
+                case 3: rho_partner<TM, 3>(pb, swb, om4, a, y, colbase); break;
+                default: rho_partner<TM, 4>(pb, swb, om4, a, y, colbase); break;
             }
         }
-        if (nkc == 1) {
-            cj = cn;
-        } else {
-            cj = next_partner(cj + 1, om_n);
-            if (cj < ncov) gather_a<TM>(sm, ncov, ri, cj, 0, Ds, lane, nxt);
-        }
+        if (nkc > 1 && bits) gather_a<TM>(sm, ncov, ri, __ffsll(bits) - 1, 0, Ds, lane, nxt);
     }
     // rho(slot) += sum over rows of Phi_row(slot) * Y(row, slot)
 #pragma unroll
@@ -452,9 +468,9 @@ __device__ __forceinline__ void rho_task(const Smem& sm, int ncov, const Task& t
     const GroupS& G = sm.grp[t.g];
     for (int i0 = 0; i0 < G.tm; i0 += 2) {
         if (G.tm - i0 >= 2)
-            rho_task_rows<2>(sm, ncov, G, G.row0 + 8 * i0, t.half, Ds, racc, lane);
+            rho_task_rows<2>(sm, ncov, t.g, G.row0 + 8 * i0, t.half, Ds, racc, lane);
         else
-            rho_task_rows<1>(sm, ncov, G, G.row0 + 8 * i0, t.half, Ds, racc, lane);
+            rho_task_rows<1>(sm, ncov, t.g, G.row0 + 8 * i0, t.half, Ds, racc, lane);
     }
 }
 
@@ -592,7 +608,7 @@ void set_smem(K kernel, size_t bytes) {
 }  // namespace
 
 size_t grid_smem_bytes(const GridArgs& g, int nwarps, bool density) {
-    size_t off[9];
+    size_t off[11];
     return smem_layout(g, density ? nwarps * 64 : 64, off);
 }
 

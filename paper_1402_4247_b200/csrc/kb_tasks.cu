@@ -56,7 +56,7 @@ __global__ void k_tasks(SysParams P, int64_t nblock, const int32_t* __restrict__
     const int ng = make_groups(ncov, [&](int c) { return norb[c]; }, g_first, g_end, g_row0, g_rows, c_row0, c_group);
     int64_t nh = 0, nr = 0;
     for (int g = 0; g < ng; ++g) {
-        const int tm = g_rows[g] >> 3;
+        const int tm = (g_rows[g] + 7) >> 3;
         for (int cj = g_first[g]; cj < ncov; ++cj) {
             const uint64_t mj = cov_mask[c0 + cj];
             uint32_t qm = 0;
