@@ -176,6 +176,7 @@ int kbg_last_tally(const kbg_ctx* ctx, kbg_tally* out);
 #define KBG_OPT_WARPS 1
 #define KBG_OPT_FAULT_SIGN 2 /* test hook: flip the sign of the H accumulate (kband fault_proc6_sign analogue) */
 #define KBG_OPT_SCATTER_STORE 3 /* timing experiment: plain stores instead of atomics (H is WRONG) */
+#define KBG_OPT_PERSIST 4 /* 1 (default): persistent warp-specialized kernels when they fit; 0: one CTA per block */
 int kbg_set_option(kbg_ctx* ctx, int option, int64_t value);
 
 const char* kbg_last_error(const kbg_ctx* ctx);

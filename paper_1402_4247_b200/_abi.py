@@ -26,6 +26,7 @@ KBG_ERR_NCCL = 6
 KBG_OPT_WARPS = 1
 KBG_OPT_FAULT_SIGN = 2
 KBG_OPT_SCATTER_STORE = 3
+KBG_OPT_PERSIST = 4
 KBG_CELL_PRIMITIVE = 0
 KBG_CELL_CUBIC = 1
 

@@ -21,6 +21,11 @@ struct kbg_ctx {
     bool built = false;
     int64_t blk_begin = 0, blk_end = 0;
     int nwarps = 8;
+    bool persist_ok = false;   // two staging buffers fit: persistent kernels
+    int persist = 1;           // option: use the persistent kernels when they fit
+    double* d_dmr = nullptr;   // repacked DM scratch
+    size_t cap_dmr = 0;
+    int* d_counter = nullptr;  // persistent work counter
     double sign = 1.0;
     int scatter = 0;
     cudaStream_t stream = nullptr;
@@ -168,6 +173,11 @@ kbg::GridArgs grid_args(kbg_ctx* c, int nspin, double dV, const double* in, doub
     g.max_rows = c->ix.max_rows_padded + 8;
     g.max_cover = c->ix.max_cover > 0 ? c->ix.max_cover : 1;
     g.max_bpairs = c->ix.max_bpairs > 0 ? c->ix.max_bpairs : 1;
+    g.task_warps = c->ix.task_warps;
+    g.order = c->ix.order;
+    g.norder = c->ix.norder;
+    g.counter = c->d_counter;
+    g.nrep = c->ix.nrep;
     g.t_ptr = density ? c->ix.rt_ptr : c->ix.ht_ptr;
     g.tasks = density ? c->ix.rt : c->ix.ht;
     g.t_wptr = density ? c->ix.rt_wptr : c->ix.ht_wptr;
@@ -187,6 +197,24 @@ kbg::GridArgs grid_args(kbg_ctx* c, int nspin, double dV, const double* in, doub
         throw Error(KBG_ERR_DIMENSION, "grid block needs " + std::to_string(smem) +
                                            " B of shared memory (> 227 KB): too many orbitals per block");
     return g;
+}
+
+int run_density(kbg_ctx* c, int nspin, const double* d_dm, double* d_rho, cudaStream_t st) {
+    ensure(c->d_dmr, c->cap_dmr, static_cast<size_t>(nspin) * std::max<int64_t>(1, c->ix.nrep));
+    int n = kbg::launch_dm_repack(c->ix, c->P, nspin, d_dm, c->d_dmr, st);
+    kbg::GridArgs g = grid_args(c, nspin, 0.0, d_dm, d_rho, true);
+    g.dmr = c->d_dmr;
+    if (c->persist_ok && c->persist)
+        n += kbg::launch_density_persist(g, st);
+    else
+        n += kbg::launch_density(g, c->blk_end - c->blk_begin, c->nwarps, st);
+    return n;
+}
+
+int run_hamiltonian(kbg_ctx* c, int nspin, double dV, const double* d_veff, double* d_h, cudaStream_t st) {
+    const kbg::GridArgs g = grid_args(c, nspin, dV, d_veff, d_h, false);
+    if (c->persist_ok && c->persist) return kbg::launch_hamiltonian_persist(g, st);
+    return kbg::launch_hamiltonian(g, c->blk_end - c->blk_begin, c->nwarps, st);
 }
 
 void shard(kbg_ctx* c) {
@@ -269,9 +297,28 @@ int kbg_build_index(kbg_ctx* c) {
         c->built = false;
         c->hix = kbg::HostIndex();
         kbg::build_index_device(c->P, c->ix, c->stream);
-        kbg::build_tasks_device(c->P, c->ix, c->stream);
+        kbg::build_tasks_device(c->P, c->ix, kbg::kPersistConsumers, c->stream);
         shard(c);
         c->built = true;
+        {
+            const kbg::GridArgs gd = grid_args(c, 1, 0.0, nullptr, nullptr, true);
+            const kbg::GridArgs gh = grid_args(c, 1, 0.0, nullptr, nullptr, false);
+            c->persist_ok = kbg::persist_fits(gd, true) && kbg::persist_fits(gh, false);
+        }
+        if (!c->persist_ok) kbg::build_tasks_device(c->P, c->ix, 8, c->stream);
+        // owned blocks, heaviest first, for the persistent kernels' work counter
+        std::vector<int64_t> cost(c->ix.nblock);
+        KBG_CUDA(cudaMemcpy(cost.data(), c->ix.blk_cost, cost.size() * sizeof(int64_t), cudaMemcpyDeviceToHost));
+        std::vector<int64_t> order;
+        for (int64_t b = c->blk_begin; b < c->blk_end; ++b) order.push_back(b);
+        std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return cost[x] > cost[y]; });
+        if (c->ix.order) cudaFree(c->ix.order);
+        c->ix.order = nullptr;
+        c->ix.norder = static_cast<int64_t>(order.size());
+        KBG_CUDA(cudaMalloc(&c->ix.order, std::max<size_t>(1, order.size()) * sizeof(int64_t)));
+        if (!order.empty())
+            KBG_CUDA(cudaMemcpy(c->ix.order, order.data(), order.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+        if (!c->d_counter) KBG_CUDA(cudaMalloc(&c->d_counter, sizeof(int)));
     });
 }
 
@@ -318,9 +365,7 @@ int kbg_density_dev(kbg_ctx* c, int nspin, const double* d_dm, double* d_rho, vo
         check_nspin(nspin);
         require_index(c);
         KBG_CUDA(cudaSetDevice(c->device));
-        const kbg::GridArgs g = grid_args(c, nspin, 0.0, d_dm, d_rho, true);
-        c->last_launches = kbg::launch_density(g, c->blk_end - c->blk_begin, c->nwarps,
-                                               static_cast<cudaStream_t>(stream));
+        c->last_launches = run_density(c, nspin, d_dm, d_rho, static_cast<cudaStream_t>(stream));
         c->tally.flops = nspin * (2.0 * c->ix.sum_m2 + 2.0 * c->ix.sum_m);
         c->tally.bytes = 8.0 * nspin * (c->ix.nnz + c->npts);
     });
@@ -335,8 +380,7 @@ int kbg_hamiltonian_accumulate_dev(kbg_ctx* c, int nspin, const double* d_veff, 
         KBG_CUDA(cudaSetDevice(c->device));
         const cudaStream_t st = static_cast<cudaStream_t>(stream);
         KBG_CUDA(cudaMemsetAsync(d_h, 0, sizeof(double) * nspin * c->ix.nnz, st));
-        const kbg::GridArgs g = grid_args(c, nspin, dV, d_veff, d_h, false);
-        c->last_launches = kbg::launch_hamiltonian(g, c->blk_end - c->blk_begin, c->nwarps, st);
+        c->last_launches = run_hamiltonian(c, nspin, dV, d_veff, d_h, st);
         c->tally.flops = nspin * 2.0 * c->ix.sum_m2;
         c->tally.bytes = 8.0 * nspin * (c->ix.nnz + c->npts);
     });
@@ -386,8 +430,7 @@ int kbg_density(kbg_ctx* c, int nspin, const double* dm, double* rho) {
         if (dmax > 1e-13 * amax)
             throw Error(KBG_ERR_CONSISTENCY, "density: DM violates DM_ba(-R) = DM_ab(R)^T by " + std::to_string(dmax));
         if (c->nranks > 1) KBG_CUDA(cudaMemsetAsync(c->d_out, 0, nout * sizeof(double), c->stream));
-        const kbg::GridArgs g = grid_args(c, nspin, 0.0, c->d_in, c->d_out, true);
-        c->last_launches = 1 + kbg::launch_density(g, c->blk_end - c->blk_begin, c->nwarps, c->stream);
+        c->last_launches = 1 + run_density(c, nspin, c->d_in, c->d_out, c->stream);
         KBG_CUDA(cudaMemcpyAsync(rho, c->d_out, nout * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         KBG_CUDA(cudaStreamSynchronize(c->stream));
         c->tally.flops = nspin * (2.0 * c->ix.sum_m2 + 2.0 * c->ix.sum_m);
@@ -407,8 +450,7 @@ int kbg_hamiltonian(kbg_ctx* c, int nspin, const double* veff, double dV, double
         ensure(c->d_out, c->cap_out, nout);
         KBG_CUDA(cudaMemcpyAsync(c->d_in, veff, nin * sizeof(double), cudaMemcpyHostToDevice, c->stream));
         KBG_CUDA(cudaMemsetAsync(c->d_out, 0, nout * sizeof(double), c->stream));
-        const kbg::GridArgs g = grid_args(c, nspin, dV, c->d_in, c->d_out, false);
-        int n = kbg::launch_hamiltonian(g, c->blk_end - c->blk_begin, c->nwarps, c->stream);
+        int n = run_hamiltonian(c, nspin, dV, c->d_in, c->d_out, c->stream);
         n += kbg::launch_mirror(c->ix, c->P, nspin, c->d_out, c->stream);
         c->last_launches = n;
         KBG_CUDA(cudaMemcpyAsync(h, c->d_out, nout * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -463,6 +505,9 @@ int kbg_set_option(kbg_ctx* c, int option, int64_t value) {
         case KBG_OPT_SCATTER_STORE:
             c->scatter = value ? 1 : 0;
             return KBG_OK;
+        case KBG_OPT_PERSIST:
+            c->persist = value ? 1 : 0;
+            return KBG_OK;
         default:
             c->err = "set_option: unknown option";
             return KBG_ERR_CONFIG;
@@ -481,6 +526,8 @@ void kbg_destroy(kbg_ctx* c) {
     if (c->d_in) cudaFree(c->d_in);
     if (c->d_out) cudaFree(c->d_out);
     if (c->d_check) cudaFree(c->d_check);
+    if (c->d_dmr) cudaFree(c->d_dmr);
+    if (c->d_counter) cudaFree(c->d_counter);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }

@@ -1,0 +1,471 @@
+// Device core of the grid kernels, shared by the one-CTA-per-block kernels
+// (kb_grid.cu) and the persistent warp-specialized kernels (kb_persist.cu).
+//
+// Per grid block (4x4x4 points = 64 slots) a shared-memory buffer holds
+//   Phi      FP64, rows x 64 slots: the covers' (atom images') orbitals, rows
+//            packed into row groups of <= 16 orbitals (two 8-row DMMA tiles);
+//            Phi[row][slot] at row*64 + (slot ^ 4*(row & 3)), so any 4
+//            consecutive rows x 4 slots (a half-warp DMMA fragment) hit 32 banks;
+//   tables   covers, groups, pair offsets off2d[ci][cj], row -> (cover,
+//            orbital), partner octets, this block's warp task list.
+// H task (group g, partner cj >= first(g)): C(16 x 8*TN) += Phi_g diag(V dV)
+//   Phi_cj^T over the common 1x2x2 quads with mma.sync.m8n8k4.f64 (SASS
+//   DMMA); canonical rows (cover ci <= cj) are scattered with FP64 atomics.
+// rho task (group g, octet half h): Y(16 x 8 slots) += D'(16 x n_cj)
+//   Phi_cj(n_cj x 8) over all partners cj >= first(g) in registers, D' =
+//   repacked DM (x2 off the (a,a,0) blocks: the symmetric half), then
+//   rho(slot) += sum_rows Phi_g * Y once per task.
+#pragma once
+
+#include "kb_device.cuh"
+
+namespace kbg {
+namespace core {
+
+struct CoverS {
+    double t[3];
+    uint64_t mask;
+    int row0;
+    int norb;
+    int sp;
+    int grp;
+};
+
+struct GroupS {
+    int first, end, row0, rows, tm;  // covers [first, end), Phi rows [row0, row0 + rows), tm = ceil(rows / 8)
+};
+
+struct Meta {
+    int64_t block;  // grid block staged in this buffer (-1: end of work)
+    int ncov, ngrp, rows, done;
+};
+
+constexpr uint8_t kNoCover = 0xFF;
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+// Octets (2x2x2 cubes, 8 consecutive slots) with any bit set: OR-fold each
+// byte into its low bit, then gather the 8 low bits with one multiply.
+__device__ __forceinline__ uint32_t octet_bits(uint64_t m) {
+    m |= m >> 4;
+    m |= m >> 2;
+    m |= m >> 1;
+    return static_cast<uint32_t>(((m & 0x0101010101010101ull) * 0x0102040810204080ull) >> 56);
+}
+
+__device__ __forceinline__ int swz(int row) { return (row & 3) << 2; }
+__device__ __forceinline__ int phi_idx(int row, int slot) { return row * 64 + (slot ^ swz(row)); }
+
+struct Smem {
+    double* phi;
+    double* acc;     // H: w[nspin][64];  rho: racc[nspin][acc_warps][64]
+    CoverS* cov;
+    GroupS* grp;
+    int32_t* off2d;  // [ncov][ncov] offset of canonical pair (ci <= cj) with common points (H: value, rho: repacked)
+    uint8_t* rcov;   // [rows] cover of each Phi row (kNoCover for the tail rows)
+    uint8_t* rorb;   // [rows] orbital index inside that cover
+    uint8_t* pom;    // [ngrp][ncov] octets shared by group g (rows ci <= cj) and cover cj
+    uint64_t* pbits; // [ngrp][2] covers cj with a shared octet in half h
+    Task* task;
+    int32_t* wptr;   // [kMaxTaskWarps + 1]
+    Meta* meta;
+};
+
+__host__ __device__ __forceinline__ size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
+
+// Byte size of one buffer; off[] receives the section offsets.
+__host__ __device__ inline size_t buffer_layout(const GridArgs& g, size_t acc_doubles, size_t* off) {
+    size_t o = 0;
+    const size_t mc = static_cast<size_t>(g.max_cover);
+    off[0] = o;
+    o += align16(static_cast<size_t>(g.max_rows) * 64 * sizeof(double));
+    off[1] = o;
+    o += align16(acc_doubles * sizeof(double));
+    off[2] = o;
+    o += align16(mc * sizeof(CoverS));
+    off[3] = o;
+    o += align16(mc * sizeof(GroupS));
+    off[4] = o;
+    o += align16(mc * mc * sizeof(int32_t));
+    off[5] = o;
+    o += align16(static_cast<size_t>(g.max_rows));
+    off[6] = o;
+    o += align16(static_cast<size_t>(g.max_rows));
+    off[7] = o;
+    o += align16(mc * mc);
+    off[8] = o;
+    o += align16(mc * 2 * sizeof(uint64_t));
+    off[9] = o;
+    o += align16(static_cast<size_t>(g.max_tasks) * sizeof(Task));
+    off[10] = o;
+    o += align16((kMaxTaskWarps + 1) * sizeof(int32_t));
+    off[11] = o;
+    o += align16(sizeof(Meta));
+    return o;
+}
+
+__device__ __forceinline__ Smem carve(unsigned char* base, const GridArgs& g, size_t acc_doubles) {
+    size_t off[12];
+    buffer_layout(g, acc_doubles, off);
+    Smem s;
+    s.phi = reinterpret_cast<double*>(base + off[0]);
+    s.acc = reinterpret_cast<double*>(base + off[1]);
+    s.cov = reinterpret_cast<CoverS*>(base + off[2]);
+    s.grp = reinterpret_cast<GroupS*>(base + off[3]);
+    s.off2d = reinterpret_cast<int32_t*>(base + off[4]);
+    s.rcov = base + off[5];
+    s.rorb = base + off[6];
+    s.pom = base + off[7];
+    s.pbits = reinterpret_cast<uint64_t*>(base + off[8]);
+    s.task = reinterpret_cast<Task*>(base + off[9]);
+    s.wptr = reinterpret_cast<int32_t*>(base + off[10]);
+    s.meta = reinterpret_cast<Meta*>(base + off[11]);
+    return s;
+}
+
+__device__ __forceinline__ int64_t slot_point(const SysParams& P, int bi, int bj, int bk, int s, bool& valid) {
+    int li, lj, lk;
+    slot_decode(s, li, lj, lk);
+    const int i = bi * 4 + li, j = bj * 4 + lj, k = bk * 4 + lk;
+    valid = i < P.N[0] && j < P.N[1] && k < P.N[2];
+    return (static_cast<int64_t>(i) * P.N[1] + j) * P.N[2] + k;
+}
+
+// Stages block b into buffer sm using threads [0, nt) (tid = this thread's
+// index among them); sync() is a barrier over exactly those threads. For H
+// (density = false) also stages w = V dV for every spin; for rho zeroes the
+// per-warp accumulators. Returns ncov (0: nothing to compute).
+template <class Sync>
+__device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int tid, int nt, Sync&& sync, bool density,
+                           int acc_warps) {
+    const int c0 = g.blk_ptr[b];
+    const int ncov = g.blk_ptr[b + 1] - c0;
+    if (tid == 0) {
+        sm.meta->block = b;
+        sm.meta->ncov = ncov;
+        sm.meta->done = 0;
+    }
+    if (ncov == 0) {
+        sync();
+        return 0;
+    }
+    const SysParams& P = g.sys;
+    if (tid < ncov) {
+        CoverS& cv = sm.cov[tid];
+        const int a = g.cov_atom[c0 + tid];
+        cv.sp = P.spc[a];
+        cv.norb = P.sp[cv.sp].norb;
+        cv.mask = g.cov_mask[c0 + tid];
+        const int R0 = g.cov_R[3 * (c0 + tid)], R1 = g.cov_R[3 * (c0 + tid) + 1], R2 = g.cov_R[3 * (c0 + tid) + 2];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) cv.t[c] = P.tau[3 * a + c] + ((R0 * P.A[c] + R1 * P.A[3 + c]) + R2 * P.A[6 + c]);
+    }
+    const int64_t tp0 = g.t_ptr[b];
+    const int ntask = static_cast<int>(g.t_ptr[b + 1] - tp0);
+    for (int i = tid; i < ntask; i += nt) sm.task[i] = g.tasks[tp0 + i];
+    if (tid <= kMaxTaskWarps) sm.wptr[tid] = g.t_wptr[b * (kMaxTaskWarps + 1) + tid];
+    for (int i = tid; i < ncov * ncov; i += nt) sm.off2d[i] = -1;
+    for (int i = tid; i < g.max_rows; i += nt) sm.rcov[i] = kNoCover;
+    int bi, bj, bk;
+    block_decode(P, b, bi, bj, bk);
+    if (density) {
+        for (int i = tid; i < g.nspin * acc_warps * 64; i += nt) sm.acc[i] = 0.0;
+    } else {
+        for (int i = tid; i < g.nspin * 64; i += nt) {
+            bool valid;
+            const int64_t pt = slot_point(P, bi, bj, bk, i & 63, valid);
+            sm.acc[i] = valid ? g.in[(i >> 6) * g.npts + pt] * g.dV : 0.0;
+        }
+    }
+    sync();
+    if (tid == 0) {
+        int gf[kMaxCoverPerBlock], ge[kMaxCoverPerBlock], gr0[kMaxCoverPerBlock], grs[kMaxCoverPerBlock],
+            cr0[kMaxCoverPerBlock], cg[kMaxCoverPerBlock];
+        const int ng = make_groups(ncov, [&](int c) { return sm.cov[c].norb; }, gf, ge, gr0, grs, cr0, cg);
+        for (int q = 0; q < ng; ++q) sm.grp[q] = GroupS{gf[q], ge[q], gr0[q], grs[q], (grs[q] + 7) >> 3};
+        for (int c = 0; c < ncov; ++c) {
+            sm.cov[c].row0 = cr0[c];
+            sm.cov[c].grp = cg[c];
+        }
+        sm.meta->ngrp = ng;
+        sm.meta->rows = gr0[ng - 1] + grs[ng - 1];
+    }
+    {
+        const int64_t p0 = g.bp_ptr[b], p1 = g.bp_ptr[b + 1];
+        for (int64_t e = p0 + tid; e < p1; e += nt) {
+            const BPair bp = g.bp[e];
+            sm.off2d[(bp.cicj & 0xffff) * ncov + (bp.cicj >> 16)] = density ? bp.roff : static_cast<int32_t>(bp.off);
+        }
+    }
+    sync();
+    const int ngrp = sm.meta->ngrp, rows = sm.meta->rows;
+    for (int i = tid; i < ngrp * ncov; i += nt) {
+        const int q = i / ncov, cj = i % ncov;
+        const GroupS& G = sm.grp[q];
+        uint64_t m = 0;
+        if (cj >= G.first)
+            for (int ci = G.first; ci < G.end && ci <= cj; ++ci) m |= sm.cov[ci].mask & sm.cov[cj].mask;
+        sm.pom[i] = static_cast<uint8_t>(octet_bits(m));
+    }
+    if (tid < ncov) {
+        const CoverS& cv = sm.cov[tid];
+        for (int o = 0; o < cv.norb; ++o) {
+            sm.rcov[cv.row0 + o] = static_cast<uint8_t>(tid);
+            sm.rorb[cv.row0 + o] = static_cast<uint8_t>(o);
+        }
+    }
+    for (int i = tid; i < 8 * 64; i += nt) sm.phi[rows * 64 + i] = 0.0;  // tail rows (tile overrun)
+    for (int task = tid; task < ncov * 64; task += nt) {
+        const int c = task >> 6, s = task & 63;
+        const CoverS& cv = sm.cov[c];
+        double* dst = sm.phi;
+        const int row0 = cv.row0;
+        if ((cv.mask >> s) & 1) {
+            int li, lj, lk;
+            slot_decode(s, li, lj, lk);
+            const double fi = static_cast<double>(bi * 4 + li) / P.N[0];
+            const double fj = static_cast<double>(bj * 4 + lj) / P.N[1];
+            const double fk = static_cast<double>(bk * 4 + lk) / P.N[2];
+            const double dx = (fi * P.A[0] + fj * P.A[3] + fk * P.A[6]) - cv.t[0];
+            const double dy = (fi * P.A[1] + fj * P.A[4] + fk * P.A[7]) - cv.t[1];
+            const double dz = (fi * P.A[2] + fj * P.A[5] + fk * P.A[8]) - cv.t[2];
+            const double d2 = dx * dx + dy * dy + dz * dz;
+            eval_orbitals(P.sp[cv.sp], P.tables, dx, dy, dz, d2,
+                          [&](int o, double v) { dst[phi_idx(row0 + o, s)] = v; });
+        } else {
+            for (int o = 0; o < cv.norb; ++o) dst[phi_idx(row0 + o, s)] = 0.0;
+        }
+    }
+    sync();
+    if (tid < ngrp * 2) {
+        const int q = tid >> 1, h = tid & 1;
+        uint64_t bits = 0;
+        for (int cj = 0; cj < ncov; ++cj)
+            if ((sm.pom[q * ncov + cj] >> (4 * h)) & 0xF) bits |= 1ull << cj;
+        sm.pbits[tid] = bits;
+    }
+    sync();
+    return ncov;
+}
+
+// ---- H --------------------------------------------------------------------------
+// Output tile rows ra0 + [0, 8*TM) (group rows < rend) x columns cb0 + [0, 8*TN)
+// of cover cj. Tiles with <= 2 DMMAs per quad alternate two accumulator sets.
+template <int TM, int TN>
+__device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict__ w, int ncov, int cj, int ra0,
+                                       int rend, int cb0, uint32_t qm, double* __restrict__ H, double sign,
+                                       int scatter, int lane) {
+    constexpr int NACC = (TM * TN <= 2) ? 2 : 1;
+    double c[NACC][TM][TN][2];
+#pragma unroll
+    for (int u = 0; u < NACC; ++u)
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) c[u][i][j][0] = c[u][i][j][1] = 0.0;
+    const CoverS& B = sm.cov[cj];
+    const int ra = ra0 + (lane >> 2), rb = B.row0 + cb0 + (lane >> 2);
+    const double* pa = sm.phi + ra * 64 + (lane & 3);
+    const double* pb = sm.phi + rb * 64 + (lane & 3);
+    const int sa = swz(ra), sb = swz(rb);  // 8-row steps keep row & 3
+    const double* pw = w + (lane & 3);
+    auto step = [&](int u, int q) {
+        const int col = 4 * q;
+        const double wv = pw[col];
+        double a[TM], bb[TN];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) a[i] = pa[i * 512 + (col ^ sa)] * wv;
+#pragma unroll
+        for (int j = 0; j < TN; ++j) bb[j] = pb[j * 512 + (col ^ sb)];
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) dmma(c[u][i][j], a[i], bb[j]);
+    };
+    while (qm) {
+        const int q0 = __ffs(qm) - 1;
+        qm &= qm - 1;
+        if (NACC == 2 && qm) {
+            const int q1 = __ffs(qm) - 1;
+            qm &= qm - 1;
+            step(0, q0);
+            step(NACC - 1, q1);
+        } else {
+            step(0, q0);
+        }
+    }
+    const int nb = B.norb;
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        const int r = ra0 + 8 * i + (lane >> 2);
+        const int ci = r < rend ? sm.rcov[r] : kNoCover;
+        const int off = ci <= cj ? sm.off2d[ci * ncov + cj] : -1;
+        const int ri = sm.rorb[r];
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = cb0 + 8 * j + (lane & 3) * 2 + e;
+                double v = c[0][i][j][e];
+                if (NACC == 2) v += c[NACC - 1][i][j][e];
+                if (off >= 0 && col < nb) {
+                    if (scatter == 0)
+                        atomicAdd(H + off + ri * nb + col, sign * v);
+                    else
+                        H[off + ri * nb + col] = sign * v;
+                }
+            }
+    }
+}
+
+__device__ __forceinline__ void h_task(const Smem& sm, const double* w, int ncov, const Task& t, double* H,
+                                       double sign, int scatter, int lane) {
+    const GroupS& G = sm.grp[t.g];
+    const int nb = sm.cov[t.cj].norb;
+    const uint32_t qm = t.qmask;
+    const int rend = G.row0 + G.rows;
+    for (int i0 = 0; i0 < G.tm; i0 += 2) {
+        const int tm = min(2, G.tm - i0);
+        for (int j0 = 0; j0 < (nb + 7) >> 3; j0 += 2) {
+            const int tn = min(2, ((nb + 7) >> 3) - j0);
+            const int ra0 = G.row0 + 8 * i0, cb0 = 8 * j0;
+            if (tm == 2 && tn == 2)
+                h_tile<2, 2>(sm, w, ncov, t.cj, ra0, rend, cb0, qm, H, sign, scatter, lane);
+            else if (tm == 2)
+                h_tile<2, 1>(sm, w, ncov, t.cj, ra0, rend, cb0, qm, H, sign, scatter, lane);
+            else if (tn == 2)
+                h_tile<1, 2>(sm, w, ncov, t.cj, ra0, rend, cb0, qm, H, sign, scatter, lane);
+            else
+                h_tile<1, 1>(sm, w, ncov, t.cj, ra0, rend, cb0, qm, H, sign, scatter, lane);
+        }
+    }
+}
+
+// ---- rho ------------------------------------------------------------------------
+// Repacked DM (k_dm_repack): canonical pair blocks, rows padded to 16-column
+// chunks, column j = 16c + 4s + k stored at 16c + 4k + s and pre-scaled (x2
+// except the (a,a,0) blocks). Lane k of a DMMA A fragment then reads its four
+// K-step values as two 16-byte loads.
+template <int TM>
+__device__ __forceinline__ void gather_a(const Smem& sm, int ncov, const int (&rci)[TM], const int (&rri)[TM], int cj,
+                                         int kc, const double* __restrict__ Dr, int lane, double (&a)[TM][4]) {
+    const int stride = 16 * ((sm.cov[cj].norb + 15) >> 4);
+#pragma unroll
+    for (int t = 0; t < TM; ++t) {
+        const int ci = rci[t];
+        const int off = ci <= cj ? sm.off2d[ci * ncov + cj] : -1;  // ci = kNoCover (255) fails ci <= cj
+        if (off >= 0) {
+            const double2* p = reinterpret_cast<const double2*>(Dr + off + rri[t] * stride + 16 * kc + 4 * (lane & 3));
+            const double2 v0 = __ldg(p), v1 = __ldg(p + 1);
+            a[t][0] = v0.x;
+            a[t][1] = v0.y;
+            a[t][2] = v1.x;
+            a[t][3] = v1.y;
+        } else {
+            a[t][0] = a[t][1] = a[t][2] = a[t][3] = 0.0;
+        }
+    }
+}
+
+template <int TM, int KS>
+__device__ __forceinline__ void rho_partner(const double* __restrict__ pb, int swb, uint32_t om4,
+                                            const double (&a)[TM][4], double (&y)[TM][4][2], int colbase) {
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+        if (!((om4 >> o) & 1u)) continue;
+        const int col = colbase + 8 * o;
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+            const double bv = pb[s * 256 + (col ^ swb)];
+#pragma unroll
+            for (int t = 0; t < TM; ++t) dmma(y[t][o], a[t][s], bv);
+        }
+    }
+}
+
+template <int TM>
+__device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, const double* __restrict__ Dr,
+                              double* __restrict__ racc, int lane) {
+    const GroupS& G = sm.grp[gi];
+    const int rend = G.row0 + G.rows;
+    int rci[TM], rri[TM];
+#pragma unroll
+    for (int t = 0; t < TM; ++t) {
+        const int r = ra0 + 8 * t + (lane >> 2);
+        rci[t] = r < rend ? sm.rcov[r] : kNoCover;
+        rri[t] = sm.rorb[r];
+    }
+    double y[TM][4][2];
+#pragma unroll
+    for (int t = 0; t < TM; ++t)
+#pragma unroll
+        for (int o = 0; o < 4; ++o) y[t][o][0] = y[t][o][1] = 0.0;
+    const uint8_t* pom = sm.pom + gi * ncov;
+    uint64_t bits = sm.pbits[2 * gi + h];
+    const int colbase = 32 * h + (lane >> 2);
+    double nxt[TM][4];
+    if (bits) gather_a<TM>(sm, ncov, rci, rri, __ffsll(bits) - 1, 0, Dr, lane, nxt);
+    while (bits) {
+        const int cj = __ffsll(bits) - 1;
+        bits &= bits - 1;
+        const uint32_t om4 = (pom[cj] >> (4 * h)) & 0xFu;
+        const CoverS& B = sm.cov[cj];
+        double a[TM][4];
+#pragma unroll
+        for (int t = 0; t < TM; ++t)
+#pragma unroll
+            for (int s = 0; s < 4; ++s) a[t][s] = nxt[t][s];
+        const int nkc = (B.norb + 15) >> 4;
+        if (nkc == 1 && bits) gather_a<TM>(sm, ncov, rci, rri, __ffsll(bits) - 1, 0, Dr, lane, nxt);
+        for (int kc = 0; kc < nkc; ++kc) {
+            if (kc > 0) gather_a<TM>(sm, ncov, rci, rri, cj, kc, Dr, lane, a);
+            const int ks = min(4, (B.norb - 16 * kc + 3) >> 2);
+            const int rb = B.row0 + 16 * kc + (lane & 3);
+            const double* pb = sm.phi + rb * 64;
+            const int swb = swz(rb);
+            switch (ks) {
+                case 1: rho_partner<TM, 1>(pb, swb, om4, a, y, colbase); break;
+                case 2: rho_partner<TM, 2>(pb, swb, om4, a, y, colbase); break;
+                case 3: rho_partner<TM, 3>(pb, swb, om4, a, y, colbase); break;
+                default: rho_partner<TM, 4>(pb, swb, om4, a, y, colbase); break;
+            }
+        }
+        if (nkc > 1 && bits) gather_a<TM>(sm, ncov, rci, rri, __ffsll(bits) - 1, 0, Dr, lane, nxt);
+    }
+    // rho(slot) += sum over rows of Phi_row(slot) * Y(row, slot)
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int p = 8 * (4 * h + o) + 2 * (lane & 3) + e;
+            double v = 0.0;
+#pragma unroll
+            for (int t = 0; t < TM; ++t) {
+                const int r = ra0 + 8 * t + (lane >> 2);
+                v += sm.phi[phi_idx(r, p)] * y[t][o][e];
+            }
+            v += __shfl_xor_sync(0xffffffffu, v, 4);
+            v += __shfl_xor_sync(0xffffffffu, v, 8);
+            v += __shfl_xor_sync(0xffffffffu, v, 16);
+            if (lane < 4) racc[p] += v;
+        }
+    }
+}
+
+__device__ __forceinline__ void rho_task(const Smem& sm, int ncov, const Task& t, const double* Dr, double* racc,
+                                         int lane) {
+    const GroupS& G = sm.grp[t.g];
+    for (int i0 = 0; i0 < G.tm; i0 += 2) {
+        if (G.tm - i0 >= 2)
+            rho_task_rows<2>(sm, ncov, t.g, G.row0 + 8 * i0, t.half, Dr, racc, lane);
+        else
+            rho_task_rows<1>(sm, ncov, t.g, G.row0 + 8 * i0, t.half, Dr, racc, lane);
+    }
+}
+
+}  // namespace core
+}  // namespace kbg

@@ -228,6 +228,16 @@ __global__ void k_pair_meta(SysParams P, int64_t npair, const int32_t* pa, const
     key[p] = pair_key(pa[p], pb[p], pR[3 * p], pR[3 * p + 1], pR[3 * p + 2], P.natom);
 }
 
+__global__ void k_pair_rsize(SysParams P, int64_t npair, const int32_t* pa, const int32_t* pb, const int32_t* pR,
+                             int64_t* size) {
+    const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (p >= npair) return;
+    const int a = pa[p], b = pb[p];
+    if (!canonical_dev(a, b, pR[3 * p], pR[3 * p + 1], pR[3 * p + 2])) return;
+    const int nb = P.sp[P.spc[b]].norb;
+    size[p] = static_cast<int64_t>(P.sp[P.spc[a]].norb) * 16 * ((nb + 15) >> 4);
+}
+
 __global__ void k_pair_mirror(SysParams P, int64_t npair, const int32_t* pa, const int32_t* pb, const int32_t* pR,
                               const int64_t* key, int32_t* mirror, int* err) {
     const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -302,7 +312,8 @@ __global__ void k_bp_count(SysParams P, int64_t nblock, const int32_t* __restric
 __global__ void k_bp_fill(SysParams P, int64_t nblock, const int32_t* __restrict__ blk_ptr,
                           const int32_t* __restrict__ cov_atom, const int32_t* __restrict__ cov_R,
                           const uint64_t* __restrict__ cov_mask, const int64_t* __restrict__ bp_ptr,
-                          const int64_t* __restrict__ pkey, const int64_t* __restrict__ poff, int64_t npair, BPair* bp,
+                          const int64_t* __restrict__ pkey, const int64_t* __restrict__ poff,
+                          const int64_t* __restrict__ proff, int64_t npair, BPair* bp,
                           int* err) {
     const int lane = threadIdx.x & 31;
     const int64_t b = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
@@ -325,32 +336,13 @@ __global__ void k_bp_fill(SysParams P, int64_t nblock, const int32_t* __restrict
                 const int64_t p = find_pair(pkey, npair, key);
                 BPair e;
                 e.cicj = (ci - c0) | ((cj - c0) << 16);
-                e.cost = na * P.sp[P.spc[aj]].norb * __popcll(both);
+                e.roff = p >= 0 ? static_cast<int32_t>(proff[p]) : 0;
                 e.off = p >= 0 ? poff[p] : 0;
                 if (p < 0) atomicCAS(err, 0, static_cast<int>(b) + 1);
                 bp[pos + __popc(bal & ((1u << lane) - 1u))] = e;
             }
             pos += __popc(bal);
         }
-    }
-}
-
-// Orders each block's work items by cost, descending (ties: original order),
-// so the static round-robin warp assignment approximates LPT scheduling.
-__global__ void k_bp_sort(int64_t nblock, const int64_t* __restrict__ bp_ptr, const BPair* __restrict__ in,
-                          BPair* __restrict__ out) {
-    const int lane = threadIdx.x & 31;
-    const int64_t b = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
-    if (b >= nblock) return;
-    const int64_t p0 = bp_ptr[b], n = bp_ptr[b + 1] - p0;
-    for (int64_t i = lane; i < n; i += 32) {
-        const BPair e = in[p0 + i];
-        int64_t rank = 0;
-        for (int64_t j = 0; j < n; ++j) {
-            const int cj = in[p0 + j].cost;
-            rank += (cj > e.cost) || (cj == e.cost && j < i);
-        }
-        out[p0 + rank] = e;
     }
 }
 
@@ -367,6 +359,8 @@ void free_index(DevIndex& ix) {
     dfree(ix.pair_R);
     dfree(ix.pair_off);
     dfree(ix.pair_key);
+    dfree(ix.pair_roff);
+    dfree(ix.order);
     dfree(ix.pair_mirror);
     dfree(ix.bp_ptr);
     dfree(ix.bp);
@@ -475,6 +469,13 @@ void build_index_device(const SysParams& P, DevIndex& ix, cudaStream_t st) {
     }
     KBG_CUDA(cudaGetLastError());
     ix.nnz = exclusive_scan(psize, ix.pair_off, ix.npair, st);
+    // repacked-DM sizes: canonical pairs only, rows padded to 16-column chunks
+    KBG_CUDA(cudaMemsetAsync(psize, 0, (ix.npair + 1) * sizeof(int64_t), st));
+    if (ix.npair) k_pair_rsize<<<grid_of(ix.npair, T), T, 0, st>>>(P, ix.npair, ix.pair_a, ix.pair_b, ix.pair_R, psize);
+    KBG_CUDA(cudaGetLastError());
+    ix.pair_roff = dalloc<int64_t>(ix.npair + 1);
+    ix.nrep = exclusive_scan(psize, ix.pair_roff, ix.npair, st);
+    if (ix.nrep >= (int64_t(1) << 31)) throw Error(KBG_ERR_DIMENSION, "build_index: repacked density matrix too large");
     cudaFree(psize);
     int herr = 0;
     KBG_CUDA(cudaMemcpy(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost));
@@ -496,11 +497,8 @@ void build_index_device(const SysParams& P, DevIndex& ix, cudaStream_t st) {
     ix.nbpair = exclusive_scan(bpc, ix.bp_ptr, nblock, st);
     cudaFree(bpc);
     ix.bp = dalloc<BPair>(ix.nbpair);
-    BPair* bp_unsorted = dalloc<BPair>(ix.nbpair);
     k_bp_fill<<<wgrid, T, 0, st>>>(P, nblock, ix.blk_ptr, ix.cov_atom, ix.cov_R, ix.cov_mask, ix.bp_ptr, ix.pair_key,
-                                   ix.pair_off, ix.npair, bp_unsorted, d_err);
-    KBG_CUDA(cudaGetLastError());
-    k_bp_sort<<<wgrid, T, 0, st>>>(nblock, ix.bp_ptr, bp_unsorted, ix.bp);
+                                   ix.pair_off, ix.pair_roff, ix.npair, ix.bp, d_err);
     KBG_CUDA(cudaGetLastError());
     Stats hs;
     KBG_CUDA(cudaMemcpyAsync(&hs, d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, st));
@@ -508,7 +506,6 @@ void build_index_device(const SysParams& P, DevIndex& ix, cudaStream_t st) {
     KBG_CUDA(cudaStreamSynchronize(st));
     cudaFree(d_stats);
     cudaFree(d_err);
-    cudaFree(bp_unsorted);
     if (herr)
         throw Error(KBG_ERR_CONSISTENCY, "build_index: block " + std::to_string(herr - 1) +
                                              " has covers that share points but form no pair");

@@ -15,7 +15,7 @@ namespace kbg {
 constexpr int kMaxSpecies = 8;
 constexpr int kMaxRad = 16;
 constexpr int kGroupRows = 16;  // covers are packed into row groups of <= 16 orbitals (2 DMMA row tiles)
-constexpr int kTaskWarps = 8;   // task lists are LPT-balanced over 8 warps (4-warp CTAs merge pairs)
+constexpr int kMaxTaskWarps = 16;  // task lists are LPT-balanced over <= 16 consumer warps
 constexpr int kMaxCoverPerBlock = 64;
 
 // Error taxonomy of kband (common.hpp:21-38) carried as a status code.
@@ -61,8 +61,8 @@ struct SysParams {
 // value offset of the pair block (a_ci, a_cj, R_cj - R_ci).
 struct BPair {
     int32_t cicj;  // ci | (cj << 16)
-    int32_t cost;  // n_a * n_b * |mask_ci & mask_cj|
-    int64_t off;
+    int32_t roff;  // offset of the pair in the repacked density matrix (see kb_grid.cu: k_dm_repack)
+    int64_t off;   // value offset of the pair block (a_ci, a_cj, R_cj - R_ci)
 };
 
 // One warp task of a grid block. H: rows of group g x columns of cover cj over
@@ -96,6 +96,8 @@ struct DevIndex {
     int32_t* pair_R = nullptr;
     int64_t* pair_off = nullptr;
     int64_t* pair_key = nullptr;
+    int64_t* pair_roff = nullptr;  // [npair+1] repacked-DM offsets (canonical pairs only)
+    int64_t nrep = 0;              // repacked DM doubles per spin
     int32_t* pair_mirror = nullptr;
     int64_t* bp_ptr = nullptr;
     BPair* bp = nullptr;
@@ -111,6 +113,9 @@ struct DevIndex {
     int64_t nhtask = 0, nrtask = 0;
     int max_rows_padded = 0;  // max Phi rows of a block (groups padded to 8-row tiles)
     int max_htask = 0, max_rtask = 0;
+    int task_warps = 0;         // warps the task lists are LPT-balanced over
+    int64_t* order = nullptr;   // owned blocks, heaviest first (persistent scheduling)
+    int64_t norder = 0;
     int max_phi = 0;     // (unused)
     int max_cover = 0;   // max covers per block
     int max_bpairs = 0;  // max work items per block
@@ -137,6 +142,12 @@ struct GridArgs {
     const int64_t* t_ptr;   // task lists of this kernel (H or rho)
     const Task* tasks;
     const int32_t* t_wptr;
+    int task_warps;
+    const double* dmr;      // density: repacked DM [nspin][nrep]
+    int64_t nrep;
+    const int64_t* order;   // persistent kernels: block order
+    int64_t norder;
+    int* counter;           // persistent kernels: work counter (zeroed per launch)
     int64_t blk_begin;  // first owned block
     int max_rows;       // Phi rows allocated (padded groups + 8 pad rows)
     int max_cover;
@@ -160,10 +171,21 @@ void copy_index_to_host(const DevIndex& ix, HostIndex& h, cudaStream_t st);
 // Grid kernels (kb_grid.cu). Return number of kernel launches.
 size_t grid_smem_bytes(const GridArgs& g, int nwarps, bool density);
 // Task lists (kb_tasks.cu), built after the index.
-void build_tasks_device(const SysParams& sys, DevIndex& ix, cudaStream_t st);
+void build_tasks_device(const SysParams& sys, DevIndex& ix, int task_warps, cudaStream_t st);
 void free_tasks(DevIndex& ix);
 int launch_density(const GridArgs& g, int64_t nblk_owned, int nwarps, cudaStream_t st);
 int launch_hamiltonian(const GridArgs& g, int64_t nblk_owned, int nwarps, cudaStream_t st);
+int launch_dm_repack(const DevIndex& ix, const SysParams& sys, int nspin, const double* dm, double* dmr,
+                     cudaStream_t st);
+// Persistent warp-specialized kernels (kb_persist.cu): kPersistProducers
+// producer warps stage block k+1 while kPersistConsumers consumer warps work
+// on block k (two shared-memory buffers). persist_fits() says whether two
+// buffers fit in shared memory for this index.
+constexpr int kPersistProducers = 4;
+constexpr int kPersistConsumers = 12;
+bool persist_fits(const GridArgs& g, bool density);
+int launch_density_persist(const GridArgs& g, cudaStream_t st);
+int launch_hamiltonian_persist(const GridArgs& g, cudaStream_t st);
 int launch_mirror(const DevIndex& ix, const SysParams& sys, int nspin, double* h, cudaStream_t st);
 int launch_dm_check(const DevIndex& ix, const SysParams& sys, int nspin, const double* dm,
                     unsigned long long* d_maxdiff_maxabs, cudaStream_t st);

@@ -1,0 +1,210 @@
+// Persistent, warp-specialized grid kernels (one CTA per SM, 16 warps).
+//
+// Warps 0..3 (producers) pull grid blocks from a global work counter (blocks
+// ordered heaviest first) and stage them -- covers, tables, task list, Phi --
+// into one of two shared-memory buffers, then arrive on the buffer's `full`
+// mbarrier. Warps 4..15 (consumers) wait on `full`, run their LPT-assigned
+// tasks (DMMA contractions, kb_gridcore.cuh) and leave for the next buffer
+// without a CTA-wide barrier; the last consumer to finish a block (SMEM
+// counter) reduces the per-warp rho accumulators in a fixed order, writes rho
+// and arrives on the buffer's `empty` mbarrier, which the producers wait on
+// before reusing it. Staging of block k+1 thus overlaps the DMMA work of
+// block k, and a slow warp only delays its own buffer.
+#include "kb_gridcore.cuh"
+
+namespace kbg {
+
+namespace {
+
+using namespace core;
+
+constexpr int NP = kPersistProducers;
+constexpr int NC = kPersistConsumers;
+constexpr int NT = (NP + NC) * 32;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile(
+        "{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        " .reg .pred p;\n"
+        " WAIT:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT;\n"
+        "}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void producer_sync() { asm volatile("bar.sync 1, %0;" ::"r"(NP * 32) : "memory"); }
+
+struct Buffers {
+    Smem buf[2];
+    uint64_t* full;   // [2]
+    uint64_t* empty;  // [2]
+    int* next;        // producer broadcast slot
+};
+
+__device__ __forceinline__ Buffers carve_all(unsigned char* base, const GridArgs& g, size_t acc) {
+    size_t off[12];
+    const size_t bsz = align16(buffer_layout(g, acc, off));
+    Buffers B;
+    B.buf[0] = carve(base, g, acc);
+    B.buf[1] = carve(base + bsz, g, acc);
+    B.full = reinterpret_cast<uint64_t*>(base + 2 * bsz);
+    B.empty = B.full + 2;
+    B.next = reinterpret_cast<int*>(B.empty + 2);
+    return B;
+}
+
+__host__ __device__ inline size_t persist_bytes(const GridArgs& g, bool density) {
+    size_t off[12];
+    const size_t acc = static_cast<size_t>(g.nspin) * 64 * (density ? NC : 1);
+    return 2 * align16(buffer_layout(g, acc, off)) + 64;
+}
+
+// Producer loop (threads 0..NP*32-1). Returns when the work is exhausted.
+template <bool DENSITY>
+__device__ void producer(const GridArgs& g, const Buffers& B, int ptid) {
+    for (int k = 0;; ++k) {
+        const int s = k & 1;
+        if (k >= 2) mbar_wait(&B.empty[s], ((k >> 1) - 1) & 1);
+        const Smem& sm = B.buf[s];
+        int64_t b = -1;
+        for (;;) {
+            if (ptid == 0) *B.next = atomicAdd(g.counter, 1);
+            producer_sync();
+            const int idx = *B.next;
+            producer_sync();
+            if (idx >= g.norder) {
+                b = -1;
+                break;
+            }
+            b = g.order[idx];
+            const int ncov = stage_block(g, b, sm, ptid, NP * 32, [] { producer_sync(); }, DENSITY, NC);
+            if (ncov > 0) break;
+            if (DENSITY && ptid < 64) {  // empty block: rho = 0 on its points
+                int bi, bj, bk;
+                block_decode(g.sys, b, bi, bj, bk);
+                bool valid;
+                const int64_t pt = slot_point(g.sys, bi, bj, bk, ptid, valid);
+                if (valid)
+                    for (int spin = 0; spin < g.nspin; ++spin) g.out[spin * g.npts + pt] = 0.0;
+            }
+        }
+        if (b < 0 && ptid == 0) sm.meta->block = -1;
+        mbar_arrive(&B.full[s]);
+        if (b < 0) return;
+    }
+}
+
+template <bool DENSITY>
+__device__ void consumer(const GridArgs& g, const Buffers& B, int cw, int lane) {
+    for (int k = 0;; ++k) {
+        const int s = k & 1;
+        mbar_wait(&B.full[s], (k >> 1) & 1);
+        const Smem& sm = B.buf[s];
+        const int64_t b = sm.meta->block;
+        if (b < 0) return;
+        const int ncov = sm.meta->ncov;
+        for (int spin = 0; spin < g.nspin; ++spin) {
+            if (DENSITY) {
+                const double* Dr = g.dmr + spin * g.nrep;
+                double* racc = sm.acc + (spin * NC + cw) * 64;
+                for (int w = cw; w < g.task_warps; w += NC)
+                    for (int e = sm.wptr[w]; e < sm.wptr[w + 1]; ++e) rho_task(sm, ncov, sm.task[e], Dr, racc, lane);
+            } else {
+                double* Hs = g.out + spin * g.nnz;
+                for (int w = cw; w < g.task_warps; w += NC)
+                    for (int e = sm.wptr[w]; e < sm.wptr[w + 1]; ++e)
+                        h_task(sm, sm.acc + spin * 64, ncov, sm.task[e], Hs, g.sign, g.scatter, lane);
+            }
+        }
+        __syncwarp();
+        int last = 0;
+        if (lane == 0) {
+            __threadfence_block();
+            last = atomicAdd(&sm.meta->done, 1) == NC - 1;
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {
+            __threadfence_block();
+            if (DENSITY) {
+                int bi, bj, bk;
+                block_decode(g.sys, b, bi, bj, bk);
+                for (int i = lane; i < g.nspin * 64; i += 32) {
+                    const int spin = i >> 6, p = i & 63;
+                    double r = 0.0;
+#pragma unroll
+                    for (int w = 0; w < NC; ++w) r += sm.acc[(spin * NC + w) * 64 + p];
+                    bool valid;
+                    const int64_t pt = slot_point(g.sys, bi, bj, bk, p, valid);
+                    if (valid) g.out[spin * g.npts + pt] = r;
+                }
+                __syncwarp();
+            }
+            if (lane == 0) mbar_arrive(&B.empty[s]);
+        }
+    }
+}
+
+template <bool DENSITY>
+__global__ void __launch_bounds__(NT, 1) k_persist(GridArgs g) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const size_t acc = static_cast<size_t>(g.nspin) * 64 * (DENSITY ? NC : 1);
+    const Buffers B = carve_all(smem_raw, g, acc);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&B.full[s], NP * 32);
+            mbar_init(&B.empty[s], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp < NP)
+        producer<DENSITY>(g, B, tid);
+    else
+        consumer<DENSITY>(g, B, warp - NP, lane);
+}
+
+template <class K>
+void set_smem(K kernel, size_t bytes) {
+    KBG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+}
+
+int launch_persist(const GridArgs& g, bool density, cudaStream_t st) {
+    if (g.norder <= 0) return 0;
+    int dev = 0, sms = 0;
+    KBG_CUDA(cudaGetDevice(&dev));
+    KBG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(sms, g.norder));
+    const size_t smem = persist_bytes(g, density);
+    KBG_CUDA(cudaMemsetAsync(g.counter, 0, sizeof(int), st));
+    if (density) {
+        set_smem(k_persist<true>, smem);
+        k_persist<true><<<grid, NT, smem, st>>>(g);
+    } else {
+        set_smem(k_persist<false>, smem);
+        k_persist<false><<<grid, NT, smem, st>>>(g);
+    }
+    KBG_CUDA(cudaGetLastError());
+    return 1;
+}
+
+}  // namespace
+
+bool persist_fits(const GridArgs& g, bool density) { return persist_bytes(g, density) <= 227 * 1024; }
+
+int launch_density_persist(const GridArgs& g, cudaStream_t st) { return launch_persist(g, true, st); }
+int launch_hamiltonian_persist(const GridArgs& g, cudaStream_t st) { return launch_persist(g, false, st); }
+
+}  // namespace kbg

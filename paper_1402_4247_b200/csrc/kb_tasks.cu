@@ -1,7 +1,7 @@
 // Per-block warp task lists for the grid kernels (built once per geometry,
 // after the index). One thread per block: row groups (make_groups), the H
 // tasks (group x partner cover, common quads) and the rho tasks (group x
-// octet half), then an LPT assignment of the tasks to kTaskWarps warps so the
+// octet half), then an LPT assignment of the tasks to `task_warps` warps so the
 // static per-warp schedule inside a CTA is balanced and deterministic.
 #include <cub/cub.cuh>
 
@@ -107,8 +107,10 @@ __global__ void k_tasks(SysParams P, int64_t nblock, const int32_t* __restrict__
 }
 
 // Sort one block's tasks by cost (descending, stable), assign each to the
-// least-loaded of kTaskWarps warps (LPT), emit warp-major into `out`.
-__global__ void k_tasks_lpt(int64_t nblock, const int64_t* __restrict__ ptr, Task* tmp, Task* out, int32_t* wptr) {
+// least-loaded of W warps (LPT), emit warp-major into `out`; wptr has a stride
+// of kMaxTaskWarps + 1 per block.
+__global__ void k_tasks_lpt(int64_t nblock, int W, const int64_t* __restrict__ ptr, Task* tmp, Task* out,
+                            int32_t* wptr) {
     const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (b >= nblock) return;
     const int64_t p0 = ptr[b];
@@ -123,25 +125,26 @@ __global__ void k_tasks_lpt(int64_t nblock, const int64_t* __restrict__ ptr, Tas
         }
         t[j + 1] = x;
     }
-    int64_t load[kTaskWarps];
-    int cnt[kTaskWarps];
-    for (int w = 0; w < kTaskWarps; ++w) load[w] = cnt[w] = 0;
+    int64_t load[kMaxTaskWarps];
+    int cnt[kMaxTaskWarps];
+    for (int w = 0; w < W; ++w) load[w] = cnt[w] = 0;
     for (int i = 0; i < n; ++i) {
         int best = 0;
-        for (int w = 1; w < kTaskWarps; ++w)
+        for (int w = 1; w < W; ++w)
             if (load[w] < load[best]) best = w;
         load[best] += t[i].cost;
         t[i].pad_ = static_cast<uint8_t>(best);
         ++cnt[best];
     }
-    int pos[kTaskWarps];
+    int pos[kMaxTaskWarps];
     int acc = 0;
-    for (int w = 0; w < kTaskWarps; ++w) {
-        wptr[b * (kTaskWarps + 1) + w] = acc;
+    int32_t* wp = wptr + b * (kMaxTaskWarps + 1);
+    for (int w = 0; w < W; ++w) {
+        wp[w] = acc;
         pos[w] = acc;
         acc += cnt[w];
     }
-    wptr[b * (kTaskWarps + 1) + kTaskWarps] = acc;
+    for (int w = W; w <= kMaxTaskWarps; ++w) wp[w] = acc;
     for (int i = 0; i < n; ++i) out[p0 + pos[t[i].pad_]++] = t[i];
 }
 
@@ -156,8 +159,9 @@ void free_tasks(DevIndex& ix) {
     ix.ht_wptr = ix.rt_wptr = nullptr;
 }
 
-void build_tasks_device(const SysParams& P, DevIndex& ix, cudaStream_t st) {
+void build_tasks_device(const SysParams& P, DevIndex& ix, int task_warps, cudaStream_t st) {
     free_tasks(ix);
+    ix.task_warps = task_warps;
     const int64_t nb = ix.nblock;
     const int T = 128;
     const unsigned grid = static_cast<unsigned>((nb + T - 1) / T);
@@ -181,10 +185,10 @@ void build_tasks_device(const SysParams& P, DevIndex& ix, cudaStream_t st) {
     KBG_CUDA(cudaGetLastError());
     ix.ht = talloc<Task>(ix.nhtask);
     ix.rt = talloc<Task>(ix.nrtask);
-    ix.ht_wptr = talloc<int32_t>(nb * (kTaskWarps + 1));
-    ix.rt_wptr = talloc<int32_t>(nb * (kTaskWarps + 1));
-    k_tasks_lpt<<<grid, T, 0, st>>>(nb, ix.ht_ptr, htmp, ix.ht, ix.ht_wptr);
-    k_tasks_lpt<<<grid, T, 0, st>>>(nb, ix.rt_ptr, rtmp, ix.rt, ix.rt_wptr);
+    ix.ht_wptr = talloc<int32_t>(nb * (kMaxTaskWarps + 1));
+    ix.rt_wptr = talloc<int32_t>(nb * (kMaxTaskWarps + 1));
+    k_tasks_lpt<<<grid, T, 0, st>>>(nb, task_warps, ix.ht_ptr, htmp, ix.ht, ix.ht_wptr);
+    k_tasks_lpt<<<grid, T, 0, st>>>(nb, task_warps, ix.rt_ptr, rtmp, ix.rt, ix.rt_wptr);
     KBG_CUDA(cudaGetLastError());
     TaskStats hs;
     KBG_CUDA(cudaMemcpyAsync(&hs, d_st, sizeof(hs), cudaMemcpyDeviceToHost, st));

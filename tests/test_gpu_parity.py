@@ -139,3 +139,17 @@ def test_errors():
     bad[0, 0] += 1.0  # breaks DM_ba(-R) = DM_ab(R)^T
     with pytest.raises(ConsistencyError):
         c.gp.density(bad)
+
+
+@pytest.mark.parametrize("persist", [0, 1])
+def test_kernel_modes_agree(persist):
+    """Persistent warp-specialized kernels and one-CTA-per-block kernels give the same results."""
+    c = case("cubic56_200Ry")
+    c.gp.set_option(_abi.KBG_OPT_PERSIST, persist)
+    try:
+        rho = c.gp.density(c.dm)
+        h = c.gp.hamiltonian(c.veff, c.f.dV)
+    finally:
+        c.gp.set_option(_abi.KBG_OPT_PERSIST, 1)
+    assert normwise(rho, c.o.density(c.dm)) <= TOL
+    assert normwise(h, c.o.hamiltonian(c.veff, c.f.dV)) <= TOL

@@ -53,19 +53,22 @@ def main():
 
     f_rho = a.nspin * (2 * ix["sum_m2"] + 2 * ix["sum_m"])
     f_h = a.nspin * 2 * ix["sum_m2"]
-    for warps in (8, 4):
+    for warps, persist in ((8, 1), (8, 0)):
         gp.set_option(_abi.KBG_OPT_WARPS, warps)
+        gp.set_option(_abi.KBG_OPT_PERSIST, persist)
         for name, fn, fl in (
             ("density", lambda: gp.density_dev(d_dm, rho, st), f_rho),
             ("h_accumulate", lambda: gp.hamiltonian_accumulate_dev(d_v, f.dV, h, st), f_h),
         ):
             med, mn = timeit(fn)
-            print(json.dumps({"config": a.config, "kernel": name, "warps": warps, "median_ms": round(med, 4),
+            print(json.dumps({"config": a.config, "kernel": name, "warps": warps, "persist": persist,
+                              "median_ms": round(med, 4),
                               "min_ms": round(mn, 4), "alg_tflops": round(fl / (med * 1e-3) / 1e12, 3)}))
         gp.set_option(_abi.KBG_OPT_SCATTER_STORE, 1)
         med, mn = timeit(lambda: gp.hamiltonian_accumulate_dev(d_v, f.dV, h, st))
         gp.set_option(_abi.KBG_OPT_SCATTER_STORE, 0)
         print(json.dumps({"config": a.config, "kernel": "h_accumulate_store_scatter(experiment)", "warps": warps,
+                          "persist": persist,
                           "median_ms": round(med, 4), "min_ms": round(mn, 4)}))
 
 
