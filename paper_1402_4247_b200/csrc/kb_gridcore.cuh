@@ -174,7 +174,7 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int tid
     block_decode(P, b, bi, bj, bk);
     if (density) {
         for (int i = tid; i < g.nspin * acc_warps * 64; i += nt) sm.acc[i] = 0.0;
-    } else {
+    } else if (g.in) {
         for (int i = tid; i < g.nspin * 64; i += nt) {
             bool valid;
             const int64_t pt = slot_point(P, bi, bj, bk, i & 63, valid);
