@@ -181,7 +181,11 @@ kbg::GridArgs grid_args(kbg_ctx* c, int nspin, double dV, const double* in, doub
     g.t_ptr = density ? c->ix.rt_ptr : c->ix.ht_ptr;
     g.tasks = density ? c->ix.rt : c->ix.ht;
     g.t_wptr = density ? c->ix.rt_wptr : c->ix.ht_wptr;
-    g.max_tasks = std::max(1, density ? c->ix.max_rtask : c->ix.max_htask);
+    g.max_tasks = std::max(1, std::max(c->ix.max_rtask, c->ix.max_htask));
+    g.tabs = density ? c->ix.rtab : c->ix.htab;
+    g.tab_bytes = c->ix.tab_bytes;
+    g.phis = c->ix.phis;
+    g.phi_off = c->ix.phi_off;
     g.nspin = nspin;
     g.nnz = c->ix.nnz;
     g.npts = c->npts;
@@ -204,7 +208,7 @@ int run_density(kbg_ctx* c, int nspin, const double* d_dm, double* d_rho, cudaSt
     int n = kbg::launch_dm_repack(c->ix, c->P, nspin, d_dm, c->d_dmr, st);
     kbg::GridArgs g = grid_args(c, nspin, 0.0, d_dm, d_rho, true);
     g.dmr = c->d_dmr;
-    if (c->persist_ok && c->persist)
+    if (c->persist_ok && c->persist && c->ix.phis)
         n += kbg::launch_density_persist(g, st);
     else
         n += kbg::launch_density(g, c->blk_end - c->blk_begin, c->nwarps, st);
@@ -213,7 +217,7 @@ int run_density(kbg_ctx* c, int nspin, const double* d_dm, double* d_rho, cudaSt
 
 int run_hamiltonian(kbg_ctx* c, int nspin, double dV, const double* d_veff, double* d_h, cudaStream_t st) {
     const kbg::GridArgs g = grid_args(c, nspin, dV, d_veff, d_h, false);
-    if (c->persist_ok && c->persist) return kbg::launch_hamiltonian_persist(g, st);
+    if (c->persist_ok && c->persist && c->ix.phis) return kbg::launch_hamiltonian_persist(g, st);
     return kbg::launch_hamiltonian(g, c->blk_end - c->blk_begin, c->nwarps, st);
 }
 
@@ -319,6 +323,10 @@ int kbg_build_index(kbg_ctx* c) {
         if (!order.empty())
             KBG_CUDA(cudaMemcpy(c->ix.order, order.data(), order.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
         if (!c->d_counter) KBG_CUDA(cudaMalloc(&c->d_counter, sizeof(int)));
+        if (c->persist_ok) {
+            kbg::build_cache_device(grid_args(c, 1, 0.0, nullptr, nullptr, false),
+                                    grid_args(c, 1, 0.0, nullptr, nullptr, true), c->ix, c->stream);
+        }
     });
 }
 

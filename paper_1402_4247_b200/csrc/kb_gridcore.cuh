@@ -77,34 +77,48 @@ struct Smem {
 
 __host__ __device__ __forceinline__ size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
 
-// Byte size of one buffer; off[] receives the section offsets.
-__host__ __device__ inline size_t buffer_layout(const GridArgs& g, size_t acc_doubles, size_t* off) {
+// Buffer layout: [tables | acc | Phi]. The tables section has a fixed size
+// (table_bytes) and is exactly what the geometry cache stores per block and
+// the persistent kernels' producer bulk-copies back (kb_cache.cu).
+__host__ __device__ inline size_t tables_layout(const GridArgs& g, size_t* off) {
     size_t o = 0;
     const size_t mc = static_cast<size_t>(g.max_cover);
-    off[0] = o;
-    o += align16(static_cast<size_t>(g.max_rows) * 64 * sizeof(double));
-    off[1] = o;
-    o += align16(acc_doubles * sizeof(double));
-    off[2] = o;
-    o += align16(mc * sizeof(CoverS));
-    off[3] = o;
-    o += align16(mc * sizeof(GroupS));
-    off[4] = o;
-    o += align16(mc * mc * sizeof(int32_t));
-    off[5] = o;
-    o += align16(static_cast<size_t>(g.max_rows));
-    off[6] = o;
-    o += align16(static_cast<size_t>(g.max_rows));
-    off[7] = o;
-    o += align16(mc * mc);
-    off[8] = o;
-    o += align16(mc * 2 * sizeof(uint64_t));
-    off[9] = o;
-    o += align16(static_cast<size_t>(g.max_tasks) * sizeof(Task));
-    off[10] = o;
-    o += align16((kMaxTaskWarps + 1) * sizeof(int32_t));
-    off[11] = o;
+    off[0] = o;  // meta
     o += align16(sizeof(Meta));
+    off[1] = o;  // covers
+    o += align16(mc * sizeof(CoverS));
+    off[2] = o;  // groups
+    o += align16(mc * sizeof(GroupS));
+    off[3] = o;  // off2d
+    o += align16(mc * mc * sizeof(int32_t));
+    off[4] = o;  // rcov
+    o += align16(static_cast<size_t>(g.max_rows));
+    off[5] = o;  // rorb
+    o += align16(static_cast<size_t>(g.max_rows));
+    off[6] = o;  // pom
+    o += align16(mc * mc);
+    off[7] = o;  // pbits
+    o += align16(mc * 2 * sizeof(uint64_t));
+    off[8] = o;  // tasks
+    o += align16(static_cast<size_t>(g.max_tasks) * sizeof(Task));
+    off[9] = o;  // wptr
+    o += align16((kMaxTaskWarps + 1) * sizeof(int32_t));
+    return o;
+}
+
+__host__ __device__ inline size_t table_bytes(const GridArgs& g) {
+    size_t off[10];
+    return tables_layout(g, off);
+}
+
+// Byte size of one buffer; off[] receives the section offsets (off[10] = acc,
+// off[11] = Phi).
+__host__ __device__ inline size_t buffer_layout(const GridArgs& g, size_t acc_doubles, size_t* off) {
+    size_t o = tables_layout(g, off);
+    off[10] = o;
+    o += align16(acc_doubles * sizeof(double));
+    off[11] = o;
+    o += align16(static_cast<size_t>(g.max_rows) * 64 * sizeof(double));
     return o;
 }
 
@@ -112,18 +126,18 @@ __device__ __forceinline__ Smem carve(unsigned char* base, const GridArgs& g, si
     size_t off[12];
     buffer_layout(g, acc_doubles, off);
     Smem s;
-    s.phi = reinterpret_cast<double*>(base + off[0]);
-    s.acc = reinterpret_cast<double*>(base + off[1]);
-    s.cov = reinterpret_cast<CoverS*>(base + off[2]);
-    s.grp = reinterpret_cast<GroupS*>(base + off[3]);
-    s.off2d = reinterpret_cast<int32_t*>(base + off[4]);
-    s.rcov = base + off[5];
-    s.rorb = base + off[6];
-    s.pom = base + off[7];
-    s.pbits = reinterpret_cast<uint64_t*>(base + off[8]);
-    s.task = reinterpret_cast<Task*>(base + off[9]);
-    s.wptr = reinterpret_cast<int32_t*>(base + off[10]);
-    s.meta = reinterpret_cast<Meta*>(base + off[11]);
+    s.meta = reinterpret_cast<Meta*>(base + off[0]);
+    s.cov = reinterpret_cast<CoverS*>(base + off[1]);
+    s.grp = reinterpret_cast<GroupS*>(base + off[2]);
+    s.off2d = reinterpret_cast<int32_t*>(base + off[3]);
+    s.rcov = base + off[4];
+    s.rorb = base + off[5];
+    s.pom = base + off[6];
+    s.pbits = reinterpret_cast<uint64_t*>(base + off[7]);
+    s.task = reinterpret_cast<Task*>(base + off[8]);
+    s.wptr = reinterpret_cast<int32_t*>(base + off[9]);
+    s.acc = reinterpret_cast<double*>(base + off[10]);
+    s.phi = reinterpret_cast<double*>(base + off[11]);
     return s;
 }
 
@@ -141,7 +155,7 @@ __device__ __forceinline__ int64_t slot_point(const SysParams& P, int bi, int bj
 // per-warp accumulators. Returns ncov (0: nothing to compute).
 template <class Sync>
 __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int tid, int nt, Sync&& sync, bool density,
-                           int acc_warps) {
+                           int acc_warps, bool eval_phi = true) {
     const int c0 = g.blk_ptr[b];
     const int ncov = g.blk_ptr[b + 1] - c0;
     if (tid == 0) {
@@ -218,8 +232,9 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int tid
             sm.rorb[cv.row0 + o] = static_cast<uint8_t>(o);
         }
     }
-    for (int i = tid; i < 8 * 64; i += nt) sm.phi[rows * 64 + i] = 0.0;  // tail rows (tile overrun)
-    for (int task = tid; task < ncov * 64; task += nt) {
+    if (eval_phi)
+        for (int i = tid; i < 8 * 64; i += nt) sm.phi[rows * 64 + i] = 0.0;  // tail rows (tile overrun)
+    for (int task = tid; eval_phi && task < ncov * 64; task += nt) {
         const int c = task >> 6, s = task & 63;
         const CoverS& cv = sm.cov[c];
         double* dst = sm.phi;

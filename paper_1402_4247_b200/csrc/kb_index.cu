@@ -349,6 +349,7 @@ __global__ void k_bp_fill(SysParams P, int64_t nblock, const int32_t* __restrict
 }  // namespace
 
 void free_index(DevIndex& ix) {
+    free_cache(ix);
     free_tasks(ix);
     dfree(ix.blk_ptr);
     dfree(ix.cov_atom);

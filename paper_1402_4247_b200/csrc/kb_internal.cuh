@@ -114,6 +114,15 @@ struct DevIndex {
     int max_rows_padded = 0;  // max Phi rows of a block (groups padded to 8-row tiles)
     int max_htask = 0, max_rtask = 0;
     int task_warps = 0;         // warps the task lists are LPT-balanced over
+    int32_t* blk_rows = nullptr;  // Phi rows of each block (without the 8 tail rows)
+    // geometry cache (kb_cache.cu): per block the H / rho table images
+    // (table_bytes each) and Phi ((rows + 8) x 64 doubles at phi_off[b])
+    unsigned char* htab = nullptr;
+    unsigned char* rtab = nullptr;
+    double* phis = nullptr;
+    int64_t* phi_off = nullptr;
+    int64_t tab_bytes = 0;
+    int64_t phi_doubles = 0;
     int64_t* order = nullptr;   // owned blocks, heaviest first (persistent scheduling)
     int64_t norder = 0;
     int max_phi = 0;     // (unused)
@@ -148,6 +157,10 @@ struct GridArgs {
     const int64_t* order;   // persistent kernels: block order
     int64_t norder;
     int* counter;           // persistent kernels: work counter (zeroed per launch)
+    const unsigned char* tabs;  // geometry cache: this kernel's table images
+    int64_t tab_bytes;
+    const double* phis;
+    const int64_t* phi_off;
     int64_t blk_begin;  // first owned block
     int max_rows;       // Phi rows allocated (padded groups + 8 pad rows)
     int max_cover;
@@ -181,8 +194,12 @@ int launch_dm_repack(const DevIndex& ix, const SysParams& sys, int nspin, const 
 // producer warps stage block k+1 while kPersistConsumers consumer warps work
 // on block k (two shared-memory buffers). persist_fits() says whether two
 // buffers fit in shared memory for this index.
-constexpr int kPersistProducers = 4;
-constexpr int kPersistConsumers = 12;
+constexpr int kPersistProducers = 1;
+constexpr int kPersistConsumers = 15;
+// Geometry cache (kb_cache.cu): Phi and the per-block tables, built once per
+// geometry after the task lists.
+void build_cache_device(GridArgs gh, GridArgs gr, DevIndex& ix, cudaStream_t st);
+void free_cache(DevIndex& ix);
 bool persist_fits(const GridArgs& g, bool density);
 int launch_density_persist(const GridArgs& g, cudaStream_t st);
 int launch_hamiltonian_persist(const GridArgs& g, cudaStream_t st);

@@ -1,15 +1,16 @@
 // Persistent, warp-specialized grid kernels (one CTA per SM, 16 warps).
 //
-// Warps 0..3 (producers) pull grid blocks from a global work counter (blocks
-// ordered heaviest first) and stage them -- covers, tables, task list, Phi --
-// into one of two shared-memory buffers, then arrive on the buffer's `full`
-// mbarrier. Warps 4..15 (consumers) wait on `full`, run their LPT-assigned
-// tasks (DMMA contractions, kb_gridcore.cuh) and leave for the next buffer
-// without a CTA-wide barrier; the last consumer to finish a block (SMEM
-// counter) reduces the per-warp rho accumulators in a fixed order, writes rho
-// and arrives on the buffer's `empty` mbarrier, which the producers wait on
-// before reusing it. Staging of block k+1 thus overlaps the DMMA work of
-// block k, and a slow warp only delays its own buffer.
+// Warp 0 (producer) pulls grid blocks from a global work counter (blocks
+// ordered heaviest first), waits for a free shared-memory buffer (`empty`
+// mbarrier) and stages the block with two TMA bulk copies from the geometry
+// cache (kb_cache.cu) -- the block's table image and its Phi rows -- which
+// complete on the buffer's `full` mbarrier (expect_tx). For H it also gathers
+// w = V dV of the block's 64 points. Warps 1..15 (consumers) wait on `full`,
+// run their LPT-assigned tasks (DMMA contractions, kb_gridcore.cuh) and move
+// on to the next buffer without a CTA-wide barrier; the last consumer to
+// finish a block (shared counter) reduces the per-warp rho accumulators in a
+// fixed order, writes rho, and arrives on `empty`. Staging of block k+1 thus
+// overlaps the DMMA work of block k.
 #include "kb_gridcore.cuh"
 
 namespace kbg {
@@ -18,9 +19,8 @@ namespace {
 
 using namespace core;
 
-constexpr int NP = kPersistProducers;
 constexpr int NC = kPersistConsumers;
-constexpr int NT = (NP + NC) * 32;
+constexpr int NT = (kPersistProducers + NC) * 32;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -29,9 +29,12 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile(
-        "{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(smem_u32(bar))
-        : "memory");
+    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
@@ -44,13 +47,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void producer_sync() { asm volatile("bar.sync 1, %0;" ::"r"(NP * 32) : "memory"); }
+// TMA bulk copy global -> shared, completing `bytes` on the mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
 
 struct Buffers {
     Smem buf[2];
     uint64_t* full;   // [2]
     uint64_t* empty;  // [2]
-    int* next;        // producer broadcast slot
 };
 
 __device__ __forceinline__ Buffers carve_all(unsigned char* base, const GridArgs& g, size_t acc) {
@@ -61,7 +69,6 @@ __device__ __forceinline__ Buffers carve_all(unsigned char* base, const GridArgs
     B.buf[1] = carve(base + bsz, g, acc);
     B.full = reinterpret_cast<uint64_t*>(base + 2 * bsz);
     B.empty = B.full + 2;
-    B.next = reinterpret_cast<int*>(B.empty + 2);
     return B;
 }
 
@@ -71,38 +78,62 @@ __host__ __device__ inline size_t persist_bytes(const GridArgs& g, bool density)
     return 2 * align16(buffer_layout(g, acc, off)) + 64;
 }
 
-// Producer loop (threads 0..NP*32-1). Returns when the work is exhausted.
 template <bool DENSITY>
-__device__ void producer(const GridArgs& g, const Buffers& B, int ptid) {
+__device__ void producer(const GridArgs& g, const Buffers& B, int lane) {
     for (int k = 0;; ++k) {
         const int s = k & 1;
         if (k >= 2) mbar_wait(&B.empty[s], ((k >> 1) - 1) & 1);
         const Smem& sm = B.buf[s];
         int64_t b = -1;
+        int ncov = 0;
         for (;;) {
-            if (ptid == 0) *B.next = atomicAdd(g.counter, 1);
-            producer_sync();
-            const int idx = *B.next;
-            producer_sync();
+            int idx = 0;
+            if (lane == 0) idx = atomicAdd(g.counter, 1);
+            idx = __shfl_sync(0xffffffffu, idx, 0);
             if (idx >= g.norder) {
                 b = -1;
                 break;
             }
             b = g.order[idx];
-            const int ncov = stage_block(g, b, sm, ptid, NP * 32, [] { producer_sync(); }, DENSITY, NC);
+            ncov = g.blk_ptr[b + 1] - g.blk_ptr[b];
             if (ncov > 0) break;
-            if (DENSITY && ptid < 64) {  // empty block: rho = 0 on its points
+            if (DENSITY) {  // empty block: rho = 0 on its points
                 int bi, bj, bk;
                 block_decode(g.sys, b, bi, bj, bk);
-                bool valid;
-                const int64_t pt = slot_point(g.sys, bi, bj, bk, ptid, valid);
-                if (valid)
-                    for (int spin = 0; spin < g.nspin; ++spin) g.out[spin * g.npts + pt] = 0.0;
+                for (int p = lane; p < 64; p += 32) {
+                    bool valid;
+                    const int64_t pt = slot_point(g.sys, bi, bj, bk, p, valid);
+                    if (valid)
+                        for (int spin = 0; spin < g.nspin; ++spin) g.out[spin * g.npts + pt] = 0.0;
+                }
             }
         }
-        if (b < 0 && ptid == 0) sm.meta->block = -1;
-        mbar_arrive(&B.full[s]);
-        if (b < 0) return;
+        if (b < 0) {
+            if (lane == 0) {
+                sm.meta->block = -1;
+                mbar_arrive(&B.full[s]);
+            }
+            return;
+        }
+        if (!DENSITY && g.in) {  // w = V dV of the block's points, every spin
+            int bi, bj, bk;
+            block_decode(g.sys, b, bi, bj, bk);
+            for (int i = lane; i < g.nspin * 64; i += 32) {
+                bool valid;
+                const int64_t pt = slot_point(g.sys, bi, bj, bk, i & 63, valid);
+                sm.acc[i] = valid ? g.in[(i >> 6) * g.npts + pt] * g.dV : 0.0;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            const int64_t i = b - g.blk_begin;
+            const uint32_t tb = static_cast<uint32_t>(g.tab_bytes);
+            const uint32_t pb = static_cast<uint32_t>((g.phi_off[i + 1] - g.phi_off[i]) * sizeof(double));
+            mbar_arrive_tx(&B.full[s], tb + pb);
+            bulk_g2s(sm.meta, g.tabs + i * g.tab_bytes, tb, &B.full[s]);
+            bulk_g2s(sm.phi, g.phis + g.phi_off[i], pb, &B.full[s]);
+        }
+        __syncwarp();
     }
 }
 
@@ -119,6 +150,9 @@ __device__ void consumer(const GridArgs& g, const Buffers& B, int cw, int lane) 
             if (DENSITY) {
                 const double* Dr = g.dmr + spin * g.nrep;
                 double* racc = sm.acc + (spin * NC + cw) * 64;
+                racc[lane] = 0.0;
+                racc[lane + 32] = 0.0;
+                __syncwarp();
                 for (int w = cw; w < g.task_warps; w += NC)
                     for (int e = sm.wptr[w]; e < sm.wptr[w + 1]; ++e) rho_task(sm, ncov, sm.task[e], Dr, racc, lane);
             } else {
@@ -164,16 +198,17 @@ __global__ void __launch_bounds__(NT, 1) k_persist(GridArgs g) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int s = 0; s < 2; ++s) {
-            mbar_init(&B.full[s], NP * 32);
+            mbar_init(&B.full[s], 1);
             mbar_init(&B.empty[s], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (warp < NP)
-        producer<DENSITY>(g, B, tid);
-    else
-        consumer<DENSITY>(g, B, warp - NP, lane);
+    if (warp < kPersistProducers) {
+        if (warp == 0) producer<DENSITY>(g, B, lane);
+    } else {
+        consumer<DENSITY>(g, B, warp - kPersistProducers, lane);
+    }
 }
 
 template <class K>

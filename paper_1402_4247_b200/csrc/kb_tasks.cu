@@ -40,7 +40,7 @@ __device__ __forceinline__ uint16_t sat16(int64_t c) { return static_cast<uint16
 __global__ void k_tasks(SysParams P, int64_t nblock, const int32_t* __restrict__ blk_ptr,
                         const int32_t* __restrict__ cov_atom, const uint64_t* __restrict__ cov_mask, int64_t* hcnt,
                         int64_t* rcnt, const int64_t* __restrict__ hptr, const int64_t* __restrict__ rptr, Task* hout,
-                        Task* rout, TaskStats* st) {
+                        Task* rout, TaskStats* st, int32_t* rows_out) {
     const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (b >= nblock) return;
     const int c0 = blk_ptr[b];
@@ -48,6 +48,7 @@ __global__ void k_tasks(SysParams P, int64_t nblock, const int32_t* __restrict__
     if (ncov > kMaxCoverPerBlock) {
         atomicMax(&st->too_many_covers, ncov);
         if (hcnt) hcnt[b] = rcnt[b] = 0;
+        if (rows_out) rows_out[b] = 0;
         return;
     }
     int norb[kMaxCoverPerBlock], g_first[kMaxCoverPerBlock], g_end[kMaxCoverPerBlock], g_row0[kMaxCoverPerBlock],
@@ -97,6 +98,7 @@ __global__ void k_tasks(SysParams P, int64_t nblock, const int32_t* __restrict__
             ++nr;
         }
     }
+    if (rows_out) rows_out[b] = ng ? g_row0[ng - 1] + g_rows[ng - 1] : 0;
     if (hcnt) {
         hcnt[b] = nh;
         rcnt[b] = nr;
@@ -157,6 +159,8 @@ void free_tasks(DevIndex& ix) {
     ix.ht_ptr = ix.rt_ptr = nullptr;
     ix.ht = ix.rt = nullptr;
     ix.ht_wptr = ix.rt_wptr = nullptr;
+    if (ix.blk_rows) cudaFree(ix.blk_rows);
+    ix.blk_rows = nullptr;
 }
 
 void build_tasks_device(const SysParams& P, DevIndex& ix, int task_warps, cudaStream_t st) {
@@ -171,8 +175,9 @@ void build_tasks_device(const SysParams& P, DevIndex& ix, int task_warps, cudaSt
     KBG_CUDA(cudaMemsetAsync(hcnt, 0, (nb + 1) * sizeof(int64_t), st));
     KBG_CUDA(cudaMemsetAsync(rcnt, 0, (nb + 1) * sizeof(int64_t), st));
     KBG_CUDA(cudaMemsetAsync(d_st, 0, sizeof(TaskStats), st));
+    if (!ix.blk_rows) ix.blk_rows = talloc<int32_t>(nb);
     k_tasks<<<grid, T, 0, st>>>(P, nb, ix.blk_ptr, ix.cov_atom, ix.cov_mask, hcnt, rcnt, nullptr, nullptr, nullptr,
-                                nullptr, d_st);
+                                nullptr, d_st, ix.blk_rows);
     KBG_CUDA(cudaGetLastError());
     ix.ht_ptr = talloc<int64_t>(nb + 1);
     ix.rt_ptr = talloc<int64_t>(nb + 1);
@@ -181,7 +186,7 @@ void build_tasks_device(const SysParams& P, DevIndex& ix, int task_warps, cudaSt
     Task* htmp = talloc<Task>(ix.nhtask);
     Task* rtmp = talloc<Task>(ix.nrtask);
     k_tasks<<<grid, T, 0, st>>>(P, nb, ix.blk_ptr, ix.cov_atom, ix.cov_mask, nullptr, nullptr, ix.ht_ptr, ix.rt_ptr,
-                                htmp, rtmp, d_st);
+                                htmp, rtmp, d_st, nullptr);
     KBG_CUDA(cudaGetLastError());
     ix.ht = talloc<Task>(ix.nhtask);
     ix.rt = talloc<Task>(ix.nrtask);
