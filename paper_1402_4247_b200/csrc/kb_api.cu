@@ -208,7 +208,7 @@ int run_density(kbg_ctx* c, int nspin, const double* d_dm, double* d_rho, cudaSt
     int n = kbg::launch_dm_repack(c->ix, c->P, nspin, d_dm, c->d_dmr, st);
     kbg::GridArgs g = grid_args(c, nspin, 0.0, d_dm, d_rho, true);
     g.dmr = c->d_dmr;
-    if (c->persist_ok && c->persist && c->ix.phis)
+    if (c->persist_ok && c->persist && c->ix.phis && kbg::persist_fits(g, true))
         n += kbg::launch_density_persist(g, st);
     else
         n += kbg::launch_density(g, c->blk_end - c->blk_begin, c->nwarps, st);
@@ -217,7 +217,8 @@ int run_density(kbg_ctx* c, int nspin, const double* d_dm, double* d_rho, cudaSt
 
 int run_hamiltonian(kbg_ctx* c, int nspin, double dV, const double* d_veff, double* d_h, cudaStream_t st) {
     const kbg::GridArgs g = grid_args(c, nspin, dV, d_veff, d_h, false);
-    if (c->persist_ok && c->persist && c->ix.phis) return kbg::launch_hamiltonian_persist(g, st);
+    if (c->persist_ok && c->persist && c->ix.phis && kbg::persist_fits(g, false))
+        return kbg::launch_hamiltonian_persist(g, st);
     return kbg::launch_hamiltonian(g, c->blk_end - c->blk_begin, c->nwarps, st);
 }
 

@@ -26,8 +26,7 @@ __global__ void k_phi_count(int64_t b0, int64_t n, const int32_t* __restrict__ r
 
 __global__ void __launch_bounds__(256) k_build_cache(GridArgs gh, GridArgs gr, const int64_t* __restrict__ phi_off,
                                                      unsigned char* htab, unsigned char* rtab, double* phis) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const Smem sm = carve(smem_raw, gh, 0);
+    const Smem sm = carve(0u, gh, 0);
     const int64_t i = blockIdx.x;
     const int64_t b = gh.blk_begin + i;
     const int tid = threadIdx.x, nt = blockDim.x;
@@ -35,19 +34,19 @@ __global__ void __launch_bounds__(256) k_build_cache(GridArgs gh, GridArgs gr, c
     const size_t T = table_bytes(gh);
     const int ncov = stage_block(gh, b, sm, tid, nt, sync, false, 0, true);
     {
-        const int4* src = reinterpret_cast<const int4*>(smem_raw);
+        const int4* src = reinterpret_cast<const int4*>(kbg_smem);
         int4* dst = reinterpret_cast<int4*>(htab + i * T);
         for (size_t k = tid; k < T / 16; k += nt) dst[k] = src[k];
     }
     if (ncov > 0) {
-        const int64_t n = static_cast<int64_t>(sm.meta->rows + 8) * 64;
+        const int64_t n = static_cast<int64_t>(sm.meta()->rows + 8) * 64;
         double* dst = phis + phi_off[i];
-        for (int64_t k = tid; k < n; k += nt) dst[k] = sm.phi[k];
+        for (int64_t k = tid; k < n; k += nt) dst[k] = sm.phi()[k];
     }
     __syncthreads();
     stage_block(gr, b, sm, tid, nt, sync, true, 0, false);
     {
-        const int4* src = reinterpret_cast<const int4*>(smem_raw);
+        const int4* src = reinterpret_cast<const int4*>(kbg_smem);
         int4* dst = reinterpret_cast<int4*>(rtab + i * T);
         for (size_t k = tid; k < T / 16; k += nt) dst[k] = src[k];
     }

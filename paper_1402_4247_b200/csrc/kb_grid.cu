@@ -12,8 +12,7 @@ using namespace core;
 
 template <int NW>
 __global__ void __launch_bounds__(NW * 32, 2) k_hamiltonian(GridArgs g) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const Smem sm = carve(smem_raw, g, static_cast<size_t>(g.nspin) * 64);
+    const Smem sm = carve(0u, g, static_cast<size_t>(g.nspin) * 64);
     const int64_t b = g.blk_begin + blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ncov = stage_block(g, b, sm, tid, NW * 32, [] { __syncthreads(); }, false, NW);
@@ -21,15 +20,14 @@ __global__ void __launch_bounds__(NW * 32, 2) k_hamiltonian(GridArgs g) {
     for (int spin = 0; spin < g.nspin; ++spin) {
         double* Hs = g.out + spin * g.nnz;
         for (int w = warp; w < g.task_warps; w += NW)
-            for (int e = sm.wptr[w]; e < sm.wptr[w + 1]; ++e)
-                h_task(sm, sm.acc + spin * 64, ncov, sm.task[e], Hs, g.sign, g.scatter, lane);
+            for (int e = sm.wptr()[w]; e < sm.wptr()[w + 1]; ++e)
+                h_task(sm, sm.acc() + spin * 64, ncov, sm.task()[e], Hs, g.sign, g.scatter, lane);
     }
 }
 
 template <int NW>
 __global__ void __launch_bounds__(NW * 32, 2) k_density(GridArgs g) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const Smem sm = carve(smem_raw, g, static_cast<size_t>(g.nspin) * NW * 64);
+    const Smem sm = carve(0u, g, static_cast<size_t>(g.nspin) * NW * 64);
     const int64_t b = g.blk_begin + blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int bi, bj, bk;
@@ -38,9 +36,9 @@ __global__ void __launch_bounds__(NW * 32, 2) k_density(GridArgs g) {
     if (ncov > 0) {
         for (int spin = 0; spin < g.nspin; ++spin) {
             const double* Dr = g.dmr + spin * g.nrep;
-            double* racc = sm.acc + (spin * NW + warp) * 64;
+            double* racc = sm.acc() + (spin * NW + warp) * 64;
             for (int w = warp; w < g.task_warps; w += NW)
-                for (int e = sm.wptr[w]; e < sm.wptr[w + 1]; ++e) rho_task(sm, ncov, sm.task[e], Dr, racc, lane);
+                for (int e = sm.wptr()[w]; e < sm.wptr()[w + 1]; ++e) rho_task(sm, ncov, sm.task()[e], Dr, racc, lane);
         }
         __syncthreads();
     }
@@ -49,7 +47,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_density(GridArgs g) {
         double r = 0.0;
         if (ncov > 0)
 #pragma unroll
-            for (int w = 0; w < NW; ++w) r += sm.acc[(spin * NW + w) * 64 + p];
+            for (int w = 0; w < NW; ++w) r += sm.acc()[(spin * NW + w) * 64 + p];
         bool valid;
         const int64_t pt = slot_point(g.sys, bi, bj, bk, p, valid);
         if (valid) g.out[spin * g.npts + pt] = r;
@@ -160,15 +158,14 @@ __global__ void k_dm_check(SysParams P, int64_t npair, int nspin, int64_t nnz, c
 }
 
 __global__ void k_block_orbitals(GridArgs g, int64_t b, double* out) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const Smem sm = carve(smem_raw, g, static_cast<size_t>(g.nspin) * 64);
+    const Smem sm = carve(0u, g, static_cast<size_t>(g.nspin) * 64);
     const int ncov = stage_block(g, b, sm, threadIdx.x, blockDim.x, [] { __syncthreads(); }, false, 1);
     // rows in cover order
     int r0 = 0;
     for (int c = 0; c < ncov; ++c) {
-        const CoverS& cv = sm.cov[c];
+        const CoverS& cv = sm.cov()[c];
         for (int i = threadIdx.x; i < cv.norb * 64; i += blockDim.x)
-            out[static_cast<size_t>(r0) * 64 + i] = sm.phi[phi_idx(cv.row0 + (i >> 6), i & 63)];
+            out[static_cast<size_t>(r0) * 64 + i] = sm.phi()[phi_idx(cv.row0 + (i >> 6), i & 63)];
         r0 += cv.norb;
     }
 }

@@ -60,19 +60,29 @@ __device__ __forceinline__ uint32_t octet_bits(uint64_t m) {
 __device__ __forceinline__ int swz(int row) { return (row & 3) << 2; }
 __device__ __forceinline__ int phi_idx(int row, int slot) { return row * 64 + (slot ^ swz(row)); }
 
+// Dynamic shared memory of every grid kernel. Buffers are addressed by byte
+// offsets from this symbol (not by pointers kept in structs) so the compiler
+// always emits shared-memory loads/stores (LDS/STS), never generic LD/ST.
+extern __shared__ __align__(16) unsigned char kbg_smem[];
+
 struct Smem {
-    double* phi;
-    double* acc;     // H: w[nspin][64];  rho: racc[nspin][acc_warps][64]
-    CoverS* cov;
-    GroupS* grp;
-    int32_t* off2d;  // [ncov][ncov] offset of canonical pair (ci <= cj) with common points (H: value, rho: repacked)
-    uint8_t* rcov;   // [rows] cover of each Phi row (kNoCover for the tail rows)
-    uint8_t* rorb;   // [rows] orbital index inside that cover
-    uint8_t* pom;    // [ngrp][ncov] octets shared by group g (rows ci <= cj) and cover cj
-    uint64_t* pbits; // [ngrp][2] covers cj with a shared octet in half h
-    Task* task;
-    int32_t* wptr;   // [kMaxTaskWarps + 1]
-    Meta* meta;
+    uint32_t o_meta, o_cov, o_grp, o_off2d, o_rcov, o_rorb, o_pom, o_pbits, o_task, o_wptr, o_acc, o_phi;
+    __device__ __forceinline__ Meta* meta() const { return reinterpret_cast<Meta*>(kbg_smem + o_meta); }
+    __device__ __forceinline__ CoverS* cov() const { return reinterpret_cast<CoverS*>(kbg_smem + o_cov); }
+    __device__ __forceinline__ GroupS* grp() const { return reinterpret_cast<GroupS*>(kbg_smem + o_grp); }
+    // [ncov][ncov] offset of canonical pair (ci <= cj) with common points (H: value, rho: repacked)
+    __device__ __forceinline__ int32_t* off2d() const { return reinterpret_cast<int32_t*>(kbg_smem + o_off2d); }
+    __device__ __forceinline__ uint8_t* rcov() const { return kbg_smem + o_rcov; }  // row -> cover (kNoCover: tail)
+    __device__ __forceinline__ uint8_t* rorb() const { return kbg_smem + o_rorb; }  // row -> orbital in cover
+    // [ngrp][ncov] octets shared by group g (rows ci <= cj) and cover cj
+    __device__ __forceinline__ uint8_t* pom() const { return kbg_smem + o_pom; }
+    // [ngrp][2] covers cj with a shared octet in half h
+    __device__ __forceinline__ uint64_t* pbits() const { return reinterpret_cast<uint64_t*>(kbg_smem + o_pbits); }
+    __device__ __forceinline__ Task* task() const { return reinterpret_cast<Task*>(kbg_smem + o_task); }
+    __device__ __forceinline__ int32_t* wptr() const { return reinterpret_cast<int32_t*>(kbg_smem + o_wptr); }
+    // H: w[nspin][64];  rho: racc[nspin][acc_warps][64]
+    __device__ __forceinline__ double* acc() const { return reinterpret_cast<double*>(kbg_smem + o_acc); }
+    __device__ __forceinline__ double* phi() const { return reinterpret_cast<double*>(kbg_smem + o_phi); }
 };
 
 __host__ __device__ __forceinline__ size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
@@ -122,22 +132,23 @@ __host__ __device__ inline size_t buffer_layout(const GridArgs& g, size_t acc_do
     return o;
 }
 
-__device__ __forceinline__ Smem carve(unsigned char* base, const GridArgs& g, size_t acc_doubles) {
+// Buffer at byte offset `base` of kbg_smem.
+__device__ __forceinline__ Smem carve(uint32_t base, const GridArgs& g, size_t acc_doubles) {
     size_t off[12];
     buffer_layout(g, acc_doubles, off);
     Smem s;
-    s.meta = reinterpret_cast<Meta*>(base + off[0]);
-    s.cov = reinterpret_cast<CoverS*>(base + off[1]);
-    s.grp = reinterpret_cast<GroupS*>(base + off[2]);
-    s.off2d = reinterpret_cast<int32_t*>(base + off[3]);
-    s.rcov = base + off[4];
-    s.rorb = base + off[5];
-    s.pom = base + off[6];
-    s.pbits = reinterpret_cast<uint64_t*>(base + off[7]);
-    s.task = reinterpret_cast<Task*>(base + off[8]);
-    s.wptr = reinterpret_cast<int32_t*>(base + off[9]);
-    s.acc = reinterpret_cast<double*>(base + off[10]);
-    s.phi = reinterpret_cast<double*>(base + off[11]);
+    s.o_meta = base + static_cast<uint32_t>(off[0]);
+    s.o_cov = base + static_cast<uint32_t>(off[1]);
+    s.o_grp = base + static_cast<uint32_t>(off[2]);
+    s.o_off2d = base + static_cast<uint32_t>(off[3]);
+    s.o_rcov = base + static_cast<uint32_t>(off[4]);
+    s.o_rorb = base + static_cast<uint32_t>(off[5]);
+    s.o_pom = base + static_cast<uint32_t>(off[6]);
+    s.o_pbits = base + static_cast<uint32_t>(off[7]);
+    s.o_task = base + static_cast<uint32_t>(off[8]);
+    s.o_wptr = base + static_cast<uint32_t>(off[9]);
+    s.o_acc = base + static_cast<uint32_t>(off[10]);
+    s.o_phi = base + static_cast<uint32_t>(off[11]);
     return s;
 }
 
@@ -159,9 +170,9 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int tid
     const int c0 = g.blk_ptr[b];
     const int ncov = g.blk_ptr[b + 1] - c0;
     if (tid == 0) {
-        sm.meta->block = b;
-        sm.meta->ncov = ncov;
-        sm.meta->done = 0;
+        sm.meta()->block = b;
+        sm.meta()->ncov = ncov;
+        sm.meta()->done = 0;
     }
     if (ncov == 0) {
         sync();
@@ -169,7 +180,7 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int tid
     }
     const SysParams& P = g.sys;
     if (tid < ncov) {
-        CoverS& cv = sm.cov[tid];
+        CoverS& cv = sm.cov()[tid];
         const int a = g.cov_atom[c0 + tid];
         cv.sp = P.spc[a];
         cv.norb = P.sp[cv.sp].norb;
@@ -180,64 +191,64 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int tid
     }
     const int64_t tp0 = g.t_ptr[b];
     const int ntask = static_cast<int>(g.t_ptr[b + 1] - tp0);
-    for (int i = tid; i < ntask; i += nt) sm.task[i] = g.tasks[tp0 + i];
-    if (tid <= kMaxTaskWarps) sm.wptr[tid] = g.t_wptr[b * (kMaxTaskWarps + 1) + tid];
-    for (int i = tid; i < ncov * ncov; i += nt) sm.off2d[i] = -1;
-    for (int i = tid; i < g.max_rows; i += nt) sm.rcov[i] = kNoCover;
+    for (int i = tid; i < ntask; i += nt) sm.task()[i] = g.tasks[tp0 + i];
+    if (tid <= kMaxTaskWarps) sm.wptr()[tid] = g.t_wptr[b * (kMaxTaskWarps + 1) + tid];
+    for (int i = tid; i < ncov * ncov; i += nt) sm.off2d()[i] = -1;
+    for (int i = tid; i < g.max_rows; i += nt) sm.rcov()[i] = kNoCover;
     int bi, bj, bk;
     block_decode(P, b, bi, bj, bk);
     if (density) {
-        for (int i = tid; i < g.nspin * acc_warps * 64; i += nt) sm.acc[i] = 0.0;
+        for (int i = tid; i < g.nspin * acc_warps * 64; i += nt) sm.acc()[i] = 0.0;
     } else if (g.in) {
         for (int i = tid; i < g.nspin * 64; i += nt) {
             bool valid;
             const int64_t pt = slot_point(P, bi, bj, bk, i & 63, valid);
-            sm.acc[i] = valid ? g.in[(i >> 6) * g.npts + pt] * g.dV : 0.0;
+            sm.acc()[i] = valid ? g.in[(i >> 6) * g.npts + pt] * g.dV : 0.0;
         }
     }
     sync();
     if (tid == 0) {
         int gf[kMaxCoverPerBlock], ge[kMaxCoverPerBlock], gr0[kMaxCoverPerBlock], grs[kMaxCoverPerBlock],
             cr0[kMaxCoverPerBlock], cg[kMaxCoverPerBlock];
-        const int ng = make_groups(ncov, [&](int c) { return sm.cov[c].norb; }, gf, ge, gr0, grs, cr0, cg);
-        for (int q = 0; q < ng; ++q) sm.grp[q] = GroupS{gf[q], ge[q], gr0[q], grs[q], (grs[q] + 7) >> 3};
+        const int ng = make_groups(ncov, [&](int c) { return sm.cov()[c].norb; }, gf, ge, gr0, grs, cr0, cg);
+        for (int q = 0; q < ng; ++q) sm.grp()[q] = GroupS{gf[q], ge[q], gr0[q], grs[q], (grs[q] + 7) >> 3};
         for (int c = 0; c < ncov; ++c) {
-            sm.cov[c].row0 = cr0[c];
-            sm.cov[c].grp = cg[c];
+            sm.cov()[c].row0 = cr0[c];
+            sm.cov()[c].grp = cg[c];
         }
-        sm.meta->ngrp = ng;
-        sm.meta->rows = gr0[ng - 1] + grs[ng - 1];
+        sm.meta()->ngrp = ng;
+        sm.meta()->rows = gr0[ng - 1] + grs[ng - 1];
     }
     {
         const int64_t p0 = g.bp_ptr[b], p1 = g.bp_ptr[b + 1];
         for (int64_t e = p0 + tid; e < p1; e += nt) {
             const BPair bp = g.bp[e];
-            sm.off2d[(bp.cicj & 0xffff) * ncov + (bp.cicj >> 16)] = density ? bp.roff : static_cast<int32_t>(bp.off);
+            sm.off2d()[(bp.cicj & 0xffff) * ncov + (bp.cicj >> 16)] = density ? bp.roff : static_cast<int32_t>(bp.off);
         }
     }
     sync();
-    const int ngrp = sm.meta->ngrp, rows = sm.meta->rows;
+    const int ngrp = sm.meta()->ngrp, rows = sm.meta()->rows;
     for (int i = tid; i < ngrp * ncov; i += nt) {
         const int q = i / ncov, cj = i % ncov;
-        const GroupS& G = sm.grp[q];
+        const GroupS& G = sm.grp()[q];
         uint64_t m = 0;
         if (cj >= G.first)
-            for (int ci = G.first; ci < G.end && ci <= cj; ++ci) m |= sm.cov[ci].mask & sm.cov[cj].mask;
-        sm.pom[i] = static_cast<uint8_t>(octet_bits(m));
+            for (int ci = G.first; ci < G.end && ci <= cj; ++ci) m |= sm.cov()[ci].mask & sm.cov()[cj].mask;
+        sm.pom()[i] = static_cast<uint8_t>(octet_bits(m));
     }
     if (tid < ncov) {
-        const CoverS& cv = sm.cov[tid];
+        const CoverS& cv = sm.cov()[tid];
         for (int o = 0; o < cv.norb; ++o) {
-            sm.rcov[cv.row0 + o] = static_cast<uint8_t>(tid);
-            sm.rorb[cv.row0 + o] = static_cast<uint8_t>(o);
+            sm.rcov()[cv.row0 + o] = static_cast<uint8_t>(tid);
+            sm.rorb()[cv.row0 + o] = static_cast<uint8_t>(o);
         }
     }
     if (eval_phi)
-        for (int i = tid; i < 8 * 64; i += nt) sm.phi[rows * 64 + i] = 0.0;  // tail rows (tile overrun)
+        for (int i = tid; i < 8 * 64; i += nt) sm.phi()[rows * 64 + i] = 0.0;  // tail rows (tile overrun)
     for (int task = tid; eval_phi && task < ncov * 64; task += nt) {
         const int c = task >> 6, s = task & 63;
-        const CoverS& cv = sm.cov[c];
-        double* dst = sm.phi;
+        const CoverS& cv = sm.cov()[c];
+        double* dst = sm.phi();
         const int row0 = cv.row0;
         if ((cv.mask >> s) & 1) {
             int li, lj, lk;
@@ -260,8 +271,8 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int tid
         const int q = tid >> 1, h = tid & 1;
         uint64_t bits = 0;
         for (int cj = 0; cj < ncov; ++cj)
-            if ((sm.pom[q * ncov + cj] >> (4 * h)) & 0xF) bits |= 1ull << cj;
-        sm.pbits[tid] = bits;
+            if ((sm.pom()[q * ncov + cj] >> (4 * h)) & 0xF) bits |= 1ull << cj;
+        sm.pbits()[tid] = bits;
     }
     sync();
     return ncov;
@@ -282,10 +293,10 @@ __device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict_
         for (int i = 0; i < TM; ++i)
 #pragma unroll
             for (int j = 0; j < TN; ++j) c[u][i][j][0] = c[u][i][j][1] = 0.0;
-    const CoverS& B = sm.cov[cj];
+    const CoverS& B = sm.cov()[cj];
     const int ra = ra0 + (lane >> 2), rb = B.row0 + cb0 + (lane >> 2);
-    const double* pa = sm.phi + ra * 64 + (lane & 3);
-    const double* pb = sm.phi + rb * 64 + (lane & 3);
+    const double* pa = sm.phi() + ra * 64 + (lane & 3);
+    const double* pb = sm.phi() + rb * 64 + (lane & 3);
     const int sa = swz(ra), sb = swz(rb);  // 8-row steps keep row & 3
     const double* pw = w + (lane & 3);
     auto step = [&](int u, int q) {
@@ -317,9 +328,9 @@ __device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict_
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
         const int r = ra0 + 8 * i + (lane >> 2);
-        const int ci = r < rend ? sm.rcov[r] : kNoCover;
-        const int off = ci <= cj ? sm.off2d[ci * ncov + cj] : -1;
-        const int ri = sm.rorb[r];
+        const int ci = r < rend ? sm.rcov()[r] : kNoCover;
+        const int off = ci <= cj ? sm.off2d()[ci * ncov + cj] : -1;
+        const int ri = sm.rorb()[r];
 #pragma unroll
         for (int j = 0; j < TN; ++j)
 #pragma unroll
@@ -339,8 +350,8 @@ __device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict_
 
 __device__ __forceinline__ void h_task(const Smem& sm, const double* w, int ncov, const Task& t, double* H,
                                        double sign, int scatter, int lane) {
-    const GroupS& G = sm.grp[t.g];
-    const int nb = sm.cov[t.cj].norb;
+    const GroupS& G = sm.grp()[t.g];
+    const int nb = sm.cov()[t.cj].norb;
     const uint32_t qm = t.qmask;
     const int rend = G.row0 + G.rows;
     for (int i0 = 0; i0 < G.tm; i0 += 2) {
@@ -368,11 +379,11 @@ __device__ __forceinline__ void h_task(const Smem& sm, const double* w, int ncov
 template <int TM>
 __device__ __forceinline__ void gather_a(const Smem& sm, int ncov, const int (&rci)[TM], const int (&rri)[TM], int cj,
                                          int kc, const double* __restrict__ Dr, int lane, double (&a)[TM][4]) {
-    const int stride = 16 * ((sm.cov[cj].norb + 15) >> 4);
+    const int stride = 16 * ((sm.cov()[cj].norb + 15) >> 4);
 #pragma unroll
     for (int t = 0; t < TM; ++t) {
         const int ci = rci[t];
-        const int off = ci <= cj ? sm.off2d[ci * ncov + cj] : -1;  // ci = kNoCover (255) fails ci <= cj
+        const int off = ci <= cj ? sm.off2d()[ci * ncov + cj] : -1;  // ci = kNoCover (255) fails ci <= cj
         if (off >= 0) {
             const double2* p = reinterpret_cast<const double2*>(Dr + off + rri[t] * stride + 16 * kc + 4 * (lane & 3));
             const double2 v0 = __ldg(p), v1 = __ldg(p + 1);
@@ -405,22 +416,22 @@ __device__ __forceinline__ void rho_partner(const double* __restrict__ pb, int s
 template <int TM>
 __device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, const double* __restrict__ Dr,
                               double* __restrict__ racc, int lane) {
-    const GroupS& G = sm.grp[gi];
+    const GroupS& G = sm.grp()[gi];
     const int rend = G.row0 + G.rows;
     int rci[TM], rri[TM];
 #pragma unroll
     for (int t = 0; t < TM; ++t) {
         const int r = ra0 + 8 * t + (lane >> 2);
-        rci[t] = r < rend ? sm.rcov[r] : kNoCover;
-        rri[t] = sm.rorb[r];
+        rci[t] = r < rend ? sm.rcov()[r] : kNoCover;
+        rri[t] = sm.rorb()[r];
     }
     double y[TM][4][2];
 #pragma unroll
     for (int t = 0; t < TM; ++t)
 #pragma unroll
         for (int o = 0; o < 4; ++o) y[t][o][0] = y[t][o][1] = 0.0;
-    const uint8_t* pom = sm.pom + gi * ncov;
-    uint64_t bits = sm.pbits[2 * gi + h];
+    const uint8_t* pom = sm.pom() + gi * ncov;
+    uint64_t bits = sm.pbits()[2 * gi + h];
     const int colbase = 32 * h + (lane >> 2);
     double nxt[TM][4];
     if (bits) gather_a<TM>(sm, ncov, rci, rri, __ffsll(bits) - 1, 0, Dr, lane, nxt);
@@ -428,7 +439,7 @@ __device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, 
         const int cj = __ffsll(bits) - 1;
         bits &= bits - 1;
         const uint32_t om4 = (pom[cj] >> (4 * h)) & 0xFu;
-        const CoverS& B = sm.cov[cj];
+        const CoverS& B = sm.cov()[cj];
         double a[TM][4];
 #pragma unroll
         for (int t = 0; t < TM; ++t)
@@ -440,7 +451,7 @@ __device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, 
             if (kc > 0) gather_a<TM>(sm, ncov, rci, rri, cj, kc, Dr, lane, a);
             const int ks = min(4, (B.norb - 16 * kc + 3) >> 2);
             const int rb = B.row0 + 16 * kc + (lane & 3);
-            const double* pb = sm.phi + rb * 64;
+            const double* pb = sm.phi() + rb * 64;
             const int swb = swz(rb);
             switch (ks) {
                 case 1: rho_partner<TM, 1>(pb, swb, om4, a, y, colbase); break;
@@ -461,7 +472,7 @@ __device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, 
 #pragma unroll
             for (int t = 0; t < TM; ++t) {
                 const int r = ra0 + 8 * t + (lane >> 2);
-                v += sm.phi[phi_idx(r, p)] * y[t][o][e];
+                v += sm.phi()[phi_idx(r, p)] * y[t][o][e];
             }
             v += __shfl_xor_sync(0xffffffffu, v, 4);
             v += __shfl_xor_sync(0xffffffffu, v, 8);
@@ -473,7 +484,7 @@ __device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, 
 
 __device__ __forceinline__ void rho_task(const Smem& sm, int ncov, const Task& t, const double* Dr, double* racc,
                                          int lane) {
-    const GroupS& G = sm.grp[t.g];
+    const GroupS& G = sm.grp()[t.g];
     for (int i0 = 0; i0 < G.tm; i0 += 2) {
         if (G.tm - i0 >= 2)
             rho_task_rows<2>(sm, ncov, t.g, G.row0 + 8 * i0, t.half, Dr, racc, lane);

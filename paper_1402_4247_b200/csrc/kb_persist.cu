@@ -61,13 +61,13 @@ struct Buffers {
     uint64_t* empty;  // [2]
 };
 
-__device__ __forceinline__ Buffers carve_all(unsigned char* base, const GridArgs& g, size_t acc) {
+__device__ __forceinline__ Buffers carve_all(const GridArgs& g, size_t acc) {
     size_t off[12];
-    const size_t bsz = align16(buffer_layout(g, acc, off));
+    const uint32_t bsz = static_cast<uint32_t>(align16(buffer_layout(g, acc, off)));
     Buffers B;
-    B.buf[0] = carve(base, g, acc);
-    B.buf[1] = carve(base + bsz, g, acc);
-    B.full = reinterpret_cast<uint64_t*>(base + 2 * bsz);
+    B.buf[0] = carve(0u, g, acc);
+    B.buf[1] = carve(bsz, g, acc);
+    B.full = reinterpret_cast<uint64_t*>(kbg_smem + 2 * bsz);
     B.empty = B.full + 2;
     return B;
 }
@@ -110,7 +110,7 @@ __device__ void producer(const GridArgs& g, const Buffers& B, int lane) {
         }
         if (b < 0) {
             if (lane == 0) {
-                sm.meta->block = -1;
+                sm.meta()->block = -1;
                 mbar_arrive(&B.full[s]);
             }
             return;
@@ -121,7 +121,7 @@ __device__ void producer(const GridArgs& g, const Buffers& B, int lane) {
             for (int i = lane; i < g.nspin * 64; i += 32) {
                 bool valid;
                 const int64_t pt = slot_point(g.sys, bi, bj, bk, i & 63, valid);
-                sm.acc[i] = valid ? g.in[(i >> 6) * g.npts + pt] * g.dV : 0.0;
+                sm.acc()[i] = valid ? g.in[(i >> 6) * g.npts + pt] * g.dV : 0.0;
             }
         }
         __syncwarp();
@@ -130,8 +130,8 @@ __device__ void producer(const GridArgs& g, const Buffers& B, int lane) {
             const uint32_t tb = static_cast<uint32_t>(g.tab_bytes);
             const uint32_t pb = static_cast<uint32_t>((g.phi_off[i + 1] - g.phi_off[i]) * sizeof(double));
             mbar_arrive_tx(&B.full[s], tb + pb);
-            bulk_g2s(sm.meta, g.tabs + i * g.tab_bytes, tb, &B.full[s]);
-            bulk_g2s(sm.phi, g.phis + g.phi_off[i], pb, &B.full[s]);
+            bulk_g2s(sm.meta(), g.tabs + i * g.tab_bytes, tb, &B.full[s]);
+            bulk_g2s(sm.phi(), g.phis + g.phi_off[i], pb, &B.full[s]);
         }
         __syncwarp();
     }
@@ -143,30 +143,30 @@ __device__ void consumer(const GridArgs& g, const Buffers& B, int cw, int lane) 
         const int s = k & 1;
         mbar_wait(&B.full[s], (k >> 1) & 1);
         const Smem& sm = B.buf[s];
-        const int64_t b = sm.meta->block;
+        const int64_t b = sm.meta()->block;
         if (b < 0) return;
-        const int ncov = sm.meta->ncov;
+        const int ncov = sm.meta()->ncov;
         for (int spin = 0; spin < g.nspin; ++spin) {
             if (DENSITY) {
                 const double* Dr = g.dmr + spin * g.nrep;
-                double* racc = sm.acc + (spin * NC + cw) * 64;
+                double* racc = sm.acc() + (spin * NC + cw) * 64;
                 racc[lane] = 0.0;
                 racc[lane + 32] = 0.0;
                 __syncwarp();
                 for (int w = cw; w < g.task_warps; w += NC)
-                    for (int e = sm.wptr[w]; e < sm.wptr[w + 1]; ++e) rho_task(sm, ncov, sm.task[e], Dr, racc, lane);
+                    for (int e = sm.wptr()[w]; e < sm.wptr()[w + 1]; ++e) rho_task(sm, ncov, sm.task()[e], Dr, racc, lane);
             } else {
                 double* Hs = g.out + spin * g.nnz;
                 for (int w = cw; w < g.task_warps; w += NC)
-                    for (int e = sm.wptr[w]; e < sm.wptr[w + 1]; ++e)
-                        h_task(sm, sm.acc + spin * 64, ncov, sm.task[e], Hs, g.sign, g.scatter, lane);
+                    for (int e = sm.wptr()[w]; e < sm.wptr()[w + 1]; ++e)
+                        h_task(sm, sm.acc() + spin * 64, ncov, sm.task()[e], Hs, g.sign, g.scatter, lane);
             }
         }
         __syncwarp();
         int last = 0;
         if (lane == 0) {
             __threadfence_block();
-            last = atomicAdd(&sm.meta->done, 1) == NC - 1;
+            last = atomicAdd(&sm.meta()->done, 1) == NC - 1;
         }
         last = __shfl_sync(0xffffffffu, last, 0);
         if (last) {
@@ -178,7 +178,7 @@ __device__ void consumer(const GridArgs& g, const Buffers& B, int cw, int lane) 
                     const int spin = i >> 6, p = i & 63;
                     double r = 0.0;
 #pragma unroll
-                    for (int w = 0; w < NC; ++w) r += sm.acc[(spin * NC + w) * 64 + p];
+                    for (int w = 0; w < NC; ++w) r += sm.acc()[(spin * NC + w) * 64 + p];
                     bool valid;
                     const int64_t pt = slot_point(g.sys, bi, bj, bk, p, valid);
                     if (valid) g.out[spin * g.npts + pt] = r;
@@ -192,9 +192,8 @@ __device__ void consumer(const GridArgs& g, const Buffers& B, int cw, int lane) 
 
 template <bool DENSITY>
 __global__ void __launch_bounds__(NT, 1) k_persist(GridArgs g) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
     const size_t acc = static_cast<size_t>(g.nspin) * 64 * (DENSITY ? NC : 1);
-    const Buffers B = carve_all(smem_raw, g, acc);
+    const Buffers B = carve_all(g, acc);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int s = 0; s < 2; ++s) {
