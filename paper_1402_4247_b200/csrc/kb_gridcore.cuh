@@ -66,23 +66,24 @@ __device__ __forceinline__ int phi_idx(int row, int slot) { return row * 64 + (s
 extern __shared__ __align__(16) unsigned char kbg_smem[];
 
 struct Smem {
+    uint32_t base;  // byte offset of this buffer in kbg_smem; o_* are relative to it
     uint32_t o_meta, o_cov, o_grp, o_off2d, o_rcov, o_rorb, o_pom, o_pbits, o_task, o_wptr, o_acc, o_phi;
-    __device__ __forceinline__ Meta* meta() const { return reinterpret_cast<Meta*>(kbg_smem + o_meta); }
-    __device__ __forceinline__ CoverS* cov() const { return reinterpret_cast<CoverS*>(kbg_smem + o_cov); }
-    __device__ __forceinline__ GroupS* grp() const { return reinterpret_cast<GroupS*>(kbg_smem + o_grp); }
+    __device__ __forceinline__ Meta* meta() const { return reinterpret_cast<Meta*>(kbg_smem + base + o_meta); }
+    __device__ __forceinline__ CoverS* cov() const { return reinterpret_cast<CoverS*>(kbg_smem + base + o_cov); }
+    __device__ __forceinline__ GroupS* grp() const { return reinterpret_cast<GroupS*>(kbg_smem + base + o_grp); }
     // [ncov][ncov] offset of canonical pair (ci <= cj) with common points (H: value, rho: repacked)
-    __device__ __forceinline__ int32_t* off2d() const { return reinterpret_cast<int32_t*>(kbg_smem + o_off2d); }
-    __device__ __forceinline__ uint8_t* rcov() const { return kbg_smem + o_rcov; }  // row -> cover (kNoCover: tail)
-    __device__ __forceinline__ uint8_t* rorb() const { return kbg_smem + o_rorb; }  // row -> orbital in cover
+    __device__ __forceinline__ int32_t* off2d() const { return reinterpret_cast<int32_t*>(kbg_smem + base + o_off2d); }
+    __device__ __forceinline__ uint8_t* rcov() const { return kbg_smem + base + o_rcov; }  // row -> cover (kNoCover: tail)
+    __device__ __forceinline__ uint8_t* rorb() const { return kbg_smem + base + o_rorb; }  // row -> orbital in cover
     // [ngrp][ncov] octets shared by group g (rows ci <= cj) and cover cj
-    __device__ __forceinline__ uint8_t* pom() const { return kbg_smem + o_pom; }
+    __device__ __forceinline__ uint8_t* pom() const { return kbg_smem + base + o_pom; }
     // [ngrp][2] covers cj with a shared octet in half h
-    __device__ __forceinline__ uint64_t* pbits() const { return reinterpret_cast<uint64_t*>(kbg_smem + o_pbits); }
-    __device__ __forceinline__ Task* task() const { return reinterpret_cast<Task*>(kbg_smem + o_task); }
-    __device__ __forceinline__ int32_t* wptr() const { return reinterpret_cast<int32_t*>(kbg_smem + o_wptr); }
+    __device__ __forceinline__ uint64_t* pbits() const { return reinterpret_cast<uint64_t*>(kbg_smem + base + o_pbits); }
+    __device__ __forceinline__ Task* task() const { return reinterpret_cast<Task*>(kbg_smem + base + o_task); }
+    __device__ __forceinline__ int32_t* wptr() const { return reinterpret_cast<int32_t*>(kbg_smem + base + o_wptr); }
     // H: w[nspin][64];  rho: racc[nspin][acc_warps][64]
-    __device__ __forceinline__ double* acc() const { return reinterpret_cast<double*>(kbg_smem + o_acc); }
-    __device__ __forceinline__ double* phi() const { return reinterpret_cast<double*>(kbg_smem + o_phi); }
+    __device__ __forceinline__ double* acc() const { return reinterpret_cast<double*>(kbg_smem + base + o_acc); }
+    __device__ __forceinline__ double* phi() const { return reinterpret_cast<double*>(kbg_smem + base + o_phi); }
 };
 
 __host__ __device__ __forceinline__ size_t align16(size_t x) { return (x + 15) & ~static_cast<size_t>(15); }
@@ -137,18 +138,19 @@ __device__ __forceinline__ Smem carve(uint32_t base, const GridArgs& g, size_t a
     size_t off[12];
     buffer_layout(g, acc_doubles, off);
     Smem s;
-    s.o_meta = base + static_cast<uint32_t>(off[0]);
-    s.o_cov = base + static_cast<uint32_t>(off[1]);
-    s.o_grp = base + static_cast<uint32_t>(off[2]);
-    s.o_off2d = base + static_cast<uint32_t>(off[3]);
-    s.o_rcov = base + static_cast<uint32_t>(off[4]);
-    s.o_rorb = base + static_cast<uint32_t>(off[5]);
-    s.o_pom = base + static_cast<uint32_t>(off[6]);
-    s.o_pbits = base + static_cast<uint32_t>(off[7]);
-    s.o_task = base + static_cast<uint32_t>(off[8]);
-    s.o_wptr = base + static_cast<uint32_t>(off[9]);
-    s.o_acc = base + static_cast<uint32_t>(off[10]);
-    s.o_phi = base + static_cast<uint32_t>(off[11]);
+    s.base = base;
+    s.o_meta = static_cast<uint32_t>(off[0]);
+    s.o_cov = static_cast<uint32_t>(off[1]);
+    s.o_grp = static_cast<uint32_t>(off[2]);
+    s.o_off2d = static_cast<uint32_t>(off[3]);
+    s.o_rcov = static_cast<uint32_t>(off[4]);
+    s.o_rorb = static_cast<uint32_t>(off[5]);
+    s.o_pom = static_cast<uint32_t>(off[6]);
+    s.o_pbits = static_cast<uint32_t>(off[7]);
+    s.o_task = static_cast<uint32_t>(off[8]);
+    s.o_wptr = static_cast<uint32_t>(off[9]);
+    s.o_acc = static_cast<uint32_t>(off[10]);
+    s.o_phi = static_cast<uint32_t>(off[11]);
     return s;
 }
 

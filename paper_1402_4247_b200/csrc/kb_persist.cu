@@ -55,19 +55,27 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// Two buffers at byte offsets 0 and bsz of kbg_smem, then the mbarriers.
+// Buffer s is selected arithmetically (no dynamically indexed struct arrays,
+// which would live in local memory).
 struct Buffers {
-    Smem buf[2];
+    Smem sm0;
+    uint32_t bsz;
     uint64_t* full;   // [2]
     uint64_t* empty;  // [2]
+    __device__ __forceinline__ Smem buf(int s) const {
+        Smem x = sm0;
+        x.base = s ? bsz : 0u;
+        return x;
+    }
 };
 
 __device__ __forceinline__ Buffers carve_all(const GridArgs& g, size_t acc) {
     size_t off[12];
-    const uint32_t bsz = static_cast<uint32_t>(align16(buffer_layout(g, acc, off)));
     Buffers B;
-    B.buf[0] = carve(0u, g, acc);
-    B.buf[1] = carve(bsz, g, acc);
-    B.full = reinterpret_cast<uint64_t*>(kbg_smem + 2 * bsz);
+    B.bsz = static_cast<uint32_t>(align16(buffer_layout(g, acc, off)));
+    B.sm0 = carve(0u, g, acc);
+    B.full = reinterpret_cast<uint64_t*>(kbg_smem + 2 * B.bsz);
     B.empty = B.full + 2;
     return B;
 }
@@ -83,7 +91,7 @@ __device__ void producer(const GridArgs& g, const Buffers& B, int lane) {
     for (int k = 0;; ++k) {
         const int s = k & 1;
         if (k >= 2) mbar_wait(&B.empty[s], ((k >> 1) - 1) & 1);
-        const Smem& sm = B.buf[s];
+        const Smem sm = B.buf(s);
         int64_t b = -1;
         int ncov = 0;
         for (;;) {
@@ -142,7 +150,7 @@ __device__ void consumer(const GridArgs& g, const Buffers& B, int cw, int lane) 
     for (int k = 0;; ++k) {
         const int s = k & 1;
         mbar_wait(&B.full[s], (k >> 1) & 1);
-        const Smem& sm = B.buf[s];
+        const Smem sm = B.buf(s);
         const int64_t b = sm.meta()->block;
         if (b < 0) return;
         const int ncov = sm.meta()->ncov;
