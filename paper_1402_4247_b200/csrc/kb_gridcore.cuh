@@ -11,8 +11,8 @@
 // H task (group g, partner cj >= first(g)): C(16 x 8*TN) += Phi_g diag(V dV)
 //   Phi_cj^T over the common 1x2x2 quads with mma.sync.m8n8k4.f64 (SASS
 //   DMMA); canonical rows (cover ci <= cj) are scattered with FP64 atomics.
-// rho task (group g, octet half h): Y(16 x 8 slots) += D'(16 x n_cj)
-//   Phi_cj(n_cj x 8) over all partners cj >= first(g) in registers, D' =
+// rho task (group g, octet half h, partner range): Y(16 x 8 slots) +=
+//   D'(16 x n_cj) Phi_cj(n_cj x 8) over the partners cj in the range in registers, D' =
 //   repacked DM (x2 off the (a,a,0) blocks: the symmetric half), then
 //   rho(slot) += sum_rows Phi_g * Y once per task.
 #pragma once
@@ -416,8 +416,8 @@ __device__ __forceinline__ void rho_partner(const double* __restrict__ pb, int s
 }
 
 template <int TM>
-__device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, const double* __restrict__ Dr,
-                              double* __restrict__ racc, int lane) {
+__device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, int cbeg, int cend,
+                              const double* __restrict__ Dr, double* __restrict__ racc, int lane) {
     const GroupS& G = sm.grp()[gi];
     const int rend = G.row0 + G.rows;
     int rci[TM], rri[TM];
@@ -433,7 +433,7 @@ __device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, 
 #pragma unroll
         for (int o = 0; o < 4; ++o) y[t][o][0] = y[t][o][1] = 0.0;
     const uint8_t* pom = sm.pom() + gi * ncov;
-    uint64_t bits = sm.pbits()[2 * gi + h];
+    uint64_t bits = sm.pbits()[2 * gi + h] & (~0ull << cbeg) & (cend >= 64 ? ~0ull : ((1ull << cend) - 1ull));
     const int colbase = 32 * h + (lane >> 2);
     double nxt[TM][4];
     if (bits) gather_a<TM>(sm, ncov, rci, rri, __ffsll(bits) - 1, 0, Dr, lane, nxt);
@@ -489,9 +489,9 @@ __device__ __forceinline__ void rho_task(const Smem& sm, int ncov, const Task& t
     const GroupS& G = sm.grp()[t.g];
     for (int i0 = 0; i0 < G.tm; i0 += 2) {
         if (G.tm - i0 >= 2)
-            rho_task_rows<2>(sm, ncov, t.g, G.row0 + 8 * i0, t.half, Dr, racc, lane);
+            rho_task_rows<2>(sm, ncov, t.g, G.row0 + 8 * i0, t.half, t.cj, t.qmask, Dr, racc, lane);
         else
-            rho_task_rows<1>(sm, ncov, t.g, G.row0 + 8 * i0, t.half, Dr, racc, lane);
+            rho_task_rows<1>(sm, ncov, t.g, G.row0 + 8 * i0, t.half, t.cj, t.qmask, Dr, racc, lane);
     }
 }
 

@@ -40,7 +40,7 @@ __device__ __forceinline__ uint16_t sat16(int64_t c) { return static_cast<uint16
 __global__ void k_tasks(SysParams P, int64_t nblock, const int32_t* __restrict__ blk_ptr,
                         const int32_t* __restrict__ cov_atom, const uint64_t* __restrict__ cov_mask, int64_t* hcnt,
                         int64_t* rcnt, const int64_t* __restrict__ hptr, const int64_t* __restrict__ rptr, Task* hout,
-                        Task* rout, TaskStats* st, int32_t* rows_out) {
+                        Task* rout, TaskStats* st, int32_t* rows_out, int W) {
     const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (b >= nblock) return;
     const int c0 = blk_ptr[b];
@@ -75,27 +75,49 @@ __global__ void k_tasks(SysParams P, int64_t nblock, const int32_t* __restrict__
             }
             ++nh;
         }
+    }
+    // rho tasks: (group, octet half, partner range). Ranges split the partner
+    // list so no task exceeds ~1/3 of a warp's average share of the block,
+    // which keeps the LPT schedule balanced over W warps.
+    int64_t rtotal = 0;
+    for (int g = 0; g < ng; ++g)
+        for (int cj = g_first[g]; cj < ncov; ++cj) {
+            uint32_t om = 0;
+            for (int ci = g_first[g]; ci < g_end[g] && ci <= cj; ++ci)
+                om |= octets_of(cov_mask[c0 + ci] & cov_mask[c0 + cj]);
+            rtotal += __popc(om) * ((g_rows[g] + 7) >> 3) * ((norb[cj] + 3) >> 2);
+        }
+    const int64_t target = rtotal / (3 * W) > 16 ? rtotal / (3 * W) : 16;
+    for (int g = 0; g < ng; ++g) {
+        const int tm = (g_rows[g] + 7) >> 3;
         for (int h = 0; h < 2; ++h) {
             int64_t cost = 0;
+            int start = -1;
             for (int cj = g_first[g]; cj < ncov; ++cj) {
                 const uint64_t mj = cov_mask[c0 + cj];
                 uint32_t om = 0;
                 for (int ci = g_first[g]; ci < g_end[g] && ci <= cj; ++ci) om |= octets_of(cov_mask[c0 + ci] & mj);
                 om &= 0xFu << (4 * h);
-                cost += __popc(om) * tm * ((norb[cj] + 3) >> 2);
+                if (om) {
+                    if (start < 0) start = cj;
+                    cost += __popc(om) * tm * ((norb[cj] + 3) >> 2);
+                }
+                if (start >= 0 && (cost >= target || cj + 1 == ncov)) {
+                    if (rout) {
+                        Task t;
+                        t.g = static_cast<uint8_t>(g);
+                        t.cj = static_cast<uint8_t>(start);  // partner range [cj, qmask)
+                        t.half = static_cast<uint8_t>(h);
+                        t.pad_ = 0;
+                        t.qmask = static_cast<uint16_t>(cj + 1);
+                        t.cost = sat16(cost + 8);
+                        rout[rptr[b] + nr] = t;
+                    }
+                    ++nr;
+                    cost = 0;
+                    start = -1;
+                }
             }
-            if (!cost) continue;
-            if (rout) {
-                Task t;
-                t.g = static_cast<uint8_t>(g);
-                t.cj = 0;
-                t.half = static_cast<uint8_t>(h);
-                t.pad_ = 0;
-                t.qmask = 0;
-                t.cost = sat16(cost + 8);
-                rout[rptr[b] + nr] = t;
-            }
-            ++nr;
         }
     }
     if (rows_out) rows_out[b] = ng ? g_row0[ng - 1] + g_rows[ng - 1] : 0;
@@ -177,7 +199,7 @@ void build_tasks_device(const SysParams& P, DevIndex& ix, int task_warps, cudaSt
     KBG_CUDA(cudaMemsetAsync(d_st, 0, sizeof(TaskStats), st));
     if (!ix.blk_rows) ix.blk_rows = talloc<int32_t>(nb);
     k_tasks<<<grid, T, 0, st>>>(P, nb, ix.blk_ptr, ix.cov_atom, ix.cov_mask, hcnt, rcnt, nullptr, nullptr, nullptr,
-                                nullptr, d_st, ix.blk_rows);
+                                nullptr, d_st, ix.blk_rows, task_warps);
     KBG_CUDA(cudaGetLastError());
     ix.ht_ptr = talloc<int64_t>(nb + 1);
     ix.rt_ptr = talloc<int64_t>(nb + 1);
@@ -186,7 +208,7 @@ void build_tasks_device(const SysParams& P, DevIndex& ix, int task_warps, cudaSt
     Task* htmp = talloc<Task>(ix.nhtask);
     Task* rtmp = talloc<Task>(ix.nrtask);
     k_tasks<<<grid, T, 0, st>>>(P, nb, ix.blk_ptr, ix.cov_atom, ix.cov_mask, nullptr, nullptr, ix.ht_ptr, ix.rt_ptr,
-                                htmp, rtmp, d_st, nullptr);
+                                htmp, rtmp, d_st, nullptr, task_warps);
     KBG_CUDA(cudaGetLastError());
     ix.ht = talloc<Task>(ix.nhtask);
     ix.rt = talloc<Task>(ix.nrtask);
