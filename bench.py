@@ -208,7 +208,7 @@ def main():
     gp = GridPass(sysm, device=local, rank=rank, nranks=world)
     gp.set_option(1, args.warps)
     t_idx = time.perf_counter()
-    ix = gp.build_index()
+    ix = gp.build_index()  # index + task lists + geometry cache (Phi), once per geometry
     t_idx = time.perf_counter() - t_idx
     nspin = args.nspin
     dm_h = f.dm(ix, nspin=nspin)
@@ -223,21 +223,26 @@ def main():
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
     def step(ev=None):
+        n = 0
         if ev:
             ev[0].record(stream)
         gp.density_dev(d_dm, d_rho, stream)
+        n += gp.last_launches
         if ev:
             ev[1].record(stream)
         gp.hamiltonian_accumulate_dev(d_veff, f.dV, d_h, stream)
+        n += gp.last_launches
         if ev:
             ev[2].record(stream)
         gp.hamiltonian_mirror_dev(d_h, stream)
+        n += gp.last_launches
         if ev:
             ev[3].record(stream)
         if world > 1:
             dist.all_reduce(d_h)
         if ev:
             ev[4].record(stream)
+        return n
 
     if args.profile:
         for _ in range(2):
@@ -260,8 +265,7 @@ def main():
     with ClockSampler(local) as clk:
         for k in range(args.steps):
             flush.zero_()  # L2 flush between timed iterations (outside the events)
-            step(evs[k])
-            launches += 3
+            launches += step(evs[k])
         torch.cuda.synchronize()
         # the timed region is shorter than nvidia-smi's sampling period: keep the
         # same workload running (untimed) until 3 samples exist
