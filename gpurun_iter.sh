@@ -8,4 +8,4 @@ timeout 300 python bench.py --profile --no-e2e > gpurun_out/plain_$tag.log 2>&1 
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_density|k_hamiltonian|k_persist" -c 2 -o gpurun_out/prof_$tag python bench.py --profile --no-e2e > gpurun_out/ncu_$tag.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/ncu_$tag.log
 fi
-tail -2 gpurun_out/pytest_gpu_$tag.log; cat gpurun_out/kernel_times_$tag.log
+tail -n 2 gpurun_out/pytest_gpu_$tag.log; cat gpurun_out/kernel_times_$tag.log
