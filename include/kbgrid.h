@@ -169,6 +169,12 @@ int kbg_block_orbitals(kbg_ctx* ctx, int64_t block, double* out, int64_t cap, in
  * kbg_hamiltonian_dev call (evidence for gpu_launches). */
 int kbg_last_launches(const kbg_ctx* ctx);
 
+/* Persistent-kernel timing counters (clock64 cycles summed over warps/CTAs
+ * since the last KBG_OPT_DEBUG_COUNTERS reset): [0] producer wait on empty,
+ * [1] producer total, [2] consumer wait on full, [3] consumer wait at the end,
+ * [4] consumer total, [5] blocks seen by consumers. Profiling aid. */
+int kbg_debug_counters(kbg_ctx* ctx, int64_t* out, int n);
+
 /* Work tally of the last density / hamiltonian call. */
 int kbg_last_tally(const kbg_ctx* ctx, kbg_tally* out);
 
@@ -177,6 +183,7 @@ int kbg_last_tally(const kbg_ctx* ctx, kbg_tally* out);
 #define KBG_OPT_FAULT_SIGN 2 /* test hook: flip the sign of the H accumulate (kband fault_proc6_sign analogue) */
 #define KBG_OPT_SCATTER_STORE 3 /* timing experiment: plain stores instead of atomics (H is WRONG) */
 #define KBG_OPT_PERSIST 4 /* 1 (default): persistent warp-specialized kernels when they fit; 0: one CTA per block */
+#define KBG_OPT_DEBUG_COUNTERS 5 /* nonzero: enable + reset the persistent kernels' timing counters */
 int kbg_set_option(kbg_ctx* ctx, int option, int64_t value);
 
 const char* kbg_last_error(const kbg_ctx* ctx);

@@ -27,6 +27,7 @@ KBG_OPT_WARPS = 1
 KBG_OPT_FAULT_SIGN = 2
 KBG_OPT_SCATTER_STORE = 3
 KBG_OPT_PERSIST = 4
+KBG_OPT_DEBUG_COUNTERS = 5
 KBG_CELL_PRIMITIVE = 0
 KBG_CELL_CUBIC = 1
 
@@ -103,6 +104,7 @@ KBGRID_SYMBOLS = [
     ("kbg_block_orbitals", _I, [_P, _I64, _DP, _I64, C.POINTER(_I)]),
     ("kbg_last_launches", _I, [_P]),
     ("kbg_last_tally", _I, [_P, C.POINTER(kbg_tally)]),
+    ("kbg_debug_counters", _I, [_P, C.POINTER(C.c_int64), _I]),
     ("kbg_set_option", _I, [_P, _I, _I64]),
     ("kbg_last_error", C.c_char_p, [_P]),
     ("kbg_status_string", C.c_char_p, [_I]),

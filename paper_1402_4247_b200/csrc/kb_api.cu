@@ -28,6 +28,7 @@ struct kbg_ctx {
     int* d_counter = nullptr;  // persistent work counter
     double sign = 1.0;
     int scatter = 0;
+    unsigned long long* d_dbg = nullptr;  // KBG_OPT_DEBUG_COUNTERS
     cudaStream_t stream = nullptr;
     double* d_in = nullptr;
     size_t cap_in = 0;
@@ -192,6 +193,7 @@ kbg::GridArgs grid_args(kbg_ctx* c, int nspin, double dV, const double* in, doub
     g.dV = dV;
     g.sign = c->sign;
     g.scatter = c->scatter;
+    g.dbg = c->d_dbg;
     g.in = in;
     g.out = out;
     if (g.max_cover > 32 * c->nwarps || g.max_cover > kbg::kMaxCoverPerBlock)
@@ -492,6 +494,16 @@ int kbg_block_orbitals(kbg_ctx* c, int64_t block, double* out, int64_t cap, int*
 
 int kbg_last_launches(const kbg_ctx* c) { return c ? c->last_launches : 0; }
 
+int kbg_debug_counters(kbg_ctx* c, int64_t* out, int n) {
+    if (!c || !out || n < 0) return KBG_ERR_CONFIG;
+    for (int i = 0; i < n; ++i) out[i] = 0;
+    if (!c->d_dbg) return KBG_OK;
+    unsigned long long h[16];
+    if (cudaMemcpy(h, c->d_dbg, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return KBG_ERR_CUDA;
+    for (int i = 0; i < n && i < 16; ++i) out[i] = static_cast<int64_t>(h[i]);
+    return KBG_OK;
+}
+
 int kbg_last_tally(const kbg_ctx* c, kbg_tally* out) {
     if (!c || !out) return KBG_ERR_CONFIG;
     *out = c->tally;
@@ -517,6 +529,12 @@ int kbg_set_option(kbg_ctx* c, int option, int64_t value) {
         case KBG_OPT_PERSIST:
             c->persist = value ? 1 : 0;
             return KBG_OK;
+        case KBG_OPT_DEBUG_COUNTERS:
+            if (value && !c->d_dbg) {
+                if (cudaMalloc(&c->d_dbg, 16 * sizeof(unsigned long long)) != cudaSuccess) return KBG_ERR_CUDA;
+            }
+            if (c->d_dbg) cudaMemset(c->d_dbg, 0, 16 * sizeof(unsigned long long));
+            return KBG_OK;
         default:
             c->err = "set_option: unknown option";
             return KBG_ERR_CONFIG;
@@ -537,6 +555,7 @@ void kbg_destroy(kbg_ctx* c) {
     if (c->d_check) cudaFree(c->d_check);
     if (c->d_dmr) cudaFree(c->d_dmr);
     if (c->d_counter) cudaFree(c->d_counter);
+    if (c->d_dbg) cudaFree(c->d_dbg);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }

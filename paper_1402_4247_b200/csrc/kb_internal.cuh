@@ -157,6 +157,7 @@ struct GridArgs {
     const int64_t* order;   // persistent kernels: block order
     int64_t norder;
     int* counter;           // persistent kernels: work counter (zeroed per launch)
+    unsigned long long* dbg;    // optional timing counters (KBG_OPT_DEBUG_COUNTERS), else nullptr
     const unsigned char* tabs;  // geometry cache: this kernel's table images
     int64_t tab_bytes;
     const double* phis;

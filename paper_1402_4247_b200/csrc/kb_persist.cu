@@ -88,9 +88,14 @@ __host__ __device__ inline size_t persist_bytes(const GridArgs& g, bool density)
 
 template <bool DENSITY>
 __device__ void producer(const GridArgs& g, const Buffers& B, int lane) {
+    unsigned long long t_wait = 0, t0 = clock64();
     for (int k = 0;; ++k) {
         const int s = k & 1;
-        if (k >= 2) mbar_wait(&B.empty[s], ((k >> 1) - 1) & 1);
+        if (k >= 2) {
+            const unsigned long long tw = clock64();
+            mbar_wait(&B.empty[s], ((k >> 1) - 1) & 1);
+            t_wait += clock64() - tw;
+        }
         const Smem sm = B.buf(s);
         int64_t b = -1;
         int ncov = 0;
@@ -120,6 +125,10 @@ __device__ void producer(const GridArgs& g, const Buffers& B, int lane) {
             if (lane == 0) {
                 sm.meta()->block = -1;
                 mbar_arrive(&B.full[s]);
+                if (g.dbg) {
+                    atomicAdd(&g.dbg[0], t_wait);
+                    atomicAdd(&g.dbg[1], clock64() - t0);
+                }
             }
             return;
         }
@@ -147,12 +156,25 @@ __device__ void producer(const GridArgs& g, const Buffers& B, int lane) {
 
 template <bool DENSITY>
 __device__ void consumer(const GridArgs& g, const Buffers& B, int cw, int lane) {
+    unsigned long long t_wait = 0, t_tail = 0, t0 = clock64();
     for (int k = 0;; ++k) {
         const int s = k & 1;
+        const unsigned long long tw = clock64();
         mbar_wait(&B.full[s], (k >> 1) & 1);
+        const unsigned long long dw = clock64() - tw;
+        t_wait += dw;
         const Smem sm = B.buf(s);
         const int64_t b = sm.meta()->block;
-        if (b < 0) return;
+        if (b < 0) {
+            t_tail += dw;
+            if (g.dbg && lane == 0) {
+                atomicAdd(&g.dbg[2], t_wait);
+                atomicAdd(&g.dbg[3], t_tail);
+                atomicAdd(&g.dbg[4], clock64() - t0);
+                atomicAdd(&g.dbg[5], static_cast<unsigned long long>(k));
+            }
+            return;
+        }
         const int ncov = sm.meta()->ncov;
         for (int spin = 0; spin < g.nspin; ++spin) {
             if (DENSITY) {
