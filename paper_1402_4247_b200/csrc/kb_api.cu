@@ -523,8 +523,8 @@ int kbg_set_option(kbg_ctx* c, int option, int64_t value) {
         case KBG_OPT_FAULT_SIGN:
             c->sign = value ? -1.0 : 1.0;
             return KBG_OK;
-        case KBG_OPT_SCATTER_STORE:
-            c->scatter = value ? 1 : 0;
+        case KBG_OPT_SCATTER_STORE:  // bit 0: stores; bits 1-3: timing experiments (see kb_gridcore.cuh)
+            c->scatter = static_cast<int>(value & 15);
             return KBG_OK;
         case KBG_OPT_PERSIST:
             c->persist = value ? 1 : 0;

@@ -306,7 +306,7 @@ __device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict_
         const double wv = pw[col];
         double a[TM], bb[TN];
 #pragma unroll
-        for (int i = 0; i < TM; ++i) a[i] = pa[i * 512 + (col ^ sa)] * wv;
+        for (int i = 0; i < TM; ++i) a[i] = (scatter & 4) ? pa[i * 512 + (col ^ sa)] : pa[i * 512 + (col ^ sa)] * wv;
 #pragma unroll
         for (int j = 0; j < TN; ++j) bb[j] = pb[j * 512 + (col ^ sb)];
 #pragma unroll
@@ -340,8 +340,8 @@ __device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict_
                 const int col = cb0 + 8 * j + (lane & 3) * 2 + e;
                 double v = c[0][i][j][e];
                 if (NACC == 2) v += c[NACC - 1][i][j][e];
-                if (off >= 0 && col < nb) {
-                    if (scatter == 0)
+                if (off >= 0 && col < nb && !(scatter & 2)) {
+                    if (!(scatter & 1))
                         atomicAdd(H + off + ri * nb + col, sign * v);
                     else
                         H[off + ri * nb + col] = sign * v;
@@ -380,14 +380,16 @@ __device__ __forceinline__ void h_task(const Smem& sm, const double* w, int ncov
 // K-step values as two 16-byte loads.
 template <int TM>
 __device__ __forceinline__ void gather_a(const Smem& sm, int ncov, const int (&rci)[TM], const int (&rri)[TM], int cj,
-                                         int kc, const double* __restrict__ Dr, int lane, double (&a)[TM][4]) {
+                                         int kc, const double* __restrict__ Dr, int lane, double (&a)[TM][4],
+                                         int exp = 0) {
     const int stride = 16 * ((sm.cov()[cj].norb + 15) >> 4);
 #pragma unroll
     for (int t = 0; t < TM; ++t) {
         const int ci = rci[t];
         const int off = ci <= cj ? sm.off2d()[ci * ncov + cj] : -1;  // ci = kNoCover (255) fails ci <= cj
         if (off >= 0) {
-            const double2* p = reinterpret_cast<const double2*>(Dr + off + rri[t] * stride + 16 * kc + 4 * (lane & 3));
+            const double2* p = reinterpret_cast<const double2*>(
+                (exp & 8) ? Dr + 4 * (lane & 3) : Dr + off + rri[t] * stride + 16 * kc + 4 * (lane & 3));
             const double2 v0 = __ldg(p), v1 = __ldg(p + 1);
             a[t][0] = v0.x;
             a[t][1] = v0.y;
@@ -417,7 +419,7 @@ __device__ __forceinline__ void rho_partner(const double* __restrict__ pb, int s
 
 template <int TM>
 __device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, int cbeg, int cend,
-                              const double* __restrict__ Dr, double* __restrict__ racc, int lane) {
+                              const double* __restrict__ Dr, double* __restrict__ racc, int lane, int exp) {
     const GroupS& G = sm.grp()[gi];
     const int rend = G.row0 + G.rows;
     int rci[TM], rri[TM];
@@ -436,7 +438,7 @@ __device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, 
     uint64_t bits = sm.pbits()[2 * gi + h] & (~0ull << cbeg) & (cend >= 64 ? ~0ull : ((1ull << cend) - 1ull));
     const int colbase = 32 * h + (lane >> 2);
     double nxt[TM][4];
-    if (bits) gather_a<TM>(sm, ncov, rci, rri, __ffsll(bits) - 1, 0, Dr, lane, nxt);
+    if (bits) gather_a<TM>(sm, ncov, rci, rri, __ffsll(bits) - 1, 0, Dr, lane, nxt, exp);
     while (bits) {
         const int cj = __ffsll(bits) - 1;
         bits &= bits - 1;
@@ -448,9 +450,9 @@ __device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, 
 #pragma unroll
             for (int s = 0; s < 4; ++s) a[t][s] = nxt[t][s];
         const int nkc = (B.norb + 15) >> 4;
-        if (nkc == 1 && bits) gather_a<TM>(sm, ncov, rci, rri, __ffsll(bits) - 1, 0, Dr, lane, nxt);
+        if (nkc == 1 && bits) gather_a<TM>(sm, ncov, rci, rri, __ffsll(bits) - 1, 0, Dr, lane, nxt, exp);
         for (int kc = 0; kc < nkc; ++kc) {
-            if (kc > 0) gather_a<TM>(sm, ncov, rci, rri, cj, kc, Dr, lane, a);
+            if (kc > 0) gather_a<TM>(sm, ncov, rci, rri, cj, kc, Dr, lane, a, exp);
             const int ks = min(4, (B.norb - 16 * kc + 3) >> 2);
             const int rb = B.row0 + 16 * kc + (lane & 3);
             const double* pb = sm.phi() + rb * 64;
@@ -462,7 +464,7 @@ __device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, 
                 default: rho_partner<TM, 4>(pb, swb, om4, a, y, colbase); break;
             }
         }
-        if (nkc > 1 && bits) gather_a<TM>(sm, ncov, rci, rri, __ffsll(bits) - 1, 0, Dr, lane, nxt);
+        if (nkc > 1 && bits) gather_a<TM>(sm, ncov, rci, rri, __ffsll(bits) - 1, 0, Dr, lane, nxt, exp);
     }
     // rho(slot) += sum over rows of Phi_row(slot) * Y(row, slot)
 #pragma unroll
@@ -485,13 +487,13 @@ __device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, 
 }
 
 __device__ __forceinline__ void rho_task(const Smem& sm, int ncov, const Task& t, const double* Dr, double* racc,
-                                         int lane) {
+                                         int lane, int exp = 0) {
     const GroupS& G = sm.grp()[t.g];
     for (int i0 = 0; i0 < G.tm; i0 += 2) {
         if (G.tm - i0 >= 2)
-            rho_task_rows<2>(sm, ncov, t.g, G.row0 + 8 * i0, t.half, t.cj, t.qmask, Dr, racc, lane);
+            rho_task_rows<2>(sm, ncov, t.g, G.row0 + 8 * i0, t.half, t.cj, t.qmask, Dr, racc, lane, exp);
         else
-            rho_task_rows<1>(sm, ncov, t.g, G.row0 + 8 * i0, t.half, t.cj, t.qmask, Dr, racc, lane);
+            rho_task_rows<1>(sm, ncov, t.g, G.row0 + 8 * i0, t.half, t.cj, t.qmask, Dr, racc, lane, exp);
     }
 }
 

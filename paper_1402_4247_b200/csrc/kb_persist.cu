@@ -184,7 +184,7 @@ __device__ void consumer(const GridArgs& g, const Buffers& B, int cw, int lane) 
                 racc[lane + 32] = 0.0;
                 __syncwarp();
                 for (int w = cw; w < g.task_warps; w += NC)
-                    for (int e = sm.wptr()[w]; e < sm.wptr()[w + 1]; ++e) rho_task(sm, ncov, sm.task()[e], Dr, racc, lane);
+                    for (int e = sm.wptr()[w]; e < sm.wptr()[w + 1]; ++e) rho_task(sm, ncov, sm.task()[e], Dr, racc, lane, g.scatter);
             } else {
                 double* Hs = g.out + spin * g.nnz;
                 for (int w = cw; w < g.task_warps; w += NC)
