@@ -306,7 +306,7 @@ __device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict_
         const double wv = pw[col];
         double a[TM], bb[TN];
 #pragma unroll
-        for (int i = 0; i < TM; ++i) a[i] = (scatter & 4) ? pa[i * 512 + (col ^ sa)] : pa[i * 512 + (col ^ sa)] * wv;
+        for (int i = 0; i < TM; ++i) a[i] = pa[i * 512 + (col ^ sa)] * wv;
 #pragma unroll
         for (int j = 0; j < TN; ++j) bb[j] = pb[j * 512 + (col ^ sb)];
 #pragma unroll
@@ -437,21 +437,13 @@ __device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, 
     const uint8_t* pom = sm.pom() + gi * ncov;
     uint64_t bits = sm.pbits()[2 * gi + h] & (~0ull << cbeg) & (cend >= 64 ? ~0ull : ((1ull << cend) - 1ull));
     const int colbase = 32 * h + (lane >> 2);
-    double nxt[TM][4];
-    if (bits) gather_a<TM>(sm, ncov, rci, rri, __ffsll(bits) - 1, 0, Dr, lane, nxt, exp);
-    while (bits) {
-        const int cj = __ffsll(bits) - 1;
-        bits &= bits - 1;
+    // one partner: D' fragments in `a` (K chunk 0); more chunks for > 16 orbitals
+    auto process = [&](int cj, double (&a)[TM][4]) {
         const uint32_t om4 = (pom[cj] >> (4 * h)) & 0xFu;
         const CoverS& B = sm.cov()[cj];
-        double a[TM][4];
-#pragma unroll
-        for (int t = 0; t < TM; ++t)
-#pragma unroll
-            for (int s = 0; s < 4; ++s) a[t][s] = nxt[t][s];
         const int nkc = (B.norb + 15) >> 4;
-        if (nkc == 1 && bits) gather_a<TM>(sm, ncov, rci, rri, __ffsll(bits) - 1, 0, Dr, lane, nxt, exp);
         for (int kc = 0; kc < nkc; ++kc) {
+            // chunk kc > 0 overwrites `a` (the next partner is prefetched into the other buffer)
             if (kc > 0) gather_a<TM>(sm, ncov, rci, rri, cj, kc, Dr, lane, a, exp);
             const int ks = min(4, (B.norb - 16 * kc + 3) >> 2);
             const int rb = B.row0 + 16 * kc + (lane & 3);
@@ -464,26 +456,66 @@ __device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, 
                 default: rho_partner<TM, 4>(pb, swb, om4, a, y, colbase); break;
             }
         }
-        if (nkc > 1 && bits) gather_a<TM>(sm, ncov, rci, rri, __ffsll(bits) - 1, 0, Dr, lane, nxt, exp);
+    };
+    // partners two at a time with ping-pong fragment registers: the gather of
+    // the next partner is in flight while the current one is contracted
+    double a0[TM][4], a1[TM][4];
+    int c0 = bits ? __ffsll(bits) - 1 : -1;
+    if (c0 >= 0) {
+        bits &= bits - 1;
+        gather_a<TM>(sm, ncov, rci, rri, c0, 0, Dr, lane, a0, exp);
     }
-    // rho(slot) += sum over rows of Phi_row(slot) * Y(row, slot)
+    while (c0 >= 0) {
+        const int c1 = bits ? __ffsll(bits) - 1 : -1;
+        if (c1 >= 0) {
+            bits &= bits - 1;
+            gather_a<TM>(sm, ncov, rci, rri, c1, 0, Dr, lane, a1, exp);
+        }
+        process(c0, a0);
+        if (c1 < 0) break;
+        c0 = bits ? __ffsll(bits) - 1 : -1;
+        if (c0 >= 0) {
+            bits &= bits - 1;
+            gather_a<TM>(sm, ncov, rci, rri, c0, 0, Dr, lane, a0, exp);
+        }
+        process(c1, a1);
+    }
+    // rho(slot) += sum over rows of Phi_row(slot) * Y(row, slot): per-lane
+    // partial products v[j] (j = 2*octet + e), then a reduce-scatter over the
+    // 8 row lanes (xor 16, 8, 4) leaves lane l with the total of j = l >> 2.
+    double v[8];
 #pragma unroll
     for (int o = 0; o < 4; ++o) {
+        const int p = 8 * (4 * h + o) + 2 * (lane & 3);
+        v[2 * o] = v[2 * o + 1] = 0.0;
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const int p = 8 * (4 * h + o) + 2 * (lane & 3) + e;
-            double v = 0.0;
-#pragma unroll
-            for (int t = 0; t < TM; ++t) {
-                const int r = ra0 + 8 * t + (lane >> 2);
-                v += sm.phi()[phi_idx(r, p)] * y[t][o][e];
-            }
-            v += __shfl_xor_sync(0xffffffffu, v, 4);
-            v += __shfl_xor_sync(0xffffffffu, v, 8);
-            v += __shfl_xor_sync(0xffffffffu, v, 16);
-            if (lane < 4) racc[p] += v;
+        for (int t = 0; t < TM; ++t) {
+            const int r = ra0 + 8 * t + (lane >> 2);
+            const double2 f2 = *reinterpret_cast<const double2*>(sm.phi() + phi_idx(r, p));
+            v[2 * o] += f2.x * y[t][o][0];
+            v[2 * o + 1] += f2.y * y[t][o][1];
         }
     }
+    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+    double w4[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const double send = b4 ? v[i] : v[i + 4];
+        const double keep = b4 ? v[i + 4] : v[i];
+        w4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+    double w2[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double send = b3 ? w4[i] : w4[i + 2];
+        const double keep = b3 ? w4[i + 2] : w4[i];
+        w2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    const double send = b2 ? w2[0] : w2[1];
+    const double keep = b2 ? w2[1] : w2[0];
+    const double tot = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    const int j = lane >> 2;
+    racc[8 * (4 * h + (j >> 1)) + 2 * (lane & 3) + (j & 1)] += tot;
 }
 
 __device__ __forceinline__ void rho_task(const Smem& sm, int ncov, const Task& t, const double* Dr, double* racc,

@@ -77,7 +77,7 @@ __global__ void k_tasks(SysParams P, int64_t nblock, const int32_t* __restrict__
         }
     }
     // rho tasks: (group, octet half, partner range). Ranges split the partner
-    // list so no task exceeds ~1/3 of a warp's average share of the block,
+    // list so no task exceeds ~1/2 of a warp's average share of the block,
     // which keeps the LPT schedule balanced over W warps.
     int64_t rtotal = 0;
     for (int g = 0; g < ng; ++g)
@@ -87,7 +87,7 @@ __global__ void k_tasks(SysParams P, int64_t nblock, const int32_t* __restrict__
                 om |= octets_of(cov_mask[c0 + ci] & cov_mask[c0 + cj]);
             rtotal += __popc(om) * ((g_rows[g] + 7) >> 3) * ((norb[cj] + 3) >> 2);
         }
-    const int64_t target = rtotal / (3 * W) > 16 ? rtotal / (3 * W) : 16;
+    const int64_t target = rtotal / (2 * W) > 16 ? rtotal / (2 * W) : 16;
     for (int g = 0; g < ng; ++g) {
         const int tm = (g_rows[g] + 7) >> 3;
         for (int h = 0; h < 2; ++h) {
