@@ -153,3 +153,69 @@ def test_kernel_modes_agree(persist):
         c.gp.set_option(_abi.KBG_OPT_PERSIST, 1)
     assert normwise(rho, c.o.density(c.dm)) <= TOL
     assert normwise(h, c.o.hamiltonian(c.veff, c.f.dV)) <= TOL
+
+
+def test_sharded_contexts_sum_to_full():
+    """Two rank contexts on one GPU: disjoint rho shards and partial H sum to the full pass."""
+    from paper_1402_4247_b200.shard import block_costs, partition
+
+    c = case("primitive14_150Ry")
+    rho_full = c.gp.density(c.dm)
+    h_full = c.gp.hamiltonian(c.veff, c.f.dV)
+    parts = []
+    for r in range(2):
+        gp = GridPass(c.f.system, device=0, rank=r, nranks=2)
+        gp.build_index()
+        parts.append((gp.shard_range(), gp.density(c.dm), gp.hamiltonian(c.veff, c.f.dV)))
+    assert parts[0][0][0] == 0 and parts[0][0][1] == parts[1][0][0] and parts[1][0][1] == c.gix["nblock"]
+    assert [p[0] for p in parts] == partition(block_costs(c.gix, c.f.system.norb_of_atom()), 2)
+    rho = parts[0][1] + parts[1][1]
+    h = parts[0][2] + parts[1][2]
+    assert normwise(rho, rho_full) <= 1e-14
+    assert normwise(h, h_full) <= 1e-13
+
+
+def test_device_api_matches_host_api():
+    import torch
+
+    c = case("primitive14_150Ry", 2)
+    dev = torch.device("cuda", 0)
+    d_dm = torch.from_numpy(c.dm).to(dev)
+    d_v = torch.from_numpy(c.veff).to(dev)
+    rho = torch.empty((2, c.f.system.npts), dtype=torch.float64, device=dev)
+    h = torch.empty((2, c.gix["nnz"]), dtype=torch.float64, device=dev)
+    c.gp.density_dev(d_dm, rho)
+    c.gp.hamiltonian_dev(d_v, c.f.dV, h)
+    torch.cuda.synchronize()
+    assert np.array_equal(rho.cpu().numpy(), c.gp.density(c.dm))
+    assert normwise(h.cpu().numpy(), c.gp.hamiltonian(c.veff, c.f.dV)) <= 1e-14
+
+
+@pytest.mark.parametrize("name", ["sweep56_100Ry", "sweep56_250Ry"])
+def test_cutoff_sweep_parity(name):
+    """Config 5 (grid-cutoff sweep) end points: coarser and finer grids than configs[1]."""
+    c = case(name)
+    assert normwise(c.gp.density(c.dm), c.o.density(c.dm)) <= TOL
+    assert normwise(c.gp.hamiltonian(c.veff, c.f.dV), c.o.hamiltonian(c.veff, c.f.dV)) <= TOL
+
+
+def test_large_config_identities():
+    """448-atom 2x2x2 supercell at full size (config 3): size-independent properties --
+    electron-count identity sum rho dV = Tr(DM S) and H_ba(-R) = H_ab(R)^T."""
+    f = Fe3O4.config("super448_200Ry")
+    gp = GridPass(f.system)
+    ix = gp.build_index()
+    dm = f.dm(ix)
+    rho = gp.density(dm)[0]
+    S = gp.hamiltonian(np.ones((1, f.system.npts)), f.dV)[0]
+    norb = f.system.norb_of_atom()
+    off, mir = ix["pair_off"], ix["pair_mirror"]
+    tr = 0.0
+    for p in range(len(mir)):
+        na, nb = norb[ix["pair_a"][p]], norb[ix["pair_b"][p]]
+        q = mir[p]
+        Sq = S[off[q]:off[q + 1]].reshape(nb, na)
+        assert np.array_equal(S[off[p]:off[p + 1]].reshape(na, nb), Sq.T)
+        tr += np.sum(dm[0, off[p]:off[p + 1]].reshape(na, nb) * Sq.T)
+    ne = rho.sum() * f.dV
+    assert abs(ne - tr) <= 1e-10 * max(1.0, abs(ne))
