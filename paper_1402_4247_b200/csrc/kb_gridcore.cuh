@@ -281,8 +281,36 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int tid
 }
 
 // ---- H --------------------------------------------------------------------------
-// Output tile rows ra0 + [0, 8*TM) (group rows < rend) x columns cb0 + [0, 8*TN)
-// of cover cj. Tiles with <= 2 DMMAs per quad alternate two accumulator sets.
+// Scatter of one accumulated tile: rows ra0 + [0, 8*TM) (group rows < rend),
+// columns cb0 + [0, 8*TN) of cover cj; canonical rows (cover ci <= cj) only.
+template <int TM, int TN>
+__device__ __forceinline__ void h_scatter(const Smem& sm, const double (&c)[TM][TN][2], int ncov, int cj, int ra0,
+                                          int rend, int cb0, double* __restrict__ H, double sign, int scatter,
+                                          int lane) {
+    const int nb = sm.cov()[cj].norb;
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        const int r = ra0 + 8 * i + (lane >> 2);
+        const int ci = r < rend ? sm.rcov()[r] : kNoCover;
+        const int off = ci <= cj ? sm.off2d()[ci * ncov + cj] : -1;  // kNoCover (255) fails ci <= cj
+        const int ri = sm.rorb()[r];
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = cb0 + 8 * j + (lane & 3) * 2 + e;
+                if (off >= 0 && col < nb && !(scatter & 2)) {
+                    if (!(scatter & 1))
+                        atomicAdd(H + off + ri * nb + col, sign * c[i][j][e]);
+                    else
+                        H[off + ri * nb + col] = sign * c[i][j][e];
+                }
+            }
+    }
+}
+
+// One partner: C(8*TM x 8*TN) += Phi_rows diag(w) Phi_cj^T over the quads in
+// qm. Tiles with <= 2 DMMAs per quad alternate two accumulator sets.
 template <int TM, int TN>
 __device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict__ w, int ncov, int cj, int ra0,
                                        int rend, int cb0, uint32_t qm, double* __restrict__ H, double sign,
@@ -326,36 +354,105 @@ __device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict_
             step(0, q0);
         }
     }
-    const int nb = B.norb;
+    if (NACC == 2)
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) {
+                c[0][i][j][0] += c[NACC - 1][i][j][0];
+                c[0][i][j][1] += c[NACC - 1][i][j][1];
+            }
+    h_scatter<TM, TN>(sm, c[0], ncov, cj, ra0, rend, cb0, H, sign, scatter, lane);
+}
+
+// Two partners sharing the group's (w-scaled) A fragments: per quad of
+// q1 | q2 the A fragments are loaded and scaled once.
+template <int TM, int TN1, int TN2>
+__device__ __forceinline__ void h_tile2(const Smem& sm, const double* __restrict__ w, int ncov, int cj1, int cj2,
+                                        int ra0, int rend, uint32_t q1, uint32_t q2, double* __restrict__ H,
+                                        double sign, int scatter, int lane) {
+    double c1[TM][TN1][2], c2[TM][TN2][2];
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
-        const int r = ra0 + 8 * i + (lane >> 2);
-        const int ci = r < rend ? sm.rcov()[r] : kNoCover;
-        const int off = ci <= cj ? sm.off2d()[ci * ncov + cj] : -1;
-        const int ri = sm.rorb()[r];
 #pragma unroll
-        for (int j = 0; j < TN; ++j)
+        for (int j = 0; j < TN1; ++j) c1[i][j][0] = c1[i][j][1] = 0.0;
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int col = cb0 + 8 * j + (lane & 3) * 2 + e;
-                double v = c[0][i][j][e];
-                if (NACC == 2) v += c[NACC - 1][i][j][e];
-                if (off >= 0 && col < nb && !(scatter & 2)) {
-                    if (!(scatter & 1))
-                        atomicAdd(H + off + ri * nb + col, sign * v);
-                    else
-                        H[off + ri * nb + col] = sign * v;
-                }
-            }
+        for (int j = 0; j < TN2; ++j) c2[i][j][0] = c2[i][j][1] = 0.0;
     }
+    const int ra = ra0 + (lane >> 2);
+    const int rb1 = sm.cov()[cj1].row0 + (lane >> 2), rb2 = sm.cov()[cj2].row0 + (lane >> 2);
+    const double* pa = sm.phi() + ra * 64 + (lane & 3);
+    const double* pb1 = sm.phi() + rb1 * 64 + (lane & 3);
+    const double* pb2 = sm.phi() + rb2 * 64 + (lane & 3);
+    const int sa = swz(ra), sb1 = swz(rb1), sb2 = swz(rb2);
+    const double* pw = w + (lane & 3);
+    uint32_t qm = q1 | q2;
+    while (qm) {
+        const int q = __ffs(qm) - 1;
+        qm &= qm - 1;
+        const int col = 4 * q;
+        const double wv = pw[col];
+        double a[TM];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) a[i] = pa[i * 512 + (col ^ sa)] * wv;
+        if ((q1 >> q) & 1u) {
+            double bb[TN1];
+#pragma unroll
+            for (int j = 0; j < TN1; ++j) bb[j] = pb1[j * 512 + (col ^ sb1)];
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN1; ++j) dmma(c1[i][j], a[i], bb[j]);
+        }
+        if ((q2 >> q) & 1u) {
+            double bb[TN2];
+#pragma unroll
+            for (int j = 0; j < TN2; ++j) bb[j] = pb2[j * 512 + (col ^ sb2)];
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN2; ++j) dmma(c2[i][j], a[i], bb[j]);
+        }
+    }
+    h_scatter<TM, TN1>(sm, c1, ncov, cj1, ra0, rend, 0, H, sign, scatter, lane);
+    h_scatter<TM, TN2>(sm, c2, ncov, cj2, ra0, rend, 0, H, sign, scatter, lane);
+}
+
+template <int TM, int TN1>
+__device__ __forceinline__ void h_tile2_tn2(int tn2, const Smem& sm, const double* w, int ncov, int cj1, int cj2,
+                                            int ra0, int rend, uint32_t q1, uint32_t q2, double* H, double sign,
+                                            int scatter, int lane) {
+    if (tn2 == 2)
+        h_tile2<TM, TN1, 2>(sm, w, ncov, cj1, cj2, ra0, rend, q1, q2, H, sign, scatter, lane);
+    else
+        h_tile2<TM, TN1, 1>(sm, w, ncov, cj1, cj2, ra0, rend, q1, q2, H, sign, scatter, lane);
 }
 
 __device__ __forceinline__ void h_task(const Smem& sm, const double* w, int ncov, const Task& t, double* H,
                                        double sign, int scatter, int lane) {
     const GroupS& G = sm.grp()[t.g];
+    const int rend = G.row0 + G.rows;
+    if (t.cj2 != 0xFF) {  // paired partners: group <= 16 rows, partners <= 16 orbitals
+        const int tn1 = (sm.cov()[t.cj].norb + 7) >> 3, tn2 = (sm.cov()[t.cj2].norb + 7) >> 3;
+        if (G.tm == 2) {
+            if (tn1 == 2)
+                h_tile2_tn2<2, 2>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, t.qmask, t.qmask2, H, sign, scatter,
+                                  lane);
+            else
+                h_tile2_tn2<2, 1>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, t.qmask, t.qmask2, H, sign, scatter,
+                                  lane);
+        } else {
+            if (tn1 == 2)
+                h_tile2_tn2<1, 2>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, t.qmask, t.qmask2, H, sign, scatter,
+                                  lane);
+            else
+                h_tile2_tn2<1, 1>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, t.qmask, t.qmask2, H, sign, scatter,
+                                  lane);
+        }
+        return;
+    }
     const int nb = sm.cov()[t.cj].norb;
     const uint32_t qm = t.qmask;
-    const int rend = G.row0 + G.rows;
     for (int i0 = 0; i0 < G.tm; i0 += 2) {
         const int tm = min(2, G.tm - i0);
         for (int j0 = 0; j0 < (nb + 7) >> 3; j0 += 2) {

@@ -66,15 +66,19 @@ struct BPair {
 };
 
 // One warp task of a grid block. H: rows of group g x columns of cover cj over
-// the quads in qmask. rho: rows of group g, octets of half `half`, partners
-// cj >= first cover of g.
+// the quads in qmask, and optionally of a second cover cj2 (quads qmask2;
+// cj2 = 0xFF: none) sharing the group's A fragments. rho: rows of group g,
+// octet half `half`, partner covers in [cj, qmask).
 struct Task {
     uint8_t g;
     uint8_t cj;
     uint8_t half;
-    uint8_t pad_;
+    uint8_t pad_;  // LPT warp during the build
     uint16_t qmask;
     uint16_t cost;
+    uint8_t cj2;
+    uint8_t pad2_;
+    uint16_t qmask2;
 };
 
 struct Candidate {

@@ -36,16 +36,23 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
                  "r"(bytes)
                  : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
     asm volatile(
         "{\n"
         " .reg .pred p;\n"
-        " WAIT:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
-        " @!p bra WAIT;\n"
-        "}" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 100000;\n"
+        " selp.u32 %0, 1, 0, p;\n"
+        "}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
+    return ok != 0;
+}
+// Waits for the phase with the given parity; sleeps `ns` between attempts so
+// a waiting warp does not take issue slots from the working ones.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, unsigned ns = 32) {
+    while (!mbar_try(bar, parity)) __nanosleep(ns);
 }
 // TMA bulk copy global -> shared, completing `bytes` on the mbarrier.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -93,7 +100,7 @@ __device__ void producer(const GridArgs& g, const Buffers& B, int lane) {
         const int s = k & 1;
         if (k >= 2) {
             const unsigned long long tw = clock64();
-            mbar_wait(&B.empty[s], ((k >> 1) - 1) & 1);
+            mbar_wait(&B.empty[s], ((k >> 1) - 1) & 1, 256);
             t_wait += clock64() - tw;
         }
         const Smem sm = B.buf(s);

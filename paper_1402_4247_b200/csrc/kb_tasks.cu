@@ -58,23 +58,49 @@ __global__ void k_tasks(SysParams P, int64_t nblock, const int32_t* __restrict__
     int64_t nh = 0, nr = 0;
     for (int g = 0; g < ng; ++g) {
         const int tm = (g_rows[g] + 7) >> 3;
+        // H: partners with common quads, paired consecutively when both have
+        // <= 16 orbitals and the group <= 16 rows (the pair shares A fragments)
+        int pend = -1;
+        uint32_t pend_q = 0;
+        auto emit = [&](int c1, uint32_t q1, int c2, uint32_t q2) {
+            if (hout) {
+                Task t;
+                t.g = static_cast<uint8_t>(g);
+                t.cj = static_cast<uint8_t>(c1);
+                t.half = 0;
+                t.pad_ = 0;
+                t.qmask = static_cast<uint16_t>(q1);
+                int64_t cost = static_cast<int64_t>(__popc(q1)) * tm * ((norb[c1] + 7) >> 3) + 2;
+                t.cj2 = 0xFF;
+                t.pad2_ = 0;
+                t.qmask2 = 0;
+                if (c2 >= 0) {
+                    t.cj2 = static_cast<uint8_t>(c2);
+                    t.qmask2 = static_cast<uint16_t>(q2);
+                    cost += static_cast<int64_t>(__popc(q2)) * tm * ((norb[c2] + 7) >> 3) + 1;
+                }
+                t.cost = sat16(cost);
+                hout[hptr[b] + nh] = t;
+            }
+            ++nh;
+        };
         for (int cj = g_first[g]; cj < ncov; ++cj) {
             const uint64_t mj = cov_mask[c0 + cj];
             uint32_t qm = 0;
             for (int ci = g_first[g]; ci < g_end[g] && ci <= cj; ++ci) qm |= quads_of(cov_mask[c0 + ci] & mj);
             if (!qm) continue;
-            if (hout) {
-                Task t;
-                t.g = static_cast<uint8_t>(g);
-                t.cj = static_cast<uint8_t>(cj);
-                t.half = 0;
-                t.pad_ = 0;
-                t.qmask = static_cast<uint16_t>(qm);
-                t.cost = sat16(__popc(qm) * tm * ((norb[cj] + 7) >> 3) + 2);
-                hout[hptr[b] + nh] = t;
+            const bool pairable = g_rows[g] <= 16 && norb[cj] <= 16;
+            if (!pairable) {
+                emit(cj, qm, -1, 0);
+            } else if (pend < 0) {
+                pend = cj;
+                pend_q = qm;
+            } else {
+                emit(pend, pend_q, cj, qm);
+                pend = -1;
             }
-            ++nh;
         }
+        if (pend >= 0) emit(pend, pend_q, -1, 0);
     }
     // rho tasks: (group, octet half, partner range). Ranges split the partner
     // list so no task exceeds ~1/2 of a warp's average share of the block,
@@ -111,6 +137,9 @@ __global__ void k_tasks(SysParams P, int64_t nblock, const int32_t* __restrict__
                         t.pad_ = 0;
                         t.qmask = static_cast<uint16_t>(cj + 1);
                         t.cost = sat16(cost + 8);
+                        t.cj2 = 0xFF;
+                        t.pad2_ = 0;
+                        t.qmask2 = 0;
                         rout[rptr[b] + nr] = t;
                     }
                     ++nr;
