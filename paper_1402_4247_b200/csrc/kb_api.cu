@@ -210,17 +210,32 @@ int run_density(kbg_ctx* c, int nspin, const double* d_dm, double* d_rho, cudaSt
     int n = kbg::launch_dm_repack(c->ix, c->P, nspin, d_dm, c->d_dmr, st);
     kbg::GridArgs g = grid_args(c, nspin, 0.0, d_dm, d_rho, true);
     g.dmr = c->d_dmr;
-    if (c->persist_ok && c->persist && c->ix.phis && kbg::persist_fits(g, true))
-        n += kbg::launch_density_persist(g, st);
-    else
-        n += kbg::launch_density(g, c->blk_end - c->blk_begin, c->nwarps, st);
-    return n;
+    if (c->persist_ok && c->persist && c->ix.phis) {
+        if (kbg::persist_fits(g, true)) return n + kbg::launch_density_persist(g, st);
+        // accumulators for every spin do not fit: one persistent launch per spin
+        for (int s = 0; s < nspin; ++s) {
+            kbg::GridArgs g1 = grid_args(c, 1, 0.0, d_dm + s * c->ix.nnz, d_rho + s * c->npts, true);
+            g1.dmr = c->d_dmr + s * c->ix.nrep;
+            if (!kbg::persist_fits(g1, true)) break;
+            n += kbg::launch_density_persist(g1, st);
+            if (s + 1 == nspin) return n;
+        }
+    }
+    return n + kbg::launch_density(g, c->blk_end - c->blk_begin, c->nwarps, st);
 }
 
 int run_hamiltonian(kbg_ctx* c, int nspin, double dV, const double* d_veff, double* d_h, cudaStream_t st) {
     const kbg::GridArgs g = grid_args(c, nspin, dV, d_veff, d_h, false);
-    if (c->persist_ok && c->persist && c->ix.phis && kbg::persist_fits(g, false))
-        return kbg::launch_hamiltonian_persist(g, st);
+    if (c->persist_ok && c->persist && c->ix.phis) {
+        if (kbg::persist_fits(g, false)) return kbg::launch_hamiltonian_persist(g, st);
+        int n = 0;
+        for (int s = 0; s < nspin; ++s) {
+            const kbg::GridArgs g1 = grid_args(c, 1, dV, d_veff + s * c->npts, d_h + s * c->ix.nnz, false);
+            if (!kbg::persist_fits(g1, false)) break;
+            n += kbg::launch_hamiltonian_persist(g1, st);
+            if (s + 1 == nspin) return n;
+        }
+    }
     return kbg::launch_hamiltonian(g, c->blk_end - c->blk_begin, c->nwarps, st);
 }
 
