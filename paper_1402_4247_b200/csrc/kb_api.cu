@@ -174,7 +174,7 @@ kbg::GridArgs grid_args(kbg_ctx* c, int nspin, double dV, const double* in, doub
     g.max_rows = c->ix.max_rows_padded + 8;
     g.max_cover = c->ix.max_cover > 0 ? c->ix.max_cover : 1;
     g.max_bpairs = c->ix.max_bpairs > 0 ? c->ix.max_bpairs : 1;
-    g.task_warps = c->ix.task_warps;
+    g.task_warps = density ? c->ix.rtask_warps : c->ix.htask_warps;
     g.order = c->ix.order;
     g.norder = c->ix.norder;
     g.counter = c->d_counter;
@@ -319,7 +319,7 @@ int kbg_build_index(kbg_ctx* c) {
         c->built = false;
         c->hix = kbg::HostIndex();
         kbg::build_index_device(c->P, c->ix, c->stream);
-        kbg::build_tasks_device(c->P, c->ix, kbg::kPersistConsumers, c->stream);
+        kbg::build_tasks_device(c->P, c->ix, kbg::kPersistConsumersH, kbg::kPersistConsumersR, c->stream);
         shard(c);
         c->built = true;
         {
@@ -327,7 +327,7 @@ int kbg_build_index(kbg_ctx* c) {
             const kbg::GridArgs gh = grid_args(c, 1, 0.0, nullptr, nullptr, false);
             c->persist_ok = kbg::persist_fits(gd, true) && kbg::persist_fits(gh, false);
         }
-        if (!c->persist_ok) kbg::build_tasks_device(c->P, c->ix, 8, c->stream);
+        if (!c->persist_ok) kbg::build_tasks_device(c->P, c->ix, 8, 8, c->stream);
         // owned blocks, heaviest first, for the persistent kernels' work counter
         std::vector<int64_t> cost(c->ix.nblock);
         KBG_CUDA(cudaMemcpy(cost.data(), c->ix.blk_cost, cost.size() * sizeof(int64_t), cudaMemcpyDeviceToHost));

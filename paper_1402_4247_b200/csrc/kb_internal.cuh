@@ -117,7 +117,7 @@ struct DevIndex {
     int64_t nhtask = 0, nrtask = 0;
     int max_rows_padded = 0;  // max Phi rows of a block (groups padded to 8-row tiles)
     int max_htask = 0, max_rtask = 0;
-    int task_warps = 0;         // warps the task lists are LPT-balanced over
+    int htask_warps = 0, rtask_warps = 0;  // warps the H / rho task lists are LPT-balanced over
     int32_t* blk_rows = nullptr;  // Phi rows of each block (without the 8 tail rows)
     // geometry cache (kb_cache.cu): per block the H / rho table images
     // (table_bytes each) and Phi ((rows + 8) x 64 doubles at phi_off[b])
@@ -189,7 +189,7 @@ void copy_index_to_host(const DevIndex& ix, HostIndex& h, cudaStream_t st);
 // Grid kernels (kb_grid.cu). Return number of kernel launches.
 size_t grid_smem_bytes(const GridArgs& g, int nwarps, bool density);
 // Task lists (kb_tasks.cu), built after the index.
-void build_tasks_device(const SysParams& sys, DevIndex& ix, int task_warps, cudaStream_t st);
+void build_tasks_device(const SysParams& sys, DevIndex& ix, int h_warps, int r_warps, cudaStream_t st);
 void free_tasks(DevIndex& ix);
 int launch_density(const GridArgs& g, int64_t nblk_owned, int nwarps, cudaStream_t st);
 int launch_hamiltonian(const GridArgs& g, int64_t nblk_owned, int nwarps, cudaStream_t st);
@@ -200,7 +200,8 @@ int launch_dm_repack(const DevIndex& ix, const SysParams& sys, int nspin, const 
 // on block k (two shared-memory buffers). persist_fits() says whether two
 // buffers fit in shared memory for this index.
 constexpr int kPersistProducers = 1;
-constexpr int kPersistConsumers = 15;
+constexpr int kPersistConsumersR = 15;  // rho: 16 warps (128 registers per thread)
+constexpr int kPersistConsumersH = 19;  // H: 20 warps (<= 102 registers per thread)
 // Geometry cache (kb_cache.cu): Phi and the per-block tables, built once per
 // geometry after the task lists.
 void build_cache_device(GridArgs gh, GridArgs gr, DevIndex& ix, cudaStream_t st);

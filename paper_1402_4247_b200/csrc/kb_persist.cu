@@ -19,8 +19,11 @@ namespace {
 
 using namespace core;
 
-constexpr int NC = kPersistConsumers;
-constexpr int NT = (kPersistProducers + NC) * 32;
+template <bool DENSITY>
+struct Cfg {
+    static constexpr int NC = DENSITY ? kPersistConsumersR : kPersistConsumersH;
+    static constexpr int NT = (kPersistProducers + NC) * 32;
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -89,7 +92,7 @@ __device__ __forceinline__ Buffers carve_all(const GridArgs& g, size_t acc) {
 
 __host__ __device__ inline size_t persist_bytes(const GridArgs& g, bool density) {
     size_t off[12];
-    const size_t acc = static_cast<size_t>(g.nspin) * 64 * (density ? NC : 1);
+    const size_t acc = static_cast<size_t>(g.nspin) * 64 * (density ? kPersistConsumersR : 1);
     return 2 * align16(buffer_layout(g, acc, off)) + 64;
 }
 
@@ -163,6 +166,7 @@ __device__ void producer(const GridArgs& g, const Buffers& B, int lane) {
 
 template <bool DENSITY>
 __device__ void consumer(const GridArgs& g, const Buffers& B, int cw, int lane) {
+    constexpr int NC = Cfg<DENSITY>::NC;
     unsigned long long t_wait = 0, t_tail = 0, t0 = clock64();
     for (int k = 0;; ++k) {
         const int s = k & 1;
@@ -228,8 +232,8 @@ __device__ void consumer(const GridArgs& g, const Buffers& B, int cw, int lane) 
 }
 
 template <bool DENSITY>
-__global__ void __launch_bounds__(NT, 1) k_persist(GridArgs g) {
-    const size_t acc = static_cast<size_t>(g.nspin) * 64 * (DENSITY ? NC : 1);
+__global__ void __launch_bounds__(Cfg<DENSITY>::NT, 1) k_persist(GridArgs g) {
+    const size_t acc = static_cast<size_t>(g.nspin) * 64 * (DENSITY ? Cfg<DENSITY>::NC : 1);
     const Buffers B = carve_all(g, acc);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
@@ -262,10 +266,10 @@ int launch_persist(const GridArgs& g, bool density, cudaStream_t st) {
     KBG_CUDA(cudaMemsetAsync(g.counter, 0, sizeof(int), st));
     if (density) {
         set_smem(k_persist<true>, smem);
-        k_persist<true><<<grid, NT, smem, st>>>(g);
+        k_persist<true><<<grid, Cfg<true>::NT, smem, st>>>(g);
     } else {
         set_smem(k_persist<false>, smem);
-        k_persist<false><<<grid, NT, smem, st>>>(g);
+        k_persist<false><<<grid, Cfg<false>::NT, smem, st>>>(g);
     }
     KBG_CUDA(cudaGetLastError());
     return 1;

@@ -214,9 +214,10 @@ void free_tasks(DevIndex& ix) {
     ix.blk_rows = nullptr;
 }
 
-void build_tasks_device(const SysParams& P, DevIndex& ix, int task_warps, cudaStream_t st) {
+void build_tasks_device(const SysParams& P, DevIndex& ix, int h_warps, int r_warps, cudaStream_t st) {
     free_tasks(ix);
-    ix.task_warps = task_warps;
+    ix.htask_warps = h_warps;
+    ix.rtask_warps = r_warps;
     const int64_t nb = ix.nblock;
     const int T = 128;
     const unsigned grid = static_cast<unsigned>((nb + T - 1) / T);
@@ -228,7 +229,7 @@ void build_tasks_device(const SysParams& P, DevIndex& ix, int task_warps, cudaSt
     KBG_CUDA(cudaMemsetAsync(d_st, 0, sizeof(TaskStats), st));
     if (!ix.blk_rows) ix.blk_rows = talloc<int32_t>(nb);
     k_tasks<<<grid, T, 0, st>>>(P, nb, ix.blk_ptr, ix.cov_atom, ix.cov_mask, hcnt, rcnt, nullptr, nullptr, nullptr,
-                                nullptr, d_st, ix.blk_rows, task_warps);
+                                nullptr, d_st, ix.blk_rows, r_warps);
     KBG_CUDA(cudaGetLastError());
     ix.ht_ptr = talloc<int64_t>(nb + 1);
     ix.rt_ptr = talloc<int64_t>(nb + 1);
@@ -237,14 +238,14 @@ void build_tasks_device(const SysParams& P, DevIndex& ix, int task_warps, cudaSt
     Task* htmp = talloc<Task>(ix.nhtask);
     Task* rtmp = talloc<Task>(ix.nrtask);
     k_tasks<<<grid, T, 0, st>>>(P, nb, ix.blk_ptr, ix.cov_atom, ix.cov_mask, nullptr, nullptr, ix.ht_ptr, ix.rt_ptr,
-                                htmp, rtmp, d_st, nullptr, task_warps);
+                                htmp, rtmp, d_st, nullptr, r_warps);
     KBG_CUDA(cudaGetLastError());
     ix.ht = talloc<Task>(ix.nhtask);
     ix.rt = talloc<Task>(ix.nrtask);
     ix.ht_wptr = talloc<int32_t>(nb * (kMaxTaskWarps + 1));
     ix.rt_wptr = talloc<int32_t>(nb * (kMaxTaskWarps + 1));
-    k_tasks_lpt<<<grid, T, 0, st>>>(nb, task_warps, ix.ht_ptr, htmp, ix.ht, ix.ht_wptr);
-    k_tasks_lpt<<<grid, T, 0, st>>>(nb, task_warps, ix.rt_ptr, rtmp, ix.rt, ix.rt_wptr);
+    k_tasks_lpt<<<grid, T, 0, st>>>(nb, h_warps, ix.ht_ptr, htmp, ix.ht, ix.ht_wptr);
+    k_tasks_lpt<<<grid, T, 0, st>>>(nb, r_warps, ix.rt_ptr, rtmp, ix.rt, ix.rt_wptr);
     KBG_CUDA(cudaGetLastError());
     TaskStats hs;
     KBG_CUDA(cudaMemcpyAsync(&hs, d_st, sizeof(hs), cudaMemcpyDeviceToHost, st));
