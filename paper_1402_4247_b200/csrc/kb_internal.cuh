@@ -15,7 +15,7 @@ namespace kbg {
 constexpr int kMaxSpecies = 8;
 constexpr int kMaxRad = 16;
 constexpr int kGroupRows = 16;  // covers are packed into row groups of <= 16 orbitals (2 DMMA row tiles)
-constexpr int kMaxTaskWarps = 16;  // task lists are LPT-balanced over <= 16 consumer warps
+constexpr int kMaxTaskWarps = 24;  // task lists are LPT-balanced over <= 24 consumer warps
 constexpr int kMaxCoverPerBlock = 64;
 
 // Error taxonomy of kband (common.hpp:21-38) carried as a status code.
