@@ -15,7 +15,7 @@ namespace kbg {
 constexpr int kMaxSpecies = 8;
 constexpr int kMaxRad = 16;
 constexpr int kGroupRows = 16;  // covers are packed into row groups of <= 16 orbitals (2 DMMA row tiles)
-constexpr int kMaxTaskWarps = 24;  // task lists are LPT-balanced over <= 24 consumer warps
+constexpr int kMaxTaskWarps = 32;  // task lists are LPT-balanced over <= 24 consumer warps
 constexpr int kMaxCoverPerBlock = 64;
 
 // Error taxonomy of kband (common.hpp:21-38) carried as a status code.
@@ -201,7 +201,7 @@ int launch_dm_repack(const DevIndex& ix, const SysParams& sys, int nspin, const 
 // buffers fit in shared memory for this index.
 constexpr int kPersistProducers = 1;
 constexpr int kPersistConsumersR = 15;  // rho: 16 warps (128 registers per thread)
-constexpr int kPersistConsumersH = 19;  // H: 20 warps (<= 102 registers per thread)
+constexpr int kPersistConsumersH = 27;  // H: 28 warps (<= 72 registers per thread)
 // Geometry cache (kb_cache.cu): Phi and the per-block tables, built once per
 // geometry after the task lists.
 void build_cache_device(GridArgs gh, GridArgs gr, DevIndex& ix, cudaStream_t st);
