@@ -11,7 +11,7 @@
 // H task (group g, partner cj >= first(g)): C(16 x 8*TN) += Phi_g diag(V dV)
 //   Phi_cj^T over the common 1x2x2 quads with mma.sync.m8n8k4.f64 (SASS
 //   DMMA); canonical rows (cover ci <= cj) are scattered with FP64 atomics.
-// rho task (group g, octet half h, partner range): Y(16 x 8 slots) +=
+// rho task (group g, octet part h of kRhoOct octets, partner range): Y(16 x 8 slots) +=
 //   D'(16 x n_cj) Phi_cj(n_cj x 8) over the partners cj in the range in registers, D' =
 //   repacked DM (x2 off the (a,a,0) blocks: the symmetric half), then
 //   rho(slot) += sum_rows Phi_g * Y once per task.
@@ -77,7 +77,7 @@ struct Smem {
     __device__ __forceinline__ uint8_t* rorb() const { return kbg_smem + base + o_rorb; }  // row -> orbital in cover
     // [ngrp][ncov] octets shared by group g (rows ci <= cj) and cover cj
     __device__ __forceinline__ uint8_t* pom() const { return kbg_smem + base + o_pom; }
-    // [ngrp][2] covers cj with a shared octet in half h
+    // [ngrp][8 / kRhoOct] covers cj with a shared octet in part h
     __device__ __forceinline__ uint64_t* pbits() const { return reinterpret_cast<uint64_t*>(kbg_smem + base + o_pbits); }
     __device__ __forceinline__ Task* task() const { return reinterpret_cast<Task*>(kbg_smem + base + o_task); }
     __device__ __forceinline__ int32_t* wptr() const { return reinterpret_cast<int32_t*>(kbg_smem + base + o_wptr); }
@@ -109,7 +109,7 @@ __host__ __device__ inline size_t tables_layout(const GridArgs& g, size_t* off) 
     off[6] = o;  // pom
     o += align16(mc * mc);
     off[7] = o;  // pbits
-    o += align16(mc * 2 * sizeof(uint64_t));
+    o += align16(mc * (8 / kRhoOct) * sizeof(uint64_t));
     off[8] = o;  // tasks
     o += align16(static_cast<size_t>(g.max_tasks) * sizeof(Task));
     off[9] = o;  // wptr
@@ -269,11 +269,12 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int tid
         }
     }
     sync();
-    if (tid < ngrp * 2) {
-        const int q = tid >> 1, h = tid & 1;
+    constexpr int kParts = 8 / kRhoOct;
+    if (tid < ngrp * kParts) {
+        const int q = tid / kParts, h = tid % kParts;
         uint64_t bits = 0;
         for (int cj = 0; cj < ncov; ++cj)
-            if ((sm.pom()[q * ncov + cj] >> (4 * h)) & 0xF) bits |= 1ull << cj;
+            if ((sm.pom()[q * ncov + cj] >> (kRhoOct * h)) & ((1u << kRhoOct) - 1u)) bits |= 1ull << cj;
         sm.pbits()[tid] = bits;
     }
     sync();
@@ -500,9 +501,9 @@ __device__ __forceinline__ void gather_a(const Smem& sm, int ncov, const int (&r
 
 template <int TM, int KS>
 __device__ __forceinline__ void rho_partner(const double* __restrict__ pb, int swb, uint32_t om4,
-                                            const double (&a)[TM][4], double (&y)[TM][4][2], int colbase) {
+                                            const double (&a)[TM][4], double (&y)[TM][kRhoOct][2], int colbase) {
 #pragma unroll
-    for (int o = 0; o < 4; ++o) {
+    for (int o = 0; o < kRhoOct; ++o) {
         if (!((om4 >> o) & 1u)) continue;
         const int col = colbase + 8 * o;
 #pragma unroll
@@ -526,17 +527,18 @@ __device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, 
         rci[t] = r < rend ? sm.rcov()[r] : kNoCover;
         rri[t] = sm.rorb()[r];
     }
-    double y[TM][4][2];
+    double y[TM][kRhoOct][2];
 #pragma unroll
     for (int t = 0; t < TM; ++t)
 #pragma unroll
-        for (int o = 0; o < 4; ++o) y[t][o][0] = y[t][o][1] = 0.0;
+        for (int o = 0; o < kRhoOct; ++o) y[t][o][0] = y[t][o][1] = 0.0;
     const uint8_t* pom = sm.pom() + gi * ncov;
-    uint64_t bits = sm.pbits()[2 * gi + h] & (~0ull << cbeg) & (cend >= 64 ? ~0ull : ((1ull << cend) - 1ull));
-    const int colbase = 32 * h + (lane >> 2);
+    uint64_t bits = sm.pbits()[(8 / kRhoOct) * gi + h] & (~0ull << cbeg) &
+                    (cend >= 64 ? ~0ull : ((1ull << cend) - 1ull));
+    const int colbase = 8 * kRhoOct * h + (lane >> 2);
     // one partner: D' fragments in `a` (K chunk 0); more chunks for > 16 orbitals
     auto process = [&](int cj, double (&a)[TM][4]) {
-        const uint32_t om4 = (pom[cj] >> (4 * h)) & 0xFu;
+        const uint32_t om4 = (pom[cj] >> (kRhoOct * h)) & ((1u << kRhoOct) - 1u);
         const CoverS& B = sm.cov()[cj];
         const int nkc = (B.norb + 15) >> 4;
         for (int kc = 0; kc < nkc; ++kc) {
@@ -579,11 +581,12 @@ __device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, 
     }
     // rho(slot) += sum over rows of Phi_row(slot) * Y(row, slot): per-lane
     // partial products v[j] (j = 2*octet + e), then a reduce-scatter over the
-    // 8 row lanes (xor 16, 8, 4) leaves lane l with the total of j = l >> 2.
-    double v[8];
+    // 8 row lanes (xor 16, 8, 4).
+    constexpr int NV = 2 * kRhoOct;
+    double v[NV];
 #pragma unroll
-    for (int o = 0; o < 4; ++o) {
-        const int p = 8 * (4 * h + o) + 2 * (lane & 3);
+    for (int o = 0; o < kRhoOct; ++o) {
+        const int p = 8 * (kRhoOct * h + o) + 2 * (lane & 3);
         v[2 * o] = v[2 * o + 1] = 0.0;
 #pragma unroll
         for (int t = 0; t < TM; ++t) {
@@ -594,25 +597,34 @@ __device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, 
         }
     }
     const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-    double w4[4];
+    double w4[NV / 2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const double send = b4 ? v[i] : v[i + 4];
-        const double keep = b4 ? v[i + 4] : v[i];
+    for (int i = 0; i < NV / 2; ++i) {
+        const double send = b4 ? v[i] : v[i + NV / 2];
+        const double keep = b4 ? v[i + NV / 2] : v[i];
         w4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
     }
-    double w2[2];
+    if (NV == 8) {  // 4 octets: lane l ends with j = l >> 2
+        double w2[2];
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const double send = b3 ? w4[i] : w4[i + 2];
-        const double keep = b3 ? w4[i + 2] : w4[i];
-        w2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        for (int i = 0; i < 2; ++i) {
+            const double send = b3 ? w4[i] : w4[i + 2];
+            const double keep = b3 ? w4[i + 2] : w4[i];
+            w2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+        const double send = b2 ? w2[0] : w2[1];
+        const double keep = b2 ? w2[1] : w2[0];
+        const double tot = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        const int j = lane >> 2;
+        racc[8 * (kRhoOct * h + (j >> 1)) + 2 * (lane & 3) + (j & 1)] += tot;
+    } else {  // 2 octets: lane l (bit 2 clear) ends with j = (l >> 3) & 3
+        const double send = b3 ? w4[0] : w4[1];
+        const double keep = b3 ? w4[1] : w4[0];
+        double tot = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        tot += __shfl_xor_sync(0xffffffffu, tot, 4);
+        const int j = (lane >> 3) & 3;
+        if (!b2) racc[8 * (kRhoOct * h + (j >> 1)) + 2 * (lane & 3) + (j & 1)] += tot;
     }
-    const double send = b2 ? w2[0] : w2[1];
-    const double keep = b2 ? w2[1] : w2[0];
-    const double tot = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    const int j = lane >> 2;
-    racc[8 * (4 * h + (j >> 1)) + 2 * (lane & 3) + (j & 1)] += tot;
 }
 
 __device__ __forceinline__ void rho_task(const Smem& sm, int ncov, const Task& t, const double* Dr, double* racc,

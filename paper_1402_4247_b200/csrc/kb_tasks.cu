@@ -116,14 +116,14 @@ __global__ void k_tasks(SysParams P, int64_t nblock, const int32_t* __restrict__
     const int64_t target = rtotal / (2 * W) > 16 ? rtotal / (2 * W) : 16;
     for (int g = 0; g < ng; ++g) {
         const int tm = (g_rows[g] + 7) >> 3;
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < 8 / kRhoOct; ++h) {
             int64_t cost = 0;
             int start = -1;
             for (int cj = g_first[g]; cj < ncov; ++cj) {
                 const uint64_t mj = cov_mask[c0 + cj];
                 uint32_t om = 0;
                 for (int ci = g_first[g]; ci < g_end[g] && ci <= cj; ++ci) om |= octets_of(cov_mask[c0 + ci] & mj);
-                om &= 0xFu << (4 * h);
+                om &= ((1u << kRhoOct) - 1u) << (kRhoOct * h);
                 if (om) {
                     if (start < 0) start = cj;
                     cost += __popc(om) * tm * ((norb[cj] + 3) >> 2);
