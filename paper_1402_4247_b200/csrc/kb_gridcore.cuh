@@ -556,28 +556,39 @@ __device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, 
             }
         }
     };
-    // partners two at a time with ping-pong fragment registers: the gather of
-    // the next partner is in flight while the current one is contracted
-    double a0[TM][4], a1[TM][4];
-    int c0 = bits ? __ffsll(bits) - 1 : -1;
-    if (c0 >= 0) {
-        bits &= bits - 1;
-        gather_a<TM>(sm, ncov, rci, rri, c0, 0, Dr, lane, a0, exp);
-    }
-    while (c0 >= 0) {
-        const int c1 = bits ? __ffsll(bits) - 1 : -1;
-        if (c1 >= 0) {
-            bits &= bits - 1;
-            gather_a<TM>(sm, ncov, rci, rri, c1, 0, Dr, lane, a1, exp);
-        }
-        process(c0, a0);
-        if (c1 < 0) break;
-        c0 = bits ? __ffsll(bits) - 1 : -1;
+    if (kRhoPrefetch) {
+        // partners two at a time with ping-pong fragment registers: the gather of
+        // the next partner is in flight while the current one is contracted
+        double a0[TM][4], a1[TM][4];
+        int c0 = bits ? __ffsll(bits) - 1 : -1;
         if (c0 >= 0) {
             bits &= bits - 1;
             gather_a<TM>(sm, ncov, rci, rri, c0, 0, Dr, lane, a0, exp);
         }
-        process(c1, a1);
+        while (c0 >= 0) {
+            const int c1 = bits ? __ffsll(bits) - 1 : -1;
+            if (c1 >= 0) {
+                bits &= bits - 1;
+                gather_a<TM>(sm, ncov, rci, rri, c1, 0, Dr, lane, a1, exp);
+            }
+            process(c0, a0);
+            if (c1 < 0) break;
+            c0 = bits ? __ffsll(bits) - 1 : -1;
+            if (c0 >= 0) {
+                bits &= bits - 1;
+                gather_a<TM>(sm, ncov, rci, rri, c0, 0, Dr, lane, a0, exp);
+            }
+            process(c1, a1);
+        }
+    } else {
+        // one fragment set: more warps per SM hide the gather latency instead
+        while (bits) {
+            const int cj = __ffsll(bits) - 1;
+            bits &= bits - 1;
+            double a[TM][4];
+            gather_a<TM>(sm, ncov, rci, rri, cj, 0, Dr, lane, a, exp);
+            process(cj, a);
+        }
     }
     // rho(slot) += sum over rows of Phi_row(slot) * Y(row, slot): per-lane
     // partial products v[j] (j = 2*octet + e), then a reduce-scatter over the

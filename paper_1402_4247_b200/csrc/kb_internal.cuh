@@ -17,6 +17,7 @@ constexpr int kMaxRad = 16;
 constexpr int kGroupRows = 16;  // covers are packed into row groups of <= 16 orbitals (2 DMMA row tiles)
 constexpr int kMaxTaskWarps = 32;  // task lists are LPT-balanced over <= 24 consumer warps
 constexpr int kMaxCoverPerBlock = 64;
+constexpr bool kRhoPrefetch = false;  // ping-pong D' prefetch (needs ~128 registers, 16 warps)
 constexpr int kRhoOct = 4;  // octets per rho task (4: halves of the block, 2: quarters; halves measured faster)
 
 // Error taxonomy of kband (common.hpp:21-38) carried as a status code.
@@ -201,7 +202,7 @@ int launch_dm_repack(const DevIndex& ix, const SysParams& sys, int nspin, const 
 // on block k (two shared-memory buffers). persist_fits() says whether two
 // buffers fit in shared memory for this index.
 constexpr int kPersistProducers = 1;
-constexpr int kPersistConsumersR = 15;  // rho: 16 warps (128 registers per thread)
+constexpr int kPersistConsumersR = 19;  // rho: 20 warps (<= 102 registers per thread)
 constexpr int kPersistConsumersH = 27;  // H: 28 warps (<= 72 registers per thread)
 // Geometry cache (kb_cache.cu): Phi and the per-block tables, built once per
 // geometry after the task lists.
