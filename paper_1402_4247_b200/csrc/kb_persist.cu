@@ -96,41 +96,68 @@ __host__ __device__ inline size_t persist_bytes(const GridArgs& g, bool density)
     return 2 * align16(buffer_layout(g, acc, off)) + 64;
 }
 
+// Next non-empty owned block from the work counter (-1: none left); empty
+// blocks get rho = 0 on the way.
+template <bool DENSITY>
+__device__ int64_t next_block(const GridArgs& g, int lane) {
+    for (;;) {
+        int idx = 0;
+        if (lane == 0) idx = atomicAdd(g.counter, 1);
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if (idx >= g.norder) return -1;
+        const int64_t b = g.order[idx];
+        if (g.blk_ptr[b + 1] > g.blk_ptr[b]) return b;
+        if (DENSITY) {
+            int bi, bj, bk;
+            block_decode(g.sys, b, bi, bj, bk);
+            for (int p = lane; p < 64; p += 32) {
+                bool valid;
+                const int64_t pt = slot_point(g.sys, bi, bj, bk, p, valid);
+                if (valid)
+                    for (int spin = 0; spin < g.nspin; ++spin) g.out[spin * g.npts + pt] = 0.0;
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+// Producer warp: block k goes to buffer k & 1. The block after the current
+// one is fetched early and its cache image prefetched into L2, so the bulk
+// copy issued when its buffer frees up is served from L2.
 template <bool DENSITY>
 __device__ void producer(const GridArgs& g, const Buffers& B, int lane) {
     unsigned long long t_wait = 0, t0 = clock64();
+    auto image = [&](int64_t b, const unsigned char*& tab, const double*& phi, uint32_t& tb, uint32_t& pb) {
+        const int64_t i = b - g.blk_begin;
+        tab = g.tabs + i * g.tab_bytes;
+        phi = g.phis + g.phi_off[i];
+        tb = static_cast<uint32_t>(g.tab_bytes);
+        pb = static_cast<uint32_t>((g.phi_off[i + 1] - g.phi_off[i]) * sizeof(double));
+    };
+    int64_t b_next = next_block<DENSITY>(g, lane);
     for (int k = 0;; ++k) {
         const int s = k & 1;
+        const int64_t b = b_next;
+        if (b >= 0) {
+            b_next = next_block<DENSITY>(g, lane);
+            if (b_next >= 0 && lane == 0) {
+                const unsigned char* tab;
+                const double* phi;
+                uint32_t tb, pb;
+                image(b_next, tab, phi, tb, pb);
+                prefetch_l2(tab, tb);
+                prefetch_l2(phi, pb);
+            }
+        }
         if (k >= 2) {
             const unsigned long long tw = clock64();
             mbar_wait(&B.empty[s], ((k >> 1) - 1) & 1, 256);
             t_wait += clock64() - tw;
         }
         const Smem sm = B.buf(s);
-        int64_t b = -1;
-        int ncov = 0;
-        for (;;) {
-            int idx = 0;
-            if (lane == 0) idx = atomicAdd(g.counter, 1);
-            idx = __shfl_sync(0xffffffffu, idx, 0);
-            if (idx >= g.norder) {
-                b = -1;
-                break;
-            }
-            b = g.order[idx];
-            ncov = g.blk_ptr[b + 1] - g.blk_ptr[b];
-            if (ncov > 0) break;
-            if (DENSITY) {  // empty block: rho = 0 on its points
-                int bi, bj, bk;
-                block_decode(g.sys, b, bi, bj, bk);
-                for (int p = lane; p < 64; p += 32) {
-                    bool valid;
-                    const int64_t pt = slot_point(g.sys, bi, bj, bk, p, valid);
-                    if (valid)
-                        for (int spin = 0; spin < g.nspin; ++spin) g.out[spin * g.npts + pt] = 0.0;
-                }
-            }
-        }
         if (b < 0) {
             if (lane == 0) {
                 sm.meta()->block = -1;
@@ -153,12 +180,13 @@ __device__ void producer(const GridArgs& g, const Buffers& B, int lane) {
         }
         __syncwarp();
         if (lane == 0) {
-            const int64_t i = b - g.blk_begin;
-            const uint32_t tb = static_cast<uint32_t>(g.tab_bytes);
-            const uint32_t pb = static_cast<uint32_t>((g.phi_off[i + 1] - g.phi_off[i]) * sizeof(double));
+            const unsigned char* tab;
+            const double* phi;
+            uint32_t tb, pb;
+            image(b, tab, phi, tb, pb);
             mbar_arrive_tx(&B.full[s], tb + pb);
-            bulk_g2s(sm.meta(), g.tabs + i * g.tab_bytes, tb, &B.full[s]);
-            bulk_g2s(sm.phi(), g.phis + g.phi_off[i], pb, &B.full[s]);
+            bulk_g2s(sm.meta(), tab, tb, &B.full[s]);
+            bulk_g2s(sm.phi(), phi, pb, &B.full[s]);
         }
         __syncwarp();
     }
