@@ -172,7 +172,10 @@ int kbg_last_launches(const kbg_ctx* ctx);
 /* Persistent-kernel timing counters (clock64 cycles summed over warps/CTAs
  * since the last KBG_OPT_DEBUG_COUNTERS reset): [0] producer wait on empty,
  * [1] producer total, [2] consumer wait on full, [3] consumer wait at the end,
- * [4] consumer total, [5] blocks seen by consumers. Profiling aid. */
+ * [4] consumer total, [5] blocks seen by consumers, [6] consumer wait on the
+ * first two blocks, [7] producer-measured copy latency (the producer waits for
+ * each copy when counters are on), [8] copies, [10] last-consumer reduce +
+ * release, [11] bytes copied. Profiling aid. */
 int kbg_debug_counters(kbg_ctx* ctx, int64_t* out, int n);
 
 /* Work tally of the last density / hamiltonian call. */
@@ -184,11 +187,55 @@ int kbg_last_tally(const kbg_ctx* ctx, kbg_tally* out);
 #define KBG_OPT_SCATTER_STORE 3 /* timing experiment: plain stores instead of atomics (H is WRONG) */
 #define KBG_OPT_PERSIST 4 /* 1 (default): persistent warp-specialized kernels when they fit; 0: one CTA per block */
 #define KBG_OPT_DEBUG_COUNTERS 5 /* nonzero: enable + reset the persistent kernels' timing counters */
+/* Intra-block schedule of the persistent kernels, read by kbg_build_index: bit 0 (H) / bit 1 (rho) set = the
+ * block's tasks, heaviest first, form one queue the consumer warps pull from; clear = static LPT lists per
+ * warp. Default 3. rho stays bitwise deterministic either way (per-task partial sums, fixed-order reduce). */
+#define KBG_OPT_SCHEDULE 6
 int kbg_set_option(kbg_ctx* ctx, int option, int64_t value);
 
 const char* kbg_last_error(const kbg_ctx* ctx);
 const char* kbg_status_string(int status);
 void kbg_destroy(kbg_ctx* ctx);
+
+/* ---- Formats either side of the grid pass ----------------
+ * The pair-sparse blocks of kbg_index (grid-pass DM input, H output) against
+ * the reference's band-pipeline types: RealSpaceOperator (dense n x n block
+ * M_R per lattice offset R), its Bloch image
+ * (Part 1 bloch_transform) and the real-space folding of
+ * k-resolved density matrices (Part 6 density_matrices).
+ * Orbital row of atom a, orbital i: orb_off[a] + i with orb_off the prefix sum
+ * of the atoms' orbital counts (n = nbasis). k points are fractional
+ * (reciprocal-lattice) coordinates, R integer lattice offsets. Complex
+ * matrices are row-major n x n of interleaved (re, im) doubles. One matrix
+ * (one spin) per call; `pairs` holds nnz values. The index must be built. */
+
+/* Distinct lattice offsets of the pair list, sorted lexicographically
+ * (R = 0 included): *nR receives the count; R (3 * nR ints) may be NULL. */
+int kbg_offsets(kbg_ctx* ctx, int* nR, int32_t* R);
+
+/* pair-sparse -> RealSpaceOperator blocks [nR][n][n] in kbg_offsets order
+ * (entries outside the pair list are 0), and back (extracts the pair-list
+ * entries of dense blocks). */
+int kbg_to_realspace(kbg_ctx* ctx, const double* pairs, double* blocks);
+int kbg_from_realspace(kbg_ctx* ctx, const double* blocks, double* pairs);
+int kbg_to_realspace_dev(kbg_ctx* ctx, const double* d_pairs, double* d_blocks, void* stream);
+int kbg_from_realspace_dev(kbg_ctx* ctx, const double* d_blocks, double* d_pairs, void* stream);
+
+/* Bloch transform M(k) = sum_R exp(+2 pi i k.R) M_R for nk k points
+ * (kpts: 3 * nk host doubles); out: [nk][n][n] complex. The host variant
+ * validates M_{-R} = M_R^T (the RealSpaceOperator invariant) first and
+ * returns KBG_ERR_CONSISTENCY naming the offending pair and R. */
+int kbg_bloch(kbg_ctx* ctx, const double* pairs, int nk, const double* kpts, double* out);
+int kbg_bloch_dev(kbg_ctx* ctx, const double* d_pairs, int nk, const double* kpts, double* d_out, void* stream);
+
+/* Real-space folding DM_R = sum_k w_k exp(-2 pi i k.R) rho_k onto the pair
+ * list (real part; for a time-reversal-symmetric k set the imaginary part
+ * vanishes -- its largest magnitude is returned in *max_imag, may be NULL).
+ * rho_k: [nk][n][n] complex; w: nk host weights. */
+int kbg_fold(kbg_ctx* ctx, int nk, const double* kpts, const double* w, const double* rho_k, double* pairs,
+             double* max_imag);
+int kbg_fold_dev(kbg_ctx* ctx, int nk, const double* kpts, const double* w, const double* d_rho_k, double* d_pairs,
+                 void* stream);
 
 /* Library identification: "kbgrid <version> sm_100a". */
 const char* kbg_version(void);

@@ -13,7 +13,8 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIBDIR = os.path.join(HERE, "lib")
-KBGRID_SO = os.path.join(LIBDIR, "libkbgrid.so")
+# KBG_LIBKBGRID: alternative build of the same library (tools/ kernel variants)
+KBGRID_SO = os.environ.get("KBG_LIBKBGRID") or os.path.join(LIBDIR, "libkbgrid.so")
 KBGSYNTH_SO = os.path.join(LIBDIR, "libkbgsynth.so")
 
 KBG_OK = 0
@@ -28,6 +29,7 @@ KBG_OPT_FAULT_SIGN = 2
 KBG_OPT_SCATTER_STORE = 3
 KBG_OPT_PERSIST = 4
 KBG_OPT_DEBUG_COUNTERS = 5
+KBG_OPT_SCHEDULE = 6
 KBG_CELL_PRIMITIVE = 0
 KBG_CELL_CUBIC = 1
 
@@ -110,6 +112,15 @@ KBGRID_SYMBOLS = [
     ("kbg_status_string", C.c_char_p, [_I]),
     ("kbg_destroy", None, [_P]),
     ("kbg_version", C.c_char_p, []),
+    ("kbg_offsets", _I, [_P, C.POINTER(_I), C.POINTER(C.c_int32)]),
+    ("kbg_to_realspace", _I, [_P, _DP, _DP]),
+    ("kbg_from_realspace", _I, [_P, _DP, _DP]),
+    ("kbg_to_realspace_dev", _I, [_P, _P, _P, _P]),
+    ("kbg_from_realspace_dev", _I, [_P, _P, _P, _P]),
+    ("kbg_bloch", _I, [_P, _DP, _I, _DP, _DP]),
+    ("kbg_bloch_dev", _I, [_P, _P, _I, _DP, _P, _P]),
+    ("kbg_fold", _I, [_P, _I, _DP, _DP, _DP, _DP, _DP]),
+    ("kbg_fold_dev", _I, [_P, _I, _DP, _DP, _P, _P, _P]),
 ]
 
 KBGSYNTH_SYMBOLS = [

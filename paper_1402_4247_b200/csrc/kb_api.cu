@@ -2,6 +2,7 @@
 // entry points. Errors follow the kband taxonomy (common.hpp:21-38) as status
 // codes with a message naming the failing field (kbg_last_error).
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -23,6 +24,7 @@ struct kbg_ctx {
     int nwarps = 8;
     bool persist_ok = false;   // two staging buffers fit: persistent kernels
     int persist = 1;           // option: use the persistent kernels when they fit
+    int schedule = 3;          // KBG_OPT_SCHEDULE
     double* d_dmr = nullptr;   // repacked DM scratch
     size_t cap_dmr = 0;
     int* d_counter = nullptr;  // persistent work counter
@@ -40,6 +42,16 @@ struct kbg_ctx {
     std::string err;
     int64_t npts = 0;
     std::vector<int> h_spc;
+    // format converters (kb_formats.cu)
+    kbg::FormatIndex fmt;
+    double* d_fa = nullptr;  // host-API staging: pairs / dense side
+    size_t cap_fa = 0;
+    double* d_fb = nullptr;
+    size_t cap_fb = 0;
+    double* d_phase = nullptr;  // [nk][npair] double2
+    size_t cap_phase = 0;
+    double* d_kw = nullptr;  // kpts (3 nk) then weights (nk)
+    size_t cap_kw = 0;
 };
 
 namespace {
@@ -318,16 +330,22 @@ int kbg_build_index(kbg_ctx* c) {
         KBG_CUDA(cudaSetDevice(c->device));
         c->built = false;
         c->hix = kbg::HostIndex();
+        kbg::free_formats(c->fmt);
         kbg::build_index_device(c->P, c->ix, c->stream);
-        kbg::build_tasks_device(c->P, c->ix, kbg::kPersistConsumersH, kbg::kPersistConsumersR, c->stream);
-        shard(c);
-        c->built = true;
-        {
+        // persistent kernels: one task queue (1 "warp") or LPT lists per consumer warp
+        auto persist_tasks = [&](int sched) {
+            kbg::build_tasks_device(c->P, c->ix, (sched & 1) ? 1 : kbg::kPersistConsumersH,
+                                    (sched & 2) ? 1 : kbg::kPersistConsumersR, kbg::kPersistConsumersR, c->stream);
             const kbg::GridArgs gd = grid_args(c, 1, 0.0, nullptr, nullptr, true);
             const kbg::GridArgs gh = grid_args(c, 1, 0.0, nullptr, nullptr, false);
-            c->persist_ok = kbg::persist_fits(gd, true) && kbg::persist_fits(gh, false);
-        }
-        if (!c->persist_ok) kbg::build_tasks_device(c->P, c->ix, 8, 8, c->stream);
+            return kbg::persist_fits(gd, true) && kbg::persist_fits(gh, false);
+        };
+        c->built = true;
+        shard(c);
+        c->persist_ok = persist_tasks(c->schedule);
+        // the rho queue keeps per-task partial sums in shared memory; drop it if they do not fit
+        if (!c->persist_ok && (c->schedule & 2)) c->persist_ok = persist_tasks(c->schedule & 1);
+        if (!c->persist_ok) kbg::build_tasks_device(c->P, c->ix, 8, 8, 8, c->stream);
         // owned blocks, heaviest first, for the persistent kernels' work counter
         std::vector<int64_t> cost(c->ix.nblock);
         KBG_CUDA(cudaMemcpy(cost.data(), c->ix.blk_cost, cost.size() * sizeof(int64_t), cudaMemcpyDeviceToHost));
@@ -519,6 +537,236 @@ int kbg_debug_counters(kbg_ctx* c, int64_t* out, int n) {
     return KBG_OK;
 }
 
+// ---- formats either side of the grid pass (kb_formats.cu) -------------------
+namespace {
+
+const kbg::FormatIndex& formats(kbg_ctx* c) {
+    require_index(c);
+    kbg::FormatIndex& f = c->fmt;
+    if (f.valid) return f;
+    if (!c->hix.valid) kbg::copy_index_to_host(c->ix, c->hix, c->stream);
+    const kbg::HostIndex& h = c->hix;
+    const int natom = c->P.natom;
+    std::vector<int32_t> off(natom + 1, 0), atom;
+    for (int a = 0; a < natom; ++a) off[a + 1] = off[a] + c->P.sp[c->h_spc[a]].norb;
+    for (int a = 0; a < natom; ++a) atom.insert(atom.end(), off[a + 1] - off[a], a);
+    const int64_t npair = c->ix.npair;
+    std::vector<std::array<int32_t, 3>> R(npair);
+    for (int64_t p = 0; p < npair; ++p) R[p] = {h.pair_R[3 * p], h.pair_R[3 * p + 1], h.pair_R[3 * p + 2]};
+    std::vector<std::array<int32_t, 3>> uniq = R;
+    std::sort(uniq.begin(), uniq.end());
+    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+    std::vector<int32_t> rid(npair), run(2 * static_cast<size_t>(natom) * natom, 0);
+    for (int64_t p = 0; p < npair; ++p) {
+        rid[p] = static_cast<int32_t>(std::lower_bound(uniq.begin(), uniq.end(), R[p]) - uniq.begin());
+        const size_t ab = static_cast<size_t>(h.pair_a[p]) * natom + h.pair_b[p];
+        if (run[2 * ab] == run[2 * ab + 1]) run[2 * ab] = static_cast<int32_t>(p);  // pairs sorted by (a, b, R)
+        run[2 * ab + 1] = static_cast<int32_t>(p + 1);
+    }
+    f.n = off[natom];
+    f.natom = natom;
+    f.nR = static_cast<int>(uniq.size());
+    f.R.clear();
+    for (const auto& r : uniq) f.R.insert(f.R.end(), r.begin(), r.end());
+    auto up = [&](int32_t*& d, const std::vector<int32_t>& v) {
+        KBG_CUDA(cudaMalloc(&d, std::max<size_t>(1, v.size()) * sizeof(int32_t)));
+        if (!v.empty()) KBG_CUDA(cudaMemcpy(d, v.data(), v.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    };
+    up(f.orb_atom, atom);
+    up(f.orb_off, off);
+    up(f.run, run);
+    up(f.rid, rid);
+    f.valid = true;
+    return f;
+}
+
+void check_nk(int nk, const double* kpts) {
+    if (nk < 1) throw Error(KBG_ERR_CONFIG, "nk must be >= 1");
+    if (!kpts) throw Error(KBG_ERR_CONFIG, "null k points");
+    for (int i = 0; i < 3 * nk; ++i)
+        if (!std::isfinite(kpts[i])) throw Error(KBG_ERR_NONFINITE, "k point " + std::to_string(i / 3) + " is not finite");
+}
+
+// k points (and weights) to the device, phases exp(sign 2 pi i k.R_p) per (k, pair)
+const double2* phases(kbg_ctx* c, int nk, const double* kpts, const double* w, double sign, cudaStream_t st) {
+    ensure(c->d_kw, c->cap_kw, 4 * static_cast<size_t>(nk));
+    KBG_CUDA(cudaMemcpyAsync(c->d_kw, kpts, 3 * nk * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (w) KBG_CUDA(cudaMemcpyAsync(c->d_kw + 3 * nk, w, nk * sizeof(double), cudaMemcpyHostToDevice, st));
+    ensure(c->d_phase, c->cap_phase, 2 * static_cast<size_t>(nk) * std::max<int64_t>(1, c->ix.npair));
+    c->last_launches =
+        kbg::launch_phase(nk, c->ix.npair, c->d_kw, c->ix.pair_R, sign, reinterpret_cast<double2*>(c->d_phase), st);
+    return reinterpret_cast<const double2*>(c->d_phase);
+}
+
+// M_{-R} = M_R^T check of one matrix already on the device (host API only);
+// names the first offending pair.
+void check_hermitian(kbg_ctx* c, const double* d_pairs, const double* h_pairs, const char* who) {
+    KBG_CUDA(cudaMemsetAsync(c->d_check, 0, 4 * sizeof(unsigned long long), c->stream));
+    kbg::launch_dm_check(c->ix, c->P, 1, d_pairs, c->d_check, c->stream);
+    unsigned long long chk[4];
+    KBG_CUDA(cudaMemcpyAsync(chk, c->d_check, sizeof(chk), cudaMemcpyDeviceToHost, c->stream));
+    KBG_CUDA(cudaStreamSynchronize(c->stream));
+    double dmax, amax;
+    std::memcpy(&dmax, &chk[0], 8);
+    std::memcpy(&amax, &chk[1], 8);
+    if (chk[2]) throw Error(KBG_ERR_NONFINITE, std::string(who) + ": non-finite entry");
+    if (dmax <= 1e-13 * amax) return;
+    if (!c->hix.valid) kbg::copy_index_to_host(c->ix, c->hix, c->stream);
+    const kbg::HostIndex& h = c->hix;
+    for (int64_t p = 0; p < c->ix.npair; ++p) {
+        const int na = c->P.sp[c->h_spc[h.pair_a[p]]].norb, nb = c->P.sp[c->h_spc[h.pair_b[p]]].norb;
+        const int64_t q = h.pair_mirror[p];
+        for (int i = 0; i < na; ++i)
+            for (int j = 0; j < nb; ++j)
+                if (std::fabs(h_pairs[h.pair_off[p] + i * nb + j] - h_pairs[h.pair_off[q] + j * na + i]) > 1e-13 * amax)
+                    throw Error(KBG_ERR_CONSISTENCY,
+                                std::string(who) + ": M_{-R} != M_R^T at pair " + std::to_string(p) + " (a=" +
+                                    std::to_string(h.pair_a[p]) + ", b=" + std::to_string(h.pair_b[p]) + ", R=(" +
+                                    std::to_string(h.pair_R[3 * p]) + "," + std::to_string(h.pair_R[3 * p + 1]) + "," +
+                                    std::to_string(h.pair_R[3 * p + 2]) + ")) by " + std::to_string(dmax));
+    }
+}
+
+}  // namespace
+
+int kbg_offsets(kbg_ctx* c, int* nR, int32_t* R) {
+    if (!c || !nR) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        KBG_CUDA(cudaSetDevice(c->device));
+        const kbg::FormatIndex& f = formats(c);
+        *nR = f.nR;
+        if (R) std::copy(f.R.begin(), f.R.end(), R);
+    });
+}
+
+int kbg_to_realspace_dev(kbg_ctx* c, const double* d_pairs, double* d_blocks, void* stream) {
+    if (!c || !d_pairs || !d_blocks) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        KBG_CUDA(cudaSetDevice(c->device));
+        const kbg::FormatIndex& f = formats(c);
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        KBG_CUDA(cudaMemsetAsync(d_blocks, 0, sizeof(double) * f.nR * f.n * f.n, st));
+        c->last_launches = kbg::launch_realspace(f, c->ix, true, const_cast<double*>(d_pairs), d_blocks, st);
+    });
+}
+
+int kbg_from_realspace_dev(kbg_ctx* c, const double* d_blocks, double* d_pairs, void* stream) {
+    if (!c || !d_pairs || !d_blocks) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        KBG_CUDA(cudaSetDevice(c->device));
+        const kbg::FormatIndex& f = formats(c);
+        c->last_launches = kbg::launch_realspace(f, c->ix, false, d_pairs, const_cast<double*>(d_blocks),
+                                                 static_cast<cudaStream_t>(stream));
+    });
+}
+
+int kbg_to_realspace(kbg_ctx* c, const double* pairs, double* blocks) {
+    if (!c || !pairs || !blocks) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        KBG_CUDA(cudaSetDevice(c->device));
+        const kbg::FormatIndex& f = formats(c);
+        const size_t nd = static_cast<size_t>(f.nR) * f.n * f.n;
+        ensure(c->d_fa, c->cap_fa, c->ix.nnz);
+        ensure(c->d_fb, c->cap_fb, nd);
+        KBG_CUDA(cudaMemcpyAsync(c->d_fa, pairs, c->ix.nnz * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        KBG_CUDA(cudaMemsetAsync(c->d_fb, 0, nd * sizeof(double), c->stream));
+        c->last_launches = kbg::launch_realspace(f, c->ix, true, c->d_fa, c->d_fb, c->stream);
+        KBG_CUDA(cudaMemcpyAsync(blocks, c->d_fb, nd * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        KBG_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int kbg_from_realspace(kbg_ctx* c, const double* blocks, double* pairs) {
+    if (!c || !pairs || !blocks) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        KBG_CUDA(cudaSetDevice(c->device));
+        const kbg::FormatIndex& f = formats(c);
+        const size_t nd = static_cast<size_t>(f.nR) * f.n * f.n;
+        ensure(c->d_fa, c->cap_fa, c->ix.nnz);
+        ensure(c->d_fb, c->cap_fb, nd);
+        KBG_CUDA(cudaMemcpyAsync(c->d_fb, blocks, nd * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        c->last_launches = kbg::launch_realspace(f, c->ix, false, c->d_fa, c->d_fb, c->stream);
+        KBG_CUDA(cudaMemcpyAsync(pairs, c->d_fa, c->ix.nnz * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        KBG_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int kbg_bloch_dev(kbg_ctx* c, const double* d_pairs, int nk, const double* kpts, double* d_out, void* stream) {
+    if (!c || !d_pairs || !d_out) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        check_nk(nk, kpts);
+        KBG_CUDA(cudaSetDevice(c->device));
+        const kbg::FormatIndex& f = formats(c);
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const double2* ph = phases(c, nk, kpts, nullptr, 1.0, st);
+        c->last_launches += kbg::launch_bloch(f, c->ix, nk, d_pairs, ph, d_out, st);
+        c->tally.flops = 4.0 * nk * c->ix.nnz;
+        c->tally.bytes = 8.0 * c->ix.nnz + 16.0 * nk * f.n * f.n;
+    });
+}
+
+int kbg_bloch(kbg_ctx* c, const double* pairs, int nk, const double* kpts, double* out) {
+    if (!c || !pairs || !out) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        check_nk(nk, kpts);
+        KBG_CUDA(cudaSetDevice(c->device));
+        const kbg::FormatIndex& f = formats(c);
+        const size_t nd = 2 * static_cast<size_t>(nk) * f.n * f.n;
+        ensure(c->d_fa, c->cap_fa, c->ix.nnz);
+        ensure(c->d_fb, c->cap_fb, nd);
+        KBG_CUDA(cudaMemcpyAsync(c->d_fa, pairs, c->ix.nnz * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        check_hermitian(c, c->d_fa, pairs, "bloch");
+        const double2* ph = phases(c, nk, kpts, nullptr, 1.0, c->stream);
+        c->last_launches += 1 + kbg::launch_bloch(f, c->ix, nk, c->d_fa, ph, c->d_fb, c->stream);
+        KBG_CUDA(cudaMemcpyAsync(out, c->d_fb, nd * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        KBG_CUDA(cudaStreamSynchronize(c->stream));
+        c->tally.flops = 4.0 * nk * c->ix.nnz;
+        c->tally.bytes = 8.0 * c->ix.nnz + 16.0 * nk * f.n * f.n;
+    });
+}
+
+int kbg_fold_dev(kbg_ctx* c, int nk, const double* kpts, const double* w, const double* d_rho_k, double* d_pairs,
+                 void* stream) {
+    if (!c || !w || !d_rho_k || !d_pairs) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        check_nk(nk, kpts);
+        KBG_CUDA(cudaSetDevice(c->device));
+        const kbg::FormatIndex& f = formats(c);
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const double2* ph = phases(c, nk, kpts, w, -1.0, st);
+        c->last_launches += kbg::launch_fold(f, c->ix, nk, c->d_kw + 3 * nk, ph, d_rho_k, d_pairs, nullptr, st);
+        c->tally.flops = 8.0 * nk * c->ix.nnz;
+        c->tally.bytes = 8.0 * c->ix.nnz + 16.0 * nk * c->ix.nnz;
+    });
+}
+
+int kbg_fold(kbg_ctx* c, int nk, const double* kpts, const double* w, const double* rho_k, double* pairs,
+             double* max_imag) {
+    if (!c || !w || !rho_k || !pairs) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        check_nk(nk, kpts);
+        for (int k = 0; k < nk; ++k)
+            if (!std::isfinite(w[k])) throw Error(KBG_ERR_NONFINITE, "fold: weight " + std::to_string(k) + " is not finite");
+        KBG_CUDA(cudaSetDevice(c->device));
+        const kbg::FormatIndex& f = formats(c);
+        const size_t nd = 2 * static_cast<size_t>(nk) * f.n * f.n;
+        ensure(c->d_fa, c->cap_fa, c->ix.nnz);
+        ensure(c->d_fb, c->cap_fb, nd);
+        KBG_CUDA(cudaMemcpyAsync(c->d_fb, rho_k, nd * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        const double2* ph = phases(c, nk, kpts, w, -1.0, c->stream);
+        KBG_CUDA(cudaMemsetAsync(c->d_check, 0, 4 * sizeof(unsigned long long), c->stream));
+        c->last_launches +=
+            kbg::launch_fold(f, c->ix, nk, c->d_kw + 3 * nk, ph, c->d_fb, c->d_fa, c->d_check, c->stream);
+        unsigned long long mi = 0;
+        KBG_CUDA(cudaMemcpyAsync(pairs, c->d_fa, c->ix.nnz * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        KBG_CUDA(cudaMemcpyAsync(&mi, c->d_check, sizeof(mi), cudaMemcpyDeviceToHost, c->stream));
+        KBG_CUDA(cudaStreamSynchronize(c->stream));
+        if (max_imag) std::memcpy(max_imag, &mi, sizeof(double));
+        c->tally.flops = 8.0 * nk * c->ix.nnz;
+        c->tally.bytes = 8.0 * c->ix.nnz + 16.0 * nk * c->ix.nnz;
+    });
+}
+
 int kbg_last_tally(const kbg_ctx* c, kbg_tally* out) {
     if (!c || !out) return KBG_ERR_CONFIG;
     *out = c->tally;
@@ -544,6 +792,13 @@ int kbg_set_option(kbg_ctx* c, int option, int64_t value) {
         case KBG_OPT_PERSIST:
             c->persist = value ? 1 : 0;
             return KBG_OK;
+        case KBG_OPT_SCHEDULE:
+            if (value < 0 || value > 3) {
+                c->err = "set_option: schedule must be 0..3";
+                return KBG_ERR_CONFIG;
+            }
+            c->schedule = static_cast<int>(value);
+            return KBG_OK;
         case KBG_OPT_DEBUG_COUNTERS:
             if (value && !c->d_dbg) {
                 if (cudaMalloc(&c->d_dbg, 16 * sizeof(unsigned long long)) != cudaSuccess) return KBG_ERR_CUDA;
@@ -562,6 +817,9 @@ void kbg_destroy(kbg_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     kbg::free_index(c->ix);
+    kbg::free_formats(c->fmt);
+    for (double* p : {c->d_fa, c->d_fb, c->d_phase, c->d_kw})
+        if (p) cudaFree(p);
     if (c->d_tau) cudaFree(c->d_tau);
     if (c->d_spc) cudaFree(c->d_spc);
     if (c->d_tables) cudaFree(c->d_tables);

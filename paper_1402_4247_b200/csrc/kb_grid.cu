@@ -10,6 +10,19 @@ namespace {
 
 using namespace core;
 
+// Tasks of this warp: its LPT lists, or every NW-th task of a single queue
+// (task_warps == 1, the persistent kernels' dynamic schedule) -- a fixed
+// assignment either way, so rho stays deterministic.
+template <int NW, class F>
+__device__ __forceinline__ void for_warp_tasks(const GridArgs& g, const Smem& sm, int warp, F&& f) {
+    if (g.task_warps == 1) {
+        for (int e = warp; e < sm.wptr()[1]; e += NW) f(e);
+    } else {
+        for (int w = warp; w < g.task_warps; w += NW)
+            for (int e = sm.wptr()[w]; e < sm.wptr()[w + 1]; ++e) f(e);
+    }
+}
+
 template <int NW>
 __global__ void __launch_bounds__(NW * 32, 2) k_hamiltonian(GridArgs g) {
     const Smem sm = carve(0u, g, static_cast<size_t>(g.nspin) * 64);
@@ -19,9 +32,8 @@ __global__ void __launch_bounds__(NW * 32, 2) k_hamiltonian(GridArgs g) {
     if (ncov == 0) return;
     for (int spin = 0; spin < g.nspin; ++spin) {
         double* Hs = g.out + spin * g.nnz;
-        for (int w = warp; w < g.task_warps; w += NW)
-            for (int e = sm.wptr()[w]; e < sm.wptr()[w + 1]; ++e)
-                h_task(sm, sm.acc() + spin * 64, ncov, sm.task()[e], Hs, g.sign, g.scatter, lane);
+        for_warp_tasks<NW>(g, sm, warp,
+                           [&](int e) { h_task(sm, sm.acc() + spin * 64, ncov, sm.task()[e], Hs, g.sign, g.scatter, lane); });
     }
 }
 
@@ -37,8 +49,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_density(GridArgs g) {
         for (int spin = 0; spin < g.nspin; ++spin) {
             const double* Dr = g.dmr + spin * g.nrep;
             double* racc = sm.acc() + (spin * NW + warp) * 64;
-            for (int w = warp; w < g.task_warps; w += NW)
-                for (int e = sm.wptr()[w]; e < sm.wptr()[w + 1]; ++e) rho_task(sm, ncov, sm.task()[e], Dr, racc, lane);
+            for_warp_tasks<NW>(g, sm, warp, [&](int e) { rho_task(sm, ncov, sm.task()[e], Dr, racc, lane); });
         }
         __syncthreads();
     }

@@ -188,10 +188,33 @@ void build_index_device(const SysParams& sys, DevIndex& ix, cudaStream_t st);
 void free_index(DevIndex& ix);
 void copy_index_to_host(const DevIndex& ix, HostIndex& h, cudaStream_t st);
 
+// Orbital / offset tables of the format converters (kb_formats.cu), built
+// lazily from the host index: orbital row of atom a, orbital i = orb_off[a] + i.
+struct FormatIndex {
+    int n = 0, natom = 0, nR = 0;
+    std::vector<int32_t> R;           // distinct pair offsets, sorted, 3 per entry
+    int32_t* orb_atom = nullptr;      // [n] atom of each orbital row
+    int32_t* orb_off = nullptr;       // [natom + 1]
+    int32_t* run = nullptr;           // [natom * natom][2] pair range of atom pair (a, b), sorted by R
+    int32_t* rid = nullptr;           // [npair] index of pair_R[p] in R
+    bool valid = false;
+};
+void free_formats(FormatIndex& f);
+int launch_phase(int nk, int64_t npair, const double* d_kpts, const int32_t* pair_R, double sign, double2* d_phase,
+                 cudaStream_t st);
+int launch_bloch(const FormatIndex& f, const DevIndex& ix, int nk, const double* d_M, const double2* d_phase,
+                 double* d_out, cudaStream_t st);
+int launch_fold(const FormatIndex& f, const DevIndex& ix, int nk, const double* d_w, const double2* d_phase,
+                const double* d_rho_k, double* d_out, unsigned long long* d_max_imag, cudaStream_t st);
+int launch_realspace(const FormatIndex& f, const DevIndex& ix, bool to_dense, double* d_sparse, double* d_dense,
+                     cudaStream_t st);
+
 // Grid kernels (kb_grid.cu). Return number of kernel launches.
 size_t grid_smem_bytes(const GridArgs& g, int nwarps, bool density);
 // Task lists (kb_tasks.cu), built after the index.
-void build_tasks_device(const SysParams& sys, DevIndex& ix, int h_warps, int r_warps, cudaStream_t st);
+// h_warps / r_warps: warps the H / rho lists are LPT-balanced over (1: one
+// queue, heaviest first); r_split: rho partner ranges are cut for this many warps.
+void build_tasks_device(const SysParams& sys, DevIndex& ix, int h_warps, int r_warps, int r_split, cudaStream_t st);
 void free_tasks(DevIndex& ix);
 int launch_density(const GridArgs& g, int64_t nblk_owned, int nwarps, cudaStream_t st);
 int launch_hamiltonian(const GridArgs& g, int64_t nblk_owned, int nwarps, cudaStream_t st);

@@ -90,10 +90,17 @@ __device__ __forceinline__ Buffers carve_all(const GridArgs& g, size_t acc) {
     return B;
 }
 
+// acc section: H w[nspin][64]; rho per-warp sums [nspin][NC][64] (static
+// lists) or per-task sums [nspin][ntask][32] (task queue, task_warps == 1).
+__host__ __device__ inline size_t persist_acc(const GridArgs& g, bool density) {
+    if (!density) return static_cast<size_t>(g.nspin) * 64;
+    if (g.task_warps == 1) return static_cast<size_t>(g.nspin) * g.max_tasks * 32;
+    return static_cast<size_t>(g.nspin) * 64 * kPersistConsumersR;
+}
+
 __host__ __device__ inline size_t persist_bytes(const GridArgs& g, bool density) {
     size_t off[12];
-    const size_t acc = static_cast<size_t>(g.nspin) * 64 * (density ? kPersistConsumersR : 1);
-    return 2 * align16(buffer_layout(g, acc, off)) + 64;
+    return 2 * align16(buffer_layout(g, persist_acc(g, density), off)) + 64;
 }
 
 // Next non-empty owned block from the work counter (-1: none left); empty
@@ -187,6 +194,13 @@ __device__ void producer(const GridArgs& g, const Buffers& B, int lane) {
             mbar_arrive_tx(&B.full[s], tb + pb);
             bulk_g2s(sm.meta(), tab, tb, &B.full[s]);
             bulk_g2s(sm.phi(), phi, pb, &B.full[s]);
+            if (g.dbg) {  // debug only: copy latency (delays the next fetch)
+                const unsigned long long tc = clock64();
+                mbar_wait(&B.full[s], (k >> 1) & 1);
+                atomicAdd(&g.dbg[7], clock64() - tc);
+                atomicAdd(&g.dbg[8], 1ull);
+                atomicAdd(&g.dbg[11], static_cast<unsigned long long>(tb + pb));
+            }
         }
         __syncwarp();
     }
@@ -202,6 +216,7 @@ __device__ void consumer(const GridArgs& g, const Buffers& B, int cw, int lane) 
         mbar_wait(&B.full[s], (k >> 1) & 1);
         const unsigned long long dw = clock64() - tw;
         t_wait += dw;
+        if (g.dbg && k < 2 && lane == 0) atomicAdd(&g.dbg[6], dw);
         const Smem sm = B.buf(s);
         const int64_t b = sm.meta()->block;
         if (b < 0) {
@@ -215,6 +230,27 @@ __device__ void consumer(const GridArgs& g, const Buffers& B, int cw, int lane) 
             return;
         }
         const int ncov = sm.meta()->ncov;
+        const int ntask = sm.wptr()[1];
+        if (g.task_warps == 1) {
+            // task queue, heaviest first: (spin, task) pairs pulled one at a time
+            for (;;) {
+                int q = 0;
+                if (lane == 0) q = atomicAdd(&sm.meta()->next, 1);
+                q = __shfl_sync(0xffffffffu, q, 0);
+                if (q >= g.nspin * ntask) break;
+                const int spin = q >= ntask, e = q - spin * ntask;
+                const Task t = sm.task()[e];
+                if (DENSITY) {
+                    // partial sums of this task's octet half, at its own slot
+                    double* res = sm.acc() + static_cast<size_t>(q) * 32;
+                    res[lane] = 0.0;
+                    __syncwarp();
+                    rho_task(sm, ncov, t, g.dmr + spin * g.nrep, res - 32 * t.half, lane, g.scatter);
+                } else {
+                    h_task(sm, sm.acc() + spin * 64, ncov, t, g.out + spin * g.nnz, g.sign, g.scatter, lane);
+                }
+            }
+        } else
         for (int spin = 0; spin < g.nspin; ++spin) {
             if (DENSITY) {
                 const double* Dr = g.dmr + spin * g.nrep;
@@ -232,6 +268,7 @@ __device__ void consumer(const GridArgs& g, const Buffers& B, int cw, int lane) 
             }
         }
         __syncwarp();
+        const unsigned long long t_red = clock64();
         int last = 0;
         if (lane == 0) {
             __threadfence_block();
@@ -243,6 +280,25 @@ __device__ void consumer(const GridArgs& g, const Buffers& B, int cw, int lane) 
             if (DENSITY) {
                 int bi, bj, bk;
                 block_decode(g.sys, b, bi, bj, bk);
+                if (g.task_warps == 1) {
+                    // per-task sums in task order: lane l owns slots l (half 0) and 32 + l (half 1)
+                    for (int spin = 0; spin < g.nspin; ++spin) {
+                        const double* res = sm.acc() + static_cast<size_t>(spin) * ntask * 32;
+                        double r0 = 0.0, r1 = 0.0;
+                        for (int e = 0; e < ntask; ++e) {
+                            const double v = res[e * 32 + lane];
+                            if (sm.task()[e].half)
+                                r1 += v;
+                            else
+                                r0 += v;
+                        }
+                        for (int hh = 0; hh < 2; ++hh) {
+                            bool valid;
+                            const int64_t pt = slot_point(g.sys, bi, bj, bk, 32 * hh + lane, valid);
+                            if (valid) g.out[spin * g.npts + pt] = hh ? r1 : r0;
+                        }
+                    }
+                } else
                 for (int i = lane; i < g.nspin * 64; i += 32) {
                     const int spin = i >> 6, p = i & 63;
                     double r = 0.0;
@@ -254,15 +310,17 @@ __device__ void consumer(const GridArgs& g, const Buffers& B, int cw, int lane) 
                 }
                 __syncwarp();
             }
-            if (lane == 0) mbar_arrive(&B.empty[s]);
+            if (lane == 0) {
+                mbar_arrive(&B.empty[s]);
+                if (g.dbg) atomicAdd(&g.dbg[10], clock64() - t_red);
+            }
         }
     }
 }
 
 template <bool DENSITY>
 __global__ void __launch_bounds__(Cfg<DENSITY>::NT, 1) k_persist(GridArgs g) {
-    const size_t acc = static_cast<size_t>(g.nspin) * 64 * (DENSITY ? Cfg<DENSITY>::NC : 1);
-    const Buffers B = carve_all(g, acc);
+    const Buffers B = carve_all(g, persist_acc(g, DENSITY));
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int s = 0; s < 2; ++s) {

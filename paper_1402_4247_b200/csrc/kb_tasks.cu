@@ -214,7 +214,7 @@ void free_tasks(DevIndex& ix) {
     ix.blk_rows = nullptr;
 }
 
-void build_tasks_device(const SysParams& P, DevIndex& ix, int h_warps, int r_warps, cudaStream_t st) {
+void build_tasks_device(const SysParams& P, DevIndex& ix, int h_warps, int r_warps, int r_split, cudaStream_t st) {
     free_tasks(ix);
     ix.htask_warps = h_warps;
     ix.rtask_warps = r_warps;
@@ -229,7 +229,7 @@ void build_tasks_device(const SysParams& P, DevIndex& ix, int h_warps, int r_war
     KBG_CUDA(cudaMemsetAsync(d_st, 0, sizeof(TaskStats), st));
     if (!ix.blk_rows) ix.blk_rows = talloc<int32_t>(nb);
     k_tasks<<<grid, T, 0, st>>>(P, nb, ix.blk_ptr, ix.cov_atom, ix.cov_mask, hcnt, rcnt, nullptr, nullptr, nullptr,
-                                nullptr, d_st, ix.blk_rows, r_warps);
+                                nullptr, d_st, ix.blk_rows, r_split);
     KBG_CUDA(cudaGetLastError());
     ix.ht_ptr = talloc<int64_t>(nb + 1);
     ix.rt_ptr = talloc<int64_t>(nb + 1);
@@ -238,7 +238,7 @@ void build_tasks_device(const SysParams& P, DevIndex& ix, int h_warps, int r_war
     Task* htmp = talloc<Task>(ix.nhtask);
     Task* rtmp = talloc<Task>(ix.nrtask);
     k_tasks<<<grid, T, 0, st>>>(P, nb, ix.blk_ptr, ix.cov_atom, ix.cov_mask, nullptr, nullptr, ix.ht_ptr, ix.rt_ptr,
-                                htmp, rtmp, d_st, nullptr, r_warps);
+                                htmp, rtmp, d_st, nullptr, r_split);
     KBG_CUDA(cudaGetLastError());
     ix.ht = talloc<Task>(ix.nhtask);
     ix.rt = talloc<Task>(ix.nrtask);

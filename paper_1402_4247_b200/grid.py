@@ -116,6 +116,85 @@ class GridPass:
         self._check(self._lib.kbg_hamiltonian_mirror_dev(self._h, h.shape[0], h.data_ptr(),
                                                          self._stream_ptr(stream)), "kbg_hamiltonian_mirror_dev")
 
+    # -- formats either side (see formats.py for the SPEC types) --
+    def offsets(self) -> np.ndarray:
+        """Distinct lattice offsets R of the pair list, sorted, shape (nR, 3)."""
+        n = C.c_int()
+        self._check(self._lib.kbg_offsets(self._h, C.byref(n), None), "kbg_offsets")
+        R = np.empty((n.value, 3), dtype=np.int32)
+        self._check(self._lib.kbg_offsets(self._h, C.byref(n), R.ctypes.data_as(C.POINTER(C.c_int32))),
+                    "kbg_offsets")
+        return R
+
+    def nbasis(self) -> int:
+        return int(self.system.nbasis)
+
+    def _pairs(self, x) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        if x.shape != (self._nnz(),):
+            raise_for_status(_abi.KBG_ERR_DIMENSION, "pairs", f"expected ({self._nnz()},) values, got {x.shape}")
+        return x
+
+    def to_realspace(self, pairs: np.ndarray) -> np.ndarray:
+        """pair-sparse (nnz,) -> dense blocks (nR, n, n) in offsets() order."""
+        pairs = self._pairs(pairs)
+        n = self.nbasis()
+        out = np.empty((len(self.offsets()), n, n))
+        self._check(self._lib.kbg_to_realspace(self._h, _abi.dptr(pairs), _abi.dptr(out)), "kbg_to_realspace")
+        return out
+
+    def from_realspace(self, blocks: np.ndarray) -> np.ndarray:
+        n = self.nbasis()
+        blocks = np.ascontiguousarray(blocks, dtype=np.float64)
+        if blocks.shape != (len(self.offsets()), n, n):
+            raise_for_status(_abi.KBG_ERR_DIMENSION, "from_realspace", f"blocks shape {blocks.shape}")
+        out = np.empty(self._nnz())
+        self._check(self._lib.kbg_from_realspace(self._h, _abi.dptr(blocks), _abi.dptr(out)), "kbg_from_realspace")
+        return out
+
+    def bloch(self, pairs: np.ndarray, kpts) -> np.ndarray:
+        """M(k) = sum_R exp(+2 pi i k.R) M_R for each k (fractional), (nk, n, n) complex."""
+        pairs = self._pairs(pairs)
+        k = np.ascontiguousarray(np.atleast_2d(kpts), dtype=np.float64)
+        n = self.nbasis()
+        out = np.empty((k.shape[0], n, n), dtype=np.complex128)
+        self._check(self._lib.kbg_bloch(self._h, _abi.dptr(pairs), k.shape[0], _abi.dptr(k),
+                                        out.ctypes.data_as(_abi._DP)), "kbg_bloch")
+        return out
+
+    def fold(self, rho_k: np.ndarray, kpts, weights) -> tuple[np.ndarray, float]:
+        """DM_R = Re sum_k w_k exp(-2 pi i k.R) rho_k on the pair list; returns (pairs, max |imag|)."""
+        k = np.ascontiguousarray(np.atleast_2d(kpts), dtype=np.float64)
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        n = self.nbasis()
+        rho_k = np.ascontiguousarray(rho_k, dtype=np.complex128)
+        if rho_k.shape != (k.shape[0], n, n) or w.shape != (k.shape[0],):
+            raise_for_status(_abi.KBG_ERR_DIMENSION, "fold", f"rho_k {rho_k.shape}, weights {w.shape}, nk {k.shape[0]}")
+        out = np.empty(self._nnz())
+        mi = C.c_double()
+        self._check(self._lib.kbg_fold(self._h, k.shape[0], _abi.dptr(k), _abi.dptr(w),
+                                       rho_k.ctypes.data_as(_abi._DP), _abi.dptr(out), C.byref(mi)), "kbg_fold")
+        return out, mi.value
+
+    def bloch_dev(self, pairs, kpts, out, stream=None) -> None:
+        k = np.ascontiguousarray(np.atleast_2d(kpts), dtype=np.float64)
+        self._check(self._lib.kbg_bloch_dev(self._h, pairs.data_ptr(), k.shape[0], _abi.dptr(k), out.data_ptr(),
+                                            self._stream_ptr(stream)), "kbg_bloch_dev")
+
+    def fold_dev(self, rho_k, kpts, weights, out, stream=None) -> None:
+        k = np.ascontiguousarray(np.atleast_2d(kpts), dtype=np.float64)
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        self._check(self._lib.kbg_fold_dev(self._h, k.shape[0], _abi.dptr(k), _abi.dptr(w), rho_k.data_ptr(),
+                                           out.data_ptr(), self._stream_ptr(stream)), "kbg_fold_dev")
+
+    def to_realspace_dev(self, pairs, blocks, stream=None) -> None:
+        self._check(self._lib.kbg_to_realspace_dev(self._h, pairs.data_ptr(), blocks.data_ptr(),
+                                                   self._stream_ptr(stream)), "kbg_to_realspace_dev")
+
+    def from_realspace_dev(self, blocks, pairs, stream=None) -> None:
+        self._check(self._lib.kbg_from_realspace_dev(self._h, blocks.data_ptr(), pairs.data_ptr(),
+                                                     self._stream_ptr(stream)), "kbg_from_realspace_dev")
+
     @property
     def last_launches(self) -> int:
         return int(self._lib.kbg_last_launches(self._h))

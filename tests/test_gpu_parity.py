@@ -155,6 +155,23 @@ def test_kernel_modes_agree(persist):
     assert normwise(h, c.o.hamiltonian(c.veff, c.f.dV)) <= TOL
 
 
+@pytest.mark.parametrize("schedule", [0, 1, 2])
+def test_schedules_agree(schedule):
+    """Static LPT lists and the per-block task queue (KBG_OPT_SCHEDULE) give the same results; rho stays
+    bitwise deterministic under the queue (per-task partial sums reduced in task order)."""
+    c = case("cubic56_200Ry")
+    gp = GridPass(c.f.system)
+    gp.set_option(_abi.KBG_OPT_SCHEDULE, schedule)
+    gp.build_index()
+    rho = gp.density(c.dm)
+    h = gp.hamiltonian(c.veff, c.f.dV)
+    assert np.array_equal(rho, gp.density(c.dm))
+    assert normwise(rho, c.gp.density(c.dm)) <= 1e-14
+    assert normwise(h, c.gp.hamiltonian(c.veff, c.f.dV)) <= 1e-13
+    with pytest.raises(ConfigError):
+        gp.set_option(_abi.KBG_OPT_SCHEDULE, 4)
+
+
 def test_sharded_contexts_sum_to_full():
     """Two rank contexts on one GPU: disjoint rho shards and partial H sum to the full pass."""
     from paper_1402_4247_b200.shard import block_costs, partition

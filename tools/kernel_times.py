@@ -25,15 +25,11 @@ def main():
     ap.add_argument("--config", default="cubic56_200Ry")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--nspin", type=int, default=1)
+    ap.add_argument("--schedules", default="3,0,1,2", help="KBG_OPT_SCHEDULE values (persistent kernels)")
+    ap.add_argument("--fallback", type=int, default=1, help="also time the one-CTA-per-block kernels")
     a = ap.parse_args()
     f = Fe3O4.config(a.config)
-    gp = GridPass(f.system)
-    ix = gp.build_index()
     dev = torch.device("cuda", 0)
-    d_dm = torch.from_numpy(f.dm(ix, nspin=a.nspin)).to(dev)
-    d_v = torch.from_numpy(f.veff(nspin=a.nspin)).to(dev)
-    rho = torch.empty((a.nspin, f.system.npts), dtype=torch.float64, device=dev)
-    h = torch.empty((a.nspin, ix["nnz"]), dtype=torch.float64, device=dev)
     flush = torch.empty(512 << 18, dtype=torch.float32, device=dev)
     st = torch.cuda.current_stream()
 
@@ -51,25 +47,41 @@ def main():
             ts.append(e0.elapsed_time(e1))
         return float(np.median(ts)), float(np.min(ts))
 
-    f_rho = a.nspin * (2 * ix["sum_m2"] + 2 * ix["sum_m"])
-    f_h = a.nspin * 2 * ix["sum_m2"]
-    for warps, persist in ((8, 1), (8, 0)):
-        gp.set_option(_abi.KBG_OPT_WARPS, warps)
+    ref = {}
+    variants = [(int(x), 1) for x in a.schedules.split(",")] + ([(3, 0)] if a.fallback else [])
+    for sched, persist in variants:
+        gp = GridPass(f.system)
+        gp.set_option(_abi.KBG_OPT_SCHEDULE, sched)
+        ix = gp.build_index()
         gp.set_option(_abi.KBG_OPT_PERSIST, persist)
-        for name, fn, fl in (
-            ("density", lambda: gp.density_dev(d_dm, rho, st), f_rho),
-            ("h_accumulate", lambda: gp.hamiltonian_accumulate_dev(d_v, f.dV, h, st), f_h),
+        d_dm = torch.from_numpy(f.dm(ix, nspin=a.nspin)).to(dev)
+        d_v = torch.from_numpy(f.veff(nspin=a.nspin)).to(dev)
+        rho = torch.empty((a.nspin, f.system.npts), dtype=torch.float64, device=dev)
+        h = torch.empty((a.nspin, ix["nnz"]), dtype=torch.float64, device=dev)
+        f_rho = a.nspin * (2 * ix["sum_m2"] + 2 * ix["sum_m"])
+        f_h = a.nspin * 2 * ix["sum_m2"]
+        for name, fn, fl, out in (
+            ("density", lambda: gp.density_dev(d_dm, rho, st), f_rho, rho),
+            ("h_accumulate", lambda: gp.hamiltonian_accumulate_dev(d_v, f.dV, h, st), f_h, h),
         ):
             med, mn = timeit(fn)
-            print(json.dumps({"config": a.config, "kernel": name, "warps": warps, "persist": persist,
-                              "median_ms": round(med, 4),
-                              "min_ms": round(mn, 4), "alg_tflops": round(fl / (med * 1e-3) / 1e12, 3)}))
-        gp.set_option(_abi.KBG_OPT_SCATTER_STORE, 1)
-        med, mn = timeit(lambda: gp.hamiltonian_accumulate_dev(d_v, f.dV, h, st))
-        gp.set_option(_abi.KBG_OPT_SCATTER_STORE, 0)
-        print(json.dumps({"config": a.config, "kernel": "h_accumulate_store_scatter(experiment)", "warps": warps,
-                          "persist": persist,
-                          "median_ms": round(med, 4), "min_ms": round(mn, 4)}))
+            out.zero_()
+            fn()
+            torch.cuda.synchronize()
+            r1 = out.clone()
+            out.zero_()
+            fn()
+            torch.cuda.synchronize()
+            rec = {"config": a.config, "lib": os.environ.get("KBG_LIBKBGRID", "default"), "kernel": name, "schedule": sched, "persist": persist,
+                   "median_ms": round(med, 4), "min_ms": round(mn, 4),
+                   "alg_tflops": round(fl / (med * 1e-3) / 1e12, 3),
+                   "bitwise_repeat": bool(torch.equal(r1, out))}
+            if name in ref:
+                rec["rel_diff_vs_first"] = float((out - ref[name]).norm() / ref[name].norm())
+            else:
+                ref[name] = r1
+            print(json.dumps(rec), flush=True)
+        del gp
 
 
 if __name__ == "__main__":

@@ -30,12 +30,17 @@ def main(cfg="cubic56_200Ry"):
         gp.set_option(_abi.KBG_OPT_DEBUG_COUNTERS, 1)
         fn()
         torch.cuda.synchronize()
-        out = (C.c_int64 * 6)()
-        gp._lib.kbg_debug_counters(gp.handle, out, 6)
-        p_wait, p_tot, c_wait, c_tail, c_tot, blocks = list(out)
+        out = (C.c_int64 * 12)()
+        gp._lib.kbg_debug_counters(gp.handle, out, 12)
+        p_wait, p_tot, c_wait, c_tail, c_tot, blocks, c_start, cp_lat, ncopy, _, red, cp_bytes = list(out)
         print(json.dumps({"kernel": name, "producer_wait_frac": round(p_wait / max(1, p_tot), 3),
                           "consumer_wait_frac": round(c_wait / max(1, c_tot), 3),
                           "consumer_tail_frac": round(c_tail / max(1, c_tot), 3),
+                          "consumer_start_frac": round(c_start / max(1, c_tot), 3),
+                          "copy_latency_cycles": round(cp_lat / max(1, ncopy)),
+                          "copy_bytes_avg": round(cp_bytes / max(1, ncopy)),
+                          "reduce_release_cycles": round(red / max(1, ncopy)),
+                          "cycles_per_block_per_sm": round(p_tot / max(1, ncopy)),
                           "consumer_blocks": blocks, "consumer_cycles": c_tot}))
 
 
