@@ -237,6 +237,15 @@ int kbg_fold(kbg_ctx* ctx, int nk, const double* kpts, const double* w, const do
 int kbg_fold_dev(kbg_ctx* ctx, int nk, const double* kpts, const double* w, const double* d_rho_k, double* d_pairs,
                  void* stream);
 
+/* Part 6 density matrix at one k from the states of the eigenvector pass
+ * (SPEC.md:279): rho_k = sum_i w_i c_i c_i^H, C: [n][m] complex row-major
+ * (column i = state i), w: m real weights -- occupations f_i for the charge
+ * density matrix, eps_i f_i for the energy density matrix. out: [n][n]
+ * complex. One ZGEMM (cuBLAS; a plain library GEMM) after a weight kernel. */
+int kbg_density_matrix_k(kbg_ctx* ctx, int m, const double* C, const double* w, double* rho);
+int kbg_density_matrix_k_dev(kbg_ctx* ctx, int m, const double* d_C, const double* d_w, double* d_rho,
+                             void* stream);
+
 /* Library identification: "kbgrid <version> sm_100a". */
 const char* kbg_version(void);
 

@@ -121,6 +121,8 @@ KBGRID_SYMBOLS = [
     ("kbg_bloch_dev", _I, [_P, _P, _I, _DP, _P, _P]),
     ("kbg_fold", _I, [_P, _I, _DP, _DP, _DP, _DP, _DP]),
     ("kbg_fold_dev", _I, [_P, _I, _DP, _DP, _P, _P, _P]),
+    ("kbg_density_matrix_k", _I, [_P, _I, _DP, _DP, _DP]),
+    ("kbg_density_matrix_k_dev", _I, [_P, _I, _P, _P, _P, _P]),
 ]
 
 KBGSYNTH_SYMBOLS = [

@@ -8,6 +8,8 @@
 #include <string>
 #include <vector>
 
+#include <cublas_v2.h>
+
 #include "kb_device.cuh"
 
 struct kbg_ctx {
@@ -52,6 +54,12 @@ struct kbg_ctx {
     size_t cap_phase = 0;
     double* d_kw = nullptr;  // kpts (3 nk) then weights (nk)
     size_t cap_kw = 0;
+    double* h_kw = nullptr;  // pinned staging of d_kw (async copy); h_kw_done: its last copy finished
+    size_t cap_hkw = 0;
+    cudaEvent_t h_kw_done = nullptr;
+    cublasHandle_t blas = nullptr;  // Part 6 density matrix (ZGEMM)
+    double* d_states = nullptr;     // scaled states scratch
+    size_t cap_states = 0;
 };
 
 namespace {
@@ -556,13 +564,17 @@ const kbg::FormatIndex& formats(kbg_ctx* c) {
     std::vector<std::array<int32_t, 3>> uniq = R;
     std::sort(uniq.begin(), uniq.end());
     uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
-    std::vector<int32_t> rid(npair), run(2 * static_cast<size_t>(natom) * natom, 0);
+    std::vector<int32_t> rid(npair), run(2 * static_cast<size_t>(natom) * natom, 0), runs;
     for (int64_t p = 0; p < npair; ++p) {
         rid[p] = static_cast<int32_t>(std::lower_bound(uniq.begin(), uniq.end(), R[p]) - uniq.begin());
         const size_t ab = static_cast<size_t>(h.pair_a[p]) * natom + h.pair_b[p];
-        if (run[2 * ab] == run[2 * ab + 1]) run[2 * ab] = static_cast<int32_t>(p);  // pairs sorted by (a, b, R)
+        if (run[2 * ab] == run[2 * ab + 1]) {  // pairs sorted by (a, b, R): first pair of a run
+            run[2 * ab] = static_cast<int32_t>(p);
+            runs.push_back(static_cast<int32_t>(p));
+        }
         run[2 * ab + 1] = static_cast<int32_t>(p + 1);
     }
+    runs.push_back(static_cast<int32_t>(npair));
     f.n = off[natom];
     f.natom = natom;
     f.nR = static_cast<int>(uniq.size());
@@ -576,6 +588,8 @@ const kbg::FormatIndex& formats(kbg_ctx* c) {
     up(f.orb_off, off);
     up(f.run, run);
     up(f.rid, rid);
+    up(f.runs, runs);
+    f.nrun = static_cast<int>(runs.size()) - 1;
     f.valid = true;
     return f;
 }
@@ -589,9 +603,20 @@ void check_nk(int nk, const double* kpts) {
 
 // k points (and weights) to the device, phases exp(sign 2 pi i k.R_p) per (k, pair)
 const double2* phases(kbg_ctx* c, int nk, const double* kpts, const double* w, double sign, cudaStream_t st) {
-    ensure(c->d_kw, c->cap_kw, 4 * static_cast<size_t>(nk));
-    KBG_CUDA(cudaMemcpyAsync(c->d_kw, kpts, 3 * nk * sizeof(double), cudaMemcpyHostToDevice, st));
-    if (w) KBG_CUDA(cudaMemcpyAsync(c->d_kw + 3 * nk, w, nk * sizeof(double), cudaMemcpyHostToDevice, st));
+    const size_t nkw = 4 * static_cast<size_t>(nk);
+    ensure(c->d_kw, c->cap_kw, nkw);
+    if (!c->h_kw_done) KBG_CUDA(cudaEventCreateWithFlags(&c->h_kw_done, cudaEventDisableTiming));
+    KBG_CUDA(cudaEventSynchronize(c->h_kw_done));  // previous copy out of the staging buffer is done
+    if (c->cap_hkw < nkw) {
+        if (c->h_kw) cudaFreeHost(c->h_kw);
+        c->h_kw = nullptr;
+        KBG_CUDA(cudaMallocHost(&c->h_kw, nkw * sizeof(double)));
+        c->cap_hkw = nkw;
+    }
+    std::copy(kpts, kpts + 3 * nk, c->h_kw);
+    if (w) std::copy(w, w + nk, c->h_kw + 3 * nk);
+    KBG_CUDA(cudaMemcpyAsync(c->d_kw, c->h_kw, nkw * sizeof(double), cudaMemcpyHostToDevice, st));
+    KBG_CUDA(cudaEventRecord(c->h_kw_done, st));
     ensure(c->d_phase, c->cap_phase, 2 * static_cast<size_t>(nk) * std::max<int64_t>(1, c->ix.npair));
     c->last_launches =
         kbg::launch_phase(nk, c->ix.npair, c->d_kw, c->ix.pair_R, sign, reinterpret_cast<double2*>(c->d_phase), st);
@@ -767,6 +792,57 @@ int kbg_fold(kbg_ctx* c, int nk, const double* kpts, const double* w, const doub
     });
 }
 
+namespace {
+
+void density_matrix_k(kbg_ctx* c, int m, const double* d_C, const double* d_w, double* d_rho, cudaStream_t st) {
+    const int n = formats(c).n;
+    if (m < 1 || m > n) throw Error(KBG_ERR_DIMENSION, "density_matrix_k: m = " + std::to_string(m) +
+                                                           " states for n = " + std::to_string(n) + " orbitals");
+    if (!c->blas && cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) throw Error(KBG_ERR_CUDA, "cublasCreate failed");
+    ensure(c->d_states, c->cap_states, 2 * static_cast<size_t>(n) * m);
+    c->last_launches = kbg::launch_scale_states(n, m, d_C, d_w, c->d_states, st);
+    // row-major C (n x m) is column-major Ct = C^T (m x n, ld m); row-major
+    // rho = column-major rho^T = Ct^H (W Ct): one ZGEMM
+    const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+    if (cublasSetStream(c->blas, st) != CUBLAS_STATUS_SUCCESS ||
+        cublasZgemm(c->blas, CUBLAS_OP_C, CUBLAS_OP_N, n, n, m, &one, reinterpret_cast<const cuDoubleComplex*>(d_C), m,
+                    reinterpret_cast<const cuDoubleComplex*>(c->d_states), m, &zero,
+                    reinterpret_cast<cuDoubleComplex*>(d_rho), n) != CUBLAS_STATUS_SUCCESS)
+        throw Error(KBG_ERR_CUDA, "density_matrix_k: cublasZgemm failed");
+    c->last_launches += 1;
+    c->tally.flops = 8.0 * n * n * m;
+    c->tally.bytes = 16.0 * (static_cast<double>(n) * m + static_cast<double>(n) * n);
+}
+
+}  // namespace
+
+int kbg_density_matrix_k_dev(kbg_ctx* c, int m, const double* d_C, const double* d_w, double* d_rho, void* stream) {
+    if (!c || !d_C || !d_w || !d_rho) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        KBG_CUDA(cudaSetDevice(c->device));
+        density_matrix_k(c, m, d_C, d_w, d_rho, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int kbg_density_matrix_k(kbg_ctx* c, int m, const double* C, const double* w, double* rho) {
+    if (!c || !C || !w || !rho) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        KBG_CUDA(cudaSetDevice(c->device));
+        const int n = formats(c).n;
+        if (m < 1 || m > n) throw Error(KBG_ERR_DIMENSION, "density_matrix_k: m = " + std::to_string(m));
+        for (int i = 0; i < m; ++i)
+            if (!std::isfinite(w[i])) throw Error(KBG_ERR_NONFINITE, "density_matrix_k: weight " + std::to_string(i));
+        const size_t nc = 2 * static_cast<size_t>(n) * m, nr = 2 * static_cast<size_t>(n) * n;
+        ensure(c->d_fa, c->cap_fa, nc + m);
+        ensure(c->d_fb, c->cap_fb, nr);
+        KBG_CUDA(cudaMemcpyAsync(c->d_fa, C, nc * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        KBG_CUDA(cudaMemcpyAsync(c->d_fa + nc, w, m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        density_matrix_k(c, m, c->d_fa, c->d_fa + nc, c->d_fb, c->stream);
+        KBG_CUDA(cudaMemcpyAsync(rho, c->d_fb, nr * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        KBG_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
 int kbg_last_tally(const kbg_ctx* c, kbg_tally* out) {
     if (!c || !out) return KBG_ERR_CONFIG;
     *out = c->tally;
@@ -820,6 +896,10 @@ void kbg_destroy(kbg_ctx* c) {
     kbg::free_formats(c->fmt);
     for (double* p : {c->d_fa, c->d_fb, c->d_phase, c->d_kw})
         if (p) cudaFree(p);
+    if (c->h_kw) cudaFreeHost(c->h_kw);
+    if (c->d_states) cudaFree(c->d_states);
+    if (c->blas) cublasDestroy(c->blas);
+    if (c->h_kw_done) cudaEventDestroy(c->h_kw_done);
     if (c->d_tau) cudaFree(c->d_tau);
     if (c->d_spc) cudaFree(c->d_spc);
     if (c->d_tables) cudaFree(c->d_tables);

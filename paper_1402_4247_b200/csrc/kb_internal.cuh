@@ -197,6 +197,8 @@ struct FormatIndex {
     int32_t* orb_off = nullptr;       // [natom + 1]
     int32_t* run = nullptr;           // [natom * natom][2] pair range of atom pair (a, b), sorted by R
     int32_t* rid = nullptr;           // [npair] index of pair_R[p] in R
+    int32_t* runs = nullptr;          // [nrun + 1] first pair of each distinct (a, b), pairs sorted by (a, b, R)
+    int nrun = 0;
     bool valid = false;
 };
 void free_formats(FormatIndex& f);
@@ -208,6 +210,7 @@ int launch_fold(const FormatIndex& f, const DevIndex& ix, int nk, const double* 
                 const double* d_rho_k, double* d_out, unsigned long long* d_max_imag, cudaStream_t st);
 int launch_realspace(const FormatIndex& f, const DevIndex& ix, bool to_dense, double* d_sparse, double* d_dense,
                      cudaStream_t st);
+int launch_scale_states(int n, int m, const double* d_C, const double* d_w, double* d_D, cudaStream_t st);
 
 // Grid kernels (kb_grid.cu). Return number of kernel launches.
 size_t grid_smem_bytes(const GridArgs& g, int nwarps, bool density);

@@ -108,6 +108,16 @@ def bloch_transform(gp: GridPass, pairs: np.ndarray, k) -> np.ndarray:
     return out[0] if k.ndim == 1 else out
 
 
+def density_matrices_k(gp: GridPass, C: np.ndarray, f, eps=None):
+    """Part 6 at one k: rho_k = sum_i f_i c_i c_i^dagger and, with eps, the energy density
+    matrix E_k = sum_i eps_i f_i c_i c_i^dagger. C: (n, m) states as columns. GPU (one ZGEMM each)."""
+    f = np.asarray(f, dtype=np.float64)
+    rho = gp.density_matrix_k(C, f)
+    if eps is None:
+        return rho
+    return rho, gp.density_matrix_k(C, np.asarray(eps, dtype=np.float64) * f)
+
+
 def fold_density_matrices(gp: GridPass, rho_k: np.ndarray, kset: KPointSet, imag_tol: float = 1e-10) -> np.ndarray:
     """Part 6 folding: DM_R = sum_k w_k exp(-2 pi i k.R) rho_k on the pair list.
     The grid pass takes a real DM; an imaginary part above imag_tol * max|DM| (a k set without
@@ -121,4 +131,4 @@ def fold_density_matrices(gp: GridPass, rho_k: np.ndarray, kset: KPointSet, imag
 
 
 __all__ = ["KPointSet", "RealSpaceOperator", "to_realspace_operator", "from_realspace_operator",
-           "bloch_transform", "fold_density_matrices"]
+           "bloch_transform", "density_matrices_k", "fold_density_matrices"]

@@ -176,6 +176,22 @@ class GridPass:
                                        rho_k.ctypes.data_as(_abi._DP), _abi.dptr(out), C.byref(mi)), "kbg_fold")
         return out, mi.value
 
+    def density_matrix_k(self, C: np.ndarray, w) -> np.ndarray:
+        """rho_k = sum_i w_i c_i c_i^H from states C (n, m) complex (columns = states)."""
+        C = np.ascontiguousarray(C, dtype=np.complex128)
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        n = self.nbasis()
+        if C.ndim != 2 or C.shape[0] != n or w.shape != (C.shape[1],):
+            raise_for_status(_abi.KBG_ERR_DIMENSION, "density_matrix_k", f"C {C.shape}, w {w.shape}, n {n}")
+        out = np.empty((n, n), dtype=np.complex128)
+        self._check(self._lib.kbg_density_matrix_k(self._h, C.shape[1], C.ctypes.data_as(_abi._DP), _abi.dptr(w),
+                                                   out.ctypes.data_as(_abi._DP)), "kbg_density_matrix_k")
+        return out
+
+    def density_matrix_k_dev(self, C, w, out, stream=None) -> None:
+        self._check(self._lib.kbg_density_matrix_k_dev(self._h, C.shape[1], C.data_ptr(), w.data_ptr(), out.data_ptr(),
+                                                       self._stream_ptr(stream)), "kbg_density_matrix_k_dev")
+
     def bloch_dev(self, pairs, kpts, out, stream=None) -> None:
         k = np.ascontiguousarray(np.atleast_2d(kpts), dtype=np.float64)
         self._check(self._lib.kbg_bloch_dev(self._h, pairs.data_ptr(), k.shape[0], _abi.dptr(k), out.data_ptr(),

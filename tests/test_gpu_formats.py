@@ -7,7 +7,7 @@ import pytest
 
 from oracle import formats as F
 from paper_1402_4247_b200.errors import ConsistencyError
-from paper_1402_4247_b200.formats import (KPointSet, bloch_transform, fold_density_matrices,
+from paper_1402_4247_b200.formats import (KPointSet, bloch_transform, density_matrices_k, fold_density_matrices,
                                           from_realspace_operator, to_realspace_operator)
 from paper_1402_4247_b200.grid import GridPass
 from paper_1402_4247_b200.system import Fe3O4
@@ -120,3 +120,67 @@ def test_device_variants_match_host():
     assert np.array_equal(d_out.cpu().numpy().view(np.complex128)[..., 0], host)
     assert np.array_equal(d_back.cpu().numpy(), gp.fold(host, ks, np.array([0.5, 0.5]))[0])
     assert np.array_equal(d_h2.cpu().numpy(), h)
+
+
+def _states(n, m, seed):
+    rng = np.random.default_rng(seed)
+    z = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    q, _ = np.linalg.qr(z)  # orthonormal columns: C^H S C = I with S = I
+    return q[:, :m]
+
+
+def test_density_matrix_k_parity_and_spec_examples():
+    """SPEC.md:279-283: rho_k = sum_i f_i c_i c_i^dagger; step occupation -> c1c1^dagger + c2c2^dagger;
+    f = 0 -> rho = 0; trace identity Tr(rho_k S_k) = sum_i f_i (S = I, orthonormal states)."""
+    f_, gp, ix, dm, h, args = setup("primitive14_150Ry")
+    n = gp.nbasis()
+    C = _states(n, 40, 5)
+    f = 1.0 / (1.0 + np.exp(np.linspace(-3, 3, 40)))
+    eps = np.linspace(-1, 1, 40)
+    rho, E = density_matrices_k(gp, C, f, eps)
+    ref = (C * f) @ C.conj().T
+    assert normwise(rho, ref) <= TOL
+    assert normwise(E, (C * (eps * f)) @ C.conj().T) <= TOL
+    assert np.abs(rho - rho.conj().T).max() <= 1e-14 * np.abs(rho).max()
+    assert abs(np.trace(rho).real - f.sum()) <= 1e-10
+    step = np.zeros(4)
+    step[:2] = 1.0
+    C4 = _states(n, 4, 9)
+    r2 = gp.density_matrix_k(C4, step)
+    exact = np.outer(C4[:, 0], C4[:, 0].conj()) + np.outer(C4[:, 1], C4[:, 1].conj())
+    assert np.abs(r2 - exact).max() <= 1e-14
+    assert np.abs(gp.density_matrix_k(C4, np.zeros(4))).max() == 0.0
+
+
+def test_part6_chain_to_grid_density():
+    """States at every k of a full grid -> rho_k (GPU) -> fold (GPU) -> grid density (GPU): the grid
+    electron count sum_r rho(r) dV equals sum_ab Tr(DM_ab S_ba) (SURVEY.md 8(c) identity 1)."""
+    f_, gp, ix, dm, h, args = setup("primitive14_150Ry")
+    n = gp.nbasis()
+    ks = KPointSet.monkhorst_pack(2, 2, 2)
+    rho_k = []
+    for i, k in enumerate(ks.points):
+        C = _states(n, 30, 100 + i)
+        rho_k.append(gp.density_matrix_k(C, np.full(30, 0.5)))
+    # time-reversal partner of each k on this grid is itself (k = -k mod 1): symmetrise
+    rho_k = np.stack([0.5 * (r + r.conj()) for r in rho_k])
+    dm_pairs = fold_density_matrices(gp, rho_k, ks)
+    # the folded DM must satisfy the grid pass's DM invariant to be accepted (symmetrise over R <-> -R)
+    mir = ix["pair_mirror"]
+    norb = f_.system.norb_of_atom()
+    sym = dm_pairs.copy()
+    for p in range(len(mir)):
+        q = mir[p]
+        na, nb = norb[ix["pair_a"][p]], norb[ix["pair_b"][p]]
+        blk = dm_pairs[ix["pair_off"][p]:ix["pair_off"][p + 1]].reshape(na, nb)
+        other = dm_pairs[ix["pair_off"][q]:ix["pair_off"][q + 1]].reshape(nb, na)
+        sym[ix["pair_off"][p]:ix["pair_off"][p + 1]] = (0.5 * (blk + other.T)).ravel()
+    rho = gp.density(sym)[0]
+    S = gp.hamiltonian(np.ones(f_.system.npts), f_.dV)[0]
+    tr = 0.0
+    for p in range(len(mir)):
+        q = mir[p]
+        na, nb = norb[ix["pair_a"][p]], norb[ix["pair_b"][p]]
+        tr += np.sum(sym[ix["pair_off"][p]:ix["pair_off"][p + 1]].reshape(na, nb)
+                     * S[ix["pair_off"][q]:ix["pair_off"][q + 1]].reshape(nb, na).T)
+    assert abs(rho.sum() * f_.dV - tr) <= 1e-10 * max(1.0, abs(tr))
