@@ -26,7 +26,7 @@ __global__ void k_phi_count(int64_t b0, int64_t n, const int32_t* __restrict__ r
 
 __global__ void __launch_bounds__(256) k_build_cache(GridArgs gh, GridArgs gr, const int64_t* __restrict__ phi_off,
                                                      unsigned char* htab, unsigned char* rtab, double* phis) {
-    const Smem sm = carve(0u, gh, 0);
+    const Smem sm = carve(0u, gh);
     const int64_t i = blockIdx.x;
     const int64_t b = gh.blk_begin + i;
     const int tid = threadIdx.x, nt = blockDim.x;
@@ -89,8 +89,9 @@ void build_cache_device(GridArgs gh, GridArgs gr, DevIndex& ix, cudaStream_t st)
     KBG_CUDA(cudaMalloc(&ix.htab, n * T));
     KBG_CUDA(cudaMalloc(&ix.rtab, n * T));
     KBG_CUDA(cudaMalloc(&ix.phis, std::max<int64_t>(1, ix.phi_doubles) * sizeof(double)));
-    size_t off[12];
-    const size_t smem = buffer_layout(gh, 0, off);
+    set_layout(gh, 0);
+    set_layout(gr, 0);
+    const size_t smem = gh.lay[12];
     KBG_CUDA(cudaFuncSetAttribute(k_build_cache, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     k_build_cache<<<static_cast<unsigned>(n), 256, smem, st>>>(gh, gr, ix.phi_off, ix.htab, ix.rtab, ix.phis);
     KBG_CUDA(cudaGetLastError());

@@ -25,7 +25,7 @@ __device__ __forceinline__ void for_warp_tasks(const GridArgs& g, const Smem& sm
 
 template <int NW>
 __global__ void __launch_bounds__(NW * 32, 2) k_hamiltonian(GridArgs g) {
-    const Smem sm = carve(0u, g, static_cast<size_t>(g.nspin) * 64);
+    const Smem sm = carve(0u, g);
     const int64_t b = g.blk_begin + blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ncov = stage_block(g, b, sm, tid, NW * 32, [] { __syncthreads(); }, false, NW);
@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_hamiltonian(GridArgs g) {
 
 template <int NW>
 __global__ void __launch_bounds__(NW * 32, 2) k_density(GridArgs g) {
-    const Smem sm = carve(0u, g, static_cast<size_t>(g.nspin) * NW * 64);
+    const Smem sm = carve(0u, g);
     const int64_t b = g.blk_begin + blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int bi, bj, bk;
@@ -169,7 +169,7 @@ __global__ void k_dm_check(SysParams P, int64_t npair, int nspin, int64_t nnz, c
 }
 
 __global__ void k_block_orbitals(GridArgs g, int64_t b, double* out) {
-    const Smem sm = carve(0u, g, static_cast<size_t>(g.nspin) * 64);
+    const Smem sm = carve(0u, g);
     const int ncov = stage_block(g, b, sm, threadIdx.x, blockDim.x, [] { __syncthreads(); }, false, 1);
     // rows in cover order
     int r0 = 0;
@@ -193,9 +193,11 @@ size_t grid_smem_bytes(const GridArgs& g, int nwarps, bool density) {
     return core::buffer_layout(g, static_cast<size_t>(g.nspin) * 64 * (density ? nwarps : 1), off);
 }
 
-int launch_density(const GridArgs& g, int64_t nblk, int nwarps, cudaStream_t st) {
+int launch_density(const GridArgs& g0, int64_t nblk, int nwarps, cudaStream_t st) {
     if (nblk <= 0) return 0;
+    GridArgs g = g0;
     const size_t smem = grid_smem_bytes(g, nwarps, true);
+    set_layout(g, static_cast<size_t>(g.nspin) * 64 * nwarps);
     if (nwarps == 4) {
         set_smem(k_density<4>, smem);
         k_density<4><<<static_cast<unsigned>(nblk), 128, smem, st>>>(g);
@@ -207,9 +209,11 @@ int launch_density(const GridArgs& g, int64_t nblk, int nwarps, cudaStream_t st)
     return 1;
 }
 
-int launch_hamiltonian(const GridArgs& g, int64_t nblk, int nwarps, cudaStream_t st) {
+int launch_hamiltonian(const GridArgs& g0, int64_t nblk, int nwarps, cudaStream_t st) {
     if (nblk <= 0) return 0;
+    GridArgs g = g0;
     const size_t smem = grid_smem_bytes(g, nwarps, false);
+    set_layout(g, static_cast<size_t>(g.nspin) * 64);
     if (nwarps == 4) {
         set_smem(k_hamiltonian<4>, smem);
         k_hamiltonian<4><<<static_cast<unsigned>(nblk), 128, smem, st>>>(g);
@@ -250,8 +254,10 @@ int launch_dm_check(const DevIndex& ix, const SysParams& sys, int nspin, const d
     return 1;
 }
 
-int launch_block_orbitals(const GridArgs& g, int64_t block, double* d_out, cudaStream_t st) {
+int launch_block_orbitals(const GridArgs& g0, int64_t block, double* d_out, cudaStream_t st) {
+    GridArgs g = g0;
     const size_t smem = grid_smem_bytes(g, 1, false);
+    set_layout(g, static_cast<size_t>(g.nspin) * 64);
     set_smem(k_block_orbitals, smem);
     k_block_orbitals<<<1, 256, smem, st>>>(g, block, d_out);
     KBG_CUDA(cudaGetLastError());

@@ -147,24 +147,31 @@ __host__ __device__ inline size_t buffer_layout(const GridArgs& g, size_t acc_do
     return o;
 }
 
-// Buffer at byte offset `base` of kbg_smem.
-__device__ __forceinline__ Smem carve(uint32_t base, const GridArgs& g, size_t acc_doubles) {
+// Host: the layout of a buffer with `acc_doubles` accumulator doubles into
+// g.lay (every launcher calls this before launching).
+inline void set_layout(GridArgs& g, size_t acc_doubles) {
     size_t off[12];
-    buffer_layout(g, acc_doubles, off);
+    const size_t bytes = buffer_layout(g, acc_doubles, off);
+    for (int i = 0; i < 12; ++i) g.lay[i] = static_cast<uint32_t>(off[i]);
+    g.lay[12] = static_cast<uint32_t>(bytes);
+}
+
+// Buffer at byte offset `base` of kbg_smem, laid out as g.lay.
+__device__ __forceinline__ Smem carve(uint32_t base, const GridArgs& g) {
     Smem s;
     s.base = base;
-    s.o_meta = static_cast<uint32_t>(off[0]);
-    s.o_cov = static_cast<uint32_t>(off[1]);
-    s.o_grp = static_cast<uint32_t>(off[2]);
-    s.o_off2d = static_cast<uint32_t>(off[3]);
-    s.o_rcov = static_cast<uint32_t>(off[4]);
-    s.o_rorb = static_cast<uint32_t>(off[5]);
-    s.o_pom = static_cast<uint32_t>(off[6]);
-    s.o_pbits = static_cast<uint32_t>(off[7]);
-    s.o_task = static_cast<uint32_t>(off[8]);
-    s.o_wptr = static_cast<uint32_t>(off[9]);
-    s.o_acc = static_cast<uint32_t>(off[10]);
-    s.o_phi = static_cast<uint32_t>(off[11]);
+    s.o_meta = g.lay[0];
+    s.o_cov = g.lay[1];
+    s.o_grp = g.lay[2];
+    s.o_off2d = g.lay[3];
+    s.o_rcov = g.lay[4];
+    s.o_rorb = g.lay[5];
+    s.o_pom = g.lay[6];
+    s.o_pbits = g.lay[7];
+    s.o_task = g.lay[8];
+    s.o_wptr = g.lay[9];
+    s.o_acc = g.lay[10];
+    s.o_phi = g.lay[11];
     return s;
 }
 

@@ -181,6 +181,11 @@ struct GridArgs {
     int scatter;        // 0: atomic scatter (product); 1: plain stores (timing experiment only, wrong H)
     const double* in;   // dm [nspin][nnz] or veff [nspin][npts]
     double* out;        // rho [nspin][npts] or h [nspin][nnz]
+    // Shared-memory buffer layout of this launch (core::set_layout, by the
+    // launcher): section byte offsets [0, 12), buffer size [12]. Kernel
+    // parameters, so the compiler reloads them from the constant bank instead
+    // of recomputing the layout arithmetic under register pressure.
+    uint32_t lay[13];
 };
 
 // Index build (kb_index.cu). Fills `ix` (device) and returns host stats.

@@ -80,11 +80,10 @@ struct Buffers {
     }
 };
 
-__device__ __forceinline__ Buffers carve_all(const GridArgs& g, size_t acc) {
-    size_t off[12];
+__device__ __forceinline__ Buffers carve_all(const GridArgs& g) {
     Buffers B;
-    B.bsz = static_cast<uint32_t>(align16(buffer_layout(g, acc, off)));
-    B.sm0 = carve(0u, g, acc);
+    B.bsz = (g.lay[12] + 15u) & ~15u;
+    B.sm0 = carve(0u, g);
     B.full = reinterpret_cast<uint64_t*>(kbg_smem + 2 * B.bsz);
     B.empty = B.full + 2;
     return B;
@@ -320,7 +319,7 @@ __device__ void consumer(const GridArgs& g, const Buffers& B, int cw, int lane) 
 
 template <bool DENSITY>
 __global__ void __launch_bounds__(Cfg<DENSITY>::NT, 1) k_persist(GridArgs g) {
-    const Buffers B = carve_all(g, persist_acc(g, DENSITY));
+    const Buffers B = carve_all(g);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
         for (int s = 0; s < 2; ++s) {
@@ -342,13 +341,15 @@ void set_smem(K kernel, size_t bytes) {
     KBG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
 }
 
-int launch_persist(const GridArgs& g, bool density, cudaStream_t st) {
+int launch_persist(const GridArgs& g0, bool density, cudaStream_t st) {
+    GridArgs g = g0;
     if (g.norder <= 0) return 0;
     int dev = 0, sms = 0;
     KBG_CUDA(cudaGetDevice(&dev));
     KBG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const unsigned grid = static_cast<unsigned>(std::min<int64_t>(sms, g.norder));
     const size_t smem = persist_bytes(g, density);
+    set_layout(g, persist_acc(g, density));
     KBG_CUDA(cudaMemsetAsync(g.counter, 0, sizeof(int), st));
     if (density) {
         set_smem(k_persist<true>, smem);
