@@ -62,6 +62,13 @@ struct kbg_ctx {
     size_t cap_states = 0;
 };
 
+// rho partner ranges are cut at 1/(2 KBG_RHO_SPLIT) of a block's work
+// (kb_tasks.cu). With the per-block task queue, long tasks win: measured
+// density pass 0.421 ms (19), 0.392 (10), 0.376 (6), 0.379 (4 .. 1, no cuts).
+#ifndef KBG_RHO_SPLIT
+#define KBG_RHO_SPLIT 6
+#endif
+
 namespace {
 
 using kbg::Error;
@@ -343,7 +350,7 @@ int kbg_build_index(kbg_ctx* c) {
         // persistent kernels: one task queue (1 "warp") or LPT lists per consumer warp
         auto persist_tasks = [&](int sched) {
             kbg::build_tasks_device(c->P, c->ix, (sched & 1) ? 1 : kbg::kPersistConsumersH,
-                                    (sched & 2) ? 1 : kbg::kPersistConsumersR, kbg::kPersistConsumersR, c->stream);
+                                    (sched & 2) ? 1 : kbg::kPersistConsumersR, KBG_RHO_SPLIT, c->stream);
             const kbg::GridArgs gd = grid_args(c, 1, 0.0, nullptr, nullptr, true);
             const kbg::GridArgs gh = grid_args(c, 1, 0.0, nullptr, nullptr, false);
             return kbg::persist_fits(gd, true) && kbg::persist_fits(gh, false);
