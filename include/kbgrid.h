@@ -246,6 +246,15 @@ int kbg_density_matrix_k(kbg_ctx* ctx, int m, const double* C, const double* w, 
 int kbg_density_matrix_k_dev(kbg_ctx* ctx, int m, const double* d_C, const double* d_w, double* d_rho,
                              void* stream);
 
+/* HBM calibration probe (the paper's Table 2 experiment,
+ * PAPER.md:56): divide each of nvec vectors of len doubles
+ * (row-major, contiguous) by its Euclidean norm; zero vectors stay zero.
+ * Context-free; device is the current CUDA device. Host variant copies in and
+ * out through the library's own staging buffers (times the transfers the
+ * paper's Table 2 discussion is about). */
+int kbg_normalize_rows_dev(double* d_x, int64_t nvec, int64_t len, void* stream);
+int kbg_normalize_rows(double* x, int64_t nvec, int64_t len);
+
 /* Library identification: "kbgrid <version> sm_100a". */
 const char* kbg_version(void);
 

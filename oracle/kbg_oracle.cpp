@@ -652,5 +652,23 @@ extern "C" int kbo_orbitals_at(kbo_ctx* ctx, int species, const double* d, doubl
     return KBG_OK;
 }
 
+// Table 2 normalization: the host backend of
+// the HBM probe, x[v][:] /= ||x[v]||, rows split over `threads` in fixed
+// contiguous chunks; zero rows stay zero.
+extern "C" int kbo_normalize_rows(double* x, int64_t nvec, int64_t len, int threads) {
+    if (!x || nvec < 0 || len < 0) return KBG_ERR_CONFIG;
+    kbo::parallel_for(nvec, threads, [&](int64_t v0, int64_t v1) {
+        for (int64_t v = v0; v < v1; ++v) {
+            double* r = x + v * len;
+            double ss = 0.0;
+            for (int64_t i = 0; i < len; ++i) ss += r[i] * r[i];
+            if (ss == 0.0) continue;
+            const double nrm = std::sqrt(ss);
+            for (int64_t i = 0; i < len; ++i) r[i] /= nrm;
+        }
+    });
+    return KBG_OK;
+}
+
 extern "C" const char* kbo_last_error(const kbo_ctx* ctx) { return ctx ? ctx->o.last_error.c_str() : "null ctx"; }
 extern "C" void kbo_destroy(kbo_ctx* ctx) { delete ctx; }

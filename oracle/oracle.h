@@ -47,6 +47,8 @@ int kbo_block_orbitals(kbo_ctx* ctx, int64_t block, double* out, int64_t cap, in
  * (d2 computed by the library): out[norb]; zero if outside rc. */
 int kbo_orbitals_at(kbo_ctx* ctx, int species, const double* d, double* out);
 const char* kbo_last_error(const kbo_ctx* ctx);
+/* HBM probe host backend (Table 2 normalization). */
+int kbo_normalize_rows(double* x, int64_t nvec, int64_t len, int threads);
 void kbo_destroy(kbo_ctx* ctx);
 
 #ifdef __cplusplus

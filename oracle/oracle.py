@@ -31,6 +31,7 @@ SYMBOLS = [
     ("kbo_block_orbitals", _I, [_P, _I64, _DP, _I64, C.POINTER(_I)]),
     ("kbo_orbitals_at", _I, [_P, _I, _DP, _DP]),
     ("kbo_last_error", C.c_char_p, [_P]),
+    ("kbo_normalize_rows", _I, [_DP, _I64, _I64, _I]),
     ("kbo_destroy", None, [_P]),
 ]
 
@@ -107,3 +108,11 @@ class Oracle:
         if h:
             self._lib.kbo_destroy(h)
             self._h = None
+
+
+def normalize_rows(x: np.ndarray, threads: int = 1) -> np.ndarray:
+    """Host backend of the HBM probe (Table 2 normalization): rows of x divided by their norms."""
+    x = np.array(x, dtype=np.float64, order="C", copy=True)
+    nvec, n = (x.shape[0], x.shape[1]) if x.ndim == 2 else (1, x.shape[0])
+    raise_for_status(lib().kbo_normalize_rows(_abi.dptr(x), nvec, n, threads), "kbo_normalize_rows")
+    return x

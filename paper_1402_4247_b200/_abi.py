@@ -123,6 +123,8 @@ KBGRID_SYMBOLS = [
     ("kbg_fold_dev", _I, [_P, _I, _DP, _DP, _P, _P, _P]),
     ("kbg_density_matrix_k", _I, [_P, _I, _DP, _DP, _DP]),
     ("kbg_density_matrix_k_dev", _I, [_P, _I, _P, _P, _P, _P]),
+    ("kbg_normalize_rows_dev", _I, [_P, _I64, _I64, _P]),
+    ("kbg_normalize_rows", _I, [_DP, _I64, _I64]),
 ]
 
 KBGSYNTH_SYMBOLS = [

@@ -850,6 +850,28 @@ int kbg_density_matrix_k(kbg_ctx* c, int m, const double* C, const double* w, do
     });
 }
 
+int kbg_normalize_rows_dev(double* d_x, int64_t nvec, int64_t len, void* stream) {
+    if (!d_x || nvec < 0 || len < 0) return KBG_ERR_CONFIG;
+    return guard(nullptr, [&] { kbg::launch_normalize(d_x, nvec, len, static_cast<cudaStream_t>(stream)); });
+}
+
+int kbg_normalize_rows(double* x, int64_t nvec, int64_t len) {
+    if (!x || nvec < 0 || len < 0) return KBG_ERR_CONFIG;
+    return guard(nullptr, [&] {
+        const size_t n = static_cast<size_t>(nvec) * len;
+        if (n == 0) return;
+        double* d = nullptr;
+        KBG_CUDA(cudaMalloc(&d, n * sizeof(double)));
+        struct Free {
+            double* p;
+            ~Free() { cudaFree(p); }
+        } guard_d{d};
+        KBG_CUDA(cudaMemcpy(d, x, n * sizeof(double), cudaMemcpyHostToDevice));
+        kbg::launch_normalize(d, nvec, len, nullptr);
+        KBG_CUDA(cudaMemcpy(x, d, n * sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+
 int kbg_last_tally(const kbg_ctx* c, kbg_tally* out) {
     if (!c || !out) return KBG_ERR_CONFIG;
     *out = c->tally;

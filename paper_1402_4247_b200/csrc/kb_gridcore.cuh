@@ -332,6 +332,11 @@ __device__ __forceinline__ void h_scatter(const Smem& sm, const double (&c)[TM][
     }
 }
 
+// Timing experiment only (H is WRONG): skip the w scaling of the A fragments.
+#ifndef KBG_H_NOSCALE
+#define KBG_H_NOSCALE 0
+#endif
+
 // One partner: C(8*TM x 8*TN) += Phi_rows diag(w) Phi_cj^T over the quads in
 // qm. Tiles with <= 2 DMMAs per quad alternate two accumulator sets.
 template <int TM, int TN>
@@ -357,7 +362,7 @@ __device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict_
         const double wv = pw[col];
         double a[TM], bb[TN];
 #pragma unroll
-        for (int i = 0; i < TM; ++i) a[i] = pa[i * 512 + (col ^ sa)] * wv;
+        for (int i = 0; i < TM; ++i) a[i] = KBG_H_NOSCALE ? pa[i * 512 + (col ^ sa)] : pa[i * 512 + (col ^ sa)] * wv;
 #pragma unroll
         for (int j = 0; j < TN; ++j) bb[j] = pb[j * 512 + (col ^ sb)];
 #pragma unroll
@@ -417,7 +422,7 @@ __device__ __forceinline__ void h_tile2(const Smem& sm, const double* __restrict
         const double wv = pw[col];
         double a[TM];
 #pragma unroll
-        for (int i = 0; i < TM; ++i) a[i] = pa[i * 512 + (col ^ sa)] * wv;
+        for (int i = 0; i < TM; ++i) a[i] = KBG_H_NOSCALE ? pa[i * 512 + (col ^ sa)] : pa[i * 512 + (col ^ sa)] * wv;
         if ((q1 >> q) & 1u) {
             double bb[TN1];
 #pragma unroll

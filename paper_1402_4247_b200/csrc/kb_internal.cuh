@@ -17,7 +17,10 @@ constexpr int kMaxRad = 16;
 constexpr int kGroupRows = 16;  // covers are packed into row groups of <= 16 orbitals (2 DMMA row tiles)
 constexpr int kMaxTaskWarps = 32;  // task lists are LPT-balanced over <= 24 consumer warps
 constexpr int kMaxCoverPerBlock = 64;
-constexpr bool kRhoPrefetch = false;  // ping-pong D' prefetch (needs ~128 registers, 16 warps)
+#ifndef KBG_RHO_PREFETCH
+#define KBG_RHO_PREFETCH 0
+#endif
+constexpr bool kRhoPrefetch = KBG_RHO_PREFETCH;  // ping-pong D' prefetch (needs ~128 registers, 16 warps)
 constexpr int kRhoOct = 4;  // octets per rho task (4: halves of the block, 2: quarters; halves measured faster)
 
 // Error taxonomy of kband (common.hpp:21-38) carried as a status code.
@@ -216,6 +219,8 @@ int launch_fold(const FormatIndex& f, const DevIndex& ix, int nk, const double* 
 int launch_realspace(const FormatIndex& f, const DevIndex& ix, bool to_dense, double* d_sparse, double* d_dense,
                      cudaStream_t st);
 int launch_scale_states(int n, int m, const double* d_C, const double* d_w, double* d_D, cudaStream_t st);
+// HBM probe (kb_probe.cu): x[v][:] /= ||x[v]|| for nvec rows of len doubles.
+int launch_normalize(double* d_x, int64_t nvec, int64_t len, cudaStream_t st);
 
 // Grid kernels (kb_grid.cu). Return number of kernel launches.
 size_t grid_smem_bytes(const GridArgs& g, int nwarps, bool density);
@@ -233,8 +238,14 @@ int launch_dm_repack(const DevIndex& ix, const SysParams& sys, int nspin, const 
 // on block k (two shared-memory buffers). persist_fits() says whether two
 // buffers fit in shared memory for this index.
 constexpr int kPersistProducers = 1;
-constexpr int kPersistConsumersR = 19;  // rho: 20 warps (<= 102 registers per thread)
-constexpr int kPersistConsumersH = 27;  // H: 28 warps (<= 72 registers per thread)
+#ifndef KBG_CONSUMERS_R
+#define KBG_CONSUMERS_R 19
+#endif
+#ifndef KBG_CONSUMERS_H
+#define KBG_CONSUMERS_H 27
+#endif
+constexpr int kPersistConsumersR = KBG_CONSUMERS_R;  // rho: 20 warps (<= 102 registers per thread)
+constexpr int kPersistConsumersH = KBG_CONSUMERS_H;  // H: 28 warps (<= 72 registers per thread)
 // Geometry cache (kb_cache.cu): Phi and the per-block tables, built once per
 // geometry after the task lists.
 void build_cache_device(GridArgs gh, GridArgs gr, DevIndex& ix, cudaStream_t st);

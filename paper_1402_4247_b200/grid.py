@@ -18,6 +18,22 @@ from .errors import raise_for_status
 from .system import System
 
 
+def normalize_rows(x: np.ndarray) -> np.ndarray:
+    """HBM probe (Table 2 of the paper): each row of x divided by its norm, on the GPU
+    through the host C-ABI (transfers included)."""
+    x = np.array(x, dtype=np.float64, order="C", copy=True)
+    nvec, n = (x.shape[0], x.shape[1]) if x.ndim == 2 else (1, x.shape[0])
+    raise_for_status(_abi.kbgrid().kbg_normalize_rows(_abi.dptr(x), nvec, n), "kbg_normalize_rows")
+    return x
+
+
+def normalize_rows_dev(x, stream=None) -> None:
+    """In place on a CUDA tensor (nvec, n) float64."""
+    st = 0 if stream is None else int(stream.cuda_stream)
+    raise_for_status(_abi.kbgrid().kbg_normalize_rows_dev(x.data_ptr(), x.shape[0], x.shape[1], st),
+                     "kbg_normalize_rows_dev")
+
+
 class GridPass:
     def __init__(self, system: System, device: int = 0, rank: int = 0, nranks: int = 1):
         self._lib = _abi.kbgrid()

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--nspin", type=int, default=1)
     ap.add_argument("--schedules", default="3,0,1,2", help="KBG_OPT_SCHEDULE values (persistent kernels)")
     ap.add_argument("--fallback", type=int, default=1, help="also time the one-CTA-per-block kernels")
+    ap.add_argument("--scatter", type=int, default=0, help="KBG_OPT_SCATTER_STORE timing experiment bits")
     a = ap.parse_args()
     f = Fe3O4.config(a.config)
     dev = torch.device("cuda", 0)
@@ -54,6 +55,7 @@ def main():
         gp.set_option(_abi.KBG_OPT_SCHEDULE, sched)
         ix = gp.build_index()
         gp.set_option(_abi.KBG_OPT_PERSIST, persist)
+        gp.set_option(_abi.KBG_OPT_SCATTER_STORE, a.scatter)
         d_dm = torch.from_numpy(f.dm(ix, nspin=a.nspin)).to(dev)
         d_v = torch.from_numpy(f.veff(nspin=a.nspin)).to(dev)
         rho = torch.empty((a.nspin, f.system.npts), dtype=torch.float64, device=dev)
@@ -72,7 +74,7 @@ def main():
             out.zero_()
             fn()
             torch.cuda.synchronize()
-            rec = {"config": a.config, "lib": os.environ.get("KBG_LIBKBGRID", "default"), "kernel": name, "schedule": sched, "persist": persist,
+            rec = {"config": a.config, "lib": os.environ.get("KBG_LIBKBGRID", "default"), "scatter_exp": a.scatter, "kernel": name, "schedule": sched, "persist": persist,
                    "median_ms": round(med, 4), "min_ms": round(mn, 4),
                    "alg_tflops": round(fl / (med * 1e-3) / 1e12, 3),
                    "bitwise_repeat": bool(torch.equal(r1, out))}

@@ -64,7 +64,8 @@ def main(cfg="cubic56_200Ry", gr=16, straddle=False):
     spc = f.system.species_of_atom
     alg = ix["sum_m2"] / 2
     r = dict(exec=0.0, exactM=0.0, exactK=0.0, exactN=0.0)
-    h = dict(exec=0.0)
+    h = dict(exec=0.0, exactM=0.0, exactN=0.0, exactK=0.0, trimDiag=0.0)
+    r["trimDiag"] = 0.0
     nb = ix["nblock"]
     sample = range(0, nb, max(1, nb // 600))
     alg_s = 0.0
@@ -95,12 +96,21 @@ def main(cfg="cubic56_200Ry", gr=16, straddle=False):
                 r["exactK"] += tm * 8 * noct * 8 * norb[cj]
                 r["exactN"] += tm * 8 * popc(um) * ks * 4
                 nq = sum(quads(um))
+                # rows of the group's covers ci <= cj only (in-group partners trim the tile)
+                rows_le = sum(norb[c] for c in range(g0, min(g1, cj + 1)))
+                tm_t = (rows_le + 7) // 8
+                r["trimDiag"] += tm_t * 8 * noct * 8 * ks * 4
+                h["trimDiag"] += tm_t * 8 * ((norb[cj] + 7) // 8) * 8 * nq * 4
                 h["exec"] += tm * 8 * ((norb[cj] + 7) // 8) * 8 * nq * 4
+                h["exactM"] += rows * ((norb[cj] + 7) // 8) * 8 * nq * 4
+                h["exactN"] += tm * 8 * norb[cj] * nq * 4
+                h["exactK"] += tm * 8 * ((norb[cj] + 7) // 8) * 8 * popc(um)
     sc = alg / alg_s
     print(f"{cfg} group_rows={gr} straddle={straddle}: sampled {len(sample)} blocks; algorithmic half-count {alg:.4g} MAC")
     for k, v in r.items():
         print(f"  rho {k:7s} {v * sc / alg:6.3f} x algorithmic")
-    print(f"  H   exec    {h['exec'] * sc / alg:6.3f} x algorithmic")
+    for k, v in h.items():
+        print(f"  H   {k:7s} {v * sc / alg:6.3f} x algorithmic")
 
 
 if __name__ == "__main__":
