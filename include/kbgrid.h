@@ -255,6 +255,38 @@ int kbg_density_matrix_k_dev(kbg_ctx* ctx, int m, const double* d_C, const doubl
 int kbg_normalize_rows_dev(double* d_x, int64_t nvec, int64_t len, void* stream);
 int kbg_normalize_rows(double* x, int64_t nvec, int64_t len);
 
+/* ---- Eigen_HH on the GPU ----------------------------------
+ * The reference's Householder eigensolver pieces (kband, /root/reference/proj/
+ * include/kband/householder.hpp:56-82), context-free. Complex arrays are
+ * interleaved (re, im) doubles, row-major. The tridiagonal QL solve between
+ * tridiagonalize and back_transform stays with the caller (kband::
+ * solve_tridiag, tridiag.hpp:18-21; the paper runs LAPACK on the CPUs there).
+ * Errors: kband taxonomy status codes, message from kbg_hh_last_error(). */
+
+/* kband::tridiagonalize (householder.hpp:65-67): a [n][n] Hermitian (defect
+ * <= 1e-13, symmetrized like HermitianMatrix::from); out d [n], e [n-1] and the
+ * stage records: u [n-1][n] complex (reflector of stage i, zero above i+1 and
+ * for skipped stages), h, s [n-1], phase [n-1] complex. fault_sign != 0 flips
+ * the procedure-6 sign (ProcedurePlan::fault_proc6_sign). n <= 7000. The _dev
+ * variant destroys d_a (working matrix) and skips the Hermitian check. */
+int kbg_hh_tridiagonalize(int64_t n, const double* a, int fault_sign, double* d, double* e, double* u, double* h,
+                          double* s, double* phase);
+int kbg_hh_tridiagonalize_dev(int64_t n, double* d_a, int fault_sign, double* d_d, double* d_e, double* d_u,
+                              double* d_h, double* d_s, double* d_phase, void* stream);
+
+/* kband::back_transform (householder.hpp:69-72): W [n][m] complex = Q Y for the
+ * real tridiagonal-basis eigenvectors Y [n][m] (columns). */
+int kbg_hh_back_transform(int64_t n, int64_t m, const double* u, const double* h, const double* phase,
+                          const double* y, double* w);
+int kbg_hh_back_transform_dev(int64_t n, int64_t m, const double* d_u, const double* d_h, const double* d_phase,
+                              const double* d_y, double* d_w, void* stream);
+
+/* kband::normalize_columns (householder.hpp:74-76): columns of c [n][m]
+ * complex to unit 2-norm in place; a zero column is KBG_ERR_CONSISTENCY. */
+int kbg_hh_normalize_columns(int64_t n, int64_t m, double* c);
+int kbg_hh_normalize_columns_dev(int64_t n, int64_t m, double* d_c, void* stream);
+const char* kbg_hh_last_error(void);
+
 /* Library identification: "kbgrid <version> sm_100a". */
 const char* kbg_version(void);
 

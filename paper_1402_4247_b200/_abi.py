@@ -125,6 +125,13 @@ KBGRID_SYMBOLS = [
     ("kbg_density_matrix_k_dev", _I, [_P, _I, _P, _P, _P, _P]),
     ("kbg_normalize_rows_dev", _I, [_P, _I64, _I64, _P]),
     ("kbg_normalize_rows", _I, [_DP, _I64, _I64]),
+    ("kbg_hh_tridiagonalize", _I, [_I64, _DP, _I, _DP, _DP, _DP, _DP, _DP, _DP]),
+    ("kbg_hh_tridiagonalize_dev", _I, [_I64, _P, _I, _P, _P, _P, _P, _P, _P, _P]),
+    ("kbg_hh_back_transform", _I, [_I64, _I64, _DP, _DP, _DP, _DP, _DP]),
+    ("kbg_hh_back_transform_dev", _I, [_I64, _I64, _P, _P, _P, _P, _P, _P]),
+    ("kbg_hh_normalize_columns", _I, [_I64, _I64, _DP]),
+    ("kbg_hh_normalize_columns_dev", _I, [_I64, _I64, _P, _P]),
+    ("kbg_hh_last_error", C.c_char_p, []),
 ]
 
 KBGSYNTH_SYMBOLS = [

@@ -5,6 +5,7 @@
 #include <array>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -869,6 +870,163 @@ int kbg_normalize_rows(double* x, int64_t nvec, int64_t len) {
         KBG_CUDA(cudaMemcpy(d, x, n * sizeof(double), cudaMemcpyHostToDevice));
         kbg::launch_normalize(d, nvec, len, nullptr);
         KBG_CUDA(cudaMemcpy(x, d, n * sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+
+// ---- Eigen_HH on the GPU (kb_eigen.cu) ------------------
+namespace {
+
+thread_local std::string g_hh_err;
+
+int hh_guard(const std::function<void()>& fn) {
+    try {
+        fn();
+        g_hh_err.clear();
+        return KBG_OK;
+    } catch (const Error& e) {
+        g_hh_err = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_hh_err = e.what();
+        return KBG_ERR_CONSISTENCY;
+    }
+}
+
+// Stream-ordered device scratch freed at scope exit.
+struct DevBuf {
+    double* p = nullptr;
+    cudaStream_t st = nullptr;
+    DevBuf(size_t n, cudaStream_t s) : st(s) { KBG_CUDA(cudaMallocAsync(&p, std::max<size_t>(1, n) * sizeof(double), s)); }
+    ~DevBuf() {
+        if (p) cudaFreeAsync(p, st);
+    }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+};
+
+void hh_check_n(int64_t n) {
+    if (n < 1) throw Error(KBG_ERR_DIMENSION, "tridiagonalize: empty matrix");
+    if (n > 7000) throw Error(KBG_ERR_DIMENSION, "tridiagonalize: n = " + std::to_string(n) + " > 7000 (shared-memory reflector)");
+}
+
+// HermitianMatrix::from on the device (linalg.cpp:44-63): reject a defect above 1e-13, then symmetrize.
+void hermitian_from(int64_t n, double* d_A, cudaStream_t st) {
+    DevBuf def(1, st);
+    KBG_CUDA(cudaMemsetAsync(def.p, 0, sizeof(double), st));
+    kbg::launch_hermitian_repair(static_cast<int>(n), d_A, reinterpret_cast<unsigned long long*>(def.p), false, st);
+    double defect = 0.0;
+    KBG_CUDA(cudaMemcpyAsync(&defect, def.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    KBG_CUDA(cudaStreamSynchronize(st));
+    if (!std::isfinite(defect)) throw Error(KBG_ERR_CONSISTENCY, "HermitianMatrix: non-finite entries");
+    if (defect > 1e-13)
+        throw Error(KBG_ERR_CONSISTENCY, "HermitianMatrix: defect " + std::to_string(defect) + " exceeds tolerance 1e-13");
+    kbg::launch_hermitian_repair(static_cast<int>(n), d_A, nullptr, true, st);
+}
+
+void tridiag_dev(int64_t n, double* d_work, int fault_sign, double* d, double* e, double* u, double* h, double* s,
+                 double* ph, cudaStream_t st) {
+    DevBuf p(2 * n, st);
+    kbg::launch_hh_tridiagonalize(static_cast<int>(n), d_work, p.p, d, e, u, h, s, ph, fault_sign ? 1.0 : -1.0, st);
+}
+
+}  // namespace
+
+const char* kbg_hh_last_error(void) { return g_hh_err.c_str(); }
+
+int kbg_hh_tridiagonalize_dev(int64_t n, double* d_a, int fault_sign, double* d_d, double* d_e, double* d_u,
+                              double* d_h, double* d_s, double* d_phase, void* stream) {
+    if (!d_a || !d_d || !d_e || !d_u || !d_h || !d_s || !d_phase) return KBG_ERR_CONFIG;
+    return hh_guard([&] {
+        hh_check_n(n);
+        tridiag_dev(n, d_a, fault_sign, d_d, d_e, d_u, d_h, d_s, d_phase, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int kbg_hh_tridiagonalize(int64_t n, const double* a, int fault_sign, double* d, double* e, double* u, double* h,
+                          double* s, double* phase) {
+    if (!a || !d || !e || !u || !h || !s || !phase) return KBG_ERR_CONFIG;
+    return hh_guard([&] {
+        hh_check_n(n);
+        const cudaStream_t st = nullptr;
+        const size_t nn = static_cast<size_t>(n) * n, nr = static_cast<size_t>(n - 1);
+        DevBuf A(2 * nn, st), D(n, st), E(std::max<size_t>(1, nr), st), U(2 * nr * n, st), H(nr, st), S(nr, st),
+            P(2 * nr, st);
+        KBG_CUDA(cudaMemcpyAsync(A.p, a, 2 * nn * sizeof(double), cudaMemcpyHostToDevice, st));
+        hermitian_from(n, A.p, st);
+        tridiag_dev(n, A.p, fault_sign, D.p, E.p, U.p, H.p, S.p, P.p, st);
+        KBG_CUDA(cudaMemcpyAsync(d, D.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        if (nr) {
+            KBG_CUDA(cudaMemcpyAsync(e, E.p, nr * sizeof(double), cudaMemcpyDeviceToHost, st));
+            KBG_CUDA(cudaMemcpyAsync(u, U.p, 2 * nr * n * sizeof(double), cudaMemcpyDeviceToHost, st));
+            KBG_CUDA(cudaMemcpyAsync(h, H.p, nr * sizeof(double), cudaMemcpyDeviceToHost, st));
+            KBG_CUDA(cudaMemcpyAsync(s, S.p, nr * sizeof(double), cudaMemcpyDeviceToHost, st));
+            KBG_CUDA(cudaMemcpyAsync(phase, P.p, 2 * nr * sizeof(double), cudaMemcpyDeviceToHost, st));
+        }
+        KBG_CUDA(cudaStreamSynchronize(st));
+        for (size_t i = 0; i < nr; ++i)
+            if (!std::isfinite(s[i]) || !std::isfinite(h[i]))
+                throw Error(KBG_ERR_NONFINITE, "tridiagonalize: non-finite reflector at stage " + std::to_string(i));
+    });
+}
+
+int kbg_hh_back_transform_dev(int64_t n, int64_t m, const double* d_u, const double* d_h, const double* d_phase,
+                              const double* d_y, double* d_w, void* stream) {
+    if (!d_u || !d_h || !d_phase || !d_y || !d_w) return KBG_ERR_CONFIG;
+    return hh_guard([&] {
+        hh_check_n(n);
+        if (m < 1) throw Error(KBG_ERR_DIMENSION, "back_transform: no columns");
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        DevBuf dph(2 * n, st);
+        kbg::launch_hh_back_transform(static_cast<int>(n), static_cast<int>(m), d_y, d_u, d_h, d_phase, dph.p, d_w, st);
+    });
+}
+
+int kbg_hh_back_transform(int64_t n, int64_t m, const double* u, const double* h, const double* phase,
+                          const double* y, double* w) {
+    if (!u || !h || !phase || !y || !w) return KBG_ERR_CONFIG;
+    return hh_guard([&] {
+        hh_check_n(n);
+        if (m < 1) throw Error(KBG_ERR_DIMENSION, "back_transform: no columns");
+        const cudaStream_t st = nullptr;
+        const size_t nr = static_cast<size_t>(n - 1);
+        DevBuf U(2 * nr * n, st), H(nr, st), P(2 * nr, st), Y(static_cast<size_t>(n) * m, st),
+            W(2 * static_cast<size_t>(n) * m, st), dph(2 * n, st);
+        if (nr) {
+            KBG_CUDA(cudaMemcpyAsync(U.p, u, 2 * nr * n * sizeof(double), cudaMemcpyHostToDevice, st));
+            KBG_CUDA(cudaMemcpyAsync(H.p, h, nr * sizeof(double), cudaMemcpyHostToDevice, st));
+            KBG_CUDA(cudaMemcpyAsync(P.p, phase, 2 * nr * sizeof(double), cudaMemcpyHostToDevice, st));
+        }
+        KBG_CUDA(cudaMemcpyAsync(Y.p, y, static_cast<size_t>(n) * m * sizeof(double), cudaMemcpyHostToDevice, st));
+        kbg::launch_hh_back_transform(static_cast<int>(n), static_cast<int>(m), Y.p, U.p, H.p, P.p, dph.p, W.p, st);
+        KBG_CUDA(cudaMemcpyAsync(w, W.p, 2 * static_cast<size_t>(n) * m * sizeof(double), cudaMemcpyDeviceToHost, st));
+        KBG_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int kbg_hh_normalize_columns_dev(int64_t n, int64_t m, double* d_c, void* stream) {
+    if (!d_c) return KBG_ERR_CONFIG;
+    return hh_guard([&] {
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        DevBuf z(1, st);
+        const int big = 0x7fffffff;
+        KBG_CUDA(cudaMemcpyAsync(z.p, &big, sizeof(int), cudaMemcpyHostToDevice, st));
+        kbg::launch_hh_normalize_columns(n, m, d_c, reinterpret_cast<int*>(z.p), st);
+        int zero = big;
+        KBG_CUDA(cudaMemcpyAsync(&zero, z.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        KBG_CUDA(cudaStreamSynchronize(st));
+        if (zero != big) throw Error(KBG_ERR_CONSISTENCY, "normalize_columns: zero column " + std::to_string(zero));
+    });
+}
+
+int kbg_hh_normalize_columns(int64_t n, int64_t m, double* c) {
+    if (!c) return KBG_ERR_CONFIG;
+    return hh_guard([&] {
+        const size_t nm = 2 * static_cast<size_t>(n) * m;
+        DevBuf C(nm, nullptr);
+        KBG_CUDA(cudaMemcpyAsync(C.p, c, nm * sizeof(double), cudaMemcpyHostToDevice, nullptr));
+        const int st = kbg_hh_normalize_columns_dev(n, m, C.p, nullptr);
+        if (st != KBG_OK) throw Error(st, g_hh_err);
+        KBG_CUDA(cudaMemcpy(c, C.p, nm * sizeof(double), cudaMemcpyDeviceToHost));
     });
 }
 

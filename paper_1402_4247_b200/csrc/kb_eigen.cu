@@ -1,0 +1,350 @@
+// Eigen_HH on the GPU: the paper's hot path downstream of
+// the grid pass -- Householder tridiagonalization of the Hermitian H(k)
+// (procedures 1-6 per stage), the eigenvector rearrangement (back transform)
+// and the column normalization -- following the reference's kband
+// conventions exactly (/root/reference/proj/src/householder.cpp):
+//   tridiagonalize    householder.cpp:60-251 (records: reflector u, h, s, phase)
+//   back_transform    householder.cpp:253-305
+//   normalize_columns householder.cpp:307-331
+// The tridiagonal QL solve between them stays with the caller, as in the
+// paper (LAPACK dstevx/dstegr/dstedc on the CPUs).
+//
+// B200 design. The working matrix (n <= 6144: <= 604 MB, L2-resident up to
+// n ~ 2800) stays on the device. tridiagonalize is one cooperative persistent
+// kernel, one CTA per SM: per stage every CTA rebuilds the reflector from row
+// i (redundantly, fixed-order reductions -> identical in every CTA), warps
+// compute p = B u / h one row each (hemv, procedure 4), a grid barrier, every
+// CTA forms K and q (procedures 4-5), warps apply the rank-2 update to their
+// rows (her2, procedure 6), a second grid barrier. Both sweeps stream the
+// trailing block from L2: BLAS-2, bound by L2 bandwidth and the two grid
+// barriers per stage. back_transform gives each warp one eigenvector column,
+// kept in shared memory through all n - 1 reflectors (read from L2), so no
+// barrier is needed at all. All reductions have a fixed order: bitwise
+// deterministic run to run.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
+#include "kb_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace kbg {
+
+namespace {
+
+constexpr double kSkipNorm = 1e-300;  // householder.cpp:46
+constexpr int kTriThreads = 512;      // 16 warps per CTA
+constexpr int kTriWarps = kTriThreads / 32;
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// Fixed-order CTA sum of one double per thread (identical in every CTA).
+__device__ double cta_sum(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[w] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int i = 0; i < kTriWarps; ++i) t += red[i];
+    return t;
+}
+
+struct TriOut {
+    double* d;      // [n]
+    double* e;      // [n - 1]
+    double2* u;     // [n - 1][n]
+    double* h;      // [n - 1]
+    double* s;      // [n - 1]
+    double2* ph;    // [n - 1]
+};
+
+__global__ void __launch_bounds__(kTriThreads, 1) k_tridiag(int n, double2* __restrict__ B, double2* __restrict__ p,
+                                                            TriOut out, double sign) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double2 tri_smem[];
+    double2* u = tri_smem;      // [n]
+    double2* q = tri_smem + n;  // [n]
+    __shared__ double red[kTriWarps];
+    __shared__ double2 bcast[2];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int gwarp = blockIdx.x * kTriWarps + (tid >> 5), nwarp = gridDim.x * kTriWarps;
+    for (int i = 0; i + 1 < n; ++i) {
+        const int lo = i + 1;
+        __syncthreads();  // u, bcast of the previous stage fully consumed (a skipped stage has no grid barrier)
+        // procedure 1: u = column i below the diagonal (read as conj of row i: B stays Hermitian)
+        double s2 = 0.0;
+        for (int r = lo + tid; r < n; r += kTriThreads) {
+            const double2 b = B[static_cast<int64_t>(i) * n + r];
+            u[r] = make_double2(b.x, -b.y);
+            s2 += b.x * b.x + b.y * b.y;
+        }
+        // procedure 2: s, the pivot phase, h
+        s2 = cta_sum(s2, red);
+        const double s = sqrt(s2);
+        if (tid == 0) {
+            const double2 u0 = u[lo];
+            const double piv = hypot(u0.x, u0.y);
+            const double2 phs = piv > 0.0 ? make_double2(u0.x / piv, u0.y / piv) : make_double2(1.0, 0.0);
+            const double h = s >= kSkipNorm ? s * (s + piv) : 0.0;
+            if (h != 0.0) u[lo] = make_double2(u0.x + phs.x * s, u0.y + phs.y * s);
+            bcast[0] = phs;
+            bcast[1] = make_double2(h, 0.0);
+        }
+        __syncthreads();
+        const double2 phs = bcast[0];
+        const double h = bcast[1].x;
+        // procedure 3: the stage record (CTA 0)
+        if (blockIdx.x == 0) {
+            if (tid == 0) {
+                out.d[i] = B[static_cast<int64_t>(i) * n + i].x;
+                out.e[i] = h == 0.0 ? 0.0 : s;
+                out.h[i] = h;
+                out.s[i] = s;
+                out.ph[i] = h == 0.0 ? make_double2(1.0, 0.0) : make_double2(-phs.x, -phs.y);
+            }
+            double2* ui = out.u + static_cast<int64_t>(i) * n;
+            for (int r = tid; r < n; r += kTriThreads)
+                ui[r] = (h == 0.0 || r < lo) ? make_double2(0.0, 0.0) : u[r];
+        }
+        if (h == 0.0) continue;  // identity reflector: B unchanged, every CTA takes this branch
+        // procedure 4: p = B u / h over the active block, one warp per row
+        for (int r = lo + gwarp; r < n; r += nwarp) {
+            const double2* br = B + static_cast<int64_t>(r) * n;
+            double ar = 0.0, ai = 0.0;
+            for (int c = lo + lane; c < n; c += 32) {
+                const double2 x = br[c], y = u[c];
+                ar += x.x * y.x - x.y * y.y;
+                ai += x.x * y.y + x.y * y.x;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                ar += __shfl_xor_sync(0xffffffffu, ar, o);
+                ai += __shfl_xor_sync(0xffffffffu, ai, o);
+            }
+            if (lane == 0) p[r] = make_double2(ar / h, ai / h);
+        }
+        grid.sync();
+        // procedures 4 (dot) and 5: K = Re(p . u) / 2h, q = p - K u
+        double dr = 0.0;
+        for (int r = lo + tid; r < n; r += kTriThreads) {
+            const double2 pr = p[r];
+            q[r] = pr;
+            dr += pr.x * u[r].x + pr.y * u[r].y;
+        }
+        const double K = cta_sum(dr, red) / (2.0 * h);
+        for (int r = lo + tid; r < n; r += kTriThreads) {
+            const double2 pr = q[r], ur = u[r];
+            q[r] = make_double2(pr.x - K * ur.x, pr.y - K * ur.y);
+        }
+        __syncthreads();
+        // procedure 6: B += sign (u q^H + q u^H) on the active block, one warp per row
+        for (int r = lo + gwarp; r < n; r += nwarp) {
+            double2* br = B + static_cast<int64_t>(r) * n;
+            const double2 ur = u[r], qr = q[r];
+            for (int c = lo + lane; c < n; c += 32) {
+                const double2 qc = q[c], uc = u[c];
+                const double xr = ur.x * qc.x + ur.y * qc.y + qr.x * uc.x + qr.y * uc.y;
+                const double xi = ur.y * qc.x - ur.x * qc.y + qr.y * uc.x - qr.x * uc.y;
+                double2 b = br[c];
+                b.x += sign * xr;
+                b.y += sign * xi;
+                br[c] = b;
+            }
+        }
+        grid.sync();
+    }
+    if (blockIdx.x == 0 && tid == 0) out.d[n - 1] = B[static_cast<int64_t>(n - 1) * n + (n - 1)].x;
+}
+
+// Cumulative chased-out phases (householder.cpp:264-273), sequential like the
+// reference: dph[row] for rows 1..n-1, dph[0] = 1.
+__global__ void k_phase_prefix(int n, const double* __restrict__ h, const double2* __restrict__ ph,
+                               double2* __restrict__ dph) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double2 acc = make_double2(1.0, 0.0);
+    dph[0] = acc;
+    for (int k = 0; k + 1 < n; ++k) {
+        if (h[k] > 0.0) acc = cmul(acc, ph[k]);
+        dph[k + 1] = acc;
+    }
+}
+
+// W = Q Y: one warp per eigenvector column j, the column in shared memory;
+// reflectors applied in reverse stage order (householder.cpp:275-296).
+constexpr int kBtWarps = 4;  // max warps (columns) per CTA; fewer when n is large
+__global__ void __launch_bounds__(kBtWarps * 32) k_back_transform(int n, int m, const double* __restrict__ Y,
+                                                                  const double2* __restrict__ U,
+                                                                  const double* __restrict__ h,
+                                                                  const double2* __restrict__ dph,
+                                                                  double2* __restrict__ W) {
+    extern __shared__ double2 bt_smem[];
+    const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int j = blockIdx.x * (blockDim.x >> 5) + wi;
+    if (j >= m) return;
+    double2* w = bt_smem + static_cast<int64_t>(wi) * n;
+    for (int r = lane; r < n; r += 32) {
+        const double y = Y[static_cast<int64_t>(r) * m + j];
+        const double2 f = dph[r];
+        w[r] = r == 0 ? make_double2(y, 0.0) : make_double2(y * f.x, y * f.y);
+    }
+    __syncwarp();
+    for (int k = n - 2; k >= 0; --k) {
+        const double hk = h[k];
+        if (hk == 0.0) continue;
+        const int lo = k + 1;
+        const double2* uk = U + static_cast<int64_t>(k) * n;
+        double ar = 0.0, ai = 0.0;  // u^H w
+        for (int r = lo + lane; r < n; r += 32) {
+            const double2 x = uk[r], y = w[r];
+            ar += x.x * y.x + x.y * y.y;
+            ai += x.x * y.y - x.y * y.x;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            ar += __shfl_xor_sync(0xffffffffu, ar, o);
+            ai += __shfl_xor_sync(0xffffffffu, ai, o);
+        }
+        ar /= hk;
+        ai /= hk;
+        for (int r = lo + lane; r < n; r += 32) {
+            const double2 x = uk[r];
+            double2 y = w[r];
+            y.x -= x.x * ar - x.y * ai;
+            y.y -= x.x * ai + x.y * ar;
+            w[r] = y;
+        }
+        __syncwarp();
+    }
+    for (int r = lane; r < n; r += 32) W[static_cast<int64_t>(r) * m + j] = w[r];
+}
+
+// Columns to unit 2-norm in row order (linalg.cpp:214-218, householder.cpp:307-331):
+// one thread per column; exact products/sums so the norms match the reference bitwise.
+__global__ void k_normalize_columns(int64_t n, int64_t m, double2* __restrict__ C, int* __restrict__ zero_col) {
+    const int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (j >= m) return;
+    double s = 0.0;
+    for (int64_t r = 0; r < n; ++r) {
+        const double2 v = C[r * m + j];
+        s = __dadd_rn(s, __dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y)));
+    }
+    const double nrm = sqrt(s);
+    if (nrm < kSkipNorm) {
+        atomicMin(zero_col, static_cast<int>(j));
+        return;
+    }
+    const double inv = 1.0 / nrm;
+    for (int64_t r = 0; r < n; ++r) {
+        double2 v = C[r * m + j];
+        v.x = __dmul_rn(v.x, inv);
+        v.y = __dmul_rn(v.y, inv);
+        C[r * m + j] = v;
+    }
+}
+
+// HermitianMatrix::from (linalg.cpp:44-63): defect max |A_ij - conj(A_ji)|
+// (bit pattern, atomicMax), then A_ij = avg, A_ji = conj(avg), diagonal real.
+__global__ void k_hermitian_repair(int n, double2* __restrict__ A, unsigned long long* defect) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const int64_t nn = static_cast<int64_t>(n) * n;
+    double d = 0.0;
+    if (t < nn) {
+        const int i = static_cast<int>(t / n), j = static_cast<int>(t - static_cast<int64_t>(i) * n);
+        if (j >= i) {
+            const double2 a = A[t], b = A[static_cast<int64_t>(j) * n + i];
+            d = hypot(a.x - b.x, a.y + b.y);
+            if (!isfinite(a.x) || !isfinite(a.y) || !isfinite(b.x) || !isfinite(b.y)) d = __longlong_as_double(0x7ff0000000000000ll);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(defect, static_cast<unsigned long long>(__double_as_longlong(d)));
+}
+
+__global__ void k_hermitian_apply(int n, double2* __restrict__ A) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t >= static_cast<int64_t>(n) * n) return;
+    const int i = static_cast<int>(t / n), j = static_cast<int>(t - static_cast<int64_t>(i) * n);
+    if (j < i) return;
+    if (j == i) {
+        A[t].y = 0.0;
+        return;
+    }
+    const double2 a = A[t], b = A[static_cast<int64_t>(j) * n + i];
+    const double2 avg = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+    A[t] = avg;
+    A[static_cast<int64_t>(j) * n + i] = make_double2(avg.x, -avg.y);
+}
+
+}  // namespace
+
+int launch_hermitian_repair(int n, double* d_A, unsigned long long* d_defect, bool apply, cudaStream_t st) {
+    const int64_t nn = static_cast<int64_t>(n) * n;
+    if (nn == 0) return 0;
+    const unsigned grid = static_cast<unsigned>((nn + 255) / 256);
+    if (!apply)
+        k_hermitian_repair<<<grid, 256, 0, st>>>(n, reinterpret_cast<double2*>(d_A), d_defect);
+    else
+        k_hermitian_apply<<<grid, 256, 0, st>>>(n, reinterpret_cast<double2*>(d_A));
+    KBG_CUDA(cudaGetLastError());
+    return 1;
+}
+
+size_t hh_tridiag_smem(int n) { return 2 * static_cast<size_t>(n) * sizeof(double2); }
+
+int launch_hh_tridiagonalize(int n, double* d_B, double* d_p, double* d, double* e, double* u, double* h, double* s,
+                             double* ph, double sign, cudaStream_t st) {
+    if (n <= 0) return 0;
+    if (n == 1) {
+        KBG_CUDA(cudaMemcpyAsync(d, d_B, sizeof(double), cudaMemcpyDeviceToDevice, st));
+        return 0;
+    }
+    int dev = 0, sms = 0, per_sm = 0;
+    KBG_CUDA(cudaGetDevice(&dev));
+    KBG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const size_t smem = hh_tridiag_smem(n);
+    KBG_CUDA(cudaFuncSetAttribute(k_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    KBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tridiag, kTriThreads, smem));
+    if (per_sm < 1) throw Error(KBG_ERR_DIMENSION, "tridiagonalize: n too large for the cooperative kernel");
+    // rows per warp: no more CTAs than rows of work keep busy
+    const int grid = std::max(1, std::min(sms, (n + kTriWarps - 1) / kTriWarps));
+    TriOut o{d, e, reinterpret_cast<double2*>(u), h, s, reinterpret_cast<double2*>(ph)};
+    int nn = n;
+    double2* B = reinterpret_cast<double2*>(d_B);
+    double2* P = reinterpret_cast<double2*>(d_p);
+    void* args[] = {&nn, &B, &P, &o, &sign};
+    KBG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_tridiag), dim3(grid), dim3(kTriThreads), args,
+                                         smem, st));
+    KBG_CUDA(cudaGetLastError());
+    return 1;
+}
+
+int launch_hh_back_transform(int n, int m, const double* d_Y, const double* d_U, const double* d_h,
+                             const double* d_ph, double* d_dph, double* d_W, cudaStream_t st) {
+    if (n <= 0 || m <= 0) return 0;
+    k_phase_prefix<<<1, 32, 0, st>>>(n, d_h, reinterpret_cast<const double2*>(d_ph), reinterpret_cast<double2*>(d_dph));
+    const int nw = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kBtWarps, (227 * 1024) / (n * 16))));
+    const size_t smem = static_cast<size_t>(nw) * n * sizeof(double2);
+    KBG_CUDA(cudaFuncSetAttribute(k_back_transform, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    k_back_transform<<<static_cast<unsigned>((m + nw - 1) / nw), nw * 32, smem, st>>>(
+        n, m, d_Y, reinterpret_cast<const double2*>(d_U), d_h, reinterpret_cast<const double2*>(d_dph),
+        reinterpret_cast<double2*>(d_W));
+    KBG_CUDA(cudaGetLastError());
+    return 2;
+}
+
+int launch_hh_normalize_columns(int64_t n, int64_t m, double* d_C, int* d_zero, cudaStream_t st) {
+    if (n <= 0 || m <= 0) return 0;
+    k_normalize_columns<<<static_cast<unsigned>((m + 127) / 128), 128, 0, st>>>(n, m, reinterpret_cast<double2*>(d_C),
+                                                                               d_zero);
+    KBG_CUDA(cudaGetLastError());
+    return 1;
+}
+
+}  // namespace kbg

@@ -219,6 +219,14 @@ int launch_fold(const FormatIndex& f, const DevIndex& ix, int nk, const double* 
 int launch_realspace(const FormatIndex& f, const DevIndex& ix, bool to_dense, double* d_sparse, double* d_dense,
                      cudaStream_t st);
 int launch_scale_states(int n, int m, const double* d_C, const double* d_w, double* d_D, cudaStream_t st);
+// Eigen_HH (kb_eigen.cu). Complex arrays interleaved.
+size_t hh_tridiag_smem(int n);
+int launch_hermitian_repair(int n, double* d_A, unsigned long long* d_defect, bool apply, cudaStream_t st);
+int launch_hh_tridiagonalize(int n, double* d_B, double* d_p, double* d, double* e, double* u, double* h, double* s,
+                             double* ph, double sign, cudaStream_t st);
+int launch_hh_back_transform(int n, int m, const double* d_Y, const double* d_U, const double* d_h,
+                             const double* d_ph, double* d_dph, double* d_W, cudaStream_t st);
+int launch_hh_normalize_columns(int64_t n, int64_t m, double* d_C, int* d_zero, cudaStream_t st);
 // HBM probe (kb_probe.cu): x[v][:] /= ||x[v]|| for nvec rows of len doubles.
 int launch_normalize(double* d_x, int64_t nvec, int64_t len, cudaStream_t st);
 

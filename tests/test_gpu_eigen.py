@@ -1,0 +1,121 @@
+"""GPU Eigen_HH (kb_eigen.cu) against the reference's own kband (oracle/_ref).
+
+Bar: FP64, different reduction order than the serial reference, so tolerances are normwise relative to
+||A||_F: tridiagonal d, e and the reflectors <= 1e-12; back transform <= 1e-12; normalization bitwise
+(same operation order). Plus the SPEC/kband contracts: eigen residual ||A c - eps c|| <= 1e-9 ||A||_F,
+C^H C = I within 1e-9, the procedure-6 fault hook, errors, determinism, and a Bloch H(k) of the grid pass.
+"""
+import numpy as np
+import pytest
+
+from oracle import kband_ref as R
+from paper_1402_4247_b200 import eigen as E
+from paper_1402_4247_b200.errors import ConsistencyError, DimensionError
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not R.available(), reason="reference kband library not built")]
+
+
+def hermitian(n, seed, scale=1.0):
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    return scale * 0.5 * (x + x.conj().T)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built(built):
+    yield
+
+
+@pytest.mark.parametrize("n", [2, 3, 16, 97, 256, 568])
+def test_tridiagonalize_matches_reference(n):
+    a = hermitian(n, 100 + n)
+    nrm = np.linalg.norm(a)
+    t = E.tridiagonalize(a)
+    d, e, u, h, s, ph = R.tridiagonalize(a)
+    assert np.abs(t.d - d).max() <= 1e-12 * nrm
+    assert np.abs(t.e - e).max() <= 1e-12 * nrm
+    assert np.abs(t.records.h - h).max() <= 1e-12 * nrm * nrm
+    assert np.abs(t.records.s - s).max() <= 1e-12 * nrm
+    assert np.abs(t.records.phase - ph).max() <= 1e-10
+    assert np.abs(t.records.u - u).max() <= 1e-11 * max(1.0, np.abs(u).max())
+    for i in range(n - 1):
+        assert np.all(t.records.u[i, :i + 1] == 0)
+
+
+def test_tridiagonalize_skipped_stages_and_1x1():
+    """Diagonal input: every stage is an identity reflector (h = 0), e = 0 (householder.cpp:134-144)."""
+    a = np.diag([3.0, -1.0, 2.0, 0.5]).astype(np.complex128)
+    t = E.tridiagonalize(a)
+    assert np.array_equal(t.d, [3.0, -1.0, 2.0, 0.5])
+    assert np.array_equal(t.e, [0.0, 0.0, 0.0]) and np.array_equal(t.records.h, [0.0, 0.0, 0.0])
+    assert np.array_equal(t.records.phase, [1, 1, 1])
+    t1 = E.tridiagonalize(np.array([[2.5]]))
+    assert np.array_equal(t1.d, [2.5]) and len(t1.e) == 0
+
+
+def test_back_transform_and_normalize_match_reference():
+    n = 200
+    a = hermitian(n, 7)
+    d, e, u, h, s, ph = R.tridiagonalize(a)
+    _, z = R.solve_tridiag(d, e, True)
+    ref_w = R.back_transform(u, h, s, ph, z)
+    w = E.back_transform(E.HouseholderRecords(u, h, s, ph), z)
+    assert np.abs(w - ref_w).max() <= 1e-12
+    assert np.array_equal(E.normalize_columns(w), R.normalize_columns(w))
+
+
+@pytest.mark.parametrize("n", [8, 142, 568])
+def test_eigen_hh_contract(n):
+    """SPEC solve_k post / kband eigen_hh: residual and orthonormality; eigenvalues vs the reference."""
+    a = hermitian(n, n)
+    nrm = np.linalg.norm(a)
+    w, v = E.eigen_hh(a, solve_tridiag=lambda d, e, want: R.solve_tridiag(d, e, want))
+    rw, _ = R.eigen_hh(a, False)
+    assert np.abs(w - rw).max() <= 1e-11 * nrm
+    assert np.abs(a @ v - v * w).max() <= 1e-9 * nrm
+    assert np.abs(v.conj().T @ v - np.eye(n)).max() <= 1e-9
+    w2, _ = E.eigen_hh(a, want_vectors=False)  # default host step: LAPACK stemr
+    assert np.abs(w2 - rw).max() <= 1e-11 * nrm
+
+
+def test_fault_hook_breaks_spectrum():
+    """test_householder.cpp:106-115 analogue on the GPU path."""
+    a = hermitian(40, 9)
+    t = E.tridiagonalize(a, fault_proc6_sign=True)
+    w, _ = R.solve_tridiag(t.d, t.e, False)
+    assert np.abs(np.sort(w) - np.linalg.eigvalsh(a)).max() > 1e-6 * np.linalg.norm(a)
+
+
+def test_errors_and_determinism():
+    a = hermitian(30, 4)
+    bad = a.copy()
+    bad[0, 1] += 1e-6
+    with pytest.raises(ConsistencyError):
+        E.tridiagonalize(bad)
+    with pytest.raises(DimensionError):
+        E.tridiagonalize(np.zeros((3, 4)))
+    c = np.ones((4, 3), dtype=np.complex128)
+    c[:, 1] = 0
+    with pytest.raises(ConsistencyError, match="zero column 1"):
+        E.normalize_columns(c)
+    t1, t2 = E.tridiagonalize(a), E.tridiagonalize(a)
+    assert np.array_equal(t1.d, t2.d) and np.array_equal(t1.records.u, t2.records.u)
+
+
+def test_bloch_hamiltonian_of_the_grid_pass():
+    """End to end on the downstream path: H(R) from the GPU grid pass -> Bloch H(k) (GPU) -> Eigen_HH."""
+    from paper_1402_4247_b200.grid import GridPass
+    from paper_1402_4247_b200.system import Fe3O4
+
+    f = Fe3O4.config("primitive14_150Ry")
+    gp = GridPass(f.system)
+    gp.build_index()
+    h = gp.hamiltonian(f.veff(), f.dV)[0]
+    hk = gp.bloch(h, [0.1, 0.2, -0.3])[0]
+    hk = 0.5 * (hk + hk.conj().T)
+    w, v = E.eigen_hh(hk, solve_tridiag=lambda d, e, want: R.solve_tridiag(d, e, want))
+    rw, _ = R.eigen_hh(hk, False)
+    nrm = np.linalg.norm(hk)
+    assert np.abs(w - rw).max() <= 1e-11 * nrm
+    assert np.abs(hk @ v - v * w).max() <= 1e-9 * nrm
