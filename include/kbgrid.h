@@ -267,7 +267,7 @@ int kbg_normalize_rows(double* x, int64_t nvec, int64_t len);
  * <= 1e-13, symmetrized like HermitianMatrix::from); out d [n], e [n-1] and the
  * stage records: u [n-1][n] complex (reflector of stage i, zero above i+1 and
  * for skipped stages), h, s [n-1], phase [n-1] complex. fault_sign != 0 flips
- * the procedure-6 sign (ProcedurePlan::fault_proc6_sign). n <= 7000. The _dev
+ * the procedure-6 sign (ProcedurePlan::fault_proc6_sign). n <= 4800. The _dev
  * variant destroys d_a (working matrix) and skips the Hermitian check. */
 int kbg_hh_tridiagonalize(int64_t n, const double* a, int fault_sign, double* d, double* e, double* u, double* h,
                           double* s, double* phase);

@@ -906,7 +906,7 @@ struct DevBuf {
 
 void hh_check_n(int64_t n) {
     if (n < 1) throw Error(KBG_ERR_DIMENSION, "tridiagonalize: empty matrix");
-    if (n > 7000) throw Error(KBG_ERR_DIMENSION, "tridiagonalize: n = " + std::to_string(n) + " > 7000 (shared-memory reflector)");
+    if (n > 4800) throw Error(KBG_ERR_DIMENSION, "tridiagonalize: n = " + std::to_string(n) + " > 4800 (shared-memory reflectors)");
 }
 
 // HermitianMatrix::from on the device (linalg.cpp:44-63): reject a defect above 1e-13, then symmetrize.
@@ -925,7 +925,7 @@ void hermitian_from(int64_t n, double* d_A, cudaStream_t st) {
 
 void tridiag_dev(int64_t n, double* d_work, int fault_sign, double* d, double* e, double* u, double* h, double* s,
                  double* ph, cudaStream_t st) {
-    DevBuf p(2 * n, st);
+    DevBuf p(4 * n, st);  // double-buffered p (complex)
     kbg::launch_hh_tridiagonalize(static_cast<int>(n), d_work, p.p, d, e, u, h, s, ph, fault_sign ? 1.0 : -1.0, st);
 }
 

@@ -63,61 +63,83 @@ struct TriOut {
     double2* ph;    // [n - 1]
 };
 
-__global__ void __launch_bounds__(kTriThreads, 1) k_tridiag(int n, double2* __restrict__ B, double2* __restrict__ p,
+// Stage-j reflector from the (updated) row j, redundantly in every CTA
+// (procedures 1-2): un[c] = conj(row j, c) for c > j, s, pivot phase, h.
+// Returns (h, s) and the phase through bc; un[lo] is the shifted pivot.
+template <class RowVal>
+__device__ void build_reflector(int n, int j, RowVal&& rowval, double2* un, double* red, double2* bc) {
+    const int lo = j + 1, tid = threadIdx.x;
+    double s2 = 0.0;
+    for (int c = lo + tid; c < n; c += kTriThreads) {
+        const double2 x = rowval(c);
+        un[c] = make_double2(x.x, -x.y);
+        s2 += x.x * x.x + x.y * x.y;
+    }
+    s2 = cta_sum(s2, red);
+    if (tid == 0) {
+        const double s = sqrt(s2);
+        const double2 u0 = un[lo];
+        const double piv = hypot(u0.x, u0.y);
+        const double2 phs = piv > 0.0 ? make_double2(u0.x / piv, u0.y / piv) : make_double2(1.0, 0.0);
+        const double h = s >= kSkipNorm ? s * (s + piv) : 0.0;
+        if (h != 0.0) un[lo] = make_double2(u0.x + phs.x * s, u0.y + phs.y * s);
+        bc[0] = phs;
+        bc[1] = make_double2(h, s);
+    }
+    __syncthreads();
+}
+
+// Record of stage j (procedure 3), CTA 0.
+__device__ void write_record(int n, int j, double dj, const double2* un, const double2* bc, const TriOut& out) {
+    if (blockIdx.x != 0) return;
+    const double h = bc[1].x, s = bc[1].y;
+    const double2 phs = bc[0];
+    if (threadIdx.x == 0) {
+        out.d[j] = dj;
+        out.e[j] = h == 0.0 ? 0.0 : s;
+        out.h[j] = h;
+        out.s[j] = s;
+        out.ph[j] = h == 0.0 ? make_double2(1.0, 0.0) : make_double2(-phs.x, -phs.y);
+    }
+    double2* uj = out.u + static_cast<int64_t>(j) * n;
+    for (int r = threadIdx.x; r < n; r += kTriThreads)
+        uj[r] = (h == 0.0 || r <= j) ? make_double2(0.0, 0.0) : un[r];
+}
+
+// Procedure-6 term u_r conj(q_c) + q_r conj(u_c) (householder.cpp:211-224).
+__device__ __forceinline__ double2 her2_term(double2 ur, double2 qr, double2 uc, double2 qc) {
+    return make_double2(ur.x * qc.x + ur.y * qc.y + qr.x * uc.x + qr.y * uc.y,
+                        ur.y * qc.x - ur.x * qc.y + qr.y * uc.x - qr.x * uc.y);
+}
+
+// One grid barrier and one pass over the trailing block per stage: the
+// rank-2 update of stage i (procedure 6) and the hemv of stage i + 1
+// (procedure 4) are fused -- every CTA first rebuilds row i + 1 as updated by
+// stage i (it needs u, q of stage i only), forms reflector i + 1 from it, then
+// each warp updates its rows r >= i + 2 in registers and immediately
+// accumulates p_{i+1}[r] from the updated values. Row/column i + 1 are never
+// read again, so they are not stored. p is double-buffered across stages.
+__global__ void __launch_bounds__(kTriThreads, 1) k_tridiag(int n, double2* __restrict__ B, double2* __restrict__ p2,
                                                             TriOut out, double sign) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double2 tri_smem[];
-    double2* u = tri_smem;      // [n]
-    double2* q = tri_smem + n;  // [n]
+    double2* ucur = tri_smem;           // [n] reflector of stage i
+    double2* unxt = tri_smem + n;       // [n] reflector of stage i + 1
+    double2* q = tri_smem + 2 * n;      // [n] p then q of stage i
     __shared__ double red[kTriWarps];
-    __shared__ double2 bcast[2];
+    __shared__ double2 bc[2];
     const int tid = threadIdx.x, lane = tid & 31;
     const int gwarp = blockIdx.x * kTriWarps + (tid >> 5), nwarp = gridDim.x * kTriWarps;
-    for (int i = 0; i + 1 < n; ++i) {
-        const int lo = i + 1;
-        __syncthreads();  // u, bcast of the previous stage fully consumed (a skipped stage has no grid barrier)
-        // procedure 1: u = column i below the diagonal (read as conj of row i: B stays Hermitian)
-        double s2 = 0.0;
-        for (int r = lo + tid; r < n; r += kTriThreads) {
-            const double2 b = B[static_cast<int64_t>(i) * n + r];
-            u[r] = make_double2(b.x, -b.y);
-            s2 += b.x * b.x + b.y * b.y;
-        }
-        // procedure 2: s, the pivot phase, h
-        s2 = cta_sum(s2, red);
-        const double s = sqrt(s2);
-        if (tid == 0) {
-            const double2 u0 = u[lo];
-            const double piv = hypot(u0.x, u0.y);
-            const double2 phs = piv > 0.0 ? make_double2(u0.x / piv, u0.y / piv) : make_double2(1.0, 0.0);
-            const double h = s >= kSkipNorm ? s * (s + piv) : 0.0;
-            if (h != 0.0) u[lo] = make_double2(u0.x + phs.x * s, u0.y + phs.y * s);
-            bcast[0] = phs;
-            bcast[1] = make_double2(h, 0.0);
-        }
-        __syncthreads();
-        const double2 phs = bcast[0];
-        const double h = bcast[1].x;
-        // procedure 3: the stage record (CTA 0)
-        if (blockIdx.x == 0) {
-            if (tid == 0) {
-                out.d[i] = B[static_cast<int64_t>(i) * n + i].x;
-                out.e[i] = h == 0.0 ? 0.0 : s;
-                out.h[i] = h;
-                out.s[i] = s;
-                out.ph[i] = h == 0.0 ? make_double2(1.0, 0.0) : make_double2(-phs.x, -phs.y);
-            }
-            double2* ui = out.u + static_cast<int64_t>(i) * n;
-            for (int r = tid; r < n; r += kTriThreads)
-                ui[r] = (h == 0.0 || r < lo) ? make_double2(0.0, 0.0) : u[r];
-        }
-        if (h == 0.0) continue;  // identity reflector: B unchanged, every CTA takes this branch
-        // procedure 4: p = B u / h over the active block, one warp per row
-        for (int r = lo + gwarp; r < n; r += nwarp) {
+    // prologue: reflector 0 from row 0 and its hemv
+    build_reflector(n, 0, [&](int c) { return B[c]; }, ucur, red, bc);
+    write_record(n, 0, B[0].x, ucur, bc, out);
+    double hcur = bc[1].x;
+    if (hcur != 0.0) {
+        for (int r = 1 + gwarp; r < n; r += nwarp) {
             const double2* br = B + static_cast<int64_t>(r) * n;
             double ar = 0.0, ai = 0.0;
-            for (int c = lo + lane; c < n; c += 32) {
-                const double2 x = br[c], y = u[c];
+            for (int c = 1 + lane; c < n; c += 32) {
+                const double2 x = br[c], y = ucur[c];
                 ar += x.x * y.x - x.y * y.y;
                 ai += x.x * y.y + x.y * y.x;
             }
@@ -126,39 +148,84 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_tridiag(int n, double2* __re
                 ar += __shfl_xor_sync(0xffffffffu, ar, o);
                 ai += __shfl_xor_sync(0xffffffffu, ai, o);
             }
-            if (lane == 0) p[r] = make_double2(ar / h, ai / h);
+            if (lane == 0) p2[r] = make_double2(ar / hcur, ai / hcur);
         }
-        grid.sync();
-        // procedures 4 (dot) and 5: K = Re(p . u) / 2h, q = p - K u
-        double dr = 0.0;
-        for (int r = lo + tid; r < n; r += kTriThreads) {
-            const double2 pr = p[r];
-            q[r] = pr;
-            dr += pr.x * u[r].x + pr.y * u[r].y;
-        }
-        const double K = cta_sum(dr, red) / (2.0 * h);
-        for (int r = lo + tid; r < n; r += kTriThreads) {
-            const double2 pr = q[r], ur = u[r];
-            q[r] = make_double2(pr.x - K * ur.x, pr.y - K * ur.y);
-        }
-        __syncthreads();
-        // procedure 6: B += sign (u q^H + q u^H) on the active block, one warp per row
-        for (int r = lo + gwarp; r < n; r += nwarp) {
-            double2* br = B + static_cast<int64_t>(r) * n;
-            const double2 ur = u[r], qr = q[r];
-            for (int c = lo + lane; c < n; c += 32) {
-                const double2 qc = q[c], uc = u[c];
-                const double xr = ur.x * qc.x + ur.y * qc.y + qr.x * uc.x + qr.y * uc.y;
-                const double xi = ur.y * qc.x - ur.x * qc.y + qr.y * uc.x - qr.x * uc.y;
-                double2 b = br[c];
-                b.x += sign * xr;
-                b.y += sign * xi;
-                br[c] = b;
-            }
-        }
-        grid.sync();
     }
-    if (blockIdx.x == 0 && tid == 0) out.d[n - 1] = B[static_cast<int64_t>(n - 1) * n + (n - 1)].x;
+    grid.sync();
+    for (int i = 0; i + 1 < n; ++i) {
+        const int lo = i + 1, lo2 = i + 2;
+        const double2* pin = p2 + (i & 1) * n;
+        double2* pout = p2 + ((i + 1) & 1) * n;
+        // procedures 4 (dot) and 5 of stage i: K = Re(p . u) / 2h, q = p - K u
+        if (hcur != 0.0) {
+            double dr = 0.0;
+            for (int r = lo + tid; r < n; r += kTriThreads) {
+                const double2 pr = pin[r];
+                q[r] = pr;
+                dr += pr.x * ucur[r].x + pr.y * ucur[r].y;
+            }
+            const double K = cta_sum(dr, red) / (2.0 * hcur);
+            for (int r = lo + tid; r < n; r += kTriThreads) {
+                const double2 pr = q[r], ur = ucur[r];
+                q[r] = make_double2(pr.x - K * ur.x, pr.y - K * ur.y);
+            }
+            __syncthreads();
+        }
+        // row lo as updated by stage i -> reflector of stage lo (d[lo] from its diagonal)
+        const bool upd = hcur != 0.0;
+        const double2 ul = upd ? ucur[lo] : make_double2(0.0, 0.0), ql = upd ? q[lo] : make_double2(0.0, 0.0);
+        auto rowval = [&](int c) {
+            double2 b = B[static_cast<int64_t>(lo) * n + c];
+            if (upd) {
+                const double2 x = her2_term(ul, ql, ucur[c], q[c]);
+                b.x += sign * x.x;
+                b.y += sign * x.y;
+            }
+            return b;
+        };
+        double hnxt = 0.0;
+        if (lo2 < n) {
+            build_reflector(n, lo, rowval, unxt, red, bc);
+            write_record(n, lo, rowval(lo).x, unxt, bc, out);
+            hnxt = bc[1].x;
+        } else if (blockIdx.x == 0 && tid == 0) {
+            out.d[lo] = rowval(lo).x;
+        }
+        // fused pass over rows/columns >= lo2: stage-i update + stage-(i+1) hemv
+        if (upd || hnxt != 0.0) {
+            for (int r = lo2 + gwarp; r < n; r += nwarp) {
+                double2* br = B + static_cast<int64_t>(r) * n;
+                const double2 ur = upd ? ucur[r] : make_double2(0.0, 0.0), qr = upd ? q[r] : make_double2(0.0, 0.0);
+                double ar = 0.0, ai = 0.0;
+                for (int c = lo2 + lane; c < n; c += 32) {
+                    double2 b = br[c];
+                    if (upd) {
+                        const double2 x = her2_term(ur, qr, ucur[c], q[c]);
+                        b.x += sign * x.x;
+                        b.y += sign * x.y;
+                        br[c] = b;
+                    }
+                    const double2 y = unxt[c];
+                    ar += b.x * y.x - b.y * y.y;
+                    ai += b.x * y.y + b.y * y.x;
+                }
+                if (hnxt != 0.0) {
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        ar += __shfl_xor_sync(0xffffffffu, ar, o);
+                        ai += __shfl_xor_sync(0xffffffffu, ai, o);
+                    }
+                    if (lane == 0) pout[r] = make_double2(ar / hnxt, ai / hnxt);
+                }
+            }
+            grid.sync();
+        }
+        double2* t = ucur;
+        ucur = unxt;
+        unxt = t;
+        hcur = hnxt;
+        __syncthreads();  // the swapped buffers are rewritten next stage
+    }
 }
 
 // Cumulative chased-out phases (householder.cpp:264-273), sequential like the
@@ -295,7 +362,7 @@ int launch_hermitian_repair(int n, double* d_A, unsigned long long* d_defect, bo
     return 1;
 }
 
-size_t hh_tridiag_smem(int n) { return 2 * static_cast<size_t>(n) * sizeof(double2); }
+size_t hh_tridiag_smem(int n) { return 3 * static_cast<size_t>(n) * sizeof(double2); }
 
 int launch_hh_tridiagonalize(int n, double* d_B, double* d_p, double* d, double* e, double* u, double* h, double* s,
                              double* ph, double sign, cudaStream_t st) {
@@ -317,7 +384,7 @@ int launch_hh_tridiagonalize(int n, double* d_B, double* d_p, double* d, double*
     int nn = n;
     double2* B = reinterpret_cast<double2*>(d_B);
     double2* P = reinterpret_cast<double2*>(d_p);
-    void* args[] = {&nn, &B, &P, &o, &sign};
+    void* args[] = {&nn, &B, &P, &o, &sign};  // P: 2 n complex (double-buffered p)
     KBG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_tridiag), dim3(grid), dim3(kTriThreads), args,
                                          smem, st));
     KBG_CUDA(cudaGetLastError());
