@@ -45,6 +45,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--warps", type=int, default=8)
     p.add_argument("--profile", action="store_true", help="one warm pass only (for ncu)")
+    p.add_argument("--collective", default="p2p", choices=["p2p", "nccl"],
+                   help="N > 1: H reduction+mirror over peer memory (kb_comm.cu) or NCCL all_reduce")
     return p.parse_args()
 
 
@@ -223,6 +225,11 @@ def main():
     d_rho = torch.empty((nspin, npts), dtype=torch.float64, device=dev)
     d_h = torch.empty((nspin, nnz), dtype=torch.float64, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    p2p = world > 1 and args.collective == "p2p"
+    if p2p:  # exchange-buffer handles (CUDA IPC) all-gathered once
+        handles = [None] * world
+        dist.all_gather_object(handles, gp.comm_handle())
+        gp.comm_open(handles)
 
     def step(ev=None, collective=True):
         n = 0
@@ -232,6 +239,15 @@ def main():
         n += gp.last_launches
         if ev:
             ev[1].record(stream)
+        if p2p and collective:
+            # accumulate + fused reduce/mirror over NVLink: full H on every rank
+            gp.hamiltonian_allreduce_dev(d_veff, f.dV, d_h, stream)
+            n += gp.last_launches
+            if ev:
+                ev[2].record(stream)
+                ev[3].record(stream)
+                ev[4].record(stream)
+            return n
         gp.hamiltonian_accumulate_dev(d_veff, f.dV, d_h, stream)
         n += gp.last_launches
         if ev:
@@ -375,6 +391,7 @@ def main():
             "config": {"workload": args.config, "atoms": sysm.natom, "grid": list(sysm.grid), "nbasis": sysm.nbasis,
                        "nspin": nspin, "pairs": int(len(ix["pair_a"])), "nnz": int(nnz),
                        "parallelism": f"grid-sharded x{world}" if world > 1 else "1 GPU",
+                       "collective": (args.collective if world > 1 else None),
                        "l2": "flushed (512 MB write) between timed steps, outside the events",
                        "pass_gflop": round(total_f / 1e9, 3),
                        "achieved_pass_tflops": round(total_f / (ms * 1e-3) / 1e12, 3)},

@@ -197,6 +197,23 @@ const char* kbg_last_error(const kbg_ctx* ctx);
 const char* kbg_status_string(int status);
 void kbg_destroy(kbg_ctx* ctx);
 
+/* ---- Multi-GPU H without NCCL --------------------------------
+ * Sharded contexts (one per GPU / process) exchange their H partials through
+ * peer memory: each rank publishes an exchange buffer (kbg_comm_handle, a
+ * KBG_COMM_HANDLE_BYTES blob to all-gather, e.g. with torch.distributed),
+ * opens every peer's (kbg_comm_open, blobs in rank order), and
+ * kbg_hamiltonian_allreduce_dev then leaves the FULL mirrored H on every rank:
+ * accumulate the shard into the own buffer, one kernel that waits for all
+ * partials (flags in peer memory), sums its slice of the canonical pairs in
+ * rank order, mirrors it and stores it into every rank's buffer over
+ * NVLink, and a copy-out once all slices have landed. Replaces
+ * hamiltonian_dev + ncclAllReduce; same bits on every rank. */
+#define KBG_COMM_HANDLE_BYTES 96
+int kbg_comm_handle(kbg_ctx* ctx, void* handle_out);
+int kbg_comm_open(kbg_ctx* ctx, const void* handles);
+int kbg_hamiltonian_allreduce_dev(kbg_ctx* ctx, int nspin, const double* d_veff, double dV, double* d_h,
+                                  void* stream);
+
 /* ---- Formats either side of the grid pass ----------------
  * The pair-sparse blocks of kbg_index (grid-pass DM input, H output) against
  * the reference's band-pipeline types: RealSpaceOperator (dense n x n block

@@ -30,6 +30,7 @@ KBG_OPT_SCATTER_STORE = 3
 KBG_OPT_PERSIST = 4
 KBG_OPT_DEBUG_COUNTERS = 5
 KBG_OPT_SCHEDULE = 6
+KBG_COMM_HANDLE_BYTES = 96
 KBG_CELL_PRIMITIVE = 0
 KBG_CELL_CUBIC = 1
 
@@ -112,6 +113,9 @@ KBGRID_SYMBOLS = [
     ("kbg_status_string", C.c_char_p, [_I]),
     ("kbg_destroy", None, [_P]),
     ("kbg_version", C.c_char_p, []),
+    ("kbg_comm_handle", _I, [_P, _P]),
+    ("kbg_comm_open", _I, [_P, _P]),
+    ("kbg_hamiltonian_allreduce_dev", _I, [_P, _I, _P, _D, _P, _P]),
     ("kbg_offsets", _I, [_P, C.POINTER(_I), C.POINTER(C.c_int32)]),
     ("kbg_to_realspace", _I, [_P, _DP, _DP]),
     ("kbg_from_realspace", _I, [_P, _DP, _DP]),

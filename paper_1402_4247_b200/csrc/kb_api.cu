@@ -10,6 +10,7 @@
 #include <vector>
 
 #include <cublas_v2.h>
+#include <unistd.h>
 
 #include "kb_device.cuh"
 
@@ -59,6 +60,14 @@ struct kbg_ctx {
     size_t cap_hkw = 0;
     cudaEvent_t h_kw_done = nullptr;
     cublasHandle_t blas = nullptr;  // Part 6 density matrix (ZGEMM)
+    // fused H reduction over peer memory (kb_comm.cu)
+    kbg::CommArgs comm;
+    double* d_xbuf = nullptr;           // own exchange buffer [2][nnz] + flags + counter
+    std::vector<void*> ipc_opened;      // peer buffers opened with cudaIpcOpenMemHandle
+    int32_t* d_canon = nullptr;
+    int64_t* d_cpre = nullptr;
+    unsigned long long epoch = 0;
+    bool comm_ready = false;
     double* d_states = nullptr;     // scaled states scratch
     size_t cap_states = 0;
 };
@@ -873,6 +882,136 @@ int kbg_normalize_rows(double* x, int64_t nvec, int64_t len) {
     });
 }
 
+// ---- fused H reduction + mirror over peer memory (kb_comm.cu) ----------------
+namespace {
+
+struct CommBlob {
+    cudaIpcMemHandle_t h;
+    uint64_t ptr;
+    int64_t pid;
+};
+static_assert(sizeof(CommBlob) <= KBG_COMM_HANDLE_BYTES, "comm handle size");
+
+size_t xbuf_doubles(const kbg_ctx* c) { return 2 * static_cast<size_t>(std::max<int64_t>(1, c->ix.nnz)); }
+
+}  // namespace
+
+int kbg_comm_handle(kbg_ctx* c, void* out) {
+    if (!c || !out) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        require_index(c);
+        KBG_CUDA(cudaSetDevice(c->device));
+        if (!c->d_xbuf) {
+            const size_t bytes = xbuf_doubles(c) * sizeof(double) + 8 * kbg::kMaxRanks + 64;
+            KBG_CUDA(cudaMalloc(&c->d_xbuf, bytes));
+            KBG_CUDA(cudaMemset(c->d_xbuf, 0, bytes));
+        }
+        CommBlob b{};
+        KBG_CUDA(cudaIpcGetMemHandle(&b.h, c->d_xbuf));
+        b.ptr = reinterpret_cast<uint64_t>(c->d_xbuf);
+        b.pid = static_cast<int64_t>(getpid());
+        std::memset(out, 0, KBG_COMM_HANDLE_BYTES);
+        std::memcpy(out, &b, sizeof(b));
+    });
+}
+
+int kbg_comm_open(kbg_ctx* c, const void* handles) {
+    if (!c || !handles) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        require_index(c);
+        if (!c->d_xbuf) throw Error(KBG_ERR_CONFIG, "comm_open: call kbg_comm_handle first");
+        if (c->nranks > kbg::kMaxRanks) throw Error(KBG_ERR_CONFIG, "comm_open: more than 8 ranks");
+        KBG_CUDA(cudaSetDevice(c->device));
+        kbg::CommArgs& cm = c->comm;
+        cm.nranks = c->nranks;
+        cm.rank = c->rank;
+        const size_t nd = xbuf_doubles(c);
+        for (int k = 0; k < c->nranks; ++k) {
+            CommBlob b;
+            std::memcpy(&b, static_cast<const char*>(handles) + k * KBG_COMM_HANDLE_BYTES, sizeof(b));
+            double* x = nullptr;
+            if (k == c->rank) {
+                x = c->d_xbuf;
+            } else if (b.pid == static_cast<int64_t>(getpid())) {
+                x = reinterpret_cast<double*>(b.ptr);  // same process (contexts sharing a device): direct pointer
+            } else {
+                void* q = nullptr;
+                KBG_CUDA(cudaIpcOpenMemHandle(&q, b.h, cudaIpcMemLazyEnablePeerAccess));
+                c->ipc_opened.push_back(q);
+                x = static_cast<double*>(q);
+            }
+            cm.x[k] = x;
+            cm.flags[k] = reinterpret_cast<unsigned long long*>(x + nd);
+        }
+        cm.counter = reinterpret_cast<unsigned int*>(cm.flags[c->rank] + kbg::kMaxRanks);
+        // canonical pairs, contiguous slices balanced by block size
+        if (!c->hix.valid) kbg::copy_index_to_host(c->ix, c->hix, c->stream);
+        const kbg::HostIndex& h = c->hix;
+        std::vector<int32_t> canon;
+        std::vector<int64_t> pre{0};
+        for (int64_t p = 0; p < c->ix.npair; ++p) {
+            const int a = h.pair_a[p], b = h.pair_b[p];
+            const int R0 = h.pair_R[3 * p], R1 = h.pair_R[3 * p + 1], R2 = h.pair_R[3 * p + 2];
+            const bool can = (a != b) ? a < b : (R0 != 0 ? R0 > 0 : (R1 != 0 ? R1 > 0 : R2 >= 0));
+            if (!can) continue;
+            canon.push_back(static_cast<int32_t>(p));
+            pre.push_back(pre.back() + (h.pair_off[p + 1] - h.pair_off[p]));
+        }
+        auto bound = [&](int r) -> int64_t {
+            const int64_t target = (pre.back() * r + c->nranks - 1) / c->nranks;
+            return std::lower_bound(pre.begin(), pre.end(), target) - pre.begin();
+        };
+        const int64_t w0 = std::min<int64_t>(bound(c->rank), static_cast<int64_t>(canon.size()));
+        const int64_t w1 = c->rank + 1 == c->nranks ? static_cast<int64_t>(canon.size())
+                                                     : std::min<int64_t>(bound(c->rank + 1), static_cast<int64_t>(canon.size()));
+        if (c->ix.nnz >= (int64_t(1) << 31)) throw Error(KBG_ERR_DIMENSION, "comm_open: nnz >= 2^31");
+        std::vector<int32_t> e0, e1;
+        for (int64_t w = w0; w < w1; ++w) {
+            const int64_t p = canon[w], q = h.pair_mirror[p];
+            const int na = c->P.sp[c->h_spc[h.pair_a[p]]].norb, nb = c->P.sp[c->h_spc[h.pair_b[p]]].norb;
+            for (int i = 0; i < na; ++i)
+                for (int j = 0; j < nb; ++j) {
+                    if (q == p && i > j) continue;  // (a, a, 0): the upper triangle carries both entries
+                    e0.push_back(static_cast<int32_t>(h.pair_off[p] + i * nb + j));
+                    if (q == p)
+                        e1.push_back(static_cast<int32_t>(h.pair_off[p] + j * na + i) | (i < j ? INT32_MIN : 0));
+                    else
+                        e1.push_back(static_cast<int32_t>(h.pair_off[q] + j * na + i));
+                }
+        }
+        if (c->d_canon) cudaFree(c->d_canon);
+        c->d_canon = nullptr;
+        KBG_CUDA(cudaMalloc(&c->d_canon, std::max<size_t>(1, 2 * e0.size()) * sizeof(int32_t)));
+        if (!e0.empty()) {
+            KBG_CUDA(cudaMemcpy(c->d_canon, e0.data(), e0.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+            KBG_CUDA(cudaMemcpy(c->d_canon + e0.size(), e1.data(), e1.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        }
+        cm.el0 = c->d_canon;
+        cm.el1 = c->d_canon + e0.size();
+        cm.ne = static_cast<int64_t>(e0.size());
+        c->comm_ready = true;
+    });
+}
+
+int kbg_hamiltonian_allreduce_dev(kbg_ctx* c, int nspin, const double* d_veff, double dV, double* d_h, void* stream) {
+    if (!c || !d_veff || !d_h) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        check_nspin(nspin);
+        require_index(c);
+        if (!c->comm_ready) throw Error(KBG_ERR_CONFIG, "hamiltonian_allreduce: call kbg_comm_open first");
+        KBG_CUDA(cudaSetDevice(c->device));
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        double* x = c->d_xbuf;
+        KBG_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * nspin * c->ix.nnz, st));
+        int n = run_hamiltonian(c, nspin, dV, d_veff, x, st);
+        c->epoch += 2;
+        n += kbg::launch_reduce_mirror(c->comm, c->ix, c->P, nspin, d_h, c->epoch - 1, st);
+        c->last_launches = n;
+        c->tally.flops = nspin * 2.0 * c->ix.sum_m2 / c->nranks;
+        c->tally.bytes = 8.0 * nspin * (c->ix.nnz + c->npts);
+    });
+}
+
 // ---- Eigen_HH on the GPU (kb_eigen.cu) ------------------
 namespace {
 
@@ -1085,6 +1224,10 @@ void kbg_destroy(kbg_ctx* c) {
         if (p) cudaFree(p);
     if (c->h_kw) cudaFreeHost(c->h_kw);
     if (c->d_states) cudaFree(c->d_states);
+    for (void* q : c->ipc_opened) cudaIpcCloseMemHandle(q);
+    if (c->d_xbuf) cudaFree(c->d_xbuf);
+    if (c->d_canon) cudaFree(c->d_canon);
+    if (c->d_cpre) cudaFree(c->d_cpre);
     if (c->blas) cublasDestroy(c->blas);
     if (c->h_kw_done) cudaEventDestroy(c->h_kw_done);
     if (c->d_tau) cudaFree(c->d_tau);

@@ -1,0 +1,144 @@
+// Fused H reduction + mirror over NVLink/NVSwitch peer memory (SURVEY.md
+// 8(e)): the multi-GPU H step without NCCL.
+//
+// Every rank accumulates its shard's partial H (canonical pairs only) into its
+// own exchange buffer X_r, which every peer has mapped (CUDA IPC). One kernel
+// then, on each rank r:
+//   1. signals "partials ready" to every peer and waits for all peers
+//      (flags in peer memory, system-scope release/acquire);
+//   2. for the canonical pairs of its slice (contiguous, balanced by size)
+//      sums the N partials in rank order (same bits on every rank), applies
+//      the mirror H_ba(-R) = H_ab(R)^T (and the (a,a,0) symmetrization of
+//      k_mirror), and stores the result into every rank's X -- a
+//      reduce-scatter + all-gather + mirror in one pass over NVLink;
+//   3. the last CTA signals "slice written".
+// A second small kernel waits for every peer's slice and copies X_self into
+// the caller's H. Per rank this moves ~2 |H| over NVLink instead of NCCL's
+// all-reduce plus a separate mirror kernel; a slice element is read and
+// written only by its owner, so X can be updated in place.
+#include "kb_internal.cuh"
+
+namespace kbg {
+
+namespace {
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Thread 0 of every CTA: wait until every rank's flag in this rank's flag
+// array has reached `epoch`. A peer that never arrives (broken setup) must not
+// hang the GPU: after 10 s the wait gives up and raises the error word
+// (flags[kMaxRanks + 1] of this rank; the result is then invalid).
+__device__ void wait_flags(const CommArgs& c, unsigned long long epoch) {
+    if (threadIdx.x == 0) {
+        const unsigned long long* f = c.flags[c.rank];
+        const unsigned long long t0 = globaltimer();
+        for (int k = 0; k < c.nranks; ++k)
+            while (ld_acquire_sys(f + k) < epoch) {
+                if (globaltimer() - t0 > 10000000000ull) {
+                    c.flags[c.rank][kMaxRanks + 1] = 1ull;
+                    break;
+                }
+                __nanosleep(64);
+            }
+    }
+    __syncthreads();
+}
+
+// Signal `epoch` into slot `rank` of every rank's flag array.
+__device__ void signal_flags(const CommArgs& c, unsigned long long epoch) {
+    __threadfence_system();
+    for (int k = 0; k < c.nranks; ++k) st_release_sys(c.flags[k] + c.rank, epoch);
+}
+
+// One thread per element of this rank's slice, with the element's two
+// offsets precomputed on the host (el0: the canonical entry, el1: its mirror
+// entry -- or the transposed entry of an (a,a,0) block, flagged by bit 31 --
+// or el0 itself on such a block's diagonal): one coalesced index load, then
+// all N partials in flight at once, then the stores.
+__global__ void __launch_bounds__(256) k_reduce_mirror(CommArgs c, int nspin, int64_t nnz, int64_t ne,
+                                                       const int32_t* __restrict__ el0,
+                                                       const int32_t* __restrict__ el1, unsigned long long epoch) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) signal_flags(c, epoch);
+    wait_flags(c, epoch);
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < ne * nspin;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int s = static_cast<int>(t / ne);
+        const int64_t el = t - s * ne;
+        const int64_t base = s * nnz;
+        const int64_t o0 = base + el0[el];
+        const int32_t m = el1[el];
+        const bool sym = m < 0;  // (a, a, 0) off-diagonal: (H + H^T) / 2
+        const int64_t o1 = base + (m & 0x7fffffff);
+        double part[kMaxRanks], part2[kMaxRanks];
+#pragma unroll
+        for (int k = 0; k < kMaxRanks; ++k) {
+            part[k] = k < c.nranks ? c.x[k][o0] : 0.0;
+            part2[k] = (sym && k < c.nranks) ? c.x[k][o1] : 0.0;
+        }
+        double v = 0.0, v2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < kMaxRanks; ++k) {
+            v += part[k];
+            v2 += part2[k];
+        }
+        if (sym) v = 0.5 * (v + v2);
+        for (int k = 0; k < c.nranks; ++k) {
+            c.x[k][o0] = v;
+            c.x[k][o1] = v;
+        }
+    }
+    // slice written everywhere: the last CTA signals epoch + 1 (the barrier
+    // makes the CTA's stores visible to thread 0, whose system fence is cumulative)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        const unsigned int done = atomicAdd(c.counter, 1u);
+        if (done == gridDim.x - 1) {
+            *c.counter = 0u;
+            signal_flags(c, epoch + 1);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_comm_copy_out(CommArgs c, int64_t n, double* __restrict__ out,
+                                                       unsigned long long epoch) {
+    wait_flags(c, epoch);
+    const double2* src = reinterpret_cast<const double2*>(c.x[c.rank]);
+    double2* dst = reinterpret_cast<double2*>(out);
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n / 2;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        dst[i] = src[i];
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) out[n - 1] = c.x[c.rank][n - 1];
+}
+
+}  // namespace
+
+int launch_reduce_mirror(const CommArgs& c, const DevIndex& ix, const SysParams& sys, int nspin, double* d_out,
+                         unsigned long long epoch, cudaStream_t st) {
+    int dev = 0, sms = 0;
+    KBG_CUDA(cudaGetDevice(&dev));
+    KBG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    // all CTAs must be co-resident (they spin on flags): at most one wave
+    const unsigned grid = static_cast<unsigned>(sms) * 2;
+    k_reduce_mirror<<<grid, 256, 0, st>>>(c, nspin, ix.nnz, c.ne, c.el0, c.el1, epoch);
+    KBG_CUDA(cudaGetLastError());
+    const int64_t n = static_cast<int64_t>(nspin) * ix.nnz;
+    k_comm_copy_out<<<static_cast<unsigned>(sms) * 4, 256, 0, st>>>(c, n, d_out, epoch + 1);
+    KBG_CUDA(cudaGetLastError());
+    return 2;
+}
+
+}  // namespace kbg

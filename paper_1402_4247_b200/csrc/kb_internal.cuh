@@ -219,6 +219,22 @@ int launch_fold(const FormatIndex& f, const DevIndex& ix, int nk, const double* 
 int launch_realspace(const FormatIndex& f, const DevIndex& ix, bool to_dense, double* d_sparse, double* d_dense,
                      cudaStream_t st);
 int launch_scale_states(int n, int m, const double* d_C, const double* d_w, double* d_D, cudaStream_t st);
+// Fused H reduction + mirror over peer memory (kb_comm.cu).
+constexpr int kMaxRanks = 8;
+struct CommArgs {
+    int nranks = 0, rank = 0;
+    double* x[kMaxRanks] = {};                  // exchange buffers [2][nnz], peer-mapped (CUDA IPC)
+    unsigned long long* flags[kMaxRanks] = {};  // flag array [kMaxRanks] at the tail of each buffer
+    unsigned int* counter = nullptr;            // local CTA counter
+    // this rank's slice of the canonical entries: el0 = entry offset, el1 =
+    // mirror offset (bit 31: transposed entry of an (a,a,0) block, averaged)
+    const int32_t* el0 = nullptr;
+    const int32_t* el1 = nullptr;
+    int64_t ne = 0;
+};
+int launch_reduce_mirror(const CommArgs& c, const DevIndex& ix, const SysParams& sys, int nspin, double* d_out,
+                         unsigned long long epoch, cudaStream_t st);
+
 // Eigen_HH (kb_eigen.cu). Complex arrays interleaved.
 size_t hh_tridiag_smem(int n);
 int launch_hermitian_repair(int n, double* d_A, unsigned long long* d_defect, bool apply, cudaStream_t st);

@@ -132,6 +132,24 @@ class GridPass:
         self._check(self._lib.kbg_hamiltonian_mirror_dev(self._h, h.shape[0], h.data_ptr(),
                                                          self._stream_ptr(stream)), "kbg_hamiltonian_mirror_dev")
 
+    # -- multi-GPU H over peer memory (kb_comm.cu) ----------------------------
+    def comm_handle(self) -> bytes:
+        """This rank's exchange-buffer handle (all-gather it, then comm_open)."""
+        buf = C.create_string_buffer(_abi.KBG_COMM_HANDLE_BYTES)
+        self._check(self._lib.kbg_comm_handle(self._h, buf), "kbg_comm_handle")
+        return buf.raw
+
+    def comm_open(self, handles) -> None:
+        blob = b"".join(handles)
+        buf = C.create_string_buffer(blob, len(blob))
+        self._check(self._lib.kbg_comm_open(self._h, buf), "kbg_comm_open")
+
+    def hamiltonian_allreduce_dev(self, veff, dV: float, h, stream=None) -> None:
+        """Sharded H pass whose result is the full, mirrored H on every rank (no NCCL)."""
+        self._check(self._lib.kbg_hamiltonian_allreduce_dev(self._h, veff.shape[0], veff.data_ptr(), dV, h.data_ptr(),
+                                                            self._stream_ptr(stream)),
+                    "kbg_hamiltonian_allreduce_dev")
+
     # -- formats either side (SURVEY.md 8(f2); see formats.py for the SPEC types) --
     def offsets(self) -> np.ndarray:
         """Distinct lattice offsets R of the pair list, sorted, shape (nR, 3)."""
