@@ -148,6 +148,15 @@ int kbg_density(kbg_ctx* ctx, int nspin, const double* dm, double* rho);
 /* veff: [nspin][npts]; h: [nspin][nnz], overwritten with sum_r phi V dV phi. */
 int kbg_hamiltonian(kbg_ctx* ctx, int nspin, const double* veff, double dV, double* h);
 
+/* One SCF grid pass through host buffers: rho from dm and h from veff in one
+ * call (the drop-in an SCF loop makes per iteration). The two halves run on
+ * two streams so each half's host<->device copies overlap the other half's
+ * kernels (pinned host buffers make the copies asynchronous). DM is checked
+ * like kbg_density; on a violation the status is KBG_ERR_CONSISTENCY and the
+ * outputs are invalid. */
+int kbg_grid_pass(kbg_ctx* ctx, int nspin, const double* dm, const double* veff, double dV, double* rho,
+                  double* h);
+
 /* Device-pointer variants (timing path). `stream` is a cudaStream_t (0 =
  * legacy default). No host synchronisation, no validation. */
 int kbg_density_dev(kbg_ctx* ctx, int nspin, const double* d_dm, double* d_rho, void* stream);

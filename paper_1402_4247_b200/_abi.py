@@ -100,6 +100,7 @@ KBGRID_SYMBOLS = [
     ("kbg_shard_range", _I, [_P, C.POINTER(_I64), C.POINTER(_I64)]),
     ("kbg_density", _I, [_P, _I, _DP, _DP]),
     ("kbg_hamiltonian", _I, [_P, _I, _DP, _D, _DP]),
+    ("kbg_grid_pass", _I, [_P, _I, _DP, _DP, _D, _DP, _DP]),
     ("kbg_density_dev", _I, [_P, _I, _P, _P, _P]),
     ("kbg_hamiltonian_dev", _I, [_P, _I, _P, _D, _P, _P]),
     ("kbg_hamiltonian_accumulate_dev", _I, [_P, _I, _P, _D, _P, _P]),

@@ -31,7 +31,7 @@ struct kbg_ctx {
     int schedule = 3;          // KBG_OPT_SCHEDULE
     double* d_dmr = nullptr;   // repacked DM scratch
     size_t cap_dmr = 0;
-    int* d_counter = nullptr;  // persistent work counter
+    int* d_counter = nullptr;  // persistent work counters: [0] density, [1] H (the two may run concurrently)
     double sign = 1.0;
     int scatter = 0;
     unsigned long long* d_dbg = nullptr;  // KBG_OPT_DEBUG_COUNTERS
@@ -65,6 +65,13 @@ struct kbg_ctx {
     double* d_xbuf = nullptr;           // own exchange buffer [2][nnz] + flags + counter
     std::vector<void*> ipc_opened;      // peer buffers opened with cudaIpcOpenMemHandle
     int32_t* d_canon = nullptr;
+    // kbg_grid_pass: second stream and buffers for the H half
+    cudaStream_t stream2 = nullptr;
+    cudaEvent_t ev_pass = nullptr;
+    double* d_in2 = nullptr;
+    size_t cap_in2 = 0;
+    double* d_out2 = nullptr;
+    size_t cap_out2 = 0;
     int64_t* d_cpre = nullptr;
     unsigned long long epoch = 0;
     bool comm_ready = false;
@@ -214,7 +221,7 @@ kbg::GridArgs grid_args(kbg_ctx* c, int nspin, double dV, const double* in, doub
     g.task_warps = density ? c->ix.rtask_warps : c->ix.htask_warps;
     g.order = c->ix.order;
     g.norder = c->ix.norder;
-    g.counter = c->d_counter;
+    g.counter = c->d_counter + (density ? 0 : 1);
     g.nrep = c->ix.nrep;
     g.t_ptr = density ? c->ix.rt_ptr : c->ix.ht_ptr;
     g.tasks = density ? c->ix.rt : c->ix.ht;
@@ -383,7 +390,7 @@ int kbg_build_index(kbg_ctx* c) {
         KBG_CUDA(cudaMalloc(&c->ix.order, std::max<size_t>(1, order.size()) * sizeof(int64_t)));
         if (!order.empty())
             KBG_CUDA(cudaMemcpy(c->ix.order, order.data(), order.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
-        if (!c->d_counter) KBG_CUDA(cudaMalloc(&c->d_counter, sizeof(int)));
+        if (!c->d_counter) KBG_CUDA(cudaMalloc(&c->d_counter, 2 * sizeof(int)));
         if (c->persist_ok) {
             kbg::build_cache_device(grid_args(c, 1, 0.0, nullptr, nullptr, false),
                                     grid_args(c, 1, 0.0, nullptr, nullptr, true), c->ix, c->stream);
@@ -526,6 +533,50 @@ int kbg_hamiltonian(kbg_ctx* c, int nspin, const double* veff, double dV, double
         KBG_CUDA(cudaStreamSynchronize(c->stream));
         c->tally.flops = nspin * 2.0 * c->ix.sum_m2;
         c->tally.bytes = 8.0 * nspin * (c->ix.nnz + c->npts);
+    });
+}
+
+int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, double dV, double* rho, double* h) {
+    if (!c || !dm || !veff || !rho || !h) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        check_nspin(nspin);
+        require_index(c);
+        if (!std::isfinite(dV)) throw Error(KBG_ERR_NONFINITE, "grid_pass: non-finite dV");
+        KBG_CUDA(cudaSetDevice(c->device));
+        if (!c->stream2) KBG_CUDA(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+        if (!c->ev_pass) KBG_CUDA(cudaEventCreateWithFlags(&c->ev_pass, cudaEventDisableTiming));
+        const size_t ndm = static_cast<size_t>(nspin) * c->ix.nnz, npt = static_cast<size_t>(nspin) * c->npts;
+        ensure(c->d_in, c->cap_in, ndm);
+        ensure(c->d_out, c->cap_out, npt);
+        ensure(c->d_in2, c->cap_in2, npt);
+        ensure(c->d_out2, c->cap_out2, ndm);
+        // stream 1: DM in -> symmetry check -> rho -> rho out; stream 2: V in -> H -> mirror -> H out.
+        // The copies of one half overlap the kernels of the other; the DM check is read at the end.
+        KBG_CUDA(cudaMemcpyAsync(c->d_in, dm, ndm * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        KBG_CUDA(cudaMemcpyAsync(c->d_in2, veff, npt * sizeof(double), cudaMemcpyHostToDevice, c->stream2));
+        KBG_CUDA(cudaMemsetAsync(c->d_check, 0, 4 * sizeof(unsigned long long), c->stream));
+        int n = kbg::launch_dm_check(c->ix, c->P, nspin, c->d_in, c->d_check, c->stream);
+        if (c->nranks > 1) KBG_CUDA(cudaMemsetAsync(c->d_out, 0, npt * sizeof(double), c->stream));
+        n += run_density(c, nspin, c->d_in, c->d_out, c->stream);
+        KBG_CUDA(cudaMemcpyAsync(rho, c->d_out, npt * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        KBG_CUDA(cudaMemsetAsync(c->d_out2, 0, ndm * sizeof(double), c->stream2));
+        n += run_hamiltonian(c, nspin, dV, c->d_in2, c->d_out2, c->stream2);
+        n += kbg::launch_mirror(c->ix, c->P, nspin, c->d_out2, c->stream2);
+        KBG_CUDA(cudaMemcpyAsync(h, c->d_out2, ndm * sizeof(double), cudaMemcpyDeviceToHost, c->stream2));
+        unsigned long long chk[4];
+        KBG_CUDA(cudaMemcpyAsync(chk, c->d_check, sizeof(chk), cudaMemcpyDeviceToHost, c->stream));
+        KBG_CUDA(cudaStreamSynchronize(c->stream2));
+        KBG_CUDA(cudaStreamSynchronize(c->stream));
+        c->last_launches = n;
+        double dmax, amax;
+        std::memcpy(&dmax, &chk[0], 8);
+        std::memcpy(&amax, &chk[1], 8);
+        if (chk[2]) throw Error(KBG_ERR_NONFINITE, "grid_pass: non-finite density-matrix entry (outputs invalid)");
+        if (dmax > 1e-13 * amax)
+            throw Error(KBG_ERR_CONSISTENCY,
+                        "grid_pass: DM violates DM_ba(-R) = DM_ab(R)^T by " + std::to_string(dmax) + " (outputs invalid)");
+        c->tally.flops = nspin * (4.0 * c->ix.sum_m2 + 2.0 * c->ix.sum_m);
+        c->tally.bytes = 16.0 * nspin * (c->ix.nnz + c->npts);
     });
 }
 
@@ -1228,6 +1279,10 @@ void kbg_destroy(kbg_ctx* c) {
     if (c->d_xbuf) cudaFree(c->d_xbuf);
     if (c->d_canon) cudaFree(c->d_canon);
     if (c->d_cpre) cudaFree(c->d_cpre);
+    if (c->d_in2) cudaFree(c->d_in2);
+    if (c->d_out2) cudaFree(c->d_out2);
+    if (c->ev_pass) cudaEventDestroy(c->ev_pass);
+    if (c->stream2) cudaStreamDestroy(c->stream2);
     if (c->blas) cublasDestroy(c->blas);
     if (c->h_kw_done) cudaEventDestroy(c->h_kw_done);
     if (c->d_tau) cudaFree(c->d_tau);

@@ -105,6 +105,22 @@ class GridPass:
                     "kbg_hamiltonian")
         return h
 
+    def grid_pass(self, dm: np.ndarray, veff: np.ndarray, dV: float) -> tuple[np.ndarray, np.ndarray]:
+        """rho and H of one SCF iteration in one call (overlapped transfers): returns (rho, h)."""
+        dm = np.ascontiguousarray(dm, dtype=np.float64)
+        veff = np.ascontiguousarray(veff, dtype=np.float64)
+        if dm.ndim == 1:
+            dm = dm[None]
+        if veff.ndim == 1:
+            veff = veff[None]
+        if dm.shape[0] != veff.shape[0]:
+            raise_for_status(_abi.KBG_ERR_DIMENSION, "grid_pass", "dm and veff spin counts differ")
+        rho = np.empty((dm.shape[0], self.system.npts))
+        h = np.empty((dm.shape[0], self._nnz()))
+        self._check(self._lib.kbg_grid_pass(self._h, dm.shape[0], _abi.dptr(dm), _abi.dptr(veff), dV, _abi.dptr(rho),
+                                            _abi.dptr(h)), "kbg_grid_pass")
+        return rho, h
+
     def _nnz(self) -> int:
         ix = _abi.kbg_index()
         self._check(self._lib.kbg_index_view(self._h, C.byref(ix)), "kbg_index_view")

@@ -192,6 +192,19 @@ def test_sharded_contexts_sum_to_full():
     assert normwise(h, h_full) <= 1e-13
 
 
+def test_grid_pass_matches_separate_calls():
+    """kbg_grid_pass (rho and H on two streams, overlapped copies) = kbg_density + kbg_hamiltonian."""
+    c = case("cubic56_200Ry")
+    rho, h = c.gp.grid_pass(c.dm, c.veff, c.f.dV)
+    assert np.array_equal(rho, c.gp.density(c.dm))
+    assert normwise(h, c.gp.hamiltonian(c.veff, c.f.dV)) <= 1e-14
+    assert normwise(h, c.o.hamiltonian(c.veff, c.f.dV)) <= TOL
+    bad = c.dm.copy()
+    bad[0, 1] += 1.0  # pair 0 is (0, 0, R=0) here: break its transpose symmetry off the diagonal
+    with pytest.raises(ConsistencyError):
+        c.gp.grid_pass(bad, c.veff, c.f.dV)
+
+
 def test_device_api_matches_host_api():
     import torch
 
