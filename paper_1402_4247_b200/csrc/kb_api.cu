@@ -550,19 +550,33 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
         ensure(c->d_out, c->cap_out, npt);
         ensure(c->d_in2, c->cap_in2, npt);
         ensure(c->d_out2, c->cap_out2, ndm);
-        // stream 1: DM in -> symmetry check -> rho -> rho out; stream 2: V in -> H -> mirror -> H out.
-        // The copies of one half overlap the kernels of the other; the DM check is read at the end.
-        KBG_CUDA(cudaMemcpyAsync(c->d_in, dm, ndm * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-        KBG_CUDA(cudaMemcpyAsync(c->d_in2, veff, npt * sizeof(double), cudaMemcpyHostToDevice, c->stream2));
-        KBG_CUDA(cudaMemsetAsync(c->d_check, 0, 4 * sizeof(unsigned long long), c->stream));
-        int n = kbg::launch_dm_check(c->ix, c->P, nspin, c->d_in, c->d_check, c->stream);
-        if (c->nranks > 1) KBG_CUDA(cudaMemsetAsync(c->d_out, 0, npt * sizeof(double), c->stream));
-        n += run_density(c, nspin, c->d_in, c->d_out, c->stream);
-        KBG_CUDA(cudaMemcpyAsync(rho, c->d_out, npt * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-        KBG_CUDA(cudaMemsetAsync(c->d_out2, 0, ndm * sizeof(double), c->stream2));
-        n += run_hamiltonian(c, nspin, dV, c->d_in2, c->d_out2, c->stream2);
-        n += kbg::launch_mirror(c->ix, c->P, nspin, c->d_out2, c->stream2);
-        KBG_CUDA(cudaMemcpyAsync(h, c->d_out2, ndm * sizeof(double), cudaMemcpyDeviceToHost, c->stream2));
+        // stream 2: V in -> H -> mirror -> H out; stream 1: DM in -> symmetry check -> rho -> rho out.
+        // The copies of one half overlap the kernels of the other. H goes first: its input (npts) is the
+        // smaller one to wait for and rho (npts) the smaller output left after the last kernel. The DM
+        // check is read at the end.
+        int n = 0;
+        auto h_half = [&] {
+            KBG_CUDA(cudaMemcpyAsync(c->d_in2, veff, npt * sizeof(double), cudaMemcpyHostToDevice, c->stream2));
+            KBG_CUDA(cudaMemsetAsync(c->d_out2, 0, ndm * sizeof(double), c->stream2));
+            n += run_hamiltonian(c, nspin, dV, c->d_in2, c->d_out2, c->stream2);
+            n += kbg::launch_mirror(c->ix, c->P, nspin, c->d_out2, c->stream2);
+            KBG_CUDA(cudaMemcpyAsync(h, c->d_out2, ndm * sizeof(double), cudaMemcpyDeviceToHost, c->stream2));
+        };
+        auto rho_half = [&] {
+            KBG_CUDA(cudaMemcpyAsync(c->d_in, dm, ndm * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+            KBG_CUDA(cudaMemsetAsync(c->d_check, 0, 4 * sizeof(unsigned long long), c->stream));
+            n += kbg::launch_dm_check(c->ix, c->P, nspin, c->d_in, c->d_check, c->stream);
+            if (c->nranks > 1) KBG_CUDA(cudaMemsetAsync(c->d_out, 0, npt * sizeof(double), c->stream));
+            n += run_density(c, nspin, c->d_in, c->d_out, c->stream);
+            KBG_CUDA(cudaMemcpyAsync(rho, c->d_out, npt * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        };
+#ifndef KBG_PASS_RHO_FIRST
+        h_half();
+        rho_half();
+#else
+        rho_half();
+        h_half();
+#endif
         unsigned long long chk[4];
         KBG_CUDA(cudaMemcpyAsync(chk, c->d_check, sizeof(chk), cudaMemcpyDeviceToHost, c->stream));
         KBG_CUDA(cudaStreamSynchronize(c->stream2));
