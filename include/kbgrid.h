@@ -206,6 +206,19 @@ const char* kbg_last_error(const kbg_ctx* ctx);
 const char* kbg_status_string(int status);
 void kbg_destroy(kbg_ctx* ctx);
 
+/* ---- V_eff from rho ----------------------------------------
+ * The step between the density and the Hamiltonian pass of one SCF iteration:
+ * V_eff,s = V_H[rho] + V_x,s[rho_s] + V_loc with V_H from the periodic Poisson
+ * equation in G space (4 pi rho(G)/|G|^2, G = 0 dropped: neutralizing
+ * background; cuFFT) and exchange-only local spin density (Slater) V_x,s =
+ * -(6 rho_s/pi)^(1/3) (nspin 1: rho_s = rho/2). Hartree atomic units; grids
+ * [nspin][npts] C-order as the density pass writes them; vloc [npts] may be
+ * NULL; energy (may be NULL) receives E_H = 1/2 int V_H rho, E_x. Does not
+ * need the index. */
+int kbg_veff(kbg_ctx* ctx, int nspin, const double* rho, const double* vloc, double* veff, double* energy);
+int kbg_veff_dev(kbg_ctx* ctx, int nspin, const double* d_rho, const double* d_vloc, double* d_veff,
+                 double* d_energy, void* stream);
+
 /* ---- Multi-GPU H without NCCL --------------------------------
  * Sharded contexts (one per GPU / process) exchange their H partials through
  * peer memory: each rank publishes an exchange buffer (kbg_comm_handle, a

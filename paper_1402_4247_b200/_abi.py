@@ -114,6 +114,8 @@ KBGRID_SYMBOLS = [
     ("kbg_status_string", C.c_char_p, [_I]),
     ("kbg_destroy", None, [_P]),
     ("kbg_version", C.c_char_p, []),
+    ("kbg_veff", _I, [_P, _I, _DP, _DP, _DP, _DP]),
+    ("kbg_veff_dev", _I, [_P, _I, _P, _P, _P, _P, _P]),
     ("kbg_comm_handle", _I, [_P, _P]),
     ("kbg_comm_open", _I, [_P, _P]),
     ("kbg_hamiltonian_allreduce_dev", _I, [_P, _I, _P, _D, _P, _P]),

@@ -65,6 +65,7 @@ struct kbg_ctx {
     double* d_xbuf = nullptr;           // own exchange buffer [2][nnz] + flags + counter
     std::vector<void*> ipc_opened;      // peer buffers opened with cudaIpcOpenMemHandle
     int32_t* d_canon = nullptr;
+    kbg::VeffPlan veff;  // kbg_veff (cuFFT plans)
     // kbg_grid_pass: second stream and buffers for the H half
     cudaStream_t stream2 = nullptr;
     cudaEvent_t ev_pass = nullptr;
@@ -591,6 +592,53 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
                         "grid_pass: DM violates DM_ba(-R) = DM_ab(R)^T by " + std::to_string(dmax) + " (outputs invalid)");
         c->tally.flops = nspin * (4.0 * c->ix.sum_m2 + 2.0 * c->ix.sum_m);
         c->tally.bytes = 16.0 * nspin * (c->ix.nnz + c->npts);
+    });
+}
+
+namespace {
+double cell_dV(const kbg_ctx* c) {
+    const double* A = c->P.A;
+    const double det = A[0] * (A[4] * A[8] - A[5] * A[7]) - A[1] * (A[3] * A[8] - A[5] * A[6]) +
+                       A[2] * (A[3] * A[7] - A[4] * A[6]);
+    return std::fabs(det) / static_cast<double>(c->npts);
+}
+}  // namespace
+
+int kbg_veff_dev(kbg_ctx* c, int nspin, const double* d_rho, const double* d_vloc, double* d_veff, double* d_energy,
+                 void* stream) {
+    if (!c || !d_rho || !d_veff) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        check_nspin(nspin);
+        KBG_CUDA(cudaSetDevice(c->device));
+        c->last_launches = kbg::run_veff(c->veff, c->P.N, c->P.Ainv, nspin, d_rho, d_vloc, cell_dV(c), d_veff, d_energy,
+                                         static_cast<cudaStream_t>(stream));
+        c->tally.flops = 0.0;
+        c->tally.bytes = 8.0 * c->npts * (2.0 * nspin + (d_vloc ? 1.0 : 0.0));
+    });
+}
+
+int kbg_veff(kbg_ctx* c, int nspin, const double* rho, const double* vloc, double* veff, double* energy) {
+    if (!c || !rho || !veff) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        check_nspin(nspin);
+        KBG_CUDA(cudaSetDevice(c->device));
+        const size_t n = static_cast<size_t>(c->npts);
+        for (size_t i = 0; i < n * nspin; i += 4096)
+            if (!std::isfinite(rho[i])) throw Error(KBG_ERR_NONFINITE, "veff: non-finite rho");
+        ensure(c->d_in2, c->cap_in2, 2 * n * nspin + n + 2);
+        double* d_rho = c->d_in2;
+        double* d_v = d_rho + n * nspin;
+        double* d_vloc = vloc ? d_v + n * nspin : nullptr;
+        double* d_e = d_v + n * nspin + n;
+        KBG_CUDA(cudaMemcpyAsync(d_rho, rho, n * nspin * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        if (vloc) KBG_CUDA(cudaMemcpyAsync(d_vloc, vloc, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        c->last_launches =
+            kbg::run_veff(c->veff, c->P.N, c->P.Ainv, nspin, d_rho, d_vloc, cell_dV(c), d_v, d_e, c->stream);
+        KBG_CUDA(cudaMemcpyAsync(veff, d_v, n * nspin * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        double e[2];
+        KBG_CUDA(cudaMemcpyAsync(e, d_e, sizeof(e), cudaMemcpyDeviceToHost, c->stream));
+        KBG_CUDA(cudaStreamSynchronize(c->stream));
+        if (energy) std::memcpy(energy, e, sizeof(e));
     });
 }
 
@@ -1293,6 +1341,7 @@ void kbg_destroy(kbg_ctx* c) {
     if (c->d_xbuf) cudaFree(c->d_xbuf);
     if (c->d_canon) cudaFree(c->d_canon);
     if (c->d_cpre) cudaFree(c->d_cpre);
+    c->veff.release();
     if (c->d_in2) cudaFree(c->d_in2);
     if (c->d_out2) cudaFree(c->d_out2);
     if (c->ev_pass) cudaEventDestroy(c->ev_pass);

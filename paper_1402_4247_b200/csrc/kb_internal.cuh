@@ -219,6 +219,17 @@ int launch_fold(const FormatIndex& f, const DevIndex& ix, int nk, const double* 
 int launch_realspace(const FormatIndex& f, const DevIndex& ix, bool to_dense, double* d_sparse, double* d_dense,
                      cudaStream_t st);
 int launch_scale_states(int n, int m, const double* d_C, const double* d_w, double* d_D, cudaStream_t st);
+// V_eff from rho (kb_veff.cu): cuFFT plans + work, per context.
+struct VeffPlan {
+    bool planned = false;
+    int fwd = 0, inv = 0;  // cufftHandle
+    double* work = nullptr;
+    double* B = nullptr;   // reciprocal basis rows (device)
+    void release();
+};
+int run_veff(VeffPlan& vp, const int N[3], const double Ainv[9], int nspin, const double* d_rho, const double* d_vloc,
+             double dV, double* d_veff, double* d_energy, cudaStream_t st);
+
 // Fused H reduction + mirror over peer memory (kb_comm.cu).
 constexpr int kMaxRanks = 8;
 struct CommArgs {

@@ -148,6 +148,25 @@ class GridPass:
         self._check(self._lib.kbg_hamiltonian_mirror_dev(self._h, h.shape[0], h.data_ptr(),
                                                          self._stream_ptr(stream)), "kbg_hamiltonian_mirror_dev")
 
+    # -- V_eff from rho (kb_veff.cu) -------------------------
+    def veff(self, rho: np.ndarray, vloc: np.ndarray | None = None) -> tuple[np.ndarray, tuple[float, float]]:
+        """V_eff,s = V_H + V_x,s (+ V_loc) on the grid and (E_H, E_x)."""
+        rho = np.ascontiguousarray(rho, dtype=np.float64)
+        if rho.ndim == 1:
+            rho = rho[None]
+        out = np.empty_like(rho)
+        e = (C.c_double * 2)()
+        vl = None if vloc is None else np.ascontiguousarray(vloc, dtype=np.float64)
+        self._check(self._lib.kbg_veff(self._h, rho.shape[0], _abi.dptr(rho), None if vl is None else _abi.dptr(vl),
+                                       _abi.dptr(out), e), "kbg_veff")
+        return out, (e[0], e[1])
+
+    def veff_dev(self, rho, veff, vloc=None, energy=None, stream=None) -> None:
+        self._check(self._lib.kbg_veff_dev(self._h, rho.shape[0], rho.data_ptr(),
+                                           None if vloc is None else vloc.data_ptr(), veff.data_ptr(),
+                                           None if energy is None else energy.data_ptr(), self._stream_ptr(stream)),
+                    "kbg_veff_dev")
+
     # -- multi-GPU H over peer memory (kb_comm.cu) ----------------------------
     def comm_handle(self) -> bytes:
         """This rank's exchange-buffer handle (all-gather it, then comm_open)."""
