@@ -324,6 +324,10 @@ int kbg_hh_back_transform_dev(int64_t n, int64_t m, const double* d_u, const dou
  * complex to unit 2-norm in place; a zero column is KBG_ERR_CONSISTENCY. */
 int kbg_hh_normalize_columns(int64_t n, int64_t m, double* c);
 int kbg_hh_normalize_columns_dev(int64_t n, int64_t m, double* d_c, void* stream);
+/* kband::triple_product (linalg.hpp:82-84, Part 3 S^H H S): c [m][m] = T^H H T
+ * for T [n][m], H [n][n] Hermitian, re-symmetrized and validated Hermitian
+ * (defect <= 1e-13 max(1, ||C||_F)). Two ZGEMMs (cuBLAS: plain library GEMMs). */
+int kbg_hh_triple_product(int64_t n, int64_t m, const double* t, const double* h, double* c);
 const char* kbg_hh_last_error(void);
 
 /* Library identification: "kbgrid <version> sm_100a". */

@@ -23,6 +23,7 @@ SYMBOLS = [
     ("kbr_normalize_columns", _I, [_I64, _I64, _DP]),
     ("kbr_solve_tridiag", _I, [_I64, _DP, _DP, _I, _DP, _DP]),
     ("kbr_eigen_hh", _I, [_I64, _DP, _I, _I, _DP, _DP]),
+    ("kbr_triple_product", _I, [_I64, _I64, _DP, _DP, _DP]),
 ]
 _lib = None
 
@@ -100,3 +101,12 @@ def eigen_hh(a, want_vectors=True, threads=1):
     v = np.empty((n, n), dtype=np.complex128) if want_vectors else np.empty(1, dtype=np.complex128)
     _call(lib().kbr_eigen_hh(n, _p(a), int(want_vectors), threads, _p(w), _p(v)), "kbr_eigen_hh")
     return w, (v if want_vectors else None)
+
+
+def triple_product(t, h):
+    t = np.ascontiguousarray(t, dtype=np.complex128)
+    h = np.ascontiguousarray(h, dtype=np.complex128)
+    n, m = t.shape
+    c = np.empty((m, m), dtype=np.complex128)
+    _call(lib().kbr_triple_product(n, m, _p(t), _p(h), _p(c)), "kbr_triple_product")
+    return c

@@ -132,6 +132,16 @@ int kbr_solve_tridiag(int64_t n, const double* d, const double* e, int want_vect
     });
 }
 
+// T^H H T (linalg.cpp triple_product): t [n x m], h [n x n] Hermitian, c [m x m].
+int kbr_triple_product(int64_t n, int64_t m, const double* t, const double* h, double* c) {
+    return guarded([&] {
+        kband::DenseMatrix T(n, m);
+        std::memcpy(static_cast<void*>(T.data()), t, sizeof(Complex) * n * m);
+        const kband::HermitianMatrix C = kband::triple_product(T, hermitian(n, h));
+        std::memcpy(c, static_cast<const void*>(C.dense().data()), sizeof(Complex) * m * m);
+    });
+}
+
 // Full reference eigensolver; vectors complex [n x n] (columns) if want_vectors.
 int kbr_eigen_hh(int64_t n, const double* a, int want_vectors, int threads, double* evals, double* vecs) {
     return guarded([&] {

@@ -138,6 +138,7 @@ KBGRID_SYMBOLS = [
     ("kbg_hh_back_transform_dev", _I, [_I64, _I64, _P, _P, _P, _P, _P, _P]),
     ("kbg_hh_normalize_columns", _I, [_I64, _I64, _DP]),
     ("kbg_hh_normalize_columns_dev", _I, [_I64, _I64, _P, _P]),
+    ("kbg_hh_triple_product", _I, [_I64, _I64, _DP, _DP, _DP]),
     ("kbg_hh_last_error", C.c_char_p, []),
 ]
 

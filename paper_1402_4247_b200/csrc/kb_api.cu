@@ -1161,8 +1161,8 @@ void hh_check_n(int64_t n) {
     if (n > 4800) throw Error(KBG_ERR_DIMENSION, "tridiagonalize: n = " + std::to_string(n) + " > 4800 (shared-memory reflectors)");
 }
 
-// HermitianMatrix::from on the device (linalg.cpp:44-63): reject a defect above 1e-13, then symmetrize.
-void hermitian_from(int64_t n, double* d_A, cudaStream_t st) {
+// HermitianMatrix::from on the device (linalg.cpp:44-63): reject a defect above tol, then symmetrize.
+void hermitian_from(int64_t n, double* d_A, cudaStream_t st, double tol = 1e-13) {
     DevBuf def(1, st);
     KBG_CUDA(cudaMemsetAsync(def.p, 0, sizeof(double), st));
     kbg::launch_hermitian_repair(static_cast<int>(n), d_A, reinterpret_cast<unsigned long long*>(def.p), false, st);
@@ -1170,8 +1170,9 @@ void hermitian_from(int64_t n, double* d_A, cudaStream_t st) {
     KBG_CUDA(cudaMemcpyAsync(&defect, def.p, sizeof(double), cudaMemcpyDeviceToHost, st));
     KBG_CUDA(cudaStreamSynchronize(st));
     if (!std::isfinite(defect)) throw Error(KBG_ERR_CONSISTENCY, "HermitianMatrix: non-finite entries");
-    if (defect > 1e-13)
-        throw Error(KBG_ERR_CONSISTENCY, "HermitianMatrix: defect " + std::to_string(defect) + " exceeds tolerance 1e-13");
+    if (defect > tol)
+        throw Error(KBG_ERR_CONSISTENCY, "HermitianMatrix: defect " + std::to_string(defect) + " exceeds tolerance " +
+                                             std::to_string(tol));
     kbg::launch_hermitian_repair(static_cast<int>(n), d_A, nullptr, true, st);
 }
 
@@ -1251,6 +1252,41 @@ int kbg_hh_back_transform(int64_t n, int64_t m, const double* u, const double* h
         KBG_CUDA(cudaMemcpyAsync(Y.p, y, static_cast<size_t>(n) * m * sizeof(double), cudaMemcpyHostToDevice, st));
         kbg::launch_hh_back_transform(static_cast<int>(n), static_cast<int>(m), Y.p, U.p, H.p, P.p, dph.p, W.p, st);
         KBG_CUDA(cudaMemcpyAsync(w, W.p, 2 * static_cast<size_t>(n) * m * sizeof(double), cudaMemcpyDeviceToHost, st));
+        KBG_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+// kband::triple_product (linalg.cpp:112-120): C = T^H H T with two ZGEMMs, then HermitianMatrix::from_scaled
+// (defect <= 1e-13 max(1, ||C||_F), symmetrized). Row-major buffers are their column-major transposes:
+// C^T = t h t^H with t = T^T (m x n), h = H^T.
+int kbg_hh_triple_product(int64_t n, int64_t m, const double* t, const double* h, double* c_out) {
+    if (!t || !h || !c_out || n < 1 || m < 1) return KBG_ERR_CONFIG;
+    return hh_guard([&] {
+        const cudaStream_t st = nullptr;
+        DevBuf T(2 * static_cast<size_t>(n) * m, st), H(2 * static_cast<size_t>(n) * n, st),
+            X(2 * static_cast<size_t>(n) * m, st), C(2 * static_cast<size_t>(m) * m, st);
+        KBG_CUDA(cudaMemcpyAsync(T.p, t, 2 * static_cast<size_t>(n) * m * sizeof(double), cudaMemcpyHostToDevice, st));
+        KBG_CUDA(cudaMemcpyAsync(H.p, h, 2 * static_cast<size_t>(n) * n * sizeof(double), cudaMemcpyHostToDevice, st));
+        cublasHandle_t bh = nullptr;
+        if (cublasCreate(&bh) != CUBLAS_STATUS_SUCCESS) throw Error(KBG_ERR_CUDA, "cublasCreate failed");
+        struct Destroy {
+            cublasHandle_t h;
+            ~Destroy() { cublasDestroy(h); }
+        } destroy{bh};
+        const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+        auto z = [](double* p) { return reinterpret_cast<cuDoubleComplex*>(p); };
+        const int N = static_cast<int>(n), M = static_cast<int>(m);
+        if (cublasSetStream(bh, st) != CUBLAS_STATUS_SUCCESS ||
+            cublasZgemm(bh, CUBLAS_OP_N, CUBLAS_OP_C, N, M, N, &one, z(H.p), N, z(T.p), M, &zero, z(X.p), N) !=
+                CUBLAS_STATUS_SUCCESS ||
+            cublasZgemm(bh, CUBLAS_OP_N, CUBLAS_OP_N, M, M, N, &one, z(T.p), M, z(X.p), N, &zero, z(C.p), M) !=
+                CUBLAS_STATUS_SUCCESS)
+            throw Error(KBG_ERR_CUDA, "triple_product: cublasZgemm failed");
+        double fro = 0.0;
+        if (cublasDznrm2(bh, M * M, z(C.p), 1, &fro) != CUBLAS_STATUS_SUCCESS)
+            throw Error(KBG_ERR_CUDA, "triple_product: cublasDznrm2 failed");
+        hermitian_from(m, C.p, st, 1e-13 * std::max(1.0, fro));
+        KBG_CUDA(cudaMemcpyAsync(c_out, C.p, 2 * static_cast<size_t>(m) * m * sizeof(double), cudaMemcpyDeviceToHost, st));
         KBG_CUDA(cudaStreamSynchronize(st));
     });
 }

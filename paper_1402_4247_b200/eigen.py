@@ -89,6 +89,18 @@ def normalize_columns(c: np.ndarray) -> np.ndarray:
     return c
 
 
+def triple_product(t: np.ndarray, h: np.ndarray) -> np.ndarray:
+    """kband::triple_product (Part 3): T^H H T, re-symmetrized and validated Hermitian (GPU ZGEMMs)."""
+    t = np.ascontiguousarray(t, dtype=np.complex128)
+    h = np.ascontiguousarray(h, dtype=np.complex128)
+    n, m = t.shape
+    if h.shape != (n, n):
+        raise DimensionError("triple_product: T rows must match H dim")
+    c = np.empty((m, m), dtype=np.complex128)
+    _check(_lib().kbg_hh_triple_product(n, m, _cptr(t), _cptr(h), _cptr(c)), "kbg_hh_triple_product")
+    return c
+
+
 def lapack_solve_tridiag(d: np.ndarray, e: np.ndarray, want_vectors: bool):
     """Host tridiagonal eigensolver (LAPACK via scipy), the paper's CPU step."""
     from scipy.linalg import eigh_tridiagonal
@@ -111,5 +123,5 @@ def eigen_hh(a: np.ndarray, want_vectors: bool = True, solve_tridiag=lapack_solv
     return np.asarray(w), normalize_columns(back_transform(t.records, np.ascontiguousarray(z)))
 
 
-__all__ = ["HouseholderRecords", "TridiagReal", "tridiagonalize", "back_transform", "normalize_columns",
+__all__ = ["HouseholderRecords", "TridiagReal", "tridiagonalize", "back_transform", "normalize_columns", "triple_product",
            "lapack_solve_tridiag", "eigen_hh"]

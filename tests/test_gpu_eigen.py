@@ -121,3 +121,15 @@ def test_bloch_hamiltonian_of_the_grid_pass():
     nrm = np.linalg.norm(hk)
     assert np.abs(w - rw).max() <= 1e-11 * nrm
     assert np.abs(hk @ v - v * w).max() <= 1e-9 * nrm
+
+
+@pytest.mark.parametrize("n,m", [(16, 16), (200, 150), (568, 568)])
+def test_triple_product_matches_reference(n, m):
+    """Part 3 S^H H S (kband triple_product): GPU ZGEMMs vs the reference's ascending-k matmul."""
+    rng = np.random.default_rng(n + m)
+    t = rng.standard_normal((n, m)) + 1j * rng.standard_normal((n, m))
+    h = hermitian(n, n + 1)
+    c = E.triple_product(t, h)
+    ref = R.triple_product(t, h)
+    assert np.abs(c - ref).max() <= 1e-12 * np.abs(ref).max()
+    assert np.array_equal(c, c.conj().T)
