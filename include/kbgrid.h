@@ -136,6 +136,12 @@ int kbg_build_index(kbg_ctx* ctx);
  * lay out DM / H in pair order). */
 int kbg_index_view(kbg_ctx* ctx, kbg_index* out);
 
+/* Execution plan chosen by kbg_build_index (diagnostics): info[0] persistent kernels in use (1/0),
+ * [1] intra-block schedule (KBG_OPT_SCHEDULE bits actually used), [2] rho partner-range split,
+ * [3] max padded Phi rows of a block, [4] max H tasks, [5] max rho tasks of a block,
+ * [6] / [7] dynamic shared memory per CTA of the H / rho persistent kernel (bytes). */
+int kbg_plan_info(const kbg_ctx* ctx, int64_t info[8]);
+
 /* Owned block range [blk_begin, blk_end) of this context (sharded or not). */
 int kbg_shard_range(const kbg_ctx* ctx, int64_t* blk_begin, int64_t* blk_end);
 
@@ -200,6 +206,10 @@ int kbg_last_tally(const kbg_ctx* ctx, kbg_tally* out);
  * block's tasks, heaviest first, form one queue the consumer warps pull from; clear = static LPT lists per
  * warp. Default 3. rho stays bitwise deterministic either way (per-task partial sums, fixed-order reduce). */
 #define KBG_OPT_SCHEDULE 6
+/* Order in which the persistent kernels pull grid blocks, read by kbg_build_index: 0 (default) heaviest
+ * first (load balance of the tail); 1 natural (i, j, k) block order (neighbouring blocks in flight share
+ * their atom pairs' DM / H entries in L1/L2). */
+#define KBG_OPT_BLOCK_ORDER 7
 int kbg_set_option(kbg_ctx* ctx, int option, int64_t value);
 
 const char* kbg_last_error(const kbg_ctx* ctx);

@@ -30,6 +30,7 @@ KBG_OPT_SCATTER_STORE = 3
 KBG_OPT_PERSIST = 4
 KBG_OPT_DEBUG_COUNTERS = 5
 KBG_OPT_SCHEDULE = 6
+KBG_OPT_BLOCK_ORDER = 7
 KBG_COMM_HANDLE_BYTES = 96
 KBG_CELL_PRIMITIVE = 0
 KBG_CELL_CUBIC = 1
@@ -98,6 +99,7 @@ KBGRID_SYMBOLS = [
     ("kbg_build_index", _I, [_P]),
     ("kbg_index_view", _I, [_P, C.POINTER(kbg_index)]),
     ("kbg_shard_range", _I, [_P, C.POINTER(_I64), C.POINTER(_I64)]),
+    ("kbg_plan_info", _I, [_P, C.POINTER(_I64)]),
     ("kbg_density", _I, [_P, _I, _DP, _DP]),
     ("kbg_hamiltonian", _I, [_P, _I, _DP, _D, _DP]),
     ("kbg_grid_pass", _I, [_P, _I, _DP, _DP, _D, _DP, _DP]),

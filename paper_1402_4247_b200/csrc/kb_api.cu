@@ -29,6 +29,9 @@ struct kbg_ctx {
     bool persist_ok = false;   // two staging buffers fit: persistent kernels
     int persist = 1;           // option: use the persistent kernels when they fit
     int schedule = 3;          // KBG_OPT_SCHEDULE
+    int block_order = 0;       // KBG_OPT_BLOCK_ORDER
+    int plan_schedule = -1;    // schedule / rho split the task lists were built with (kbg_plan_info)
+    int plan_split = 0;
     double* d_dmr = nullptr;   // repacked DM scratch
     size_t cap_dmr = 0;
     int* d_counter = nullptr;  // persistent work counters: [0] density, [1] H (the two may run concurrently)
@@ -228,6 +231,7 @@ kbg::GridArgs grid_args(kbg_ctx* c, int nspin, double dV, const double* in, doub
     g.tasks = density ? c->ix.rt : c->ix.ht;
     g.t_wptr = density ? c->ix.rt_wptr : c->ix.ht_wptr;
     g.max_tasks = std::max(1, std::max(c->ix.max_rtask, c->ix.max_htask));
+    g.max_rtasks = std::max(1, c->ix.max_rtask);
     g.tabs = density ? c->ix.rtab : c->ix.htab;
     g.tab_bytes = c->ix.tab_bytes;
     g.phis = c->ix.phis;
@@ -366,25 +370,30 @@ int kbg_build_index(kbg_ctx* c) {
         kbg::free_formats(c->fmt);
         kbg::build_index_device(c->P, c->ix, c->stream);
         // persistent kernels: one task queue (1 "warp") or LPT lists per consumer warp
-        auto persist_tasks = [&](int sched) {
+        auto persist_tasks = [&](int sched, int split) {
+            c->plan_schedule = sched;
+            c->plan_split = split;
             kbg::build_tasks_device(c->P, c->ix, (sched & 1) ? 1 : kbg::kPersistConsumersH,
-                                    (sched & 2) ? 1 : kbg::kPersistConsumersR, KBG_RHO_SPLIT, c->stream);
+                                    (sched & 2) ? 1 : kbg::kPersistConsumersR, split, c->stream);
             const kbg::GridArgs gd = grid_args(c, 1, 0.0, nullptr, nullptr, true);
             const kbg::GridArgs gh = grid_args(c, 1, 0.0, nullptr, nullptr, false);
             return kbg::persist_fits(gd, true) && kbg::persist_fits(gh, false);
         };
         c->built = true;
         shard(c);
-        c->persist_ok = persist_tasks(c->schedule);
-        // the rho queue keeps per-task partial sums in shared memory; drop it if they do not fit
-        if (!c->persist_ok && (c->schedule & 2)) c->persist_ok = persist_tasks(c->schedule & 1);
+        c->persist_ok = persist_tasks(c->schedule, KBG_RHO_SPLIT);
+        // The rho queue keeps per-task partial sums in shared memory (max_rtasks x 32 doubles per
+        // buffer); if they do not fit next to the largest block's Phi rows, fall back to static
+        // per-warp lists (~30 % slower rho).
+        if (!c->persist_ok && (c->schedule & 2)) c->persist_ok = persist_tasks(c->schedule & 1, KBG_RHO_SPLIT);
         if (!c->persist_ok) kbg::build_tasks_device(c->P, c->ix, 8, 8, 8, c->stream);
         // owned blocks, heaviest first, for the persistent kernels' work counter
         std::vector<int64_t> cost(c->ix.nblock);
         KBG_CUDA(cudaMemcpy(cost.data(), c->ix.blk_cost, cost.size() * sizeof(int64_t), cudaMemcpyDeviceToHost));
         std::vector<int64_t> order;
         for (int64_t b = c->blk_begin; b < c->blk_end; ++b) order.push_back(b);
-        std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return cost[x] > cost[y]; });
+        if (c->block_order == 0)
+            std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return cost[x] > cost[y]; });
         if (c->ix.order) cudaFree(c->ix.order);
         c->ix.order = nullptr;
         c->ix.norder = static_cast<int64_t>(order.size());
@@ -397,6 +406,21 @@ int kbg_build_index(kbg_ctx* c) {
                                     grid_args(c, 1, 0.0, nullptr, nullptr, true), c->ix, c->stream);
         }
     });
+}
+
+int kbg_plan_info(const kbg_ctx* c, int64_t info[8]) {
+    if (!c || !info) return KBG_ERR_CONFIG;
+    if (!c->built) return KBG_ERR_CONFIG;
+    kbg_ctx* m = const_cast<kbg_ctx*>(c);
+    info[0] = c->persist_ok ? 1 : 0;
+    info[1] = c->plan_schedule;
+    info[2] = c->plan_split;
+    info[3] = c->ix.max_rows_padded;
+    info[4] = c->ix.max_htask;
+    info[5] = c->ix.max_rtask;
+    info[6] = static_cast<int64_t>(kbg::persist_smem(grid_args(m, 1, 0.0, nullptr, nullptr, false), false));
+    info[7] = static_cast<int64_t>(kbg::persist_smem(grid_args(m, 1, 0.0, nullptr, nullptr, true), true));
+    return KBG_OK;
 }
 
 int kbg_index_view(kbg_ctx* c, kbg_index* out) {
@@ -1342,6 +1366,13 @@ int kbg_set_option(kbg_ctx* c, int option, int64_t value) {
             return KBG_OK;
         case KBG_OPT_PERSIST:
             c->persist = value ? 1 : 0;
+            return KBG_OK;
+        case KBG_OPT_BLOCK_ORDER:
+            if (value < 0 || value > 1) {
+                c->err = "set_option: block order must be 0 or 1";
+                return KBG_ERR_CONFIG;
+            }
+            c->block_order = static_cast<int>(value);
             return KBG_OK;
         case KBG_OPT_SCHEDULE:
             if (value < 0 || value > 3) {

@@ -19,6 +19,12 @@
 
 #include "kb_device.cuh"
 
+// L2 policy of the persistent kernels: 1 streams the geometry cache with
+// evict_first; 2 also loads the repacked DM with evict_last.
+#ifndef KBG_L2_HINT
+#define KBG_L2_HINT 1
+#endif
+
 namespace kbg {
 namespace core {
 
@@ -508,6 +514,10 @@ __device__ __forceinline__ void gather_a(const Smem& sm, int ncov, const int (&r
                                          int kc, const double* __restrict__ Dr, int lane, double (&a)[TM][4],
                                          int exp = 0) {
     const int stride = 16 * ((sm.cov()[cj].norb + 15) >> 4);
+#if KBG_L2_HINT >= 2
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#endif
 #pragma unroll
     for (int t = 0; t < TM; ++t) {
         const int ci = rci[t];
@@ -515,7 +525,13 @@ __device__ __forceinline__ void gather_a(const Smem& sm, int ncov, const int (&r
         if (off >= 0) {
             const double2* p = reinterpret_cast<const double2*>(
                 Dr + off + rri[t] * stride + 16 * kc + 4 * (lane & 3));
+#if KBG_L2_HINT >= 2
+            double2 v0, v1;
+            asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v0.x), "=d"(v0.y) : "l"(p), "l"(pol));
+            asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v1.x), "=d"(v1.y) : "l"(p + 1), "l"(pol));
+#else
             const double2 v0 = __ldg(p), v1 = __ldg(p + 1);
+#endif
             a[t][0] = v0.x;
             a[t][1] = v0.y;
             a[t][2] = v1.x;

@@ -175,7 +175,8 @@ struct GridArgs {
     int max_rows;       // Phi rows allocated (padded groups + 8 pad rows)
     int max_cover;
     int max_bpairs;
-    int max_tasks;
+    int max_tasks;      // table layout (shared by the H and rho images): max over both task kinds
+    int max_rtasks;     // rho tasks of a block (per-task partial sums of the rho queue)
     int nspin;
     int64_t nnz;
     int64_t npts;
@@ -286,6 +287,7 @@ constexpr int kPersistConsumersH = KBG_CONSUMERS_H;  // H: 28 warps (<= 72 regis
 void build_cache_device(GridArgs gh, GridArgs gr, DevIndex& ix, cudaStream_t st);
 void free_cache(DevIndex& ix);
 bool persist_fits(const GridArgs& g, bool density);
+size_t persist_smem(const GridArgs& g, bool density);
 int launch_density_persist(const GridArgs& g, cudaStream_t st);
 int launch_hamiltonian_persist(const GridArgs& g, cudaStream_t st);
 int launch_mirror(const DevIndex& ix, const SysParams& sys, int nspin, double* h, cudaStream_t st);

@@ -65,6 +65,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// Same with an L2 cache policy (createpolicy): the geometry cache is streamed
+// once per pass, so its lines are marked evict_first and do not push the
+// gathered operands (repacked DM, H accumulators, V) out of L2.
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
 // Two buffers at byte offsets 0 and bsz of kbg_smem, then the mbarriers.
 // Buffer s is selected arithmetically (no dynamically indexed struct arrays,
 // which would live in local memory).
@@ -93,7 +104,7 @@ __device__ __forceinline__ Buffers carve_all(const GridArgs& g) {
 // lists) or per-task sums [nspin][ntask][32] (task queue, task_warps == 1).
 __host__ __device__ inline size_t persist_acc(const GridArgs& g, bool density) {
     if (!density) return static_cast<size_t>(g.nspin) * 64;
-    if (g.task_warps == 1) return static_cast<size_t>(g.nspin) * g.max_tasks * 32;
+    if (g.task_warps == 1) return static_cast<size_t>(g.nspin) * g.max_rtasks * 32;
     return static_cast<size_t>(g.nspin) * 64 * kPersistConsumersR;
 }
 
@@ -126,8 +137,13 @@ __device__ int64_t next_block(const GridArgs& g, int lane) {
     }
 }
 
-__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes, uint64_t pol) {
+#if KBG_L2_HINT
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(src), "r"(bytes), "l"(pol)
+                 : "memory");
+#else
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+#endif
 }
 
 // Producer warp: block k goes to buffer k & 1. The block after the current
@@ -136,6 +152,10 @@ __device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
 template <bool DENSITY>
 __device__ void producer(const GridArgs& g, const Buffers& B, int lane) {
     unsigned long long t_wait = 0, t0 = clock64();
+    uint64_t pol = 0;
+#if KBG_L2_HINT
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#endif
     auto image = [&](int64_t b, const unsigned char*& tab, const double*& phi, uint32_t& tb, uint32_t& pb) {
         const int64_t i = b - g.blk_begin;
         tab = g.tabs + i * g.tab_bytes;
@@ -154,8 +174,8 @@ __device__ void producer(const GridArgs& g, const Buffers& B, int lane) {
                 const double* phi;
                 uint32_t tb, pb;
                 image(b_next, tab, phi, tb, pb);
-                prefetch_l2(tab, tb);
-                prefetch_l2(phi, pb);
+                prefetch_l2(tab, tb, pol);
+                prefetch_l2(phi, pb, pol);
             }
         }
         if (k >= 2) {
@@ -191,8 +211,13 @@ __device__ void producer(const GridArgs& g, const Buffers& B, int lane) {
             uint32_t tb, pb;
             image(b, tab, phi, tb, pb);
             mbar_arrive_tx(&B.full[s], tb + pb);
+#if KBG_L2_HINT
+            bulk_g2s_hint(sm.meta(), tab, tb, &B.full[s], pol);
+            bulk_g2s_hint(sm.phi(), phi, pb, &B.full[s], pol);
+#else
             bulk_g2s(sm.meta(), tab, tb, &B.full[s]);
             bulk_g2s(sm.phi(), phi, pb, &B.full[s]);
+#endif
             if (g.dbg) {  // debug only: copy latency (delays the next fetch)
                 const unsigned long long tc = clock64();
                 mbar_wait(&B.full[s], (k >> 1) & 1);
@@ -365,6 +390,7 @@ int launch_persist(const GridArgs& g0, bool density, cudaStream_t st) {
 }  // namespace
 
 bool persist_fits(const GridArgs& g, bool density) { return persist_bytes(g, density) <= 227 * 1024; }
+size_t persist_smem(const GridArgs& g, bool density) { return persist_bytes(g, density); }
 
 int launch_density_persist(const GridArgs& g, cudaStream_t st) { return launch_persist(g, true, st); }
 int launch_hamiltonian_persist(const GridArgs& g, cudaStream_t st) { return launch_persist(g, false, st); }

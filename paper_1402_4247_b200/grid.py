@@ -77,6 +77,13 @@ class GridPass:
         self._check(self._lib.kbg_shard_range(self._h, C.byref(b0), C.byref(b1)), "kbg_shard_range")
         return b0.value, b1.value
 
+    def plan_info(self) -> dict:
+        """Execution plan kbg_build_index chose (persistent kernels, schedule, rho split, sizes)."""
+        v = (C.c_int64 * 8)()
+        self._check(self._lib.kbg_plan_info(self._h, v), "kbg_plan_info")
+        keys = ("persist", "schedule", "rho_split", "max_rows", "max_htask", "max_rtask", "smem_h", "smem_rho")
+        return dict(zip(keys, (int(x) for x in v)))
+
     # -- G2 ------------------------------------------------------------------
     def block_orbitals(self, block: int) -> np.ndarray:
         cap = 64 * 64 * 32

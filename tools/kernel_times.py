@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--nspin", type=int, default=1)
     ap.add_argument("--schedules", default="3,0,1,2", help="KBG_OPT_SCHEDULE values (persistent kernels)")
     ap.add_argument("--fallback", type=int, default=1, help="also time the one-CTA-per-block kernels")
+    ap.add_argument("--orders", default="0", help="KBG_OPT_BLOCK_ORDER values (persistent kernels)")
     ap.add_argument("--scatter", type=int, default=0, help="KBG_OPT_SCATTER_STORE timing experiment bits")
     a = ap.parse_args()
     f = Fe3O4.config(a.config)
@@ -49,12 +50,15 @@ def main():
         return float(np.median(ts)), float(np.min(ts))
 
     ref = {}
-    variants = [(int(x), 1) for x in a.schedules.split(",")] + ([(3, 0)] if a.fallback else [])
-    for sched, persist in variants:
+    variants = [(int(x), 1, int(o)) for x in a.schedules.split(",") for o in a.orders.split(",")]
+    variants += [(3, 0, 0)] if a.fallback else []
+    for sched, persist, order in variants:
         gp = GridPass(f.system)
         gp.set_option(_abi.KBG_OPT_SCHEDULE, sched)
+        gp.set_option(_abi.KBG_OPT_BLOCK_ORDER, order)
         ix = gp.build_index()
         gp.set_option(_abi.KBG_OPT_PERSIST, persist)
+        plan = gp.plan_info()
         gp.set_option(_abi.KBG_OPT_SCATTER_STORE, a.scatter)
         d_dm = torch.from_numpy(f.dm(ix, nspin=a.nspin)).to(dev)
         d_v = torch.from_numpy(f.veff(nspin=a.nspin)).to(dev)
@@ -75,6 +79,7 @@ def main():
             fn()
             torch.cuda.synchronize()
             rec = {"config": a.config, "lib": os.environ.get("KBG_LIBKBGRID", "default"), "scatter_exp": a.scatter, "kernel": name, "schedule": sched, "persist": persist,
+                   "block_order": order, "plan": plan,
                    "median_ms": round(med, 4), "min_ms": round(mn, 4),
                    "alg_tflops": round(fl / (med * 1e-3) / 1e12, 3),
                    "bitwise_repeat": bool(torch.equal(r1, out))}

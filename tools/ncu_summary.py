@@ -25,6 +25,9 @@ KEYS = {
     "launch__grid_size": "grid",
     "launch__block_size": "block",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum": "smem_ld_bank_conflicts",
+    "lts__t_sector_hit_rate.pct": "l2_hit_pct",
+    "l1tex__t_sector_hit_rate.pct": "l1_hit_pct",
+    "lts__t_sectors_srcunit_tex_op_read.sum": "l2_read_sectors_from_sm",
 }
 
 
