@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <string>
@@ -288,6 +289,31 @@ int run_hamiltonian(kbg_ctx* c, int nspin, double dV, const double* d_veff, doub
     return kbg::launch_hamiltonian(g, c->blk_end - c->blk_begin, c->nwarps, st);
 }
 
+// Device alias of a caller's host buffer that the GPU can read in place (pinned
+// or registered, hence mapped under UVA), else nullptr. Only the persistent H
+// kernel reads its input this way: its producer warp loads a block's 64 V
+// values one block ahead, so the PCIe reads hide behind the DMMA work and the
+// pass does not wait for a whole-array H2D copy first.
+const double* mapped_input(const kbg_ctx* c, const double* host) {
+    if (!(c->persist_ok && c->persist && c->ix.phis) || std::getenv("KBG_NO_ZERO_COPY")) return nullptr;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, host) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return nullptr;
+    }
+    if (a.type != cudaMemoryTypeHost || !a.devicePointer) return nullptr;
+    return static_cast<const double*>(a.devicePointer);
+}
+
+// Same for an output: the persistent density kernel stores each finished
+// block's 64 points in C order (32-byte segments), so with rho in pinned host
+// memory the result streams over PCIe during the kernel instead of in one D2H
+// copy after it. Single-rank contexts only (a shard must zero foreign points).
+double* mapped_output(const kbg_ctx* c, double* host) {
+    if (c->nranks > 1 || std::getenv("KBG_NO_ZERO_COPY_OUT")) return nullptr;
+    return const_cast<double*>(mapped_input(c, host));
+}
+
 void shard(kbg_ctx* c) {
     const int64_t nb = c->ix.nblock;
     if (c->nranks == 1) {
@@ -549,9 +575,10 @@ int kbg_hamiltonian(kbg_ctx* c, int nspin, const double* veff, double dV, double
         const size_t nin = static_cast<size_t>(nspin) * c->npts, nout = static_cast<size_t>(nspin) * c->ix.nnz;
         ensure(c->d_in, c->cap_in, nin);
         ensure(c->d_out, c->cap_out, nout);
-        KBG_CUDA(cudaMemcpyAsync(c->d_in, veff, nin * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        const double* v_map = mapped_input(c, veff);
+        if (!v_map) KBG_CUDA(cudaMemcpyAsync(c->d_in, veff, nin * sizeof(double), cudaMemcpyHostToDevice, c->stream));
         KBG_CUDA(cudaMemsetAsync(c->d_out, 0, nout * sizeof(double), c->stream));
-        int n = run_hamiltonian(c, nspin, dV, c->d_in, c->d_out, c->stream);
+        int n = run_hamiltonian(c, nspin, dV, v_map ? v_map : c->d_in, c->d_out, c->stream);
         n += kbg::launch_mirror(c->ix, c->P, nspin, c->d_out, c->stream);
         c->last_launches = n;
         KBG_CUDA(cudaMemcpyAsync(h, c->d_out, nout * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -580,10 +607,14 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
         // smaller one to wait for and rho (npts) the smaller output left after the last kernel. The DM
         // check is read at the end.
         int n = 0;
+        // V from pinned host memory is read in place by the H kernel (mapped_input)
+        const double* v_map = mapped_input(c, veff);
+        double* rho_map = mapped_output(c, rho);
         auto h_half = [&] {
-            KBG_CUDA(cudaMemcpyAsync(c->d_in2, veff, npt * sizeof(double), cudaMemcpyHostToDevice, c->stream2));
+            if (!v_map)
+                KBG_CUDA(cudaMemcpyAsync(c->d_in2, veff, npt * sizeof(double), cudaMemcpyHostToDevice, c->stream2));
             KBG_CUDA(cudaMemsetAsync(c->d_out2, 0, ndm * sizeof(double), c->stream2));
-            n += run_hamiltonian(c, nspin, dV, c->d_in2, c->d_out2, c->stream2);
+            n += run_hamiltonian(c, nspin, dV, v_map ? v_map : c->d_in2, c->d_out2, c->stream2);
             n += kbg::launch_mirror(c->ix, c->P, nspin, c->d_out2, c->stream2);
             KBG_CUDA(cudaMemcpyAsync(h, c->d_out2, ndm * sizeof(double), cudaMemcpyDeviceToHost, c->stream2));
         };
@@ -592,8 +623,9 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
             KBG_CUDA(cudaMemsetAsync(c->d_check, 0, 4 * sizeof(unsigned long long), c->stream));
             n += kbg::launch_dm_check(c->ix, c->P, nspin, c->d_in, c->d_check, c->stream);
             if (c->nranks > 1) KBG_CUDA(cudaMemsetAsync(c->d_out, 0, npt * sizeof(double), c->stream));
-            n += run_density(c, nspin, c->d_in, c->d_out, c->stream);
-            KBG_CUDA(cudaMemcpyAsync(rho, c->d_out, npt * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+            n += run_density(c, nspin, c->d_in, rho_map ? rho_map : c->d_out, c->stream);
+            if (!rho_map)
+                KBG_CUDA(cudaMemcpyAsync(rho, c->d_out, npt * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         };
 #ifndef KBG_PASS_RHO_FIRST
         h_half();

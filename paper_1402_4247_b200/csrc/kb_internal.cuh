@@ -14,6 +14,7 @@ namespace kbg {
 
 constexpr int kMaxSpecies = 8;
 constexpr int kMaxRad = 16;
+constexpr int kMaxSpin = 2;  // nspin is 1 or 2 (check_nspin)
 constexpr int kGroupRows = 16;  // covers are packed into row groups of <= 16 orbitals (2 DMMA row tiles)
 constexpr int kMaxTaskWarps = 32;  // task lists are LPT-balanced over <= 24 consumer warps
 constexpr int kMaxCoverPerBlock = 64;

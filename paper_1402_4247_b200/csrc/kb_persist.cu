@@ -163,12 +163,33 @@ __device__ void producer(const GridArgs& g, const Buffers& B, int lane) {
         tb = static_cast<uint32_t>(g.tab_bytes);
         pb = static_cast<uint32_t>((g.phi_off[i + 1] - g.phi_off[i]) * sizeof(double));
     };
+    // H: w = V dV of a block's points is loaded into registers one block ahead
+    // (lane l holds points l and 32 + l of every spin), so the loads -- from
+    // HBM, or over PCIe when V is mapped host memory (kbg_grid_pass on pinned
+    // buffers) -- are in flight while the producer waits for a free buffer.
+    double w_cur[2 * kMaxSpin], w_next[2 * kMaxSpin];
+    auto load_w = [&](int64_t b, double (&w)[2 * kMaxSpin]) {
+        if (DENSITY || !g.in || b < 0) return;
+        int bi, bj, bk;
+        block_decode(g.sys, b, bi, bj, bk);
+#pragma unroll
+        for (int j = 0; j < 2 * kMaxSpin; ++j) {
+            const int i = lane + 32 * j;
+            bool valid = false;
+            const int64_t pt = slot_point(g.sys, bi, bj, bk, i & 63, valid);
+            w[j] = (valid && i < g.nspin * 64) ? g.in[(i >> 6) * g.npts + pt] : 0.0;
+        }
+    };
     int64_t b_next = next_block<DENSITY>(g, lane);
+    load_w(b_next, w_next);
     for (int k = 0;; ++k) {
         const int s = k & 1;
         const int64_t b = b_next;
+#pragma unroll
+        for (int j = 0; j < 2 * kMaxSpin; ++j) w_cur[j] = w_next[j];
         if (b >= 0) {
             b_next = next_block<DENSITY>(g, lane);
+            load_w(b_next, w_next);
             if (b_next >= 0 && lane == 0) {
                 const unsigned char* tab;
                 const double* phi;
@@ -196,12 +217,10 @@ __device__ void producer(const GridArgs& g, const Buffers& B, int lane) {
             return;
         }
         if (!DENSITY && g.in) {  // w = V dV of the block's points, every spin
-            int bi, bj, bk;
-            block_decode(g.sys, b, bi, bj, bk);
-            for (int i = lane; i < g.nspin * 64; i += 32) {
-                bool valid;
-                const int64_t pt = slot_point(g.sys, bi, bj, bk, i & 63, valid);
-                sm.acc()[i] = valid ? g.in[(i >> 6) * g.npts + pt] * g.dV : 0.0;
+#pragma unroll
+            for (int j = 0; j < 2 * kMaxSpin; ++j) {
+                const int i = lane + 32 * j;
+                if (i < g.nspin * 64) sm.acc()[i] = w_cur[j] * g.dV;
             }
         }
         __syncwarp();
@@ -306,22 +325,45 @@ __device__ void consumer(const GridArgs& g, const Buffers& B, int cw, int lane) 
                 block_decode(g.sys, b, bi, bj, bk);
                 if (g.task_warps == 1) {
                     // per-task sums in task order: lane l owns slots l (half 0) and 32 + l (half 1)
-                    for (int spin = 0; spin < g.nspin; ++spin) {
+                    double r[kMaxSpin][2];
+#pragma unroll
+                    for (int spin = 0; spin < kMaxSpin; ++spin) {
+                        r[spin][0] = r[spin][1] = 0.0;
+                        if (spin >= g.nspin) continue;
                         const double* res = sm.acc() + static_cast<size_t>(spin) * ntask * 32;
-                        double r0 = 0.0, r1 = 0.0;
                         for (int e = 0; e < ntask; ++e) {
                             const double v = res[e * 32 + lane];
                             if (sm.task()[e].half)
-                                r1 += v;
+                                r[spin][1] += v;
                             else
-                                r0 += v;
-                        }
-                        for (int hh = 0; hh < 2; ++hh) {
-                            bool valid;
-                            const int64_t pt = slot_point(g.sys, bi, bj, bk, 32 * hh + lane, valid);
-                            if (valid) g.out[spin * g.npts + pt] = hh ? r1 : r0;
+                                r[spin][0] += v;
                         }
                     }
+                    // Store in C order: the slots go through the (now idle) Phi rows so each
+                    // group of 4 lanes writes 4 consecutive k -- 32-byte segments instead of
+                    // the octet layout's 16 (HBM sectors; PCIe writes when rho is mapped host
+                    // memory). The next block's bulk copy rewrites these rows.
+                    double* tmp = sm.phi();
+                    __syncwarp();
+#pragma unroll
+                    for (int spin = 0; spin < kMaxSpin; ++spin) {
+                        tmp[spin * 64 + lane] = r[spin][0];
+                        tmp[spin * 64 + 32 + lane] = r[spin][1];
+                    }
+                    __syncwarp();
+                    const int lj = (lane >> 2) & 3, lk = lane & 3;
+                    const int j = bj * 4 + lj, kk = bk * 4 + lk;
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const int li = 2 * hh + (lane >> 4);
+                        const int slot = ((((li >> 1) << 2) | ((lj >> 1) << 1) | (lk >> 1)) << 3) |
+                                         ((li & 1) << 2) | ((lj & 1) << 1) | (lk & 1);
+                        const int i = bi * 4 + li;
+                        if (i < g.sys.N[0] && j < g.sys.N[1] && kk < g.sys.N[2]) {
+                            const int64_t pt = (static_cast<int64_t>(i) * g.sys.N[1] + j) * g.sys.N[2] + kk;
+                            for (int spin = 0; spin < g.nspin; ++spin) g.out[spin * g.npts + pt] = tmp[spin * 64 + slot];
+                        }
+                    }
+                    __syncwarp();
                 } else
                 for (int i = lane; i < g.nspin * 64; i += 32) {
                     const int spin = i >> 6, p = i & 63;

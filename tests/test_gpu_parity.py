@@ -262,3 +262,20 @@ def test_plan_uses_task_queues(name):
     plan = gp.plan_info()
     assert plan["persist"] == 1 and plan["schedule"] == 3, plan
     assert max(plan["smem_h"], plan["smem_rho"]) <= 227 * 1024, plan
+
+
+@pytest.mark.parametrize("name,nspin", [("cubic56_200Ry", 1), ("primitive14_150Ry", 2)])
+def test_grid_pass_pinned_zero_copy(name, nspin):
+    """Pinned (mapped) host V is read in place by the persistent H kernel (no H2D copy of V):
+    the same H as from pageable buffers, rho unchanged bitwise."""
+    import torch
+
+    c = case(name, nspin)
+    dm_p = torch.from_numpy(c.dm).pin_memory().numpy()
+    v_p = torch.from_numpy(c.veff).pin_memory().numpy()
+    rho_p, h_p = c.gp.grid_pass(dm_p, v_p, c.f.dV)
+    rho, h = c.gp.grid_pass(c.dm, c.veff, c.f.dV)
+    assert np.array_equal(rho_p, rho)
+    assert normwise(h_p, h) <= 1e-14
+    assert normwise(h_p, c.o.hamiltonian(c.veff, c.f.dV)) <= TOL
+    assert normwise(c.gp.hamiltonian(v_p, c.f.dV), h) <= 1e-14
