@@ -325,7 +325,7 @@ def main():
             # one SCF grid pass through the host C-ABI: rho and H with overlapped transfers
             st = lib.kbg_grid_pass(gp.handle, nspin, C.cast(p_dm.data_ptr(), dp), C.cast(p_veff.data_ptr(), dp),
                                    f.dV, C.cast(p_rho.data_ptr(), dp), C.cast(p_h.data_ptr(), dp))
-            if world > 1:
+            if world > 1 and not p2p:  # NCCL mode: partial H summed through the device
                 t = p_h.to(dev, non_blocking=False)
                 dist.all_reduce(t)
                 p_h.copy_(t)
@@ -347,10 +347,12 @@ def main():
             t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
-        h2d = 8 * nspin * (nnz + npts) + (8 * nspin * nnz if world > 1 else 0)
-        d2h = 8 * nspin * (npts + nnz) + (8 * nspin * nnz if world > 1 else 0)
+        extra = 8 * nspin * nnz if (world > 1 and not p2p) else 0
+        h2d = 8 * nspin * (nnz + npts) + extra
+        d2h = 8 * nspin * (npts + nnz) + extra
         e2e = {"value": round(e_ms, 4), "unit": "ms", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "api": "kbg_grid_pass (host pointers, pinned; rho and H halves on two streams)"}
+               "api": "kbg_grid_pass (host pointers, pinned: V read / rho written in place by the kernels; "
+                      "rho and H halves on two streams" + ("; full H via the fused NVLink reduction)" if p2p else ")")}
 
     # roofline of the dominant kernel (FP64 DMMA pipe)
     peak = dgemm_peak_tflops(torch, dev) if rank == 0 else None

@@ -159,7 +159,10 @@ int kbg_hamiltonian(kbg_ctx* ctx, int nspin, const double* veff, double dV, doub
  * two streams so each half's host<->device copies overlap the other half's
  * kernels (pinned host buffers make the copies asynchronous). DM is checked
  * like kbg_density; on a violation the status is KBG_ERR_CONSISTENCY and the
- * outputs are invalid. */
+ * outputs are invalid. Pinned (mapped) host veff / rho are read / written in
+ * place by the kernels, without staging copies. On a sharded context after
+ * kbg_comm_open, h is the full H on every rank (fused NVLink reduction; every
+ * rank must make the call) and rho holds this rank's points. */
 int kbg_grid_pass(kbg_ctx* ctx, int nspin, const double* dm, const double* veff, double dV, double* rho,
                   double* h);
 

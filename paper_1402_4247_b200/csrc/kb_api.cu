@@ -314,13 +314,12 @@ double* mapped_output(const kbg_ctx* c, double* host) {
     return const_cast<double*>(mapped_input(c, host));
 }
 
-void shard(kbg_ctx* c) {
+// Block ranges of every rank: rank r owns [bounds[r], bounds[r + 1]).
+std::vector<int64_t> shard_bounds(kbg_ctx* c) {
     const int64_t nb = c->ix.nblock;
-    if (c->nranks == 1) {
-        c->blk_begin = 0;
-        c->blk_end = nb;
-        return;
-    }
+    std::vector<int64_t> out(c->nranks + 1, nb);
+    out[0] = 0;
+    if (c->nranks == 1) return out;
     std::vector<int64_t> cost(nb);
     KBG_CUDA(cudaMemcpy(cost.data(), c->ix.blk_cost, nb * sizeof(int64_t), cudaMemcpyDeviceToHost));
     // Contiguous cost-balanced split; mirrors
@@ -343,8 +342,14 @@ void shard(kbg_ctx* c) {
         }
         return lo;
     };
-    c->blk_begin = bound(c->rank);
-    c->blk_end = bound(c->rank + 1);
+    for (int r = 0; r <= c->nranks; ++r) out[r] = bound(r);
+    return out;
+}
+
+void shard(kbg_ctx* c) {
+    const std::vector<int64_t> b = shard_bounds(c);
+    c->blk_begin = b[c->rank];
+    c->blk_end = b[c->rank + 1];
 }
 
 }  // namespace
@@ -613,9 +618,19 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
         auto h_half = [&] {
             if (!v_map)
                 KBG_CUDA(cudaMemcpyAsync(c->d_in2, veff, npt * sizeof(double), cudaMemcpyHostToDevice, c->stream2));
-            KBG_CUDA(cudaMemsetAsync(c->d_out2, 0, ndm * sizeof(double), c->stream2));
-            n += run_hamiltonian(c, nspin, dV, v_map ? v_map : c->d_in2, c->d_out2, c->stream2);
-            n += kbg::launch_mirror(c->ix, c->P, nspin, c->d_out2, c->stream2);
+            const double* vin = v_map ? v_map : c->d_in2;
+            if (c->comm_ready) {
+                // sharded: partials into the peer-mapped exchange buffer, then the fused reduce +
+                // mirror over NVLink (kb_comm.cu) -- the full H on every rank
+                KBG_CUDA(cudaMemsetAsync(c->d_xbuf, 0, ndm * sizeof(double), c->stream2));
+                n += run_hamiltonian(c, nspin, dV, vin, c->d_xbuf, c->stream2);
+                c->epoch += 2;
+                n += kbg::launch_reduce_mirror(c->comm, c->ix, c->P, nspin, c->d_out2, c->epoch - 1, c->stream2);
+            } else {
+                KBG_CUDA(cudaMemsetAsync(c->d_out2, 0, ndm * sizeof(double), c->stream2));
+                n += run_hamiltonian(c, nspin, dV, vin, c->d_out2, c->stream2);
+                n += kbg::launch_mirror(c->ix, c->P, nspin, c->d_out2, c->stream2);
+            }
             KBG_CUDA(cudaMemcpyAsync(h, c->d_out2, ndm * sizeof(double), cudaMemcpyDeviceToHost, c->stream2));
         };
         auto rho_half = [&] {
@@ -1134,14 +1149,20 @@ int kbg_comm_open(kbg_ctx* c, const void* handles) {
         const int64_t w1 = c->rank + 1 == c->nranks ? static_cast<int64_t>(canon.size())
                                                      : std::min<int64_t>(bound(c->rank + 1), static_cast<int64_t>(canon.size()));
         if (c->ix.nnz >= (int64_t(1) << 31)) throw Error(KBG_ERR_DIMENSION, "comm_open: nnz >= 2^31");
+        // ranks whose shard accumulates into each pair (the others' partials are exact zeros)
+        std::vector<uint32_t> owners;
+        kbg::pair_owners(c->ix, shard_bounds(c), owners, c->stream);
         std::vector<int32_t> e0, e1;
+        std::vector<uint8_t> em;
         for (int64_t w = w0; w < w1; ++w) {
             const int64_t p = canon[w], q = h.pair_mirror[p];
+            const uint8_t om = static_cast<uint8_t>(owners[p]);
             const int na = c->P.sp[c->h_spc[h.pair_a[p]]].norb, nb = c->P.sp[c->h_spc[h.pair_b[p]]].norb;
             for (int i = 0; i < na; ++i)
                 for (int j = 0; j < nb; ++j) {
                     if (q == p && i > j) continue;  // (a, a, 0): the upper triangle carries both entries
                     e0.push_back(static_cast<int32_t>(h.pair_off[p] + i * nb + j));
+                    em.push_back(om);
                     if (q == p)
                         e1.push_back(static_cast<int32_t>(h.pair_off[p] + j * na + i) | (i < j ? INT32_MIN : 0));
                     else
@@ -1150,13 +1171,15 @@ int kbg_comm_open(kbg_ctx* c, const void* handles) {
         }
         if (c->d_canon) cudaFree(c->d_canon);
         c->d_canon = nullptr;
-        KBG_CUDA(cudaMalloc(&c->d_canon, std::max<size_t>(1, 2 * e0.size()) * sizeof(int32_t)));
+        KBG_CUDA(cudaMalloc(&c->d_canon, std::max<size_t>(1, 2 * e0.size() + (e0.size() + 3) / 4) * sizeof(int32_t)));
         if (!e0.empty()) {
             KBG_CUDA(cudaMemcpy(c->d_canon, e0.data(), e0.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
             KBG_CUDA(cudaMemcpy(c->d_canon + e0.size(), e1.data(), e1.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+            KBG_CUDA(cudaMemcpy(c->d_canon + 2 * e0.size(), em.data(), em.size(), cudaMemcpyHostToDevice));
         }
         cm.el0 = c->d_canon;
         cm.el1 = c->d_canon + e0.size();
+        cm.elm = reinterpret_cast<const uint8_t*>(c->d_canon + 2 * e0.size());
         cm.ne = static_cast<int64_t>(e0.size());
         c->comm_ready = true;
     });

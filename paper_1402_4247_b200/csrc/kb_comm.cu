@@ -82,11 +82,15 @@ __global__ void __launch_bounds__(256) k_reduce_mirror(CommArgs c, int nspin, in
         const int32_t m = el1[el];
         const bool sym = m < 0;  // (a, a, 0) off-diagonal: (H + H^T) / 2
         const int64_t o1 = base + (m & 0x7fffffff);
+        // only the ranks whose shard touches the pair are read: the other partials are exact
+        // zeros, so the rank-order sum has the same bits as over all N
+        const uint32_t om = c.elm[el];
         double part[kMaxRanks], part2[kMaxRanks];
 #pragma unroll
         for (int k = 0; k < kMaxRanks; ++k) {
-            part[k] = k < c.nranks ? c.x[k][o0] : 0.0;
-            part2[k] = (sym && k < c.nranks) ? c.x[k][o1] : 0.0;
+            const bool on = k < c.nranks && ((om >> k) & 1u);
+            part[k] = on ? c.x[k][o0] : 0.0;
+            part2[k] = (sym && on) ? c.x[k][o1] : 0.0;
         }
         double v = 0.0, v2 = 0.0;
 #pragma unroll
@@ -95,9 +99,11 @@ __global__ void __launch_bounds__(256) k_reduce_mirror(CommArgs c, int nspin, in
             v2 += part2[k];
         }
         if (sym) v = 0.5 * (v + v2);
+        // canonical entries only (and both halves of an (a, a, 0) block): every rank then fills
+        // the mirror blocks H_ba(-R) = H_ab(R)^T locally (k_mirror), halving the NVLink writes
         for (int k = 0; k < c.nranks; ++k) {
             c.x[k][o0] = v;
-            c.x[k][o1] = v;
+            if (sym) c.x[k][o1] = v;
         }
     }
     // slice written everywhere: the last CTA signals epoch + 1 (the barrier
@@ -138,7 +144,50 @@ int launch_reduce_mirror(const CommArgs& c, const DevIndex& ix, const SysParams&
     const int64_t n = static_cast<int64_t>(nspin) * ix.nnz;
     k_comm_copy_out<<<static_cast<unsigned>(sms) * 4, 256, 0, st>>>(c, n, d_out, epoch + 1);
     KBG_CUDA(cudaGetLastError());
-    return 2;
+    return 2 + launch_mirror(ix, sys, nspin, d_out, st);
+}
+
+namespace {
+__global__ void k_pair_owners(int64_t nblock, const int64_t* __restrict__ bp_ptr, const BPair* __restrict__ bp,
+                              const int64_t* __restrict__ pair_off, int64_t npair, const int64_t* __restrict__ bounds,
+                              int nranks, uint32_t* own) {
+    const int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (b >= nblock) return;
+    int r = 0;
+    while (r + 1 < nranks && b >= bounds[r + 1]) ++r;
+    for (int64_t e = bp_ptr[b]; e < bp_ptr[b + 1]; ++e) {
+        const int64_t off = bp[e].off;
+        int64_t lo = 0, hi = npair - 1;  // pair with pair_off[p] == off
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) / 2;
+            if (pair_off[mid] <= off)
+                lo = mid;
+            else
+                hi = mid - 1;
+        }
+        atomicOr(own + lo, 1u << r);
+    }
+}
+}  // namespace
+
+void pair_owners(const DevIndex& ix, const std::vector<int64_t>& bounds, std::vector<uint32_t>& out, cudaStream_t st) {
+    const int nranks = static_cast<int>(bounds.size()) - 1;
+    out.assign(ix.npair, 0u);
+    if (ix.npair == 0) return;
+    uint32_t* d_own = nullptr;
+    int64_t* d_b = nullptr;
+    KBG_CUDA(cudaMalloc(&d_own, ix.npair * sizeof(uint32_t)));
+    KBG_CUDA(cudaMalloc(&d_b, bounds.size() * sizeof(int64_t)));
+    KBG_CUDA(cudaMemsetAsync(d_own, 0, ix.npair * sizeof(uint32_t), st));
+    KBG_CUDA(cudaMemcpyAsync(d_b, bounds.data(), bounds.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    k_pair_owners<<<static_cast<unsigned>((ix.nblock + 127) / 128), 128, 0, st>>>(ix.nblock, ix.bp_ptr, ix.bp,
+                                                                                 ix.pair_off, ix.npair, d_b, nranks,
+                                                                                 d_own);
+    KBG_CUDA(cudaGetLastError());
+    KBG_CUDA(cudaMemcpyAsync(out.data(), d_own, ix.npair * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    KBG_CUDA(cudaStreamSynchronize(st));
+    cudaFree(d_own);
+    cudaFree(d_b);
 }
 
 }  // namespace kbg

@@ -243,8 +243,12 @@ struct CommArgs {
     // mirror offset (bit 31: transposed entry of an (a,a,0) block, averaged)
     const int32_t* el0 = nullptr;
     const int32_t* el1 = nullptr;
+    const uint8_t* elm = nullptr;  // ranks whose partial of the entry can be nonzero (bit k: rank k)
     int64_t ne = 0;
 };
+// Per pair, the ranks (bit k) whose block range [bounds[k], bounds[k + 1]) holds
+// a canonical (block, cover pair) work item of that pair.
+void pair_owners(const DevIndex& ix, const std::vector<int64_t>& bounds, std::vector<uint32_t>& out, cudaStream_t st);
 int launch_reduce_mirror(const CommArgs& c, const DevIndex& ix, const SysParams& sys, int nspin, double* d_out,
                          unsigned long long epoch, cudaStream_t st);
 

@@ -74,6 +74,34 @@ def main(cfg="cubic56_200Ry"):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    # host API on the sharded context: kbg_grid_pass returns the full H (fused reduction) on every rank
+    dm = f.dm(ix)
+    dm_p = torch.from_numpy(dm).pin_memory().numpy()
+    v_p = torch.from_numpy(f.veff()).pin_memory().numpy()
+    rho_g, h_g = gp.grid_pass(dm_p, v_p, f.dV)
+    d_gp = float(np.abs(h_g[0] - h_p2p.cpu().numpy()[0]).max() / np.abs(h_g[0]).max())
+    d_gp_t = torch.tensor([d_gp], device=dev)
+    dist.all_reduce(d_gp_t, op=dist.ReduceOp.MAX)
+    d_gp = float(d_gp_t.item())
+    rho_t = torch.from_numpy(rho_g).to(dev)
+    dist.all_reduce(rho_t)  # owned points only per rank: the sum is the full density
+
+    def local_ms(fn, reps=20):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            fn()
+            e1.record(st)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return float(np.median(ts))
+
+    acc_ranks = [None] * world
+    dist.all_gather_object(acc_ranks, round(local_ms(lambda: gp.hamiltonian_accumulate_dev(v, f.dV, h_nccl, st)), 4))
     t_p2p = timeit(p2p)
     t_nccl = timeit(nccl)
     t_acc = timeit(lambda: gp.hamiltonian_accumulate_dev(v, f.dV, h_nccl, st))
@@ -82,12 +110,16 @@ def main(cfg="cubic56_200Ry"):
         full.build_index()
         ref = full.hamiltonian(f.veff(), f.dV)[0]
         d_full = float(np.abs(h_p2p.cpu().numpy()[0] - ref).max() / np.abs(ref).max())
+        rho_ref = full.density(dm)[0]
+        d_rho = float(np.abs(rho_t.cpu().numpy()[0] - rho_ref).max() / np.abs(rho_ref).max())
         print(json.dumps({"config": cfg, "world": world, "same_bits_all_ranks": same_bits, "repeatable": repeat,
                           "rel_diff_vs_nccl": d_nccl, "rel_diff_vs_single_gpu": d_full,
                           "h_ms_p2p": round(t_p2p, 4), "h_ms_nccl_incl_mirror": round(t_nccl, 4),
-                          "h_ms_accumulate_only": round(t_acc, 4),
+                          "h_ms_accumulate_only": round(t_acc, 4), "accumulate_ms_per_rank": acc_ranks,
+                          "grid_pass_h_vs_p2p": d_gp, "grid_pass_rho_sum_vs_single_gpu": d_rho,
                           "note": "H partials use atomics: not bitwise repeatable run to run (single GPU neither)",
-                          "ok": bool(same_bits and d_nccl <= 1e-14 and d_full <= 1e-13)}), flush=True)
+                          "ok": bool(same_bits and d_nccl <= 1e-14 and d_full <= 1e-13 and d_gp <= 1e-14
+                                     and d_rho == 0.0)}), flush=True)
     dist.destroy_process_group()
 
 
