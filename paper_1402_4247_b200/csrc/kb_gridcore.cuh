@@ -342,6 +342,9 @@ __device__ __forceinline__ void h_scatter(const Smem& sm, const double (&c)[TM][
 #ifndef KBG_H_NOSCALE
 #define KBG_H_NOSCALE 0
 #endif
+#ifndef KBG_H_UNIFORM
+#define KBG_H_UNIFORM 0
+#endif
 
 // One partner: C(8*TM x 8*TN) += Phi_rows diag(w) Phi_cj^T over the quads in
 // qm. Tiles with <= 2 DMMAs per quad alternate two accumulator sets.
@@ -376,6 +379,9 @@ __device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict_
 #pragma unroll
             for (int j = 0; j < TN; ++j) dmma(c[u][i][j], a[i], bb[j]);
     };
+#if KBG_H_UNIFORM
+    qm = __shfl_sync(0xffffffffu, qm, 0);  // provably warp-uniform branches
+#endif
     while (qm) {
         const int q0 = __ffs(qm) - 1;
         qm &= qm - 1;
@@ -420,6 +426,10 @@ __device__ __forceinline__ void h_tile2(const Smem& sm, const double* __restrict
     const double* pb2 = sm.phi() + rb2 * 64 + (lane & 3);
     const int sa = swz(ra), sb1 = swz(rb1), sb2 = swz(rb2);
     const double* pw = w + (lane & 3);
+#if KBG_H_UNIFORM
+    q1 = __shfl_sync(0xffffffffu, q1, 0);  // provably warp-uniform branches
+    q2 = __shfl_sync(0xffffffffu, q2, 0);
+#endif
     uint32_t qm = q1 | q2;
     while (qm) {
         const int q = __ffs(qm) - 1;
@@ -542,15 +552,19 @@ __device__ __forceinline__ void gather_a(const Smem& sm, int ncov, const int (&r
     }
 }
 
-// Order of one partner's DMMAs: 0 octet-major, branching over octets outside
-// the partner's overlap; 1 k-step-major, branching; 2 k-step-major over all
-// octets of the part (Phi is exactly 0 outside a cover's support, so the extra
-// products add exact zeros); 3 (default) k-step-major with the DMMAs of
-// octets outside the overlap predicated off. 2 and 3 keep 8 independent
-// accumulator chains in straight-line code: measured 0.433 ms (2, 3) vs
-// 0.437 (0) and 0.452 (1) for the 56-atom density pass.
+// Order of one partner's DMMAs: 0 (default) octet-major, branching over octets
+// outside the partner's overlap; 1 k-step-major, branching; 2 k-step-major over
+// all octets of the part (Phi is exactly 0 outside a cover's support, so the
+// extra products add exact zeros); 3 k-step-major with the DMMAs of octets
+// outside the overlap predicated off. With the octet mask made provably
+// warp-uniform (KBG_RHO_UNIFORM: a shuffle from lane 0), order 0 measures
+// 0.359 ms for the 56-atom density pass vs 0.370 (3), 0.372 (3 uniform),
+// 0.373 (0 without the shuffle) and 0.402 (2).
 #ifndef KBG_RHO_ORDER
-#define KBG_RHO_ORDER 3
+#define KBG_RHO_ORDER 0
+#endif
+#ifndef KBG_RHO_UNIFORM
+#define KBG_RHO_UNIFORM 1
 #endif
 template <int TM, int KS>
 __device__ __forceinline__ void rho_partner(const double* __restrict__ pb, int swb, uint32_t om4,
@@ -613,7 +627,12 @@ __device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, 
     const int colbase = 8 * kRhoOct * h + (lane >> 2);
     // one partner: D' fragments in `a` (K chunk 0); more chunks for > 16 orbitals
     auto process = [&](int cj, double (&a)[TM][4]) {
+#if KBG_RHO_UNIFORM
+        // provably warp-uniform (shuffle from lane 0): the octet branches need no WARPSYNC
+        const uint32_t om4 = __shfl_sync(0xffffffffu, (pom[cj] >> (kRhoOct * h)) & ((1u << kRhoOct) - 1u), 0);
+#else
         const uint32_t om4 = (pom[cj] >> (kRhoOct * h)) & ((1u << kRhoOct) - 1u);
+#endif
         const CoverS& B = sm.cov()[cj];
         const int nkc = (B.norb + 15) >> 4;
         for (int kc = 0; kc < nkc; ++kc) {
