@@ -342,9 +342,6 @@ __device__ __forceinline__ void h_scatter(const Smem& sm, const double (&c)[TM][
 #ifndef KBG_H_NOSCALE
 #define KBG_H_NOSCALE 0
 #endif
-#ifndef KBG_H_UNIFORM
-#define KBG_H_UNIFORM 0
-#endif
 
 // One partner: C(8*TM x 8*TN) += Phi_rows diag(w) Phi_cj^T over the quads in
 // qm. Tiles with <= 2 DMMAs per quad alternate two accumulator sets.
@@ -379,9 +376,6 @@ __device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict_
 #pragma unroll
             for (int j = 0; j < TN; ++j) dmma(c[u][i][j], a[i], bb[j]);
     };
-#if KBG_H_UNIFORM
-    qm = __shfl_sync(0xffffffffu, qm, 0);  // provably warp-uniform branches
-#endif
     while (qm) {
         const int q0 = __ffs(qm) - 1;
         qm &= qm - 1;
@@ -426,10 +420,6 @@ __device__ __forceinline__ void h_tile2(const Smem& sm, const double* __restrict
     const double* pb2 = sm.phi() + rb2 * 64 + (lane & 3);
     const int sa = swz(ra), sb1 = swz(rb1), sb2 = swz(rb2);
     const double* pw = w + (lane & 3);
-#if KBG_H_UNIFORM
-    q1 = __shfl_sync(0xffffffffu, q1, 0);  // provably warp-uniform branches
-    q2 = __shfl_sync(0xffffffffu, q2, 0);
-#endif
     uint32_t qm = q1 | q2;
     while (qm) {
         const int q = __ffs(qm) - 1;
