@@ -85,6 +85,9 @@ __global__ void k_dm_repack(SysParams P, int64_t npair, int nspin, int64_t nnz, 
     for (int s = 0; s < nspin; ++s) {
         const double* src = dm + s * nnz + poff[p];
         double* dst = dmr + s * nrep + proff[p];
+        // unrolled so several loads per lane are in flight (a pair block is only a few
+        // iterations; a rolled loop pays the full load latency each time)
+#pragma unroll 4
         for (int e = lane; e < na * stride; e += 32) {
             const int i = e / stride, pos = e % stride;
             const int c = pos >> 4, k = (pos >> 2) & 3, st = pos & 3;
@@ -110,6 +113,7 @@ __global__ void k_mirror(SysParams P, int64_t npair, int nspin, int64_t nnz, con
         // (a, a, 0): re-symmetrise (H + H^T)/2, like kband triple_product (linalg.cpp:120-128)
         for (int s = 0; s < nspin; ++s) {
             double* x = h + s * nnz + poff[p];
+#pragma unroll 4
             for (int e = lane; e < na * na; e += 32) {
                 const int i = e / na, j = e % na;
                 if (i < j) {
@@ -125,6 +129,7 @@ __global__ void k_mirror(SysParams P, int64_t npair, int nspin, int64_t nnz, con
     for (int s = 0; s < nspin; ++s) {
         const double* src = h + s * nnz + poff[q];  // nb x na
         double* dst = h + s * nnz + poff[p];        // na x nb
+#pragma unroll 4
         for (int e = lane; e < na * nb; e += 32) {
             const int i = e / nb, j = e % nb;
             dst[e] = src[j * na + i];
@@ -139,14 +144,15 @@ __global__ void k_dm_check(SysParams P, int64_t npair, int nspin, int64_t nnz, c
                            unsigned long long* out) {
     const int lane = threadIdx.x & 31;
     const int64_t p = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
-    if (p >= npair) return;
-    const int na = P.sp[P.spc[pa[p]]].norb, nb = P.sp[P.spc[pb[p]]].norb;
-    const int64_t q = mirror[p];
     double dmax = 0.0, amax = 0.0;
     bool finite = true;
-    for (int s = 0; s < nspin; ++s) {
+    const bool live = p < npair;
+    const int na = live ? P.sp[P.spc[pa[p]]].norb : 0, nb = live ? P.sp[P.spc[pb[p]]].norb : 0;
+    const int64_t q = live ? mirror[p] : 0;
+    for (int s = 0; s < nspin && live; ++s) {
         const double* x = dm + s * nnz + poff[p];
         const double* y = dm + s * nnz + poff[q];
+#pragma unroll 4
         for (int e = lane; e < na * nb; e += 32) {
             const int i = e / nb, j = e % nb;
             const double v = x[e];
@@ -161,10 +167,26 @@ __global__ void k_dm_check(SysParams P, int64_t npair, int nspin, int64_t nnz, c
         amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     }
     finite = __all_sync(0xffffffffu, finite);
+    // one atomic per CTA (not per warp: thousands of warps on the same two words serialize in L2)
+    __shared__ double s_d[32], s_a[32];
+    __shared__ int s_f;
+    if (threadIdx.x == 0) s_f = 1;
+    __syncthreads();
+    const int w = threadIdx.x >> 5;
     if (lane == 0) {
+        s_d[w] = dmax;
+        s_a[w] = amax;
+        if (!finite) s_f = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < static_cast<int>(blockDim.x >> 5); ++k) {
+            dmax = fmax(dmax, s_d[k]);
+            amax = fmax(amax, s_a[k]);
+        }
         atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(dmax)));
         atomicMax(out + 1, static_cast<unsigned long long>(__double_as_longlong(amax)));
-        if (!finite) atomicMax(out + 2, 1ull);
+        if (!s_f) atomicMax(out + 2, 1ull);
     }
 }
 
