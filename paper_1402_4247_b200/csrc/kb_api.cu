@@ -67,6 +67,7 @@ struct kbg_ctx {
     // fused H reduction over peer memory (kb_comm.cu)
     kbg::CommArgs comm;
     double* d_xbuf = nullptr;           // own exchange buffer [2][nnz] + flags + counter
+    unsigned char* d_pairtab = nullptr; // per-pair na, nb, canonical flag (fused copy-out + mirror)
     std::vector<void*> ipc_opened;      // peer buffers opened with cudaIpcOpenMemHandle
     int32_t* d_canon = nullptr;
     kbg::VeffPlan veff;  // kbg_veff (cuFFT plans)
@@ -1177,6 +1178,30 @@ int kbg_comm_open(kbg_ctx* c, const void* handles) {
             KBG_CUDA(cudaMemcpy(c->d_canon + e0.size(), e1.data(), e1.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
             KBG_CUDA(cudaMemcpy(c->d_canon + 2 * e0.size(), em.data(), em.size(), cudaMemcpyHostToDevice));
         }
+        // per-pair tables of the fused copy-out + mirror
+        {
+            const int64_t np = c->ix.npair;
+            std::vector<int32_t> na(np), nb(np);
+            std::vector<uint8_t> cf(np);
+            for (int64_t p = 0; p < np; ++p) {
+                const int a = h.pair_a[p], b = h.pair_b[p];
+                const int R0 = h.pair_R[3 * p], R1 = h.pair_R[3 * p + 1], R2 = h.pair_R[3 * p + 2];
+                na[p] = c->P.sp[c->h_spc[a]].norb;
+                nb[p] = c->P.sp[c->h_spc[b]].norb;
+                cf[p] = (a != b) ? a < b : (R0 != 0 ? R0 > 0 : (R1 != 0 ? R1 > 0 : R2 >= 0));
+            }
+            if (c->d_pairtab) cudaFree(c->d_pairtab);
+            c->d_pairtab = nullptr;
+            KBG_CUDA(cudaMalloc(&c->d_pairtab, std::max<size_t>(1, 9 * np)));
+            if (np) {
+                KBG_CUDA(cudaMemcpy(c->d_pairtab, na.data(), 4 * np, cudaMemcpyHostToDevice));
+                KBG_CUDA(cudaMemcpy(c->d_pairtab + 4 * np, nb.data(), 4 * np, cudaMemcpyHostToDevice));
+                KBG_CUDA(cudaMemcpy(c->d_pairtab + 8 * np, cf.data(), np, cudaMemcpyHostToDevice));
+            }
+            cm.pair_na = reinterpret_cast<const int32_t*>(c->d_pairtab);
+            cm.pair_nb = reinterpret_cast<const int32_t*>(c->d_pairtab + 4 * np);
+            cm.pair_canon = reinterpret_cast<const uint8_t*>(c->d_pairtab + 8 * np);
+        }
         cm.el0 = c->d_canon;
         cm.el1 = c->d_canon + e0.size();
         cm.elm = reinterpret_cast<const uint8_t*>(c->d_canon + 2 * e0.size());
@@ -1462,6 +1487,7 @@ void kbg_destroy(kbg_ctx* c) {
     for (void* q : c->ipc_opened) cudaIpcCloseMemHandle(q);
     if (c->d_xbuf) cudaFree(c->d_xbuf);
     if (c->d_canon) cudaFree(c->d_canon);
+    if (c->d_pairtab) cudaFree(c->d_pairtab);
     if (c->d_cpre) cudaFree(c->d_cpre);
     c->veff.release();
     if (c->d_in2) cudaFree(c->d_in2);

@@ -130,6 +130,40 @@ __global__ void __launch_bounds__(256) k_comm_copy_out(CommArgs c, int64_t n, do
     if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) out[n - 1] = c.x[c.rank][n - 1];
 }
 
+// Copy-out fused with the mirror: one warp per canonical pair block waits for
+// every peer's slice, copies the block from the exchange buffer into the
+// caller's H and writes its transpose into the mirror block H_ba(-R) (the
+// (a, a, 0) blocks arrive symmetrized from the reduce and are copied as is).
+// Replaces a full-array copy plus k_mirror (two kernels, two passes over H).
+__global__ void __launch_bounds__(256) k_comm_copy_mirror(CommArgs c, int64_t npair, int nspin, int64_t nnz,
+                                                          const int32_t* __restrict__ norb_a,
+                                                          const int32_t* __restrict__ norb_b,
+                                                          const int64_t* __restrict__ poff,
+                                                          const int32_t* __restrict__ mirror,
+                                                          const uint8_t* __restrict__ canon, double* __restrict__ out,
+                                                          unsigned long long epoch) {
+    wait_flags(c, epoch);
+    const int lane = threadIdx.x & 31;
+    const double* x = c.x[c.rank];
+    for (int64_t p = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; p < npair;
+         p += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+        if (!canon[p]) continue;  // written by its canonical partner
+        const int na = norb_a[p], nb = norb_b[p];
+        const int64_t q = mirror[p];
+        for (int s = 0; s < nspin; ++s) {
+            const double* src = x + s * nnz + poff[p];
+            double* dst = out + s * nnz + poff[p];
+            double* dq = out + s * nnz + poff[q];
+#pragma unroll 4
+            for (int e = lane; e < na * nb; e += 32) {
+                const double v = src[e];
+                dst[e] = v;
+                if (q != p) dq[(e % nb) * na + e / nb] = v;
+            }
+        }
+    }
+}
+
 }  // namespace
 
 int launch_reduce_mirror(const CommArgs& c, const DevIndex& ix, const SysParams& sys, int nspin, double* d_out,
@@ -141,6 +175,13 @@ int launch_reduce_mirror(const CommArgs& c, const DevIndex& ix, const SysParams&
     const unsigned grid = static_cast<unsigned>(sms) * 2;
     k_reduce_mirror<<<grid, 256, 0, st>>>(c, nspin, ix.nnz, c.ne, c.el0, c.el1, epoch);
     KBG_CUDA(cudaGetLastError());
+    if (c.pair_na) {
+        k_comm_copy_mirror<<<static_cast<unsigned>(sms) * 4, 256, 0, st>>>(c, ix.npair, nspin, ix.nnz, c.pair_na,
+                                                                          c.pair_nb, ix.pair_off, ix.pair_mirror,
+                                                                          c.pair_canon, d_out, epoch + 1);
+        KBG_CUDA(cudaGetLastError());
+        return 2;
+    }
     const int64_t n = static_cast<int64_t>(nspin) * ix.nnz;
     k_comm_copy_out<<<static_cast<unsigned>(sms) * 4, 256, 0, st>>>(c, n, d_out, epoch + 1);
     KBG_CUDA(cudaGetLastError());

@@ -245,6 +245,10 @@ struct CommArgs {
     const int32_t* el1 = nullptr;
     const uint8_t* elm = nullptr;  // ranks whose partial of the entry can be nonzero (bit k: rank k)
     int64_t ne = 0;
+    // per pair: orbital counts and canonical flag (fused copy-out + mirror)
+    const int32_t* pair_na = nullptr;
+    const int32_t* pair_nb = nullptr;
+    const uint8_t* pair_canon = nullptr;
 };
 // Per pair, the ranks (bit k) whose block range [bounds[k], bounds[k + 1]) holds
 // a canonical (block, cover pair) work item of that pair.
