@@ -213,6 +213,9 @@ int kbg_last_tally(const kbg_ctx* ctx, kbg_tally* out);
  * first (load balance of the tail); 1 natural (i, j, k) block order (neighbouring blocks in flight share
  * their atom pairs' DM / H entries in L1/L2). */
 #define KBG_OPT_BLOCK_ORDER 7
+/* Exchange-correlation of kbg_veff: 0 (default) Slater exchange only; 1 LSDA = exchange + Perdew-Wang 1992
+ * correlation (energy[1] is then E_xc). */
+#define KBG_OPT_XC 8
 int kbg_set_option(kbg_ctx* ctx, int option, int64_t value);
 
 const char* kbg_last_error(const kbg_ctx* ctx);
@@ -226,8 +229,8 @@ void kbg_destroy(kbg_ctx* ctx);
  * background; cuFFT) and exchange-only local spin density (Slater) V_x,s =
  * -(6 rho_s/pi)^(1/3) (nspin 1: rho_s = rho/2). Hartree atomic units; grids
  * [nspin][npts] C-order as the density pass writes them; vloc [npts] may be
- * NULL; energy (may be NULL) receives E_H = 1/2 int V_H rho, E_x. Does not
- * need the index. */
+ * NULL; energy (may be NULL) receives E_H = 1/2 int V_H rho, E_x (E_xc with
+ * KBG_OPT_XC = 1: + PW92 correlation). Does not need the index. */
 int kbg_veff(kbg_ctx* ctx, int nspin, const double* rho, const double* vloc, double* veff, double* energy);
 int kbg_veff_dev(kbg_ctx* ctx, int nspin, const double* d_rho, const double* d_vloc, double* d_veff,
                  double* d_energy, void* stream);

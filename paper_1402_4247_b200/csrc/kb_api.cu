@@ -31,6 +31,7 @@ struct kbg_ctx {
     int persist = 1;           // option: use the persistent kernels when they fit
     int schedule = 3;          // KBG_OPT_SCHEDULE
     int block_order = 0;       // KBG_OPT_BLOCK_ORDER
+    int xc = 0;                // KBG_OPT_XC
     int plan_schedule = -1;    // schedule / rho split the task lists were built with (kbg_plan_info)
     int plan_split = 0;
     double* d_dmr = nullptr;   // repacked DM scratch
@@ -682,7 +683,8 @@ int kbg_veff_dev(kbg_ctx* c, int nspin, const double* d_rho, const double* d_vlo
     return guard(c, [&] {
         check_nspin(nspin);
         KBG_CUDA(cudaSetDevice(c->device));
-        c->last_launches = kbg::run_veff(c->veff, c->P.N, c->P.Ainv, nspin, d_rho, d_vloc, cell_dV(c), d_veff, d_energy,
+        c->last_launches = kbg::run_veff(c->veff, c->P.N, c->P.Ainv, nspin, c->xc, d_rho, d_vloc, cell_dV(c), d_veff,
+                                         d_energy,
                                          static_cast<cudaStream_t>(stream));
         c->tally.flops = 0.0;
         c->tally.bytes = 8.0 * c->npts * (2.0 * nspin + (d_vloc ? 1.0 : 0.0));
@@ -705,7 +707,7 @@ int kbg_veff(kbg_ctx* c, int nspin, const double* rho, const double* vloc, doubl
         KBG_CUDA(cudaMemcpyAsync(d_rho, rho, n * nspin * sizeof(double), cudaMemcpyHostToDevice, c->stream));
         if (vloc) KBG_CUDA(cudaMemcpyAsync(d_vloc, vloc, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
         c->last_launches =
-            kbg::run_veff(c->veff, c->P.N, c->P.Ainv, nspin, d_rho, d_vloc, cell_dV(c), d_v, d_e, c->stream);
+            kbg::run_veff(c->veff, c->P.N, c->P.Ainv, nspin, c->xc, d_rho, d_vloc, cell_dV(c), d_v, d_e, c->stream);
         KBG_CUDA(cudaMemcpyAsync(veff, d_v, n * nspin * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         double e[2];
         KBG_CUDA(cudaMemcpyAsync(e, d_e, sizeof(e), cudaMemcpyDeviceToHost, c->stream));
@@ -1446,6 +1448,13 @@ int kbg_set_option(kbg_ctx* c, int option, int64_t value) {
             return KBG_OK;
         case KBG_OPT_PERSIST:
             c->persist = value ? 1 : 0;
+            return KBG_OK;
+        case KBG_OPT_XC:
+            if (value < 0 || value > 1) {
+                c->err = "set_option: xc must be 0 (exchange only) or 1 (LSDA, PW92 correlation)";
+                return KBG_ERR_CONFIG;
+            }
+            c->xc = static_cast<int>(value);
             return KBG_OK;
         case KBG_OPT_BLOCK_ORDER:
             if (value < 0 || value > 1) {

@@ -229,8 +229,8 @@ struct VeffPlan {
     double* B = nullptr;   // reciprocal basis rows (device)
     void release();
 };
-int run_veff(VeffPlan& vp, const int N[3], const double Ainv[9], int nspin, const double* d_rho, const double* d_vloc,
-             double dV, double* d_veff, double* d_energy, cudaStream_t st);
+int run_veff(VeffPlan& vp, const int N[3], const double Ainv[9], int nspin, int xc, const double* d_rho,
+             const double* d_vloc, double dV, double* d_veff, double* d_energy, cudaStream_t st);
 
 // Fused H reduction + mirror over peer memory (kb_comm.cu).
 constexpr int kMaxRanks = 8;

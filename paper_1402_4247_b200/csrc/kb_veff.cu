@@ -2,8 +2,9 @@
 // pass (G3) and the Hamiltonian pass (G4) of one SCF iteration.
 //   V_H:  Poisson in G space, V_H(G) = 4 pi rho(G) / |G|^2, V_H(G = 0) = 0
 //         (neutralizing background); cuFFT D2Z / Z2D (library FFTs).
-//   V_x:  exchange-only local spin density (Slater), V_x,s = -(6 rho_s / pi)^(1/3)
+//   V_x:  local spin density exchange (Slater), V_x,s = -(6 rho_s / pi)^(1/3)
 //         (nspin = 1: rho_s = rho / 2, i.e. -(3 rho / pi)^(1/3)).
+//   V_c:  with KBG_OPT_XC = 1, the Perdew-Wang 1992 LSDA correlation (full LDA).
 //   V_eff,s = V_H + V_x,s + V_loc (V_loc optional).
 // Energies: E_H = 1/2 sum V_H rho dV, E_x = -3/4 (6/pi)^(1/3) sum_s sum rho_s^(4/3) dV,
 // reduced in a fixed order (two passes) -> deterministic.
@@ -51,57 +52,110 @@ __global__ void k_poisson(int N0, int N1, int N2, const double* __restrict__ B, 
     }
 }
 
-// V_eff,s = V_H + V_x,s (+ V_loc); per-block partial energies (fixed order).
+// Perdew-Wang 1992 LSDA correlation (Phys. Rev. B 45, 13244; Table I, p = 1,
+// Hartree): G(rs) and dG/drs for eps_c(rs, 0), eps_c(rs, 1) and -alpha_c(rs).
+__device__ __forceinline__ void pw92_g(double rs, double sr, double A, double a1, double b1, double b2, double b3,
+                                       double b4, double& g, double& dg) {
+    const double q0 = -2.0 * A * (1.0 + a1 * rs);
+    const double q1 = 2.0 * A * (b1 * sr + b2 * rs + b3 * rs * sr + b4 * rs * rs);
+    const double q1p = A * (b1 / sr + 2.0 * b2 + 3.0 * b3 * sr + 4.0 * b4 * rs);
+    const double lg = log1p(1.0 / q1);
+    g = q0 * lg;
+    dg = -2.0 * A * a1 * lg - q0 * q1p / (q1 * q1 + q1);
+}
+
+// eps_c and v_c,up / v_c,down at total density n > 0, polarization zeta.
+__device__ void pw92(double n, double zeta, double& eps, double& vu, double& vd) {
+    zeta = fmin(1.0, fmax(-1.0, zeta));
+    const double rs = cbrt(3.0 / (4.0 * kPi * n)), sr = sqrt(rs);
+    double e0, d0, e1, d1, ma, dma;
+    pw92_g(rs, sr, 0.031091, 0.21370, 7.5957, 3.5876, 1.6382, 0.49294, e0, d0);
+    pw92_g(rs, sr, 0.015545, 0.20548, 14.1189, 6.1977, 3.3662, 0.62517, e1, d1);
+    pw92_g(rs, sr, 0.016887, 0.11125, 10.357, 3.6231, 0.88026, 0.49671, ma, dma);
+    const double ac = -ma, dac = -dma, fz0 = 1.709921;
+    const double c43 = 0.5198420997897464;  // 2^(4/3) - 2
+    const double cp = cbrt(1.0 + zeta), cm = cbrt(1.0 - zeta);
+    const double f = ((1.0 + zeta) * cp + (1.0 - zeta) * cm - 2.0) / c43;
+    const double fp = (4.0 / 3.0) * (cp - cm) / c43;
+    const double z3 = zeta * zeta * zeta, z4 = z3 * zeta;
+    eps = e0 + ac * f / fz0 * (1.0 - z4) + (e1 - e0) * f * z4;
+    const double de_rs = d0 + dac * f / fz0 * (1.0 - z4) + (d1 - d0) * f * z4;
+    const double de_z = ac / fz0 * (fp * (1.0 - z4) - 4.0 * z3 * f) + (e1 - e0) * (fp * z4 + 4.0 * z3 * f);
+    const double common = eps - rs / 3.0 * de_rs - zeta * de_z;
+    vu = common + de_z;
+    vd = common - de_z;
+}
+
+// V_eff,s = V_H + V_x,s [+ V_c,s (xc = 1)] (+ V_loc); per-block partial energies (fixed order):
+// part[0] sum V_H rho, part[1] sum_s rho_s^(4/3) (exchange), part[2] sum n eps_c.
+template <int XC>
 __global__ void __launch_bounds__(256) k_veff(int64_t n, int nspin, const double* __restrict__ rho,
                                               const double* __restrict__ vh, const double* __restrict__ vloc,
                                               double* __restrict__ veff, double* __restrict__ part) {
     const double cx = -cbrt(6.0 / kPi);  // V_x,s = cx rho_s^(1/3)
-    double eh = 0.0, ex = 0.0;
+    double eh = 0.0, ex = 0.0, ec = 0.0;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const double h = vh[i];
         const double vl = vloc ? vloc[i] : 0.0;
-        double rt = 0.0;
+        double rt = 0.0, sp[2] = {0.0, 0.0};
         for (int s = 0; s < nspin; ++s) {
             const double rs = nspin == 2 ? fmax(rho[s * n + i], 0.0) : 0.5 * fmax(rho[i], 0.0);
             const double c = cbrt(rs);
+            sp[s] = rs;
             veff[s * n + i] = h + cx * c + vl;
             ex += (nspin == 2 ? 1.0 : 2.0) * rs * c;
             rt += nspin == 2 ? rho[s * n + i] : rho[i];
         }
+        if (XC == 1) {
+            const double up = sp[0], dn = nspin == 2 ? sp[1] : sp[0], nt = up + dn;
+            if (nt > 1e-30) {
+                double eps, vu, vd;
+                pw92(nt, (up - dn) / nt, eps, vu, vd);
+                veff[i] += vu;
+                if (nspin == 2) veff[n + i] += vd;
+                ec += nt * eps;
+            }
+        }
         eh += h * rt;
     }
-    __shared__ double sh[2][8];
+    __shared__ double sh[3][8];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         eh += __shfl_xor_sync(0xffffffffu, eh, o);
         ex += __shfl_xor_sync(0xffffffffu, ex, o);
+        ec += __shfl_xor_sync(0xffffffffu, ec, o);
     }
     if ((threadIdx.x & 31) == 0) {
         sh[0][threadIdx.x >> 5] = eh;
         sh[1][threadIdx.x >> 5] = ex;
+        sh[2][threadIdx.x >> 5] = ec;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        double a = 0.0, b = 0.0;
+        double a = 0.0, b = 0.0, c = 0.0;
         for (int w = 0; w < 8; ++w) {
             a += sh[0][w];
             b += sh[1][w];
+            c += sh[2][w];
         }
-        part[2 * blockIdx.x] = a;
-        part[2 * blockIdx.x + 1] = b;
+        part[3 * blockIdx.x] = a;
+        part[3 * blockIdx.x + 1] = b;
+        part[3 * blockIdx.x + 2] = c;
     }
 }
 
+// e[0] = E_H, e[1] = E_xc (exchange, plus PW92 correlation when xc = 1)
 __global__ void k_energy_final(int nblk, const double* __restrict__ part, double dV, double* __restrict__ e) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    double a = 0.0, b = 0.0;
+    double a = 0.0, b = 0.0, c = 0.0;
     for (int i = 0; i < nblk; ++i) {
-        a += part[2 * i];
-        b += part[2 * i + 1];
+        a += part[3 * i];
+        b += part[3 * i + 1];
+        c += part[3 * i + 2];
     }
     e[0] = 0.5 * a * dV;
-    e[1] = -0.75 * cbrt(6.0 / kPi) * b * dV;
+    e[1] = -0.75 * cbrt(6.0 / kPi) * b * dV + c * dV;
 }
 
 void cufft_check(cufftResult r, const char* what) {
@@ -120,8 +174,8 @@ void VeffPlan::release() {
     *this = VeffPlan();
 }
 
-int run_veff(VeffPlan& vp, const int N[3], const double Ainv[9], int nspin, const double* d_rho, const double* d_vloc,
-             double dV, double* d_veff, double* d_energy, cudaStream_t st) {
+int run_veff(VeffPlan& vp, const int N[3], const double Ainv[9], int nspin, int xc, const double* d_rho,
+             const double* d_vloc, double dV, double* d_veff, double* d_energy, cudaStream_t st) {
     const int64_t n = static_cast<int64_t>(N[0]) * N[1] * N[2];
     const int64_t nc = static_cast<int64_t>(N[0]) * N[1] * (N[2] / 2 + 1);
     const int64_t nr = (n + 1) & ~int64_t(1);  // complex spectrum 16-byte aligned
@@ -133,7 +187,7 @@ int run_veff(VeffPlan& vp, const int N[3], const double Ainv[9], int nspin, cons
         vp.fwd = static_cast<int>(f);
         vp.inv = static_cast<int>(i);
         // work: real grid (rho_tot, then V_H) | complex half spectrum | energy partials
-        KBG_CUDA(cudaMalloc(&vp.work, (nr + 2 * nc + 2 * sms_grid) * sizeof(double)));
+        KBG_CUDA(cudaMalloc(&vp.work, (nr + 2 * nc + 3 * sms_grid) * sizeof(double)));
         // reciprocal basis b_i = rows of A^-T: (A^-1)^T rows = columns of A^-1
         double Bh[9];
         for (int r = 0; r < 3; ++r)
@@ -151,7 +205,10 @@ int run_veff(VeffPlan& vp, const int N[3], const double Ainv[9], int nspin, cons
     cufft_check(cufftExecD2Z(static_cast<cufftHandle>(vp.fwd), real, spec), "cufftExecD2Z");
     k_poisson<<<sms_grid, 256, 0, st>>>(N[0], N[1], N[2], vp.B, spec);
     cufft_check(cufftExecZ2D(static_cast<cufftHandle>(vp.inv), spec, real), "cufftExecZ2D");
-    k_veff<<<sms_grid, 256, 0, st>>>(n, nspin, d_rho, real, d_vloc, d_veff, part);
+    if (xc == 1)
+        k_veff<1><<<sms_grid, 256, 0, st>>>(n, nspin, d_rho, real, d_vloc, d_veff, part);
+    else
+        k_veff<0><<<sms_grid, 256, 0, st>>>(n, nspin, d_rho, real, d_vloc, d_veff, part);
     if (d_energy) k_energy_final<<<1, 32, 0, st>>>(sms_grid, part, dV, d_energy);
     KBG_CUDA(cudaGetLastError());
     return 4 + (d_energy ? 1 : 0);

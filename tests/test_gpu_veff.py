@@ -51,3 +51,22 @@ def test_plane_wave_hartree_on_the_cell(setup):
     v, _ = gp.veff(test)
     vx = -(3 * test[0] / np.pi) ** (1 / 3)
     assert np.abs(v[0] - vx - 4 * np.pi * 0.01 * cosg / (G @ G)).max() <= 1e-12
+
+
+@pytest.mark.parametrize("nspin", [1, 2])
+def test_lda_pw92_parity(setup, nspin):
+    """KBG_OPT_XC = 1: exchange + Perdew-Wang 1992 correlation, nspin 1 and 2 (polarized split)."""
+    from paper_1402_4247_b200 import _abi
+
+    f, gp, rho, lat, N = setup
+    r = np.abs(rho) if nspin == 1 else np.concatenate([0.7 * np.abs(rho), 0.3 * np.abs(rho)])
+    gp.set_option(_abi.KBG_OPT_XC, 1)
+    try:
+        v, e = gp.veff(r)
+    finally:
+        gp.set_option(_abi.KBG_OPT_XC, 0)
+    rv, re = V.veff(r, lat, N, xc=1)
+    assert np.abs(v - rv).max() <= 1e-12 * np.abs(rv).max()
+    assert abs(e[1] - re[1]) <= 1e-12 * abs(re[1])
+    vx, ex = V.veff(r, lat, N)  # correlation lowers V and E_xc
+    assert (v <= vx + 1e-15).all() and e[1] < ex[1]

@@ -40,3 +40,40 @@ def test_spin_split_equals_unpolarized():
     v2, e2 = V.veff(np.concatenate([rho / 2, rho / 2]), LAT, N)
     assert np.abs(v2[0] - v1[0]).max() <= 1e-14 and np.abs(v2[1] - v1[0]).max() <= 1e-14
     assert np.allclose(e1, e2, rtol=1e-13)
+
+
+def test_pw92_published_value():
+    """PW92 paramagnetic correlation at rs = 1 and 2 (Hartree): -0.0598 and -0.0448."""
+    for rs, ref in ((1.0, -0.0598), (2.0, -0.0448)):
+        n = 3.0 / (4.0 * np.pi * rs ** 3)
+        eps, vu, vd = V.pw92(n, 0.0)
+        assert abs(eps - ref) <= 5e-4, (rs, eps)
+        assert vu == vd
+
+
+@pytest.mark.parametrize("zeta", [0.0, 0.3, -0.7, 1.0])
+def test_pw92_potential_is_the_derivative(zeta):
+    """v_c,s = d(n eps_c)/d rho_s, central finite differences in rho_up and rho_down."""
+    n = 0.037
+    up, dn = n * (1 + zeta) / 2, n * (1 - zeta) / 2
+
+    def energy(u, d):
+        t = u + d
+        return t * V.pw92(t, (u - d) / t)[0]
+
+    _, vu, vd = V.pw92(n, zeta)
+    h = 1e-6 * n
+    fu = (energy(up + h, dn) - energy(up - h, dn)) / (2 * h)
+    assert abs(fu - vu) <= 1e-7 * abs(vu)
+    if zeta < 1.0:
+        fd = (energy(up, dn + h) - energy(up, dn - h)) / (2 * h)
+        assert abs(fd - vd) <= 1e-7 * abs(vd)
+
+
+def test_lda_spin_split_equals_unpolarized():
+    rng = np.random.default_rng(5)
+    rho = rng.uniform(0.0, 0.1, (1, int(np.prod(N))))
+    v1, e1 = V.veff(rho, LAT, N, xc=1)
+    v2, e2 = V.veff(np.concatenate([rho / 2, rho / 2]), LAT, N, xc=1)
+    assert np.abs(v2[0] - v1[0]).max() <= 1e-13 and np.abs(v2[1] - v1[0]).max() <= 1e-13
+    assert np.allclose(e1, e2, rtol=1e-13)

@@ -20,6 +20,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from oracle import veff as V  # noqa: E402  (host reference leg, timed)
+from paper_1402_4247_b200 import _abi  # noqa: E402
 from paper_1402_4247_b200.grid import GridPass  # noqa: E402
 from paper_1402_4247_b200.system import Fe3O4  # noqa: E402
 
@@ -42,6 +43,7 @@ def ev_time(fn, st, flush, reps=10):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="cubic56_200Ry,super448_200Ry,super1512_200Ry")
+    ap.add_argument("--xc", type=int, default=0, help="KBG_OPT_XC: 0 exchange only, 1 LSDA (PW92)")
     a = ap.parse_args()
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
     dev = torch.device("cuda", 0)
@@ -50,6 +52,7 @@ def main():
     for cfg in a.configs.split(","):
         f = Fe3O4.config(cfg)
         gp = GridPass(f.system)
+        gp.set_option(_abi.KBG_OPT_XC, a.xc)
         n = f.system.npts
         rng = np.random.default_rng(1402)
         rho_h = rng.uniform(0.0, 0.2, (1, n))
@@ -61,9 +64,9 @@ def main():
         ms = ev_time(lambda: gp.veff_dev(rho, out, vloc, en, st), st, flush)
         nbytes = 8 * n * (3 + 4)
         t0 = time.perf_counter()
-        V.veff(rho_h, f.system.lattice, tuple(f.system.grid), vloc_h)
+        V.veff(rho_h, f.system.lattice, tuple(f.system.grid), vloc_h, xc=a.xc)
         host_ms = (time.perf_counter() - t0) * 1e3
-        rec = {"config": cfg, "grid": list(f.system.grid), "npts": n, "veff_ms": round(ms, 4),
+        rec = {"config": cfg, "xc": ["exchange", "lsda_pw92"][a.xc], "grid": list(f.system.grid), "npts": n, "veff_ms": round(ms, 4),
                "bytes_compulsory_plus_fft": nbytes, "achieved_gbs": round(nbytes / (ms * 1e-3) / 1e9, 1),
                "hbm_frac": round(nbytes / (ms * 1e-3) / 1e9 / peak, 3), "numpy_host_ms": round(host_ms, 1)}
         if cfg == "cubic56_200Ry":
