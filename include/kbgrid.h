@@ -344,6 +344,22 @@ int kbg_hh_normalize_columns_dev(int64_t n, int64_t m, double* d_c, void* stream
  * for T [n][m], H [n][n] Hermitian, re-symmetrized and validated Hermitian
  * (defect <= 1e-13 max(1, ||C||_F)). Two ZGEMMs (cuBLAS: plain library GEMMs). */
 int kbg_hh_triple_product(int64_t n, int64_t m, const double* t, const double* h, double* c);
+/* The tridiagonal eigensolve between tridiagonalize and back_transform
+ * (kband::solve_tridiag, tridiag.hpp:18-21: implicit QL on the host in the
+ * reference, LAPACK on the CPUs in the paper) on the GPU: multisection on
+ * kband's Sturm count for the eigenvalues (ascending into w [n]), inverse
+ * iteration with re-orthogonalization inside clusters (gaps < 1e-3 ||T||_1)
+ * for the eigenvectors (columns of z [n][n], row-major; want_vectors = 0 leaves
+ * z untouched). d [n], e [n-1]. n <= 12000. */
+int kbg_tridiag_solve(int64_t n, const double* d, const double* e, int want_vectors, double* w, double* z);
+int kbg_tridiag_solve_dev(int64_t n, const double* d_d, const double* d_e, int want_vectors, double* d_w, double* d_z,
+                          void* stream);
+/* kband::eigen_hh (householder.hpp:78-80) on the device end to end: a [n][n]
+ * Hermitian (defect <= 1e-13) -> eigenvalues ascending w [n] and, if
+ * want_vectors, normalized eigenvectors as the columns of c [n][n] complex;
+ * tridiagonalize, kbg_tridiag_solve, back_transform and normalize_columns with
+ * the data resident on the GPU (only a in and w, c out cross PCIe). n <= 4800. */
+int kbg_hh_eigen(int64_t n, const double* a, int want_vectors, double* w, double* c);
 const char* kbg_hh_last_error(void);
 
 /* Library identification: "kbgrid <version> sm_100a". */

@@ -142,6 +142,9 @@ KBGRID_SYMBOLS = [
     ("kbg_hh_normalize_columns", _I, [_I64, _I64, _DP]),
     ("kbg_hh_normalize_columns_dev", _I, [_I64, _I64, _P, _P]),
     ("kbg_hh_triple_product", _I, [_I64, _I64, _DP, _DP, _DP]),
+    ("kbg_hh_eigen", _I, [_I64, _DP, _I, _DP, _DP]),
+    ("kbg_tridiag_solve", _I, [_I64, _DP, _DP, _I, _DP, _DP]),
+    ("kbg_tridiag_solve_dev", _I, [_I64, C.c_void_p, C.c_void_p, _I, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("kbg_hh_last_error", C.c_char_p, []),
 ]
 

@@ -1424,6 +1424,74 @@ int kbg_hh_normalize_columns(int64_t n, int64_t m, double* c) {
     });
 }
 
+// kband::eigen_hh (householder.cpp:333-351) device-resident end to end: Hermitian check,
+// tridiagonalize, tridiagonal solve, back transform, column normalization; only A in and
+// (w, C) out cross PCIe.
+int kbg_hh_eigen(int64_t n, const double* a, int want_vectors, double* w, double* c) {
+    if (!a || !w || (want_vectors && !c)) return KBG_ERR_CONFIG;
+    return hh_guard([&] {
+        hh_check_n(n);
+        const cudaStream_t st = nullptr;
+        const size_t nn = static_cast<size_t>(n) * n, nr = static_cast<size_t>(n - 1);
+        DevBuf A(2 * nn, st), D(n, st), E(std::max<size_t>(1, nr), st), U(2 * std::max<size_t>(1, nr) * n, st),
+            H(std::max<size_t>(1, nr), st), S(std::max<size_t>(1, nr), st), P(2 * std::max<size_t>(1, nr), st),
+            W(n, st), Y(want_vectors ? nn : 1, st), scr(kbg::tridiag_scratch_doubles(static_cast<int>(n), want_vectors != 0), st);
+        KBG_CUDA(cudaMemcpyAsync(A.p, a, 2 * nn * sizeof(double), cudaMemcpyHostToDevice, st));
+        hermitian_from(n, A.p, st);
+        tridiag_dev(n, A.p, 0, D.p, E.p, U.p, H.p, S.p, P.p, st);
+        kbg::launch_tridiag_solve(static_cast<int>(n), D.p, n > 1 ? E.p : D.p, want_vectors != 0, W.p, Y.p, scr.p, st);
+        KBG_CUDA(cudaMemcpyAsync(w, W.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        if (want_vectors) {
+            double* C = A.p;  // the working matrix is free again
+            if (n == 1) {
+                const double one[2] = {1.0, 0.0};
+                KBG_CUDA(cudaMemcpyAsync(C, one, sizeof(one), cudaMemcpyHostToDevice, st));
+            } else {
+                DevBuf dph(2 * n, st);
+                kbg::launch_hh_back_transform(static_cast<int>(n), static_cast<int>(n), Y.p, U.p, H.p, P.p, dph.p, C,
+                                              st);
+            }
+            const int stn = kbg_hh_normalize_columns_dev(n, n, C, st);
+            if (stn != KBG_OK) throw Error(stn, g_hh_err);
+            KBG_CUDA(cudaMemcpyAsync(c, C, 2 * nn * sizeof(double), cudaMemcpyDeviceToHost, st));
+        }
+        KBG_CUDA(cudaStreamSynchronize(st));
+        for (int64_t i = 0; i < n; ++i)
+            if (!std::isfinite(w[i])) throw Error(KBG_ERR_NONFINITE, "eigen_hh: non-finite eigenvalue " + std::to_string(i));
+    });
+}
+
+int kbg_tridiag_solve_dev(int64_t n, const double* d_d, const double* d_e, int want_vectors, double* d_w,
+                          double* d_z, void* stream) {
+    if (!d_d || !d_w || (n > 1 && !d_e) || (want_vectors && !d_z)) return KBG_ERR_CONFIG;
+    return hh_guard([&] {
+        if (n < 1) throw Error(KBG_ERR_DIMENSION, "solve_tridiag: empty problem");
+        if (n > 12000) throw Error(KBG_ERR_DIMENSION, "solve_tridiag: n = " + std::to_string(n) + " > 12000");
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        DevBuf scr(kbg::tridiag_scratch_doubles(static_cast<int>(n), want_vectors != 0), st);
+        kbg::launch_tridiag_solve(static_cast<int>(n), d_d, n > 1 ? d_e : d_d, want_vectors != 0, d_w, d_z, scr.p,
+                                  st);
+    });
+}
+
+int kbg_tridiag_solve(int64_t n, const double* d, const double* e, int want_vectors, double* w, double* z) {
+    if (!d || !w || (n > 1 && !e) || (want_vectors && !z)) return KBG_ERR_CONFIG;
+    return hh_guard([&] {
+        if (n < 1) throw Error(KBG_ERR_DIMENSION, "solve_tridiag: empty problem");
+        for (int64_t i = 0; i < n; ++i)
+            if (!std::isfinite(d[i]) || (i + 1 < n && !std::isfinite(e[i])))
+                throw Error(KBG_ERR_NONFINITE, "solve_tridiag: non-finite entry at index " + std::to_string(i));
+        DevBuf D(n, nullptr), E(std::max<int64_t>(1, n - 1), nullptr), W(n, nullptr),
+            Z(want_vectors ? n * n : 1, nullptr);
+        KBG_CUDA(cudaMemcpyAsync(D.p, d, n * sizeof(double), cudaMemcpyHostToDevice, nullptr));
+        if (n > 1) KBG_CUDA(cudaMemcpyAsync(E.p, e, (n - 1) * sizeof(double), cudaMemcpyHostToDevice, nullptr));
+        const int st = kbg_tridiag_solve_dev(n, D.p, E.p, want_vectors, W.p, Z.p, nullptr);
+        if (st != KBG_OK) throw Error(st, g_hh_err);
+        KBG_CUDA(cudaMemcpy(w, W.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+        if (want_vectors) KBG_CUDA(cudaMemcpy(z, Z.p, n * n * sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+
 int kbg_last_tally(const kbg_ctx* c, kbg_tally* out) {
     if (!c || !out) return KBG_ERR_CONFIG;
     *out = c->tally;

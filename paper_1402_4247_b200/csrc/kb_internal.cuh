@@ -258,6 +258,11 @@ int launch_reduce_mirror(const CommArgs& c, const DevIndex& ix, const SysParams&
 
 // Eigen_HH (kb_eigen.cu). Complex arrays interleaved.
 size_t hh_tridiag_smem(int n);
+// Tridiagonal eigensolver (kb_tridiag.cu): eigenvalues ascending into d_w, eigenvectors as the
+// columns of d_z [n][n]; d_scr holds tridiag_scratch_doubles(n, vectors).
+size_t tridiag_scratch_doubles(int n, bool vectors);
+int launch_tridiag_solve(int n, const double* d_d, const double* d_e, bool vectors, double* d_w, double* d_z,
+                         double* d_scr, cudaStream_t st);
 int launch_hermitian_repair(int n, double* d_A, unsigned long long* d_defect, bool apply, cudaStream_t st);
 int launch_hh_tridiagonalize(int n, double* d_B, double* d_p, double* d, double* e, double* u, double* h, double* s,
                              double* ph, double sign, cudaStream_t st);

@@ -113,9 +113,37 @@ def lapack_solve_tridiag(d: np.ndarray, e: np.ndarray, want_vectors: bool):
     return eigh_tridiagonal(d, e, eigvals_only=True, lapack_driver="stemr"), None
 
 
-def eigen_hh(a: np.ndarray, want_vectors: bool = True, solve_tridiag=lapack_solve_tridiag):
-    """kband::eigen_hh (householder.cpp:333-351): GPU tridiagonalize -> host tridiagonal solve ->
+def gpu_solve_tridiag(d: np.ndarray, e: np.ndarray, want_vectors: bool):
+    """kband::solve_tridiag on the GPU (kbg_tridiag_solve: Sturm multisection + inverse iteration):
+    (eigenvalues ascending, eigenvectors as columns or None)."""
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    e = np.ascontiguousarray(e, dtype=np.float64)
+    n = len(d)
+    if len(e) + 1 != n:
+        raise DimensionError("solve_tridiag: off-diagonal length must be n-1")
+    w = np.empty(n)
+    z = np.empty((n, n)) if want_vectors else None
+    ee = e if n > 1 else np.zeros(1)
+    _check(_lib().kbg_tridiag_solve(n, _abi.dptr(d), _abi.dptr(ee), int(want_vectors), _abi.dptr(w),
+                                    _abi.dptr(z) if want_vectors else None), "kbg_tridiag_solve")
+    return w, z
+
+
+def eigen_hh(a: np.ndarray, want_vectors: bool = True, solve_tridiag=None):
+    """kband::eigen_hh (householder.cpp:333-351). Default: the whole pipeline on the GPU, device-resident
+    (kbg_hh_eigen: tridiagonalize -> GPU tridiagonal solve -> back transform -> normalization). With a host
+    `solve_tridiag` (e.g. lapack_solve_tridiag, the paper's CPU step): GPU tridiagonalize -> that solver ->
     GPU back transform + normalization. Returns (eigenvalues ascending, eigenvectors as columns or None)."""
+    if solve_tridiag is None:
+        a = np.ascontiguousarray(a, dtype=np.complex128)
+        n = a.shape[0]
+        if a.ndim != 2 or a.shape[1] != n:
+            raise DimensionError(f"eigen_hh: matrix not square {a.shape}")
+        w = np.empty(n)
+        c = np.empty((n, n), dtype=np.complex128) if want_vectors else None
+        _check(_lib().kbg_hh_eigen(n, _cptr(a), int(want_vectors), _abi.dptr(w), _cptr(c) if want_vectors else None),
+               "kbg_hh_eigen")
+        return w, c
     t = tridiagonalize(a)
     w, z = solve_tridiag(t.d, t.e, want_vectors)
     if not want_vectors:
@@ -124,4 +152,4 @@ def eigen_hh(a: np.ndarray, want_vectors: bool = True, solve_tridiag=lapack_solv
 
 
 __all__ = ["HouseholderRecords", "TridiagReal", "tridiagonalize", "back_transform", "normalize_columns", "triple_product",
-           "lapack_solve_tridiag", "eigen_hh"]
+           "lapack_solve_tridiag", "gpu_solve_tridiag", "eigen_hh"]

@@ -77,8 +77,14 @@ def test_eigen_hh_contract(n):
     assert np.abs(w - rw).max() <= 1e-11 * nrm
     assert np.abs(a @ v - v * w).max() <= 1e-9 * nrm
     assert np.abs(v.conj().T @ v - np.eye(n)).max() <= 1e-9
-    w2, _ = E.eigen_hh(a, want_vectors=False)  # default host step: LAPACK stemr
+    w2, _ = E.eigen_hh(a, want_vectors=False, solve_tridiag=E.lapack_solve_tridiag)  # the paper's CPU step
     assert np.abs(w2 - rw).max() <= 1e-11 * nrm
+    w3, v3 = E.eigen_hh(a)  # default: device-resident pipeline with the GPU tridiagonal solver
+    assert np.abs(w3 - rw).max() <= 1e-11 * nrm
+    assert np.abs(a @ v3 - v3 * w3).max() <= 1e-9 * nrm
+    assert np.abs(v3.conj().T @ v3 - np.eye(n)).max() <= 1e-9
+    w4, v4 = E.eigen_hh(a, want_vectors=False)
+    assert v4 is None and np.array_equal(w4, w3)
 
 
 def test_fault_hook_breaks_spectrum():

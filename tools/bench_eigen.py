@@ -103,7 +103,27 @@ def main():
         e1.record(st)
         e1.synchronize()
         rec["gpu_normalize_ms"] = round(e0.elapsed_time(e1), 3)
-        rec["gpu_eigen_hh_e2e_ms"] = round(wall(lambda: E.eigen_hh(A, True)), 2)
+        rec["gpu_eigen_hh_e2e_host_lapack_ms"] = round(
+            wall(lambda: E.eigen_hh(A, True, solve_tridiag=E.lapack_solve_tridiag)), 2)
+        rec["gpu_eigen_hh_e2e_ms"] = round(wall(lambda: E.eigen_hh(A, True)), 2)  # kbg_hh_eigen, device-resident
+        # the tridiagonal step: GPU (kbg_tridiag_solve, device-resident, events) vs host LAPACK stemr
+        t = E.tridiagonalize(A)
+        Dd = torch.from_numpy(t.d).to(dev)
+        De = torch.from_numpy(t.e if n > 1 else np.zeros(1)).to(dev)
+        Dw = torch.empty(n, dtype=torch.float64, device=dev)
+        Dz = torch.empty((n, n), dtype=torch.float64, device=dev)
+        ts = []
+        for _ in range(4):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            assert lib.kbg_tridiag_solve_dev(n, Dd.data_ptr(), De.data_ptr(), 1, Dw.data_ptr(), Dz.data_ptr(),
+                                             st.cuda_stream) == 0
+            e1.record(st)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        rec["gpu_tridiag_solve_ms"] = round(float(np.median(ts[1:])), 3)
+        rec["host_lapack_stemr_ms"] = round(wall(lambda: E.lapack_solve_tridiag(t.d, t.e, True)), 2)
+
         # reference kband on the host
         if n <= 1100:
             rec["ref_tridiagonalize_serial_ms"] = round(wall(lambda: R.tridiagonalize(A), 1), 1)
@@ -113,8 +133,10 @@ def main():
         rd, re_, ru, rh, rs, rph = R.tridiagonalize(A)
         rec["ref_back_transform_threaded_ms"] = round(wall(lambda: R.back_transform(ru, rh, rs, rph, z, nt), 1), 1)
         rec["max_eig_residual_rel"] = None
-        w, v = E.eigen_hh(A, True)
+        w, v = E.eigen_hh(A, True, solve_tridiag=E.lapack_solve_tridiag)
         rec["max_eig_residual_rel"] = float(np.abs(A @ v - v * w).max() / np.linalg.norm(A))
+        w, v = E.eigen_hh(A, True)
+        rec["max_eig_residual_rel_gpu_solver"] = float(np.abs(A @ v - v * w).max() / np.linalg.norm(A))
         print(json.dumps(rec), flush=True)
 
 
