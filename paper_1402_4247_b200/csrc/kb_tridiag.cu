@@ -148,8 +148,11 @@ __global__ void __launch_bounds__(128) k_tri_eigvecs(int n, const double* __rest
             zc(0, j) = 1.0;
             continue;
         }
-        // LU of T - lam I with partial pivoting (rows k, k+1), LAPACK dgttrf layout
+        // LU of T - lam I with partial pivoting (rows k, k+1), LAPACK dgttrf layout. The loops
+        // below are unrolled so the (independent) scratch loads of several steps are in flight
+        // ahead of the dependent recurrence.
         double dk = d[0] - lam, uk = e[0];
+#pragma unroll 4
         for (int k = 0; k < n - 1; ++k) {
             const double lk = e[k];                                 // sub-diagonal entry below dk
             const double dn = d[k + 1] - lam, un = k + 1 < n - 1 ? e[k + 1] : 0.0;
@@ -178,6 +181,7 @@ __global__ void __launch_bounds__(128) k_tri_eigvecs(int n, const double* __rest
         for (int k = 0; k < n; ++k) at(B, k) = start_value(j, k);
         for (int it = 0; it < 3; ++it) {
             // forward: apply the row interchanges and L
+#pragma unroll 8
             for (int k = 0; k < n - 1; ++k) {
                 const double bk = at(B, k), bn = at(B, k + 1);
                 if (at(Sw, k) != 0.0) {
@@ -190,6 +194,7 @@ __global__ void __launch_bounds__(128) k_tri_eigvecs(int n, const double* __rest
             // back substitution with U (diagonal, u1, u2) into column j of z
             double x2 = 0.0, x1 = at(B, n - 1) * at(Pi, n - 1);
             zc(n - 1, j) = x1;
+#pragma unroll 8
             for (int k = n - 2; k >= 0; --k) {
                 const double x = (at(B, k) - at(U1, k) * x1 - at(U2, k) * x2) * at(Pi, k);
                 zc(k, j) = x;
