@@ -1262,6 +1262,21 @@ struct DevBuf {
     DevBuf& operator=(const DevBuf&) = delete;
 };
 
+// W = Q Y on the device: per-column reflector chain for small n, blocked compact WY (ZGEMMs) from
+// kWyMinN (set KBG_BT_WY=0 to force the per-column kernel, =1 to force WY).
+void back_transform_dev(int64_t n, int64_t m, const double* Y, const double* U, const double* H, const double* P,
+                        double* W, cudaStream_t st) {
+    DevBuf dph(2 * n, st);
+    const char* env = std::getenv("KBG_BT_WY");
+    const bool wy = env ? env[0] == '1' : n >= kbg::kWyMinN;
+    if (wy && n > 1) {
+        DevBuf scr(kbg::hh_back_transform_wy_scratch(static_cast<int>(n), static_cast<int>(m)), st);
+        kbg::launch_hh_back_transform_wy(static_cast<int>(n), static_cast<int>(m), Y, U, H, P, dph.p, W, scr.p, st);
+    } else {
+        kbg::launch_hh_back_transform(static_cast<int>(n), static_cast<int>(m), Y, U, H, P, dph.p, W, st);
+    }
+}
+
 void hh_check_n(int64_t n) {
     if (n < 1) throw Error(KBG_ERR_DIMENSION, "tridiagonalize: empty matrix");
     if (n > 4800) throw Error(KBG_ERR_DIMENSION, "tridiagonalize: n = " + std::to_string(n) + " > 4800 (shared-memory reflectors)");
@@ -1335,8 +1350,7 @@ int kbg_hh_back_transform_dev(int64_t n, int64_t m, const double* d_u, const dou
         hh_check_n(n);
         if (m < 1) throw Error(KBG_ERR_DIMENSION, "back_transform: no columns");
         const cudaStream_t st = static_cast<cudaStream_t>(stream);
-        DevBuf dph(2 * n, st);
-        kbg::launch_hh_back_transform(static_cast<int>(n), static_cast<int>(m), d_y, d_u, d_h, d_phase, dph.p, d_w, st);
+        back_transform_dev(n, m, d_y, d_u, d_h, d_phase, d_w, st);
     });
 }
 
@@ -1356,7 +1370,7 @@ int kbg_hh_back_transform(int64_t n, int64_t m, const double* u, const double* h
             KBG_CUDA(cudaMemcpyAsync(P.p, phase, 2 * nr * sizeof(double), cudaMemcpyHostToDevice, st));
         }
         KBG_CUDA(cudaMemcpyAsync(Y.p, y, static_cast<size_t>(n) * m * sizeof(double), cudaMemcpyHostToDevice, st));
-        kbg::launch_hh_back_transform(static_cast<int>(n), static_cast<int>(m), Y.p, U.p, H.p, P.p, dph.p, W.p, st);
+        back_transform_dev(n, m, Y.p, U.p, H.p, P.p, W.p, st);
         KBG_CUDA(cudaMemcpyAsync(w, W.p, 2 * static_cast<size_t>(n) * m * sizeof(double), cudaMemcpyDeviceToHost, st));
         KBG_CUDA(cudaStreamSynchronize(st));
     });
@@ -1447,9 +1461,7 @@ int kbg_hh_eigen(int64_t n, const double* a, int want_vectors, double* w, double
                 const double one[2] = {1.0, 0.0};
                 KBG_CUDA(cudaMemcpyAsync(C, one, sizeof(one), cudaMemcpyHostToDevice, st));
             } else {
-                DevBuf dph(2 * n, st);
-                kbg::launch_hh_back_transform(static_cast<int>(n), static_cast<int>(n), Y.p, U.p, H.p, P.p, dph.p, C,
-                                              st);
+                back_transform_dev(n, n, Y.p, U.p, H.p, P.p, C, st);
             }
             const int stn = kbg_hh_normalize_columns_dev(n, n, C, st);
             if (stn != KBG_OK) throw Error(stn, g_hh_err);

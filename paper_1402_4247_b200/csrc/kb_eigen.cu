@@ -22,6 +22,7 @@
 // barrier is needed at all. All reductions have a fixed order: bitwise
 // deterministic run to run.
 #include <cooperative_groups.h>
+#include <cublas_v2.h>
 
 #include <algorithm>
 
@@ -37,6 +38,7 @@ constexpr double kSkipNorm = 1e-300;  // householder.cpp:46
 constexpr int kTriThreads = 512;      // 16 warps per CTA
 constexpr int kTriWarps = kTriThreads / 32;
 
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
@@ -404,6 +406,150 @@ int launch_hh_back_transform(int n, int m, const double* d_Y, const double* d_U,
         reinterpret_cast<double2*>(d_W));
     KBG_CUDA(cudaGetLastError());
     return 2;
+}
+
+// ---- blocked (compact WY) back transform ------------------------------------------
+// W = P_0 P_1 ... P_{n-2} D Y with P_k = I - u_k u_k^H / h_k (householder.cpp:275-296; D the chased
+// phases). Reflectors are grouped in blocks of kWyBlock: P_k0 ... P_k0+K-1 = I - V T V^H (LAPACK
+// zlarft, forward, columnwise: T upper triangular, T_ii = tau_i = 1/h_i, T(0:i, i) = -tau_i T(0:i,0:i)
+// V(:,0:i)^H v_i), and each block is applied with ZGEMMs, last block first: W -= V (T (V^H W)). W is
+// kept column-major (n x m, ld n) during the sweep; V is the block's rows of U read as a column-major
+// n x K matrix, restricted to its nonzero rows k0+1..n-1.
+constexpr int kWyBlock = 64;
+constexpr int kWySplit = 16;
+
+namespace {
+
+// W_cm[j][r] = D_r Y[r][j]
+__global__ void k_bt_wy_init(int n, int m, const double* __restrict__ Y, const double2* __restrict__ dph,
+                             double2* __restrict__ Wc) {
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < static_cast<int64_t>(n) * m;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t j = t / n, r = t % n;
+        const double y = Y[r * m + j];
+        const double2 f = dph[r];
+        Wc[t] = r == 0 ? make_double2(y, 0.0) : make_double2(y * f.x, y * f.y);
+    }
+}
+
+__global__ void k_bt_wy_out(int n, int m, const double2* __restrict__ Wc, double2* __restrict__ W) {
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < static_cast<int64_t>(n) * m;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = t / m, j = t % m;
+        W[t] = Wc[j * n + r];
+    }
+}
+
+// T (K x K, column-major, upper) of one block from G = V^H V (K x K, column-major) and h.
+// One CTA of K threads; column i needs the finished columns 0..i-1.
+__global__ void k_bt_wy_larft(int K, const double2* __restrict__ G, const double* __restrict__ h,
+                              double2* __restrict__ T) {
+    const int r = threadIdx.x;
+    for (int i = 0; i < K; ++i) {
+        const double tau = h[i] != 0.0 ? 1.0 / h[i] : 0.0;
+        double2 acc = make_double2(0.0, 0.0);
+        if (r < i) {  // (T(0:i,0:i) G(0:i, i))_r, T upper: columns c >= r
+            for (int c = r; c < i; ++c) acc = cadd(acc, cmul(T[c * K + r], G[i * K + c]));
+            T[i * K + r] = make_double2(-tau * acc.x, -tau * acc.y);
+        } else if (r == i) {
+            T[i * K + i] = make_double2(tau, 0.0);
+        } else if (r < K) {
+            T[i * K + r] = make_double2(0.0, 0.0);
+        }
+        __syncthreads();
+    }
+}
+
+// out = sum over chunks of P[c] (fixed order: deterministic)
+__global__ void k_bt_wy_sum(int64_t len, int chunks, const double2* __restrict__ P, double2* __restrict__ out) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= len) return;
+    double2 a = P[i];
+    for (int c = 1; c < chunks; ++c) a = cadd(a, P[c * len + i]);
+    out[i] = a;
+}
+
+cublasHandle_t wy_handle() {
+    static thread_local cublasHandle_t hnd = nullptr;
+    static thread_local int dev = -1;
+    int cur = 0;
+    KBG_CUDA(cudaGetDevice(&cur));
+    if (!hnd || dev != cur) {
+        if (cublasCreate(&hnd) != CUBLAS_STATUS_SUCCESS) throw Error(KBG_ERR_CUDA, "cublasCreate failed");
+        dev = cur;
+    }
+    return hnd;
+}
+
+void cublas_ok(cublasStatus_t s, const char* what) {
+    if (s != CUBLAS_STATUS_SUCCESS) throw Error(KBG_ERR_CUDA, std::string("back_transform: ") + what + " failed");
+}
+
+}  // namespace
+
+int launch_hh_back_transform_wy(int n, int m, const double* d_Y, const double* d_U, const double* d_h,
+                                const double* d_ph, double* d_dph, double* d_W, double* d_scr, cudaStream_t st) {
+    if (n <= 0 || m <= 0) return 0;
+    const int K = kWyBlock;
+    double2* Wc = reinterpret_cast<double2*>(d_scr);                     // n x m
+    double2* G = Wc + static_cast<int64_t>(n) * m;                       // K x K
+    double2* T = G + K * K;                                              // K x K
+    double2* X = T + K * K;                                              // K x m
+    double2* X2 = X + static_cast<int64_t>(K) * m;                       // K x m
+    double2* P = X2 + static_cast<int64_t>(K) * m;                       // kWySplit partials of K x max(K, m)
+    const double2* U = reinterpret_cast<const double2*>(d_U);
+    k_phase_prefix<<<1, 32, 0, st>>>(n, d_h, reinterpret_cast<const double2*>(d_ph), reinterpret_cast<double2*>(d_dph));
+    k_bt_wy_init<<<148 * 4, 256, 0, st>>>(n, m, d_Y, reinterpret_cast<const double2*>(d_dph), Wc);
+    cublasHandle_t hb = wy_handle();
+    cublas_ok(cublasSetStream(hb, st), "cublasSetStream");
+    const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0),
+                          mone = make_cuDoubleComplex(-1.0, 0.0);
+    auto z = [](const double2* p) { return reinterpret_cast<const cuDoubleComplex*>(p); };
+    auto zm = [](double2* p) { return reinterpret_cast<cuDoubleComplex*>(p); };
+    int launches = 2;
+    const int nref = n - 1;
+    for (int k0 = ((nref - 1) / K) * K; k0 >= 0; k0 -= K) {
+        const int kb = std::min(K, nref - k0);
+        const int r0 = k0 + 1, rows = n - r0;  // nonzero rows of the block's reflectors
+        const cuDoubleComplex* V = z(U + static_cast<int64_t>(k0) * n + r0);  // column i = u_{k0+i}, ld n
+        // G = V^H V, T = larft(G, h); X = V^H W. Both reduce over the long row dimension into a small
+        // output, so they are split over row chunks (strided-batched ZGEMMs into partials + a
+        // fixed-order sum): a plain ZGEMM of that shape runs on a handful of CTAs.
+        cuDoubleComplex* Wr = zm(Wc + r0);
+        const int chunks = std::max(1, std::min(kWySplit, rows / 128));
+        const int clen = (rows + chunks - 1) / chunks, last = rows - (chunks - 1) * clen;
+        auto splitk = [&](const cuDoubleComplex* B, int ncol, double2* out, const char* what) {
+            // full chunks batched; the (shorter) last chunk separately; then sum in chunk order
+            if (chunks > 1)
+                cublas_ok(cublasZgemmStridedBatched(hb, CUBLAS_OP_C, CUBLAS_OP_N, kb, ncol, clen, &one, V, n, clen, B,
+                                                    n, clen, &zero, zm(P), kb, static_cast<long long>(kb) * ncol,
+                                                    chunks - 1),
+                          what);
+            cublas_ok(cublasZgemm(hb, CUBLAS_OP_C, CUBLAS_OP_N, kb, ncol, last, &one, V + (chunks - 1) * clen, n,
+                                  B + (chunks - 1) * clen, n, &zero, zm(P + static_cast<int64_t>(chunks - 1) * kb * ncol),
+                                  kb),
+                      what);
+            k_bt_wy_sum<<<(kb * ncol + 255) / 256, 256, 0, st>>>(static_cast<int64_t>(kb) * ncol, chunks, P, out);
+        };
+        splitk(V, kb, G, "ZGEMM V^H V");
+        k_bt_wy_larft<<<1, ((kb + 31) / 32) * 32, 0, st>>>(kb, G, d_h + k0, T);
+        // X = V^H W, X2 = T X, W -= V X2 (rows r0..n-1 of W)
+        splitk(Wr, m, X, "ZGEMM V^H W");
+        cublas_ok(cublasZgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, kb, m, kb, &one, z(T), kb, z(X), kb, &zero, zm(X2), kb),
+                  "ZGEMM T X");
+        cublas_ok(cublasZgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, rows, m, kb, &mone, V, n, z(X2), kb, &one, Wr, n),
+                  "ZGEMM W -= V X");
+        launches += 5;
+    }
+    k_bt_wy_out<<<148 * 4, 256, 0, st>>>(n, m, Wc, reinterpret_cast<double2*>(d_W));
+    KBG_CUDA(cudaGetLastError());
+    return launches + 1;
+}
+
+size_t hh_back_transform_wy_scratch(int n, int m) {
+    const size_t wide = std::max<size_t>(kWyBlock, m);
+    return 2 * (static_cast<size_t>(n) * m + 2 * kWyBlock * kWyBlock + 2 * static_cast<size_t>(kWyBlock) * m +
+                static_cast<size_t>(kWySplit) * kWyBlock * wide);
 }
 
 int launch_hh_normalize_columns(int64_t n, int64_t m, double* d_C, int* d_zero, cudaStream_t st) {

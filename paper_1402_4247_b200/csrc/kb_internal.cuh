@@ -268,6 +268,12 @@ int launch_hh_tridiagonalize(int n, double* d_B, double* d_p, double* d, double*
                              double* ph, double sign, cudaStream_t st);
 int launch_hh_back_transform(int n, int m, const double* d_Y, const double* d_U, const double* d_h,
                              const double* d_ph, double* d_dph, double* d_W, cudaStream_t st);
+// Blocked (compact WY, cuBLAS ZGEMM) variant of the same W = Q Y; d_scr holds
+// hh_back_transform_wy_scratch(n, m) doubles. Used from n >= kWyMinN.
+int launch_hh_back_transform_wy(int n, int m, const double* d_Y, const double* d_U, const double* d_h,
+                                const double* d_ph, double* d_dph, double* d_W, double* d_scr, cudaStream_t st);
+size_t hh_back_transform_wy_scratch(int n, int m);
+constexpr int kWyMinN = 1024;  // measured crossover vs the per-column kernel (profiles/eigen_wy*.jsonl)
 int launch_hh_normalize_columns(int64_t n, int64_t m, double* d_C, int* d_zero, cudaStream_t st);
 // HBM probe (kb_probe.cu): x[v][:] /= ||x[v]|| for nvec rows of len doubles.
 int launch_normalize(double* d_x, int64_t nvec, int64_t len, cudaStream_t st);

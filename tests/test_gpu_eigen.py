@@ -139,3 +139,16 @@ def test_triple_product_matches_reference(n, m):
     ref = R.triple_product(t, h)
     assert np.abs(c - ref).max() <= 1e-12 * np.abs(ref).max()
     assert np.array_equal(c, c.conj().T)
+
+
+def test_back_transform_blocked_wy_matches_reference(monkeypatch):
+    """The blocked compact-WY back transform (ZGEMMs, used from n = 1024) forced at n = 300: same W as the
+    reference within 1e-12."""
+    monkeypatch.setenv("KBG_BT_WY", "1")
+    n = 300
+    a = hermitian(n, 31)
+    d, e, u, h, s, ph = R.tridiagonalize(a)
+    _, z = R.solve_tridiag(d, e, True)
+    ref_w = R.back_transform(u, h, s, ph, z)
+    w = E.back_transform(E.HouseholderRecords(u, h, s, ph), z)
+    assert np.abs(w - ref_w).max() <= 1e-12
