@@ -118,7 +118,10 @@ constexpr int kOrthWindow = 32;
 
 // One thread per cluster (started by its first member). z: [n][n] row-major,
 // column j = eigenvector j. Scratch (interleaved, stride n): lower multipliers,
-// 1/pivots, super diagonals u1, u2, swap flags, right-hand side.
+// 1/pivots, super diagonals u1, u2, swap flags, right-hand side. Every array
+// has its own restrict-qualified pointer and the recurrences carry their state
+// in registers, so the (independent) loads of later steps can be issued ahead
+// of the dependent chain.
 __global__ void __launch_bounds__(128) k_tri_eigvecs(int n, const double* __restrict__ d, const double* __restrict__ e,
                                                      const double* __restrict__ w, const double* __restrict__ aux,
                                                      double* __restrict__ scr, double* __restrict__ z) {
@@ -130,97 +133,105 @@ __global__ void __launch_bounds__(128) k_tri_eigvecs(int n, const double* __rest
     int end = t + 1;
     while (end < n && w[end] - w[end - 1] < ctol) ++end;
     const int64_t S = n;
-    double* Lm = scr;          // [n-1]
-    double* Pi = scr + S * n;  // [n] 1 / pivot
-    double* U1 = scr + 2 * S * n;
-    double* U2 = scr + 3 * S * n;
-    double* Sw = scr + 4 * S * n;  // swap flag of step k (1.0 / 0.0)
-    double* B = scr + 5 * S * n;
-    auto at = [&](double* a, int k) -> double& { return a[static_cast<int64_t>(k) * S + t]; };
-    auto zc = [&](int k, int j) -> double& { return z[static_cast<int64_t>(k) * n + j]; };
+    const int64_t nn = static_cast<int64_t>(n) * n;
+    double* __restrict__ Lm = scr + t;  // element k at [k * S]
+    double* __restrict__ Pi = scr + nn + t;
+    double* __restrict__ U1 = scr + 2 * nn + t;
+    double* __restrict__ U2 = scr + 3 * nn + t;
+    double* __restrict__ Sw = scr + 4 * nn + t;
+    double* __restrict__ B = scr + 5 * nn + t;
     const double tiny = DBL_EPSILON * tnorm;
     double lprev = 0.0;
     for (int j = t; j < end; ++j) {
+        double* __restrict__ zj = z + j;  // element k at [k * n]
         double lam = w[j];
         if (j > t && lam - lprev < pertol) lam = lprev + pertol;
         lprev = lam;
         if (n == 1) {
-            zc(0, j) = 1.0;
+            zj[0] = 1.0;
             continue;
         }
-        // LU of T - lam I with partial pivoting (rows k, k+1), LAPACK dgttrf layout. The loops
-        // below are unrolled so the (independent) scratch loads of several steps are in flight
-        // ahead of the dependent recurrence.
+        // LU of T - lam I with partial pivoting (rows k, k+1), LAPACK dgttrf layout
         double dk = d[0] - lam, uk = e[0];
 #pragma unroll 4
         for (int k = 0; k < n - 1; ++k) {
-            const double lk = e[k];                                 // sub-diagonal entry below dk
+            const double lk = e[k];  // sub-diagonal entry below dk
             const double dn = d[k + 1] - lam, un = k + 1 < n - 1 ? e[k + 1] : 0.0;
+            const int64_t o = k * S;
             if (fabs(dk) >= fabs(lk)) {
                 const double piv = fabs(dk) < tiny ? copysign(tiny, dk) : dk;
                 const double f = lk / piv;
-                at(Lm, k) = f;
-                at(Pi, k) = 1.0 / piv;
-                at(U1, k) = uk;
-                at(U2, k) = 0.0;
-                at(Sw, k) = 0.0;
+                Lm[o] = f;
+                Pi[o] = 1.0 / piv;
+                U1[o] = uk;
+                U2[o] = 0.0;
+                Sw[o] = 0.0;
                 dk = dn - f * uk;
                 uk = un;
             } else {
                 const double f = dk / lk;
-                at(Lm, k) = f;
-                at(Pi, k) = 1.0 / lk;
-                at(U1, k) = dn;
-                at(U2, k) = un;
-                at(Sw, k) = 1.0;
+                Lm[o] = f;
+                Pi[o] = 1.0 / lk;
+                U1[o] = dn;
+                U2[o] = un;
+                Sw[o] = 1.0;
                 dk = uk - f * dn;
                 uk = -f * un;
             }
         }
-        at(Pi, n - 1) = 1.0 / (fabs(dk) < tiny ? copysign(tiny, dk) : dk);
-        for (int k = 0; k < n; ++k) at(B, k) = start_value(j, k);
+        Pi[(n - 1) * S] = 1.0 / (fabs(dk) < tiny ? copysign(tiny, dk) : dk);
+        for (int k = 0; k < n; ++k) B[k * S] = start_value(j, k);
         for (int it = 0; it < 3; ++it) {
-            // forward: apply the row interchanges and L
+            // forward: apply the row interchanges and L (b_k carried in a register)
+            double bk = B[0];
 #pragma unroll 8
             for (int k = 0; k < n - 1; ++k) {
-                const double bk = at(B, k), bn = at(B, k + 1);
-                if (at(Sw, k) != 0.0) {
-                    at(B, k) = bn;
-                    at(B, k + 1) = bk - at(Lm, k) * bn;
-                } else {
-                    at(B, k + 1) = bn - at(Lm, k) * bk;
-                }
+                const int64_t o = k * S;
+                const double bn = B[o + S], f = Lm[o];
+                const bool sw = Sw[o] != 0.0;
+                B[o] = sw ? bn : bk;
+                bk = sw ? bk - f * bn : bn - f * bk;
             }
+            B[(n - 1) * S] = bk;
             // back substitution with U (diagonal, u1, u2) into column j of z
-            double x2 = 0.0, x1 = at(B, n - 1) * at(Pi, n - 1);
-            zc(n - 1, j) = x1;
+            double x2 = 0.0, x1 = bk * Pi[(n - 1) * S];
+            zj[static_cast<int64_t>(n - 1) * n] = x1;
+            double nrm = x1 * x1;
 #pragma unroll 8
             for (int k = n - 2; k >= 0; --k) {
-                const double x = (at(B, k) - at(U1, k) * x1 - at(U2, k) * x2) * at(Pi, k);
-                zc(k, j) = x;
+                const int64_t o = k * S;
+                const double x = (B[o] - U1[o] * x1 - U2[o] * x2) * Pi[o];
+                zj[static_cast<int64_t>(k) * n] = x;
+                nrm += x * x;
                 x2 = x1;
                 x1 = x;
             }
             // re-orthogonalize against the earlier members of the cluster, normalize
-            for (int p = t; p < j; ++p) {
-                double dot = 0.0;
-                for (int k = 0; k < n; ++k) dot += zc(k, p) * zc(k, j);
-                for (int k = 0; k < n; ++k) zc(k, j) -= dot * zc(k, p);
+            if (j > t) {
+                for (int p = t; p < j; ++p) {
+                    const double* __restrict__ zp = z + p;
+                    double dot = 0.0;
+                    for (int k = 0; k < n; ++k) dot += zp[static_cast<int64_t>(k) * n] * zj[static_cast<int64_t>(k) * n];
+                    for (int k = 0; k < n; ++k) zj[static_cast<int64_t>(k) * n] -= dot * zp[static_cast<int64_t>(k) * n];
+                }
+                nrm = 0.0;
+                for (int k = 0; k < n; ++k) nrm += zj[static_cast<int64_t>(k) * n] * zj[static_cast<int64_t>(k) * n];
             }
-            double nrm = 0.0;
-            for (int k = 0; k < n; ++k) nrm += zc(k, j) * zc(k, j);
-            const double s = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
+            const double sc = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
+#pragma unroll 8
             for (int k = 0; k < n; ++k) {
-                const double v = zc(k, j) * s;
-                zc(k, j) = v;
-                at(B, k) = v;
+                const double v = zj[static_cast<int64_t>(k) * n] * sc;
+                zj[static_cast<int64_t>(k) * n] = v;
+                B[k * S] = v;
             }
         }
     }
 }
 
 // One windowed symmetric correction: zout_j = (z_j - 1/2 sum_k (z_k . z_j) z_k) / norm, k over the
-// neighbours of j (|w_k - w_j| < 1e-3 ||T||_1, at most kOrthWindow each side). Thread per vector.
+// neighbours of j (|w_k - w_j| < 1e-3 ||T||_1, at most kOrthWindow each side). Thread per vector; the
+// window's columns are a contiguous segment of each row, so one pass over the rows gathers all dots
+// and a second applies the correction.
 __global__ void __launch_bounds__(128) k_tri_orth(int n, const double* __restrict__ w, const double* __restrict__ aux,
                                                   const double* __restrict__ zin, double* __restrict__ zout) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -229,22 +240,30 @@ __global__ void __launch_bounds__(128) k_tri_orth(int n, const double* __restric
     int lo = j, hi = j;
     while (lo > 0 && j - lo < kOrthWindow && w[j] - w[lo - 1] < ortol) --lo;
     while (hi + 1 < n && hi - j < kOrthWindow && w[hi + 1] - w[j] < ortol) ++hi;
-    auto zi = [&](int i, int k) { return zin[static_cast<int64_t>(i) * n + k]; };
-    for (int i = 0; i < n; ++i) zout[static_cast<int64_t>(i) * n + j] = zi(i, j);
-    for (int k = lo; k <= hi; ++k) {
-        if (k == j) continue;
-        double dot = 0.0;
-        for (int i = 0; i < n; ++i) dot += zi(i, k) * zi(i, j);
-        const double c = 0.5 * dot;
-        for (int i = 0; i < n; ++i) zout[static_cast<int64_t>(i) * n + j] -= c * zi(i, k);
+    if (lo == hi) {  // no close neighbour: copy
+        for (int64_t i = 0; i < n; ++i) zout[i * n + j] = zin[i * n + j];
+        return;
     }
+    double dots[2 * kOrthWindow + 1];
+    const int nw = hi - lo + 1;
+    for (int k = 0; k < nw; ++k) dots[k] = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        const double* __restrict__ row = zin + i * n + lo;
+        const double zj = zin[i * n + j];
+        for (int k = 0; k < nw; ++k) dots[k] += row[k] * zj;
+    }
+    for (int k = 0; k < nw; ++k) dots[k] *= 0.5;
+    dots[j - lo] = 0.0;
     double nrm = 0.0;
-    for (int i = 0; i < n; ++i) {
-        const double v = zout[static_cast<int64_t>(i) * n + j];
+    for (int64_t i = 0; i < n; ++i) {
+        const double* __restrict__ row = zin + i * n + lo;
+        double v = zin[i * n + j];
+        for (int k = 0; k < nw; ++k) v -= dots[k] * row[k];
+        zout[i * n + j] = v;
         nrm += v * v;
     }
-    const double s = 1.0 / sqrt(nrm);
-    for (int i = 0; i < n; ++i) zout[static_cast<int64_t>(i) * n + j] *= s;
+    const double sc = 1.0 / sqrt(nrm);
+    for (int64_t i = 0; i < n; ++i) zout[i * n + j] *= sc;
 }
 
 }  // namespace
