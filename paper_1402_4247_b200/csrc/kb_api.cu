@@ -1251,10 +1251,27 @@ int hh_guard(const std::function<void()>& fn) {
 }
 
 // Stream-ordered device scratch freed at scope exit.
+// Stream-ordered allocations come from the device's default pool; keep freed memory in the pool
+// (release threshold: unlimited) so repeated calls do not re-map hundreds of MB each time.
+void keep_pool() {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    KBG_CUDA(cudaGetDevice(&dev));
+    if (done_dev == dev) return;
+    cudaMemPool_t pool;
+    KBG_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thr = UINT64_MAX;
+    KBG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    done_dev = dev;
+}
+
 struct DevBuf {
     double* p = nullptr;
     cudaStream_t st = nullptr;
-    DevBuf(size_t n, cudaStream_t s) : st(s) { KBG_CUDA(cudaMallocAsync(&p, std::max<size_t>(1, n) * sizeof(double), s)); }
+    DevBuf(size_t n, cudaStream_t s) : st(s) {
+        keep_pool();
+        KBG_CUDA(cudaMallocAsync(&p, std::max<size_t>(1, n) * sizeof(double), s));
+    }
     ~DevBuf() {
         if (p) cudaFreeAsync(p, st);
     }
