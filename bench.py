@@ -380,8 +380,11 @@ def main():
         o.build_index()
         threads = os.cpu_count() or 1
         cms, sample = cpu_oracle_pass(f, o, dm_h, veff_h, threads, budget_s=20.0)
+        # also 1 thread, on a bounded sample (~8 s)
+        c1ms, sample1 = cpu_oracle_pass(f, o, dm_h, veff_h, 1, budget_s=8.0)
         cpu = {"value": round(cms, 3), "unit": "ms", "cores": threads, "kind": "port",
-               "sample": sample + f"; oracle/ C++ port, {threads} threads"}
+               "sample": sample + f"; oracle/ C++ port, {threads} threads",
+               "single_thread": {"value": round(c1ms, 3), "unit": "ms", "cores": 1, "sample": sample1}}
 
     if rank == 0:
         total_f = nspin * (4.0 * ix["sum_m2"] + 2.0 * ix["sum_m"])
