@@ -294,6 +294,8 @@ def main():
                 step(collective=False)
             torch.cuda.synchronize()
             extra += 20
+    if p2p:
+        gp.comm_check()  # raises if a peer exchange timed out (results invalid)
     if world > 1:
         dist.barrier()
     for e in evs:

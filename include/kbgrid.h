@@ -251,6 +251,11 @@ int kbg_comm_handle(kbg_ctx* ctx, void* handle_out);
 int kbg_comm_open(kbg_ctx* ctx, const void* handles);
 int kbg_hamiltonian_allreduce_dev(kbg_ctx* ctx, int nspin, const double* d_veff, double dV, double* d_h,
                                   void* stream);
+/* After synchronizing a kbg_hamiltonian_allreduce_dev: KBG_ERR_NCCL if a peer
+ * never arrived (the kernels give up after 10 s instead of hanging the GPU;
+ * the H of that call is invalid), else KBG_OK. Clears the flag. kbg_grid_pass
+ * on a sharded context checks it itself. */
+int kbg_comm_check(kbg_ctx* ctx);
 
 /* ---- Formats either side of the grid pass ----------------
  * The pair-sparse blocks of kbg_index (grid-pass DM input, H output) against

@@ -276,6 +276,18 @@ int run_density(kbg_ctx* c, int nspin, const double* d_dm, double* d_rho, cudaSt
     return n + kbg::launch_density(g, c->blk_end - c->blk_begin, c->nwarps, st);
 }
 
+// Reads and clears this rank's exchange error word (kb_comm.cu wait_flags); after a synchronize.
+void comm_check(kbg_ctx* c) {
+    unsigned long long* err = c->comm.flags[c->rank] + kbg::kMaxRanks + 1;
+    unsigned long long v = 0;
+    KBG_CUDA(cudaMemcpy(&v, err, sizeof(v), cudaMemcpyDeviceToHost));
+    if (v) {
+        const unsigned long long zero = 0;
+        KBG_CUDA(cudaMemcpy(err, &zero, sizeof(zero), cudaMemcpyHostToDevice));
+        throw Error(KBG_ERR_NCCL, "peer-memory H exchange: a peer did not arrive within 10 s (H invalid)");
+    }
+}
+
 int run_hamiltonian(kbg_ctx* c, int nspin, double dV, const double* d_veff, double* d_h, cudaStream_t st) {
     const kbg::GridArgs g = grid_args(c, nspin, dV, d_veff, d_h, false);
     if (c->persist_ok && c->persist && c->ix.phis) {
@@ -655,6 +667,7 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
         KBG_CUDA(cudaMemcpyAsync(chk, c->d_check, sizeof(chk), cudaMemcpyDeviceToHost, c->stream));
         KBG_CUDA(cudaStreamSynchronize(c->stream2));
         KBG_CUDA(cudaStreamSynchronize(c->stream));
+        if (c->comm_ready) comm_check(c);
         c->last_launches = n;
         double dmax, amax;
         std::memcpy(&dmax, &chk[0], 8);
@@ -1209,6 +1222,16 @@ int kbg_comm_open(kbg_ctx* c, const void* handles) {
         cm.elm = reinterpret_cast<const uint8_t*>(c->d_canon + 2 * e0.size());
         cm.ne = static_cast<int64_t>(e0.size());
         c->comm_ready = true;
+    });
+}
+
+
+int kbg_comm_check(kbg_ctx* c) {
+    if (!c) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        if (!c->comm_ready) throw Error(KBG_ERR_CONFIG, "comm_check: call kbg_comm_open first");
+        KBG_CUDA(cudaSetDevice(c->device));
+        comm_check(c);
     });
 }
 

@@ -192,6 +192,10 @@ class GridPass:
                                                             self._stream_ptr(stream)),
                     "kbg_hamiltonian_allreduce_dev")
 
+    def comm_check(self) -> None:
+        """After synchronizing a hamiltonian_allreduce_dev: raise if a peer never arrived."""
+        self._check(self._lib.kbg_comm_check(self._h), "kbg_comm_check")
+
     # -- formats either side (SURVEY.md 8(f2); see formats.py for the SPEC types) --
     def offsets(self) -> np.ndarray:
         """Distinct lattice offsets R of the pair list, sorted, shape (nR, 3)."""

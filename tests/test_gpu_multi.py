@@ -30,3 +30,31 @@ def test_p2p_reduce_mirror_two_ranks(built):
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
     rec = json.loads(line)
     assert rec["ok"], rec
+
+
+@pytest.mark.gpu
+def test_p2p_missing_peer_fails_loudly(built):
+    """Two sharded contexts in one process on one GPU (direct-pointer peers): only rank 0 runs the
+    exchange, so its kernels give up after 10 s instead of hanging, and kbg_comm_check reports
+    KBG_ERR_NCCL instead of handing back an invalid H."""
+    import torch
+
+    from paper_1402_4247_b200.errors import CollectiveError
+    from paper_1402_4247_b200.grid import GridPass
+    from paper_1402_4247_b200.system import Fe3O4
+
+    f = Fe3O4.config("primitive14_150Ry")
+    gps = [GridPass(f.system, device=0, rank=r, nranks=2) for r in range(2)]
+    for gp in gps:
+        gp.build_index()
+    handles = [gp.comm_handle() for gp in gps]
+    for gp in gps:
+        gp.comm_open(handles)
+    ix = gps[0].build_index()
+    dev = torch.device("cuda", 0)
+    v = torch.from_numpy(f.veff()).to(dev)
+    h = torch.empty((1, ix["nnz"]), dtype=torch.float64, device=dev)
+    gps[0].hamiltonian_allreduce_dev(v, f.dV, h)
+    torch.cuda.synchronize()
+    with pytest.raises(CollectiveError):
+        gps[0].comm_check()

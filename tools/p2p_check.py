@@ -47,6 +47,7 @@ def main(cfg="cubic56_200Ry"):
     p2p()
     nccl()
     torch.cuda.synchronize()
+    gp.comm_check()
     first = h_p2p.clone()
     p2p()
     torch.cuda.synchronize()
