@@ -19,6 +19,7 @@
 // Scratch is interleaved [k][thread] so a warp's threads touch consecutive
 // addresses at every step of their (sequential) recurrences.
 #include <cfloat>
+#include <cstdlib>
 
 #include "kb_internal.cuh"
 
@@ -228,47 +229,161 @@ __global__ void __launch_bounds__(128) k_tri_eigvecs(int n, const double* __rest
     }
 }
 
+// Shared-memory variant (n <= kTriSmemMaxN): one warp per cluster, the LU factors and the
+// right-hand side in the CTA's shared memory, so every step of lane 0's sequential recurrences is a
+// shared-memory access instead of a DRAM round trip through the interleaved scratch (at n = 2048 the
+// scratch of all vectors is 200 MB, past L2); normalization and re-orthogonalization use all lanes.
+constexpr int kTriSmemMaxN = 5120;
+
+__global__ void __launch_bounds__(32) k_tri_eigvecs_smem(int n, const double* __restrict__ d,
+                                                         const double* __restrict__ e, const double* __restrict__ w,
+                                                         const double* __restrict__ aux, double* __restrict__ z) {
+    extern __shared__ double vsm[];
+    const int t = blockIdx.x, lane = threadIdx.x;
+    const double tnorm = fmax(aux[2], DBL_MIN);
+    const double ctol = kTightGap * tnorm, pertol = 10.0 * DBL_EPSILON * tnorm;
+    if (t > 0 && w[t] - w[t - 1] < ctol) return;  // not the first member of its (near-degenerate) cluster
+    int end = t + 1;
+    while (end < n && w[end] - w[end - 1] < ctol) ++end;
+    double* __restrict__ Lm = vsm;
+    double* __restrict__ Pi = vsm + n;
+    double* __restrict__ U1 = vsm + 2 * n;
+    double* __restrict__ U2 = vsm + 3 * n;
+    double* __restrict__ B = vsm + 4 * n;  // right-hand side, then the solution in place
+    unsigned char* __restrict__ Sw = reinterpret_cast<unsigned char*>(vsm + 5 * n);
+    const double tiny = DBL_EPSILON * tnorm;
+    double lprev = 0.0;
+    for (int j = t; j < end; ++j) {
+        double lam = w[j];
+        if (j > t && lam - lprev < pertol) lam = lprev + pertol;
+        lprev = lam;
+        if (n == 1) {
+            if (lane == 0) z[0] = 1.0;
+            continue;
+        }
+        if (lane == 0) {
+            double dk = d[0] - lam, uk = e[0];
+            for (int k = 0; k < n - 1; ++k) {
+                const double lk = e[k];
+                const double dn = d[k + 1] - lam, un = k + 1 < n - 1 ? e[k + 1] : 0.0;
+                if (fabs(dk) >= fabs(lk)) {
+                    const double piv = fabs(dk) < tiny ? copysign(tiny, dk) : dk;
+                    const double f = lk / piv;
+                    Lm[k] = f;
+                    Pi[k] = 1.0 / piv;
+                    U1[k] = uk;
+                    U2[k] = 0.0;
+                    Sw[k] = 0;
+                    dk = dn - f * uk;
+                    uk = un;
+                } else {
+                    const double f = dk / lk;
+                    Lm[k] = f;
+                    Pi[k] = 1.0 / lk;
+                    U1[k] = dn;
+                    U2[k] = un;
+                    Sw[k] = 1;
+                    dk = uk - f * dn;
+                    uk = -f * un;
+                }
+            }
+            Pi[n - 1] = 1.0 / (fabs(dk) < tiny ? copysign(tiny, dk) : dk);
+        }
+        for (int k = lane; k < n; k += 32) B[k] = start_value(j, k);
+        __syncwarp();
+        for (int it = 0; it < 3; ++it) {
+            if (lane == 0) {
+                double bk = B[0];
+                for (int k = 0; k < n - 1; ++k) {
+                    const double bn = B[k + 1], f = Lm[k];
+                    const bool sw = Sw[k] != 0;
+                    B[k] = sw ? bn : bk;
+                    bk = sw ? bk - f * bn : bn - f * bk;
+                }
+                double x2 = 0.0, x1 = bk * Pi[n - 1];
+                B[n - 1] = x1;
+                for (int k = n - 2; k >= 0; --k) {
+                    const double x = (B[k] - U1[k] * x1 - U2[k] * x2) * Pi[k];
+                    B[k] = x;
+                    x2 = x1;
+                    x1 = x;
+                }
+            }
+            __syncwarp();
+            // re-orthogonalize against the earlier members of the cluster (columns of z), normalize
+            for (int p = t; p < j; ++p) {
+                double dot = 0.0;
+                for (int k = lane; k < n; k += 32) dot += z[static_cast<int64_t>(k) * n + p] * B[k];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+                for (int k = lane; k < n; k += 32) B[k] -= dot * z[static_cast<int64_t>(k) * n + p];
+                __syncwarp();
+            }
+            double nrm = 0.0;
+            for (int k = lane; k < n; k += 32) nrm += B[k] * B[k];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+            const double sc = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
+            for (int k = lane; k < n; k += 32) B[k] *= sc;
+            __syncwarp();
+        }
+        for (int k = lane; k < n; k += 32) z[static_cast<int64_t>(k) * n + j] = B[k];
+        __syncwarp();
+    }
+}
+
 // One windowed symmetric correction: zout_j = (z_j - 1/2 sum_k (z_k . z_j) z_k) / norm, k over the
-// neighbours of j (|w_k - w_j| < 1e-3 ||T||_1, at most kOrthWindow each side). Thread per vector; the
-// window's columns are a contiguous segment of each row, so one pass over the rows gathers all dots
-// and a second applies the correction.
-__global__ void __launch_bounds__(128) k_tri_orth(int n, const double* __restrict__ w, const double* __restrict__ aux,
-                                                  const double* __restrict__ zin, double* __restrict__ zout) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+// neighbours of j (|w_k - w_j| < 1e-3 ||T||_1, at most kOrthWindow each side). One warp per vector:
+// lanes split the rows, and since the window's columns are a contiguous segment of each row, one pass
+// gathers all (per-lane partial) dots, reduced with shuffles, and a second applies the correction.
+__global__ void __launch_bounds__(128) k_tri_orth_warp(int n, const double* __restrict__ w,
+                                                       const double* __restrict__ aux, const double* __restrict__ zin,
+                                                       double* __restrict__ zout) {
+    const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (j >= n) return;
     const double ortol = 1e-3 * fmax(aux[2], DBL_MIN);
     int lo = j, hi = j;
     while (lo > 0 && j - lo < kOrthWindow && w[j] - w[lo - 1] < ortol) --lo;
     while (hi + 1 < n && hi - j < kOrthWindow && w[hi + 1] - w[j] < ortol) ++hi;
-    if (lo == hi) {  // no close neighbour: copy
-        for (int64_t i = 0; i < n; ++i) zout[i * n + j] = zin[i * n + j];
+    if (lo == hi) {
+        for (int64_t i = lane; i < n; i += 32) zout[i * n + j] = zin[i * n + j];
         return;
     }
-    double dots[2 * kOrthWindow + 1];
     const int nw = hi - lo + 1;
+    double dots[2 * kOrthWindow + 1];
     for (int k = 0; k < nw; ++k) dots[k] = 0.0;
-    for (int64_t i = 0; i < n; ++i) {
+    for (int64_t i = lane; i < n; i += 32) {
         const double* __restrict__ row = zin + i * n + lo;
         const double zj = zin[i * n + j];
         for (int k = 0; k < nw; ++k) dots[k] += row[k] * zj;
     }
-    for (int k = 0; k < nw; ++k) dots[k] *= 0.5;
-    dots[j - lo] = 0.0;
+    for (int k = 0; k < nw; ++k) {
+        double v = dots[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        dots[k] = k == j - lo ? 0.0 : 0.5 * v;
+    }
     double nrm = 0.0;
-    for (int64_t i = 0; i < n; ++i) {
+    for (int64_t i = lane; i < n; i += 32) {
         const double* __restrict__ row = zin + i * n + lo;
         double v = zin[i * n + j];
         for (int k = 0; k < nw; ++k) v -= dots[k] * row[k];
         zout[i * n + j] = v;
         nrm += v * v;
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
     const double sc = 1.0 / sqrt(nrm);
-    for (int64_t i = 0; i < n; ++i) zout[i * n + j] *= sc;
+    for (int64_t i = lane; i < n; i += 32) zout[i * n + j] *= sc;
 }
 
 }  // namespace
 
-size_t tridiag_scratch_doubles(int n, bool vectors) { return 4 + (vectors ? 6 * static_cast<size_t>(n) * n : 0); }
+size_t tridiag_scratch_doubles(int n, bool vectors) {
+    if (!vectors) return 4;
+    const bool smem = n <= kTriSmemMaxN && !std::getenv("KBG_TRI_GLOBAL");
+    return 4 + (smem ? 1 : 6) * static_cast<size_t>(n) * n;  // smem path: only the re-orthogonalization buffer
+}
 
 int launch_tridiag_solve(int n, const double* d_d, const double* d_e, bool vectors, double* d_w, double* d_z,
                          double* d_scr, cudaStream_t st) {
@@ -282,10 +397,18 @@ int launch_tridiag_solve(int n, const double* d_d, const double* d_e, bool vecto
     KBG_CUDA(cudaGetLastError());
     if (!vectors) return 2;
     const unsigned g = static_cast<unsigned>((n + 127) / 128);
-    k_tri_eigvecs<<<g, 128, 0, st>>>(n, d_d, d_e, d_w, aux, d_scr, d_z);
+    if (n <= kTriSmemMaxN && !std::getenv("KBG_TRI_GLOBAL")) {
+        const size_t vs = 5 * static_cast<size_t>(n) * sizeof(double) + ((n + 15) & ~15);
+        KBG_CUDA(cudaFuncSetAttribute(k_tri_eigvecs_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(vs)));
+        k_tri_eigvecs_smem<<<static_cast<unsigned>(n), 32, vs, st>>>(n, d_d, d_e, d_w, aux, d_z);
+    } else {
+        k_tri_eigvecs<<<g, 128, 0, st>>>(n, d_d, d_e, d_w, aux, d_scr, d_z);
+    }
     // two windowed corrections, ping-pong through the (now free) LU scratch
-    k_tri_orth<<<g, 128, 0, st>>>(n, d_w, aux, d_z, d_scr);
-    k_tri_orth<<<g, 128, 0, st>>>(n, d_w, aux, d_scr, d_z);
+    const unsigned gw = static_cast<unsigned>((static_cast<int64_t>(n) * 32 + 127) / 128);
+    k_tri_orth_warp<<<gw, 128, 0, st>>>(n, d_w, aux, d_z, d_scr);
+    k_tri_orth_warp<<<gw, 128, 0, st>>>(n, d_w, aux, d_scr, d_z);
     KBG_CUDA(cudaGetLastError());
     return 5;
 }
