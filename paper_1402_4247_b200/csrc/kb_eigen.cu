@@ -25,6 +25,7 @@
 #include <cublas_v2.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "kb_internal.cuh"
 
@@ -35,6 +36,12 @@ namespace kbg {
 namespace {
 
 constexpr double kSkipNorm = 1e-300;  // householder.cpp:46
+// Unroll of the fused per-row sweep (her2 update + next hemv): keeps several L2 loads of a row in
+// flight per lane; measured n = 1040 10.4 -> 8.2 ms (4), 8.5 (8).
+#ifndef KBG_TRI_UNROLL
+#define KBG_TRI_UNROLL 4
+#endif
+constexpr int kTriUnroll = KBG_TRI_UNROLL;
 constexpr int kTriThreads = 512;      // 16 warps per CTA
 constexpr int kTriWarps = kTriThreads / 32;
 
@@ -199,6 +206,9 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_tridiag(int n, double2* __re
                 double2* br = B + static_cast<int64_t>(r) * n;
                 const double2 ur = upd ? ucur[r] : make_double2(0.0, 0.0), qr = upd ? q[r] : make_double2(0.0, 0.0);
                 double ar = 0.0, ai = 0.0;
+#if KBG_TRI_UNROLL > 1
+#pragma unroll kTriUnroll
+#endif
                 for (int c = lo2 + lane; c < n; c += 32) {
                     double2 b = br[c];
                     if (upd) {
@@ -268,6 +278,7 @@ __global__ void __launch_bounds__(kBtWarps * 32) k_back_transform(int n, int m, 
         const int lo = k + 1;
         const double2* uk = U + static_cast<int64_t>(k) * n;
         double ar = 0.0, ai = 0.0;  // u^H w
+#pragma unroll 4
         for (int r = lo + lane; r < n; r += 32) {
             const double2 x = uk[r], y = w[r];
             ar += x.x * y.x + x.y * y.y;
@@ -280,6 +291,7 @@ __global__ void __launch_bounds__(kBtWarps * 32) k_back_transform(int n, int m, 
         }
         ar /= hk;
         ai /= hk;
+#pragma unroll 4
         for (int r = lo + lane; r < n; r += 32) {
             const double2 x = uk[r];
             double2 y = w[r];
@@ -381,7 +393,8 @@ int launch_hh_tridiagonalize(int n, double* d_B, double* d_p, double* d, double*
     KBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tridiag, kTriThreads, smem));
     if (per_sm < 1) throw Error(KBG_ERR_DIMENSION, "tridiagonalize: n too large for the cooperative kernel");
     // rows per warp: no more CTAs than rows of work keep busy
-    const int grid = std::max(1, std::min(sms, (n + kTriWarps - 1) / kTriWarps));
+    int grid = std::max(1, std::min(sms, (n + kTriWarps - 1) / kTriWarps));
+    if (const char* g = std::getenv("KBG_TRI_GRID")) grid = std::max(1, std::min(sms * per_sm, std::atoi(g)));  // tuning
     TriOut o{d, e, reinterpret_cast<double2*>(u), h, s, reinterpret_cast<double2*>(ph)};
     int nn = n;
     double2* B = reinterpret_cast<double2*>(d_B);
