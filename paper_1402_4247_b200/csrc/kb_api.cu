@@ -257,9 +257,10 @@ kbg::GridArgs grid_args(kbg_ctx* c, int nspin, double dV, const double* in, doub
     return g;
 }
 
-int run_density(kbg_ctx* c, int nspin, const double* d_dm, double* d_rho, cudaStream_t st) {
+int run_density(kbg_ctx* c, int nspin, const double* d_dm, double* d_rho, cudaStream_t st,
+                unsigned long long* chk = nullptr) {
     ensure(c->d_dmr, c->cap_dmr, static_cast<size_t>(nspin) * std::max<int64_t>(1, c->ix.nrep));
-    int n = kbg::launch_dm_repack(c->ix, c->P, nspin, d_dm, c->d_dmr, st);
+    int n = kbg::launch_dm_repack(c->ix, c->P, nspin, d_dm, c->d_dmr, st, chk);
     kbg::GridArgs g = grid_args(c, nspin, 0.0, d_dm, d_rho, true);
     g.dmr = c->d_dmr;
     if (c->persist_ok && c->persist && c->ix.phis) {
@@ -650,9 +651,9 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
         auto rho_half = [&] {
             KBG_CUDA(cudaMemcpyAsync(c->d_in, dm, ndm * sizeof(double), cudaMemcpyHostToDevice, c->stream));
             KBG_CUDA(cudaMemsetAsync(c->d_check, 0, 4 * sizeof(unsigned long long), c->stream));
-            n += kbg::launch_dm_check(c->ix, c->P, nspin, c->d_in, c->d_check, c->stream);
             if (c->nranks > 1) KBG_CUDA(cudaMemsetAsync(c->d_out, 0, npt * sizeof(double), c->stream));
-            n += run_density(c, nspin, c->d_in, rho_map ? rho_map : c->d_out, c->stream);
+            // the DM symmetry check rides along in the repack pass (no separate k_dm_check)
+            n += run_density(c, nspin, c->d_in, rho_map ? rho_map : c->d_out, c->stream, c->d_check);
             if (!rho_map)
                 KBG_CUDA(cudaMemcpyAsync(rho, c->d_out, npt * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         };

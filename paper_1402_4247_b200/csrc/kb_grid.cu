@@ -68,32 +68,81 @@ __global__ void __launch_bounds__(NW * 32, 2) k_density(GridArgs g) {
 // Repacked, pre-scaled DM for the rho kernels (see kb_gridcore.cuh gather_a):
 // canonical pairs only; row i of pair p at roff[p] + i * 16 * ceil(nb/16);
 // column j = 16c + 4s + k stored at position 16c + 4k + s; x2 except (a,a,0).
+// With chk != nullptr the same pass validates the DensityMatrices invariant
+// DM_ba(-R) = DM_ab(R)^T (what k_dm_check does): per canonical
+// pair it compares the block with its mirror block and reduces max|defect|,
+// max|DM| and a non-finite flag into chk[0..2] (one atomic per CTA).
 __global__ void k_dm_repack(SysParams P, int64_t npair, int nspin, int64_t nnz, int64_t nrep,
                             const int32_t* __restrict__ pa, const int32_t* __restrict__ pb,
                             const int32_t* __restrict__ pR, const int64_t* __restrict__ poff,
-                            const int64_t* __restrict__ proff, const double* __restrict__ dm, double* __restrict__ dmr) {
+                            const int64_t* __restrict__ proff, const int32_t* __restrict__ mirror,
+                            const double* __restrict__ dm, double* __restrict__ dmr, unsigned long long* chk) {
     const int lane = threadIdx.x & 31;
     const int64_t p = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
-    if (p >= npair) return;
-    const int a = pa[p], b = pb[p];
-    const int R0 = pR[3 * p], R1 = pR[3 * p + 1], R2 = pR[3 * p + 2];
-    const bool canon = (a != b) ? a < b : (R0 != 0 ? R0 > 0 : (R1 != 0 ? R1 > 0 : R2 >= 0));
-    if (!canon) return;
-    const double fac = (a == b && R0 == 0 && R1 == 0 && R2 == 0) ? 1.0 : 2.0;
-    const int na = P.sp[P.spc[a]].norb, nb = P.sp[P.spc[b]].norb;
-    const int stride = 16 * ((nb + 15) >> 4);
-    for (int s = 0; s < nspin; ++s) {
-        const double* src = dm + s * nnz + poff[p];
-        double* dst = dmr + s * nrep + proff[p];
-        // unrolled so several loads per lane are in flight (a pair block is only a few
-        // iterations; a rolled loop pays the full load latency each time)
+    double dmax = 0.0, amax = 0.0;
+    bool finite = true;
+    bool canon = false;
+    int a = 0, b = 0, R0 = 0, R1 = 0, R2 = 0;
+    if (p < npair) {
+        a = pa[p];
+        b = pb[p];
+        R0 = pR[3 * p];
+        R1 = pR[3 * p + 1];
+        R2 = pR[3 * p + 2];
+        canon = (a != b) ? a < b : (R0 != 0 ? R0 > 0 : (R1 != 0 ? R1 > 0 : R2 >= 0));
+    }
+    if (canon) {
+        const double fac = (a == b && R0 == 0 && R1 == 0 && R2 == 0) ? 1.0 : 2.0;
+        const int na = P.sp[P.spc[a]].norb, nb = P.sp[P.spc[b]].norb;
+        const int stride = 16 * ((nb + 15) >> 4);
+        const int64_t q = chk ? mirror[p] : p;
+        for (int s = 0; s < nspin; ++s) {
+            const double* src = dm + s * nnz + poff[p];
+            const double* srq = dm + s * nnz + poff[q];  // nb x na
+            double* dst = dmr + s * nrep + proff[p];
+            // unrolled so several loads per lane are in flight (a pair block is only a few
+            // iterations; a rolled loop pays the full load latency each time)
 #pragma unroll 4
-        for (int e = lane; e < na * stride; e += 32) {
-            const int i = e / stride, pos = e % stride;
-            const int c = pos >> 4, k = (pos >> 2) & 3, st = pos & 3;
-            const int j = 16 * c + 4 * st + k;
-            dst[e] = j < nb ? fac * src[i * nb + j] : 0.0;
+            for (int e = lane; e < na * stride; e += 32) {
+                const int i = e / stride, pos = e % stride;
+                const int c = pos >> 4, k = (pos >> 2) & 3, st = pos & 3;
+                const int j = 16 * c + 4 * st + k;
+                const double v = j < nb ? src[i * nb + j] : 0.0;
+                dst[e] = fac * v;
+                if (chk && j < nb) {
+                    const double y = srq[j * na + i];
+                    finite &= isfinite(v) && isfinite(y);
+                    dmax = fmax(dmax, fabs(v - y));
+                    amax = fmax(amax, fmax(fabs(v), fabs(y)));
+                }
+            }
         }
+    }
+    if (!chk) return;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+        amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    }
+    finite = __all_sync(0xffffffffu, finite);
+    __shared__ double s_d[32], s_a[32];
+    __shared__ int s_f;
+    if (threadIdx.x == 0) s_f = 1;
+    __syncthreads();
+    if (lane == 0) {
+        s_d[threadIdx.x >> 5] = dmax;
+        s_a[threadIdx.x >> 5] = amax;
+        if (!finite) s_f = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < static_cast<int>(blockDim.x >> 5); ++k) {
+            dmax = fmax(dmax, s_d[k]);
+            amax = fmax(amax, s_a[k]);
+        }
+        atomicMax(chk, static_cast<unsigned long long>(__double_as_longlong(dmax)));
+        atomicMax(chk + 1, static_cast<unsigned long long>(__double_as_longlong(amax)));
+        if (!s_f) atomicMax(chk + 2, 1ull);
     }
 }
 
@@ -257,11 +306,11 @@ int launch_mirror(const DevIndex& ix, const SysParams& sys, int nspin, double* h
 }
 
 int launch_dm_repack(const DevIndex& ix, const SysParams& sys, int nspin, const double* dm, double* dmr,
-                     cudaStream_t st) {
+                     cudaStream_t st, unsigned long long* chk) {
     if (ix.npair == 0) return 0;
     const unsigned grid = static_cast<unsigned>((ix.npair * 32 + 255) / 256);
     k_dm_repack<<<grid, 256, 0, st>>>(sys, ix.npair, nspin, ix.nnz, ix.nrep, ix.pair_a, ix.pair_b, ix.pair_R,
-                                      ix.pair_off, ix.pair_roff, dm, dmr);
+                                      ix.pair_off, ix.pair_roff, ix.pair_mirror, dm, dmr, chk);
     KBG_CUDA(cudaGetLastError());
     return 1;
 }

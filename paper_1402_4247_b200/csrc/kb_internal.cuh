@@ -288,7 +288,7 @@ void free_tasks(DevIndex& ix);
 int launch_density(const GridArgs& g, int64_t nblk_owned, int nwarps, cudaStream_t st);
 int launch_hamiltonian(const GridArgs& g, int64_t nblk_owned, int nwarps, cudaStream_t st);
 int launch_dm_repack(const DevIndex& ix, const SysParams& sys, int nspin, const double* dm, double* dmr,
-                     cudaStream_t st);
+                     cudaStream_t st, unsigned long long* chk = nullptr);
 // Persistent warp-specialized kernels (kb_persist.cu): kPersistProducers
 // producer warps stage block k+1 while kPersistConsumers consumer warps work
 // on block k (two shared-memory buffers). persist_fits() says whether two

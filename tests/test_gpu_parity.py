@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 from paper_1402_4247_b200 import _abi
-from paper_1402_4247_b200.errors import ConfigError, ConsistencyError
+from paper_1402_4247_b200.errors import ConfigError, ConsistencyError, ConvergenceError
 from paper_1402_4247_b200.grid import GridPass
 from paper_1402_4247_b200.system import Fe3O4
 
@@ -201,6 +201,15 @@ def test_grid_pass_matches_separate_calls():
     assert normwise(h, c.o.hamiltonian(c.veff, c.f.dV)) <= TOL
     bad = c.dm.copy()
     bad[0, 1] += 1.0  # pair 0 is (0, 0, R=0) here: break its transpose symmetry off the diagonal
+    with pytest.raises(ConsistencyError):
+        c.gp.grid_pass(bad, c.veff, c.f.dV)
+    bad = c.dm.copy()
+    bad[0, c.gix["pair_off"][len(c.gix["pair_off"]) // 2] + 3] = np.nan  # a non-canonical or canonical pair
+    with pytest.raises(ConvergenceError):
+        c.gp.grid_pass(bad, c.veff, c.f.dV)
+    bad = c.dm.copy()
+    p = int(np.nonzero(c.gix["pair_mirror"] != np.arange(len(c.gix["pair_mirror"])))[0][-1])  # last a != b or R != 0 pair
+    bad[0, c.gix["pair_off"][p]] += 1e-6  # its mirror block no longer matches
     with pytest.raises(ConsistencyError):
         c.gp.grid_pass(bad, c.veff, c.f.dV)
 
