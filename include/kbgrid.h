@@ -256,6 +256,10 @@ int kbg_hamiltonian_allreduce_dev(kbg_ctx* ctx, int nspin, const double* d_veff,
  * the H of that call is invalid), else KBG_OK. Clears the flag. kbg_grid_pass
  * on a sharded context checks it itself. */
 int kbg_comm_check(kbg_ctx* ctx);
+/* Timing aid: with KBG_COMM_TIMING set in the environment at kbg_comm_open, the
+ * phase times (ns from the reduce kernel's start) of the last exchange: all
+ * partials ready, slice reduced, copy kernel start, all slices landed, done. */
+int kbg_comm_timing(kbg_ctx* ctx, double* out5);
 
 /* ---- Formats either side of the grid pass ----------------
  * The pair-sparse blocks of kbg_index (grid-pass DM input, H output) against

@@ -122,6 +122,7 @@ KBGRID_SYMBOLS = [
     ("kbg_comm_handle", _I, [_P, _P]),
     ("kbg_comm_open", _I, [_P, _P]),
     ("kbg_comm_check", _I, [_P]),
+    ("kbg_comm_timing", _I, [_P, _DP]),
     ("kbg_hamiltonian_allreduce_dev", _I, [_P, _I, _P, _D, _P, _P]),
     ("kbg_offsets", _I, [_P, C.POINTER(_I), C.POINTER(C.c_int32)]),
     ("kbg_to_realspace", _I, [_P, _DP, _DP]),

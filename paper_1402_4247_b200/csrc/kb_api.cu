@@ -1207,6 +1207,7 @@ int kbg_comm_open(kbg_ctx* c, const void* handles) {
                 cf[p] = (a != b) ? a < b : (R0 != 0 ? R0 > 0 : (R1 != 0 ? R1 > 0 : R2 >= 0));
             }
             if (c->d_pairtab) cudaFree(c->d_pairtab);
+    if (c->comm.tstamp) cudaFree(c->comm.tstamp);
             c->d_pairtab = nullptr;
             KBG_CUDA(cudaMalloc(&c->d_pairtab, std::max<size_t>(1, 9 * np)));
             if (np) {
@@ -1218,6 +1219,10 @@ int kbg_comm_open(kbg_ctx* c, const void* handles) {
             cm.pair_nb = reinterpret_cast<const int32_t*>(c->d_pairtab + 4 * np);
             cm.pair_canon = reinterpret_cast<const uint8_t*>(c->d_pairtab + 8 * np);
         }
+        if (std::getenv("KBG_COMM_TIMING") && !cm.tstamp) {
+            KBG_CUDA(cudaMalloc(&cm.tstamp, 8 * sizeof(unsigned long long)));
+            KBG_CUDA(cudaMemset(cm.tstamp, 0, 8 * sizeof(unsigned long long)));
+        }
         cm.el0 = c->d_canon;
         cm.el1 = c->d_canon + e0.size();
         cm.elm = reinterpret_cast<const uint8_t*>(c->d_canon + 2 * e0.size());
@@ -1226,6 +1231,20 @@ int kbg_comm_open(kbg_ctx* c, const void* handles) {
     });
 }
 
+
+// Timing aid (KBG_COMM_TIMING set at kbg_comm_open): the last exchange's phase stamps in ns relative to
+// the reduce kernel's start: [0] all partials ready, [1] slice reduced and signalled, [2] copy kernel start,
+// [3] all slices landed, [4] copy + mirror done. Returns KBG_ERR_CONFIG when timing is off.
+int kbg_comm_timing(kbg_ctx* c, double* out5) {
+    if (!c || !out5 || !c->comm.tstamp) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        KBG_CUDA(cudaSetDevice(c->device));
+        unsigned long long t[8];
+        KBG_CUDA(cudaMemcpy(t, c->comm.tstamp, sizeof(t), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < 5; ++i) out5[i] = static_cast<double>(t[i + 1]) - static_cast<double>(t[0]);
+        KBG_CUDA(cudaMemset(c->comm.tstamp, 0, sizeof(t)));
+    });
+}
 
 int kbg_comm_check(kbg_ctx* c) {
     if (!c) return KBG_ERR_CONFIG;

@@ -6,16 +6,17 @@
 // then, on each rank r:
 //   1. signals "partials ready" to every peer and waits for all peers
 //      (flags in peer memory, system-scope release/acquire);
-//   2. for the canonical pairs of its slice (contiguous, balanced by size)
-//      sums the N partials in rank order (same bits on every rank), applies
-//      the mirror H_ba(-R) = H_ab(R)^T (and the (a,a,0) symmetrization of
-//      k_mirror), and stores the result into every rank's X -- a
-//      reduce-scatter + all-gather + mirror in one pass over NVLink;
-//   3. the last CTA signals "slice written".
-// A second small kernel waits for every peer's slice and copies X_self into
-// the caller's H. Per rank this moves ~2 |H| over NVLink instead of NCCL's
-// all-reduce plus a separate mirror kernel; a slice element is read and
-// written only by its owner, so X can be updated in place.
+//   2. for the canonical entries of its slice (contiguous, balanced by size)
+//      sums the partials of the ranks whose shard touches the pair (owner
+//      masks; the others are exact zeros) in rank order (same bits on every
+//      rank), symmetrizes the (a, a, 0) blocks, and stores each result into
+//      every rank's buffer -- a reduce-scatter + all-gather in one pass over
+//      NVLink; the last CTA signals "slice written";
+//   3. once every rank's slice has landed, copies X_r into the caller's H and
+//      fills the mirror blocks H_ba(-R) = H_ab(R)^T locally (warp per pair).
+// All CTAs fit on the GPU at once (4 per SM, no shared memory) and nothing they
+// wait for depends on a later kernel, so the waits cannot deadlock; every wait
+// gives up after 10 s anyway (error word, kbg_comm_check).
 #include "kb_internal.cuh"
 
 namespace kbg {
@@ -63,6 +64,34 @@ __device__ void signal_flags(const CommArgs& c, unsigned long long epoch) {
     for (int k = 0; k < c.nranks; ++k) st_release_sys(c.flags[k] + c.rank, epoch);
 }
 
+// Copy-out fused with the mirror: one warp per canonical pair block copies the
+// block from the exchange buffer into the caller's H and writes its transpose
+// into the mirror block H_ba(-R) (the (a, a, 0) blocks arrive symmetrized from
+// the reduce and are copied as is). Replaces a full-array copy plus k_mirror.
+__device__ __forceinline__ void copy_mirror(const CommArgs& c, int64_t npair, int nspin, int64_t nnz,
+                                            const int64_t* __restrict__ poff, const int32_t* __restrict__ mirror,
+                                            double* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const double* x = c.x[c.rank];
+    for (int64_t p = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; p < npair;
+         p += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+        if (!c.pair_canon[p]) continue;  // written by its canonical partner
+        const int na = c.pair_na[p], nb = c.pair_nb[p];
+        const int64_t q = mirror[p];
+        for (int s = 0; s < nspin; ++s) {
+            const double* src = x + s * nnz + poff[p];
+            double* dst = out + s * nnz + poff[p];
+            double* dq = out + s * nnz + poff[q];
+#pragma unroll 4
+            for (int e = lane; e < na * nb; e += 32) {
+                const double v = src[e];
+                dst[e] = v;
+                if (q != p) dq[(e % nb) * na + e / nb] = v;
+            }
+        }
+    }
+}
+
 // One thread per element of this rank's slice, with the element's two
 // offsets precomputed on the host (el0: the canonical entry, el1: its mirror
 // entry -- or the transposed entry of an (a,a,0) block, flagged by bit 31 --
@@ -70,9 +99,13 @@ __device__ void signal_flags(const CommArgs& c, unsigned long long epoch) {
 // all N partials in flight at once, then the stores.
 __global__ void __launch_bounds__(256) k_reduce_mirror(CommArgs c, int nspin, int64_t nnz, int64_t ne,
                                                        const int32_t* __restrict__ el0,
-                                                       const int32_t* __restrict__ el1, unsigned long long epoch) {
+                                                       const int32_t* __restrict__ el1, unsigned long long epoch,
+                                                       int64_t npair, const int64_t* __restrict__ poff,
+                                                       const int32_t* __restrict__ pmirror, double* __restrict__ out) {
+    if (c.tstamp && blockIdx.x == 0 && threadIdx.x == 0) c.tstamp[0] = globaltimer();
     if (blockIdx.x == 0 && threadIdx.x == 0) signal_flags(c, epoch);
     wait_flags(c, epoch);
+    if (c.tstamp && threadIdx.x == 0) atomicMax(c.tstamp + 1, globaltimer());
     for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < ne * nspin;
          t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int s = static_cast<int>(t / ne);
@@ -114,8 +147,19 @@ __global__ void __launch_bounds__(256) k_reduce_mirror(CommArgs c, int nspin, in
         const unsigned int done = atomicAdd(c.counter, 1u);
         if (done == gridDim.x - 1) {
             *c.counter = 0u;
+            if (c.tstamp) c.tstamp[2] = globaltimer();
             signal_flags(c, epoch + 1);
         }
+    }
+    if (!out) return;
+    // fused copy-out + mirror (all CTAs are resident): wait until every rank's slice has landed here
+    if (c.tstamp && blockIdx.x == 0 && threadIdx.x == 0) c.tstamp[3] = globaltimer();
+    wait_flags(c, epoch + 1);
+    if (c.tstamp && threadIdx.x == 0) atomicMax(c.tstamp + 4, globaltimer());
+    copy_mirror(c, npair, nspin, nnz, poff, pmirror, out);
+    if (c.tstamp) {
+        __syncthreads();
+        if (threadIdx.x == 0) atomicMax(c.tstamp + 5, globaltimer());
     }
 }
 
@@ -130,40 +174,6 @@ __global__ void __launch_bounds__(256) k_comm_copy_out(CommArgs c, int64_t n, do
     if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) out[n - 1] = c.x[c.rank][n - 1];
 }
 
-// Copy-out fused with the mirror: one warp per canonical pair block waits for
-// every peer's slice, copies the block from the exchange buffer into the
-// caller's H and writes its transpose into the mirror block H_ba(-R) (the
-// (a, a, 0) blocks arrive symmetrized from the reduce and are copied as is).
-// Replaces a full-array copy plus k_mirror (two kernels, two passes over H).
-__global__ void __launch_bounds__(256) k_comm_copy_mirror(CommArgs c, int64_t npair, int nspin, int64_t nnz,
-                                                          const int32_t* __restrict__ norb_a,
-                                                          const int32_t* __restrict__ norb_b,
-                                                          const int64_t* __restrict__ poff,
-                                                          const int32_t* __restrict__ mirror,
-                                                          const uint8_t* __restrict__ canon, double* __restrict__ out,
-                                                          unsigned long long epoch) {
-    wait_flags(c, epoch);
-    const int lane = threadIdx.x & 31;
-    const double* x = c.x[c.rank];
-    for (int64_t p = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; p < npair;
-         p += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
-        if (!canon[p]) continue;  // written by its canonical partner
-        const int na = norb_a[p], nb = norb_b[p];
-        const int64_t q = mirror[p];
-        for (int s = 0; s < nspin; ++s) {
-            const double* src = x + s * nnz + poff[p];
-            double* dst = out + s * nnz + poff[p];
-            double* dq = out + s * nnz + poff[q];
-#pragma unroll 4
-            for (int e = lane; e < na * nb; e += 32) {
-                const double v = src[e];
-                dst[e] = v;
-                if (q != p) dq[(e % nb) * na + e / nb] = v;
-            }
-        }
-    }
-}
-
 }  // namespace
 
 int launch_reduce_mirror(const CommArgs& c, const DevIndex& ix, const SysParams& sys, int nspin, double* d_out,
@@ -171,17 +181,17 @@ int launch_reduce_mirror(const CommArgs& c, const DevIndex& ix, const SysParams&
     int dev = 0, sms = 0;
     KBG_CUDA(cudaGetDevice(&dev));
     KBG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    // all CTAs must be co-resident (they spin on flags): at most one wave
-    const unsigned grid = static_cast<unsigned>(sms) * 2;
-    k_reduce_mirror<<<grid, 256, 0, st>>>(c, nspin, ix.nnz, c.ne, c.el0, c.el1, epoch);
-    KBG_CUDA(cudaGetLastError());
-    if (c.pair_na) {
-        k_comm_copy_mirror<<<static_cast<unsigned>(sms) * 4, 256, 0, st>>>(c, ix.npair, nspin, ix.nnz, c.pair_na,
-                                                                          c.pair_nb, ix.pair_off, ix.pair_mirror,
-                                                                          c.pair_canon, d_out, epoch + 1);
+    // all CTAs fit at once (4 per SM x 256 threads, <= 64 registers): the copy-out phase of large H
+    // wants the warps (2 per SM measured 4 % slower at 448 atoms on 4 GPUs)
+    const unsigned grid = static_cast<unsigned>(sms) * 4;
+    if (c.pair_na) {  // reduce, then (same kernel) copy-out + mirror once every slice has landed
+        k_reduce_mirror<<<grid, 256, 0, st>>>(c, nspin, ix.nnz, c.ne, c.el0, c.el1, epoch, ix.npair, ix.pair_off,
+                                              ix.pair_mirror, d_out);
         KBG_CUDA(cudaGetLastError());
-        return 2;
+        return 1;
     }
+    k_reduce_mirror<<<grid, 256, 0, st>>>(c, nspin, ix.nnz, c.ne, c.el0, c.el1, epoch, 0, nullptr, nullptr, nullptr);
+    KBG_CUDA(cudaGetLastError());
     const int64_t n = static_cast<int64_t>(nspin) * ix.nnz;
     k_comm_copy_out<<<static_cast<unsigned>(sms) * 4, 256, 0, st>>>(c, n, d_out, epoch + 1);
     KBG_CUDA(cudaGetLastError());

@@ -249,6 +249,7 @@ struct CommArgs {
     const int32_t* pair_na = nullptr;
     const int32_t* pair_nb = nullptr;
     const uint8_t* pair_canon = nullptr;
+    unsigned long long* tstamp = nullptr;  // KBG_COMM_TIMING: globaltimer stamps of the exchange phases [8]
 };
 // Per pair, the ranks (bit k) whose block range [bounds[k], bounds[k + 1]) holds
 // a canonical (block, cover pair) work item of that pair.

@@ -104,6 +104,18 @@ def main(cfg="cubic56_200Ry"):
     acc_ranks = [None] * world
     dist.all_gather_object(acc_ranks, round(local_ms(lambda: gp.hamiltonian_accumulate_dev(v, f.dV, h_nccl, st)), 4))
     t_p2p = timeit(p2p)
+    phases = None
+    if os.environ.get("KBG_COMM_TIMING"):
+        import ctypes as C
+
+        p2p()
+        torch.cuda.synchronize()
+        buf = (C.c_double * 5)()
+        if gp._lib.kbg_comm_timing(gp.handle, buf) == 0:
+            phases = [round(x / 1e3, 2) for x in buf]  # us from the reduce kernel's start
+        allp = [None] * world
+        dist.all_gather_object(allp, phases)
+        phases = allp
     t_nccl = timeit(nccl)
     t_acc = timeit(lambda: gp.hamiltonian_accumulate_dev(v, f.dV, h_nccl, st))
     if rank == 0:
@@ -118,6 +130,7 @@ def main(cfg="cubic56_200Ry"):
                           "h_ms_p2p": round(t_p2p, 4), "h_ms_nccl_incl_mirror": round(t_nccl, 4),
                           "h_ms_accumulate_only": round(t_acc, 4), "accumulate_ms_per_rank": acc_ranks,
                           "grid_pass_h_vs_p2p": d_gp, "grid_pass_rho_sum_vs_single_gpu": d_rho,
+                          "exchange_phases_us_per_rank": phases,
                           "note": "H partials use atomics: not bitwise repeatable run to run (single GPU neither)",
                           "ok": bool(same_bits and d_nccl <= 1e-14 and d_full <= 1e-13 and d_gp <= 1e-14
                                      and d_rho == 0.0)}), flush=True)
