@@ -1,7 +1,9 @@
 """ctypes wrapper of oracle/liboracle.so -- TEST INFRASTRUCTURE.
 
-Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline legs may use
-this module, and only as the checker / the timed CPU baseline. PARITY
+Only tests/, __graft_entry__.smoke(), bench.py's CPU-baseline legs and offline
+analysis tools (tools/padding_model.py, tools/crossover_model.py: index statistics)
+use this module -- as the checker, the timed CPU baseline or an index source; never
+the package. PARITY
 UNPINNED: see oracle/oracle.h.
 """
 from __future__ import annotations
