@@ -268,7 +268,13 @@ __global__ void k_bp_count(SysParams P, int64_t nblock, const int32_t* __restric
             const uint64_t both = mi & cov_mask[cj];
             if (both) {
                 ++cnt;
-                cost += static_cast<long long>(na) * P.sp[P.spc[cov_atom[cj]]].norb * __popcll(both);
+                // padded tile work, as the DMMA kernels execute it: rows and columns in 8-orbital tiles,
+                // points in 1x2x2 quads (weights the shard split and the heaviest-first order)
+                uint32_t nq = 0;
+#pragma unroll
+                for (int q = 0; q < 16; ++q) nq += ((both >> (4 * q)) & 0xFull) != 0;
+                const int nb = P.sp[P.spc[cov_atom[cj]]].norb;
+                cost += static_cast<long long>((na + 7) & ~7) * ((nb + 7) & ~7) * 4 * nq;
             }
         }
     }

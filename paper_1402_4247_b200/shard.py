@@ -36,7 +36,8 @@ def partition(block_cost: np.ndarray, nranks: int) -> list[tuple[int, int]]:
 
 def block_costs(index: dict, norb_of_atom: np.ndarray) -> np.ndarray:
     """Per-block cost = sum over canonical cover pairs (ci <= cj) sharing points
-    of n_a * n_b * |mask_ci & mask_cj| (the device's blk_cost)."""
+    of ceil8(n_a) * ceil8(n_b) * 4 * (1x2x2 quads of mask_ci & mask_cj): the padded
+    tile work of the DMMA kernels (the device's blk_cost, kb_index.cu:k_bp_count)."""
     bp, ca, cm = index["blk_ptr"], index["cov_atom"], index["cov_mask"].astype(np.uint64)
     out = np.zeros(index["nblock"], dtype=np.int64)
     for b in range(index["nblock"]):
@@ -47,6 +48,8 @@ def block_costs(index: dict, norb_of_atom: np.ndarray) -> np.ndarray:
             for j in range(i, c1):
                 both = int(cm[i]) & int(cm[j])
                 if both:
-                    tot += ni * int(norb_of_atom[ca[j]]) * bin(both).count("1")
+                    nq = sum(1 for q in range(16) if (both >> (4 * q)) & 0xF)
+                    nj = int(norb_of_atom[ca[j]])
+                    tot += ((ni + 7) & ~7) * ((nj + 7) & ~7) * 4 * nq
         out[b] = tot
     return out
