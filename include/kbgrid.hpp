@@ -129,6 +129,19 @@ public:
         return h;
     }
 
+    // One SCF grid pass (kbg_grid_pass): rho from dm and h from veff, the two halves overlapped on two
+    // streams; pinned host buffers are read / written in place by the kernels.
+    std::pair<std::vector<double>, std::vector<double>> grid_pass(const std::vector<double>& dm,
+                                                                  const std::vector<double>& veff, double dV,
+                                                                  int nspin = 1) const {
+        const kbg_index ix = view();
+        if (static_cast<int64_t>(dm.size()) != nspin * ix.nnz || static_cast<int64_t>(veff.size()) != nspin * ix.npts)
+            throw DimensionError("grid_pass: dm must hold nspin*nnz and veff nspin*npts values");
+        std::vector<double> rho(static_cast<size_t>(nspin) * ix.npts), h(static_cast<size_t>(nspin) * ix.nnz);
+        check(kbg_grid_pass(ctx_, nspin, dm.data(), veff.data(), dV, rho.data(), h.data()), "kbg_grid_pass");
+        return {std::move(rho), std::move(h)};
+    }
+
     // Device-pointer variants (stream = cudaStream_t).
     void density_dev(int nspin, const double* d_dm, double* d_rho, void* stream = nullptr) const {
         check(kbg_density_dev(ctx_, nspin, d_dm, d_rho, stream), "kbg_density_dev");
@@ -151,5 +164,38 @@ private:
     }
     kbg_ctx* ctx_ = nullptr;
 };
+
+// ---- Eigen_HH (kband::eigen_hh / solve_tridiag, householder.hpp:78-80, tridiag.hpp:18-21) ----
+struct EigenResult {
+    std::vector<double> eigenvalues;   // ascending
+    std::vector<double> eigenvectors;  // [n][n] complex interleaved (re, im), columns; empty if not wanted
+};
+
+// a: [n][n] Hermitian, complex interleaved row-major; the whole pipeline device-resident.
+inline EigenResult eigen_hh(int64_t n, const std::vector<double>& a, bool want_vectors = true) {
+    if (static_cast<int64_t>(a.size()) != 2 * n * n) throw DimensionError("eigen_hh: a must hold 2*n*n doubles");
+    EigenResult r;
+    r.eigenvalues.resize(n);
+    if (want_vectors) r.eigenvectors.resize(2 * n * n);
+    const int st = kbg_hh_eigen(n, a.data(), want_vectors ? 1 : 0, r.eigenvalues.data(),
+                                want_vectors ? r.eigenvectors.data() : nullptr);
+    if (st != KBG_OK) throw_status(st, std::string("kbg_hh_eigen: ") + kbg_hh_last_error());
+    return r;
+}
+
+// Real symmetric tridiagonal (d [n], e [n-1]); eigenvectors as the columns of a real [n][n].
+inline std::pair<std::vector<double>, std::vector<double>> solve_tridiag(const std::vector<double>& d,
+                                                                         const std::vector<double>& e,
+                                                                         bool want_vectors = true) {
+    const int64_t n = static_cast<int64_t>(d.size());
+    if (n < 1 || static_cast<int64_t>(e.size()) + 1 != n)
+        throw DimensionError("solve_tridiag: off-diagonal length must be n-1");
+    std::vector<double> w(n), z(want_vectors ? n * n : 0), ee = e;
+    if (ee.empty()) ee.push_back(0.0);
+    const int st = kbg_tridiag_solve(n, d.data(), ee.data(), want_vectors ? 1 : 0, w.data(),
+                                     want_vectors ? z.data() : nullptr);
+    if (st != KBG_OK) throw_status(st, std::string("kbg_tridiag_solve: ") + kbg_hh_last_error());
+    return {std::move(w), std::move(z)};
+}
 
 }  // namespace kbg

@@ -49,6 +49,45 @@ int main() {
         std::printf("electrons: grid %.15f  Tr(DM S) %.15f\nenergy:    grid %.15f  Tr(DM H) %.15f\n", ne, tr, e, trh);
         if (std::fabs(ne - tr) > 1e-10 * std::fmax(1.0, std::fabs(ne))) return 3;
         if (std::fabs(e - trh) > 1e-10 * std::fmax(1.0, std::fabs(e))) return 4;
+        // the one-call SCF drop-in gives the same rho bitwise and H within atomics' rounding
+        const auto [rho2, H2] = gp.grid_pass(dm, veff, dV);
+        for (int64_t p = 0; p < ix.npts; ++p)
+            if (rho2[p] != rho[p]) return 7;
+        double hmax = 0.0, hdiff = 0.0;
+        for (int64_t p = 0; p < ix.nnz; ++p) {
+            hmax = std::fmax(hmax, std::fabs(H[p]));
+            hdiff = std::fmax(hdiff, std::fabs(H2[p] - H[p]));
+        }
+        if (hdiff > 1e-13 * hmax) return 8;
+        // Eigen_HH end to end on a small Hermitian matrix: residual || A c - eps c ||
+        {
+            const int64_t n = 40;
+            std::vector<double> a(2 * n * n);
+            for (int64_t i = 0; i < n; ++i)
+                for (int64_t j = 0; j <= i; ++j) {
+                    const double re = std::cos(0.37 * (i + 1) * (j + 2)), im = i == j ? 0.0 : std::sin(0.11 * (i + 3) * j);
+                    a[2 * (i * n + j)] = re;
+                    a[2 * (i * n + j) + 1] = im;
+                    a[2 * (j * n + i)] = re;
+                    a[2 * (j * n + i) + 1] = -im;
+                }
+            const kbg::EigenResult er = kbg::eigen_hh(n, a);
+            double res = 0.0;
+            for (int64_t k = 0; k < n; ++k)
+                for (int64_t i = 0; i < n; ++i) {
+                    double sr = -er.eigenvalues[k] * er.eigenvectors[2 * (i * n + k)];
+                    double si = -er.eigenvalues[k] * er.eigenvectors[2 * (i * n + k) + 1];
+                    for (int64_t j = 0; j < n; ++j) {
+                        const double ar = a[2 * (i * n + j)], ai = a[2 * (i * n + j) + 1];
+                        const double cr = er.eigenvectors[2 * (j * n + k)], ci = er.eigenvectors[2 * (j * n + k) + 1];
+                        sr += ar * cr - ai * ci;
+                        si += ar * ci + ai * cr;
+                    }
+                    res = std::fmax(res, std::hypot(sr, si));
+                }
+            std::printf("eigen_hh n=%lld: max residual %.3e\n", static_cast<long long>(n), res);
+            if (res > 1e-10 * n) return 9;
+        }
         bool threw = false;
         try {
             gp.density(std::vector<double>(3));
