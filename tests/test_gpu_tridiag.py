@@ -83,3 +83,18 @@ def test_eigen_hh_with_gpu_solver(n):
     assert np.abs(w - wr).max() <= 1e-11 * nrm
     assert np.linalg.norm(a @ c - c * w) <= 1e-9 * nrm
     assert np.abs(c.conj().T @ c - np.eye(n)).max() <= 1e-9
+
+
+def test_eigen_hh_small_and_diagonal():
+    """kbg_hh_eigen edge cases: 1x1, 2x2, and a diagonal matrix (every Householder stage skipped)."""
+    w1, c1 = E.eigen_hh(np.array([[2.5 + 0j]]))
+    assert np.array_equal(w1, [2.5]) and abs(abs(c1[0, 0]) - 1.0) <= 1e-15
+    a2 = np.array([[1.0, 2.0 - 1.0j], [2.0 + 1.0j, -3.0]])
+    w2, c2 = E.eigen_hh(a2)
+    assert np.abs(w2 - np.linalg.eigvalsh(a2)).max() <= 1e-13
+    assert np.abs(a2 @ c2 - c2 * w2).max() <= 1e-13
+    dg = np.diag([3.0, -1.0, 2.0, 0.5, -1.0]).astype(np.complex128)
+    wd, cd = E.eigen_hh(dg)
+    assert np.allclose(wd, [-1.0, -1.0, 0.5, 2.0, 3.0], atol=1e-15)
+    assert np.abs(dg @ cd - cd * wd).max() <= 1e-14
+    assert np.abs(cd.conj().T @ cd - np.eye(5)).max() <= 1e-13
