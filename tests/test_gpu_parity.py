@@ -230,7 +230,7 @@ def test_device_api_matches_host_api():
     assert normwise(h.cpu().numpy(), c.gp.hamiltonian(c.veff, c.f.dV)) <= 1e-14
 
 
-@pytest.mark.parametrize("name", ["sweep56_100Ry", "sweep56_250Ry"])
+@pytest.mark.parametrize("name", ["sweep56_100Ry", "sweep56_250Ry", "sweep56_400Ry"])
 def test_cutoff_sweep_parity(name):
     """Config 5 (grid-cutoff sweep) end points: coarser and finer grids than configs[1]."""
     c = case(name)
