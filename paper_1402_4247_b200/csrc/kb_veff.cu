@@ -70,6 +70,11 @@ __device__ void pw92(double n, double zeta, double& eps, double& vu, double& vd)
     const double rs = cbrt(3.0 / (4.0 * kPi * n)), sr = sqrt(rs);
     double e0, d0, e1, d1, ma, dma;
     pw92_g(rs, sr, 0.031091, 0.21370, 7.5957, 3.5876, 1.6382, 0.49294, e0, d0);
+    if (zeta == 0.0) {  // unpolarized: f(0) = f'(0) = 0, the other two fits drop out (same bits)
+        eps = e0;
+        vu = vd = e0 - rs / 3.0 * d0;
+        return;
+    }
     pw92_g(rs, sr, 0.015545, 0.20548, 14.1189, 6.1977, 3.3662, 0.62517, e1, d1);
     pw92_g(rs, sr, 0.016887, 0.11125, 10.357, 3.6231, 0.88026, 0.49671, ma, dma);
     const double ac = -ma, dac = -dma, fz0 = 1.709921;
