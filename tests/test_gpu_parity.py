@@ -260,6 +260,29 @@ def test_large_config_identities():
     assert abs(ne - tr) <= 1e-10 * max(1.0, abs(ne))
 
 
+def test_largest_config_identities():
+    """1512-atom 3x3x3 supercell at full size (config 5, 216^3 points): electron count
+    sum rho dV = sum DM.S and energy sum rho V dV = sum DM.H over the pair-sparse blocks (both
+    orientations stored), and H_ba(-R) = H_ab(R)^T on a sample of the ~118 k pairs."""
+    f = Fe3O4.config("super1512_200Ry")
+    gp = GridPass(f.system)
+    ix = gp.build_index()
+    dm = f.dm(ix)
+    veff = f.veff()
+    rho = gp.density(dm)[0]
+    S = gp.hamiltonian(np.ones((1, f.system.npts)), f.dV)[0]
+    H = gp.hamiltonian(veff, f.dV)[0]
+    ne, e = rho.sum() * f.dV, float(np.dot(rho, veff[0])) * f.dV
+    assert abs(ne - float(np.dot(dm[0], S))) <= 1e-10 * abs(ne)
+    assert abs(e - float(np.dot(dm[0], H))) <= 1e-10 * np.abs(rho * veff[0]).sum() * f.dV
+    norb = f.system.norb_of_atom()
+    off, mir = ix["pair_off"], ix["pair_mirror"]
+    for p in range(0, len(mir), 97):
+        na, nb = norb[ix["pair_a"][p]], norb[ix["pair_b"][p]]
+        q = mir[p]
+        assert np.array_equal(H[off[p]:off[p + 1]].reshape(na, nb), H[off[q]:off[q + 1]].reshape(nb, na).T)
+
+
 @pytest.mark.parametrize("name", ["sweep56_100Ry", "cubic56_200Ry", "super448_200Ry"])
 def test_plan_uses_task_queues(name):
     """The persistent kernels with both task queues (schedule 3) fit shared memory on the sweep's
