@@ -314,15 +314,32 @@ struct Oracle {
         X.built = true;
     }
 
+    // Pair id of covers (ci, cj): binary search of (a, b, R) in the lexicographically sorted pair list.
     int64_t lookup_pair(int ci, int cj, int64_t blk) const {
         const Index& X = idx;
-        int R[3];
-        for (int c = 0; c < 3; ++c) R[c] = X.cov_R[3 * cj + c] - X.cov_R[3 * ci + c];
-        auto it = X.pair_id.find(std::make_tuple(X.cov_atom[ci], X.cov_atom[cj], R[0], R[1], R[2]));
-        if (it == X.pair_id.end())
+        const int key[5] = {X.cov_atom[ci], X.cov_atom[cj], X.cov_R[3 * cj] - X.cov_R[3 * ci],
+                            X.cov_R[3 * cj + 1] - X.cov_R[3 * ci + 1], X.cov_R[3 * cj + 2] - X.cov_R[3 * ci + 2]};
+        auto less = [&](int64_t p) {  // pair p < key
+            const int v[5] = {X.pair_a[p], X.pair_b[p], X.pair_R[3 * p], X.pair_R[3 * p + 1], X.pair_R[3 * p + 2]};
+            for (int c = 0; c < 5; ++c)
+                if (v[c] != key[c]) return v[c] < key[c];
+            return false;
+        };
+        int64_t lo = 0, hi = static_cast<int64_t>(X.pair_a.size());
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) / 2;
+            if (less(mid))
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        const bool hit = lo < static_cast<int64_t>(X.pair_a.size()) && X.pair_a[lo] == key[0] &&
+                         X.pair_b[lo] == key[1] && X.pair_R[3 * lo] == key[2] && X.pair_R[3 * lo + 1] == key[3] &&
+                         X.pair_R[3 * lo + 2] == key[4];
+        if (!hit)
             throw Error(KBG_ERR_CONSISTENCY, "block " + std::to_string(blk) + ": covers " + std::to_string(ci) +
                                                  "," + std::to_string(cj) + " share points but form no pair");
-        return it->second;
+        return lo;
     }
 
     // ---- G2 orbitals ------------------------------------------------------
@@ -406,7 +423,12 @@ struct Oracle {
         return (static_cast<int64_t>(i) * N[1] + j) * N[2] + k;
     }
 
-    // ---- G3 density: rho(p) = sum_{c1,c2 ∋ p} phi_c1^T DM(c1,c2) phi_c2 -------
+    // ---- G3 density: rho(s) = sum_{ci,cj ∋ s} phi_ci(s)^T DM(ci,cj) phi_cj(s) ---
+    // Per block and row cover ci: Y_ci(s) = sum_cj DM(ci,cj) phi_cj(s) over the
+    // covers cj sharing points with ci (all 64 slots at once: phi is exactly 0
+    // outside a cover's mask, so the extra terms are exact zeros), then
+    // rho(s) += sum_i phi_ci,i(s) Y_ci,i(s). Full (ci, cj) range, no symmetry
+    // used. Blocks write disjoint points: bitwise independent of the thread count.
     void density(int nspin, const double* dm, double* rho, int threads, int64_t blo, int64_t bhi) const {
         const Index& X = idx;
         const int64_t npts = static_cast<int64_t>(N[0]) * N[1] * N[2];
@@ -415,88 +437,138 @@ struct Oracle {
         parallel_for(bhi - blo, threads, [&](int64_t b0, int64_t b1) {
             std::vector<double> phi;
             std::vector<int> row0;
+            std::vector<int64_t> off;
+            double y[KBG_MAX_ORB_PER_ATOM][64];
+            double acc[64];
             for (int64_t b = blo + b0; b < blo + b1; ++b) {
                 const int c0 = X.blk_ptr[b], c1 = X.blk_ptr[b + 1];
                 if (c0 == c1) continue;
                 block_phi(b, phi, row0);
                 const int nc = c1 - c0;
-                std::vector<int64_t> off(static_cast<size_t>(nc) * nc, -1);
+                off.assign(static_cast<size_t>(nc) * nc, -1);
                 for (int i = 0; i < nc; ++i)
                     for (int j = 0; j < nc; ++j)
                         if (X.cov_mask[c0 + i] & X.cov_mask[c0 + j]) off[i * nc + j] = X.pair_off[lookup_pair(c0 + i, c0 + j, b)];
-                for (int s = 0; s < 64; ++s) {
-                    bool valid;
-                    const int64_t pt = point_of(b, s, &valid);
-                    if (!valid) continue;
-                    for (int sp = 0; sp < nspin; ++sp) {
-                        const double* D = dm + sp * nnz;
-                        double acc = 0.0;
-                        for (int i = 0; i < nc; ++i) {
-                            if (!((X.cov_mask[c0 + i] >> s) & 1)) continue;
-                            const int na = spec[species[X.cov_atom[c0 + i]]].norb;
-                            for (int j = 0; j < nc; ++j) {
-                                if (!((X.cov_mask[c0 + j] >> s) & 1)) continue;
-                                const int nb = spec[species[X.cov_atom[c0 + j]]].norb;
-                                const double* blk = D + off[i * nc + j];
-                                for (int ii = 0; ii < na; ++ii) {
-                                    double dot = 0.0;
-                                    for (int jj = 0; jj < nb; ++jj) dot += blk[ii * nb + jj] * phi[static_cast<size_t>(row0[j] + jj) * 64 + s];
-                                    acc += phi[static_cast<size_t>(row0[i] + ii) * 64 + s] * dot;
+                for (int sp = 0; sp < nspin; ++sp) {
+                    const double* D = dm + sp * nnz;
+                    for (int s = 0; s < 64; ++s) acc[s] = 0.0;
+                    for (int i = 0; i < nc; ++i) {
+                        const int na = spec[species[X.cov_atom[c0 + i]]].norb;
+                        for (int ii = 0; ii < na; ++ii)
+                            for (int s = 0; s < 64; ++s) y[ii][s] = 0.0;
+                        for (int j = 0; j < nc; ++j) {
+                            if (off[i * nc + j] < 0) continue;
+                            const int nb = spec[species[X.cov_atom[c0 + j]]].norb;
+                            const double* blk = D + off[i * nc + j];
+                            for (int ii = 0; ii < na; ++ii)
+                                for (int jj = 0; jj < nb; ++jj) {
+                                    const double d = blk[ii * nb + jj];
+                                    const double* pj = &phi[static_cast<size_t>(row0[j] + jj) * 64];
+                                    for (int s = 0; s < 64; ++s) y[ii][s] += d * pj[s];
                                 }
-                            }
                         }
-                        rho[sp * npts + pt] = acc;
+                        for (int ii = 0; ii < na; ++ii) {
+                            const double* pi = &phi[static_cast<size_t>(row0[i] + ii) * 64];
+                            for (int s = 0; s < 64; ++s) acc[s] += pi[s] * y[ii][s];
+                        }
+                    }
+                    for (int s = 0; s < 64; ++s) {
+                        bool valid;
+                        const int64_t pt = point_of(b, s, &valid);
+                        if (valid) rho[sp * npts + pt] = acc[s];
                     }
                 }
             }
         });
     }
 
-    // ---- G4 hamiltonian: all ordered cover pairs, owner = atom of c1 -------
+    // ---- G4 hamiltonian: all ordered cover pairs --------------------------
+    // Blocks are processed in windows of kWindow (fixed, independent of the
+    // thread count). Phase 1, parallel over the window's blocks: each block's
+    // tiles T(ci, cj) = sum_s phi_ci(s) w(s) phi_cj(s)^T for every ordered cover
+    // pair with common points (full na x nb, no symmetry used). Phase 2,
+    // parallel over contiguous pair ranges: each thread adds the window's tiles
+    // of its pairs into H in block order, then (ci, cj) order. Every entry is
+    // therefore summed in one fixed order: results are bitwise independent of
+    // the thread count (kband common.hpp:58-64).
+    static constexpr int64_t kWindow = 512;
+    struct Tile {
+        int64_t pair;
+        int64_t off;  // into the block's tile values
+        int na, nb;
+    };
     void hamiltonian(int nspin, const double* veff, double dV, double* h, int threads, int64_t blo,
                      int64_t bhi) const {
         const Index& X = idx;
         const int64_t npts = static_cast<int64_t>(N[0]) * N[1] * N[2];
         const int64_t nnz = X.pair_off.back();
+        const int64_t npair = static_cast<int64_t>(X.pair_a.size());
         for (int64_t p = 0; p < nspin * nnz; ++p) h[p] = 0.0;
-        parallel_for(natom, threads, [&](int64_t a0, int64_t a1) {
-            std::vector<double> phi;
-            std::vector<int> row0;
-            double w[64];
-            for (int64_t b = blo; b < bhi; ++b) {
-                const int c0 = X.blk_ptr[b], c1 = X.blk_ptr[b + 1];
-                bool mine = false;
-                for (int c = c0; c < c1; ++c) mine |= (X.cov_atom[c] >= a0 && X.cov_atom[c] < a1);
-                if (!mine) continue;
-                block_phi(b, phi, row0);
-                for (int sp = 0; sp < nspin; ++sp) {
-                    for (int s = 0; s < 64; ++s) {
-                        bool valid;
-                        const int64_t pt = point_of(b, s, &valid);
-                        w[s] = valid ? veff[sp * npts + pt] * dV : 0.0;
-                    }
-                    double* H = h + sp * nnz;
-                    for (int i = c0; i < c1; ++i) {
-                        if (X.cov_atom[i] < a0 || X.cov_atom[i] >= a1) continue;
-                        const int na = spec[species[X.cov_atom[i]]].norb;
-                        for (int j = c0; j < c1; ++j) {
-                            const uint64_t both = X.cov_mask[i] & X.cov_mask[j];
-                            if (!both) continue;
-                            const int nb = spec[species[X.cov_atom[j]]].norb;
-                            double* blk = H + X.pair_off[lookup_pair(i, j, b)];
-                            for (int s = 0; s < 64; ++s) {
-                                if (!((both >> s) & 1)) continue;
+        std::vector<std::vector<Tile>> tiles(kWindow);
+        std::vector<std::vector<double>> vals(kWindow);
+        for (int64_t w0 = blo; w0 < bhi; w0 += kWindow) {
+            const int64_t w1 = std::min(bhi, w0 + kWindow);
+            parallel_for(w1 - w0, threads, [&](int64_t i0, int64_t i1) {
+                std::vector<double> phi;
+                std::vector<int> row0;
+                double w[64];
+                for (int64_t i = i0; i < i1; ++i) {
+                    const int64_t b = w0 + i;
+                    std::vector<Tile>& T = tiles[i];
+                    std::vector<double>& V = vals[i];
+                    T.clear();
+                    V.clear();
+                    const int c0 = X.blk_ptr[b], c1 = X.blk_ptr[b + 1];
+                    if (c0 == c1) continue;
+                    block_phi(b, phi, row0);
+                    for (int sp = 0; sp < nspin; ++sp) {
+                        for (int s = 0; s < 64; ++s) {
+                            bool valid;
+                            const int64_t pt = point_of(b, s, &valid);
+                            w[s] = valid ? veff[sp * npts + pt] * dV : 0.0;
+                        }
+                        for (int ci = c0; ci < c1; ++ci) {
+                            const int na = spec[species[X.cov_atom[ci]]].norb;
+                            for (int cj = c0; cj < c1; ++cj) {
+                                const uint64_t both = X.cov_mask[ci] & X.cov_mask[cj];
+                                if (!both) continue;
+                                const int nb = spec[species[X.cov_atom[cj]]].norb;
+                                const int64_t pair = lookup_pair(ci, cj, b);
+                                T.push_back({pair + sp * npair, static_cast<int64_t>(V.size()), na, nb});
+                                V.resize(V.size() + static_cast<size_t>(na) * nb, 0.0);
+                                double* blk = V.data() + T.back().off;
+                                // sum over the octets (8 consecutive slots) holding common points, in
+                                // 8 slot-lanes combined in a fixed tree: exact zeros outside the masks
                                 for (int ii = 0; ii < na; ++ii) {
-                                    const double av = phi[static_cast<size_t>(row0[i - c0] + ii) * 64 + s] * w[s];
-                                    for (int jj = 0; jj < nb; ++jj)
-                                        blk[ii * nb + jj] += av * phi[static_cast<size_t>(row0[j - c0] + jj) * 64 + s];
+                                    const double* pa = &phi[static_cast<size_t>(row0[ci - c0] + ii) * 64];
+                                    double aw[64];
+                                    for (int s = 0; s < 64; ++s) aw[s] = pa[s] * w[s];
+                                    for (int jj = 0; jj < nb; ++jj) {
+                                        const double* pb = &phi[static_cast<size_t>(row0[cj - c0] + jj) * 64];
+                                        double l[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                                        for (int o = 0; o < 8; ++o) {
+                                            if (!((both >> (8 * o)) & 0xFFu)) continue;
+                                            for (int k = 0; k < 8; ++k) l[k] += aw[8 * o + k] * pb[8 * o + k];
+                                        }
+                                        blk[ii * nb + jj] = ((l[0] + l[1]) + (l[2] + l[3])) + ((l[4] + l[5]) + (l[6] + l[7]));
+                                    }
                                 }
                             }
                         }
                     }
                 }
-            }
-        });
+            });
+            parallel_for(nspin * npair, threads, [&](int64_t p0, int64_t p1) {
+                for (int64_t i = 0; i < w1 - w0; ++i)
+                    for (const Tile& t : tiles[i]) {
+                        if (t.pair < p0 || t.pair >= p1) continue;
+                        const int64_t sp = t.pair / npair, p = t.pair - sp * npair;
+                        double* dst = h + sp * nnz + X.pair_off[p];
+                        const double* src = vals[i].data() + t.off;
+                        for (int e = 0; e < t.na * t.nb; ++e) dst[e] += src[e];
+                    }
+            });
+        }
     }
 };
 
