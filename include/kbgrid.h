@@ -216,6 +216,13 @@ int kbg_last_tally(const kbg_ctx* ctx, kbg_tally* out);
 /* Exchange-correlation of kbg_veff: 0 (default) Slater exchange only; 1 LSDA = exchange + Perdew-Wang 1992
  * correlation (energy[1] is then E_xc). */
 #define KBG_OPT_XC 8
+/* H accumulation: 1 deterministic -- every H contribution is split into two parts on fixed power-of-two
+ * grids derived from max|V_eff| (one extra max-reduction over V per H pass) and added with exact FP64
+ * atomics, so H has the same bits on every run, with every kernel/schedule, and on any number of GPUs
+ * (the multi-GPU reduction adds the limbs the same way); 0 (default) plain FP64 atomics, ~1.4x faster on
+ * the 56-atom cell, whose last bits depend on the order of arrival (<= 1e-15 relative run to run).
+ * Either way a non-finite V_eff gives KBG_ERR_NONFINITE from the host API. */
+#define KBG_OPT_DETERMINISTIC 9
 int kbg_set_option(kbg_ctx* ctx, int option, int64_t value);
 
 const char* kbg_last_error(const kbg_ctx* ctx);

@@ -32,6 +32,7 @@ KBG_OPT_DEBUG_COUNTERS = 5
 KBG_OPT_SCHEDULE = 6
 KBG_OPT_BLOCK_ORDER = 7
 KBG_OPT_XC = 8
+KBG_OPT_DETERMINISTIC = 9
 KBG_COMM_HANDLE_BYTES = 96
 KBG_CELL_PRIMITIVE = 0
 KBG_CELL_CUBIC = 1

@@ -84,6 +84,12 @@ struct kbg_ctx {
     bool comm_ready = false;
     double* d_states = nullptr;     // scaled states scratch
     size_t cap_states = 0;
+    // deterministic H (KBG_OPT_DETERMINISTIC, kb_gridcore.cuh h_scatter)
+    int det = 0;  // KBG_OPT_DETERMINISTIC (off by default: +43 % H time on 56 atoms)
+    double hbound = 0.0;            // >= sum over r of |phi_i(r) phi_j(r)| for any orbital pair (h_bound)
+    double* d_hacc = nullptr;       // two-limb accumulator [nspin][nnz][2]
+    size_t cap_hacc = 0;
+    unsigned long long* d_vbits = nullptr;  // max|V| bit pattern of the current H pass
 };
 
 // rho partner ranges are cut at 1/(2 KBG_RHO_SPLIT) of a block's work
@@ -110,6 +116,47 @@ int guard(kbg_ctx* ctx, F&& fn) {
         if (ctx) ctx->err = e.what();
         return KBG_ERR_CONSISTENCY;
     }
+}
+
+// Bound used by the deterministic H accumulation (kb_gridcore.cuh h_scatter):
+// hbound >= sum over the grid of |phi_i(r)| |phi_j(r)| for any two orbitals,
+// so max|V| |dV| hbound bounds the sum of |contributions| of every H entry.
+// |phi| <= umax rc^l A_l with umax bounding the cubic-Hermite interpolant
+// (|h00|+|h01| = 1, |h10|, |h11| <= 4/27 on [0, 1]) and A_l the largest real
+// solid-harmonic prefactor; an orbital is nonzero on at most P grid points,
+// P <= volume(ball of radius rc + cell diameter) / dV + 1.
+double h_bound(const kbg::SysParams& P, const kbg_system& s) {
+    const double* A = P.A;
+    const double det = std::fabs(A[0] * (A[4] * A[8] - A[5] * A[7]) - A[1] * (A[3] * A[8] - A[5] * A[6]) +
+                                 A[2] * (A[3] * A[7] - A[4] * A[6]));
+    const double dv = det / (static_cast<double>(s.grid[0]) * s.grid[1] * s.grid[2]);
+    double diam = 0.0;
+    for (int sg = 0; sg < 8; ++sg) {
+        double d[3] = {0, 0, 0};
+        for (int i = 0; i < 3; ++i) {
+            const double f = ((sg >> i) & 1 ? -1.0 : 1.0) / s.grid[i];
+            for (int q = 0; q < 3; ++q) d[q] += f * A[3 * i + q];
+        }
+        diam = std::max(diam, std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]));
+    }
+    const double Al[3] = {0.28209479177387814, 0.4886025119029199, 0.6307831305050401};
+    double phimax = 0.0, pmax = 0.0;
+    for (int t = 0; t < s.nspecies; ++t) {
+        const kbg_species& sp = s.spec[t];
+        const double h = sp.rc / (sp.ntab - 1);
+        for (int r = 0; r < sp.nrad; ++r) {
+            double u = 0.0, du = 0.0;
+            for (int k = 0; k < sp.ntab; ++k) {
+                u = std::max(u, std::fabs(sp.table[2 * (static_cast<size_t>(r) * sp.ntab + k)]));
+                du = std::max(du, std::fabs(sp.table[2 * (static_cast<size_t>(r) * sp.ntab + k) + 1]));
+            }
+            const double umax = u + (8.0 / 27.0) * h * du;
+            phimax = std::max(phimax, umax * std::pow(sp.rc, sp.l[r]) * Al[sp.l[r]]);
+        }
+        const double rr = sp.rc + diam;
+        pmax = std::max(pmax, std::floor(4.18879020478639 * rr * rr * rr / dv) + 1.0);
+    }
+    return pmax * phimax * phimax * (1.0 + 1e-12);
 }
 
 void validate_and_load(kbg_ctx* c, const kbg_system& s) {
@@ -177,6 +224,7 @@ void validate_and_load(kbg_ctx* c, const kbg_system& s) {
                 throw Error(KBG_ERR_NONFINITE, "atom " + std::to_string(a) + ": non-finite position");
     }
     c->npts = static_cast<int64_t>(s.grid[0]) * s.grid[1] * s.grid[2];
+    c->hbound = h_bound(P, s);
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         throw Error(KBG_ERR_CUDA, "no CUDA device available (libkbgrid has no CPU fallback)");
@@ -187,6 +235,7 @@ void validate_and_load(kbg_ctx* c, const kbg_system& s) {
     KBG_CUDA(cudaMalloc(&c->d_spc, sizeof(int) * s.natom));
     KBG_CUDA(cudaMalloc(&c->d_tables, sizeof(double) * tables.size()));
     KBG_CUDA(cudaMalloc(&c->d_check, sizeof(unsigned long long) * 4));
+    KBG_CUDA(cudaMalloc(&c->d_vbits, sizeof(unsigned long long) * 2));
     KBG_CUDA(cudaMemcpy(c->d_tau, s.tau, sizeof(double) * 3 * s.natom, cudaMemcpyHostToDevice));
     KBG_CUDA(cudaMemcpy(c->d_spc, s.species, sizeof(int) * s.natom, cudaMemcpyHostToDevice));
     KBG_CUDA(cudaMemcpy(c->d_tables, tables.data(), sizeof(double) * tables.size(), cudaMemcpyHostToDevice));
@@ -248,6 +297,13 @@ kbg::GridArgs grid_args(kbg_ctx* c, int nspin, double dV, const double* in, doub
     g.dbg = c->d_dbg;
     g.in = in;
     g.out = out;
+    if (!density) {
+        g.vbits = c->d_vbits;  // deterministic: max|V| (k_absmax); legacy: non-finite flag of the kernels
+        if (c->det) {
+            g.scatter |= 16;
+            g.wfac = std::fabs(dV) * c->hbound;
+        }
+    }
     if (g.max_cover > 32 * c->nwarps || g.max_cover > kbg::kMaxCoverPerBlock)
         throw Error(KBG_ERR_DIMENSION, "a grid block is covered by too many atom images");
     const size_t smem = kbg::grid_smem_bytes(g, c->nwarps, density);
@@ -295,13 +351,46 @@ int run_hamiltonian(kbg_ctx* c, int nspin, double dV, const double* d_veff, doub
         if (kbg::persist_fits(g, false)) return kbg::launch_hamiltonian_persist(g, st);
         int n = 0;
         for (int s = 0; s < nspin; ++s) {
-            const kbg::GridArgs g1 = grid_args(c, 1, dV, d_veff + s * c->npts, d_h + s * c->ix.nnz, false);
+            const kbg::GridArgs g1 =
+                grid_args(c, 1, dV, d_veff + s * c->npts, d_h + s * c->ix.nnz * (c->det ? 2 : 1), false);
             if (!kbg::persist_fits(g1, false)) break;
             n += kbg::launch_hamiltonian_persist(g1, st);
             if (s + 1 == nspin) return n;
         }
     }
     return kbg::launch_hamiltonian(g, c->blk_end - c->blk_begin, c->nwarps, st);
+}
+
+// One H accumulation into `acc`: deterministic (default) -- zero the two-limb
+// accumulator [nspin][nnz][2] and the max|V| word, reduce max|V| over every
+// point of the device-resident V, accumulate; legacy -- zero [nspin][nnz] and
+// accumulate with FP64 atomics. The caller finalizes (launch_finalize) or
+// reduces across ranks (kb_comm.cu).
+int h_accumulate(kbg_ctx* c, int nspin, double dV, const double* d_veff, double* acc, cudaStream_t st) {
+    int n = 0;
+    const size_t ne = static_cast<size_t>(nspin) * c->ix.nnz * (c->det ? 2 : 1);
+    KBG_CUDA(cudaMemsetAsync(acc, 0, ne * sizeof(double), st));
+    KBG_CUDA(cudaMemsetAsync(c->d_vbits, 0, sizeof(unsigned long long), st));
+    if (c->det) n += kbg::launch_absmax(d_veff, static_cast<int64_t>(nspin) * c->npts, c->d_vbits, st);
+    return n + run_hamiltonian(c, nspin, dV, d_veff, acc, st);
+}
+
+// Accumulator of the single-rank H paths: the context's two-limb scratch when
+// deterministic, else the output itself.
+double* h_acc_buffer(kbg_ctx* c, int nspin, double* d_out) {
+    if (!c->det) return d_out;
+    ensure(c->d_hacc, c->cap_hacc, static_cast<size_t>(2) * nspin * std::max<int64_t>(1, c->ix.nnz));
+    return c->d_hacc;
+}
+
+// Max|V| of the last H pass (legacy path: only the non-finite flag): non-finite V -> KBG_ERR_NONFINITE
+// (kband raises on non-finite values, householder.cpp:119-123). Host API only
+// (after its synchronize).
+void check_vbits(kbg_ctx* c, const char* who) {
+    unsigned long long v = 0;
+    KBG_CUDA(cudaMemcpy(&v, c->d_vbits, sizeof(v), cudaMemcpyDeviceToHost));
+    if (v >= 0x7ff0000000000000ull)
+        throw Error(KBG_ERR_NONFINITE, std::string(who) + ": non-finite V_eff (outputs invalid)");
 }
 
 // Device alias of a caller's host buffer that the GPU can read in place (pinned
@@ -526,8 +615,9 @@ int kbg_hamiltonian_accumulate_dev(kbg_ctx* c, int nspin, const double* d_veff, 
         require_index(c);
         KBG_CUDA(cudaSetDevice(c->device));
         const cudaStream_t st = static_cast<cudaStream_t>(stream);
-        KBG_CUDA(cudaMemsetAsync(d_h, 0, sizeof(double) * nspin * c->ix.nnz, st));
-        c->last_launches = run_hamiltonian(c, nspin, dV, d_veff, d_h, st);
+        double* acc = h_acc_buffer(c, nspin, d_h);
+        c->last_launches = h_accumulate(c, nspin, dV, d_veff, acc, st);
+        if (c->det) c->last_launches += kbg::launch_finalize(c->ix, c->P, nspin, acc, d_h, false, st);
         c->tally.flops = nspin * 2.0 * c->ix.sum_m2;
         c->tally.bytes = 8.0 * nspin * (c->ix.nnz + c->npts);
     });
@@ -544,6 +634,20 @@ int kbg_hamiltonian_mirror_dev(kbg_ctx* c, int nspin, double* d_h, void* stream)
 }
 
 int kbg_hamiltonian_dev(kbg_ctx* c, int nspin, const double* d_veff, double dV, double* d_h, void* stream) {
+    if (c && c->det) {  // accumulate + one fused finalize/mirror kernel
+        if (!d_veff || !d_h) return KBG_ERR_CONFIG;
+        return guard(c, [&] {
+            check_nspin(nspin);
+            require_index(c);
+            KBG_CUDA(cudaSetDevice(c->device));
+            const cudaStream_t st = static_cast<cudaStream_t>(stream);
+            double* acc = h_acc_buffer(c, nspin, d_h);
+            c->last_launches = h_accumulate(c, nspin, dV, d_veff, acc, st);
+            c->last_launches += kbg::launch_finalize(c->ix, c->P, nspin, acc, d_h, true, st);
+            c->tally.flops = nspin * 2.0 * c->ix.sum_m2;
+            c->tally.bytes = 8.0 * nspin * (c->ix.nnz + c->npts);
+        });
+    }
     int st = kbg_hamiltonian_accumulate_dev(c, nspin, d_veff, dV, d_h, stream);
     if (st != KBG_OK) return st;
     const int n1 = c->last_launches;
@@ -595,14 +699,19 @@ int kbg_hamiltonian(kbg_ctx* c, int nspin, const double* veff, double dV, double
         const size_t nin = static_cast<size_t>(nspin) * c->npts, nout = static_cast<size_t>(nspin) * c->ix.nnz;
         ensure(c->d_in, c->cap_in, nin);
         ensure(c->d_out, c->cap_out, nout);
-        const double* v_map = mapped_input(c, veff);
+        // deterministic H needs max|V| before the first contribution: V goes to the device first
+        const double* v_map = c->det ? nullptr : mapped_input(c, veff);
         if (!v_map) KBG_CUDA(cudaMemcpyAsync(c->d_in, veff, nin * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-        KBG_CUDA(cudaMemsetAsync(c->d_out, 0, nout * sizeof(double), c->stream));
-        int n = run_hamiltonian(c, nspin, dV, v_map ? v_map : c->d_in, c->d_out, c->stream);
-        n += kbg::launch_mirror(c->ix, c->P, nspin, c->d_out, c->stream);
+        double* acc = h_acc_buffer(c, nspin, c->d_out);
+        int n = h_accumulate(c, nspin, dV, v_map ? v_map : c->d_in, acc, c->stream);
+        if (c->det)
+            n += kbg::launch_finalize(c->ix, c->P, nspin, acc, c->d_out, true, c->stream);
+        else
+            n += kbg::launch_mirror(c->ix, c->P, nspin, c->d_out, c->stream);
         c->last_launches = n;
         KBG_CUDA(cudaMemcpyAsync(h, c->d_out, nout * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         KBG_CUDA(cudaStreamSynchronize(c->stream));
+        check_vbits(c, "hamiltonian");
         c->tally.flops = nspin * 2.0 * c->ix.sum_m2;
         c->tally.bytes = 8.0 * nspin * (c->ix.nnz + c->npts);
     });
@@ -627,28 +736,36 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
         // smaller one to wait for and rho (npts) the smaller output left after the last kernel. The DM
         // check is read at the end.
         int n = 0;
-        // V from pinned host memory is read in place by the H kernel (mapped_input)
-        const double* v_map = mapped_input(c, veff);
+        // Legacy H: V from pinned host memory is read in place by the H kernel (mapped_input), so the
+        // first DMMAs do not wait for a whole-array copy. Deterministic H needs max|V| before the
+        // first contribution: V is copied first, at the full PCIe bandwidth (the DM copy waits for
+        // it, ev_pass), then the H pass runs while the DM crosses.
+        const double* v_map = c->det ? nullptr : mapped_input(c, veff);
         double* rho_map = mapped_output(c, rho);
         auto h_half = [&] {
             if (!v_map)
                 KBG_CUDA(cudaMemcpyAsync(c->d_in2, veff, npt * sizeof(double), cudaMemcpyHostToDevice, c->stream2));
+            KBG_CUDA(cudaEventRecord(c->ev_pass, c->stream2));
             const double* vin = v_map ? v_map : c->d_in2;
             if (c->comm_ready) {
                 // sharded: partials into the peer-mapped exchange buffer, then the fused reduce +
                 // mirror over NVLink (kb_comm.cu) -- the full H on every rank
-                KBG_CUDA(cudaMemsetAsync(c->d_xbuf, 0, ndm * sizeof(double), c->stream2));
-                n += run_hamiltonian(c, nspin, dV, vin, c->d_xbuf, c->stream2);
+                n += h_accumulate(c, nspin, dV, vin, c->d_xbuf, c->stream2);
                 c->epoch += 2;
+                c->comm.ls = c->det ? 2 : 1;
                 n += kbg::launch_reduce_mirror(c->comm, c->ix, c->P, nspin, c->d_out2, c->epoch - 1, c->stream2);
             } else {
-                KBG_CUDA(cudaMemsetAsync(c->d_out2, 0, ndm * sizeof(double), c->stream2));
-                n += run_hamiltonian(c, nspin, dV, vin, c->d_out2, c->stream2);
-                n += kbg::launch_mirror(c->ix, c->P, nspin, c->d_out2, c->stream2);
+                double* acc = h_acc_buffer(c, nspin, c->d_out2);
+                n += h_accumulate(c, nspin, dV, vin, acc, c->stream2);
+                if (c->det)
+                    n += kbg::launch_finalize(c->ix, c->P, nspin, acc, c->d_out2, true, c->stream2);
+                else
+                    n += kbg::launch_mirror(c->ix, c->P, nspin, c->d_out2, c->stream2);
             }
             KBG_CUDA(cudaMemcpyAsync(h, c->d_out2, ndm * sizeof(double), cudaMemcpyDeviceToHost, c->stream2));
         };
         auto rho_half = [&] {
+            if (c->det) KBG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_pass, 0));
             KBG_CUDA(cudaMemcpyAsync(c->d_in, dm, ndm * sizeof(double), cudaMemcpyHostToDevice, c->stream));
             KBG_CUDA(cudaMemsetAsync(c->d_check, 0, 4 * sizeof(unsigned long long), c->stream));
             if (c->nranks > 1) KBG_CUDA(cudaMemsetAsync(c->d_out, 0, npt * sizeof(double), c->stream));
@@ -669,6 +786,7 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
         KBG_CUDA(cudaStreamSynchronize(c->stream2));
         KBG_CUDA(cudaStreamSynchronize(c->stream));
         if (c->comm_ready) comm_check(c);
+        check_vbits(c, "grid_pass");
         c->last_launches = n;
         double dmax, amax;
         std::memcpy(&dmax, &chk[0], 8);
@@ -711,8 +829,6 @@ int kbg_veff(kbg_ctx* c, int nspin, const double* rho, const double* vloc, doubl
         check_nspin(nspin);
         KBG_CUDA(cudaSetDevice(c->device));
         const size_t n = static_cast<size_t>(c->npts);
-        for (size_t i = 0; i < n * nspin; i += 4096)
-            if (!std::isfinite(rho[i])) throw Error(KBG_ERR_NONFINITE, "veff: non-finite rho");
         ensure(c->d_in2, c->cap_in2, 2 * n * nspin + n + 2);
         double* d_rho = c->d_in2;
         double* d_v = d_rho + n * nspin;
@@ -720,12 +836,19 @@ int kbg_veff(kbg_ctx* c, int nspin, const double* rho, const double* vloc, doubl
         double* d_e = d_v + n * nspin + n;
         KBG_CUDA(cudaMemcpyAsync(d_rho, rho, n * nspin * sizeof(double), cudaMemcpyHostToDevice, c->stream));
         if (vloc) KBG_CUDA(cudaMemcpyAsync(d_vloc, vloc, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-        c->last_launches =
-            kbg::run_veff(c->veff, c->P.N, c->P.Ainv, nspin, c->xc, d_rho, d_vloc, cell_dV(c), d_v, d_e, c->stream);
+        // every rho value is checked on the device (k_rho_total) -- kband raises on any non-finite
+        // input (householder.cpp:119-123)
+        unsigned int* d_bad = reinterpret_cast<unsigned int*>(c->d_check + 3);
+        KBG_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(unsigned int), c->stream));
+        c->last_launches = kbg::run_veff(c->veff, c->P.N, c->P.Ainv, nspin, c->xc, d_rho, d_vloc, cell_dV(c), d_v, d_e,
+                                         c->stream, d_bad);
         KBG_CUDA(cudaMemcpyAsync(veff, d_v, n * nspin * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         double e[2];
+        unsigned int bad = 0;
         KBG_CUDA(cudaMemcpyAsync(e, d_e, sizeof(e), cudaMemcpyDeviceToHost, c->stream));
+        KBG_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, c->stream));
         KBG_CUDA(cudaStreamSynchronize(c->stream));
+        if (bad) throw Error(KBG_ERR_NONFINITE, "veff: non-finite rho (outputs invalid)");
         if (energy) std::memcpy(energy, e, sizeof(e));
     });
 }
@@ -1090,10 +1213,12 @@ struct CommBlob {
     cudaIpcMemHandle_t h;
     uint64_t ptr;
     int64_t pid;
+    int32_t device;  // CUDA ordinal of the owner (same-process peers must be reachable from this device)
 };
 static_assert(sizeof(CommBlob) <= KBG_COMM_HANDLE_BYTES, "comm handle size");
 
-size_t xbuf_doubles(const kbg_ctx* c) { return 2 * static_cast<size_t>(std::max<int64_t>(1, c->ix.nnz)); }
+// [nspin <= 2][nnz][2 limbs] (the legacy FP64 path uses the first half as [nspin][nnz])
+size_t xbuf_doubles(const kbg_ctx* c) { return 4 * static_cast<size_t>(std::max<int64_t>(1, c->ix.nnz)); }
 
 }  // namespace
 
@@ -1111,6 +1236,7 @@ int kbg_comm_handle(kbg_ctx* c, void* out) {
         KBG_CUDA(cudaIpcGetMemHandle(&b.h, c->d_xbuf));
         b.ptr = reinterpret_cast<uint64_t>(c->d_xbuf);
         b.pid = static_cast<int64_t>(getpid());
+        b.device = c->device;
         std::memset(out, 0, KBG_COMM_HANDLE_BYTES);
         std::memcpy(out, &b, sizeof(b));
     });
@@ -1134,7 +1260,21 @@ int kbg_comm_open(kbg_ctx* c, const void* handles) {
             if (k == c->rank) {
                 x = c->d_xbuf;
             } else if (b.pid == static_cast<int64_t>(getpid())) {
-                x = reinterpret_cast<double*>(b.ptr);  // same process (contexts sharing a device): direct pointer
+                // same process: direct pointer, valid from this device only on the same device or with peer access
+                if (b.device != c->device) {
+                    int can = 0;
+                    KBG_CUDA(cudaDeviceCanAccessPeer(&can, c->device, b.device));
+                    if (!can)
+                        throw Error(KBG_ERR_CONFIG, "comm_open: rank " + std::to_string(k) + " lives on device " +
+                                                        std::to_string(b.device) + " in this process, which device " +
+                                                        std::to_string(c->device) + " cannot access (no P2P)");
+                    const cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+                    if (e == cudaErrorPeerAccessAlreadyEnabled)
+                        (void)cudaGetLastError();
+                    else
+                        KBG_CUDA(e);
+                }
+                x = reinterpret_cast<double*>(b.ptr);
             } else {
                 void* q = nullptr;
                 KBG_CUDA(cudaIpcOpenMemHandle(&q, b.h, cudaIpcMemLazyEnablePeerAccess));
@@ -1207,7 +1347,6 @@ int kbg_comm_open(kbg_ctx* c, const void* handles) {
                 cf[p] = (a != b) ? a < b : (R0 != 0 ? R0 > 0 : (R1 != 0 ? R1 > 0 : R2 >= 0));
             }
             if (c->d_pairtab) cudaFree(c->d_pairtab);
-    if (c->comm.tstamp) cudaFree(c->comm.tstamp);
             c->d_pairtab = nullptr;
             KBG_CUDA(cudaMalloc(&c->d_pairtab, std::max<size_t>(1, 9 * np)));
             if (np) {
@@ -1263,10 +1402,9 @@ int kbg_hamiltonian_allreduce_dev(kbg_ctx* c, int nspin, const double* d_veff, d
         if (!c->comm_ready) throw Error(KBG_ERR_CONFIG, "hamiltonian_allreduce: call kbg_comm_open first");
         KBG_CUDA(cudaSetDevice(c->device));
         const cudaStream_t st = static_cast<cudaStream_t>(stream);
-        double* x = c->d_xbuf;
-        KBG_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * nspin * c->ix.nnz, st));
-        int n = run_hamiltonian(c, nspin, dV, d_veff, x, st);
+        int n = h_accumulate(c, nspin, dV, d_veff, c->d_xbuf, st);
         c->epoch += 2;
+        c->comm.ls = c->det ? 2 : 1;
         n += kbg::launch_reduce_mirror(c->comm, c->ix, c->P, nspin, d_h, c->epoch - 1, st);
         c->last_launches = n;
         c->tally.flops = nspin * 2.0 * c->ix.sum_m2 / c->nranks;
@@ -1610,6 +1748,9 @@ int kbg_set_option(kbg_ctx* c, int option, int64_t value) {
             }
             c->schedule = static_cast<int>(value);
             return KBG_OK;
+        case KBG_OPT_DETERMINISTIC:
+            c->det = value ? 1 : 0;
+            return KBG_OK;
         case KBG_OPT_DEBUG_COUNTERS:
             if (value && !c->d_dbg) {
                 if (cudaMalloc(&c->d_dbg, 16 * sizeof(unsigned long long)) != cudaSuccess) return KBG_ERR_CUDA;
@@ -1637,6 +1778,7 @@ void kbg_destroy(kbg_ctx* c) {
     if (c->d_xbuf) cudaFree(c->d_xbuf);
     if (c->d_canon) cudaFree(c->d_canon);
     if (c->d_pairtab) cudaFree(c->d_pairtab);
+    if (c->comm.tstamp) cudaFree(c->comm.tstamp);
     if (c->d_cpre) cudaFree(c->d_cpre);
     c->veff.release();
     if (c->d_in2) cudaFree(c->d_in2);

@@ -39,23 +39,35 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 
 // Thread 0 of every CTA: wait until every rank's flag in this rank's flag
-// array has reached `epoch`. A peer that never arrives (broken setup) must not
-// hang the GPU: after 10 s the wait gives up and raises the error word
-// (flags[kMaxRanks + 1] of this rank; the result is then invalid).
-__device__ void wait_flags(const CommArgs& c, unsigned long long epoch) {
+// array lies in [lo, lo + 1] (a peer may already be one phase ahead: it
+// signals its next phase once it has seen ours, never two). A flag outside
+// that window means the ranks' call sequences drifted apart (e.g. after a
+// failed call); a peer that never arrives must not hang the GPU, so the wait
+// gives up after 10 s. Either way the error word of EVERY rank is raised
+// (flags[kMaxRanks + 1], read by kbg_comm_check on each rank) and the caller
+// skips all further reads and writes of peer buffers. Returns false then.
+__device__ bool wait_flags(const CommArgs& c, unsigned long long lo) {
+    __shared__ int s_ok;
     if (threadIdx.x == 0) {
         const unsigned long long* f = c.flags[c.rank];
         const unsigned long long t0 = globaltimer();
-        for (int k = 0; k < c.nranks; ++k)
-            while (ld_acquire_sys(f + k) < epoch) {
-                if (globaltimer() - t0 > 10000000000ull) {
-                    c.flags[c.rank][kMaxRanks + 1] = 1ull;
+        bool ok = true;
+        for (int k = 0; k < c.nranks && ok; ++k)
+            for (;;) {
+                const unsigned long long v = ld_acquire_sys(f + k);
+                if (v == lo || v == lo + 1) break;
+                if (v > lo + 1 || globaltimer() - t0 > 10000000000ull) {
+                    ok = false;
                     break;
                 }
                 __nanosleep(64);
             }
+        if (!ok)
+            for (int k = 0; k < c.nranks; ++k) c.flags[k][kMaxRanks + 1] = 1ull;
+        s_ok = ok;
     }
     __syncthreads();
+    return s_ok != 0;
 }
 
 // Signal `epoch` into slot `rank` of every rank's flag array.
@@ -79,12 +91,13 @@ __device__ __forceinline__ void copy_mirror(const CommArgs& c, int64_t npair, in
         const int na = c.pair_na[p], nb = c.pair_nb[p];
         const int64_t q = mirror[p];
         for (int s = 0; s < nspin; ++s) {
-            const double* src = x + s * nnz + poff[p];
+            // reduced values sit in the hi limb's slot
+            const double* src = x + (c.ls == 2 ? det_hi(s, poff[p], nnz) : s * nnz + poff[p]);
             double* dst = out + s * nnz + poff[p];
             double* dq = out + s * nnz + poff[q];
 #pragma unroll 4
             for (int e = lane; e < na * nb; e += 32) {
-                const double v = src[e];
+                const double v = src[(KBG_DET_SPLIT || c.ls == 1) ? e : 2 * e];
                 dst[e] = v;
                 if (q != p) dq[(e % nb) * na + e / nb] = v;
             }
@@ -104,36 +117,63 @@ __global__ void __launch_bounds__(256) k_reduce_mirror(CommArgs c, int nspin, in
                                                        const int32_t* __restrict__ pmirror, double* __restrict__ out) {
     if (c.tstamp && blockIdx.x == 0 && threadIdx.x == 0) c.tstamp[0] = globaltimer();
     if (blockIdx.x == 0 && threadIdx.x == 0) signal_flags(c, epoch);
-    wait_flags(c, epoch);
+    // on a failed wait this CTA neither reads nor writes peer memory (every rank's error word is set)
+    const bool ok = wait_flags(c, epoch);
     if (c.tstamp && threadIdx.x == 0) atomicMax(c.tstamp + 1, globaltimer());
-    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < ne * nspin;
+    for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; ok && t < ne * nspin;
          t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int s = static_cast<int>(t / ne);
         const int64_t el = t - s * ne;
         const int64_t base = s * nnz;
-        const int64_t o0 = base + el0[el];
+        const int64_t e0 = el0[el];
         const int32_t m = el1[el];
         const bool sym = m < 0;  // (a, a, 0) off-diagonal: (H + H^T) / 2
-        const int64_t o1 = base + (m & 0x7fffffff);
+        const int64_t e1 = m & 0x7fffffff;
+        const int64_t o0 = c.ls == 2 ? det_hi(s, e0, nnz) : base + e0;  // result slot: the (hi) value
+        const int64_t o1 = c.ls == 2 ? det_hi(s, e1, nnz) : base + e1;
+        const int64_t lo = c.ls == 2 ? det_lo(s, e0, nnz) - o0 : 0;     // lo limb offset from hi
         // only the ranks whose shard touches the pair are read: the other partials are exact
         // zeros, so the rank-order sum has the same bits as over all N
         const uint32_t om = c.elm[el];
-        double part[kMaxRanks], part2[kMaxRanks];
-#pragma unroll
-        for (int k = 0; k < kMaxRanks; ++k) {
-            const bool on = k < c.nranks && ((om >> k) & 1u);
-            part[k] = on ? c.x[k][o0] : 0.0;
-            part2[k] = (sym && on) ? c.x[k][o1] : 0.0;
-        }
         double v = 0.0, v2 = 0.0;
+        if (c.ls == 2) {
+            // two-limb partials (deterministic H): the hi and the lo sums are exact in any order
+            // (kb_gridcore.cuh h_scatter), so H = hi + lo has the bits of the single-GPU pass
+            double2 part[kMaxRanks], part2[kMaxRanks];
 #pragma unroll
-        for (int k = 0; k < kMaxRanks; ++k) {
-            v += part[k];
-            v2 += part2[k];
+            for (int k = 0; k < kMaxRanks; ++k) {
+                const bool on = k < c.nranks && ((om >> k) & 1u);
+                part[k] = on ? make_double2(c.x[k][o0], c.x[k][o0 + lo]) : make_double2(0.0, 0.0);
+                part2[k] = (sym && on) ? make_double2(c.x[k][o1], c.x[k][o1 + lo]) : make_double2(0.0, 0.0);
+            }
+            double hi = 0.0, lo = 0.0, hi2 = 0.0, lo2 = 0.0;
+#pragma unroll
+            for (int k = 0; k < kMaxRanks; ++k) {
+                hi += part[k].x;
+                lo += part[k].y;
+                hi2 += part2[k].x;
+                lo2 += part2[k].y;
+            }
+            v = hi + lo;
+            v2 = hi2 + lo2;
+        } else {
+            double part[kMaxRanks], part2[kMaxRanks];
+#pragma unroll
+            for (int k = 0; k < kMaxRanks; ++k) {
+                const bool on = k < c.nranks && ((om >> k) & 1u);
+                part[k] = on ? c.x[k][o0] : 0.0;
+                part2[k] = (sym && on) ? c.x[k][o1] : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < kMaxRanks; ++k) {
+                v += part[k];
+                v2 += part2[k];
+            }
         }
-        if (sym) v = 0.5 * (v + v2);
+        if (sym) v = 0.5 * (v + v2);  // same expression as k_mirror / k_finalize
         // canonical entries only (and both halves of an (a, a, 0) block): every rank then fills
-        // the mirror blocks H_ba(-R) = H_ab(R)^T locally (k_mirror), halving the NVLink writes
+        // the mirror blocks H_ba(-R) = H_ab(R)^T locally, halving the NVLink writes; the result
+        // goes to the first limb's slot
         for (int k = 0; k < c.nranks; ++k) {
             c.x[k][o0] = v;
             if (sym) c.x[k][o1] = v;
@@ -151,10 +191,10 @@ __global__ void __launch_bounds__(256) k_reduce_mirror(CommArgs c, int nspin, in
             signal_flags(c, epoch + 1);
         }
     }
-    if (!out) return;
+    if (!out || !ok) return;
     // fused copy-out + mirror (all CTAs are resident): wait until every rank's slice has landed here
     if (c.tstamp && blockIdx.x == 0 && threadIdx.x == 0) c.tstamp[3] = globaltimer();
-    wait_flags(c, epoch + 1);
+    if (!wait_flags(c, epoch + 1)) return;
     if (c.tstamp && threadIdx.x == 0) atomicMax(c.tstamp + 4, globaltimer());
     copy_mirror(c, npair, nspin, nnz, poff, pmirror, out);
     if (c.tstamp) {
@@ -163,9 +203,15 @@ __global__ void __launch_bounds__(256) k_reduce_mirror(CommArgs c, int nspin, in
     }
 }
 
-__global__ void __launch_bounds__(256) k_comm_copy_out(CommArgs c, int64_t n, double* __restrict__ out,
+__global__ void __launch_bounds__(256) k_comm_copy_out(CommArgs c, int64_t n, int64_t nnz, double* __restrict__ out,
                                                        unsigned long long epoch) {
-    wait_flags(c, epoch);
+    if (!wait_flags(c, epoch)) return;
+    if (c.ls == 2) {  // reduced values in the hi limbs' slots; n = nspin * nnz, nnz = n_per_spin
+        for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+             i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+            out[i] = c.x[c.rank][det_hi(static_cast<int>(i / nnz), i % nnz, nnz)];
+        return;
+    }
     const double2* src = reinterpret_cast<const double2*>(c.x[c.rank]);
     double2* dst = reinterpret_cast<double2*>(out);
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n / 2;
@@ -193,7 +239,7 @@ int launch_reduce_mirror(const CommArgs& c, const DevIndex& ix, const SysParams&
     k_reduce_mirror<<<grid, 256, 0, st>>>(c, nspin, ix.nnz, c.ne, c.el0, c.el1, epoch, 0, nullptr, nullptr, nullptr);
     KBG_CUDA(cudaGetLastError());
     const int64_t n = static_cast<int64_t>(nspin) * ix.nnz;
-    k_comm_copy_out<<<static_cast<unsigned>(sms) * 4, 256, 0, st>>>(c, n, d_out, epoch + 1);
+    k_comm_copy_out<<<static_cast<unsigned>(sms) * 4, 256, 0, st>>>(c, n, ix.nnz, d_out, epoch + 1);
     KBG_CUDA(cudaGetLastError());
     return 2 + launch_mirror(ix, sys, nspin, d_out, st);
 }

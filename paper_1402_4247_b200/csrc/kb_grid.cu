@@ -23,17 +23,18 @@ __device__ __forceinline__ void for_warp_tasks(const GridArgs& g, const Smem& sm
     }
 }
 
-template <int NW>
+template <int NW, bool DET>
 __global__ void __launch_bounds__(NW * 32, 2) k_hamiltonian(GridArgs g) {
     const Smem sm = carve(0u, g);
     const int64_t b = g.blk_begin + blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (DET && tid == 0) s_hscale = hscale_of(*g.vbits, g.wfac, g.nnz);  // stage_block syncs
     const int ncov = stage_block(g, b, sm, tid, NW * 32, [] { __syncthreads(); }, false, NW);
     if (ncov == 0) return;
     for (int spin = 0; spin < g.nspin; ++spin) {
-        double* Hs = g.out + spin * g.nnz;
+        double* Hs = g.out + spin * g.nnz * (DET ? 2 : 1);
         for_warp_tasks<NW>(g, sm, warp,
-                           [&](int e) { h_task(sm, sm.acc() + spin * 64, ncov, sm.task()[e], Hs, g.sign, g.scatter, lane); });
+                           [&](int e) { h_task<DET>(sm, sm.acc() + spin * 64, ncov, sm.task()[e], Hs, g.sign, g.scatter, lane); });
     }
 }
 
@@ -186,6 +187,79 @@ __global__ void k_mirror(SysParams P, int64_t npair, int nspin, int64_t nnz, con
     }
 }
 
+// ---- deterministic H: max|V| and the final rounding (kb_gridcore.cuh h_scatter) ---
+// max|x| over n doubles as the bit pattern of |x| (sign cleared): non-negative
+// doubles order like their bits, and NaN > inf > finite, so a non-finite input
+// shows up as a maximum above the largest finite double. Order-independent.
+__global__ void __launch_bounds__(256) k_absmax(const double* __restrict__ x, int64_t n,
+                                                unsigned long long* __restrict__ out) {
+    unsigned long long m = 0;
+    const int64_t n2 = n >> 1;
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n2;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double2 v = x2[i];
+        m = max(m, static_cast<unsigned long long>(__double_as_longlong(v.x)) & 0x7fffffffffffffffull);
+        m = max(m, static_cast<unsigned long long>(__double_as_longlong(v.y)) & 0x7fffffffffffffffull);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1))
+        m = max(m, static_cast<unsigned long long>(__double_as_longlong(x[n - 1])) & 0x7fffffffffffffffull);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+// H = hi + lo of the two-limb accumulator (det_hi / det_lo layout), one warp
+// per pair. mirror = 0: canonical pair blocks get H, the others 0 (the layout
+// kbg_hamiltonian_accumulate_dev returns). mirror = 1: also the mirror blocks
+// H_ba(-R) = H_ab(R)^T, and the (a, a, 0) blocks re-symmetrised as
+// (H + H^T)/2 -- the same expression as k_mirror and kb_comm.cu's reduction,
+// so the result has the same bits on any number of GPUs.
+__global__ void k_finalize(SysParams P, int64_t npair, int nspin, int64_t nnz, const int32_t* __restrict__ pa,
+                           const int32_t* __restrict__ pb, const int32_t* __restrict__ pR,
+                           const int64_t* __restrict__ poff, const int32_t* __restrict__ mirror,
+                           const double* __restrict__ acc, double* __restrict__ h, int do_mirror) {
+    const int lane = threadIdx.x & 31;
+    const int64_t p = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    if (p >= npair) return;
+    const int a = pa[p], b = pb[p];
+    const int R0 = pR[3 * p], R1 = pR[3 * p + 1], R2 = pR[3 * p + 2];
+    const bool canon = (a != b) ? a < b : (R0 != 0 ? R0 > 0 : (R1 != 0 ? R1 > 0 : R2 >= 0));
+    const int na = P.sp[P.spc[a]].norb, nb = P.sp[P.spc[b]].norb;
+    const int64_t q = mirror[p];
+    for (int s = 0; s < nspin; ++s) {
+        const int64_t o = poff[p];
+        auto val = [&](int e) { return acc[det_hi(s, o + e, nnz)] + acc[det_lo(s, o + e, nnz)]; };
+        double* dst = h + s * nnz + o;
+        if (!canon) {
+            if (!do_mirror)
+                for (int e = lane; e < na * nb; e += 32) dst[e] = 0.0;
+            continue;
+        }
+        if (q == p && do_mirror) {
+#pragma unroll 4
+            for (int e = lane; e < na * na; e += 32) {
+                const int i = e / na, j = e % na;
+                const double v = val(e);
+                if (i == j) {
+                    dst[e] = v;
+                } else {
+                    const double w = val(j * na + i);
+                    dst[e] = i < j ? 0.5 * (v + w) : 0.5 * (w + v);
+                }
+            }
+            continue;
+        }
+        double* dq = h + s * nnz + poff[q];
+#pragma unroll 4
+        for (int e = lane; e < na * nb; e += 32) {
+            const double v = val(e);
+            dst[e] = v;
+            if (do_mirror && q != p) dq[(e % nb) * na + e / nb] = v;
+        }
+    }
+}
+
 // ---- DM symmetry validation (host API only) ---------------------------------------
 __global__ void k_dm_check(SysParams P, int64_t npair, int nspin, int64_t nnz, const int32_t* __restrict__ pa,
                            const int32_t* __restrict__ pb, const int64_t* __restrict__ poff,
@@ -285,13 +359,15 @@ int launch_hamiltonian(const GridArgs& g0, int64_t nblk, int nwarps, cudaStream_
     GridArgs g = g0;
     const size_t smem = grid_smem_bytes(g, nwarps, false);
     set_layout(g, static_cast<size_t>(g.nspin) * 64);
-    if (nwarps == 4) {
-        set_smem(k_hamiltonian<4>, smem);
-        k_hamiltonian<4><<<static_cast<unsigned>(nblk), 128, smem, st>>>(g);
-    } else {
-        set_smem(k_hamiltonian<8>, smem);
-        k_hamiltonian<8><<<static_cast<unsigned>(nblk), 256, smem, st>>>(g);
-    }
+    const bool det = g.scatter & 16;  // deterministic two-limb scatter (KBG_OPT_DETERMINISTIC)
+    auto go = [&](auto kernel, int threads) {
+        set_smem(kernel, smem);
+        kernel<<<static_cast<unsigned>(nblk), threads, smem, st>>>(g);
+    };
+    if (nwarps == 4)
+        det ? go(k_hamiltonian<4, true>, 128) : go(k_hamiltonian<4, false>, 128);
+    else
+        det ? go(k_hamiltonian<8, true>, 256) : go(k_hamiltonian<8, false>, 256);
     KBG_CUDA(cudaGetLastError());
     return 1;
 }
@@ -301,6 +377,24 @@ int launch_mirror(const DevIndex& ix, const SysParams& sys, int nspin, double* h
     const unsigned grid = static_cast<unsigned>((ix.npair * 32 + 255) / 256);
     k_mirror<<<grid, 256, 0, st>>>(sys, ix.npair, nspin, ix.nnz, ix.pair_a, ix.pair_b, ix.pair_R, ix.pair_off,
                                    ix.pair_mirror, h);
+    KBG_CUDA(cudaGetLastError());
+    return 1;
+}
+
+int launch_absmax(const double* d_x, int64_t n, unsigned long long* d_out, cudaStream_t st) {
+    if (n <= 0) return 0;
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(148 * 4, (n / 2 + 255) / 256 + 1));
+    k_absmax<<<grid, 256, 0, st>>>(d_x, n, d_out);
+    KBG_CUDA(cudaGetLastError());
+    return 1;
+}
+
+int launch_finalize(const DevIndex& ix, const SysParams& sys, int nspin, const double* acc, double* h, bool mirror,
+                    cudaStream_t st) {
+    if (ix.npair == 0) return 0;
+    const unsigned grid = static_cast<unsigned>((ix.npair * 32 + 255) / 256);
+    k_finalize<<<grid, 256, 0, st>>>(sys, ix.npair, nspin, ix.nnz, ix.pair_a, ix.pair_b, ix.pair_R, ix.pair_off,
+                                     ix.pair_mirror, acc, h, mirror ? 1 : 0);
     KBG_CUDA(cudaGetLastError());
     return 1;
 }

@@ -233,7 +233,10 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int tid
         for (int i = tid; i < g.nspin * 64; i += nt) {
             bool valid;
             const int64_t pt = slot_point(P, bi, bj, bk, i & 63, valid);
-            sm.acc()[i] = valid ? g.in[(i >> 6) * g.npts + pt] * g.dV : 0.0;
+            const double v = valid ? g.in[(i >> 6) * g.npts + pt] : 0.0;
+            sm.acc()[i] = v * g.dV;
+            if (!isfinite(v) && g.vbits)  // non-finite V: flag for the host API (KBG_ERR_NONFINITE)
+                atomicMax(const_cast<unsigned long long*>(g.vbits), 0x7ff8000000000000ull);
         }
     }
     sync();
@@ -310,13 +313,63 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int tid
 }
 
 // ---- H --------------------------------------------------------------------------
+// Deterministic accumulation (KBG_OPT_DETERMINISTIC, scatter bit value 16, default).
+// FP64 atomics add in arrival order, so plain RED.ADD.F64 makes H's last bits
+// depend on the schedule. Instead every contribution v (one task's sum over
+// the block points it covers) is split into two parts that lie on FIXED grids,
+//   hi = round(v, g1), g1 = 2^(E-50);   lo = round(v - hi, g2), g2 = 2^(E-84),
+// with 2^E >= max|w| * hbound >= sum of |contributions| of any H entry (kb_api.cu:
+// h_bound). Every partial sum of the hi parts is then a multiple of g1 below
+// 2^53 g1 and every partial sum of the lo parts a multiple of g2 below 2^53 g2:
+// all additions are exact, so the two accumulators (interleaved [entry][2])
+// hold the same bits whatever the order of the atomics -- across runs, kernels,
+// and rank counts (the multi-GPU reduction adds the limbs the same way,
+// kb_comm.cu). H = hi + lo is rounded once at the end (k_finalize). Rounding
+// to a grid is two exact additions of C = 1.5 * 2^(k+52) (|x| < 2^(k+51)):
+// (x + C) - C is x rounded to a multiple of 2^k.
+struct HScale {
+    double c1, c2;   // rounding constants of the hi and lo grids
+    long long lo;    // offset (doubles) of an entry's lo limb from its hi limb (KBG_DET_SPLIT: nnz, else 1)
+};
+__shared__ HScale s_hscale;  // per CTA, set by thread 0 at kernel start
+
+// FP64 reduction into global memory as a fire-and-forget RED (the compiler
+// otherwise emits ATOMG with a discarded return value here).
+__device__ __forceinline__ void red_add(double* p, double v) {
+    asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+// (C1, C2) from the bit pattern of max|V| (sign cleared; NaN/inf give NaN H)
+// and wfac = |dV| * hbound.
+__device__ __forceinline__ HScale hscale_of(unsigned long long vbits, double wfac, int64_t nnz) {
+    HScale h;
+    h.lo = KBG_DET_SPLIT ? nnz : 1;
+    const double m = __longlong_as_double(static_cast<long long>(vbits & 0x7fffffffffffffffull)) * wfac;
+    if (!(m <= 1.79e308)) {
+        h.c1 = __longlong_as_double(0x7ff8000000000000ll);
+        h.c2 = 0.0;
+        return h;
+    }
+    int E = -900;
+    if (m > 0.0) {
+        int e;
+        frexp(m, &e);  // m < 2^e
+        E = e > -900 ? e : -900;
+    }
+    h.c1 = ldexp(1.5, E + 2);
+    h.c2 = ldexp(1.5, E - 32);
+    return h;
+}
+
 // Scatter of one accumulated tile: rows ra0 + [0, 8*TM) (group rows < rend),
 // columns cb0 + [0, 8*TN) of cover cj; canonical rows (cover ci <= cj) only.
-template <int TM, int TN>
+template <bool DET, int TM, int TN>
 __device__ __forceinline__ void h_scatter(const Smem& sm, const double (&c)[TM][TN][2], int ncov, int cj, int ra0,
                                           int rend, int cb0, double* __restrict__ H, double sign, int scatter,
                                           int lane) {
     const int nb = sm.cov()[cj].norb;
+    const double c1 = DET ? s_hscale.c1 : 0.0, c2 = DET ? s_hscale.c2 : 0.0;
+    const long long lo_off = DET ? s_hscale.lo : 0;
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
         const int r = ra0 + 8 * i + (lane >> 2);
@@ -329,10 +382,18 @@ __device__ __forceinline__ void h_scatter(const Smem& sm, const double (&c)[TM][
             for (int e = 0; e < 2; ++e) {
                 const int col = cb0 + 8 * j + (lane & 3) * 2 + e;
                 if (off >= 0 && col < nb && !(scatter & 2)) {
-                    if (!(scatter & 1))
-                        atomicAdd(H + off + ri * nb + col, sign * c[i][j][e]);
-                    else
-                        H[off + ri * nb + col] = sign * c[i][j][e];
+                    const double v = sign * c[i][j][e];
+                    if (DET) {
+                        const double hi = __dsub_rn(__dadd_rn(v, c1), c1);
+                        const double lo = __dsub_rn(__dadd_rn(__dsub_rn(v, hi), c2), c2);
+                        double* p = H + (KBG_DET_SPLIT ? 1 : 2) * (off + ri * nb + col);
+                        if (!(scatter & 8)) red_add(p, hi);           // bit 8: timing experiment only
+                        if (!(scatter & 4)) red_add(p + lo_off, lo);  // bit 4: timing experiment only
+                    } else if (!(scatter & 1)) {
+                        red_add(H + off + ri * nb + col, v);
+                    } else {
+                        H[off + ri * nb + col] = v;
+                    }
                 }
             }
     }
@@ -345,7 +406,7 @@ __device__ __forceinline__ void h_scatter(const Smem& sm, const double (&c)[TM][
 
 // One partner: C(8*TM x 8*TN) += Phi_rows diag(w) Phi_cj^T over the quads in
 // qm. Tiles with <= 2 DMMAs per quad alternate two accumulator sets.
-template <int TM, int TN>
+template <bool DET, int TM, int TN>
 __device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict__ w, int ncov, int cj, int ra0,
                                        int rend, int cb0, uint32_t qm, double* __restrict__ H, double sign,
                                        int scatter, int lane) {
@@ -396,12 +457,12 @@ __device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict_
                 c[0][i][j][0] += c[NACC - 1][i][j][0];
                 c[0][i][j][1] += c[NACC - 1][i][j][1];
             }
-    h_scatter<TM, TN>(sm, c[0], ncov, cj, ra0, rend, cb0, H, sign, scatter, lane);
+    h_scatter<DET, TM, TN>(sm, c[0], ncov, cj, ra0, rend, cb0, H, sign, scatter, lane);
 }
 
 // Two partners sharing the group's (w-scaled) A fragments: per quad of
 // q1 | q2 the A fragments are loaded and scaled once.
-template <int TM, int TN1, int TN2>
+template <bool DET, int TM, int TN1, int TN2>
 __device__ __forceinline__ void h_tile2(const Smem& sm, const double* __restrict__ w, int ncov, int cj1, int cj2,
                                         int ra0, int rend, uint32_t q1, uint32_t q2, double* __restrict__ H,
                                         double sign, int scatter, int lane) {
@@ -448,20 +509,21 @@ __device__ __forceinline__ void h_tile2(const Smem& sm, const double* __restrict
                 for (int j = 0; j < TN2; ++j) dmma(c2[i][j], a[i], bb[j]);
         }
     }
-    h_scatter<TM, TN1>(sm, c1, ncov, cj1, ra0, rend, 0, H, sign, scatter, lane);
-    h_scatter<TM, TN2>(sm, c2, ncov, cj2, ra0, rend, 0, H, sign, scatter, lane);
+    h_scatter<DET, TM, TN1>(sm, c1, ncov, cj1, ra0, rend, 0, H, sign, scatter, lane);
+    h_scatter<DET, TM, TN2>(sm, c2, ncov, cj2, ra0, rend, 0, H, sign, scatter, lane);
 }
 
-template <int TM, int TN1>
+template <bool DET, int TM, int TN1>
 __device__ __forceinline__ void h_tile2_tn2(int tn2, const Smem& sm, const double* w, int ncov, int cj1, int cj2,
                                             int ra0, int rend, uint32_t q1, uint32_t q2, double* H, double sign,
                                             int scatter, int lane) {
     if (tn2 == 2)
-        h_tile2<TM, TN1, 2>(sm, w, ncov, cj1, cj2, ra0, rend, q1, q2, H, sign, scatter, lane);
+        h_tile2<DET, TM, TN1, 2>(sm, w, ncov, cj1, cj2, ra0, rend, q1, q2, H, sign, scatter, lane);
     else
-        h_tile2<TM, TN1, 1>(sm, w, ncov, cj1, cj2, ra0, rend, q1, q2, H, sign, scatter, lane);
+        h_tile2<DET, TM, TN1, 1>(sm, w, ncov, cj1, cj2, ra0, rend, q1, q2, H, sign, scatter, lane);
 }
 
+template <bool DET>
 __device__ __forceinline__ void h_task(const Smem& sm, const double* w, int ncov, const Task& t, double* H,
                                        double sign, int scatter, int lane) {
     const GroupS& G = sm.grp()[t.g];
@@ -470,17 +532,17 @@ __device__ __forceinline__ void h_task(const Smem& sm, const double* w, int ncov
         const int tn1 = (sm.cov()[t.cj].norb + 7) >> 3, tn2 = (sm.cov()[t.cj2].norb + 7) >> 3;
         if (G.tm == 2) {
             if (tn1 == 2)
-                h_tile2_tn2<2, 2>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, t.qmask, t.qmask2, H, sign, scatter,
+                h_tile2_tn2<DET, 2, 2>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, t.qmask, t.qmask2, H, sign, scatter,
                                   lane);
             else
-                h_tile2_tn2<2, 1>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, t.qmask, t.qmask2, H, sign, scatter,
+                h_tile2_tn2<DET, 2, 1>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, t.qmask, t.qmask2, H, sign, scatter,
                                   lane);
         } else {
             if (tn1 == 2)
-                h_tile2_tn2<1, 2>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, t.qmask, t.qmask2, H, sign, scatter,
+                h_tile2_tn2<DET, 1, 2>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, t.qmask, t.qmask2, H, sign, scatter,
                                   lane);
             else
-                h_tile2_tn2<1, 1>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, t.qmask, t.qmask2, H, sign, scatter,
+                h_tile2_tn2<DET, 1, 1>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, t.qmask, t.qmask2, H, sign, scatter,
                                   lane);
         }
         return;
@@ -493,13 +555,13 @@ __device__ __forceinline__ void h_task(const Smem& sm, const double* w, int ncov
             const int tn = min(2, ((nb + 7) >> 3) - j0);
             const int ra0 = G.row0 + 8 * i0, cb0 = 8 * j0;
             if (tm == 2 && tn == 2)
-                h_tile<2, 2>(sm, w, ncov, t.cj, ra0, rend, cb0, qm, H, sign, scatter, lane);
+                h_tile<DET, 2, 2>(sm, w, ncov, t.cj, ra0, rend, cb0, qm, H, sign, scatter, lane);
             else if (tm == 2)
-                h_tile<2, 1>(sm, w, ncov, t.cj, ra0, rend, cb0, qm, H, sign, scatter, lane);
+                h_tile<DET, 2, 1>(sm, w, ncov, t.cj, ra0, rend, cb0, qm, H, sign, scatter, lane);
             else if (tn == 2)
-                h_tile<1, 2>(sm, w, ncov, t.cj, ra0, rend, cb0, qm, H, sign, scatter, lane);
+                h_tile<DET, 1, 2>(sm, w, ncov, t.cj, ra0, rend, cb0, qm, H, sign, scatter, lane);
             else
-                h_tile<1, 1>(sm, w, ncov, t.cj, ra0, rend, cb0, qm, H, sign, scatter, lane);
+                h_tile<DET, 1, 1>(sm, w, ncov, t.cj, ra0, rend, cb0, qm, H, sign, scatter, lane);
         }
     }
 }

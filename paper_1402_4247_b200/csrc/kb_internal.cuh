@@ -15,6 +15,19 @@ namespace kbg {
 constexpr int kMaxSpecies = 8;
 constexpr int kMaxRad = 16;
 constexpr int kMaxSpin = 2;  // nspin is 1 or 2 (check_nspin)
+// Two-limb H accumulator of the deterministic scatter (kb_gridcore.cuh h_scatter):
+// KBG_DET_SPLIT 1 = [nspin][2][nnz] (per spin the hi limbs, then the lo limbs: a
+// warp's RED of one limb touches as many L2 sectors as a plain FP64 scatter),
+// 0 = [nspin][nnz][2] interleaved.
+#ifndef KBG_DET_SPLIT
+#define KBG_DET_SPLIT 1
+#endif
+__host__ __device__ __forceinline__ int64_t det_hi(int s, int64_t e, int64_t nnz) {
+    return KBG_DET_SPLIT ? 2 * s * nnz + e : 2 * (s * nnz + e);
+}
+__host__ __device__ __forceinline__ int64_t det_lo(int s, int64_t e, int64_t nnz) {
+    return KBG_DET_SPLIT ? 2 * s * nnz + nnz + e : 2 * (s * nnz + e) + 1;
+}
 constexpr int kGroupRows = 16;  // covers are packed into row groups of <= 16 orbitals (2 DMMA row tiles)
 constexpr int kMaxTaskWarps = 32;  // task lists are LPT-balanced over <= 24 consumer warps
 constexpr int kMaxCoverPerBlock = 64;
@@ -183,7 +196,10 @@ struct GridArgs {
     int64_t npts;
     double dV;
     double sign;        // +1, or -1 under the fault hook
-    int scatter;        // 0: atomic scatter (product); 1: plain stores (timing experiment only, wrong H)
+    int scatter;        // 0: FP64 atomic scatter; 1: plain stores (timing experiment only, wrong H);
+                        // bit value 16: deterministic two-limb scatter into out [nspin][nnz][2] (default)
+    const unsigned long long* vbits;  // H, deterministic: bit pattern of max|V| (written by a preceding kernel)
+    double wfac;        // H, deterministic: |dV| * hbound (kb_gridcore.cuh hscale_of)
     const double* in;   // dm [nspin][nnz] or veff [nspin][npts]
     double* out;        // rho [nspin][npts] or h [nspin][nnz]
     // Shared-memory buffer layout of this launch (core::set_layout, by the
@@ -230,7 +246,8 @@ struct VeffPlan {
     void release();
 };
 int run_veff(VeffPlan& vp, const int N[3], const double Ainv[9], int nspin, int xc, const double* d_rho,
-             const double* d_vloc, double dV, double* d_veff, double* d_energy, cudaStream_t st);
+             const double* d_vloc, double dV, double* d_veff, double* d_energy, cudaStream_t st,
+             unsigned int* d_bad = nullptr);
 
 // Fused H reduction + mirror over peer memory (kb_comm.cu).
 constexpr int kMaxRanks = 8;
@@ -250,6 +267,7 @@ struct CommArgs {
     const int32_t* pair_nb = nullptr;
     const uint8_t* pair_canon = nullptr;
     unsigned long long* tstamp = nullptr;  // KBG_COMM_TIMING: globaltimer stamps of the exchange phases [8]
+    int ls = 1;  // doubles per entry of the partials: 2 = two-limb deterministic accumulators, 1 = FP64
 };
 // Per pair, the ranks (bit k) whose block range [bounds[k], bounds[k + 1]) holds
 // a canonical (block, cover pair) work item of that pair.
@@ -312,6 +330,11 @@ size_t persist_smem(const GridArgs& g, bool density);
 int launch_density_persist(const GridArgs& g, cudaStream_t st);
 int launch_hamiltonian_persist(const GridArgs& g, cudaStream_t st);
 int launch_mirror(const DevIndex& ix, const SysParams& sys, int nspin, double* h, cudaStream_t st);
+// Deterministic H (kb_gridcore.cuh h_scatter): max|x| as a bit pattern (atomicMax into *d_out, which the
+// caller zeroes), and H = hi + lo of the two-limb accumulator [nspin][nnz][2] (+ mirror blocks).
+int launch_absmax(const double* d_x, int64_t n, unsigned long long* d_out, cudaStream_t st);
+int launch_finalize(const DevIndex& ix, const SysParams& sys, int nspin, const double* acc, double* h, bool mirror,
+                    cudaStream_t st);
 int launch_dm_check(const DevIndex& ix, const SysParams& sys, int nspin, const double* dm,
                     unsigned long long* d_maxdiff_maxabs, cudaStream_t st);
 int launch_block_orbitals(const GridArgs& g, int64_t block, double* d_out, cudaStream_t st);

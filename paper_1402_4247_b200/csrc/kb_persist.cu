@@ -167,7 +167,7 @@ __device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes, uin
 // Producer warp: block k goes to buffer k & 1. The block after the current
 // one is fetched early and its cache image prefetched into L2, so the bulk
 // copy issued when its buffer frees up is served from L2.
-template <bool DENSITY>
+template <bool DENSITY, bool DET>
 __device__ void producer(const GridArgs& g, const Buffers<DENSITY>& B, int lane) {
     unsigned long long t_wait = 0, t0 = clock64();
     uint64_t pol = 0;
@@ -235,11 +235,17 @@ __device__ void producer(const GridArgs& g, const Buffers<DENSITY>& B, int lane)
             return;
         }
         if (!DENSITY && g.in) {  // w = V dV of the block's points, every spin
+            bool fin = true;
 #pragma unroll
             for (int j = 0; j < 2 * kMaxSpin; ++j) {
                 const int i = lane + 32 * j;
                 if (i < g.nspin * 64) sm.acc()[i] = w_cur[j] * g.dV;
+                fin = fin && isfinite(w_cur[j]);
             }
+            // non-finite V (the deterministic path sees it in its max|V| pass instead): flag it for
+            // the host API's KBG_ERR_NONFINITE, like kband's check (householder.cpp:119-123)
+            if (!DET && !__all_sync(0xffffffffu, fin) && lane == 0 && g.vbits)
+                atomicMax(const_cast<unsigned long long*>(g.vbits), 0x7ff8000000000000ull);
         }
         __syncwarp();
         if (lane == 0) {
@@ -267,7 +273,7 @@ __device__ void producer(const GridArgs& g, const Buffers<DENSITY>& B, int lane)
     }
 }
 
-template <bool DENSITY>
+template <bool DENSITY, bool DET>
 __device__ void consumer(const GridArgs& g, const Buffers<DENSITY>& B, int cw, int lane) {
     constexpr int NC = Cfg<DENSITY>::NC;
     unsigned long long t_wait = 0, t_tail = 0, t0 = clock64();
@@ -308,7 +314,8 @@ __device__ void consumer(const GridArgs& g, const Buffers<DENSITY>& B, int cw, i
                     __syncwarp();
                     rho_task(sm, ncov, t, g.dmr + spin * g.nrep, res - 32 * t.half, lane, g.scatter);
                 } else {
-                    h_task(sm, sm.acc() + spin * 64, ncov, t, g.out + spin * g.nnz, g.sign, g.scatter, lane);
+                    h_task<DET>(sm, sm.acc() + spin * 64, ncov, t, g.out + spin * g.nnz * (DET ? 2 : 1), g.sign,
+                                g.scatter, lane);
                 }
             }
         } else
@@ -322,10 +329,10 @@ __device__ void consumer(const GridArgs& g, const Buffers<DENSITY>& B, int cw, i
                 for (int w = cw; w < g.task_warps; w += NC)
                     for (int e = sm.wptr()[w]; e < sm.wptr()[w + 1]; ++e) rho_task(sm, ncov, sm.task()[e], Dr, racc, lane, g.scatter);
             } else {
-                double* Hs = g.out + spin * g.nnz;
+                double* Hs = g.out + spin * g.nnz * (DET ? 2 : 1);
                 for (int w = cw; w < g.task_warps; w += NC)
                     for (int e = sm.wptr()[w]; e < sm.wptr()[w + 1]; ++e)
-                        h_task(sm, sm.acc() + spin * 64, ncov, sm.task()[e], Hs, g.sign, g.scatter, lane);
+                        h_task<DET>(sm, sm.acc() + spin * 64, ncov, sm.task()[e], Hs, g.sign, g.scatter, lane);
             }
         }
         __syncwarp();
@@ -402,7 +409,7 @@ __device__ void consumer(const GridArgs& g, const Buffers<DENSITY>& B, int cw, i
     }
 }
 
-template <bool DENSITY>
+template <bool DENSITY, bool DET>
 __global__ void __launch_bounds__(Cfg<DENSITY>::NT, 1) k_persist(GridArgs g) {
     const Buffers<DENSITY> B = carve_all<DENSITY>(g);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -412,12 +419,13 @@ __global__ void __launch_bounds__(Cfg<DENSITY>::NT, 1) k_persist(GridArgs g) {
             mbar_init(&B.empty[s], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (DET) s_hscale = hscale_of(*g.vbits, g.wfac, g.nnz);
     }
     __syncthreads();
     if (warp < kPersistProducers) {
-        if (warp == 0) producer<DENSITY>(g, B, lane);
+        if (warp == 0) producer<DENSITY, DET>(g, B, lane);
     } else {
-        consumer<DENSITY>(g, B, warp - kPersistProducers, lane);
+        consumer<DENSITY, DET>(g, B, warp - kPersistProducers, lane);
     }
 }
 
@@ -437,11 +445,14 @@ int launch_persist(const GridArgs& g0, bool density, cudaStream_t st) {
     set_layout(g, persist_acc(g, density));
     KBG_CUDA(cudaMemsetAsync(g.counter, 0, sizeof(int), st));
     if (density) {
-        set_smem(k_persist<true>, smem);
-        k_persist<true><<<grid, Cfg<true>::NT, smem, st>>>(g);
+        set_smem(k_persist<true, false>, smem);
+        k_persist<true, false><<<grid, Cfg<true>::NT, smem, st>>>(g);
+    } else if (g.scatter & 16) {  // deterministic two-limb scatter (KBG_OPT_DETERMINISTIC)
+        set_smem(k_persist<false, true>, smem);
+        k_persist<false, true><<<grid, Cfg<false>::NT, smem, st>>>(g);
     } else {
-        set_smem(k_persist<false>, smem);
-        k_persist<false><<<grid, Cfg<false>::NT, smem, st>>>(g);
+        set_smem(k_persist<false, false>, smem);
+        k_persist<false, false><<<grid, Cfg<false>::NT, smem, st>>>(g);
     }
     KBG_CUDA(cudaGetLastError());
     return 1;

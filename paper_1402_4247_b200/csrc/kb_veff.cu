@@ -23,11 +23,18 @@ namespace {
 
 constexpr double kPi = 3.14159265358979323846;
 
-// rho_tot = sum_s rho_s -> real FFT input
-__global__ void k_rho_total(int64_t n, int nspin, const double* __restrict__ rho, double* __restrict__ out) {
+// rho_tot = sum_s rho_s -> real FFT input; a non-finite rho anywhere raises *bad
+// (the host API turns it into KBG_ERR_NONFINITE before returning V_eff).
+__global__ void k_rho_total(int64_t n, int nspin, const double* __restrict__ rho, double* __restrict__ out,
+                            unsigned int* bad) {
+    bool fin = true;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        out[i] = nspin == 2 ? rho[i] + rho[n + i] : rho[i];
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double r0 = rho[i], r1 = nspin == 2 ? rho[n + i] : 0.0;
+        fin = fin && isfinite(r0) && isfinite(r1);
+        out[i] = nspin == 2 ? r0 + r1 : r0;
+    }
+    if (bad && !__all_sync(0xffffffffu, fin) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
 }
 
 // rho(G) -> V_H(G) (with the 1/N of the inverse transform folded in).
@@ -180,7 +187,7 @@ void VeffPlan::release() {
 }
 
 int run_veff(VeffPlan& vp, const int N[3], const double Ainv[9], int nspin, int xc, const double* d_rho,
-             const double* d_vloc, double dV, double* d_veff, double* d_energy, cudaStream_t st) {
+             const double* d_vloc, double dV, double* d_veff, double* d_energy, cudaStream_t st, unsigned int* d_bad) {
     const int64_t n = static_cast<int64_t>(N[0]) * N[1] * N[2];
     const int64_t nc = static_cast<int64_t>(N[0]) * N[1] * (N[2] / 2 + 1);
     const int64_t nr = (n + 1) & ~int64_t(1);  // complex spectrum 16-byte aligned
@@ -206,7 +213,7 @@ int run_veff(VeffPlan& vp, const int N[3], const double Ainv[9], int nspin, int 
     double* part = vp.work + nr + 2 * nc;
     cufft_check(cufftSetStream(static_cast<cufftHandle>(vp.fwd), st), "cufftSetStream");
     cufft_check(cufftSetStream(static_cast<cufftHandle>(vp.inv), st), "cufftSetStream");
-    k_rho_total<<<sms_grid, 256, 0, st>>>(n, nspin, d_rho, real);
+    k_rho_total<<<sms_grid, 256, 0, st>>>(n, nspin, d_rho, real, d_bad);
     cufft_check(cufftExecD2Z(static_cast<cufftHandle>(vp.fwd), real, spec), "cufftExecD2Z");
     k_poisson<<<sms_grid, 256, 0, st>>>(N[0], N[1], N[2], vp.B, spec);
     cufft_check(cufftExecZ2D(static_cast<cufftHandle>(vp.inv), spec, real), "cufftExecZ2D");

@@ -93,19 +93,43 @@ class GridPass:
                     "kbg_block_orbitals")
         return out[: m.value * 64].reshape(m.value, 64)
 
+    # -- input validation (the C-ABI reads nspin * n doubles from each pointer) --
+    @staticmethod
+    def _spin_array(x, n: int, what: str) -> np.ndarray:
+        """(n,) or (nspin, n) float64, C-contiguous; a flat 2n array is rejected, not reinterpreted."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        if x.ndim == 1:
+            x = x[None]
+        if x.ndim != 2 or x.shape[1] != n:
+            raise_for_status(_abi.KBG_ERR_DIMENSION, what, f"expected ({n},) or (nspin, {n}), got {x.shape}")
+        if x.shape[0] not in (1, 2):
+            raise_for_status(_abi.KBG_ERR_CONFIG, what, f"nspin must be 1 or 2, got {x.shape[0]}")
+        return x
+
+    @staticmethod
+    def _spin_tensor(t, n: int, what: str) -> int:
+        """CUDA float64 tensor (nspin, n), contiguous; returns nspin."""
+        import torch
+
+        if t.dtype != torch.float64:
+            raise_for_status(_abi.KBG_ERR_DIMENSION, what, f"dtype {t.dtype} (float64 required)")
+        if not t.is_cuda or not t.is_contiguous():
+            raise_for_status(_abi.KBG_ERR_CONFIG, what, "a contiguous CUDA tensor is required")
+        if t.dim() != 2 or t.shape[1] != n:
+            raise_for_status(_abi.KBG_ERR_DIMENSION, what, f"expected (nspin, {n}), got {tuple(t.shape)}")
+        if t.shape[0] not in (1, 2):
+            raise_for_status(_abi.KBG_ERR_CONFIG, what, f"nspin must be 1 or 2, got {t.shape[0]}")
+        return int(t.shape[0])
+
     # -- G3 / G4, host buffers (drop-in) ---------------------------------------
     def density(self, dm: np.ndarray) -> np.ndarray:
-        dm = np.ascontiguousarray(dm, dtype=np.float64)
-        if dm.ndim == 1:
-            dm = dm[None]
+        dm = self._spin_array(dm, self._nnz(), "density: dm")
         rho = np.empty((dm.shape[0], self.system.npts))
         self._check(self._lib.kbg_density(self._h, dm.shape[0], _abi.dptr(dm), _abi.dptr(rho)), "kbg_density")
         return rho
 
     def hamiltonian(self, veff: np.ndarray, dV: float) -> np.ndarray:
-        veff = np.ascontiguousarray(veff, dtype=np.float64)
-        if veff.ndim == 1:
-            veff = veff[None]
+        veff = self._spin_array(veff, self.system.npts, "hamiltonian: veff")
         nnz = self._nnz()
         h = np.empty((veff.shape[0], nnz))
         self._check(self._lib.kbg_hamiltonian(self._h, veff.shape[0], _abi.dptr(veff), dV, _abi.dptr(h)),
@@ -114,12 +138,8 @@ class GridPass:
 
     def grid_pass(self, dm: np.ndarray, veff: np.ndarray, dV: float) -> tuple[np.ndarray, np.ndarray]:
         """rho and H of one SCF iteration in one call (overlapped transfers): returns (rho, h)."""
-        dm = np.ascontiguousarray(dm, dtype=np.float64)
-        veff = np.ascontiguousarray(veff, dtype=np.float64)
-        if dm.ndim == 1:
-            dm = dm[None]
-        if veff.ndim == 1:
-            veff = veff[None]
+        dm = self._spin_array(dm, self._nnz(), "grid_pass: dm")
+        veff = self._spin_array(veff, self.system.npts, "grid_pass: veff")
         if dm.shape[0] != veff.shape[0]:
             raise_for_status(_abi.KBG_ERR_DIMENSION, "grid_pass", "dm and veff spin counts differ")
         rho = np.empty((dm.shape[0], self.system.npts))
@@ -139,19 +159,30 @@ class GridPass:
         return 0 if stream is None else int(stream.cuda_stream)
 
     def density_dev(self, dm, rho, stream=None) -> None:
+        ns = self._spin_tensor(dm, self._nnz(), "density_dev: dm")
+        if self._spin_tensor(rho, self.system.npts, "density_dev: rho") != ns:
+            raise_for_status(_abi.KBG_ERR_DIMENSION, "density_dev", "dm and rho spin counts differ")
         self._check(self._lib.kbg_density_dev(self._h, dm.shape[0], dm.data_ptr(), rho.data_ptr(),
                                               self._stream_ptr(stream)), "kbg_density_dev")
 
+    def _check_h_args(self, veff, h, what: str) -> None:
+        ns = self._spin_tensor(veff, self.system.npts, what + ": veff")
+        if self._spin_tensor(h, self._nnz(), what + ": h") != ns:
+            raise_for_status(_abi.KBG_ERR_DIMENSION, what, "veff and h spin counts differ")
+
     def hamiltonian_dev(self, veff, dV: float, h, stream=None) -> None:
+        self._check_h_args(veff, h, "hamiltonian_dev")
         self._check(self._lib.kbg_hamiltonian_dev(self._h, veff.shape[0], veff.data_ptr(), dV, h.data_ptr(),
                                                   self._stream_ptr(stream)), "kbg_hamiltonian_dev")
 
     def hamiltonian_accumulate_dev(self, veff, dV: float, h, stream=None) -> None:
+        self._check_h_args(veff, h, "hamiltonian_accumulate_dev")
         self._check(self._lib.kbg_hamiltonian_accumulate_dev(self._h, veff.shape[0], veff.data_ptr(), dV,
                                                              h.data_ptr(), self._stream_ptr(stream)),
                     "kbg_hamiltonian_accumulate_dev")
 
     def hamiltonian_mirror_dev(self, h, stream=None) -> None:
+        self._spin_tensor(h, self._nnz(), "hamiltonian_mirror_dev: h")
         self._check(self._lib.kbg_hamiltonian_mirror_dev(self._h, h.shape[0], h.data_ptr(),
                                                          self._stream_ptr(stream)), "kbg_hamiltonian_mirror_dev")
 
@@ -188,6 +219,7 @@ class GridPass:
 
     def hamiltonian_allreduce_dev(self, veff, dV: float, h, stream=None) -> None:
         """Sharded H pass whose result is the full, mirrored H on every rank (no NCCL)."""
+        self._check_h_args(veff, h, "hamiltonian_allreduce_dev")
         self._check(self._lib.kbg_hamiltonian_allreduce_dev(self._h, veff.shape[0], veff.data_ptr(), dV, h.data_ptr(),
                                                             self._stream_ptr(stream)),
                     "kbg_hamiltonian_allreduce_dev")

@@ -3,7 +3,10 @@
 Bar (BASELINE.json north_star): index lists bit-exact; rho and H within 1e-10
 relative, normwise max|d|/max|ref| (the reference's normwise convention,
 /root/reference/proj/tests/test_householder.cpp:67), plus per-element relative
-1e-10 on entries with |ref| > 1e-4 max|ref|.
+error on every entry with |ref| > 1e-8 max|ref| (hard part 8):
+<= 1e-10 above 1e-4 max|ref|, <= ELEM_TOL_SMALL between 1e-8 and 1e-4 max|ref|
+(there the oracle's own rounding, ~n eps sum|terms|, is no longer negligible
+against |ref|).
 """
 import numpy as np
 import pytest
@@ -23,9 +26,24 @@ def normwise(x, ref):
     return float(np.abs(x - ref).max() / np.abs(ref).max())
 
 
-def elementwise(x, ref, floor=1e-4):
-    m = np.abs(ref) > floor * np.abs(ref).max()
+ELEM_TOL_SMALL = 1e-8
+
+
+def elementwise(x, ref, floor=1e-4, ceil=None):
+    """max relative error over the entries with floor < |ref| / max|ref| (<= ceil)."""
+    a = np.abs(ref) / np.abs(ref).max()
+    m = a > floor
+    if ceil is not None:
+        m &= a <= ceil
+    if not m.any():
+        return 0.0
     return float((np.abs(x - ref)[m] / np.abs(ref)[m]).max())
+
+
+def assert_parity(x, ref):
+    assert normwise(x, ref) <= TOL
+    assert elementwise(x, ref, 1e-4) <= TOL
+    assert elementwise(x, ref, 1e-8, 1e-4) <= ELEM_TOL_SMALL
 
 
 class Case:
@@ -57,7 +75,8 @@ def _built(built):
     _cases.clear()
 
 
-@pytest.mark.parametrize("name", ["primitive14_150Ry", "sweep56_100Ry", "cubic56_200Ry"])
+@pytest.mark.parametrize("name", ["primitive14_150Ry", "sweep56_100Ry", "cubic56_200Ry", "super448_200Ry",
+                                  "super1512_200Ry"])
 def test_index_bit_exact(name):
     c = case(name)
     for k in INDEX_KEYS:
@@ -73,22 +92,50 @@ def test_cubic_index_matches_survey_figures():
     assert ix["sum_m2"] == 4_146_964_624 or abs(ix["sum_m2"] - 4.147e9) < 1e6
 
 
-@pytest.mark.parametrize("name,nspin", [("primitive14_150Ry", 1), ("primitive14_150Ry", 2), ("cubic56_200Ry", 1)])
+PARITY_CASES = [("primitive14_150Ry", 1), ("primitive14_150Ry", 2), ("cubic56_200Ry", 1), ("cubic56_200Ry", 2)]
+
+
+@pytest.mark.parametrize("name,nspin", PARITY_CASES)
 def test_density_parity(name, nspin):
     c = case(name, nspin)
-    rho = c.gp.density(c.dm)
-    ref = c.o.density(c.dm)
-    assert normwise(rho, ref) <= TOL
-    assert elementwise(rho, ref) <= TOL
+    assert_parity(c.gp.density(c.dm), c.o.density(c.dm))
 
 
-@pytest.mark.parametrize("name,nspin", [("primitive14_150Ry", 1), ("primitive14_150Ry", 2), ("cubic56_200Ry", 1)])
+@pytest.mark.parametrize("name,nspin", PARITY_CASES)
 def test_hamiltonian_parity(name, nspin):
     c = case(name, nspin)
-    h = c.gp.hamiltonian(c.veff, c.f.dV)
-    ref = c.o.hamiltonian(c.veff, c.f.dV)
-    assert normwise(h, ref) <= TOL
-    assert elementwise(h, ref) <= TOL
+    assert_parity(c.gp.hamiltonian(c.veff, c.f.dV), c.o.hamiltonian(c.veff, c.f.dV))
+
+
+def test_supercell448_full_parity():
+    """Config 3 (448 atoms, 144^3 points) against the oracle over the whole grid: rho and H."""
+    c = case("super448_200Ry")
+    assert_parity(c.gp.density(c.dm), c.o.density(c.dm))
+    assert_parity(c.gp.hamiltonian(c.veff, c.f.dV), c.o.hamiltonian(c.veff, c.f.dV))
+
+
+@pytest.mark.parametrize("nranks,ranks", [(40, (0, 19, 39))])
+def test_supercell1512_sampled_parity(nranks, ranks):
+    """Config 4 (1512 atoms, 216^3 points): a full oracle pass is minutes of host time, so the
+    comparison is on samples -- a sharded context of `nranks` owns a contiguous, cost-balanced ~1/40
+    of the blocks; its rho (owned points, others 0) and its partial H (the contributions of its blocks,
+    mirrored) must match the oracle run over exactly the same block range. Three shards: both ends of
+    the grid (periodic wrap-around images) and the middle."""
+    from oracle.oracle import Oracle
+
+    f = Fe3O4.config("super1512_200Ry")
+    o = Oracle(f.system)
+    oix = o.build_index()
+    dm = f.dm(oix)
+    veff = f.veff()
+    for r in ranks:
+        gp = GridPass(f.system, device=0, rank=r, nranks=nranks)
+        gp.build_index()
+        b0, b1 = gp.shard_range()
+        assert 0 <= b0 < b1 <= oix["nblock"]
+        assert_parity(gp.density(dm), o.density(dm, blocks=(b0, b1)))
+        assert_parity(gp.hamiltonian(veff, f.dV), o.hamiltonian(veff, f.dV, blocks=(b0, b1)))
+        gp.close()
 
 
 def test_block_orbitals_parity():

@@ -2,8 +2,10 @@
 
 torchrun --nproc-per-node N tools/p2p_check.py [config]
 Every rank: sharded context, kbg_hamiltonian_allreduce_dev -> full H. Checks (rank 0 prints one JSON line):
-identical bits on every rank; equal to the NCCL path (accumulate + mirror + all_reduce) within 1e-14;
-equal to the single-context full H within 1e-13; repeatable bitwise; times both collectives.
+identical bits on every rank; repeatable bitwise; bit-for-bit equal to the single-GPU H (deterministic
+accumulation, KBG_OPT_DETERMINISTIC); equal to the NCCL path (accumulate + mirror + all_reduce) within
+1e-14; the sharded H and the assembled rho against the CPU oracle (normwise and per element 1e-10);
+the host API (kbg_grid_pass) on the sharded contexts; times both collectives.
 """
 import hashlib
 import json
@@ -12,11 +14,13 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+os.chdir(ROOT)
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
+from paper_1402_4247_b200 import _abi  # noqa: E402
 from paper_1402_4247_b200.grid import GridPass  # noqa: E402
 from paper_1402_4247_b200.system import Fe3O4  # noqa: E402
 
@@ -28,6 +32,7 @@ def main(cfg="cubic56_200Ry"):
     dist.init_process_group("nccl", device_id=dev)
     f = Fe3O4.config(cfg)
     gp = GridPass(f.system, device=local, rank=rank, nranks=world)
+    gp.set_option(_abi.KBG_OPT_DETERMINISTIC, 1)
     ix = gp.build_index()
     handles = [None] * world
     dist.all_gather_object(handles, gp.comm_handle())
@@ -119,21 +124,47 @@ def main(cfg="cubic56_200Ry"):
     t_nccl = timeit(nccl)
     t_acc = timeit(lambda: gp.hamiltonian_accumulate_dev(v, f.dV, h_nccl, st))
     if rank == 0:
+        from oracle.oracle import Oracle
+
         full = GridPass(f.system, device=local)
+        full.set_option(_abi.KBG_OPT_DETERMINISTIC, 1)
         full.build_index()
         ref = full.hamiltonian(f.veff(), f.dV)[0]
-        d_full = float(np.abs(h_p2p.cpu().numpy()[0] - ref).max() / np.abs(ref).max())
+        h_np = h_p2p.cpu().numpy()[0]
+        d_full = float(np.abs(h_np - ref).max() / np.abs(ref).max())
+        bitwise_single = bool(np.array_equal(h_np, ref))
         rho_ref = full.density(dm)[0]
-        d_rho = float(np.abs(rho_t.cpu().numpy()[0] - rho_ref).max() / np.abs(rho_ref).max())
+        rho_sum = rho_t.cpu().numpy()[0]
+        d_rho = float(np.abs(rho_sum - rho_ref).max() / np.abs(rho_ref).max())
+        # the CPU oracle on the same inputs: the sharded H and the assembled rho (parity bar of
+        # tests/test_gpu_parity.py: normwise 1e-10, per element 1e-10 where |ref| > 1e-8 max|ref|)
+        o = Oracle(f.system)
+        o.build_index()
+        h_or = o.hamiltonian(f.veff(), f.dV)[0]
+        rho_or = o.density(dm)[0]
+
+        def errs(x, r):
+            m = np.abs(r) > 1e-8 * np.abs(r).max()
+            return (float(np.abs(x - r).max() / np.abs(r).max()),
+                    float((np.abs(x - r)[m] / np.abs(r)[m]).max()))
+
+        h_norm, h_elem = errs(h_np, h_or)
+        r_norm, r_elem = errs(rho_sum, rho_or)
+        det = bool(repeat and bitwise_single)
         print(json.dumps({"config": cfg, "world": world, "same_bits_all_ranks": same_bits, "repeatable": repeat,
+                          "bitwise_equal_single_gpu": bitwise_single,
                           "rel_diff_vs_nccl": d_nccl, "rel_diff_vs_single_gpu": d_full,
+                          "oracle_h_normwise": h_norm, "oracle_h_elementwise": h_elem,
+                          "oracle_rho_normwise": r_norm, "oracle_rho_elementwise": r_elem,
                           "h_ms_p2p": round(t_p2p, 4), "h_ms_nccl_incl_mirror": round(t_nccl, 4),
                           "h_ms_accumulate_only": round(t_acc, 4), "accumulate_ms_per_rank": acc_ranks,
                           "grid_pass_h_vs_p2p": d_gp, "grid_pass_rho_sum_vs_single_gpu": d_rho,
                           "exchange_phases_us_per_rank": phases,
-                          "note": "H partials use atomics: not bitwise repeatable run to run (single GPU neither)",
-                          "ok": bool(same_bits and d_nccl <= 1e-14 and d_full <= 1e-13 and d_gp <= 1e-14
-                                     and d_rho == 0.0)}), flush=True)
+                          "note": "deterministic H (KBG_OPT_DETERMINISTIC): the sharded H must equal the "
+                                  "single-GPU H bit for bit and repeat bitwise",
+                          "ok": bool(same_bits and det and d_nccl <= 1e-14 and d_gp == 0.0 and d_rho == 0.0
+                                     and h_norm <= 1e-10 and h_elem <= 1e-10 and r_norm <= 1e-10
+                                     and r_elem <= 1e-10)}), flush=True)
     dist.destroy_process_group()
 
 
