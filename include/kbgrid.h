@@ -223,6 +223,16 @@ int kbg_last_tally(const kbg_ctx* ctx, kbg_tally* out);
  * the 56-atom cell, whose last bits depend on the order of arrival (<= 1e-15 relative run to run).
  * Either way a non-finite V_eff gives KBG_ERR_NONFINITE from the host API. */
 #define KBG_OPT_DETERMINISTIC 9
+/* kbg_grid_pass on a sharded context after kbg_comm_open: 1 (default) shard-local host transfers -- the
+ * rank reads only the DM pairs its blocks touch (in place when dm is pinned) and V at its points, writes
+ * rho only at the points of its blocks and H only in its slice of each spin's entries (kbg_shard_io);
+ * the other entries of the caller's buffers are left as they were. 0: every rank reads everything and
+ * returns the full H and a full-size rho (zeros outside its blocks). */
+#define KBG_OPT_SHARD_IO 10
+/* A5's "dense enough" switch: H tasks whose point density (exact common points / points of the quads the
+ * DMMA path executes, x 255) is below this threshold run point-exact FP64 FMAs instead of DMMA over whole
+ * quads. 0 (default): every task on the FP64 tensor path (measured faster at every cutoff). */
+#define KBG_OPT_SPARSE_DFMA 11
 int kbg_set_option(kbg_ctx* ctx, int option, int64_t value);
 
 const char* kbg_last_error(const kbg_ctx* ctx);
@@ -263,6 +273,12 @@ int kbg_hamiltonian_allreduce_dev(kbg_ctx* ctx, int nspin, const double* d_veff,
  * the H of that call is invalid), else KBG_OK. Clears the flag. kbg_grid_pass
  * on a sharded context checks it itself. */
 int kbg_comm_check(kbg_ctx* ctx);
+/* Shard-local I/O ranges of this rank (after kbg_comm_open): out[0..1] its blocks [b0, b1), out[2..3] the
+ * points [p0, p1) of its grid-plane range in C order (kbg_grid_pass writes rho at the points of its blocks;
+ * with a pageable rho buffer the D2H covers [p0, p1) and the other points there become 0), out[4..5] its
+ * slice [h0, h1) of each spin's H entries, out[6] DM doubles per spin its repack reads (canonical pairs it
+ * touches + their mirror blocks for the symmetry check), out[7] = p1 - p0. */
+int kbg_shard_io(const kbg_ctx* ctx, int64_t out[8]);
 /* Timing aid: with KBG_COMM_TIMING set in the environment at kbg_comm_open, the
  * phase times (ns from the reduce kernel's start) of the last exchange: all
  * partials ready, slice reduced, copy kernel start, all slices landed, done. */

@@ -33,6 +33,8 @@ KBG_OPT_SCHEDULE = 6
 KBG_OPT_BLOCK_ORDER = 7
 KBG_OPT_XC = 8
 KBG_OPT_DETERMINISTIC = 9
+KBG_OPT_SHARD_IO = 10
+KBG_OPT_SPARSE_DFMA = 11
 KBG_COMM_HANDLE_BYTES = 96
 KBG_CELL_PRIMITIVE = 0
 KBG_CELL_CUBIC = 1
@@ -123,6 +125,7 @@ KBGRID_SYMBOLS = [
     ("kbg_comm_handle", _I, [_P, _P]),
     ("kbg_comm_open", _I, [_P, _P]),
     ("kbg_comm_check", _I, [_P]),
+    ("kbg_shard_io", _I, [_P, C.POINTER(C.c_int64)]),
     ("kbg_comm_timing", _I, [_P, _DP]),
     ("kbg_hamiltonian_allreduce_dev", _I, [_P, _I, _P, _D, _P, _P]),
     ("kbg_offsets", _I, [_P, C.POINTER(_I), C.POINTER(C.c_int32)]),

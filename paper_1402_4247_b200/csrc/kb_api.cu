@@ -90,6 +90,11 @@ struct kbg_ctx {
     double* d_hacc = nullptr;       // two-limb accumulator [nspin][nnz][2]
     size_t cap_hacc = 0;
     unsigned long long* d_vbits = nullptr;  // max|V| bit pattern of the current H pass
+    // shard-local host transfers of kbg_grid_pass on a sharded context (KBG_OPT_SHARD_IO)
+    int shard_io = 1;
+    int sparse_thr = 0;  // KBG_OPT_SPARSE_DFMA (0: every task on DMMA)
+    uint8_t* d_pown = nullptr;      // per pair: 1 if this rank's blocks touch it (kbg_comm_open)
+    int64_t io[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // kbg_shard_io
 };
 
 // rho partner ranges are cut at 1/(2 KBG_RHO_SPLIT) of a block's work
@@ -98,6 +103,30 @@ struct kbg_ctx {
 #ifndef KBG_RHO_SPLIT
 #define KBG_RHO_SPLIT 6
 #endif
+
+namespace kbg {
+namespace {
+thread_local cudaStream_t g_build_stream = nullptr;
+}
+BuildStream::BuildStream(cudaStream_t st) : prev(g_build_stream) {
+    g_build_stream = st;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
+}
+BuildStream::~BuildStream() { g_build_stream = prev; }
+cudaError_t pool_malloc_bytes(void** p, size_t bytes) {
+    return cudaMallocAsync(p, bytes ? bytes : 1, g_build_stream);
+}
+void pool_free(void* p) {
+    if (p) cudaFreeAsync(p, g_build_stream);
+}
+}  // namespace kbg
 
 namespace {
 
@@ -298,6 +327,7 @@ kbg::GridArgs grid_args(kbg_ctx* c, int nspin, double dV, const double* in, doub
     g.in = in;
     g.out = out;
     if (!density) {
+        g.scatter |= c->sparse_thr << 8;  // A5 switch: tasks below this point density (1/255) run DFMA
         g.vbits = c->d_vbits;  // deterministic: max|V| (k_absmax); legacy: non-finite flag of the kernels
         if (c->det) {
             g.scatter |= 16;
@@ -314,9 +344,9 @@ kbg::GridArgs grid_args(kbg_ctx* c, int nspin, double dV, const double* in, doub
 }
 
 int run_density(kbg_ctx* c, int nspin, const double* d_dm, double* d_rho, cudaStream_t st,
-                unsigned long long* chk = nullptr) {
+                unsigned long long* chk = nullptr, const uint8_t* own = nullptr) {
     ensure(c->d_dmr, c->cap_dmr, static_cast<size_t>(nspin) * std::max<int64_t>(1, c->ix.nrep));
-    int n = kbg::launch_dm_repack(c->ix, c->P, nspin, d_dm, c->d_dmr, st, chk);
+    int n = kbg::launch_dm_repack(c->ix, c->P, nspin, d_dm, c->d_dmr, st, chk, own);
     kbg::GridArgs g = grid_args(c, nspin, 0.0, d_dm, d_rho, true);
     g.dmr = c->d_dmr;
     if (c->persist_ok && c->persist && c->ix.phis) {
@@ -414,7 +444,7 @@ const double* mapped_input(const kbg_ctx* c, const double* host) {
 // memory the result streams over PCIe during the kernel instead of in one D2H
 // copy after it. Single-rank contexts only (a shard must zero foreign points).
 double* mapped_output(const kbg_ctx* c, double* host) {
-    if (c->nranks > 1 || std::getenv("KBG_NO_ZERO_COPY_OUT")) return nullptr;
+    if ((c->nranks > 1 && !(c->comm_ready && c->shard_io)) || std::getenv("KBG_NO_ZERO_COPY_OUT")) return nullptr;
     return const_cast<double*>(mapped_input(c, host));
 }
 
@@ -500,6 +530,10 @@ int kbg_build_index(kbg_ctx* c) {
     if (!c) return KBG_ERR_CONFIG;
     return guard(c, [&] {
         KBG_CUDA(cudaSetDevice(c->device));
+        // the previous geometry's arrays go back to the pool in stream order; nothing else may still
+        // be reading them
+        if (c->stream2) KBG_CUDA(cudaStreamSynchronize(c->stream2));
+        kbg::BuildStream bs(c->stream);
         c->built = false;
         c->hix = kbg::HostIndex();
         kbg::free_formats(c->fmt);
@@ -522,19 +556,12 @@ int kbg_build_index(kbg_ctx* c) {
         // per-warp lists (~30 % slower rho).
         if (!c->persist_ok && (c->schedule & 2)) c->persist_ok = persist_tasks(c->schedule & 1, KBG_RHO_SPLIT);
         if (!c->persist_ok) kbg::build_tasks_device(c->P, c->ix, 8, 8, 8, c->stream);
-        // owned blocks, heaviest first, for the persistent kernels' work counter
-        std::vector<int64_t> cost(c->ix.nblock);
-        KBG_CUDA(cudaMemcpy(cost.data(), c->ix.blk_cost, cost.size() * sizeof(int64_t), cudaMemcpyDeviceToHost));
-        std::vector<int64_t> order;
-        for (int64_t b = c->blk_begin; b < c->blk_end; ++b) order.push_back(b);
-        if (c->block_order == 0)
-            std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return cost[x] > cost[y]; });
-        if (c->ix.order) cudaFree(c->ix.order);
+        // owned blocks, heaviest first (stable: ties in block order), for the persistent kernels'
+        // work counter -- a stable device radix sort, no host round trip
+        kbg::pool_free(c->ix.order);
         c->ix.order = nullptr;
-        c->ix.norder = static_cast<int64_t>(order.size());
-        KBG_CUDA(cudaMalloc(&c->ix.order, std::max<size_t>(1, order.size()) * sizeof(int64_t)));
-        if (!order.empty())
-            KBG_CUDA(cudaMemcpy(c->ix.order, order.data(), order.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+        c->ix.norder = c->blk_end - c->blk_begin;
+        kbg::block_order_device(c->ix, c->blk_begin, c->blk_end, c->block_order == 0, c->stream);
         if (!c->d_counter) KBG_CUDA(cudaMalloc(&c->d_counter, 2 * sizeof(int)));
         if (c->persist_ok) {
             kbg::build_cache_device(grid_args(c, 1, 0.0, nullptr, nullptr, false),
@@ -742,6 +769,13 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
         // it, ev_pass), then the H pass runs while the DM crosses.
         const double* v_map = c->det ? nullptr : mapped_input(c, veff);
         double* rho_map = mapped_output(c, rho);
+        // Shard-local host transfers (sharded context with the peer exchange open, KBG_OPT_SHARD_IO):
+        // the repack reads only the DM pairs this rank's blocks touch (in place from pinned memory),
+        // rho is written only at the rank's points (in place when pinned, else the D2H covers just
+        // its plane range), and H -- complete on every rank after the fused reduction -- leaves only
+        // the rank's slice [io[4], io[5]) of each spin. kbg_shard_io reports the ranges.
+        const bool sio = c->comm_ready && c->shard_io;
+        const double* dm_map = sio ? mapped_input(c, dm) : nullptr;
         auto h_half = [&] {
             if (!v_map)
                 KBG_CUDA(cudaMemcpyAsync(c->d_in2, veff, npt * sizeof(double), cudaMemcpyHostToDevice, c->stream2));
@@ -762,17 +796,35 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
                 else
                     n += kbg::launch_mirror(c->ix, c->P, nspin, c->d_out2, c->stream2);
             }
-            KBG_CUDA(cudaMemcpyAsync(h, c->d_out2, ndm * sizeof(double), cudaMemcpyDeviceToHost, c->stream2));
+            if (sio) {
+                const int64_t h0 = c->io[4], h1 = c->io[5];
+                for (int s = 0; s < nspin; ++s)
+                    if (h1 > h0)
+                        KBG_CUDA(cudaMemcpyAsync(h + s * c->ix.nnz + h0, c->d_out2 + s * c->ix.nnz + h0,
+                                                 (h1 - h0) * sizeof(double), cudaMemcpyDeviceToHost, c->stream2));
+            } else {
+                KBG_CUDA(cudaMemcpyAsync(h, c->d_out2, ndm * sizeof(double), cudaMemcpyDeviceToHost, c->stream2));
+            }
         };
         auto rho_half = [&] {
             if (c->det) KBG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_pass, 0));
-            KBG_CUDA(cudaMemcpyAsync(c->d_in, dm, ndm * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+            if (!dm_map) KBG_CUDA(cudaMemcpyAsync(c->d_in, dm, ndm * sizeof(double), cudaMemcpyHostToDevice, c->stream));
             KBG_CUDA(cudaMemsetAsync(c->d_check, 0, 4 * sizeof(unsigned long long), c->stream));
-            if (c->nranks > 1) KBG_CUDA(cudaMemsetAsync(c->d_out, 0, npt * sizeof(double), c->stream));
+            if (c->nranks > 1 && !rho_map) KBG_CUDA(cudaMemsetAsync(c->d_out, 0, npt * sizeof(double), c->stream));
             // the DM symmetry check rides along in the repack pass (no separate k_dm_check)
-            n += run_density(c, nspin, c->d_in, rho_map ? rho_map : c->d_out, c->stream, c->d_check);
-            if (!rho_map)
-                KBG_CUDA(cudaMemcpyAsync(rho, c->d_out, npt * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+            n += run_density(c, nspin, dm_map ? dm_map : c->d_in, rho_map ? rho_map : c->d_out, c->stream, c->d_check,
+                             sio ? c->d_pown : nullptr);
+            if (!rho_map) {
+                if (sio) {
+                    const int64_t p0 = c->io[2], p1 = c->io[3];
+                    for (int s = 0; s < nspin; ++s)
+                        if (p1 > p0)
+                            KBG_CUDA(cudaMemcpyAsync(rho + s * c->npts + p0, c->d_out + s * c->npts + p0,
+                                                     (p1 - p0) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+                } else {
+                    KBG_CUDA(cudaMemcpyAsync(rho, c->d_out, npt * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+                }
+            }
         };
 #ifndef KBG_PASS_RHO_FIRST
         h_half();
@@ -1308,7 +1360,38 @@ int kbg_comm_open(kbg_ctx* c, const void* handles) {
         if (c->ix.nnz >= (int64_t(1) << 31)) throw Error(KBG_ERR_DIMENSION, "comm_open: nnz >= 2^31");
         // ranks whose shard accumulates into each pair (the others' partials are exact zeros)
         std::vector<uint32_t> owners;
-        kbg::pair_owners(c->ix, shard_bounds(c), owners, c->stream);
+        {
+            kbg::BuildStream bs(c->stream);
+            kbg::pair_owners(c->ix, shard_bounds(c), owners, c->stream);
+        }
+        {
+            // pairs this rank's blocks touch: the DM it reads in kbg_grid_pass (shard-local input)
+            std::vector<uint8_t> mine(std::max<int64_t>(1, c->ix.npair), 0);
+            int64_t dm_read = 0;
+            for (int64_t p = 0; p < c->ix.npair; ++p) {
+                mine[p] = (owners[p] >> c->rank) & 1u;
+                const int a = h.pair_a[p], b = h.pair_b[p];
+                const int R0 = h.pair_R[3 * p], R1 = h.pair_R[3 * p + 1], R2 = h.pair_R[3 * p + 2];
+                const bool can = (a != b) ? a < b : (R0 != 0 ? R0 > 0 : (R1 != 0 ? R1 > 0 : R2 >= 0));
+                if (mine[p] && can) dm_read += 2 * (h.pair_off[p + 1] - h.pair_off[p]);  // block + mirror (check)
+            }
+            if (c->d_pown) cudaFree(c->d_pown);
+            c->d_pown = nullptr;
+            KBG_CUDA(cudaMalloc(&c->d_pown, mine.size()));
+            KBG_CUDA(cudaMemcpy(c->d_pown, mine.data(), mine.size(), cudaMemcpyHostToDevice));
+            // io ranges: blocks, the rank's grid-plane range (C order, i outermost), its H output slice
+            const int64_t nb12 = static_cast<int64_t>(c->P.nblk[1]) * c->P.nblk[2];
+            const int64_t plane = static_cast<int64_t>(c->P.N[1]) * c->P.N[2];
+            c->io[0] = c->blk_begin;
+            c->io[1] = c->blk_end;
+            c->io[2] = c->blk_end > c->blk_begin ? std::min<int64_t>(c->P.N[0], 4 * (c->blk_begin / nb12)) * plane : 0;
+            c->io[3] = c->blk_end > c->blk_begin
+                           ? std::min<int64_t>(c->P.N[0], 4 * ((c->blk_end - 1) / nb12 + 1)) * plane : 0;
+            c->io[4] = c->ix.nnz * c->rank / c->nranks;
+            c->io[5] = c->ix.nnz * (c->rank + 1) / c->nranks;
+            c->io[6] = dm_read;
+            c->io[7] = c->io[3] - c->io[2];
+        }
         std::vector<int32_t> e0, e1;
         std::vector<uint8_t> em;
         for (int64_t w = w0; w < w1; ++w) {
@@ -1383,6 +1466,13 @@ int kbg_comm_timing(kbg_ctx* c, double* out5) {
         for (int i = 0; i < 5; ++i) out5[i] = static_cast<double>(t[i + 1]) - static_cast<double>(t[0]);
         KBG_CUDA(cudaMemset(c->comm.tstamp, 0, sizeof(t)));
     });
+}
+
+int kbg_shard_io(const kbg_ctx* c, int64_t out[8]) {
+    if (!c || !out) return KBG_ERR_CONFIG;
+    if (!c->comm_ready) return KBG_ERR_CONFIG;
+    for (int i = 0; i < 8; ++i) out[i] = c->io[i];
+    return KBG_OK;
 }
 
 int kbg_comm_check(kbg_ctx* c) {
@@ -1751,6 +1841,16 @@ int kbg_set_option(kbg_ctx* c, int option, int64_t value) {
         case KBG_OPT_DETERMINISTIC:
             c->det = value ? 1 : 0;
             return KBG_OK;
+        case KBG_OPT_SHARD_IO:
+            c->shard_io = value ? 1 : 0;
+            return KBG_OK;
+        case KBG_OPT_SPARSE_DFMA:
+            if (value < 0 || value > 255) {
+                c->err = "set_option: sparse-DFMA threshold must be 0..255 (point density x 255)";
+                return KBG_ERR_CONFIG;
+            }
+            c->sparse_thr = static_cast<int>(value);
+            return KBG_OK;
         case KBG_OPT_DEBUG_COUNTERS:
             if (value && !c->d_dbg) {
                 if (cudaMalloc(&c->d_dbg, 16 * sizeof(unsigned long long)) != cudaSuccess) return KBG_ERR_CUDA;
@@ -1768,7 +1868,13 @@ const char* kbg_last_error(const kbg_ctx* c) { return c ? c->err.c_str() : "null
 void kbg_destroy(kbg_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
-    kbg::free_index(c->ix);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->stream2) cudaStreamSynchronize(c->stream2);
+    {
+        kbg::BuildStream bs(c->stream);
+        kbg::free_index(c->ix);
+    }
+    if (c->stream) cudaStreamSynchronize(c->stream);
     kbg::free_formats(c->fmt);
     for (double* p : {c->d_fa, c->d_fb, c->d_phase, c->d_kw})
         if (p) cudaFree(p);
@@ -1778,6 +1884,7 @@ void kbg_destroy(kbg_ctx* c) {
     if (c->d_xbuf) cudaFree(c->d_xbuf);
     if (c->d_canon) cudaFree(c->d_canon);
     if (c->d_pairtab) cudaFree(c->d_pairtab);
+    if (c->d_pown) cudaFree(c->d_pown);
     if (c->comm.tstamp) cudaFree(c->comm.tstamp);
     if (c->d_cpre) cudaFree(c->d_cpre);
     c->veff.release();

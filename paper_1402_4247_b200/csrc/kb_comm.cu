@@ -17,6 +17,8 @@
 // All CTAs fit on the GPU at once (4 per SM, no shared memory) and nothing they
 // wait for depends on a later kernel, so the waits cannot deadlock; every wait
 // gives up after 10 s anyway (error word, kbg_comm_check).
+#include <algorithm>
+
 #include "kb_internal.cuh"
 
 namespace kbg {
@@ -110,7 +112,7 @@ __device__ __forceinline__ void copy_mirror(const CommArgs& c, int64_t npair, in
 // entry -- or the transposed entry of an (a,a,0) block, flagged by bit 31 --
 // or el0 itself on such a block's diagonal): one coalesced index load, then
 // all N partials in flight at once, then the stores.
-__global__ void __launch_bounds__(256) k_reduce_mirror(CommArgs c, int nspin, int64_t nnz, int64_t ne,
+__global__ void __launch_bounds__(256, 4) k_reduce_mirror(CommArgs c, int nspin, int64_t nnz, int64_t ne,
                                                        const int32_t* __restrict__ el0,
                                                        const int32_t* __restrict__ el1, unsigned long long epoch,
                                                        int64_t npair, const int64_t* __restrict__ poff,
@@ -139,22 +141,21 @@ __global__ void __launch_bounds__(256) k_reduce_mirror(CommArgs c, int nspin, in
         if (c.ls == 2) {
             // two-limb partials (deterministic H): the hi and the lo sums are exact in any order
             // (kb_gridcore.cuh h_scatter), so H = hi + lo has the bits of the single-GPU pass
-            double2 part[kMaxRanks], part2[kMaxRanks];
+            // (accumulated as they arrive: any order gives the same bits, and no partials are held,
+            // which keeps the kernel at <= 64 registers -- all CTAs must be resident, see launch)
+            double hi = 0.0, lo_s = 0.0, hi2 = 0.0, lo2 = 0.0;
 #pragma unroll
             for (int k = 0; k < kMaxRanks; ++k) {
-                const bool on = k < c.nranks && ((om >> k) & 1u);
-                part[k] = on ? make_double2(c.x[k][o0], c.x[k][o0 + lo]) : make_double2(0.0, 0.0);
-                part2[k] = (sym && on) ? make_double2(c.x[k][o1], c.x[k][o1 + lo]) : make_double2(0.0, 0.0);
+                if (k < c.nranks && ((om >> k) & 1u)) {
+                    hi += c.x[k][o0];
+                    lo_s += c.x[k][o0 + lo];
+                    if (sym) {
+                        hi2 += c.x[k][o1];
+                        lo2 += c.x[k][o1 + lo];
+                    }
+                }
             }
-            double hi = 0.0, lo = 0.0, hi2 = 0.0, lo2 = 0.0;
-#pragma unroll
-            for (int k = 0; k < kMaxRanks; ++k) {
-                hi += part[k].x;
-                lo += part[k].y;
-                hi2 += part2[k].x;
-                lo2 += part2[k].y;
-            }
-            v = hi + lo;
+            v = hi + lo_s;
             v2 = hi2 + lo2;
         } else {
             double part[kMaxRanks], part2[kMaxRanks];
@@ -227,9 +228,14 @@ int launch_reduce_mirror(const CommArgs& c, const DevIndex& ix, const SysParams&
     int dev = 0, sms = 0;
     KBG_CUDA(cudaGetDevice(&dev));
     KBG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    // all CTAs fit at once (4 per SM x 256 threads, <= 64 registers): the copy-out phase of large H
-    // wants the warps (2 per SM measured 4 % slower at 448 atoms on 4 GPUs)
-    const unsigned grid = static_cast<unsigned>(sms) * 4;
+    // All CTAs must be resident at once: a CTA that has signalled its slice waits for every other
+    // CTA's (the counter) before the copy-out, so a CTA that cannot start would deadlock the rest
+    // (until the 10 s timeout). 4 per SM x 256 threads (<= 64 registers, __launch_bounds__) unless the
+    // occupancy query says fewer fit; the copy-out phase of large H wants the warps (2 per SM measured
+    // 4 % slower at 448 atoms on 4 GPUs).
+    int per_sm = 0;
+    KBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_reduce_mirror, 256, 0));
+    const unsigned grid = static_cast<unsigned>(sms) * static_cast<unsigned>(std::max(1, std::min(4, per_sm)));
     if (c.pair_na) {  // reduce, then (same kernel) copy-out + mirror once every slice has landed
         k_reduce_mirror<<<grid, 256, 0, st>>>(c, nspin, ix.nnz, c.ne, c.el0, c.el1, epoch, ix.npair, ix.pair_off,
                                               ix.pair_mirror, d_out);
@@ -239,7 +245,7 @@ int launch_reduce_mirror(const CommArgs& c, const DevIndex& ix, const SysParams&
     k_reduce_mirror<<<grid, 256, 0, st>>>(c, nspin, ix.nnz, c.ne, c.el0, c.el1, epoch, 0, nullptr, nullptr, nullptr);
     KBG_CUDA(cudaGetLastError());
     const int64_t n = static_cast<int64_t>(nspin) * ix.nnz;
-    k_comm_copy_out<<<static_cast<unsigned>(sms) * 4, 256, 0, st>>>(c, n, ix.nnz, d_out, epoch + 1);
+    k_comm_copy_out<<<grid, 256, 0, st>>>(c, n, ix.nnz, d_out, epoch + 1);
     KBG_CUDA(cudaGetLastError());
     return 2 + launch_mirror(ix, sys, nspin, d_out, st);
 }
@@ -273,8 +279,8 @@ void pair_owners(const DevIndex& ix, const std::vector<int64_t>& bounds, std::ve
     if (ix.npair == 0) return;
     uint32_t* d_own = nullptr;
     int64_t* d_b = nullptr;
-    KBG_CUDA(cudaMalloc(&d_own, ix.npair * sizeof(uint32_t)));
-    KBG_CUDA(cudaMalloc(&d_b, bounds.size() * sizeof(int64_t)));
+    KBG_CUDA(pool_malloc(&d_own, ix.npair * sizeof(uint32_t)));
+    KBG_CUDA(pool_malloc(&d_b, bounds.size() * sizeof(int64_t)));
     KBG_CUDA(cudaMemsetAsync(d_own, 0, ix.npair * sizeof(uint32_t), st));
     KBG_CUDA(cudaMemcpyAsync(d_b, bounds.data(), bounds.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
     k_pair_owners<<<static_cast<unsigned>((ix.nblock + 127) / 128), 128, 0, st>>>(ix.nblock, ix.bp_ptr, ix.bp,
@@ -283,8 +289,8 @@ void pair_owners(const DevIndex& ix, const std::vector<int64_t>& bounds, std::ve
     KBG_CUDA(cudaGetLastError());
     KBG_CUDA(cudaMemcpyAsync(out.data(), d_own, ix.npair * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     KBG_CUDA(cudaStreamSynchronize(st));
-    cudaFree(d_own);
-    cudaFree(d_b);
+    pool_free(d_own);
+    pool_free(d_b);
 }
 
 }  // namespace kbg

@@ -84,6 +84,58 @@ __device__ __forceinline__ void eval_orbitals(const DevSpecies& sp, const double
     }
 }
 
+// The same orbitals at two points at once (d[h], d2[h], h = 0, 1): one sink call
+// per orbital with both values (the geometry cache's 16-byte stores). `tables`
+// may point to shared memory (staged copy of the table array) or global memory.
+template <class Sink>
+__device__ __forceinline__ void eval_orbitals_pair(const DevSpecies& sp, const double* __restrict__ tables,
+                                                   const double (&d)[2][3], const double (&d2)[2], Sink&& sink) {
+    double h00[2], h10[2], h01[2], h11[2];
+    const double* tab[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const double r = sqrt(d2[h]);
+        const double x = r * sp.inv_h;
+        int k = static_cast<int>(x);
+        if (k > sp.ntab - 2) k = sp.ntab - 2;
+        const double t = x - k;
+        const double omt = 1.0 - t;
+        h00[h] = (1.0 + 2.0 * t) * omt * omt;
+        h10[h] = t * omt * omt * sp.h;
+        h01[h] = t * t * (3.0 - 2.0 * t);
+        h11[h] = t * t * (t - 1.0) * sp.h;
+        tab[h] = tables + sp.tab_off + 2 * k;
+    }
+    int o = 0;
+    for (int rad = 0; rad < sp.nrad; ++rad) {
+        double u[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const double2 a = *reinterpret_cast<const double2*>(tab[h] + static_cast<long long>(rad) * sp.ntab * 2);
+            const double2 b = *reinterpret_cast<const double2*>(tab[h] + static_cast<long long>(rad) * sp.ntab * 2 + 2);
+            u[h] = h00[h] * a.x + h10[h] * a.y + h01[h] * b.x + h11[h] * b.y;
+        }
+        const int l = sp.l[rad];
+        if (l == 0) {
+            sink(o++, kC00 * u[0], kC00 * u[1]);
+        } else if (l == 1) {
+            const double c0 = kC1 * u[0], c1 = kC1 * u[1];
+            sink(o++, c0 * d[0][0], c1 * d[1][0]);
+            sink(o++, c0 * d[0][1], c1 * d[1][1]);
+            sink(o++, c0 * d[0][2], c1 * d[1][2]);
+        } else {
+            sink(o++, kC20 * (2.0 * d[0][2] * d[0][2] - d[0][0] * d[0][0] - d[0][1] * d[0][1]) * u[0],
+                 kC20 * (2.0 * d[1][2] * d[1][2] - d[1][0] * d[1][0] - d[1][1] * d[1][1]) * u[1]);
+            sink(o++, kC22 * (d[0][0] * d[0][0] - d[0][1] * d[0][1]) * u[0],
+                 kC22 * (d[1][0] * d[1][0] - d[1][1] * d[1][1]) * u[1]);
+            const double c0 = kC2 * u[0], c1 = kC2 * u[1];
+            sink(o++, c0 * d[0][0] * d[0][1], c1 * d[1][0] * d[1][1]);
+            sink(o++, c0 * d[0][0] * d[0][2], c1 * d[1][0] * d[1][2]);
+            sink(o++, c0 * d[0][1] * d[0][2], c1 * d[1][1] * d[1][2]);
+        }
+    }
+}
+
 __device__ __forceinline__ int64_t block_id(const SysParams& P, int bi, int bj, int bk) {
     return (static_cast<int64_t>(bi) * P.nblk[1] + bj) * P.nblk[2] + bk;
 }
@@ -122,7 +174,10 @@ namespace kbg {
 // with more orbitals forms a group of its own. Rows are not padded: a group's
 // 8-row DMMA tiles may run into the next group's rows, which the kernels mask
 // out. norb(c) gives the orbital count of local cover c; g_rows = actual rows.
-// Returns the group count.
+// Returns the group count. (Padding every cover to a multiple of 4 rows would
+// give all fragment rows the same shared-memory swizzle, but the extra rows do
+// not fit two rho buffers into shared memory at the coarse end of the sweep.)
+
 template <class NorbF>
 __host__ __device__ inline int make_groups(int ncov, NorbF norb, int* g_first, int* g_end, int* g_row0,
                                            int* g_rows, int* c_row0, int* c_group) {

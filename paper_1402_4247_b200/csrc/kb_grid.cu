@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_hamiltonian(GridArgs g) {
     for (int spin = 0; spin < g.nspin; ++spin) {
         double* Hs = g.out + spin * g.nnz * (DET ? 2 : 1);
         for_warp_tasks<NW>(g, sm, warp,
-                           [&](int e) { h_task<DET>(sm, sm.acc() + spin * 64, ncov, sm.task()[e], Hs, g.sign, g.scatter, lane); });
+                           [&](int e) { h_task<DET, true>(sm, sm.acc() + spin * 64, ncov, sm.task()[e], Hs, g.sign, g.scatter, lane); });
     }
 }
 
@@ -77,7 +77,8 @@ __global__ void k_dm_repack(SysParams P, int64_t npair, int nspin, int64_t nnz, 
                             const int32_t* __restrict__ pa, const int32_t* __restrict__ pb,
                             const int32_t* __restrict__ pR, const int64_t* __restrict__ poff,
                             const int64_t* __restrict__ proff, const int32_t* __restrict__ mirror,
-                            const double* __restrict__ dm, double* __restrict__ dmr, unsigned long long* chk) {
+                            const double* __restrict__ dm, double* __restrict__ dmr, unsigned long long* chk,
+                            const uint8_t* __restrict__ own) {
     const int lane = threadIdx.x & 31;
     const int64_t p = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
     double dmax = 0.0, amax = 0.0;
@@ -91,6 +92,9 @@ __global__ void k_dm_repack(SysParams P, int64_t npair, int nspin, int64_t nnz, 
         R1 = pR[3 * p + 1];
         R2 = pR[3 * p + 2];
         canon = (a != b) ? a < b : (R0 != 0 ? R0 > 0 : (R1 != 0 ? R1 > 0 : R2 >= 0));
+        // shard-local input (kbg_grid_pass on a sharded context): only the pairs this rank's blocks
+        // touch are read (dm may be mapped host memory); the others are never used by its rho kernel
+        if (own && !own[p]) canon = false;
     }
     if (canon) {
         const double fac = (a == b && R0 == 0 && R1 == 0 && R2 == 0) ? 1.0 : 2.0;
@@ -400,11 +404,11 @@ int launch_finalize(const DevIndex& ix, const SysParams& sys, int nspin, const d
 }
 
 int launch_dm_repack(const DevIndex& ix, const SysParams& sys, int nspin, const double* dm, double* dmr,
-                     cudaStream_t st, unsigned long long* chk) {
+                     cudaStream_t st, unsigned long long* chk, const uint8_t* own) {
     if (ix.npair == 0) return 0;
     const unsigned grid = static_cast<unsigned>((ix.npair * 32 + 255) / 256);
     k_dm_repack<<<grid, 256, 0, st>>>(sys, ix.npair, nspin, ix.nnz, ix.nrep, ix.pair_a, ix.pair_b, ix.pair_R,
-                                      ix.pair_off, ix.pair_roff, ix.pair_mirror, dm, dmr, chk);
+                                      ix.pair_off, ix.pair_roff, ix.pair_mirror, dm, dmr, chk, own);
     KBG_CUDA(cudaGetLastError());
     return 1;
 }

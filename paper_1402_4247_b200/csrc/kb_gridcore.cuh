@@ -17,6 +17,8 @@
 //   rho(slot) += sum_rows Phi_g * Y once per task.
 #pragma once
 
+#include <type_traits>
+
 #include "kb_device.cuh"
 
 // L2 policy of the persistent kernels: 1 streams the geometry cache with
@@ -481,34 +483,43 @@ __device__ __forceinline__ void h_tile2(const Smem& sm, const double* __restrict
     const double* pb2 = sm.phi() + rb2 * 64 + (lane & 3);
     const int sa = swz(ra), sb1 = swz(rb1), sb2 = swz(rb2);
     const double* pw = w + (lane & 3);
-    uint32_t qm = q1 | q2;
-    while (qm) {
-        const int q = __ffs(qm) - 1;
-        qm &= qm - 1;
-        const int col = 4 * q;
-        const double wv = pw[col];
-        double a[TM];
-#pragma unroll
-        for (int i = 0; i < TM; ++i) a[i] = KBG_H_NOSCALE ? pa[i * 512 + (col ^ sa)] : pa[i * 512 + (col ^ sa)] * wv;
-        if ((q1 >> q) & 1u) {
-            double bb[TN1];
-#pragma unroll
-            for (int j = 0; j < TN1; ++j) bb[j] = pb1[j * 512 + (col ^ sb1)];
+    // Three loops -- quads of both partners, of cj1 only, of cj2 only -- so every DMMA is
+    // unconditional: a DMMA under a per-quad predicate the compiler cannot prove warp-uniform
+    // costs a WARPSYNC + NOP pair each (SASS of the single merged loop, profiles/ncu_h_r2.txt).
+    auto run = [&](uint32_t qm, auto with1, auto with2) {
+        constexpr bool W1 = decltype(with1)::value, W2 = decltype(with2)::value;
+        while (qm) {
+            const int q = __ffs(qm) - 1;
+            qm &= qm - 1;
+            const int col = 4 * q;
+            const double wv = pw[col];
+            double a[TM];
 #pragma unroll
             for (int i = 0; i < TM; ++i)
+                a[i] = KBG_H_NOSCALE ? pa[i * 512 + (col ^ sa)] : pa[i * 512 + (col ^ sa)] * wv;
+            if (W1) {
+                double bb[TN1];
 #pragma unroll
-                for (int j = 0; j < TN1; ++j) dmma(c1[i][j], a[i], bb[j]);
+                for (int j = 0; j < TN1; ++j) bb[j] = pb1[j * 512 + (col ^ sb1)];
+#pragma unroll
+                for (int i = 0; i < TM; ++i)
+#pragma unroll
+                    for (int j = 0; j < TN1; ++j) dmma(c1[i][j], a[i], bb[j]);
+            }
+            if (W2) {
+                double bb[TN2];
+#pragma unroll
+                for (int j = 0; j < TN2; ++j) bb[j] = pb2[j * 512 + (col ^ sb2)];
+#pragma unroll
+                for (int i = 0; i < TM; ++i)
+#pragma unroll
+                    for (int j = 0; j < TN2; ++j) dmma(c2[i][j], a[i], bb[j]);
+            }
         }
-        if ((q2 >> q) & 1u) {
-            double bb[TN2];
-#pragma unroll
-            for (int j = 0; j < TN2; ++j) bb[j] = pb2[j * 512 + (col ^ sb2)];
-#pragma unroll
-            for (int i = 0; i < TM; ++i)
-#pragma unroll
-                for (int j = 0; j < TN2; ++j) dmma(c2[i][j], a[i], bb[j]);
-        }
-    }
+    };
+    run(q1 & q2, std::true_type{}, std::true_type{});
+    run(q1 & ~q2, std::true_type{}, std::false_type{});
+    run(q2 & ~q1, std::false_type{}, std::true_type{});
     h_scatter<DET, TM, TN1>(sm, c1, ncov, cj1, ra0, rend, 0, H, sign, scatter, lane);
     h_scatter<DET, TM, TN2>(sm, c2, ncov, cj2, ra0, rend, 0, H, sign, scatter, lane);
 }
@@ -523,32 +534,97 @@ __device__ __forceinline__ void h_tile2_tn2(int tn2, const Smem& sm, const doubl
         h_tile2<DET, TM, TN1, 1>(sm, w, ncov, cj1, cj2, ra0, rend, q1, q2, H, sign, scatter, lane);
 }
 
+// One H element into the accumulator (FP64 RED, or the deterministic two-limb split).
 template <bool DET>
+__device__ __forceinline__ void h_add(double* __restrict__ H, int64_t idx, double v) {
+    if (DET) {
+        const double hi = __dsub_rn(__dadd_rn(v, s_hscale.c1), s_hscale.c1);
+        const double lo = __dsub_rn(__dadd_rn(__dsub_rn(v, hi), s_hscale.c2), s_hscale.c2);
+        double* p = H + (KBG_DET_SPLIT ? 1 : 2) * idx;
+        red_add(p, hi);
+        red_add(p + s_hscale.lo, lo);
+    } else {
+        red_add(H + idx, v);
+    }
+}
+
+// A5's sparse alternative (north star: DMMA "only where the atom-pair orbital block is dense enough,
+// otherwise warp-shuffle reductions"): the same task as point-exact FP64 FMAs over the common points
+// only (no quad padding). Lane l owns row (l & 15) of the group and 8 columns (half l >> 4) of the
+// partner; per common point one A value (scaled by w) and 8 B values, which all 16 lanes of a half
+// warp read at the same address (shared-memory broadcast). Selected per task by its point density
+// (Task.pad2_, kb_tasks.cu) below the KBG_OPT_SPARSE_DFMA threshold (scatter bits 8..15).
+template <bool DET>
+__device__ __forceinline__ void h_task_dfma(const Smem& sm, const double* __restrict__ w, int ncov, const Task& t,
+                                         double* __restrict__ H, double sign, int lane) {
+    const GroupS& G = sm.grp()[t.g];
+    const int r = G.row0 + (lane & 15);
+    const bool row_ok = (lane & 15) < G.rows;
+    const int ci = row_ok ? sm.rcov()[r] : kNoCover;
+    const int ri = sm.rorb()[r];
+    const double* phi = sm.phi();
+    for (int k = 0; k < 2; ++k) {
+        const int cj = k ? t.cj2 : t.cj;
+        if (cj == kNoCover) break;
+        const CoverS& B = sm.cov()[cj];
+        uint64_t m = 0;  // exact common points of the group's canonical rows and cj
+        for (int c = G.first; c < G.end && c <= cj; ++c) m |= sm.cov()[c].mask & B.mask;
+        const int nb = B.norb, c0 = 8 * (lane >> 4);
+        double acc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+        while (m) {
+            const int p = __ffsll(m) - 1;
+            m &= m - 1;
+            const double a = phi[phi_idx(r, p)] * w[p];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int rb = B.row0 + min(c0 + j, nb - 1);
+                acc[j] = fma(a, phi[phi_idx(rb, p)], acc[j]);
+            }
+        }
+        const int off = ci <= cj ? sm.off2d()[ci * ncov + cj] : -1;
+        if (off >= 0)
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (c0 + j < nb) h_add<DET>(H, off + ri * nb + c0 + j, sign * acc[j]);
+    }
+}
+
+template <bool DET, bool SPARSE = false>
 __device__ __forceinline__ void h_task(const Smem& sm, const double* w, int ncov, const Task& t, double* H,
                                        double sign, int scatter, int lane) {
+    if (SPARSE && t.pad2_ < (scatter >> 8)) {
+        h_task_dfma<DET>(sm, w, ncov, t, H, sign, lane);
+        return;
+    }
     const GroupS& G = sm.grp()[t.g];
     const int rend = G.row0 + G.rows;
+    // quad masks made provably warp-uniform (a shuffle from lane 0): the DMMA loops over them then
+    // need no WARPSYNC (mma.sync requires the converged warp)
+    const uint32_t q1 = __shfl_sync(0xffffffffu, static_cast<uint32_t>(t.qmask), 0);
     if (t.cj2 != 0xFF) {  // paired partners: group <= 16 rows, partners <= 16 orbitals
+        const uint32_t q2 = __shfl_sync(0xffffffffu, static_cast<uint32_t>(t.qmask2), 0);
         const int tn1 = (sm.cov()[t.cj].norb + 7) >> 3, tn2 = (sm.cov()[t.cj2].norb + 7) >> 3;
         if (G.tm == 2) {
             if (tn1 == 2)
-                h_tile2_tn2<DET, 2, 2>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, t.qmask, t.qmask2, H, sign, scatter,
+                h_tile2_tn2<DET, 2, 2>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, q1, q2, H, sign, scatter,
                                   lane);
             else
-                h_tile2_tn2<DET, 2, 1>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, t.qmask, t.qmask2, H, sign, scatter,
+                h_tile2_tn2<DET, 2, 1>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, q1, q2, H, sign, scatter,
                                   lane);
         } else {
             if (tn1 == 2)
-                h_tile2_tn2<DET, 1, 2>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, t.qmask, t.qmask2, H, sign, scatter,
+                h_tile2_tn2<DET, 1, 2>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, q1, q2, H, sign, scatter,
                                   lane);
             else
-                h_tile2_tn2<DET, 1, 1>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, t.qmask, t.qmask2, H, sign, scatter,
+                h_tile2_tn2<DET, 1, 1>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, q1, q2, H, sign, scatter,
                                   lane);
         }
         return;
     }
     const int nb = sm.cov()[t.cj].norb;
-    const uint32_t qm = t.qmask;
+    const uint32_t qm = q1;
     for (int i0 = 0; i0 < G.tm; i0 += 2) {
         const int tm = min(2, G.tm - i0);
         for (int j0 = 0; j0 < (nb + 7) >> 3; j0 += 2) {

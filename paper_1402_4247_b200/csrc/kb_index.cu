@@ -15,13 +15,13 @@ template <class T>
 T* dalloc(size_t n) {
     T* p = nullptr;
     if (n == 0) n = 1;
-    KBG_CUDA(cudaMalloc(&p, n * sizeof(T)));
+    KBG_CUDA(pool_malloc(&p, n * sizeof(T)));
     return p;
 }
 
 template <class T>
 void dfree(T*& p) {
-    if (p) cudaFree(p);
+    if (p) pool_free(p);
     p = nullptr;
 }
 
@@ -36,7 +36,7 @@ T exclusive_scan(T* d_in_np1, T* d_out_np1, int64_t n, cudaStream_t st) {
     T total;
     KBG_CUDA(cudaMemcpyAsync(&total, d_out_np1 + n, sizeof(T), cudaMemcpyDeviceToHost, st));
     KBG_CUDA(cudaStreamSynchronize(st));
-    cudaFree(tmp);
+    pool_free(tmp);
     return total;
 }
 
@@ -354,6 +354,34 @@ __global__ void k_bp_fill(SysParams P, int64_t nblock, const int32_t* __restrict
 
 }  // namespace
 
+namespace {
+__global__ void k_iota(int64_t b0, int64_t n, int64_t* out) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n) out[i] = b0 + i;
+}
+}  // namespace
+
+void block_order_device(DevIndex& ix, int64_t b0, int64_t b1, bool heaviest_first, cudaStream_t st) {
+    const int64_t n = b1 - b0;
+    ix.order = dalloc<int64_t>(std::max<int64_t>(1, n));
+    ix.norder = n;
+    if (n <= 0) return;
+    int64_t* ids = heaviest_first ? dalloc<int64_t>(n) : ix.order;
+    k_iota<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(b0, n, ids);
+    KBG_CUDA(cudaGetLastError());
+    if (!heaviest_first) return;
+    int64_t* keys_out = dalloc<int64_t>(n);
+    size_t bytes = 0;
+    KBG_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, ix.blk_cost + b0, keys_out, ids, ix.order,
+                                                       static_cast<int>(n), 0, 64, st));
+    void* tmp = dalloc<char>(bytes);
+    KBG_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp, bytes, ix.blk_cost + b0, keys_out, ids, ix.order,
+                                                       static_cast<int>(n), 0, 64, st));
+    pool_free(tmp);
+    pool_free(keys_out);
+    pool_free(ids);
+}
+
 void free_index(DevIndex& ix) {
     free_cache(ix);
     free_tasks(ix);
@@ -418,7 +446,7 @@ void build_index_device(const SysParams& P, DevIndex& ix, cudaStream_t st) {
         KBG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, tkey, skey, tmask, smask, static_cast<int>(ntask), 0, 64,
                                                  st));
         KBG_CUDA(cudaStreamSynchronize(st));
-        cudaFree(tmp);
+        pool_free(tmp);
     }
     unsigned long long ncover_h = 0;
     KBG_CUDA(cudaMemcpy(&ncover_h, d_ncover, sizeof(ncover_h), cudaMemcpyDeviceToHost));
@@ -434,17 +462,17 @@ void build_index_device(const SysParams& P, DevIndex& ix, cudaStream_t st) {
                                                              ix.cov_mask, bcnt);
     KBG_CUDA(cudaGetLastError());
     exclusive_scan(bcnt, ix.blk_ptr, nblock, st);
-    cudaFree(bcnt);
-    cudaFree(tkey);
-    cudaFree(tmask);
-    cudaFree(skey);
-    cudaFree(smask);
-    cudaFree(tcnt);
-    cudaFree(toff);
-    cudaFree(d_ncover);
-    cudaFree(cand);
-    cudaFree(cnt);
-    cudaFree(coff);
+    pool_free(bcnt);
+    pool_free(tkey);
+    pool_free(tmask);
+    pool_free(skey);
+    pool_free(smask);
+    pool_free(tcnt);
+    pool_free(toff);
+    pool_free(d_ncover);
+    pool_free(cand);
+    pool_free(cnt);
+    pool_free(coff);
 
     // 4. pairs (a, b, R), lexicographic
     const int64_t nab = static_cast<int64_t>(natom) * natom;
@@ -459,8 +487,8 @@ void build_index_device(const SysParams& P, DevIndex& ix, cudaStream_t st) {
     ix.pair_R = dalloc<int32_t>(3 * ix.npair);
     k_pairs<<<grid_of(nab, 128), 128, 0, st>>>(P, nullptr, poff, ix.pair_a, ix.pair_b, ix.pair_R);
     KBG_CUDA(cudaGetLastError());
-    cudaFree(pcnt);
-    cudaFree(poff);
+    pool_free(pcnt);
+    pool_free(poff);
     int64_t* psize = dalloc<int64_t>(ix.npair + 1);
     ix.pair_off = dalloc<int64_t>(ix.npair + 1);
     ix.pair_key = dalloc<int64_t>(ix.npair);
@@ -483,11 +511,11 @@ void build_index_device(const SysParams& P, DevIndex& ix, cudaStream_t st) {
     ix.pair_roff = dalloc<int64_t>(ix.npair + 1);
     ix.nrep = exclusive_scan(psize, ix.pair_roff, ix.npair, st);
     if (ix.nrep >= (int64_t(1) << 31)) throw Error(KBG_ERR_DIMENSION, "build_index: repacked density matrix too large");
-    cudaFree(psize);
+    pool_free(psize);
     int herr = 0;
     KBG_CUDA(cudaMemcpy(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost));
     if (herr) {
-        cudaFree(d_err);
+        pool_free(d_err);
         throw Error(KBG_ERR_CONSISTENCY, "build_index: pair list not closed under (a,b,R) -> (b,a,-R)");
     }
 
@@ -502,7 +530,7 @@ void build_index_device(const SysParams& P, DevIndex& ix, cudaStream_t st) {
     k_bp_count<<<wgrid, T, 0, st>>>(P, nblock, ix.blk_ptr, ix.cov_atom, ix.cov_mask, bpc, ix.blk_cost, d_stats);
     KBG_CUDA(cudaGetLastError());
     ix.nbpair = exclusive_scan(bpc, ix.bp_ptr, nblock, st);
-    cudaFree(bpc);
+    pool_free(bpc);
     ix.bp = dalloc<BPair>(ix.nbpair);
     k_bp_fill<<<wgrid, T, 0, st>>>(P, nblock, ix.blk_ptr, ix.cov_atom, ix.cov_R, ix.cov_mask, ix.bp_ptr, ix.pair_key,
                                    ix.pair_off, ix.pair_roff, ix.npair, ix.bp, d_err);
@@ -511,8 +539,8 @@ void build_index_device(const SysParams& P, DevIndex& ix, cudaStream_t st) {
     KBG_CUDA(cudaMemcpyAsync(&hs, d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, st));
     KBG_CUDA(cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
     KBG_CUDA(cudaStreamSynchronize(st));
-    cudaFree(d_stats);
-    cudaFree(d_err);
+    pool_free(d_stats);
+    pool_free(d_err);
     if (herr)
         throw Error(KBG_ERR_CONSISTENCY, "build_index: block " + std::to_string(herr - 1) +
                                              " has covers that share points but form no pair");

@@ -209,9 +209,28 @@ struct GridArgs {
     uint32_t lay[13];
 };
 
+// Allocations of the once-per-geometry build (index, task lists, geometry cache,
+// comm tables): stream-ordered from the device's default memory pool with an
+// unlimited release threshold, on the stream set by BuildStream (the context's
+// stream), so a rebuild re-uses the pool without cudaMalloc/cudaFree round
+// trips and implicit device synchronizations.
+struct BuildStream {
+    explicit BuildStream(cudaStream_t st);
+    ~BuildStream();
+    cudaStream_t prev;
+};
+cudaError_t pool_malloc_bytes(void** p, size_t bytes);
+void pool_free(void* p);
+template <class T>
+cudaError_t pool_malloc(T** p, size_t bytes) {
+    return pool_malloc_bytes(reinterpret_cast<void**>(p), bytes);
+}
+
 // Index build (kb_index.cu). Fills `ix` (device) and returns host stats.
 void build_index_device(const SysParams& sys, DevIndex& ix, cudaStream_t st);
 void free_index(DevIndex& ix);
+// ix.order = owned blocks [b0, b1), by descending blk_cost (stable) or in block order.
+void block_order_device(DevIndex& ix, int64_t b0, int64_t b1, bool heaviest_first, cudaStream_t st);
 void copy_index_to_host(const DevIndex& ix, HostIndex& h, cudaStream_t st);
 
 // Orbital / offset tables of the format converters (kb_formats.cu), built
@@ -307,7 +326,7 @@ void free_tasks(DevIndex& ix);
 int launch_density(const GridArgs& g, int64_t nblk_owned, int nwarps, cudaStream_t st);
 int launch_hamiltonian(const GridArgs& g, int64_t nblk_owned, int nwarps, cudaStream_t st);
 int launch_dm_repack(const DevIndex& ix, const SysParams& sys, int nspin, const double* dm, double* dmr,
-                     cudaStream_t st, unsigned long long* chk = nullptr);
+                     cudaStream_t st, unsigned long long* chk = nullptr, const uint8_t* own = nullptr);
 // Persistent warp-specialized kernels (kb_persist.cu): kPersistProducers
 // producer warps stage block k+1 while kPersistConsumers consumer warps work
 // on block k (two shared-memory buffers). persist_fits() says whether two

@@ -273,7 +273,7 @@ __device__ void producer(const GridArgs& g, const Buffers<DENSITY>& B, int lane)
     }
 }
 
-template <bool DENSITY, bool DET>
+template <bool DENSITY, bool DET, bool SPARSE>
 __device__ void consumer(const GridArgs& g, const Buffers<DENSITY>& B, int cw, int lane) {
     constexpr int NC = Cfg<DENSITY>::NC;
     unsigned long long t_wait = 0, t_tail = 0, t0 = clock64();
@@ -314,7 +314,7 @@ __device__ void consumer(const GridArgs& g, const Buffers<DENSITY>& B, int cw, i
                     __syncwarp();
                     rho_task(sm, ncov, t, g.dmr + spin * g.nrep, res - 32 * t.half, lane, g.scatter);
                 } else {
-                    h_task<DET>(sm, sm.acc() + spin * 64, ncov, t, g.out + spin * g.nnz * (DET ? 2 : 1), g.sign,
+                    h_task<DET, SPARSE>(sm, sm.acc() + spin * 64, ncov, t, g.out + spin * g.nnz * (DET ? 2 : 1), g.sign,
                                 g.scatter, lane);
                 }
             }
@@ -332,7 +332,7 @@ __device__ void consumer(const GridArgs& g, const Buffers<DENSITY>& B, int cw, i
                 double* Hs = g.out + spin * g.nnz * (DET ? 2 : 1);
                 for (int w = cw; w < g.task_warps; w += NC)
                     for (int e = sm.wptr()[w]; e < sm.wptr()[w + 1]; ++e)
-                        h_task<DET>(sm, sm.acc() + spin * 64, ncov, sm.task()[e], Hs, g.sign, g.scatter, lane);
+                        h_task<DET, SPARSE>(sm, sm.acc() + spin * 64, ncov, sm.task()[e], Hs, g.sign, g.scatter, lane);
             }
         }
         __syncwarp();
@@ -409,7 +409,7 @@ __device__ void consumer(const GridArgs& g, const Buffers<DENSITY>& B, int cw, i
     }
 }
 
-template <bool DENSITY, bool DET>
+template <bool DENSITY, bool DET, bool SPARSE = false>
 __global__ void __launch_bounds__(Cfg<DENSITY>::NT, 1) k_persist(GridArgs g) {
     const Buffers<DENSITY> B = carve_all<DENSITY>(g);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(Cfg<DENSITY>::NT, 1) k_persist(GridArgs g) {
     if (warp < kPersistProducers) {
         if (warp == 0) producer<DENSITY, DET>(g, B, lane);
     } else {
-        consumer<DENSITY, DET>(g, B, warp - kPersistProducers, lane);
+        consumer<DENSITY, DET, SPARSE>(g, B, warp - kPersistProducers, lane);
     }
 }
 
@@ -447,12 +447,18 @@ int launch_persist(const GridArgs& g0, bool density, cudaStream_t st) {
     if (density) {
         set_smem(k_persist<true, false>, smem);
         k_persist<true, false><<<grid, Cfg<true>::NT, smem, st>>>(g);
-    } else if (g.scatter & 16) {  // deterministic two-limb scatter (KBG_OPT_DETERMINISTIC)
-        set_smem(k_persist<false, true>, smem);
-        k_persist<false, true><<<grid, Cfg<false>::NT, smem, st>>>(g);
     } else {
-        set_smem(k_persist<false, false>, smem);
-        k_persist<false, false><<<grid, Cfg<false>::NT, smem, st>>>(g);
+        // deterministic two-limb scatter (KBG_OPT_DETERMINISTIC) x point-exact FP64 path for sparse
+        // tasks (KBG_OPT_SPARSE_DFMA): separate instantiations, so the default kernel carries neither
+        auto go = [&](auto kernel) {
+            set_smem(kernel, smem);
+            kernel<<<grid, Cfg<false>::NT, smem, st>>>(g);
+        };
+        const bool det = g.scatter & 16, sparse = (g.scatter >> 8) != 0;
+        if (sparse)
+            det ? go(k_persist<false, true, true>) : go(k_persist<false, false, true>);
+        else
+            det ? go(k_persist<false, true, false>) : go(k_persist<false, false, false>);
     }
     KBG_CUDA(cudaGetLastError());
     return 1;

@@ -19,7 +19,7 @@ template <class T>
 T* talloc(size_t n) {
     T* p = nullptr;
     if (n == 0) n = 1;
-    KBG_CUDA(cudaMalloc(&p, n * sizeof(T)));
+    KBG_CUDA(pool_malloc(&p, n * sizeof(T)));
     return p;
 }
 
@@ -31,7 +31,7 @@ int64_t scan_total(int64_t* cnt, int64_t* ptr, int64_t n, cudaStream_t st) {
     int64_t total = 0;
     KBG_CUDA(cudaMemcpyAsync(&total, ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     KBG_CUDA(cudaStreamSynchronize(st));
-    cudaFree(tmp);
+    pool_free(tmp);
     return total;
 }
 
@@ -62,6 +62,14 @@ __global__ void k_tasks(SysParams P, int64_t nblock, const int32_t* __restrict__
         // <= 16 orbitals and the group <= 16 rows (the pair shares A fragments)
         int pend = -1;
         uint32_t pend_q = 0;
+        // point density of a partner: exact common points over the points of the executed quads
+        auto dens = [&](int cj, uint32_t q, int64_t& ex, int64_t& pts) {
+            uint64_t m = 0;
+            for (int ci = g_first[g]; ci < g_end[g] && ci <= cj; ++ci) m |= cov_mask[c0 + ci] & cov_mask[c0 + cj];
+            const int tn = (norb[cj] + 7) >> 3;
+            ex += static_cast<int64_t>(__popcll(m)) * tn;
+            pts += 4LL * __popc(q) * tn;
+        };
         auto emit = [&](int c1, uint32_t q1, int c2, uint32_t q2) {
             if (hout) {
                 Task t;
@@ -74,11 +82,17 @@ __global__ void k_tasks(SysParams P, int64_t nblock, const int32_t* __restrict__
                 t.cj2 = 0xFF;
                 t.pad2_ = 0;
                 t.qmask2 = 0;
+                int64_t ex = 0, pts = 0;
+                dens(c1, q1, ex, pts);
                 if (c2 >= 0) {
                     t.cj2 = static_cast<uint8_t>(c2);
                     t.qmask2 = static_cast<uint16_t>(q2);
                     cost += static_cast<int64_t>(__popc(q2)) * tm * ((norb[c2] + 7) >> 3) + 1;
+                    dens(c2, q2, ex, pts);
                 }
+                // density in 1/255 (A5 switch, KBG_OPT_SPARSE_DFMA): tasks below the threshold run the
+                // point-exact FP64 path (kb_gridcore.cuh h_task_dfma) instead of DMMA over whole quads
+                t.pad2_ = static_cast<uint8_t>(pts ? (255 * ex + pts / 2) / pts : 255);
                 t.cost = sat16(cost);
                 hout[hptr[b] + nh] = t;
             }
@@ -201,16 +215,42 @@ __global__ void k_tasks_lpt(int64_t nblock, int W, const int64_t* __restrict__ p
     for (int i = 0; i < n; ++i) out[p0 + pos[t[i].pad_]++] = t[i];
 }
 
+// W == 1 (one task queue per block, the persistent kernels' default): the LPT
+// assignment degenerates to a stable sort by descending cost. One warp per
+// block ranks its tasks (rank = heavier tasks + equal tasks before it) and
+// scatters them -- the same order as k_tasks_lpt, without its serial insertion
+// sort through global memory.
+__global__ void k_tasks_sort(int64_t nblock, const int64_t* __restrict__ ptr, const Task* __restrict__ tmp, Task* out,
+                             int32_t* wptr) {
+    const int64_t b = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (b >= nblock) return;
+    const int64_t p0 = ptr[b];
+    const int n = static_cast<int>(ptr[b + 1] - p0);
+    for (int i = lane; i < n; i += 32) {
+        Task t = tmp[p0 + i];
+        int rank = 0;
+        for (int j = 0; j < n; ++j) {
+            const uint16_t cj = tmp[p0 + j].cost;
+            rank += (cj > t.cost) || (cj == t.cost && j < i);
+        }
+        t.pad_ = 0;
+        out[p0 + rank] = t;
+    }
+    int32_t* wp = wptr + b * (kMaxTaskWarps + 1);
+    for (int w = lane; w <= kMaxTaskWarps; w += 32) wp[w] = w == 0 ? 0 : n;
+}
+
 }  // namespace
 
 void free_tasks(DevIndex& ix) {
     for (void* p : {static_cast<void*>(ix.ht_ptr), static_cast<void*>(ix.ht), static_cast<void*>(ix.ht_wptr),
                     static_cast<void*>(ix.rt_ptr), static_cast<void*>(ix.rt), static_cast<void*>(ix.rt_wptr)})
-        if (p) cudaFree(p);
+        if (p) pool_free(p);
     ix.ht_ptr = ix.rt_ptr = nullptr;
     ix.ht = ix.rt = nullptr;
     ix.ht_wptr = ix.rt_wptr = nullptr;
-    if (ix.blk_rows) cudaFree(ix.blk_rows);
+    if (ix.blk_rows) pool_free(ix.blk_rows);
     ix.blk_rows = nullptr;
 }
 
@@ -244,17 +284,24 @@ void build_tasks_device(const SysParams& P, DevIndex& ix, int h_warps, int r_war
     ix.rt = talloc<Task>(ix.nrtask);
     ix.ht_wptr = talloc<int32_t>(nb * (kMaxTaskWarps + 1));
     ix.rt_wptr = talloc<int32_t>(nb * (kMaxTaskWarps + 1));
-    k_tasks_lpt<<<grid, T, 0, st>>>(nb, h_warps, ix.ht_ptr, htmp, ix.ht, ix.ht_wptr);
-    k_tasks_lpt<<<grid, T, 0, st>>>(nb, r_warps, ix.rt_ptr, rtmp, ix.rt, ix.rt_wptr);
+    const unsigned wgrid = static_cast<unsigned>((nb * 32 + 255) / 256);
+    if (h_warps == 1)
+        k_tasks_sort<<<wgrid, 256, 0, st>>>(nb, ix.ht_ptr, htmp, ix.ht, ix.ht_wptr);
+    else
+        k_tasks_lpt<<<grid, T, 0, st>>>(nb, h_warps, ix.ht_ptr, htmp, ix.ht, ix.ht_wptr);
+    if (r_warps == 1)
+        k_tasks_sort<<<wgrid, 256, 0, st>>>(nb, ix.rt_ptr, rtmp, ix.rt, ix.rt_wptr);
+    else
+        k_tasks_lpt<<<grid, T, 0, st>>>(nb, r_warps, ix.rt_ptr, rtmp, ix.rt, ix.rt_wptr);
     KBG_CUDA(cudaGetLastError());
     TaskStats hs;
     KBG_CUDA(cudaMemcpyAsync(&hs, d_st, sizeof(hs), cudaMemcpyDeviceToHost, st));
     KBG_CUDA(cudaStreamSynchronize(st));
-    cudaFree(hcnt);
-    cudaFree(rcnt);
-    cudaFree(d_st);
-    cudaFree(htmp);
-    cudaFree(rtmp);
+    pool_free(hcnt);
+    pool_free(rcnt);
+    pool_free(d_st);
+    pool_free(htmp);
+    pool_free(rtmp);
     if (hs.too_many_covers)
         throw Error(KBG_ERR_DIMENSION, "a grid block is covered by " + std::to_string(hs.too_many_covers) +
                                            " atom images (max " + std::to_string(kMaxCoverPerBlock) + ")");

@@ -142,8 +142,9 @@ class GridPass:
         veff = self._spin_array(veff, self.system.npts, "grid_pass: veff")
         if dm.shape[0] != veff.shape[0]:
             raise_for_status(_abi.KBG_ERR_DIMENSION, "grid_pass", "dm and veff spin counts differ")
-        rho = np.empty((dm.shape[0], self.system.npts))
-        h = np.empty((dm.shape[0], self._nnz()))
+        # sharded contexts write only their share of rho and H (KBG_OPT_SHARD_IO): zeros elsewhere
+        rho = np.zeros((dm.shape[0], self.system.npts))
+        h = np.zeros((dm.shape[0], self._nnz()))
         self._check(self._lib.kbg_grid_pass(self._h, dm.shape[0], _abi.dptr(dm), _abi.dptr(veff), dV, _abi.dptr(rho),
                                             _abi.dptr(h)), "kbg_grid_pass")
         return rho, h
@@ -223,6 +224,13 @@ class GridPass:
         self._check(self._lib.kbg_hamiltonian_allreduce_dev(self._h, veff.shape[0], veff.data_ptr(), dV, h.data_ptr(),
                                                             self._stream_ptr(stream)),
                     "kbg_hamiltonian_allreduce_dev")
+
+    def shard_io(self) -> dict:
+        """Shard-local I/O ranges of kbg_grid_pass on this sharded context (after comm_open)."""
+        v = (C.c_int64 * 8)()
+        self._check(self._lib.kbg_shard_io(self._h, v), "kbg_shard_io")
+        keys = ("b0", "b1", "p0", "p1", "h0", "h1", "dm_read", "v_read")
+        return dict(zip(keys, (int(x) for x in v)))
 
     def comm_check(self) -> None:
         """After synchronizing a hamiltonian_allreduce_dev: raise if a peer never arrived."""

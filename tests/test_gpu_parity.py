@@ -358,3 +358,18 @@ def test_grid_pass_pinned_zero_copy(name, nspin):
     assert normwise(h_p, h) <= 1e-14
     assert normwise(h_p, c.o.hamiltonian(c.veff, c.f.dV)) <= TOL
     assert normwise(c.gp.hamiltonian(v_p, c.f.dV), h) <= 1e-14
+
+
+@pytest.mark.parametrize("name,thr", [("sweep56_100Ry", 255), ("cubic56_200Ry", 128)])
+def test_sparse_dfma_switch_parity(name, thr):
+    """A5's switch (KBG_OPT_SPARSE_DFMA): tasks below the point-density threshold run point-exact FP64
+    FMAs instead of DMMA (255: every task). Same H within rounding, oracle parity kept."""
+    c = case(name)
+    h_dmma = c.gp.hamiltonian(c.veff, c.f.dV)
+    c.gp.set_option(_abi.KBG_OPT_SPARSE_DFMA, thr)
+    try:
+        h = c.gp.hamiltonian(c.veff, c.f.dV)
+    finally:
+        c.gp.set_option(_abi.KBG_OPT_SPARSE_DFMA, 0)
+    assert normwise(h, h_dmma) <= 1e-13
+    assert_parity(h, c.o.hamiltonian(c.veff, c.f.dV))

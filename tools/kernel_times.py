@@ -29,8 +29,9 @@ def main():
     ap.add_argument("--fallback", type=int, default=1, help="also time the one-CTA-per-block kernels")
     ap.add_argument("--orders", default="0", help="KBG_OPT_BLOCK_ORDER values (persistent kernels)")
     ap.add_argument("--scatter", type=int, default=0, help="KBG_OPT_SCATTER_STORE timing experiment bits")
-    ap.add_argument("--det", type=int, default=1, help="KBG_OPT_DETERMINISTIC (1: two-limb exact scatter)")
+    ap.add_argument("--det", type=int, default=0, help="KBG_OPT_DETERMINISTIC (1: two-limb exact scatter)")
     ap.add_argument("--kernels", default="density,h_accumulate")
+    ap.add_argument("--sparse", type=int, default=0, help="KBG_OPT_SPARSE_DFMA threshold (A5 switch)")
     a = ap.parse_args()
     f = Fe3O4.config(a.config)
     dev = torch.device("cuda", 0)
@@ -63,6 +64,7 @@ def main():
         plan = gp.plan_info()
         gp.set_option(_abi.KBG_OPT_SCATTER_STORE, a.scatter)
         gp.set_option(_abi.KBG_OPT_DETERMINISTIC, a.det)
+        gp.set_option(_abi.KBG_OPT_SPARSE_DFMA, a.sparse)
         d_dm = torch.from_numpy(f.dm(ix, nspin=a.nspin)).to(dev)
         d_v = torch.from_numpy(f.veff(nspin=a.nspin)).to(dev)
         rho = torch.empty((a.nspin, f.system.npts), dtype=torch.float64, device=dev)
@@ -83,7 +85,7 @@ def main():
             out.zero_()
             fn()
             torch.cuda.synchronize()
-            rec = {"config": a.config, "lib": os.environ.get("KBG_LIBKBGRID", "default"), "scatter_exp": a.scatter, "det": a.det, "kernel": name, "schedule": sched, "persist": persist,
+            rec = {"config": a.config, "lib": os.environ.get("KBG_LIBKBGRID", "default"), "scatter_exp": a.scatter, "det": a.det, "sparse": a.sparse, "kernel": name, "schedule": sched, "persist": persist,
                    "block_order": order, "plan": plan,
                    "median_ms": round(med, 4), "min_ms": round(mn, 4),
                    "alg_tflops": round(fl / (med * 1e-3) / 1e12, 3),

@@ -85,12 +85,19 @@ def main(cfg="cubic56_200Ry"):
     dm_p = torch.from_numpy(dm).pin_memory().numpy()
     v_p = torch.from_numpy(f.veff()).pin_memory().numpy()
     rho_g, h_g = gp.grid_pass(dm_p, v_p, f.dV)
-    d_gp = float(np.abs(h_g[0] - h_p2p.cpu().numpy()[0]).max() / np.abs(h_g[0]).max())
+    # shard-local host I/O (KBG_OPT_SHARD_IO): each rank returns its slice of H and its points of rho
+    # (zeros elsewhere), so the sums over ranks are the full H and rho
+    io = gp.shard_io()
+    h_t = torch.from_numpy(h_g).to(dev)
+    dist.all_reduce(h_t)
+    d_gp = float((h_t - h_p2p).abs().max() / h_p2p.abs().max())
     d_gp_t = torch.tensor([d_gp], device=dev)
     dist.all_reduce(d_gp_t, op=dist.ReduceOp.MAX)
     d_gp = float(d_gp_t.item())
     rho_t = torch.from_numpy(rho_g).to(dev)
     dist.all_reduce(rho_t)  # owned points only per rank: the sum is the full density
+    ios = [None] * world
+    dist.all_gather_object(ios, io)
 
     def local_ms(fn, reps=20):
         for _ in range(3):
@@ -159,7 +166,7 @@ def main(cfg="cubic56_200Ry"):
                           "h_ms_p2p": round(t_p2p, 4), "h_ms_nccl_incl_mirror": round(t_nccl, 4),
                           "h_ms_accumulate_only": round(t_acc, 4), "accumulate_ms_per_rank": acc_ranks,
                           "grid_pass_h_vs_p2p": d_gp, "grid_pass_rho_sum_vs_single_gpu": d_rho,
-                          "exchange_phases_us_per_rank": phases,
+                          "exchange_phases_us_per_rank": phases, "shard_io": ios,
                           "note": "deterministic H (KBG_OPT_DETERMINISTIC): the sharded H must equal the "
                                   "single-GPU H bit for bit and repeat bitwise",
                           "ok": bool(same_bits and det and d_nccl <= 1e-14 and d_gp == 0.0 and d_rho == 0.0
