@@ -104,35 +104,13 @@ __device__ __forceinline__ void phi_covers(const SysParams& P, const double* __r
         int bi, bj, bk;
         block_decode(P, b, bi, bj, bk);
         double r[2][3];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            int li, lj, lk;
-            slot_decode(2 * lane + h, li, lj, lk);
-            const double fi = static_cast<double>(bi * 4 + li) / P.N[0];
-            const double fj = static_cast<double>(bj * 4 + lj) / P.N[1];
-            const double fk = static_cast<double>(bk * 4 + lk) / P.N[2];
-#pragma unroll
-            for (int q = 0; q < 3; ++q) r[h][q] = fi * P.A[q] + fj * P.A[3 + q] + fk * P.A[6 + q];
-        }
+        slot_pair_pos(P, bi, bj, bk, lane, r);
         double* blk = phis + phi_off[b - b0];
         for (int c = first; c < end; ++c) {
             const CoverS cv = reinterpret_cast<const CoverS*>(img + o_cov)[c - first];
-            const DevSpecies& sp = P.sp[cv.sp];
             double* dst = blk + static_cast<int64_t>(cv.row0) * 64;
-            double d[2][3], d2[2];
-            bool in[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                in[h] = (cv.mask >> (2 * lane + h)) & 1;
-#pragma unroll
-                for (int q = 0; q < 3; ++q) d[h][q] = r[h][q] - cv.t[q];
-                d2[h] = d[h][0] * d[h][0] + d[h][1] * d[h][1] + d[h][2] * d[h][2];
-                if (!in[h]) d2[h] = 0.0;  // unused value, keeps the table index in range
-            }
-            eval_orbitals_pair(sp, tables, d, d2, [&](int o, double v0, double v1) {
-                const int row = cv.row0 + o;
-                const double2 v = make_double2(in[0] ? v0 : 0.0, in[1] ? v1 : 0.0);
-                *reinterpret_cast<double2*>(dst + o * 64 + ((2 * lane) ^ swz(row))) = v;
+            phi_slot_pair(P, tables, cv.t, cv.mask, cv.sp, r, lane, [&](int o, double2 v) {
+                *reinterpret_cast<double2*>(dst + o * 64 + ((2 * lane) ^ swz(cv.row0 + o))) = v;
             });
             if (c == end - 1) {  // 8 zero tail rows after the block's last cover (DMMA tile overrun)
                 double2* tail = reinterpret_cast<double2*>(dst + static_cast<int64_t>(cv.norb) * 64);

@@ -44,66 +44,34 @@ __device__ __forceinline__ double dist2_exact(const double d[3]) {
     return __dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])), __dmul_rn(d[2], d[2]));
 }
 
-// Orbitals of one atom at displacement d (inside the sphere): out[norb].
-// Cubic Hermite on the uniform radial table times real solid harmonics.
-template <class Sink>
-__device__ __forceinline__ void eval_orbitals(const DevSpecies& sp, const double* __restrict__ tables, double dx,
-                                              double dy, double dz, double d2, Sink&& sink) {
-    const double r = sqrt(d2);
-    const double x = r * sp.inv_h;
-    int k = static_cast<int>(x);
-    if (k > sp.ntab - 2) k = sp.ntab - 2;
-    const double t = x - k;
-    const double omt = 1.0 - t;
-    const double h00 = (1.0 + 2.0 * t) * omt * omt;
-    const double h10 = t * omt * omt * sp.h;
-    const double h01 = t * t * (3.0 - 2.0 * t);
-    const double h11 = t * t * (t - 1.0) * sp.h;
-    const double* tab = tables + sp.tab_off + 2 * k;
-    int o = 0;
-    for (int rad = 0; rad < sp.nrad; ++rad) {
-        const double2 a = __ldg(reinterpret_cast<const double2*>(tab + static_cast<long long>(rad) * sp.ntab * 2));
-        const double2 b = __ldg(reinterpret_cast<const double2*>(tab + static_cast<long long>(rad) * sp.ntab * 2 + 2));
-        const double u = h00 * a.x + h10 * a.y + h01 * b.x + h11 * b.y;
-        const int l = sp.l[rad];
-        if (l == 0) {
-            sink(o++, kC00 * u);
-        } else if (l == 1) {
-            const double cu = kC1 * u;
-            sink(o++, cu * dx);
-            sink(o++, cu * dy);
-            sink(o++, cu * dz);
-        } else {
-            sink(o++, kC20 * (2.0 * dz * dz - dx * dx - dy * dy) * u);
-            sink(o++, kC22 * (dx * dx - dy * dy) * u);
-            const double cu = kC2 * u;
-            sink(o++, cu * dx * dy);
-            sink(o++, cu * dx * dz);
-            sink(o++, cu * dy * dz);
-        }
-    }
-}
-
-// The same orbitals at two points at once (d[h], d2[h], h = 0, 1): one sink call
-// per orbital with both values (the geometry cache's 16-byte stores). `tables`
-// may point to shared memory (staged copy of the table array) or global memory.
+// Orbitals of one atom at two points (displacements d[h], squared lengths d2[h],
+// h = 0, 1): cubic Hermite on the uniform radial table (u = R / r^l and du/dr)
+// times real solid harmonics in the fixed order of include/kbgrid.h; one sink
+// call per orbital with both values (the geometry cache's 16-byte stores).
+// `tables` may point to shared memory (staged copy of the table array) or
+// global memory.
 template <class Sink>
 __device__ __forceinline__ void eval_orbitals_pair(const DevSpecies& sp, const double* __restrict__ tables,
                                                    const double (&d)[2][3], const double (&d2)[2], Sink&& sink) {
-    double h00[2], h10[2], h01[2], h11[2];
+    // Explicit round-to-nearest operations in the oracle's exact expression order
+    // (oracle/kbg_oracle.cpp orbitals(), compiled with -ffp-contract=off): no compiler-chosen FMA
+    // contraction, so every kernel that inlines this produces the same Phi bits -- the oracle's.
+    auto m = [](double x, double y) { return __dmul_rn(x, y); };
+    auto p = [](double x, double y) { return __dadd_rn(x, y); };
+    auto s = [](double x, double y) { return __dsub_rn(x, y); };
+    double h00[2], h10h[2], h01[2], h11h[2];
     const double* tab[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-        const double r = sqrt(d2[h]);
-        const double x = r * sp.inv_h;
+        const double x = __ddiv_rn(__dsqrt_rn(d2[h]), sp.h);
         int k = static_cast<int>(x);
         if (k > sp.ntab - 2) k = sp.ntab - 2;
-        const double t = x - k;
-        const double omt = 1.0 - t;
-        h00[h] = (1.0 + 2.0 * t) * omt * omt;
-        h10[h] = t * omt * omt * sp.h;
-        h01[h] = t * t * (3.0 - 2.0 * t);
-        h11[h] = t * t * (t - 1.0) * sp.h;
+        const double t = s(x, static_cast<double>(k));
+        const double omt = s(1.0, t);
+        h00[h] = m(m(p(1.0, m(2.0, t)), omt), omt);
+        h10h[h] = m(m(m(t, omt), omt), sp.h);
+        h01[h] = m(m(t, t), s(3.0, m(2.0, t)));
+        h11h[h] = m(m(m(t, t), s(t, 1.0)), sp.h);
         tab[h] = tables + sp.tab_off + 2 * k;
     }
     int o = 0;
@@ -113,25 +81,27 @@ __device__ __forceinline__ void eval_orbitals_pair(const DevSpecies& sp, const d
         for (int h = 0; h < 2; ++h) {
             const double2 a = *reinterpret_cast<const double2*>(tab[h] + static_cast<long long>(rad) * sp.ntab * 2);
             const double2 b = *reinterpret_cast<const double2*>(tab[h] + static_cast<long long>(rad) * sp.ntab * 2 + 2);
-            u[h] = h00[h] * a.x + h10[h] * a.y + h01[h] * b.x + h11[h] * b.y;
+            u[h] = p(p(p(m(h00[h], a.x), m(h10h[h], a.y)), m(h01[h], b.x)), m(h11h[h], b.y));
         }
         const int l = sp.l[rad];
         if (l == 0) {
-            sink(o++, kC00 * u[0], kC00 * u[1]);
+            sink(o++, m(kC00, u[0]), m(kC00, u[1]));
         } else if (l == 1) {
-            const double c0 = kC1 * u[0], c1 = kC1 * u[1];
-            sink(o++, c0 * d[0][0], c1 * d[1][0]);
-            sink(o++, c0 * d[0][1], c1 * d[1][1]);
-            sink(o++, c0 * d[0][2], c1 * d[1][2]);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) sink(o++, m(m(kC1, d[0][c]), u[0]), m(m(kC1, d[1][c]), u[1]));
         } else {
-            sink(o++, kC20 * (2.0 * d[0][2] * d[0][2] - d[0][0] * d[0][0] - d[0][1] * d[0][1]) * u[0],
-                 kC20 * (2.0 * d[1][2] * d[1][2] - d[1][0] * d[1][0] - d[1][1] * d[1][1]) * u[1]);
-            sink(o++, kC22 * (d[0][0] * d[0][0] - d[0][1] * d[0][1]) * u[0],
-                 kC22 * (d[1][0] * d[1][0] - d[1][1] * d[1][1]) * u[1]);
-            const double c0 = kC2 * u[0], c1 = kC2 * u[1];
-            sink(o++, c0 * d[0][0] * d[0][1], c1 * d[1][0] * d[1][1]);
-            sink(o++, c0 * d[0][0] * d[0][2], c1 * d[1][0] * d[1][2]);
-            sink(o++, c0 * d[0][1] * d[0][2], c1 * d[1][1] * d[1][2]);
+            double v[5][2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const double x = d[h][0], y = d[h][1], z = d[h][2];
+                v[0][h] = m(m(kC20, s(s(m(m(2.0, z), z), m(x, x)), m(y, y))), u[h]);
+                v[1][h] = m(m(kC22, s(m(x, x), m(y, y))), u[h]);
+                v[2][h] = m(m(m(kC2, x), y), u[h]);
+                v[3][h] = m(m(m(kC2, x), z), u[h]);
+                v[4][h] = m(m(m(kC2, y), z), u[h]);
+            }
+#pragma unroll
+            for (int q = 0; q < 5; ++q) sink(o++, v[q][0], v[q][1]);
         }
     }
 }

@@ -191,6 +191,39 @@ __device__ __forceinline__ int64_t slot_point(const SysParams& P, int bi, int bj
     return (static_cast<int64_t>(i) * P.N[1] + j) * P.N[2] + k;
 }
 
+// Positions of slots 2l and 2l + 1 of block (bi, bj, bk). The geometry cache and stage_block share
+// these expressions, written with explicit round-to-nearest operations (no FMA contraction left to
+// the compiler, like the oracle's -ffp-contract=off), so both produce the same Phi bits in any kernel.
+__device__ __forceinline__ void slot_pair_pos(const SysParams& P, int bi, int bj, int bk, int l, double (&r)[2][3]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        int li, lj, lk;
+        slot_decode(2 * l + h, li, lj, lk);
+        point_pos_exact(P, bi * 4 + li, bj * 4 + lj, bk * 4 + lk, r[h]);
+    }
+}
+
+// Orbitals of one cover (image position t, slot mask, species) at slots 2l, 2l + 1 (positions r):
+// sink(o, {value at 2l, value at 2l + 1}), exact zeros outside the mask.
+template <class Sink>
+__device__ __forceinline__ void phi_slot_pair(const SysParams& P, const double* __restrict__ tables,
+                                              const double (&t)[3], uint64_t mask, int sp, const double (&r)[2][3],
+                                              int l, Sink&& sink) {
+    double d[2][3], d2[2];
+    bool in[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        in[h] = (mask >> (2 * l + h)) & 1;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) d[h][q] = __dsub_rn(r[h][q], t[q]);
+        d2[h] = dist2_exact(d[h]);
+        if (!in[h]) d2[h] = 0.0;  // unused value, keeps the table index in range
+    }
+    eval_orbitals_pair(P.sp[sp], tables, d, d2, [&](int o, double v0, double v1) {
+        sink(o, make_double2(in[0] ? v0 : 0.0, in[1] ? v1 : 0.0));
+    });
+}
+
 // Stages block b into buffer sm using threads [0, nt) (tid = this thread's
 // index among them); sync() is a barrier over exactly those threads. For H
 // (density = false) also stages w = V dV for every spin; for rho zeroes the
@@ -218,8 +251,7 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int tid
         cv.norb = P.sp[cv.sp].norb;
         cv.mask = g.cov_mask[c0 + tid];
         const int R0 = g.cov_R[3 * (c0 + tid)], R1 = g.cov_R[3 * (c0 + tid) + 1], R2 = g.cov_R[3 * (c0 + tid) + 2];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) cv.t[c] = P.tau[3 * a + c] + ((R0 * P.A[c] + R1 * P.A[3 + c]) + R2 * P.A[6 + c]);
+        image_pos_exact(P, P.tau + 3 * a, R0, R1, R2, cv.t);  // the oracle's expression, no contraction
     }
     const int64_t tp0 = g.t_ptr[b];
     const int ntask = static_cast<int>(g.t_ptr[b + 1] - tp0);
@@ -280,26 +312,16 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int tid
     }
     if (eval_phi)
         for (int i = tid; i < 8 * 64; i += nt) sm.phi()[rows * 64 + i] = 0.0;  // tail rows (tile overrun)
-    for (int task = tid; eval_phi && task < ncov * 64; task += nt) {
-        const int c = task >> 6, s = task & 63;
+    // two slots per thread, the same expressions as the geometry cache (kb_cache.cu k_phi_cache):
+    // both Phi paths give the same bits, so H/rho do not depend on the kernel choice
+    for (int task = tid; eval_phi && task < ncov * 32; task += nt) {
+        const int c = task >> 5, l = task & 31;
         const CoverS& cv = sm.cov()[c];
-        double* dst = sm.phi();
-        const int row0 = cv.row0;
-        if ((cv.mask >> s) & 1) {
-            int li, lj, lk;
-            slot_decode(s, li, lj, lk);
-            const double fi = static_cast<double>(bi * 4 + li) / P.N[0];
-            const double fj = static_cast<double>(bj * 4 + lj) / P.N[1];
-            const double fk = static_cast<double>(bk * 4 + lk) / P.N[2];
-            const double dx = (fi * P.A[0] + fj * P.A[3] + fk * P.A[6]) - cv.t[0];
-            const double dy = (fi * P.A[1] + fj * P.A[4] + fk * P.A[7]) - cv.t[1];
-            const double dz = (fi * P.A[2] + fj * P.A[5] + fk * P.A[8]) - cv.t[2];
-            const double d2 = dx * dx + dy * dy + dz * dz;
-            eval_orbitals(P.sp[cv.sp], P.tables, dx, dy, dz, d2,
-                          [&](int o, double v) { dst[phi_idx(row0 + o, s)] = v; });
-        } else {
-            for (int o = 0; o < cv.norb; ++o) dst[phi_idx(row0 + o, s)] = 0.0;
-        }
+        double r[2][3];
+        slot_pair_pos(P, bi, bj, bk, l, r);
+        phi_slot_pair(P, P.tables, cv.t, cv.mask, cv.sp, r, l, [&](int o, double2 v) {
+            *reinterpret_cast<double2*>(sm.phi() + (cv.row0 + o) * 64 + ((2 * l) ^ swz(cv.row0 + o))) = v;
+        });
     }
     sync();
     constexpr int kParts = 8 / kRhoOct;
@@ -661,8 +683,10 @@ __device__ __forceinline__ void gather_a(const Smem& sm, int ncov, const int (&r
         const int ci = rci[t];
         const int off = ci <= cj ? sm.off2d()[ci * ncov + cj] : -1;  // ci = kNoCover (255) fails ci <= cj
         if (off >= 0) {
-            const double2* p = reinterpret_cast<const double2*>(
-                Dr + off + rri[t] * stride + 16 * kc + 4 * (lane & 3));
+            // 32-bit element offset (one IMAD.WIDE for the address instead of a 64-bit add chain)
+            const uint32_t e = static_cast<uint32_t>(off) + static_cast<uint32_t>(rri[t] * stride + 16 * kc) +
+                               4u * static_cast<uint32_t>(lane & 3);
+            const double2* p = reinterpret_cast<const double2*>(Dr + e);
 #if KBG_L2_HINT >= 2
             double2 v0, v1;
             asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v0.x), "=d"(v0.y) : "l"(p), "l"(pol));

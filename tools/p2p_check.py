@@ -151,18 +151,24 @@ def main(cfg="cubic56_200Ry"):
         rho_or = o.density(dm)[0]
 
         def errs(x, r):
-            m = np.abs(r) > 1e-8 * np.abs(r).max()
-            return (float(np.abs(x - r).max() / np.abs(r).max()),
-                    float((np.abs(x - r)[m] / np.abs(r)[m]).max()))
+            # the parity bar of tests/test_gpu_parity.py: normwise; per element above 1e-4 max|ref|;
+            # per element between 1e-8 and 1e-4 max|ref| (tolerance 1e-8 there)
+            a = np.abs(r) / np.abs(r).max()
+            rel = np.abs(x - r) / np.where(np.abs(r) > 0, np.abs(r), 1.0)
+            big, small = a > 1e-4, (a > 1e-8) & (a <= 1e-4)
+            return (float(np.abs(x - r).max() / np.abs(r).max()), float(rel[big].max()),
+                    float(rel[small].max()) if small.any() else 0.0)
 
-        h_norm, h_elem = errs(h_np, h_or)
-        r_norm, r_elem = errs(rho_sum, rho_or)
+        h_norm, h_elem, h_small = errs(h_np, h_or)
+        r_norm, r_elem, r_small = errs(rho_sum, rho_or)
         det = bool(repeat and bitwise_single)
         print(json.dumps({"config": cfg, "world": world, "same_bits_all_ranks": same_bits, "repeatable": repeat,
                           "bitwise_equal_single_gpu": bitwise_single,
                           "rel_diff_vs_nccl": d_nccl, "rel_diff_vs_single_gpu": d_full,
                           "oracle_h_normwise": h_norm, "oracle_h_elementwise": h_elem,
+                          "oracle_h_elementwise_small": h_small,
                           "oracle_rho_normwise": r_norm, "oracle_rho_elementwise": r_elem,
+                          "oracle_rho_elementwise_small": r_small,
                           "h_ms_p2p": round(t_p2p, 4), "h_ms_nccl_incl_mirror": round(t_nccl, 4),
                           "h_ms_accumulate_only": round(t_acc, 4), "accumulate_ms_per_rank": acc_ranks,
                           "grid_pass_h_vs_p2p": d_gp, "grid_pass_rho_sum_vs_single_gpu": d_rho,
@@ -171,7 +177,7 @@ def main(cfg="cubic56_200Ry"):
                                   "single-GPU H bit for bit and repeat bitwise",
                           "ok": bool(same_bits and det and d_nccl <= 1e-14 and d_gp == 0.0 and d_rho == 0.0
                                      and h_norm <= 1e-10 and h_elem <= 1e-10 and r_norm <= 1e-10
-                                     and r_elem <= 1e-10)}), flush=True)
+                                     and r_elem <= 1e-10 and h_small <= 1e-8 and r_small <= 1e-8)}), flush=True)
     dist.destroy_process_group()
 
 
