@@ -224,7 +224,7 @@ int kbg_last_tally(const kbg_ctx* ctx, kbg_tally* out);
  * Either way a non-finite V_eff gives KBG_ERR_NONFINITE from the host API. */
 #define KBG_OPT_DETERMINISTIC 9
 /* kbg_grid_pass on a sharded context after kbg_comm_open: 1 (default) shard-local host transfers -- the
- * rank reads only the DM pairs its blocks touch (in place when dm is pinned) and V at its points, writes
+ * rank copies in only the DM ranges holding the pairs its blocks touch, reads V at its points, writes
  * rho only at the points of its blocks and H only in its slice of each spin's entries (kbg_shard_io);
  * the other entries of the caller's buffers are left as they were. 0: every rank reads everything and
  * returns the full H and a full-size rho (zeros outside its blocks). */
@@ -268,6 +268,12 @@ int kbg_comm_handle(kbg_ctx* ctx, void* handle_out);
 int kbg_comm_open(kbg_ctx* ctx, const void* handles);
 int kbg_hamiltonian_allreduce_dev(kbg_ctx* ctx, int nspin, const double* d_veff, double dV, double* d_h,
                                   void* stream);
+/* The two halves of kbg_hamiltonian_allreduce_dev: accumulate this rank's partial H into its exchange
+ * buffer, then (same nspin, later on the stream, after any independent work such as the density pass)
+ * the fused reduce + mirror that leaves the full H in d_h. Placing the density pass between them lets
+ * the exchange find every peer ready instead of waiting for the slowest rank. */
+int kbg_hamiltonian_partial_dev(kbg_ctx* ctx, int nspin, const double* d_veff, double dV, void* stream);
+int kbg_hamiltonian_exchange_dev(kbg_ctx* ctx, int nspin, double* d_h, void* stream);
 /* After synchronizing a kbg_hamiltonian_allreduce_dev: KBG_ERR_NCCL if a peer
  * never arrived (the kernels give up after 10 s instead of hanging the GPU;
  * the H of that call is invalid), else KBG_OK. Clears the flag. kbg_grid_pass
@@ -276,8 +282,8 @@ int kbg_comm_check(kbg_ctx* ctx);
 /* Shard-local I/O ranges of this rank (after kbg_comm_open): out[0..1] its blocks [b0, b1), out[2..3] the
  * points [p0, p1) of its grid-plane range in C order (kbg_grid_pass writes rho at the points of its blocks;
  * with a pageable rho buffer the D2H covers [p0, p1) and the other points there become 0), out[4..5] its
- * slice [h0, h1) of each spin's H entries, out[6] DM doubles per spin its repack reads (canonical pairs it
- * touches + their mirror blocks for the symmetry check), out[7] = p1 - p0. */
+ * slice [h0, h1) of each spin's H entries, out[6] DM doubles per spin it copies in (ranges covering the
+ * pairs its blocks touch and their mirror blocks, for the symmetry check), out[7] = p1 - p0. */
 int kbg_shard_io(const kbg_ctx* ctx, int64_t out[8]);
 /* Timing aid: with KBG_COMM_TIMING set in the environment at kbg_comm_open, the
  * phase times (ns from the reduce kernel's start) of the last exchange: all

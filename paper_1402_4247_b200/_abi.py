@@ -128,6 +128,8 @@ KBGRID_SYMBOLS = [
     ("kbg_shard_io", _I, [_P, C.POINTER(C.c_int64)]),
     ("kbg_comm_timing", _I, [_P, _DP]),
     ("kbg_hamiltonian_allreduce_dev", _I, [_P, _I, _P, _D, _P, _P]),
+    ("kbg_hamiltonian_partial_dev", _I, [_P, _I, _P, _D, _P]),
+    ("kbg_hamiltonian_exchange_dev", _I, [_P, _I, _P, _P]),
     ("kbg_offsets", _I, [_P, C.POINTER(_I), C.POINTER(C.c_int32)]),
     ("kbg_to_realspace", _I, [_P, _DP, _DP]),
     ("kbg_from_realspace", _I, [_P, _DP, _DP]),

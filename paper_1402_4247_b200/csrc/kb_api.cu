@@ -75,6 +75,7 @@ struct kbg_ctx {
     // kbg_grid_pass: second stream and buffers for the H half
     cudaStream_t stream2 = nullptr;
     cudaEvent_t ev_pass = nullptr;
+    cudaEvent_t ev_rho = nullptr;  // sharded kbg_grid_pass: density kernel done (the exchange waits for it)
     double* d_in2 = nullptr;
     size_t cap_in2 = 0;
     double* d_out2 = nullptr;
@@ -93,7 +94,9 @@ struct kbg_ctx {
     // shard-local host transfers of kbg_grid_pass on a sharded context (KBG_OPT_SHARD_IO)
     int shard_io = 1;
     int sparse_thr = 0;  // KBG_OPT_SPARSE_DFMA (0: every task on DMMA)
+    int pending_nspin = 0;  // kbg_hamiltonian_partial_dev done, exchange pending
     uint8_t* d_pown = nullptr;      // per pair: 1 if this rank's blocks touch it (kbg_comm_open)
+    std::vector<int64_t> dm_runs;   // [off, len] pairs: DM ranges (per spin) covering the pairs the repack reads
     int64_t io[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // kbg_shard_io
 };
 
@@ -744,6 +747,21 @@ int kbg_hamiltonian(kbg_ctx* c, int nspin, const double* veff, double dV, double
     });
 }
 
+namespace {
+// Host-to-device copy of the DM pair blocks a shard reads (c->dm_runs, per spin): one cudaMemcpyAsync
+// per run on c->stream (copy engine; overlaps the H kernel on the other stream). kbg_comm_open merges
+// the runs to at most kMaxDmRuns, so the host issues only a few dozen copies per call.
+void dm_run_copy(kbg_ctx* c, int nspin, const double* dm) {
+    const size_t nr = c->dm_runs.size() / 2;
+    for (int s = 0; s < nspin; ++s)
+        for (size_t r = 0; r < nr; ++r) {
+            const int64_t o = s * c->ix.nnz + c->dm_runs[2 * r];
+            KBG_CUDA(cudaMemcpyAsync(c->d_in + o, dm + o, static_cast<size_t>(c->dm_runs[2 * r + 1]) * sizeof(double),
+                                     cudaMemcpyHostToDevice, c->stream));
+        }
+}
+}  // namespace
+
 int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, double dV, double* rho, double* h) {
     if (!c || !dm || !veff || !rho || !h) return KBG_ERR_CONFIG;
     return guard(c, [&] {
@@ -753,6 +771,7 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
         KBG_CUDA(cudaSetDevice(c->device));
         if (!c->stream2) KBG_CUDA(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
         if (!c->ev_pass) KBG_CUDA(cudaEventCreateWithFlags(&c->ev_pass, cudaEventDisableTiming));
+        if (!c->ev_rho) KBG_CUDA(cudaEventCreateWithFlags(&c->ev_rho, cudaEventDisableTiming));
         const size_t ndm = static_cast<size_t>(nspin) * c->ix.nnz, npt = static_cast<size_t>(nspin) * c->npts;
         ensure(c->d_in, c->cap_in, ndm);
         ensure(c->d_out, c->cap_out, npt);
@@ -775,7 +794,31 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
         // its plane range), and H -- complete on every rank after the fused reduction -- leaves only
         // the rank's slice [io[4], io[5]) of each spin. kbg_shard_io reports the ranges.
         const bool sio = c->comm_ready && c->shard_io;
-        const double* dm_map = sio ? mapped_input(c, dm) : nullptr;
+        auto rho_half = [&] {
+            if (c->det) KBG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_pass, 0));
+            // the DM crosses on the copy engine while the H kernel computes; a shard copies only the pair
+            // blocks its rho reads (a few dozen copies of their merged contiguous runs)
+            if (sio && !c->dm_runs.empty())
+                dm_run_copy(c, nspin, dm);
+            else
+                KBG_CUDA(cudaMemcpyAsync(c->d_in, dm, ndm * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+            KBG_CUDA(cudaMemsetAsync(c->d_check, 0, 4 * sizeof(unsigned long long), c->stream));
+            if (c->nranks > 1 && !rho_map) KBG_CUDA(cudaMemsetAsync(c->d_out, 0, npt * sizeof(double), c->stream));
+            // the DM symmetry check rides along in the repack pass (no separate k_dm_check)
+            n += run_density(c, nspin, c->d_in, rho_map ? rho_map : c->d_out, c->stream, c->d_check,
+                             sio ? c->d_pown : nullptr);
+            if (!rho_map) {
+                if (sio) {
+                    const int64_t p0 = c->io[2], p1 = c->io[3];
+                    for (int s = 0; s < nspin; ++s)
+                        if (p1 > p0)
+                            KBG_CUDA(cudaMemcpyAsync(rho + s * c->npts + p0, c->d_out + s * c->npts + p0,
+                                                     (p1 - p0) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+                } else {
+                    KBG_CUDA(cudaMemcpyAsync(rho, c->d_out, npt * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+                }
+            }
+        };
         auto h_half = [&] {
             if (!v_map)
                 KBG_CUDA(cudaMemcpyAsync(c->d_in2, veff, npt * sizeof(double), cudaMemcpyHostToDevice, c->stream2));
@@ -783,8 +826,13 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
             const double* vin = v_map ? v_map : c->d_in2;
             if (c->comm_ready) {
                 // sharded: partials into the peer-mapped exchange buffer, then the fused reduce +
-                // mirror over NVLink (kb_comm.cu) -- the full H on every rank
+                // mirror over NVLink (kb_comm.cu) -- the full H on every rank. The reduce waits for this
+                // rank's density kernel (ev_rho): the rank spread and the flag round trip hide behind it,
+                // and its spinning CTAs never keep the density kernel off the SMs.
                 n += h_accumulate(c, nspin, dV, vin, c->d_xbuf, c->stream2);
+                rho_half();
+                KBG_CUDA(cudaEventRecord(c->ev_rho, c->stream));
+                KBG_CUDA(cudaStreamWaitEvent(c->stream2, c->ev_rho, 0));
                 c->epoch += 2;
                 c->comm.ls = c->det ? 2 : 1;
                 n += kbg::launch_reduce_mirror(c->comm, c->ix, c->P, nspin, c->d_out2, c->epoch - 1, c->stream2);
@@ -806,33 +854,8 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
                 KBG_CUDA(cudaMemcpyAsync(h, c->d_out2, ndm * sizeof(double), cudaMemcpyDeviceToHost, c->stream2));
             }
         };
-        auto rho_half = [&] {
-            if (c->det) KBG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_pass, 0));
-            if (!dm_map) KBG_CUDA(cudaMemcpyAsync(c->d_in, dm, ndm * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-            KBG_CUDA(cudaMemsetAsync(c->d_check, 0, 4 * sizeof(unsigned long long), c->stream));
-            if (c->nranks > 1 && !rho_map) KBG_CUDA(cudaMemsetAsync(c->d_out, 0, npt * sizeof(double), c->stream));
-            // the DM symmetry check rides along in the repack pass (no separate k_dm_check)
-            n += run_density(c, nspin, dm_map ? dm_map : c->d_in, rho_map ? rho_map : c->d_out, c->stream, c->d_check,
-                             sio ? c->d_pown : nullptr);
-            if (!rho_map) {
-                if (sio) {
-                    const int64_t p0 = c->io[2], p1 = c->io[3];
-                    for (int s = 0; s < nspin; ++s)
-                        if (p1 > p0)
-                            KBG_CUDA(cudaMemcpyAsync(rho + s * c->npts + p0, c->d_out + s * c->npts + p0,
-                                                     (p1 - p0) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-                } else {
-                    KBG_CUDA(cudaMemcpyAsync(rho, c->d_out, npt * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-                }
-            }
-        };
-#ifndef KBG_PASS_RHO_FIRST
         h_half();
-        rho_half();
-#else
-        rho_half();
-        h_half();
-#endif
+        if (!c->comm_ready) rho_half();  // sharded: h_half runs rho_half between accumulate and reduce
         unsigned long long chk[4];
         KBG_CUDA(cudaMemcpyAsync(chk, c->d_check, sizeof(chk), cudaMemcpyDeviceToHost, c->stream));
         KBG_CUDA(cudaStreamSynchronize(c->stream2));
@@ -1366,15 +1389,45 @@ int kbg_comm_open(kbg_ctx* c, const void* handles) {
         }
         {
             // pairs this rank's blocks touch: the DM it reads in kbg_grid_pass (shard-local input)
-            std::vector<uint8_t> mine(std::max<int64_t>(1, c->ix.npair), 0);
-            int64_t dm_read = 0;
+            std::vector<uint8_t> mine(std::max<int64_t>(1, c->ix.npair), 0), need(std::max<int64_t>(1, c->ix.npair), 0);
             for (int64_t p = 0; p < c->ix.npair; ++p) {
                 mine[p] = (owners[p] >> c->rank) & 1u;
-                const int a = h.pair_a[p], b = h.pair_b[p];
-                const int R0 = h.pair_R[3 * p], R1 = h.pair_R[3 * p + 1], R2 = h.pair_R[3 * p + 2];
-                const bool can = (a != b) ? a < b : (R0 != 0 ? R0 > 0 : (R1 != 0 ? R1 > 0 : R2 >= 0));
-                if (mine[p] && can) dm_read += 2 * (h.pair_off[p + 1] - h.pair_off[p]);  // block + mirror (check)
+                if (mine[p]) need[p] = need[h.pair_mirror[p]] = 1;  // the block and its mirror (symmetry check)
             }
+            // contiguous runs of the needed pair blocks, then the smallest gaps merged until at most
+            // kMaxDmRuns copies remain (448 atoms on 4 GPUs: 2.5 k runs, 42 % of the DM -> 40 runs, ~60 %)
+            std::vector<int64_t> runs;
+            for (int64_t p = 0; p < c->ix.npair; ++p) {
+                if (!need[p]) continue;
+                const int64_t o = h.pair_off[p], n = h.pair_off[p + 1] - o;
+                if (!runs.empty() && runs[runs.size() - 2] + runs.back() == o)
+                    runs.back() += n;
+                else {
+                    runs.push_back(o);
+                    runs.push_back(n);
+                }
+            }
+            constexpr size_t kMaxDmRuns = 48;
+            if (runs.size() / 2 > kMaxDmRuns) {
+                std::vector<int64_t> gaps;
+                for (size_t r = 1; r < runs.size() / 2; ++r) gaps.push_back(runs[2 * r] - runs[2 * r - 2] - runs[2 * r - 1]);
+                std::nth_element(gaps.begin(), gaps.begin() + (gaps.size() - (kMaxDmRuns - 1)), gaps.end());
+                const int64_t gmax = gaps[gaps.size() - (kMaxDmRuns - 1)];  // gaps below this are bridged
+                std::vector<int64_t> merged{runs[0], runs[1]};
+                for (size_t r = 1; r < runs.size() / 2; ++r) {
+                    const int64_t gap = runs[2 * r] - merged[merged.size() - 2] - merged.back();
+                    if (gap < gmax) {
+                        merged.back() = runs[2 * r] + runs[2 * r + 1] - merged[merged.size() - 2];
+                    } else {
+                        merged.push_back(runs[2 * r]);
+                        merged.push_back(runs[2 * r + 1]);
+                    }
+                }
+                runs.swap(merged);
+            }
+            c->dm_runs = runs;
+            int64_t dm_read = 0;
+            for (size_t r = 0; r < runs.size() / 2; ++r) dm_read += runs[2 * r + 1];
             if (c->d_pown) cudaFree(c->d_pown);
             c->d_pown = nullptr;
             KBG_CUDA(cudaMalloc(&c->d_pown, mine.size()));
@@ -1499,6 +1552,40 @@ int kbg_hamiltonian_allreduce_dev(kbg_ctx* c, int nspin, const double* d_veff, d
         c->last_launches = n;
         c->tally.flops = nspin * 2.0 * c->ix.sum_m2 / c->nranks;
         c->tally.bytes = 8.0 * nspin * (c->ix.nnz + c->npts);
+    });
+}
+
+// The two halves of kbg_hamiltonian_allreduce_dev, so a caller can put independent work (the density
+// pass) between them: the exchange then finds every peer's partials ready instead of spinning on the
+// slowest rank, and the rank spread and flag latency hide behind that work.
+int kbg_hamiltonian_partial_dev(kbg_ctx* c, int nspin, const double* d_veff, double dV, void* stream) {
+    if (!c || !d_veff) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        check_nspin(nspin);
+        require_index(c);
+        if (!c->comm_ready) throw Error(KBG_ERR_CONFIG, "hamiltonian_partial: call kbg_comm_open first");
+        KBG_CUDA(cudaSetDevice(c->device));
+        c->last_launches = h_accumulate(c, nspin, dV, d_veff, c->d_xbuf, static_cast<cudaStream_t>(stream));
+        c->pending_nspin = nspin;
+        c->tally.flops = nspin * 2.0 * c->ix.sum_m2 / c->nranks;
+        c->tally.bytes = 8.0 * nspin * (c->ix.nnz + c->npts);
+    });
+}
+
+int kbg_hamiltonian_exchange_dev(kbg_ctx* c, int nspin, double* d_h, void* stream) {
+    if (!c || !d_h) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        check_nspin(nspin);
+        require_index(c);
+        if (!c->comm_ready) throw Error(KBG_ERR_CONFIG, "hamiltonian_exchange: call kbg_comm_open first");
+        if (c->pending_nspin != nspin)
+            throw Error(KBG_ERR_CONFIG, "hamiltonian_exchange: no kbg_hamiltonian_partial_dev with this nspin before");
+        KBG_CUDA(cudaSetDevice(c->device));
+        c->pending_nspin = 0;
+        c->epoch += 2;
+        c->comm.ls = c->det ? 2 : 1;
+        c->last_launches = kbg::launch_reduce_mirror(c->comm, c->ix, c->P, nspin, d_h, c->epoch - 1,
+                                                     static_cast<cudaStream_t>(stream));
     });
 }
 
@@ -1891,6 +1978,7 @@ void kbg_destroy(kbg_ctx* c) {
     if (c->d_in2) cudaFree(c->d_in2);
     if (c->d_out2) cudaFree(c->d_out2);
     if (c->ev_pass) cudaEventDestroy(c->ev_pass);
+    if (c->ev_rho) cudaEventDestroy(c->ev_rho);
     if (c->stream2) cudaStreamDestroy(c->stream2);
     if (c->blas) cublasDestroy(c->blas);
     if (c->h_kw_done) cudaEventDestroy(c->h_kw_done);

@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_hamiltonian(GridArgs g) {
     for (int spin = 0; spin < g.nspin; ++spin) {
         double* Hs = g.out + spin * g.nnz * (DET ? 2 : 1);
         for_warp_tasks<NW>(g, sm, warp,
-                           [&](int e) { h_task<DET, true>(sm, sm.acc() + spin * 64, ncov, sm.task()[e], Hs, g.sign, g.scatter, lane); });
+                           [&](int e) { h_task<DET, true>(sm, sm.acc() + spin * 64, ncov, sm.task()[e], Hs, g.scatter, lane); });
     }
 }
 

@@ -21,6 +21,12 @@
 
 #include "kb_device.cuh"
 
+// Timing-experiment paths (KBG_OPT_SCATTER_STORE bits, KBG_OPT_DEBUG_COUNTERS) exist only in builds
+// with -DKBG_EXPERIMENTS=1 (tools/build_variants.sh): the product kernels carry no runtime checks for them.
+#ifndef KBG_EXPERIMENTS
+#define KBG_EXPERIMENTS 0
+#endif
+
 // L2 policy of the persistent kernels: 1 streams the geometry cache with
 // evict_first; 2 also loads the repacked DM with evict_last.
 #ifndef KBG_L2_HINT
@@ -268,7 +274,7 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int tid
             bool valid;
             const int64_t pt = slot_point(P, bi, bj, bk, i & 63, valid);
             const double v = valid ? g.in[(i >> 6) * g.npts + pt] : 0.0;
-            sm.acc()[i] = v * g.dV;
+            sm.acc()[i] = v * (g.dV * g.sign);  // fault hook (sign -1) folded into w
             if (!isfinite(v) && g.vbits)  // non-finite V: flag for the host API (KBG_ERR_NONFINITE)
                 atomicMax(const_cast<unsigned long long*>(g.vbits), 0x7ff8000000000000ull);
         }
@@ -389,7 +395,7 @@ __device__ __forceinline__ HScale hscale_of(unsigned long long vbits, double wfa
 // columns cb0 + [0, 8*TN) of cover cj; canonical rows (cover ci <= cj) only.
 template <bool DET, int TM, int TN>
 __device__ __forceinline__ void h_scatter(const Smem& sm, const double (&c)[TM][TN][2], int ncov, int cj, int ra0,
-                                          int rend, int cb0, double* __restrict__ H, double sign, int scatter,
+                                          int rend, int cb0, double* __restrict__ H, int scatter,
                                           int lane) {
     const int nb = sm.cov()[cj].norb;
     const double c1 = DET ? s_hscale.c1 : 0.0, c2 = DET ? s_hscale.c2 : 0.0;
@@ -405,15 +411,15 @@ __device__ __forceinline__ void h_scatter(const Smem& sm, const double (&c)[TM][
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int col = cb0 + 8 * j + (lane & 3) * 2 + e;
-                if (off >= 0 && col < nb && !(scatter & 2)) {
-                    const double v = sign * c[i][j][e];
+                if (off >= 0 && col < nb && !(KBG_EXPERIMENTS && (scatter & 2))) {
+                    const double v = c[i][j][e];  // the fault hook's sign is folded into w
                     if (DET) {
                         const double hi = __dsub_rn(__dadd_rn(v, c1), c1);
                         const double lo = __dsub_rn(__dadd_rn(__dsub_rn(v, hi), c2), c2);
                         double* p = H + (KBG_DET_SPLIT ? 1 : 2) * (off + ri * nb + col);
-                        if (!(scatter & 8)) red_add(p, hi);           // bit 8: timing experiment only
-                        if (!(scatter & 4)) red_add(p + lo_off, lo);  // bit 4: timing experiment only
-                    } else if (!(scatter & 1)) {
+                        if (!(KBG_EXPERIMENTS && (scatter & 8))) red_add(p, hi);  // bits 8, 4: timing
+                        if (!(KBG_EXPERIMENTS && (scatter & 4))) red_add(p + lo_off, lo);  // experiments only
+                    } else if (!(KBG_EXPERIMENTS && (scatter & 1))) {
                         red_add(H + off + ri * nb + col, v);
                     } else {
                         H[off + ri * nb + col] = v;
@@ -432,8 +438,8 @@ __device__ __forceinline__ void h_scatter(const Smem& sm, const double (&c)[TM][
 // qm. Tiles with <= 2 DMMAs per quad alternate two accumulator sets.
 template <bool DET, int TM, int TN>
 __device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict__ w, int ncov, int cj, int ra0,
-                                       int rend, int cb0, uint32_t qm, double* __restrict__ H, double sign,
-                                       int scatter, int lane) {
+                                       int rend, int cb0, uint32_t qm, double* __restrict__ H, int scatter,
+                                       int lane) {
     constexpr int NACC = (TM * TN <= 2) ? 2 : 1;
     double c[NACC][TM][TN][2];
 #pragma unroll
@@ -481,7 +487,7 @@ __device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict_
                 c[0][i][j][0] += c[NACC - 1][i][j][0];
                 c[0][i][j][1] += c[NACC - 1][i][j][1];
             }
-    h_scatter<DET, TM, TN>(sm, c[0], ncov, cj, ra0, rend, cb0, H, sign, scatter, lane);
+    h_scatter<DET, TM, TN>(sm, c[0], ncov, cj, ra0, rend, cb0, H, scatter, lane);
 }
 
 // Two partners sharing the group's (w-scaled) A fragments: per quad of
@@ -489,7 +495,7 @@ __device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict_
 template <bool DET, int TM, int TN1, int TN2>
 __device__ __forceinline__ void h_tile2(const Smem& sm, const double* __restrict__ w, int ncov, int cj1, int cj2,
                                         int ra0, int rend, uint32_t q1, uint32_t q2, double* __restrict__ H,
-                                        double sign, int scatter, int lane) {
+                                        int scatter, int lane) {
     double c1[TM][TN1][2], c2[TM][TN2][2];
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
@@ -542,18 +548,18 @@ __device__ __forceinline__ void h_tile2(const Smem& sm, const double* __restrict
     run(q1 & q2, std::true_type{}, std::true_type{});
     run(q1 & ~q2, std::true_type{}, std::false_type{});
     run(q2 & ~q1, std::false_type{}, std::true_type{});
-    h_scatter<DET, TM, TN1>(sm, c1, ncov, cj1, ra0, rend, 0, H, sign, scatter, lane);
-    h_scatter<DET, TM, TN2>(sm, c2, ncov, cj2, ra0, rend, 0, H, sign, scatter, lane);
+    h_scatter<DET, TM, TN1>(sm, c1, ncov, cj1, ra0, rend, 0, H, scatter, lane);
+    h_scatter<DET, TM, TN2>(sm, c2, ncov, cj2, ra0, rend, 0, H, scatter, lane);
 }
 
 template <bool DET, int TM, int TN1>
 __device__ __forceinline__ void h_tile2_tn2(int tn2, const Smem& sm, const double* w, int ncov, int cj1, int cj2,
-                                            int ra0, int rend, uint32_t q1, uint32_t q2, double* H, double sign,
+                                            int ra0, int rend, uint32_t q1, uint32_t q2, double* H,
                                             int scatter, int lane) {
     if (tn2 == 2)
-        h_tile2<DET, TM, TN1, 2>(sm, w, ncov, cj1, cj2, ra0, rend, q1, q2, H, sign, scatter, lane);
+        h_tile2<DET, TM, TN1, 2>(sm, w, ncov, cj1, cj2, ra0, rend, q1, q2, H, scatter, lane);
     else
-        h_tile2<DET, TM, TN1, 1>(sm, w, ncov, cj1, cj2, ra0, rend, q1, q2, H, sign, scatter, lane);
+        h_tile2<DET, TM, TN1, 1>(sm, w, ncov, cj1, cj2, ra0, rend, q1, q2, H, scatter, lane);
 }
 
 // One H element into the accumulator (FP64 RED, or the deterministic two-limb split).
@@ -578,7 +584,7 @@ __device__ __forceinline__ void h_add(double* __restrict__ H, int64_t idx, doubl
 // (Task.pad2_, kb_tasks.cu) below the KBG_OPT_SPARSE_DFMA threshold (scatter bits 8..15).
 template <bool DET>
 __device__ __forceinline__ void h_task_dfma(const Smem& sm, const double* __restrict__ w, int ncov, const Task& t,
-                                         double* __restrict__ H, double sign, int lane) {
+                                         double* __restrict__ H, int lane) {
     const GroupS& G = sm.grp()[t.g];
     const int r = G.row0 + (lane & 15);
     const bool row_ok = (lane & 15) < G.rows;
@@ -609,15 +615,15 @@ __device__ __forceinline__ void h_task_dfma(const Smem& sm, const double* __rest
         if (off >= 0)
 #pragma unroll
             for (int j = 0; j < 8; ++j)
-                if (c0 + j < nb) h_add<DET>(H, off + ri * nb + c0 + j, sign * acc[j]);
+                if (c0 + j < nb) h_add<DET>(H, off + ri * nb + c0 + j, acc[j]);
     }
 }
 
 template <bool DET, bool SPARSE = false>
 __device__ __forceinline__ void h_task(const Smem& sm, const double* w, int ncov, const Task& t, double* H,
-                                       double sign, int scatter, int lane) {
+                                       int scatter, int lane) {
     if (SPARSE && t.pad2_ < (scatter >> 8)) {
-        h_task_dfma<DET>(sm, w, ncov, t, H, sign, lane);
+        h_task_dfma<DET>(sm, w, ncov, t, H, lane);
         return;
     }
     const GroupS& G = sm.grp()[t.g];
@@ -630,17 +636,17 @@ __device__ __forceinline__ void h_task(const Smem& sm, const double* w, int ncov
         const int tn1 = (sm.cov()[t.cj].norb + 7) >> 3, tn2 = (sm.cov()[t.cj2].norb + 7) >> 3;
         if (G.tm == 2) {
             if (tn1 == 2)
-                h_tile2_tn2<DET, 2, 2>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, q1, q2, H, sign, scatter,
+                h_tile2_tn2<DET, 2, 2>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, q1, q2, H, scatter,
                                   lane);
             else
-                h_tile2_tn2<DET, 2, 1>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, q1, q2, H, sign, scatter,
+                h_tile2_tn2<DET, 2, 1>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, q1, q2, H, scatter,
                                   lane);
         } else {
             if (tn1 == 2)
-                h_tile2_tn2<DET, 1, 2>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, q1, q2, H, sign, scatter,
+                h_tile2_tn2<DET, 1, 2>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, q1, q2, H, scatter,
                                   lane);
             else
-                h_tile2_tn2<DET, 1, 1>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, q1, q2, H, sign, scatter,
+                h_tile2_tn2<DET, 1, 1>(tn2, sm, w, ncov, t.cj, t.cj2, G.row0, rend, q1, q2, H, scatter,
                                   lane);
         }
         return;
@@ -653,13 +659,13 @@ __device__ __forceinline__ void h_task(const Smem& sm, const double* w, int ncov
             const int tn = min(2, ((nb + 7) >> 3) - j0);
             const int ra0 = G.row0 + 8 * i0, cb0 = 8 * j0;
             if (tm == 2 && tn == 2)
-                h_tile<DET, 2, 2>(sm, w, ncov, t.cj, ra0, rend, cb0, qm, H, sign, scatter, lane);
+                h_tile<DET, 2, 2>(sm, w, ncov, t.cj, ra0, rend, cb0, qm, H, scatter, lane);
             else if (tm == 2)
-                h_tile<DET, 2, 1>(sm, w, ncov, t.cj, ra0, rend, cb0, qm, H, sign, scatter, lane);
+                h_tile<DET, 2, 1>(sm, w, ncov, t.cj, ra0, rend, cb0, qm, H, scatter, lane);
             else if (tn == 2)
-                h_tile<DET, 1, 2>(sm, w, ncov, t.cj, ra0, rend, cb0, qm, H, sign, scatter, lane);
+                h_tile<DET, 1, 2>(sm, w, ncov, t.cj, ra0, rend, cb0, qm, H, scatter, lane);
             else
-                h_tile<DET, 1, 1>(sm, w, ncov, t.cj, ra0, rend, cb0, qm, H, sign, scatter, lane);
+                h_tile<DET, 1, 1>(sm, w, ncov, t.cj, ra0, rend, cb0, qm, H, scatter, lane);
         }
     }
 }

@@ -227,7 +227,7 @@ __device__ void producer(const GridArgs& g, const Buffers<DENSITY>& B, int lane)
             if (lane == 0) {
                 sm.meta()->block = -1;
                 mbar_arrive(&B.full[s]);
-                if (g.dbg) {
+                if (KBG_EXPERIMENTS && g.dbg) {
                     atomicAdd(&g.dbg[0], t_wait);
                     atomicAdd(&g.dbg[1], clock64() - t0);
                 }
@@ -239,7 +239,7 @@ __device__ void producer(const GridArgs& g, const Buffers<DENSITY>& B, int lane)
 #pragma unroll
             for (int j = 0; j < 2 * kMaxSpin; ++j) {
                 const int i = lane + 32 * j;
-                if (i < g.nspin * 64) sm.acc()[i] = w_cur[j] * g.dV;
+                if (i < g.nspin * 64) sm.acc()[i] = w_cur[j] * (g.dV * g.sign);  // fault hook sign folded into w
                 fin = fin && isfinite(w_cur[j]);
             }
             // non-finite V (the deterministic path sees it in its max|V| pass instead): flag it for
@@ -261,7 +261,7 @@ __device__ void producer(const GridArgs& g, const Buffers<DENSITY>& B, int lane)
             bulk_g2s(sm.meta(), tab, tb, &B.full[s]);
             bulk_g2s(sm.phi(), phi, pb, &B.full[s]);
 #endif
-            if (g.dbg) {  // debug only: copy latency (delays the next fetch)
+            if (KBG_EXPERIMENTS && g.dbg) {  // debug only: copy latency (delays the next fetch)
                 const unsigned long long tc = clock64();
                 mbar_wait(&B.full[s], (k >> 1) & 1);
                 atomicAdd(&g.dbg[7], clock64() - tc);
@@ -283,12 +283,12 @@ __device__ void consumer(const GridArgs& g, const Buffers<DENSITY>& B, int cw, i
         mbar_wait(&B.full[s], (k >> 1) & 1);
         const unsigned long long dw = clock64() - tw;
         t_wait += dw;
-        if (g.dbg && k < 2 && lane == 0) atomicAdd(&g.dbg[6], dw);
+        if (KBG_EXPERIMENTS && g.dbg && k < 2 && lane == 0) atomicAdd(&g.dbg[6], dw);
         const Smem sm = B.buf(s);
         const int64_t b = sm.meta()->block;
         if (b < 0) {
             t_tail += dw;
-            if (g.dbg && lane == 0) {
+            if (KBG_EXPERIMENTS && g.dbg && lane == 0) {
                 atomicAdd(&g.dbg[2], t_wait);
                 atomicAdd(&g.dbg[3], t_tail);
                 atomicAdd(&g.dbg[4], clock64() - t0);
@@ -314,8 +314,8 @@ __device__ void consumer(const GridArgs& g, const Buffers<DENSITY>& B, int cw, i
                     __syncwarp();
                     rho_task(sm, ncov, t, g.dmr + spin * g.nrep, res - 32 * t.half, lane, g.scatter);
                 } else {
-                    h_task<DET, SPARSE>(sm, sm.acc() + spin * 64, ncov, t, g.out + spin * g.nnz * (DET ? 2 : 1), g.sign,
-                                g.scatter, lane);
+                    h_task<DET, SPARSE>(sm, sm.acc() + spin * 64, ncov, t, g.out + spin * g.nnz * (DET ? 2 : 1), g.scatter,
+                                        lane);
                 }
             }
         } else
@@ -332,7 +332,7 @@ __device__ void consumer(const GridArgs& g, const Buffers<DENSITY>& B, int cw, i
                 double* Hs = g.out + spin * g.nnz * (DET ? 2 : 1);
                 for (int w = cw; w < g.task_warps; w += NC)
                     for (int e = sm.wptr()[w]; e < sm.wptr()[w + 1]; ++e)
-                        h_task<DET, SPARSE>(sm, sm.acc() + spin * 64, ncov, sm.task()[e], Hs, g.sign, g.scatter, lane);
+                        h_task<DET, SPARSE>(sm, sm.acc() + spin * 64, ncov, sm.task()[e], Hs, g.scatter, lane);
             }
         }
         __syncwarp();
@@ -403,7 +403,7 @@ __device__ void consumer(const GridArgs& g, const Buffers<DENSITY>& B, int cw, i
             }
             if (lane == 0) {
                 mbar_arrive(&B.empty[s]);
-                if (g.dbg) atomicAdd(&g.dbg[10], clock64() - t_red);
+                if (KBG_EXPERIMENTS && g.dbg) atomicAdd(&g.dbg[10], clock64() - t_red);
             }
         }
     }

@@ -232,6 +232,18 @@ class GridPass:
         keys = ("b0", "b1", "p0", "p1", "h0", "h1", "dm_read", "v_read")
         return dict(zip(keys, (int(x) for x in v)))
 
+    def hamiltonian_partial_dev(self, veff, dV: float, stream=None) -> None:
+        """First half of hamiltonian_allreduce_dev: this rank's partial H into its exchange buffer."""
+        self._spin_tensor(veff, self.system.npts, "hamiltonian_partial_dev: veff")
+        self._check(self._lib.kbg_hamiltonian_partial_dev(self._h, veff.shape[0], veff.data_ptr(), dV,
+                                                          self._stream_ptr(stream)), "kbg_hamiltonian_partial_dev")
+
+    def hamiltonian_exchange_dev(self, h, stream=None) -> None:
+        """Second half: the fused reduce + mirror over peer memory -> the full H in h."""
+        ns = self._spin_tensor(h, self._nnz(), "hamiltonian_exchange_dev: h")
+        self._check(self._lib.kbg_hamiltonian_exchange_dev(self._h, ns, h.data_ptr(), self._stream_ptr(stream)),
+                    "kbg_hamiltonian_exchange_dev")
+
     def comm_check(self) -> None:
         """After synchronizing a hamiltonian_allreduce_dev: raise if a peer never arrived."""
         self._check(self._lib.kbg_comm_check(self._h), "kbg_comm_check")

@@ -57,6 +57,13 @@ def main(cfg="cubic56_200Ry"):
     p2p()
     torch.cuda.synchronize()
     repeat = bool(torch.equal(first, h_p2p))
+    # the split API (partial -> independent work -> exchange) gives the same bits
+    h_split = torch.empty_like(h_p2p)
+    gp.hamiltonian_partial_dev(v, f.dV, st)
+    gp.hamiltonian_exchange_dev(h_split, st)
+    torch.cuda.synchronize()
+    gp.comm_check()
+    split_same = bool(torch.equal(h_split, h_p2p))
     sums = [None] * world
     dist.all_gather_object(sums, hashlib.sha256(h_p2p.cpu().numpy().tobytes()).hexdigest())
     same_bits = len(set(sums)) == 1
@@ -163,7 +170,7 @@ def main(cfg="cubic56_200Ry"):
         r_norm, r_elem, r_small = errs(rho_sum, rho_or)
         det = bool(repeat and bitwise_single)
         print(json.dumps({"config": cfg, "world": world, "same_bits_all_ranks": same_bits, "repeatable": repeat,
-                          "bitwise_equal_single_gpu": bitwise_single,
+                          "bitwise_equal_single_gpu": bitwise_single, "split_api_same_bits": split_same,
                           "rel_diff_vs_nccl": d_nccl, "rel_diff_vs_single_gpu": d_full,
                           "oracle_h_normwise": h_norm, "oracle_h_elementwise": h_elem,
                           "oracle_h_elementwise_small": h_small,
@@ -175,7 +182,7 @@ def main(cfg="cubic56_200Ry"):
                           "exchange_phases_us_per_rank": phases, "shard_io": ios,
                           "note": "deterministic H (KBG_OPT_DETERMINISTIC): the sharded H must equal the "
                                   "single-GPU H bit for bit and repeat bitwise",
-                          "ok": bool(same_bits and det and d_nccl <= 1e-14 and d_gp == 0.0 and d_rho == 0.0
+                          "ok": bool(same_bits and det and split_same and d_nccl <= 1e-14 and d_gp == 0.0 and d_rho == 0.0
                                      and h_norm <= 1e-10 and h_elem <= 1e-10 and r_norm <= 1e-10
                                      and r_elem <= 1e-10 and h_small <= 1e-8 and r_small <= 1e-8)}), flush=True)
     dist.destroy_process_group()
