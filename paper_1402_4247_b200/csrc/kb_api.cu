@@ -86,11 +86,13 @@ struct kbg_ctx {
     double* d_states = nullptr;     // scaled states scratch
     size_t cap_states = 0;
     // deterministic H (KBG_OPT_DETERMINISTIC, kb_gridcore.cuh h_scatter)
-    int det = 0;  // KBG_OPT_DETERMINISTIC (off by default: +43 % H time on 56 atoms)
+    int det = 0;  // KBG_OPT_DETERMINISTIC: 0 FP64 atomics, 1 per-entry grid (one limb), 2 two limbs
     double hbound = 0.0;            // >= sum over r of |phi_i(r) phi_j(r)| for any orbital pair (h_bound)
     double* d_hacc = nullptr;       // two-limb accumulator [nspin][nnz][2]
     size_t cap_hacc = 0;
     unsigned long long* d_vbits = nullptr;  // max|V| bit pattern of the current H pass
+    int16_t* d_etab = nullptr;      // mode 1: per-entry bound exponents, T_ij < 2^etab (built on first use)
+    bool etab_ok = false;
     // shard-local host transfers of kbg_grid_pass on a sharded context (KBG_OPT_SHARD_IO)
     int shard_io = 1;
     int sparse_thr = 0;  // KBG_OPT_SPARSE_DFMA (0: every task on DMMA)
@@ -332,10 +334,9 @@ kbg::GridArgs grid_args(kbg_ctx* c, int nspin, double dV, const double* in, doub
     if (!density) {
         g.scatter |= c->sparse_thr << 8;  // A5 switch: tasks below this point density (1/255) run DFMA
         g.vbits = c->d_vbits;  // deterministic: max|V| (k_absmax); legacy: non-finite flag of the kernels
-        if (c->det) {
-            g.scatter |= 16;
-            g.wfac = std::fabs(dV) * c->hbound;
-        }
+        g.scatter |= c->det << 4;        // KBG_OPT_DETERMINISTIC mode (kb_gridcore.cuh h_scatter)
+        g.wfac = c->det == 2 ? std::fabs(dV) * c->hbound : std::fabs(dV);
+        g.etab = c->d_etab;
     }
     if (g.max_cover > 32 * c->nwarps || g.max_cover > kbg::kMaxCoverPerBlock)
         throw Error(KBG_ERR_DIMENSION, "a grid block is covered by too many atom images");
@@ -378,6 +379,9 @@ void comm_check(kbg_ctx* c) {
     }
 }
 
+// Doubles per H entry of the deterministic accumulator (mode 2: hi and lo limbs).
+int h_limbs(const kbg_ctx* c) { return c->det == 2 ? 2 : 1; }
+
 int run_hamiltonian(kbg_ctx* c, int nspin, double dV, const double* d_veff, double* d_h, cudaStream_t st) {
     const kbg::GridArgs g = grid_args(c, nspin, dV, d_veff, d_h, false);
     if (c->persist_ok && c->persist && c->ix.phis) {
@@ -385,7 +389,7 @@ int run_hamiltonian(kbg_ctx* c, int nspin, double dV, const double* d_veff, doub
         int n = 0;
         for (int s = 0; s < nspin; ++s) {
             const kbg::GridArgs g1 =
-                grid_args(c, 1, dV, d_veff + s * c->npts, d_h + s * c->ix.nnz * (c->det ? 2 : 1), false);
+                grid_args(c, 1, dV, d_veff + s * c->npts, d_h + s * c->ix.nnz * h_limbs(c), false);
             if (!kbg::persist_fits(g1, false)) break;
             n += kbg::launch_hamiltonian_persist(g1, st);
             if (s + 1 == nspin) return n;
@@ -399,9 +403,12 @@ int run_hamiltonian(kbg_ctx* c, int nspin, double dV, const double* d_veff, doub
 // point of the device-resident V, accumulate; legacy -- zero [nspin][nnz] and
 // accumulate with FP64 atomics. The caller finalizes (launch_finalize) or
 // reduces across ranks (kb_comm.cu).
+void ensure_etab(kbg_ctx* c, cudaStream_t st);
+
 int h_accumulate(kbg_ctx* c, int nspin, double dV, const double* d_veff, double* acc, cudaStream_t st) {
     int n = 0;
-    const size_t ne = static_cast<size_t>(nspin) * c->ix.nnz * (c->det ? 2 : 1);
+    if (c->det == 1) ensure_etab(c, st);
+    const size_t ne = static_cast<size_t>(nspin) * c->ix.nnz * h_limbs(c);
     KBG_CUDA(cudaMemsetAsync(acc, 0, ne * sizeof(double), st));
     KBG_CUDA(cudaMemsetAsync(c->d_vbits, 0, sizeof(unsigned long long), st));
     if (c->det) n += kbg::launch_absmax(d_veff, static_cast<int64_t>(nspin) * c->npts, c->d_vbits, st);
@@ -414,6 +421,46 @@ double* h_acc_buffer(kbg_ctx* c, int nspin, double* d_out) {
     if (!c->det) return d_out;
     ensure(c->d_hacc, c->cap_hacc, static_cast<size_t>(2) * nspin * std::max<int64_t>(1, c->ix.nnz));
     return c->d_hacc;
+}
+
+// Mode 1's per-entry bounds: T_ij = sum_r |phi_i(r)| |phi_j(r)| over the grid, accumulated once per
+// geometry by the H kernels themselves with |Phi| operands and w = 1 (mode 3: two exact limbs, so T has
+// the same bits on any number of GPUs; sharded contexts sum their partials through the peer exchange),
+// then etab = exponent of T. Every later mode-1 contribution to entry ij is rounded to the grid
+// 2^(ew + etab_ij - 51) with max|w| < 2^ew: its partial sums stay below 2^52 grid steps (exact, any order).
+void ensure_etab(kbg_ctx* c, cudaStream_t st) {
+    if (c->etab_ok) return;
+    const int64_t nnz = std::max<int64_t>(1, c->ix.nnz);
+    if (c->d_etab) cudaFree(c->d_etab);
+    c->d_etab = nullptr;
+    KBG_CUDA(cudaMalloc(&c->d_etab, nnz * sizeof(int16_t)));
+    double* T = nullptr;  // [nnz] bounds, then the accumulator [2][nnz] behind them
+    KBG_CUDA(cudaMallocAsync(&T, 3 * nnz * sizeof(double), st));
+    static const unsigned long long one_bits = 0x3ff0000000000000ull;  // max|w| = 1
+    KBG_CUDA(cudaMemcpyAsync(c->d_vbits, &one_bits, sizeof(one_bits), cudaMemcpyHostToDevice, st));
+    const int det = c->det;
+    c->det = 2;  // grid_args with the two-limb layout; the mode bits become 3 below
+    double* acc = c->comm_ready ? c->d_xbuf : T + nnz;
+    KBG_CUDA(cudaMemsetAsync(acc, 0, 2 * nnz * sizeof(double), st));
+    kbg::GridArgs g = grid_args(c, 1, 1.0, nullptr, acc, false);
+    g.scatter = (g.scatter & ~((3 << 4) | (0xFF << 8))) | (3 << 4);  // mode 3, no point-exact DFMA tasks
+    g.wfac = c->hbound;
+    g.in = nullptr;  // w = 1 (mode 3 ignores it)
+    if (c->persist_ok && c->persist && c->ix.phis && kbg::persist_fits(g, false))
+        kbg::launch_hamiltonian_persist(g, st);
+    else
+        kbg::launch_hamiltonian(g, c->blk_end - c->blk_begin, c->nwarps, st);
+    if (c->comm_ready) {
+        c->epoch += 2;
+        c->comm.ls = 2;
+        kbg::launch_reduce_mirror(c->comm, c->ix, c->P, 1, T, c->epoch - 1, st);
+    } else {
+        kbg::launch_finalize(c->ix, c->P, 1, acc, T, true, st, 2);
+    }
+    c->det = det;
+    kbg::launch_etab(T, c->ix.nnz, c->d_etab, st);
+    KBG_CUDA(cudaFreeAsync(T, st));
+    c->etab_ok = true;
 }
 
 // Max|V| of the last H pass (legacy path: only the non-finite flag): non-finite V -> KBG_ERR_NONFINITE
@@ -538,6 +585,7 @@ int kbg_build_index(kbg_ctx* c) {
         if (c->stream2) KBG_CUDA(cudaStreamSynchronize(c->stream2));
         kbg::BuildStream bs(c->stream);
         c->built = false;
+        c->etab_ok = false;
         c->hix = kbg::HostIndex();
         kbg::free_formats(c->fmt);
         kbg::build_index_device(c->P, c->ix, c->stream);
@@ -647,7 +695,7 @@ int kbg_hamiltonian_accumulate_dev(kbg_ctx* c, int nspin, const double* d_veff, 
         const cudaStream_t st = static_cast<cudaStream_t>(stream);
         double* acc = h_acc_buffer(c, nspin, d_h);
         c->last_launches = h_accumulate(c, nspin, dV, d_veff, acc, st);
-        if (c->det) c->last_launches += kbg::launch_finalize(c->ix, c->P, nspin, acc, d_h, false, st);
+        if (c->det) c->last_launches += kbg::launch_finalize(c->ix, c->P, nspin, acc, d_h, false, st, h_limbs(c));
         c->tally.flops = nspin * 2.0 * c->ix.sum_m2;
         c->tally.bytes = 8.0 * nspin * (c->ix.nnz + c->npts);
     });
@@ -673,7 +721,7 @@ int kbg_hamiltonian_dev(kbg_ctx* c, int nspin, const double* d_veff, double dV, 
             const cudaStream_t st = static_cast<cudaStream_t>(stream);
             double* acc = h_acc_buffer(c, nspin, d_h);
             c->last_launches = h_accumulate(c, nspin, dV, d_veff, acc, st);
-            c->last_launches += kbg::launch_finalize(c->ix, c->P, nspin, acc, d_h, true, st);
+            c->last_launches += kbg::launch_finalize(c->ix, c->P, nspin, acc, d_h, true, st, h_limbs(c));
             c->tally.flops = nspin * 2.0 * c->ix.sum_m2;
             c->tally.bytes = 8.0 * nspin * (c->ix.nnz + c->npts);
         });
@@ -735,7 +783,7 @@ int kbg_hamiltonian(kbg_ctx* c, int nspin, const double* veff, double dV, double
         double* acc = h_acc_buffer(c, nspin, c->d_out);
         int n = h_accumulate(c, nspin, dV, v_map ? v_map : c->d_in, acc, c->stream);
         if (c->det)
-            n += kbg::launch_finalize(c->ix, c->P, nspin, acc, c->d_out, true, c->stream);
+            n += kbg::launch_finalize(c->ix, c->P, nspin, acc, c->d_out, true, c->stream, h_limbs(c));
         else
             n += kbg::launch_mirror(c->ix, c->P, nspin, c->d_out, c->stream);
         c->last_launches = n;
@@ -834,13 +882,13 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
                 KBG_CUDA(cudaEventRecord(c->ev_rho, c->stream));
                 KBG_CUDA(cudaStreamWaitEvent(c->stream2, c->ev_rho, 0));
                 c->epoch += 2;
-                c->comm.ls = c->det ? 2 : 1;
+                c->comm.ls = h_limbs(c);
                 n += kbg::launch_reduce_mirror(c->comm, c->ix, c->P, nspin, c->d_out2, c->epoch - 1, c->stream2);
             } else {
                 double* acc = h_acc_buffer(c, nspin, c->d_out2);
                 n += h_accumulate(c, nspin, dV, vin, acc, c->stream2);
                 if (c->det)
-                    n += kbg::launch_finalize(c->ix, c->P, nspin, acc, c->d_out2, true, c->stream2);
+                    n += kbg::launch_finalize(c->ix, c->P, nspin, acc, c->d_out2, true, c->stream2, h_limbs(c));
                 else
                     n += kbg::launch_mirror(c->ix, c->P, nspin, c->d_out2, c->stream2);
             }
@@ -1327,6 +1375,7 @@ int kbg_comm_open(kbg_ctx* c, const void* handles) {
         kbg::CommArgs& cm = c->comm;
         cm.nranks = c->nranks;
         cm.rank = c->rank;
+        c->etab_ok = false;  // sharded: the bounds are summed over the ranks (first mode-1 call)
         const size_t nd = xbuf_doubles(c);
         for (int k = 0; k < c->nranks; ++k) {
             CommBlob b;
@@ -1395,7 +1444,7 @@ int kbg_comm_open(kbg_ctx* c, const void* handles) {
                 if (mine[p]) need[p] = need[h.pair_mirror[p]] = 1;  // the block and its mirror (symmetry check)
             }
             // contiguous runs of the needed pair blocks, then the smallest gaps merged until at most
-            // kMaxDmRuns copies remain (448 atoms on 4 GPUs: 2.5 k runs, 42 % of the DM -> 40 runs, ~60 %)
+            // kMaxDmRuns copies remain (448 atoms on 4 GPUs: 2.5 k runs, 42 % of the DM)
             std::vector<int64_t> runs;
             for (int64_t p = 0; p < c->ix.npair; ++p) {
                 if (!need[p]) continue;
@@ -1407,7 +1456,10 @@ int kbg_comm_open(kbg_ctx* c, const void* handles) {
                     runs.push_back(n);
                 }
             }
-            constexpr size_t kMaxDmRuns = 48;
+            // a copy costs the host a few us to issue: about one per 4 MB of DM, at most 48 (56 atoms:
+            // a single copy of the whole 3.8 MB DM; 448 atoms: 7; 1512 atoms: 24)
+            const size_t kMaxDmRuns = static_cast<size_t>(
+                std::max<int64_t>(1, std::min<int64_t>(48, c->ix.nnz * 8 / (4 << 20))));
             if (runs.size() / 2 > kMaxDmRuns) {
                 std::vector<int64_t> gaps;
                 for (size_t r = 1; r < runs.size() / 2; ++r) gaps.push_back(runs[2 * r] - runs[2 * r - 2] - runs[2 * r - 1]);
@@ -1547,7 +1599,7 @@ int kbg_hamiltonian_allreduce_dev(kbg_ctx* c, int nspin, const double* d_veff, d
         const cudaStream_t st = static_cast<cudaStream_t>(stream);
         int n = h_accumulate(c, nspin, dV, d_veff, c->d_xbuf, st);
         c->epoch += 2;
-        c->comm.ls = c->det ? 2 : 1;
+        c->comm.ls = h_limbs(c);
         n += kbg::launch_reduce_mirror(c->comm, c->ix, c->P, nspin, d_h, c->epoch - 1, st);
         c->last_launches = n;
         c->tally.flops = nspin * 2.0 * c->ix.sum_m2 / c->nranks;
@@ -1583,7 +1635,7 @@ int kbg_hamiltonian_exchange_dev(kbg_ctx* c, int nspin, double* d_h, void* strea
         KBG_CUDA(cudaSetDevice(c->device));
         c->pending_nspin = 0;
         c->epoch += 2;
-        c->comm.ls = c->det ? 2 : 1;
+        c->comm.ls = h_limbs(c);
         c->last_launches = kbg::launch_reduce_mirror(c->comm, c->ix, c->P, nspin, d_h, c->epoch - 1,
                                                      static_cast<cudaStream_t>(stream));
     });
@@ -1926,7 +1978,11 @@ int kbg_set_option(kbg_ctx* c, int option, int64_t value) {
             c->schedule = static_cast<int>(value);
             return KBG_OK;
         case KBG_OPT_DETERMINISTIC:
-            c->det = value ? 1 : 0;
+            if (value < 0 || value > 2) {
+                c->err = "set_option: deterministic must be 0 (FP64 atomics), 1 (per-entry grid) or 2 (two limbs)";
+                return KBG_ERR_CONFIG;
+            }
+            c->det = static_cast<int>(value);
             return KBG_OK;
         case KBG_OPT_SHARD_IO:
             c->shard_io = value ? 1 : 0;
@@ -1972,6 +2028,7 @@ void kbg_destroy(kbg_ctx* c) {
     if (c->d_canon) cudaFree(c->d_canon);
     if (c->d_pairtab) cudaFree(c->d_pairtab);
     if (c->d_pown) cudaFree(c->d_pown);
+    if (c->d_etab) cudaFree(c->d_etab);
     if (c->comm.tstamp) cudaFree(c->comm.tstamp);
     if (c->d_cpre) cudaFree(c->d_cpre);
     c->veff.release();

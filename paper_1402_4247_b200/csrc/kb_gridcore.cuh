@@ -357,9 +357,14 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int tid
 // kb_comm.cu). H = hi + lo is rounded once at the end (k_finalize). Rounding
 // to a grid is two exact additions of C = 1.5 * 2^(k+52) (|x| < 2^(k+51)):
 // (x + C) - C is x rounded to a multiple of 2^k.
+// DET modes of the H kernels: 0 FP64 atomics; 1 deterministic, one limb on a per-entry grid (etab);
+// 2 deterministic, two limbs on global grids; 3 = 2 with |Phi| operands and w = 1 (the geometry pass that
+// computes the per-entry bounds T_ij = sum_r |phi_i(r)| |phi_j(r)| of mode 1).
 struct HScale {
-    double c1, c2;   // rounding constants of the hi and lo grids
-    long long lo;    // offset (doubles) of an entry's lo limb from its hi limb (KBG_DET_SPLIT: nnz, else 1)
+    double c1, c2;   // mode 2: rounding constants of the hi and lo grids
+    long long lo;    // mode 2: offset (doubles) of an entry's lo limb from its hi limb (KBG_DET_SPLIT: nnz, else 1)
+    int ew;          // mode 1: max|w| < 2^ew
+    const int16_t* etab;  // mode 1: T_ij < 2^etab[entry]
 };
 __shared__ HScale s_hscale;  // per CTA, set by thread 0 at kernel start
 
@@ -371,10 +376,18 @@ __device__ __forceinline__ void red_add(double* p, double v) {
 
 // (C1, C2) from the bit pattern of max|V| (sign cleared; NaN/inf give NaN H)
 // and wfac = |dV| * hbound.
-__device__ __forceinline__ HScale hscale_of(unsigned long long vbits, double wfac, int64_t nnz) {
+__device__ __forceinline__ HScale hscale_of(unsigned long long vbits, double wfac, int64_t nnz,
+                                            const int16_t* etab = nullptr) {
     HScale h;
     h.lo = KBG_DET_SPLIT ? nnz : 1;
+    h.etab = etab;
     const double m = __longlong_as_double(static_cast<long long>(vbits & 0x7fffffffffffffffull)) * wfac;
+    h.ew = 5000;  // non-finite V: C overflows to inf and H becomes NaN (loud)
+    if (m <= 1.79e308) {
+        int e = -1100;
+        if (m > 0.0) frexp(m, &e);  // m < 2^e
+        h.ew = e;
+    }
     if (!(m <= 1.79e308)) {
         h.c1 = __longlong_as_double(0x7ff8000000000000ll);
         h.c2 = 0.0;
@@ -391,9 +404,19 @@ __device__ __forceinline__ HScale hscale_of(unsigned long long vbits, double wfa
     return h;
 }
 
+// Mode 1: v rounded to the grid 2^(k-51) of entry idx, k = ew + etab[idx] (max|w| T_ij < 2^k, so every
+// partial sum of the entry stays below 2^52 grid steps: exact FP64 additions, any order). The rounding
+// constant 1.5 * 2^(k+1) is built from its bits.
+__device__ __forceinline__ double grid_round1(double v, int64_t idx) {
+    int k = s_hscale.ew + static_cast<int>(s_hscale.etab[idx]) + 1 + 1023;
+    k = k < 1 ? 1 : (k > 2047 ? 2047 : k);  // 2047: inf -> NaN result (bound overflow is loud)
+    const double C = __longlong_as_double((static_cast<long long>(k) << 52) | (1ll << 51));
+    return __dsub_rn(__dadd_rn(v, C), C);
+}
+
 // Scatter of one accumulated tile: rows ra0 + [0, 8*TM) (group rows < rend),
 // columns cb0 + [0, 8*TN) of cover cj; canonical rows (cover ci <= cj) only.
-template <bool DET, int TM, int TN>
+template <int DET, int TM, int TN>
 __device__ __forceinline__ void h_scatter(const Smem& sm, const double (&c)[TM][TN][2], int ncov, int cj, int ra0,
                                           int rend, int cb0, double* __restrict__ H, int scatter,
                                           int lane) {
@@ -413,7 +436,10 @@ __device__ __forceinline__ void h_scatter(const Smem& sm, const double (&c)[TM][
                 const int col = cb0 + 8 * j + (lane & 3) * 2 + e;
                 if (off >= 0 && col < nb && !(KBG_EXPERIMENTS && (scatter & 2))) {
                     const double v = c[i][j][e];  // the fault hook's sign is folded into w
-                    if (DET) {
+                    if (DET == 1) {
+                        const int64_t idx = off + ri * nb + col;
+                        red_add(H + idx, grid_round1(v, idx));
+                    } else if (DET) {
                         const double hi = __dsub_rn(__dadd_rn(v, c1), c1);
                         const double lo = __dsub_rn(__dadd_rn(__dsub_rn(v, hi), c2), c2);
                         double* p = H + (KBG_DET_SPLIT ? 1 : 2) * (off + ri * nb + col);
@@ -429,14 +455,9 @@ __device__ __forceinline__ void h_scatter(const Smem& sm, const double (&c)[TM][
     }
 }
 
-// Timing experiment only (H is WRONG): skip the w scaling of the A fragments.
-#ifndef KBG_H_NOSCALE
-#define KBG_H_NOSCALE 0
-#endif
-
 // One partner: C(8*TM x 8*TN) += Phi_rows diag(w) Phi_cj^T over the quads in
 // qm. Tiles with <= 2 DMMAs per quad alternate two accumulator sets.
-template <bool DET, int TM, int TN>
+template <int DET, int TM, int TN>
 __device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict__ w, int ncov, int cj, int ra0,
                                        int rend, int cb0, uint32_t qm, double* __restrict__ H, int scatter,
                                        int lane) {
@@ -459,9 +480,9 @@ __device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict_
         const double wv = pw[col];
         double a[TM], bb[TN];
 #pragma unroll
-        for (int i = 0; i < TM; ++i) a[i] = KBG_H_NOSCALE ? pa[i * 512 + (col ^ sa)] : pa[i * 512 + (col ^ sa)] * wv;
+        for (int i = 0; i < TM; ++i) a[i] = DET == 3 ? fabs(pa[i * 512 + (col ^ sa)]) : pa[i * 512 + (col ^ sa)] * wv;
 #pragma unroll
-        for (int j = 0; j < TN; ++j) bb[j] = pb[j * 512 + (col ^ sb)];
+        for (int j = 0; j < TN; ++j) bb[j] = DET == 3 ? fabs(pb[j * 512 + (col ^ sb)]) : pb[j * 512 + (col ^ sb)];
 #pragma unroll
         for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -492,7 +513,7 @@ __device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict_
 
 // Two partners sharing the group's (w-scaled) A fragments: per quad of
 // q1 | q2 the A fragments are loaded and scaled once.
-template <bool DET, int TM, int TN1, int TN2>
+template <int DET, int TM, int TN1, int TN2>
 __device__ __forceinline__ void h_tile2(const Smem& sm, const double* __restrict__ w, int ncov, int cj1, int cj2,
                                         int ra0, int rend, uint32_t q1, uint32_t q2, double* __restrict__ H,
                                         int scatter, int lane) {
@@ -524,11 +545,11 @@ __device__ __forceinline__ void h_tile2(const Smem& sm, const double* __restrict
             double a[TM];
 #pragma unroll
             for (int i = 0; i < TM; ++i)
-                a[i] = KBG_H_NOSCALE ? pa[i * 512 + (col ^ sa)] : pa[i * 512 + (col ^ sa)] * wv;
+                a[i] = DET == 3 ? fabs(pa[i * 512 + (col ^ sa)]) : pa[i * 512 + (col ^ sa)] * wv;
             if (W1) {
                 double bb[TN1];
 #pragma unroll
-                for (int j = 0; j < TN1; ++j) bb[j] = pb1[j * 512 + (col ^ sb1)];
+                for (int j = 0; j < TN1; ++j) bb[j] = DET == 3 ? fabs(pb1[j * 512 + (col ^ sb1)]) : pb1[j * 512 + (col ^ sb1)];
 #pragma unroll
                 for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -537,7 +558,7 @@ __device__ __forceinline__ void h_tile2(const Smem& sm, const double* __restrict
             if (W2) {
                 double bb[TN2];
 #pragma unroll
-                for (int j = 0; j < TN2; ++j) bb[j] = pb2[j * 512 + (col ^ sb2)];
+                for (int j = 0; j < TN2; ++j) bb[j] = DET == 3 ? fabs(pb2[j * 512 + (col ^ sb2)]) : pb2[j * 512 + (col ^ sb2)];
 #pragma unroll
                 for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -552,7 +573,7 @@ __device__ __forceinline__ void h_tile2(const Smem& sm, const double* __restrict
     h_scatter<DET, TM, TN2>(sm, c2, ncov, cj2, ra0, rend, 0, H, scatter, lane);
 }
 
-template <bool DET, int TM, int TN1>
+template <int DET, int TM, int TN1>
 __device__ __forceinline__ void h_tile2_tn2(int tn2, const Smem& sm, const double* w, int ncov, int cj1, int cj2,
                                             int ra0, int rend, uint32_t q1, uint32_t q2, double* H,
                                             int scatter, int lane) {
@@ -563,9 +584,11 @@ __device__ __forceinline__ void h_tile2_tn2(int tn2, const Smem& sm, const doubl
 }
 
 // One H element into the accumulator (FP64 RED, or the deterministic two-limb split).
-template <bool DET>
+template <int DET>
 __device__ __forceinline__ void h_add(double* __restrict__ H, int64_t idx, double v) {
-    if (DET) {
+    if (DET == 1) {
+        red_add(H + idx, grid_round1(v, idx));
+    } else if (DET) {
         const double hi = __dsub_rn(__dadd_rn(v, s_hscale.c1), s_hscale.c1);
         const double lo = __dsub_rn(__dadd_rn(__dsub_rn(v, hi), s_hscale.c2), s_hscale.c2);
         double* p = H + (KBG_DET_SPLIT ? 1 : 2) * idx;
@@ -582,7 +605,7 @@ __device__ __forceinline__ void h_add(double* __restrict__ H, int64_t idx, doubl
 // partner; per common point one A value (scaled by w) and 8 B values, which all 16 lanes of a half
 // warp read at the same address (shared-memory broadcast). Selected per task by its point density
 // (Task.pad2_, kb_tasks.cu) below the KBG_OPT_SPARSE_DFMA threshold (scatter bits 8..15).
-template <bool DET>
+template <int DET>
 __device__ __forceinline__ void h_task_dfma(const Smem& sm, const double* __restrict__ w, int ncov, const Task& t,
                                          double* __restrict__ H, int lane) {
     const GroupS& G = sm.grp()[t.g];
@@ -619,7 +642,7 @@ __device__ __forceinline__ void h_task_dfma(const Smem& sm, const double* __rest
     }
 }
 
-template <bool DET, bool SPARSE = false>
+template <int DET, bool SPARSE = false>
 __device__ __forceinline__ void h_task(const Smem& sm, const double* w, int ncov, const Task& t, double* H,
                                        int scatter, int lane) {
     if (SPARSE && t.pad2_ < (scatter >> 8)) {

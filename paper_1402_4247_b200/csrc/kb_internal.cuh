@@ -197,8 +197,9 @@ struct GridArgs {
     double dV;
     double sign;        // +1, or -1 under the fault hook
     int scatter;        // 0: FP64 atomic scatter; 1: plain stores (timing experiment only, wrong H);
-                        // bit value 16: deterministic two-limb scatter into out [nspin][nnz][2] (default)
+                        // bits 4..5: KBG_OPT_DETERMINISTIC mode (1 per-entry grid, 2 two limbs, 3 |Phi| pass)
     const unsigned long long* vbits;  // H, deterministic: bit pattern of max|V| (written by a preceding kernel)
+    const int16_t* etab;              // H, deterministic mode 1: per-entry bound exponents (T_ij < 2^etab)
     double wfac;        // H, deterministic: |dV| * hbound (kb_gridcore.cuh hscale_of)
     const double* in;   // dm [nspin][nnz] or veff [nspin][npts]
     double* out;        // rho [nspin][npts] or h [nspin][nnz]
@@ -353,7 +354,8 @@ int launch_mirror(const DevIndex& ix, const SysParams& sys, int nspin, double* h
 // caller zeroes), and H = hi + lo of the two-limb accumulator [nspin][nnz][2] (+ mirror blocks).
 int launch_absmax(const double* d_x, int64_t n, unsigned long long* d_out, cudaStream_t st);
 int launch_finalize(const DevIndex& ix, const SysParams& sys, int nspin, const double* acc, double* h, bool mirror,
-                    cudaStream_t st);
+                    cudaStream_t st, int limbs = 2);
+int launch_etab(const double* d_T, int64_t n, int16_t* d_etab, cudaStream_t st);
 int launch_dm_check(const DevIndex& ix, const SysParams& sys, int nspin, const double* dm,
                     unsigned long long* d_maxdiff_maxabs, cudaStream_t st);
 int launch_block_orbitals(const GridArgs& g, int64_t block, double* d_out, cudaStream_t st);
