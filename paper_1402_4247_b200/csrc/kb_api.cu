@@ -86,13 +86,11 @@ struct kbg_ctx {
     double* d_states = nullptr;     // scaled states scratch
     size_t cap_states = 0;
     // deterministic H (KBG_OPT_DETERMINISTIC, kb_gridcore.cuh h_scatter)
-    int det = 0;  // KBG_OPT_DETERMINISTIC: 0 FP64 atomics, 1 per-entry grid (one limb), 2 two limbs
+    int det = 0;  // KBG_OPT_DETERMINISTIC (off by default: +68 % H time on 56 atoms)
     double hbound = 0.0;            // >= sum over r of |phi_i(r) phi_j(r)| for any orbital pair (h_bound)
     double* d_hacc = nullptr;       // two-limb accumulator [nspin][nnz][2]
     size_t cap_hacc = 0;
     unsigned long long* d_vbits = nullptr;  // max|V| bit pattern of the current H pass
-    int16_t* d_etab = nullptr;      // mode 1: per-entry bound exponents, T_ij < 2^etab (built on first use)
-    bool etab_ok = false;
     // shard-local host transfers of kbg_grid_pass on a sharded context (KBG_OPT_SHARD_IO)
     int shard_io = 1;
     int sparse_thr = 0;  // KBG_OPT_SPARSE_DFMA (0: every task on DMMA)
@@ -334,9 +332,10 @@ kbg::GridArgs grid_args(kbg_ctx* c, int nspin, double dV, const double* in, doub
     if (!density) {
         g.scatter |= c->sparse_thr << 8;  // A5 switch: tasks below this point density (1/255) run DFMA
         g.vbits = c->d_vbits;  // deterministic: max|V| (k_absmax); legacy: non-finite flag of the kernels
-        g.scatter |= c->det << 4;        // KBG_OPT_DETERMINISTIC mode (kb_gridcore.cuh h_scatter)
-        g.wfac = c->det == 2 ? std::fabs(dV) * c->hbound : std::fabs(dV);
-        g.etab = c->d_etab;
+        if (c->det) {
+            g.scatter |= 16;  // deterministic two-limb scatter (kb_gridcore.cuh h_scatter)
+            g.wfac = std::fabs(dV) * c->hbound;
+        }
     }
     if (g.max_cover > 32 * c->nwarps || g.max_cover > kbg::kMaxCoverPerBlock)
         throw Error(KBG_ERR_DIMENSION, "a grid block is covered by too many atom images");
@@ -379,8 +378,8 @@ void comm_check(kbg_ctx* c) {
     }
 }
 
-// Doubles per H entry of the deterministic accumulator (mode 2: hi and lo limbs).
-int h_limbs(const kbg_ctx* c) { return c->det == 2 ? 2 : 1; }
+// Doubles per H entry of the accumulator (deterministic: hi and lo limbs).
+int h_limbs(const kbg_ctx* c) { return c->det ? 2 : 1; }
 
 int run_hamiltonian(kbg_ctx* c, int nspin, double dV, const double* d_veff, double* d_h, cudaStream_t st) {
     const kbg::GridArgs g = grid_args(c, nspin, dV, d_veff, d_h, false);
@@ -403,11 +402,8 @@ int run_hamiltonian(kbg_ctx* c, int nspin, double dV, const double* d_veff, doub
 // point of the device-resident V, accumulate; legacy -- zero [nspin][nnz] and
 // accumulate with FP64 atomics. The caller finalizes (launch_finalize) or
 // reduces across ranks (kb_comm.cu).
-void ensure_etab(kbg_ctx* c, cudaStream_t st);
-
 int h_accumulate(kbg_ctx* c, int nspin, double dV, const double* d_veff, double* acc, cudaStream_t st) {
     int n = 0;
-    if (c->det == 1) ensure_etab(c, st);
     const size_t ne = static_cast<size_t>(nspin) * c->ix.nnz * h_limbs(c);
     KBG_CUDA(cudaMemsetAsync(acc, 0, ne * sizeof(double), st));
     KBG_CUDA(cudaMemsetAsync(c->d_vbits, 0, sizeof(unsigned long long), st));
@@ -421,46 +417,6 @@ double* h_acc_buffer(kbg_ctx* c, int nspin, double* d_out) {
     if (!c->det) return d_out;
     ensure(c->d_hacc, c->cap_hacc, static_cast<size_t>(2) * nspin * std::max<int64_t>(1, c->ix.nnz));
     return c->d_hacc;
-}
-
-// Mode 1's per-entry bounds: T_ij = sum_r |phi_i(r)| |phi_j(r)| over the grid, accumulated once per
-// geometry by the H kernels themselves with |Phi| operands and w = 1 (mode 3: two exact limbs, so T has
-// the same bits on any number of GPUs; sharded contexts sum their partials through the peer exchange),
-// then etab = exponent of T. Every later mode-1 contribution to entry ij is rounded to the grid
-// 2^(ew + etab_ij - 51) with max|w| < 2^ew: its partial sums stay below 2^52 grid steps (exact, any order).
-void ensure_etab(kbg_ctx* c, cudaStream_t st) {
-    if (c->etab_ok) return;
-    const int64_t nnz = std::max<int64_t>(1, c->ix.nnz);
-    if (c->d_etab) cudaFree(c->d_etab);
-    c->d_etab = nullptr;
-    KBG_CUDA(cudaMalloc(&c->d_etab, nnz * sizeof(int16_t)));
-    double* T = nullptr;  // [nnz] bounds, then the accumulator [2][nnz] behind them
-    KBG_CUDA(cudaMallocAsync(&T, 3 * nnz * sizeof(double), st));
-    static const unsigned long long one_bits = 0x3ff0000000000000ull;  // max|w| = 1
-    KBG_CUDA(cudaMemcpyAsync(c->d_vbits, &one_bits, sizeof(one_bits), cudaMemcpyHostToDevice, st));
-    const int det = c->det;
-    c->det = 2;  // grid_args with the two-limb layout; the mode bits become 3 below
-    double* acc = c->comm_ready ? c->d_xbuf : T + nnz;
-    KBG_CUDA(cudaMemsetAsync(acc, 0, 2 * nnz * sizeof(double), st));
-    kbg::GridArgs g = grid_args(c, 1, 1.0, nullptr, acc, false);
-    g.scatter = (g.scatter & ~((3 << 4) | (0xFF << 8))) | (3 << 4);  // mode 3, no point-exact DFMA tasks
-    g.wfac = c->hbound;
-    g.in = nullptr;  // w = 1 (mode 3 ignores it)
-    if (c->persist_ok && c->persist && c->ix.phis && kbg::persist_fits(g, false))
-        kbg::launch_hamiltonian_persist(g, st);
-    else
-        kbg::launch_hamiltonian(g, c->blk_end - c->blk_begin, c->nwarps, st);
-    if (c->comm_ready) {
-        c->epoch += 2;
-        c->comm.ls = 2;
-        kbg::launch_reduce_mirror(c->comm, c->ix, c->P, 1, T, c->epoch - 1, st);
-    } else {
-        kbg::launch_finalize(c->ix, c->P, 1, acc, T, true, st, 2);
-    }
-    c->det = det;
-    kbg::launch_etab(T, c->ix.nnz, c->d_etab, st);
-    KBG_CUDA(cudaFreeAsync(T, st));
-    c->etab_ok = true;
 }
 
 // Max|V| of the last H pass (legacy path: only the non-finite flag): non-finite V -> KBG_ERR_NONFINITE
@@ -585,7 +541,6 @@ int kbg_build_index(kbg_ctx* c) {
         if (c->stream2) KBG_CUDA(cudaStreamSynchronize(c->stream2));
         kbg::BuildStream bs(c->stream);
         c->built = false;
-        c->etab_ok = false;
         c->hix = kbg::HostIndex();
         kbg::free_formats(c->fmt);
         kbg::build_index_device(c->P, c->ix, c->stream);
@@ -1375,7 +1330,6 @@ int kbg_comm_open(kbg_ctx* c, const void* handles) {
         kbg::CommArgs& cm = c->comm;
         cm.nranks = c->nranks;
         cm.rank = c->rank;
-        c->etab_ok = false;  // sharded: the bounds are summed over the ranks (first mode-1 call)
         const size_t nd = xbuf_doubles(c);
         for (int k = 0; k < c->nranks; ++k) {
             CommBlob b;
@@ -1978,11 +1932,7 @@ int kbg_set_option(kbg_ctx* c, int option, int64_t value) {
             c->schedule = static_cast<int>(value);
             return KBG_OK;
         case KBG_OPT_DETERMINISTIC:
-            if (value < 0 || value > 2) {
-                c->err = "set_option: deterministic must be 0 (FP64 atomics), 1 (per-entry grid) or 2 (two limbs)";
-                return KBG_ERR_CONFIG;
-            }
-            c->det = static_cast<int>(value);
+            c->det = value ? 1 : 0;
             return KBG_OK;
         case KBG_OPT_SHARD_IO:
             c->shard_io = value ? 1 : 0;
@@ -2028,7 +1978,6 @@ void kbg_destroy(kbg_ctx* c) {
     if (c->d_canon) cudaFree(c->d_canon);
     if (c->d_pairtab) cudaFree(c->d_pairtab);
     if (c->d_pown) cudaFree(c->d_pown);
-    if (c->d_etab) cudaFree(c->d_etab);
     if (c->comm.tstamp) cudaFree(c->comm.tstamp);
     if (c->d_cpre) cudaFree(c->d_cpre);
     c->veff.release();

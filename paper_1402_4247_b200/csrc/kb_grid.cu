@@ -23,16 +23,16 @@ __device__ __forceinline__ void for_warp_tasks(const GridArgs& g, const Smem& sm
     }
 }
 
-template <int NW, int DET>
+template <int NW, bool DET>
 __global__ void __launch_bounds__(NW * 32, 2) k_hamiltonian(GridArgs g) {
     const Smem sm = carve(0u, g);
     const int64_t b = g.blk_begin + blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (DET && tid == 0) s_hscale = hscale_of(*g.vbits, g.wfac, g.nnz, g.etab);  // stage_block syncs
+    if (DET && tid == 0) s_hscale = hscale_of(*g.vbits, g.wfac, g.nnz);  // stage_block syncs
     const int ncov = stage_block(g, b, sm, tid, NW * 32, [] { __syncthreads(); }, false, NW);
     if (ncov == 0) return;
     for (int spin = 0; spin < g.nspin; ++spin) {
-        double* Hs = g.out + spin * g.nnz * (DET >= 2 ? 2 : 1);
+        double* Hs = g.out + spin * g.nnz * (DET ? 2 : 1);
         for_warp_tasks<NW>(g, sm, warp,
                            [&](int e) { h_task<DET, true>(sm, sm.acc() + spin * 64, ncov, sm.task()[e], Hs, g.scatter, lane); });
     }
@@ -365,17 +365,15 @@ int launch_hamiltonian(const GridArgs& g0, int64_t nblk, int nwarps, cudaStream_
     GridArgs g = g0;
     const size_t smem = grid_smem_bytes(g, nwarps, false);
     set_layout(g, static_cast<size_t>(g.nspin) * 64);
-    const int det = (g.scatter >> 4) & 3;  // KBG_OPT_DETERMINISTIC mode (3: the |Phi| bound pass)
+    const bool det = g.scatter & 16;  // deterministic two-limb scatter (KBG_OPT_DETERMINISTIC)
     auto go = [&](auto kernel, int threads) {
         set_smem(kernel, smem);
         kernel<<<static_cast<unsigned>(nblk), threads, smem, st>>>(g);
     };
     if (nwarps == 4)
-        det == 3 ? go(k_hamiltonian<4, 3>, 128) : det == 2 ? go(k_hamiltonian<4, 2>, 128)
-        : det == 1 ? go(k_hamiltonian<4, 1>, 128) : go(k_hamiltonian<4, 0>, 128);
+        det ? go(k_hamiltonian<4, true>, 128) : go(k_hamiltonian<4, false>, 128);
     else
-        det == 3 ? go(k_hamiltonian<8, 3>, 256) : det == 2 ? go(k_hamiltonian<8, 2>, 256)
-        : det == 1 ? go(k_hamiltonian<8, 1>, 256) : go(k_hamiltonian<8, 0>, 256);
+        det ? go(k_hamiltonian<8, true>, 256) : go(k_hamiltonian<8, false>, 256);
     KBG_CUDA(cudaGetLastError());
     return 1;
 }
@@ -403,27 +401,6 @@ int launch_finalize(const DevIndex& ix, const SysParams& sys, int nspin, const d
     const unsigned grid = static_cast<unsigned>((ix.npair * 32 + 255) / 256);
     k_finalize<<<grid, 256, 0, st>>>(sys, ix.npair, nspin, ix.nnz, ix.pair_a, ix.pair_b, ix.pair_R, ix.pair_off,
                                      ix.pair_mirror, acc, h, mirror ? 1 : 0, limbs);
-    KBG_CUDA(cudaGetLastError());
-    return 1;
-}
-
-// Deterministic mode 1: per-entry bound exponents from T_ij = sum_r |phi_i| |phi_j| (T < 2^etab).
-__global__ void k_etab(const double* __restrict__ T, int64_t n, int16_t* __restrict__ etab) {
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const double t = T[i];
-        int e = -1100;  // T = 0: every contribution is an exact zero
-        if (!(t <= 1.79e308))
-            e = 5000;  // non-finite: H becomes NaN
-        else if (t > 0.0)
-            frexp(t, &e);
-        etab[i] = static_cast<int16_t>(e);
-    }
-}
-
-int launch_etab(const double* d_T, int64_t n, int16_t* d_etab, cudaStream_t st) {
-    if (n <= 0) return 0;
-    k_etab<<<148 * 4, 256, 0, st>>>(d_T, n, d_etab);
     KBG_CUDA(cudaGetLastError());
     return 1;
 }

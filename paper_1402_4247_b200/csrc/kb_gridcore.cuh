@@ -343,7 +343,7 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int tid
 }
 
 // ---- H --------------------------------------------------------------------------
-// Deterministic accumulation (KBG_OPT_DETERMINISTIC, scatter bit value 16, default).
+// Deterministic accumulation (KBG_OPT_DETERMINISTIC; scatter bit value 16).
 // FP64 atomics add in arrival order, so plain RED.ADD.F64 makes H's last bits
 // depend on the schedule. Instead every contribution v (one task's sum over
 // the block points it covers) is split into two parts that lie on FIXED grids,
@@ -357,14 +357,9 @@ __device__ int stage_block(const GridArgs& g, int64_t b, const Smem& sm, int tid
 // kb_comm.cu). H = hi + lo is rounded once at the end (k_finalize). Rounding
 // to a grid is two exact additions of C = 1.5 * 2^(k+52) (|x| < 2^(k+51)):
 // (x + C) - C is x rounded to a multiple of 2^k.
-// DET modes of the H kernels: 0 FP64 atomics; 1 deterministic, one limb on a per-entry grid (etab);
-// 2 deterministic, two limbs on global grids; 3 = 2 with |Phi| operands and w = 1 (the geometry pass that
-// computes the per-entry bounds T_ij = sum_r |phi_i(r)| |phi_j(r)| of mode 1).
 struct HScale {
-    double c1, c2;   // mode 2: rounding constants of the hi and lo grids
-    long long lo;    // mode 2: offset (doubles) of an entry's lo limb from its hi limb (KBG_DET_SPLIT: nnz, else 1)
-    int ew;          // mode 1: max|w| < 2^ew
-    const int16_t* etab;  // mode 1: T_ij < 2^etab[entry]
+    double c1, c2;   // rounding constants of the hi and lo grids
+    long long lo;    // offset (doubles) of an entry's lo limb from its hi limb (KBG_DET_SPLIT: nnz, else 1)
 };
 __shared__ HScale s_hscale;  // per CTA, set by thread 0 at kernel start
 
@@ -376,18 +371,10 @@ __device__ __forceinline__ void red_add(double* p, double v) {
 
 // (C1, C2) from the bit pattern of max|V| (sign cleared; NaN/inf give NaN H)
 // and wfac = |dV| * hbound.
-__device__ __forceinline__ HScale hscale_of(unsigned long long vbits, double wfac, int64_t nnz,
-                                            const int16_t* etab = nullptr) {
+__device__ __forceinline__ HScale hscale_of(unsigned long long vbits, double wfac, int64_t nnz) {
     HScale h;
     h.lo = KBG_DET_SPLIT ? nnz : 1;
-    h.etab = etab;
     const double m = __longlong_as_double(static_cast<long long>(vbits & 0x7fffffffffffffffull)) * wfac;
-    h.ew = 5000;  // non-finite V: C overflows to inf and H becomes NaN (loud)
-    if (m <= 1.79e308) {
-        int e = -1100;
-        if (m > 0.0) frexp(m, &e);  // m < 2^e
-        h.ew = e;
-    }
     if (!(m <= 1.79e308)) {
         h.c1 = __longlong_as_double(0x7ff8000000000000ll);
         h.c2 = 0.0;
@@ -404,19 +391,9 @@ __device__ __forceinline__ HScale hscale_of(unsigned long long vbits, double wfa
     return h;
 }
 
-// Mode 1: v rounded to the grid 2^(k-51) of entry idx, k = ew + etab[idx] (max|w| T_ij < 2^k, so every
-// partial sum of the entry stays below 2^52 grid steps: exact FP64 additions, any order). The rounding
-// constant 1.5 * 2^(k+1) is built from its bits.
-__device__ __forceinline__ double grid_round1(double v, int64_t idx) {
-    int k = s_hscale.ew + static_cast<int>(s_hscale.etab[idx]) + 1 + 1023;
-    k = k < 1 ? 1 : (k > 2047 ? 2047 : k);  // 2047: inf -> NaN result (bound overflow is loud)
-    const double C = __longlong_as_double((static_cast<long long>(k) << 52) | (1ll << 51));
-    return __dsub_rn(__dadd_rn(v, C), C);
-}
-
 // Scatter of one accumulated tile: rows ra0 + [0, 8*TM) (group rows < rend),
 // columns cb0 + [0, 8*TN) of cover cj; canonical rows (cover ci <= cj) only.
-template <int DET, int TM, int TN>
+template <bool DET, int TM, int TN>
 __device__ __forceinline__ void h_scatter(const Smem& sm, const double (&c)[TM][TN][2], int ncov, int cj, int ra0,
                                           int rend, int cb0, double* __restrict__ H, int scatter,
                                           int lane) {
@@ -436,10 +413,7 @@ __device__ __forceinline__ void h_scatter(const Smem& sm, const double (&c)[TM][
                 const int col = cb0 + 8 * j + (lane & 3) * 2 + e;
                 if (off >= 0 && col < nb && !(KBG_EXPERIMENTS && (scatter & 2))) {
                     const double v = c[i][j][e];  // the fault hook's sign is folded into w
-                    if (DET == 1) {
-                        const int64_t idx = off + ri * nb + col;
-                        red_add(H + idx, grid_round1(v, idx));
-                    } else if (DET) {
+                    if (DET) {
                         const double hi = __dsub_rn(__dadd_rn(v, c1), c1);
                         const double lo = __dsub_rn(__dadd_rn(__dsub_rn(v, hi), c2), c2);
                         double* p = H + (KBG_DET_SPLIT ? 1 : 2) * (off + ri * nb + col);
@@ -457,7 +431,7 @@ __device__ __forceinline__ void h_scatter(const Smem& sm, const double (&c)[TM][
 
 // One partner: C(8*TM x 8*TN) += Phi_rows diag(w) Phi_cj^T over the quads in
 // qm. Tiles with <= 2 DMMAs per quad alternate two accumulator sets.
-template <int DET, int TM, int TN>
+template <bool DET, int TM, int TN>
 __device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict__ w, int ncov, int cj, int ra0,
                                        int rend, int cb0, uint32_t qm, double* __restrict__ H, int scatter,
                                        int lane) {
@@ -480,9 +454,9 @@ __device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict_
         const double wv = pw[col];
         double a[TM], bb[TN];
 #pragma unroll
-        for (int i = 0; i < TM; ++i) a[i] = DET == 3 ? fabs(pa[i * 512 + (col ^ sa)]) : pa[i * 512 + (col ^ sa)] * wv;
+        for (int i = 0; i < TM; ++i) a[i] = pa[i * 512 + (col ^ sa)] * wv;
 #pragma unroll
-        for (int j = 0; j < TN; ++j) bb[j] = DET == 3 ? fabs(pb[j * 512 + (col ^ sb)]) : pb[j * 512 + (col ^ sb)];
+        for (int j = 0; j < TN; ++j) bb[j] = pb[j * 512 + (col ^ sb)];
 #pragma unroll
         for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -513,7 +487,7 @@ __device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict_
 
 // Two partners sharing the group's (w-scaled) A fragments: per quad of
 // q1 | q2 the A fragments are loaded and scaled once.
-template <int DET, int TM, int TN1, int TN2>
+template <bool DET, int TM, int TN1, int TN2>
 __device__ __forceinline__ void h_tile2(const Smem& sm, const double* __restrict__ w, int ncov, int cj1, int cj2,
                                         int ra0, int rend, uint32_t q1, uint32_t q2, double* __restrict__ H,
                                         int scatter, int lane) {
@@ -545,11 +519,11 @@ __device__ __forceinline__ void h_tile2(const Smem& sm, const double* __restrict
             double a[TM];
 #pragma unroll
             for (int i = 0; i < TM; ++i)
-                a[i] = DET == 3 ? fabs(pa[i * 512 + (col ^ sa)]) : pa[i * 512 + (col ^ sa)] * wv;
+                a[i] = pa[i * 512 + (col ^ sa)] * wv;
             if (W1) {
                 double bb[TN1];
 #pragma unroll
-                for (int j = 0; j < TN1; ++j) bb[j] = DET == 3 ? fabs(pb1[j * 512 + (col ^ sb1)]) : pb1[j * 512 + (col ^ sb1)];
+                for (int j = 0; j < TN1; ++j) bb[j] = pb1[j * 512 + (col ^ sb1)];
 #pragma unroll
                 for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -558,7 +532,7 @@ __device__ __forceinline__ void h_tile2(const Smem& sm, const double* __restrict
             if (W2) {
                 double bb[TN2];
 #pragma unroll
-                for (int j = 0; j < TN2; ++j) bb[j] = DET == 3 ? fabs(pb2[j * 512 + (col ^ sb2)]) : pb2[j * 512 + (col ^ sb2)];
+                for (int j = 0; j < TN2; ++j) bb[j] = pb2[j * 512 + (col ^ sb2)];
 #pragma unroll
                 for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -573,7 +547,7 @@ __device__ __forceinline__ void h_tile2(const Smem& sm, const double* __restrict
     h_scatter<DET, TM, TN2>(sm, c2, ncov, cj2, ra0, rend, 0, H, scatter, lane);
 }
 
-template <int DET, int TM, int TN1>
+template <bool DET, int TM, int TN1>
 __device__ __forceinline__ void h_tile2_tn2(int tn2, const Smem& sm, const double* w, int ncov, int cj1, int cj2,
                                             int ra0, int rend, uint32_t q1, uint32_t q2, double* H,
                                             int scatter, int lane) {
@@ -584,11 +558,9 @@ __device__ __forceinline__ void h_tile2_tn2(int tn2, const Smem& sm, const doubl
 }
 
 // One H element into the accumulator (FP64 RED, or the deterministic two-limb split).
-template <int DET>
+template <bool DET>
 __device__ __forceinline__ void h_add(double* __restrict__ H, int64_t idx, double v) {
-    if (DET == 1) {
-        red_add(H + idx, grid_round1(v, idx));
-    } else if (DET) {
+    if (DET) {
         const double hi = __dsub_rn(__dadd_rn(v, s_hscale.c1), s_hscale.c1);
         const double lo = __dsub_rn(__dadd_rn(__dsub_rn(v, hi), s_hscale.c2), s_hscale.c2);
         double* p = H + (KBG_DET_SPLIT ? 1 : 2) * idx;
@@ -605,7 +577,7 @@ __device__ __forceinline__ void h_add(double* __restrict__ H, int64_t idx, doubl
 // partner; per common point one A value (scaled by w) and 8 B values, which all 16 lanes of a half
 // warp read at the same address (shared-memory broadcast). Selected per task by its point density
 // (Task.pad2_, kb_tasks.cu) below the KBG_OPT_SPARSE_DFMA threshold (scatter bits 8..15).
-template <int DET>
+template <bool DET>
 __device__ __forceinline__ void h_task_dfma(const Smem& sm, const double* __restrict__ w, int ncov, const Task& t,
                                          double* __restrict__ H, int lane) {
     const GroupS& G = sm.grp()[t.g];
@@ -642,7 +614,7 @@ __device__ __forceinline__ void h_task_dfma(const Smem& sm, const double* __rest
     }
 }
 
-template <int DET, bool SPARSE = false>
+template <bool DET, bool SPARSE = false>
 __device__ __forceinline__ void h_task(const Smem& sm, const double* w, int ncov, const Task& t, double* H,
                                        int scatter, int lane) {
     if (SPARSE && t.pad2_ < (scatter >> 8)) {
@@ -700,8 +672,7 @@ __device__ __forceinline__ void h_task(const Smem& sm, const double* w, int ncov
 // K-step values as two 16-byte loads.
 template <int TM>
 __device__ __forceinline__ void gather_a(const Smem& sm, int ncov, const int (&rci)[TM], const int (&rri)[TM], int cj,
-                                         int kc, const double* __restrict__ Dr, int lane, double (&a)[TM][4],
-                                         int exp = 0) {
+                                         int kc, const double* __restrict__ Dr, int lane, double (&a)[TM][4]) {
     const int stride = 16 * ((sm.cov()[cj].norb + 15) >> 4);
 #if KBG_L2_HINT >= 2
     uint64_t pol;
@@ -787,7 +758,7 @@ __device__ __forceinline__ void rho_partner(const double* __restrict__ pb, int s
 
 template <int TM>
 __device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, int cbeg, int cend,
-                              const double* __restrict__ Dr, double* __restrict__ racc, int lane, int exp) {
+                              const double* __restrict__ Dr, double* __restrict__ racc, int lane) {
     const GroupS& G = sm.grp()[gi];
     const int rend = G.row0 + G.rows;
     int rci[TM], rri[TM];
@@ -806,63 +777,41 @@ __device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, 
     uint64_t bits = sm.pbits()[(8 / kRhoOct) * gi + h] & (~0ull << cbeg) &
                     (cend >= 64 ? ~0ull : ((1ull << cend) - 1ull));
     const int colbase = 8 * kRhoOct * h + (lane >> 2);
-    // one partner: D' fragments in `a` (K chunk 0); more chunks for > 16 orbitals
-    auto process = [&](int cj, double (&a)[TM][4]) {
-#if KBG_RHO_UNIFORM
-        // provably warp-uniform (shuffle from lane 0): the octet branches need no WARPSYNC
-        const uint32_t om4 = __shfl_sync(0xffffffffu, (pom[cj] >> (kRhoOct * h)) & ((1u << kRhoOct) - 1u), 0);
-#else
-        const uint32_t om4 = (pom[cj] >> (kRhoOct * h)) & ((1u << kRhoOct) - 1u);
-#endif
-        const CoverS& B = sm.cov()[cj];
-        const int nkc = (B.norb + 15) >> 4;
-        for (int kc = 0; kc < nkc; ++kc) {
-            // chunk kc > 0 overwrites `a` (the next partner is prefetched into the other buffer)
-            if (kc > 0) gather_a<TM>(sm, ncov, rci, rri, cj, kc, Dr, lane, a, exp);
-            const int ks = min(4, (B.norb - 16 * kc + 3) >> 2);
-            const int rb = B.row0 + 16 * kc + (lane & 3);
-            const double* pb = sm.phi() + rb * 64;
-            const int swb = swz(rb);
-            switch (ks) {
-                case 1: rho_partner<TM, 1>(pb, swb, om4, a, y, colbase); break;
-                case 2: rho_partner<TM, 2>(pb, swb, om4, a, y, colbase); break;
-                case 3: rho_partner<TM, 3>(pb, swb, om4, a, y, colbase); break;
-                default: rho_partner<TM, 4>(pb, swb, om4, a, y, colbase); break;
-            }
+    // one K chunk (<= 16 orbitals of cj from orbital 16 kc) of one partner, D' fragments in `a`
+    auto chunk = [&](const CoverS& B, int kc, uint32_t om4, const double (&a)[TM][4]) {
+        const int ks = min(4, (B.norb - 16 * kc + 3) >> 2);
+        const int rb = B.row0 + 16 * kc + (lane & 3);
+        const double* pb = sm.phi() + rb * 64;
+        const int swb = swz(rb);
+        switch (ks) {
+            case 1: rho_partner<TM, 1>(pb, swb, om4, a, y, colbase); break;
+            case 2: rho_partner<TM, 2>(pb, swb, om4, a, y, colbase); break;
+            case 3: rho_partner<TM, 3>(pb, swb, om4, a, y, colbase); break;
+            default: rho_partner<TM, 4>(pb, swb, om4, a, y, colbase); break;
         }
     };
-    if (kRhoPrefetch) {
-        // partners two at a time with ping-pong fragment registers: the gather of
-        // the next partner is in flight while the current one is contracted
-        double a0[TM][4], a1[TM][4];
-        int c0 = bits ? __ffsll(bits) - 1 : -1;
-        if (c0 >= 0) {
-            bits &= bits - 1;
-            gather_a<TM>(sm, ncov, rci, rri, c0, 0, Dr, lane, a0, exp);
-        }
-        while (c0 >= 0) {
-            const int c1 = bits ? __ffsll(bits) - 1 : -1;
-            if (c1 >= 0) {
-                bits &= bits - 1;
-                gather_a<TM>(sm, ncov, rci, rri, c1, 0, Dr, lane, a1, exp);
-            }
-            process(c0, a0);
-            if (c1 < 0) break;
-            c0 = bits ? __ffsll(bits) - 1 : -1;
-            if (c0 >= 0) {
-                bits &= bits - 1;
-                gather_a<TM>(sm, ncov, rci, rri, c0, 0, Dr, lane, a0, exp);
-            }
-            process(c1, a1);
-        }
-    } else {
-        // one fragment set: more warps per SM hide the gather latency instead
-        while (bits) {
-            const int cj = __ffsll(bits) - 1;
-            bits &= bits - 1;
+    // Partners in two 32-bit passes (blocks rarely have more than 32 covers: the common pass costs
+    // 32-bit find-first-set and clear instead of 64-bit ones). One fragment set: more warps per SM hide
+    // the gather latency (a ping-pong prefetch spills at 96 and 128 registers).
+    for (int w32 = 0; w32 < 2; ++w32) {
+        uint32_t bits32 = static_cast<uint32_t>(bits >> (32 * w32));
+        while (bits32) {
+            const int cj = 32 * w32 + __ffs(bits32) - 1;
+            bits32 &= bits32 - 1;
             double a[TM][4];
-            gather_a<TM>(sm, ncov, rci, rri, cj, 0, Dr, lane, a, exp);
-            process(cj, a);
+            gather_a<TM>(sm, ncov, rci, rri, cj, 0, Dr, lane, a);
+#if KBG_RHO_UNIFORM
+            // provably warp-uniform (shuffle from lane 0): the octet branches need no WARPSYNC
+            const uint32_t om4 = __shfl_sync(0xffffffffu, (pom[cj] >> (kRhoOct * h)) & ((1u << kRhoOct) - 1u), 0);
+#else
+            const uint32_t om4 = (pom[cj] >> (kRhoOct * h)) & ((1u << kRhoOct) - 1u);
+#endif
+            const CoverS& B = sm.cov()[cj];
+            for (int kc = 0;;) {  // K chunks of 16 orbitals (one for every Fe3O4 cover)
+                chunk(B, kc, om4, a);
+                if (16 * ++kc >= B.norb) break;
+                gather_a<TM>(sm, ncov, rci, rri, cj, kc, Dr, lane, a);
+            }
         }
     }
     // rho(slot) += sum over rows of Phi_row(slot) * Y(row, slot): per-lane
@@ -914,13 +863,13 @@ __device__ void rho_task_rows(const Smem& sm, int ncov, int gi, int ra0, int h, 
 }
 
 __device__ __forceinline__ void rho_task(const Smem& sm, int ncov, const Task& t, const double* Dr, double* racc,
-                                         int lane, int exp = 0) {
+                                         int lane) {
     const GroupS& G = sm.grp()[t.g];
     for (int i0 = 0; i0 < G.tm; i0 += 2) {
         if (G.tm - i0 >= 2)
-            rho_task_rows<2>(sm, ncov, t.g, G.row0 + 8 * i0, t.half, t.cj, t.qmask, Dr, racc, lane, exp);
+            rho_task_rows<2>(sm, ncov, t.g, G.row0 + 8 * i0, t.half, t.cj, t.qmask, Dr, racc, lane);
         else
-            rho_task_rows<1>(sm, ncov, t.g, G.row0 + 8 * i0, t.half, t.cj, t.qmask, Dr, racc, lane, exp);
+            rho_task_rows<1>(sm, ncov, t.g, G.row0 + 8 * i0, t.half, t.cj, t.qmask, Dr, racc, lane);
     }
 }
 

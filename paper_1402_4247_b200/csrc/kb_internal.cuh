@@ -31,10 +31,6 @@ __host__ __device__ __forceinline__ int64_t det_lo(int s, int64_t e, int64_t nnz
 constexpr int kGroupRows = 16;  // covers are packed into row groups of <= 16 orbitals (2 DMMA row tiles)
 constexpr int kMaxTaskWarps = 32;  // task lists are LPT-balanced over <= 24 consumer warps
 constexpr int kMaxCoverPerBlock = 64;
-#ifndef KBG_RHO_PREFETCH
-#define KBG_RHO_PREFETCH 0
-#endif
-constexpr bool kRhoPrefetch = KBG_RHO_PREFETCH;  // ping-pong D' prefetch (needs ~128 registers, 16 warps)
 constexpr int kRhoOct = 4;  // octets per rho task (4: halves of the block, 2: quarters; halves measured faster)
 
 // Error taxonomy of kband (common.hpp:21-38) carried as a status code.
@@ -197,9 +193,8 @@ struct GridArgs {
     double dV;
     double sign;        // +1, or -1 under the fault hook
     int scatter;        // 0: FP64 atomic scatter; 1: plain stores (timing experiment only, wrong H);
-                        // bits 4..5: KBG_OPT_DETERMINISTIC mode (1 per-entry grid, 2 two limbs, 3 |Phi| pass)
+                        // bit value 16: deterministic two-limb scatter into out [nspin][2][nnz]
     const unsigned long long* vbits;  // H, deterministic: bit pattern of max|V| (written by a preceding kernel)
-    const int16_t* etab;              // H, deterministic mode 1: per-entry bound exponents (T_ij < 2^etab)
     double wfac;        // H, deterministic: |dV| * hbound (kb_gridcore.cuh hscale_of)
     const double* in;   // dm [nspin][nnz] or veff [nspin][npts]
     double* out;        // rho [nspin][npts] or h [nspin][nnz]
@@ -355,7 +350,6 @@ int launch_mirror(const DevIndex& ix, const SysParams& sys, int nspin, double* h
 int launch_absmax(const double* d_x, int64_t n, unsigned long long* d_out, cudaStream_t st);
 int launch_finalize(const DevIndex& ix, const SysParams& sys, int nspin, const double* acc, double* h, bool mirror,
                     cudaStream_t st, int limbs = 2);
-int launch_etab(const double* d_T, int64_t n, int16_t* d_etab, cudaStream_t st);
 int launch_dm_check(const DevIndex& ix, const SysParams& sys, int nspin, const double* dm,
                     unsigned long long* d_maxdiff_maxabs, cudaStream_t st);
 int launch_block_orbitals(const GridArgs& g, int64_t block, double* d_out, cudaStream_t st);

@@ -167,7 +167,7 @@ __device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes, uin
 // Producer warp: block k goes to buffer k & 1. The block after the current
 // one is fetched early and its cache image prefetched into L2, so the bulk
 // copy issued when its buffer frees up is served from L2.
-template <bool DENSITY, int DET>
+template <bool DENSITY, bool DET>
 __device__ void producer(const GridArgs& g, const Buffers<DENSITY>& B, int lane) {
     unsigned long long t_wait = 0, t0 = clock64();
     uint64_t pol = 0;
@@ -273,7 +273,7 @@ __device__ void producer(const GridArgs& g, const Buffers<DENSITY>& B, int lane)
     }
 }
 
-template <bool DENSITY, int DET, bool SPARSE>
+template <bool DENSITY, bool DET, bool SPARSE>
 __device__ void consumer(const GridArgs& g, const Buffers<DENSITY>& B, int cw, int lane) {
     constexpr int NC = Cfg<DENSITY>::NC;
     unsigned long long t_wait = 0, t_tail = 0, t0 = clock64();
@@ -312,9 +312,9 @@ __device__ void consumer(const GridArgs& g, const Buffers<DENSITY>& B, int cw, i
                     double* res = sm.acc() + static_cast<size_t>(q) * 32;
                     res[lane] = 0.0;
                     __syncwarp();
-                    rho_task(sm, ncov, t, g.dmr + spin * g.nrep, res - 32 * t.half, lane, g.scatter);
+                    rho_task(sm, ncov, t, g.dmr + spin * g.nrep, res - 32 * t.half, lane);
                 } else {
-                    h_task<DET, SPARSE>(sm, sm.acc() + spin * 64, ncov, t, g.out + spin * g.nnz * (DET >= 2 ? 2 : 1), g.scatter,
+                    h_task<DET, SPARSE>(sm, sm.acc() + spin * 64, ncov, t, g.out + spin * g.nnz * (DET ? 2 : 1), g.scatter,
                                         lane);
                 }
             }
@@ -327,9 +327,9 @@ __device__ void consumer(const GridArgs& g, const Buffers<DENSITY>& B, int cw, i
                 racc[lane + 32] = 0.0;
                 __syncwarp();
                 for (int w = cw; w < g.task_warps; w += NC)
-                    for (int e = sm.wptr()[w]; e < sm.wptr()[w + 1]; ++e) rho_task(sm, ncov, sm.task()[e], Dr, racc, lane, g.scatter);
+                    for (int e = sm.wptr()[w]; e < sm.wptr()[w + 1]; ++e) rho_task(sm, ncov, sm.task()[e], Dr, racc, lane);
             } else {
-                double* Hs = g.out + spin * g.nnz * (DET >= 2 ? 2 : 1);
+                double* Hs = g.out + spin * g.nnz * (DET ? 2 : 1);
                 for (int w = cw; w < g.task_warps; w += NC)
                     for (int e = sm.wptr()[w]; e < sm.wptr()[w + 1]; ++e)
                         h_task<DET, SPARSE>(sm, sm.acc() + spin * 64, ncov, sm.task()[e], Hs, g.scatter, lane);
@@ -409,7 +409,7 @@ __device__ void consumer(const GridArgs& g, const Buffers<DENSITY>& B, int cw, i
     }
 }
 
-template <bool DENSITY, int DET, bool SPARSE = false>
+template <bool DENSITY, bool DET, bool SPARSE = false>
 __global__ void __launch_bounds__(Cfg<DENSITY>::NT, 1) k_persist(GridArgs g) {
     const Buffers<DENSITY> B = carve_all<DENSITY>(g);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(Cfg<DENSITY>::NT, 1) k_persist(GridArgs g) {
             mbar_init(&B.empty[s], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        if (DET) s_hscale = hscale_of(*g.vbits, g.wfac, g.nnz, g.etab);
+        if (DET) s_hscale = hscale_of(*g.vbits, g.wfac, g.nnz);
     }
     __syncthreads();
     if (warp < kPersistProducers) {
@@ -445,8 +445,8 @@ int launch_persist(const GridArgs& g0, bool density, cudaStream_t st) {
     set_layout(g, persist_acc(g, density));
     KBG_CUDA(cudaMemsetAsync(g.counter, 0, sizeof(int), st));
     if (density) {
-        set_smem(k_persist<true, 0>, smem);
-        k_persist<true, 0><<<grid, Cfg<true>::NT, smem, st>>>(g);
+        set_smem(k_persist<true, false>, smem);
+        k_persist<true, false><<<grid, Cfg<true>::NT, smem, st>>>(g);
     } else {
         // deterministic two-limb scatter (KBG_OPT_DETERMINISTIC) x point-exact FP64 path for sparse
         // tasks (KBG_OPT_SPARSE_DFMA): separate instantiations, so the default kernel carries neither
@@ -454,17 +454,11 @@ int launch_persist(const GridArgs& g0, bool density, cudaStream_t st) {
             set_smem(kernel, smem);
             kernel<<<grid, Cfg<false>::NT, smem, st>>>(g);
         };
-        // DET mode (scatter bits 4..5): 0 FP64 atomics, 1 per-entry grid, 2 two limbs, 3 two limbs on |Phi|
-        const int det = (g.scatter >> 4) & 3;
-        const bool sparse = (g.scatter >> 8) != 0;
+        const bool det = g.scatter & 16, sparse = (g.scatter >> 8) != 0;
         if (sparse)
-            det == 2 ? go(k_persist<false, 2, true>) : det == 1 ? go(k_persist<false, 1, true>)
-                                                     : go(k_persist<false, 0, true>);
-        else if (det == 3)
-            go(k_persist<false, 3, false>);
+            det ? go(k_persist<false, true, true>) : go(k_persist<false, false, true>);
         else
-            det == 2 ? go(k_persist<false, 2, false>) : det == 1 ? go(k_persist<false, 1, false>)
-                                                     : go(k_persist<false, 0, false>);
+            det ? go(k_persist<false, true, false>) : go(k_persist<false, false, false>);
     }
     KBG_CUDA(cudaGetLastError());
     return 1;

@@ -2,10 +2,9 @@
 value (/root/reference/proj/include/kband/common.hpp:58-64: results "bitwise independent of the team
 size"; SPEC.md:307 topology invariance).
 
-Mode 1 rounds every H contribution to a per-entry power-of-two grid (from max|V| and the entry's bound
-T_ij = sum |phi_i| |phi_j|, computed once per geometry) and mode 2 splits it into two limbs on global
-grids; either way every FP64 atomic addition is exact (kb_gridcore.cuh h_scatter), so the order in which
-blocks, tasks and kernels arrive cannot change a bit. The tests check that on the product path and
+Every H contribution is split into two limbs on fixed power-of-two grids derived from max|V| and added
+with exact FP64 atomics (kb_gridcore.cuh h_scatter), so the order in which blocks, tasks and kernels
+arrive cannot change a bit. The tests check that on the product path and
 through properties only an order-independent accumulation has: the one-CTA-per-block kernels and the
 persistent kernels (with every intra-block schedule) give the SAME bits, and scaling V by 2^k scales H
 by exactly 2^k.
@@ -21,7 +20,7 @@ from paper_1402_4247_b200.system import Fe3O4
 pytestmark = pytest.mark.gpu
 
 
-MODES = (1, 2)
+MODES = (1,)
 
 
 def det_pass(system, mode=1, **kw):
@@ -131,7 +130,7 @@ def test_zero_potential_gives_exact_zero(mode):
     assert not np.any(c.gp.hamiltonian(np.zeros_like(c.veff), c.f.dV))
 
 
-@pytest.mark.parametrize("det", [1, 2, 0])
+@pytest.mark.parametrize("det", [1, 0])
 @pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
 def test_nonfinite_potential_raises(bad, det):
     """kband raises ConvergenceError on non-finite values (householder.cpp:119-123): every V value is
@@ -154,8 +153,8 @@ def test_nonfinite_potential_raises(bad, det):
 
 
 @pytest.mark.parametrize("name,nspin", [("cubic56_200Ry", 1), ("cubic56_200Ry", 2), ("sweep56_400Ry", 1)])
-def test_mode1_oracle_parity(name, nspin):
-    """The per-entry-grid mode keeps the parity bar of tests/test_gpu_parity.py against the oracle."""
+def test_deterministic_oracle_parity(name, nspin):
+    """The deterministic accumulation keeps the parity bar of tests/test_gpu_parity.py against the oracle."""
     from oracle.oracle import Oracle
 
     from test_gpu_parity import assert_parity

@@ -5,4 +5,8 @@ timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_ou
 timeout 300 python tools/kernel_times.py --schedules 3 --fallback 0 > gpurun_out/kernel_times_$tag.log 2>&1
 timeout 300 python tools/kernel_times.py --schedules 3 --fallback 0 --det 1 --kernels h_accumulate >> gpurun_out/kernel_times_$tag.log 2>&1
 timeout 300 python tools/kernel_times.py --schedules 3 --fallback 0 --config super448_200Ry >> gpurun_out/kernel_times_$tag.log 2>&1
-tail -n 3 gpurun_out/pytest_gpu_$tag.log; grep -o '"config": "[a-z0-9_]*".*"det": [01], "sparse": [0-9]*, "kernel": "[a-z_]*".*"median_ms": [0-9.]*' gpurun_out/kernel_times_$tag.log | sed 's/"lib".*"det"/"det"/; s/"plan".*"median/median/'
+tail -n 3 gpurun_out/pytest_gpu_$tag.log; python3 -c "
+import json
+for l in open('gpurun_out/kernel_times_$tag.log'):
+    if l.startswith('{'):
+        d=json.loads(l); print(d['config'], d['det'], d['kernel'], d['median_ms'])"

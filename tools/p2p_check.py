@@ -25,8 +25,8 @@ from paper_1402_4247_b200.grid import GridPass  # noqa: E402
 from paper_1402_4247_b200.system import Fe3O4  # noqa: E402
 
 
-def main(cfg="cubic56_200Ry", mode="1"):
-    mode = int(mode)  # KBG_OPT_DETERMINISTIC mode of the bitwise checks (1 per-entry grid, 2 two limbs)
+def main(cfg="cubic56_200Ry"):
+    mode = 1  # KBG_OPT_DETERMINISTIC for the bitwise checks
     world, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -170,7 +170,7 @@ def main(cfg="cubic56_200Ry", mode="1"):
         h_norm, h_elem, h_small = errs(h_np, h_or)
         r_norm, r_elem, r_small = errs(rho_sum, rho_or)
         det = bool(repeat and bitwise_single)
-        print(json.dumps({"config": cfg, "world": world, "det_mode": mode, "same_bits_all_ranks": same_bits, "repeatable": repeat,
+        print(json.dumps({"config": cfg, "world": world, "same_bits_all_ranks": same_bits, "repeatable": repeat,
                           "bitwise_equal_single_gpu": bitwise_single, "split_api_same_bits": split_same,
                           "rel_diff_vs_nccl": d_nccl, "rel_diff_vs_single_gpu": d_full,
                           "oracle_h_normwise": h_norm, "oracle_h_elementwise": h_elem,
