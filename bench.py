@@ -4,14 +4,17 @@
 Metric (BASELINE.json): ms per SCF-iteration grid pass (rho + H_ij) on
 synthetic Fe3O4, plus the FP64 roofline fraction of the dominant kernel.
 A "step" = one density pass (DM -> rho) + one Hamiltonian pass (V_eff -> H,
-incl. the mirror and, for N > 1, the NCCL allreduce of H) over the whole
+incl. the mirror and, for N > 1, the cross-rank reduction of H) over the whole
 grid. Default workload: the 56-atom conventional cell at 200 Ry (configs[1]).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl ours|reference]
 
-N > 1: launched by torch.distributed.run; the grid is split into contiguous
-cost-balanced block ranges (strong scaling); H partials are summed with
-torch.distributed.all_reduce (NCCL); time = max over ranks.
+N > 1: `--gpus N` re-launches itself under torch.distributed.run (N ranks, 127.0.0.1); the grid is
+split into contiguous cost-balanced block ranges (strong scaling); H partials are reduced and mirrored
+by the library's peer-memory exchange kernel (kb_comm.cu; `--collective nccl`: torch.distributed
+all_reduce instead); time = max over ranks.
+Diagnostics: BENCH_STEP_LOG=1 prints every timed step's segments to stderr; BENCH_NO_CLOCKS=1 skips
+the nvidia-smi sampler.
 """
 from __future__ import annotations
 
@@ -90,8 +93,9 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, enabled: bool = True):
         self.index = index
+        self.enabled = enabled
         self.rows = []
         self._stop = threading.Event()
         self._t = None
@@ -108,8 +112,9 @@ class ClockSampler:
             self._stop.wait(0.2)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        if self.enabled:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
         return self
 
     def __exit__(self, *a):
@@ -336,7 +341,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with ClockSampler(local, enabled=not os.environ.get("BENCH_NO_CLOCKS")) as clk:
         for k in range(args.steps):
             flush.zero_()  # L2 flush between timed iterations (outside the events)
             launches += step(evs[k])
@@ -358,6 +363,8 @@ def main():
         t = [e[i].elapsed_time(e[i + 1]) for i in range(4)]
         seg += np.array(t)
         tot.append(sum(t))
+        if os.environ.get("BENCH_STEP_LOG"):
+            print("step segments ms", [round(x, 4) for x in t], file=sys.stderr)
     ms_local = float(np.mean(tot))
     seg /= args.steps
     if world > 1:

@@ -33,6 +33,18 @@
 #define KBG_L2_HINT 1
 #endif
 
+// H tiles: 1 = permuted B-fragment column order (hcol_of_n): the scatter's RED instructions touch half
+// the L2 sectors, which removes the H pass's dependence on where the output buffer lies in memory
+// (56 atoms: 0.321-0.382 ms over 21 buffer placements -> 0.3185-0.3205; deterministic 0.539 -> 0.429)
+#ifndef KBG_H_PERMCOL
+#define KBG_H_PERMCOL 1
+#endif
+// rho D' gather: 1 = predicated loads (no per-lane branch around rows without a pair to the partner;
+// the density pass 0.352 -> 0.343 ms at 56 atoms and no register spills), 0 = branch + zero fill.
+#ifndef KBG_RHO_PGATHER
+#define KBG_RHO_PGATHER 1
+#endif
+
 namespace kbg {
 namespace core {
 
@@ -391,6 +403,15 @@ __device__ __forceinline__ HScale hscale_of(unsigned long long vbits, double wfa
     return h;
 }
 
+// Column of cj (within an 8-column tile) behind DMMA column n of the H tiles. With KBG_H_PERMCOL the
+// B fragments load orbital rows in the order 0 6 1 7 2 4 3 5, so a RED instruction (fixed e of the C
+// fragment's column pair 2q + e) covers 4 contiguous columns of every row -- half the L2 sectors of the
+// identity order's alternate columns -- and the 4 rows of a half-warp's B loads keep distinct row & 3
+// (conflict-free under the Phi swizzle).
+__device__ __forceinline__ int hcol_of_n(int n) {
+    return KBG_H_PERMCOL ? ((n & 1) ? 4 + ((n >> 1) ^ 2) : (n >> 1)) : n;
+}
+
 // Scatter of one accumulated tile: rows ra0 + [0, 8*TM) (group rows < rend),
 // columns cb0 + [0, 8*TN) of cover cj; canonical rows (cover ci <= cj) only.
 template <bool DET, int TM, int TN>
@@ -410,7 +431,7 @@ __device__ __forceinline__ void h_scatter(const Smem& sm, const double (&c)[TM][
         for (int j = 0; j < TN; ++j)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const int col = cb0 + 8 * j + (lane & 3) * 2 + e;
+                const int col = cb0 + 8 * j + hcol_of_n((lane & 3) * 2 + e);
                 if (off >= 0 && col < nb && !(KBG_EXPERIMENTS && (scatter & 2))) {
                     const double v = c[i][j][e];  // the fault hook's sign is folded into w
                     if (DET) {
@@ -444,7 +465,7 @@ __device__ __forceinline__ void h_tile(const Smem& sm, const double* __restrict_
 #pragma unroll
             for (int j = 0; j < TN; ++j) c[u][i][j][0] = c[u][i][j][1] = 0.0;
     const CoverS& B = sm.cov()[cj];
-    const int ra = ra0 + (lane >> 2), rb = B.row0 + cb0 + (lane >> 2);
+    const int ra = ra0 + (lane >> 2), rb = B.row0 + cb0 + hcol_of_n(lane >> 2);
     const double* pa = sm.phi() + ra * 64 + (lane & 3);
     const double* pb = sm.phi() + rb * 64 + (lane & 3);
     const int sa = swz(ra), sb = swz(rb);  // 8-row steps keep row & 3
@@ -500,7 +521,7 @@ __device__ __forceinline__ void h_tile2(const Smem& sm, const double* __restrict
         for (int j = 0; j < TN2; ++j) c2[i][j][0] = c2[i][j][1] = 0.0;
     }
     const int ra = ra0 + (lane >> 2);
-    const int rb1 = sm.cov()[cj1].row0 + (lane >> 2), rb2 = sm.cov()[cj2].row0 + (lane >> 2);
+    const int rb1 = sm.cov()[cj1].row0 + hcol_of_n(lane >> 2), rb2 = sm.cov()[cj2].row0 + hcol_of_n(lane >> 2);
     const double* pa = sm.phi() + ra * 64 + (lane & 3);
     const double* pb1 = sm.phi() + rb1 * 64 + (lane & 3);
     const double* pb2 = sm.phi() + rb2 * 64 + (lane & 3);
@@ -682,6 +703,17 @@ __device__ __forceinline__ void gather_a(const Smem& sm, int ncov, const int (&r
     for (int t = 0; t < TM; ++t) {
         const int ci = rci[t];
         const int off = ci <= cj ? sm.off2d()[ci * ncov + cj] : -1;  // ci = kNoCover (255) fails ci <= cj
+#if KBG_RHO_PGATHER
+        // predicated loads (no divergent branch: rows without a pair to cj differ per lane)
+        const uint32_t e = static_cast<uint32_t>(off) + static_cast<uint32_t>(rri[t] * stride + 16 * kc) +
+                           4u * static_cast<uint32_t>(lane & 3);
+        const double* p = Dr + e;
+        asm("{\n\t.reg .pred q;\n\tsetp.ge.s32 q, %4, 0;\n\t"
+            "mov.b64 %0, 0;\n\tmov.b64 %1, 0;\n\tmov.b64 %2, 0;\n\tmov.b64 %3, 0;\n\t"
+            "@q ld.global.nc.v2.f64 {%0, %1}, [%5];\n\t@q ld.global.nc.v2.f64 {%2, %3}, [%5+16];\n\t}"
+            : "=d"(a[t][0]), "=d"(a[t][1]), "=d"(a[t][2]), "=d"(a[t][3])
+            : "r"(off), "l"(p));
+#else
         if (off >= 0) {
             // 32-bit element offset (one IMAD.WIDE for the address instead of a 64-bit add chain)
             const uint32_t e = static_cast<uint32_t>(off) + static_cast<uint32_t>(rri[t] * stride + 16 * kc) +
@@ -701,6 +733,7 @@ __device__ __forceinline__ void gather_a(const Smem& sm, int ncov, const int (&r
         } else {
             a[t][0] = a[t][1] = a[t][2] = a[t][3] = 0.0;
         }
+#endif
     }
 }
 

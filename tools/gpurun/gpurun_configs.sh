@@ -11,6 +11,6 @@ done
 python -c "
 import json
 for l in open('$out'):
-    d = json.loads(l); c = d['config']
-    print(c['workload'], c['grid'], d['value'], 'ms', c['achieved_pass_tflops'], 'TF', d['segments_ms'], d['roofline']['frac'], d['e2e'] and d['e2e']['value'])
+    d = json.loads(l); c = d['config']; r = d.get('run', c)
+    print(c['workload'], c['grid'], d['value'], 'ms', r['achieved_pass_tflops'], 'TF', d['segments_ms'], d['roofline']['frac'], d['e2e'] and d['e2e']['value'])
 "

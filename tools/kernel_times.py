@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--det", type=int, default=0, help="KBG_OPT_DETERMINISTIC (1: two-limb exact scatter)")
     ap.add_argument("--kernels", default="density,h_accumulate")
     ap.add_argument("--sparse", type=int, default=0, help="KBG_OPT_SPARSE_DFMA threshold (A5 switch)")
+    ap.add_argument("--rebuild", type=int, default=0, help="extra build_index calls (bench.py builds twice)")
     a = ap.parse_args()
     f = Fe3O4.config(a.config)
     dev = torch.device("cuda", 0)
@@ -60,6 +61,8 @@ def main():
         gp.set_option(_abi.KBG_OPT_SCHEDULE, sched)
         gp.set_option(_abi.KBG_OPT_BLOCK_ORDER, order)
         ix = gp.build_index()
+        for _ in range(a.rebuild):
+            ix = gp.build_index()
         gp.set_option(_abi.KBG_OPT_PERSIST, persist)
         plan = gp.plan_info()
         gp.set_option(_abi.KBG_OPT_SCATTER_STORE, a.scatter)
@@ -95,6 +98,29 @@ def main():
             else:
                 ref[name] = r1
             print(json.dumps(rec), flush=True)
+        if "pass" in a.kernels.split(","):
+            # density then H back to back on one stream, as in bench.py's step (and H then density):
+            # per-kernel medians inside the pass
+            for order in (("density", "h_accumulate"), ("h_accumulate", "density")):
+                fns = {"density": lambda: gp.density_dev(d_dm, rho, st),
+                       "h_accumulate": lambda: gp.hamiltonian_accumulate_dev(d_v, f.dV, h, st)}
+                ts = {k: [] for k in order}
+                for rep in range(a.reps + 3):
+                    flush.zero_()
+                    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+                    ev[0].record(st)
+                    fns[order[0]]()
+                    ev[1].record(st)
+                    fns[order[1]]()
+                    ev[2].record(st)
+                    ev[2].synchronize()
+                    if rep >= 3:
+                        ts[order[0]].append(ev[0].elapsed_time(ev[1]))
+                        ts[order[1]].append(ev[1].elapsed_time(ev[2]))
+                print(json.dumps({"config": a.config, "lib": os.environ.get("KBG_LIBKBGRID", "default"),
+                                  "pass_order": list(order), "det": a.det,
+                                  **{k + "_median_ms": round(float(np.median(v)), 4) for k, v in ts.items()},
+                                  **{k + "_mean_ms": round(float(np.mean(v)), 4) for k, v in ts.items()}}), flush=True)
         del gp
 
 
