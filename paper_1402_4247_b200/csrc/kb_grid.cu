@@ -191,6 +191,70 @@ __global__ void k_mirror(SysParams P, int64_t npair, int nspin, int64_t nnz, con
     }
 }
 
+// Mirror over the work list (one warp per item, kb_index.cu k_mirror_items): blocks of <= 16 x 16
+// orbitals as two rows per pass, lane = (row parity, column), all loads of an item issued up front;
+// the same expressions as k_mirror (bitwise identical result).
+__global__ void __launch_bounds__(256) k_mirror_list(const MirrorItem* __restrict__ items,
+                                                     const int* __restrict__ count, int nspin, int64_t nnz,
+                                                     double* h) {
+    const int lane = threadIdx.x & 31;
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (w >= *count) return;
+    const MirrorItem it = items[w];
+    const int na = it.na, nb = it.nb;
+    const int j = lane & 15, i0 = lane >> 4;
+    for (int s = 0; s < nspin; ++s) {
+        double* x = h + s * nnz;
+        if (it.dst == it.src) {  // (a, a, 0): (H + H^T) / 2 on i < j
+            if (na <= 16) {
+                double u[8], v[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int i = i0 + 2 * k;
+                    const bool on = i < j && j < na;
+                    u[k] = on ? x[it.dst + i * na + j] : 0.0;
+                    v[k] = on ? x[it.dst + j * na + i] : 0.0;
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int i = i0 + 2 * k;
+                    if (i < j && j < na) {
+                        const double m = 0.5 * (u[k] + v[k]);
+                        x[it.dst + i * na + j] = m;
+                        x[it.dst + j * na + i] = m;
+                    }
+                }
+            } else {
+                for (int e = lane; e < na * na; e += 32) {
+                    const int i = e / na, jj = e % na;
+                    if (i < jj) {
+                        const double m = 0.5 * (x[it.dst + i * na + jj] + x[it.dst + jj * na + i]);
+                        x[it.dst + i * na + jj] = m;
+                        x[it.dst + jj * na + i] = m;
+                    }
+                }
+            }
+        } else if (na <= 16 && nb <= 16) {  // dst(i, j) = src(j, i)
+            double u[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int i = i0 + 2 * k;
+                u[k] = (i < na && j < nb) ? x[it.src + j * na + i] : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int i = i0 + 2 * k;
+                if (i < na && j < nb) x[it.dst + i * nb + j] = u[k];
+            }
+        } else {
+            for (int e = lane; e < na * nb; e += 32) {
+                const int i = e / nb, jj = e % nb;
+                x[it.dst + e] = x[it.src + jj * na + i];
+            }
+        }
+    }
+}
+
 // ---- deterministic H: max|V| and the final rounding (kb_gridcore.cuh h_scatter) ---
 // max|x| over n doubles as the bit pattern of |x| (sign cleared): non-negative
 // doubles order like their bits, and NaN > inf > finite, so a non-finite input
@@ -380,6 +444,12 @@ int launch_hamiltonian(const GridArgs& g0, int64_t nblk, int nwarps, cudaStream_
 
 int launch_mirror(const DevIndex& ix, const SysParams& sys, int nspin, double* h, cudaStream_t st) {
     if (ix.npair == 0) return 0;
+    if (ix.mir && ix.nmir > 0) {
+        const unsigned grid = static_cast<unsigned>((ix.nmir * 32 + 255) / 256);
+        k_mirror_list<<<grid, 256, 0, st>>>(ix.mir, ix.mir_count, nspin, ix.nnz, h);
+        KBG_CUDA(cudaGetLastError());
+        return 1;
+    }
     const unsigned grid = static_cast<unsigned>((ix.npair * 32 + 255) / 256);
     k_mirror<<<grid, 256, 0, st>>>(sys, ix.npair, nspin, ix.nnz, ix.pair_a, ix.pair_b, ix.pair_R, ix.pair_off,
                                    ix.pair_mirror, h);

@@ -247,6 +247,22 @@ __global__ void k_pair_mirror(SysParams P, int64_t npair, const int32_t* pa, con
     if (q < 0) atomicCAS(err, 0, 1);
 }
 
+// Mirror work list: non-canonical pairs (dst) with their canonical mirror (src), and the (a, a, 0) pairs.
+__global__ void k_mirror_items(SysParams P, int64_t npair, const int32_t* pa, const int32_t* pb, const int32_t* pR,
+                               const int64_t* poff, const int32_t* mirror, MirrorItem* items, int* count) {
+    const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (p >= npair) return;
+    const int64_t q = mirror[p];
+    const int a = pa[p], b = pb[p];
+    if (q != p && canonical_dev(a, b, pR[3 * p], pR[3 * p + 1], pR[3 * p + 2])) return;
+    MirrorItem it;
+    it.dst = poff[p];
+    it.src = poff[q];
+    it.na = P.sp[P.spc[a]].norb;
+    it.nb = P.sp[P.spc[b]].norb;
+    items[atomicAdd(count, 1)] = it;  // item order is free: every item writes its own block
+}
+
 // ---- block work items -------------------------------------------------------
 struct Stats {
     unsigned long long sum_m, sum_m2, natompt;
@@ -397,6 +413,8 @@ void free_index(DevIndex& ix) {
     dfree(ix.pair_roff);
     dfree(ix.order);
     dfree(ix.pair_mirror);
+    dfree(ix.mir);
+    dfree(ix.mir_count);
     dfree(ix.bp_ptr);
     dfree(ix.bp);
     dfree(ix.blk_cost);
@@ -508,6 +526,13 @@ void build_index_device(const SysParams& P, DevIndex& ix, cudaStream_t st) {
     KBG_CUDA(cudaMemsetAsync(psize, 0, (ix.npair + 1) * sizeof(int64_t), st));
     if (ix.npair) k_pair_rsize<<<grid_of(ix.npair, T), T, 0, st>>>(P, ix.npair, ix.pair_a, ix.pair_b, ix.pair_R, psize);
     KBG_CUDA(cudaGetLastError());
+    ix.mir = dalloc<MirrorItem>(std::max<int64_t>(1, ix.npair));
+    ix.mir_count = dalloc<int>(1);
+    KBG_CUDA(cudaMemsetAsync(ix.mir_count, 0, sizeof(int), st));
+    if (ix.npair)
+        k_mirror_items<<<grid_of(ix.npair, T), T, 0, st>>>(P, ix.npair, ix.pair_a, ix.pair_b, ix.pair_R, ix.pair_off,
+                                                           ix.pair_mirror, ix.mir, ix.mir_count);
+    KBG_CUDA(cudaGetLastError());
     ix.pair_roff = dalloc<int64_t>(ix.npair + 1);
     ix.nrep = exclusive_scan(psize, ix.pair_roff, ix.npair, st);
     if (ix.nrep >= (int64_t(1) << 31)) throw Error(KBG_ERR_DIMENSION, "build_index: repacked density matrix too large");
@@ -536,7 +561,9 @@ void build_index_device(const SysParams& P, DevIndex& ix, cudaStream_t st) {
                                    ix.pair_off, ix.pair_roff, ix.npair, ix.bp, d_err);
     KBG_CUDA(cudaGetLastError());
     Stats hs;
+    int hmir = 0;
     KBG_CUDA(cudaMemcpyAsync(&hs, d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, st));
+    KBG_CUDA(cudaMemcpyAsync(&hmir, ix.mir_count, sizeof(int), cudaMemcpyDeviceToHost, st));
     KBG_CUDA(cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
     KBG_CUDA(cudaStreamSynchronize(st));
     pool_free(d_stats);
@@ -544,6 +571,7 @@ void build_index_device(const SysParams& P, DevIndex& ix, cudaStream_t st) {
     if (herr)
         throw Error(KBG_ERR_CONSISTENCY, "build_index: block " + std::to_string(herr - 1) +
                                              " has covers that share points but form no pair");
+    ix.nmir = hmir;
     ix.sum_m = static_cast<double>(hs.sum_m);
     ix.sum_m2 = static_cast<double>(hs.sum_m2);
     ix.natompt = static_cast<int64_t>(hs.natompt);

@@ -104,6 +104,11 @@ struct Candidate {
 };
 
 // Device-resident index.
+struct MirrorItem {
+    int64_t dst, src;  // pair-block offsets in H (dst = src: an (a, a, 0) block)
+    int32_t na, nb;    // dst block is na x nb (src nb x na)
+};
+
 struct DevIndex {
     int64_t nblock = 0, ncover = 0, npair = 0, nnz = 0, nbpair = 0;
     int32_t* blk_ptr = nullptr;
@@ -118,6 +123,11 @@ struct DevIndex {
     int64_t* pair_roff = nullptr;  // [npair+1] repacked-DM offsets (canonical pairs only)
     int64_t nrep = 0;              // repacked DM doubles per spin
     int32_t* pair_mirror = nullptr;
+    // mirror work list (k_mirror): one item per non-canonical pair (filled from its canonical
+    // mirror) and per (a, a, 0) pair (re-symmetrised); nmir items, count also at mir_count[0]
+    MirrorItem* mir = nullptr;
+    int* mir_count = nullptr;
+    int64_t nmir = 0;
     int64_t* bp_ptr = nullptr;
     BPair* bp = nullptr;
     int64_t* blk_cost = nullptr;
