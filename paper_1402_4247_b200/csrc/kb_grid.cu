@@ -151,6 +151,98 @@ __global__ void k_dm_repack(SysParams P, int64_t npair, int nspin, int64_t nnz, 
     }
 }
 
+#ifndef KBG_REPACK_LIST
+#define KBG_REPACK_LIST 1
+#endif
+// The same repack over the canonical-pair work list (kb_index.cu k_repack_items): one warp per
+// item, metadata in one load; for nb <= 16 (one 16-column chunk) lane l always handles repacked
+// column l & 15 and rows (l >> 4) + 2k, all loads of an item issued up front.
+template <bool CHK>
+__global__ void __launch_bounds__(256) k_dm_repack_list(const RepackItem* __restrict__ items,
+                                                        const int* __restrict__ count, int nspin, int64_t nnz,
+                                                        int64_t nrep, const double* __restrict__ dm,
+                                                        double* __restrict__ dmr, unsigned long long* chk,
+                                                        const uint8_t* __restrict__ own) {
+    const int lane = threadIdx.x & 31;
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    double dmax = 0.0, amax = 0.0;
+    bool finite = true;
+    if (w < *count) {
+        const RepackItem it = items[w];
+        if (!own || own[it.p]) {
+            const double fac = it.fac2 ? 2.0 : 1.0;
+            const int na = it.na, nb = it.nb;
+            for (int s = 0; s < nspin; ++s) {
+                const double* src = dm + s * nnz + it.src;
+                const double* srq = dm + s * nnz + it.srq;  // nb x na
+                double* dst = dmr + s * nrep + it.dst;
+                if (nb <= 16 && na <= 16) {
+                    const int pos = lane & 15, i0 = lane >> 4;
+                    const int j = 4 * (pos & 3) + ((pos >> 2) & 3);  // column stored at pos
+                    double v[8], y[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const int i = i0 + 2 * k;
+                        v[k] = (i < na && j < nb) ? src[i * nb + j] : 0.0;
+                        y[k] = (CHK && i < na && j < nb) ? srq[j * na + i] : 0.0;
+                    }
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const int i = i0 + 2 * k;
+                        if (i < na) dst[i * 16 + pos] = fac * v[k];
+                        if (CHK && i < na && j < nb) {
+                            finite &= isfinite(v[k]) && isfinite(y[k]);
+                            dmax = fmax(dmax, fabs(v[k] - y[k]));
+                            amax = fmax(amax, fmax(fabs(v[k]), fabs(y[k])));
+                        }
+                    }
+                } else {
+                    const int stride = 16 * ((nb + 15) >> 4);
+                    for (int e = lane; e < na * stride; e += 32) {
+                        const int i = e / stride, pos = e % stride;
+                        const int c = pos >> 4, k = (pos >> 2) & 3, st = pos & 3;
+                        const int j = 16 * c + 4 * st + k;
+                        const double v = j < nb ? src[i * nb + j] : 0.0;
+                        dst[e] = fac * v;
+                        if (CHK && j < nb) {
+                            const double y = srq[j * na + i];
+                            finite &= isfinite(v) && isfinite(y);
+                            dmax = fmax(dmax, fabs(v - y));
+                            amax = fmax(amax, fmax(fabs(v), fabs(y)));
+                        }
+                    }
+                }
+            }
+        }
+    }
+    if (!CHK) return;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+        amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    }
+    finite = __all_sync(0xffffffffu, finite);
+    __shared__ double s_d[8], s_a[8];
+    __shared__ int s_f;
+    if (threadIdx.x == 0) s_f = 1;
+    __syncthreads();
+    if (lane == 0) {
+        s_d[threadIdx.x >> 5] = dmax;
+        s_a[threadIdx.x >> 5] = amax;
+        if (!finite) s_f = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < 8; ++k) {
+            dmax = fmax(dmax, s_d[k]);
+            amax = fmax(amax, s_a[k]);
+        }
+        atomicMax(chk, static_cast<unsigned long long>(__double_as_longlong(dmax)));
+        atomicMax(chk + 1, static_cast<unsigned long long>(__double_as_longlong(amax)));
+        if (!s_f) atomicMax(chk + 2, 1ull);
+    }
+}
+
 // ---- mirror: H_ba(-R) = H_ab(R)^T ------------------------------------------------
 __global__ void k_mirror(SysParams P, int64_t npair, int nspin, int64_t nnz, const int32_t* __restrict__ pa,
                          const int32_t* __restrict__ pb, const int32_t* __restrict__ pR,
@@ -478,6 +570,17 @@ int launch_finalize(const DevIndex& ix, const SysParams& sys, int nspin, const d
 int launch_dm_repack(const DevIndex& ix, const SysParams& sys, int nspin, const double* dm, double* dmr,
                      cudaStream_t st, unsigned long long* chk, const uint8_t* own) {
     if (ix.npair == 0) return 0;
+    if (KBG_REPACK_LIST && ix.rep && ix.nrep_items > 0) {
+        const unsigned g = static_cast<unsigned>((ix.nrep_items * 32 + 255) / 256);
+        if (chk)
+            k_dm_repack_list<true><<<g, 256, 0, st>>>(ix.rep, ix.mir_count + 1, nspin, ix.nnz, ix.nrep, dm, dmr, chk,
+                                                      own);
+        else
+            k_dm_repack_list<false><<<g, 256, 0, st>>>(ix.rep, ix.mir_count + 1, nspin, ix.nnz, ix.nrep, dm, dmr,
+                                                       chk, own);
+        KBG_CUDA(cudaGetLastError());
+        return 1;
+    }
     const unsigned grid = static_cast<unsigned>((ix.npair * 32 + 255) / 256);
     k_dm_repack<<<grid, 256, 0, st>>>(sys, ix.npair, nspin, ix.nnz, ix.nrep, ix.pair_a, ix.pair_b, ix.pair_R,
                                       ix.pair_off, ix.pair_roff, ix.pair_mirror, dm, dmr, chk, own);

@@ -263,6 +263,26 @@ __global__ void k_mirror_items(SysParams P, int64_t npair, const int32_t* pa, co
     items[atomicAdd(count, 1)] = it;  // item order is free: every item writes its own block
 }
 
+// DM repack work list: one item per canonical pair (order free: every item writes its own block).
+__global__ void k_repack_items(SysParams P, int64_t npair, const int32_t* pa, const int32_t* pb, const int32_t* pR,
+                               const int64_t* poff, const int64_t* proff, const int32_t* mirror, RepackItem* items,
+                               int* count) {
+    const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (p >= npair) return;
+    const int a = pa[p], b = pb[p];
+    const int R0 = pR[3 * p], R1 = pR[3 * p + 1], R2 = pR[3 * p + 2];
+    if (!canonical_dev(a, b, R0, R1, R2)) return;
+    RepackItem it;
+    it.p = static_cast<int32_t>(p);
+    it.src = poff[p];
+    it.dst = proff[p];
+    it.srq = poff[mirror[p]];
+    it.na = P.sp[P.spc[a]].norb;
+    it.nb = P.sp[P.spc[b]].norb;
+    it.fac2 = !(a == b && R0 == 0 && R1 == 0 && R2 == 0);
+    items[atomicAdd(count, 1)] = it;
+}
+
 // ---- block work items -------------------------------------------------------
 struct Stats {
     unsigned long long sum_m, sum_m2, natompt;
@@ -414,6 +434,7 @@ void free_index(DevIndex& ix) {
     dfree(ix.order);
     dfree(ix.pair_mirror);
     dfree(ix.mir);
+    dfree(ix.rep);
     dfree(ix.mir_count);
     dfree(ix.bp_ptr);
     dfree(ix.bp);
@@ -527,8 +548,8 @@ void build_index_device(const SysParams& P, DevIndex& ix, cudaStream_t st) {
     if (ix.npair) k_pair_rsize<<<grid_of(ix.npair, T), T, 0, st>>>(P, ix.npair, ix.pair_a, ix.pair_b, ix.pair_R, psize);
     KBG_CUDA(cudaGetLastError());
     ix.mir = dalloc<MirrorItem>(std::max<int64_t>(1, ix.npair));
-    ix.mir_count = dalloc<int>(1);
-    KBG_CUDA(cudaMemsetAsync(ix.mir_count, 0, sizeof(int), st));
+    ix.mir_count = dalloc<int>(2);  // [0] mirror items, [1] repack items
+    KBG_CUDA(cudaMemsetAsync(ix.mir_count, 0, 2 * sizeof(int), st));
     if (ix.npair)
         k_mirror_items<<<grid_of(ix.npair, T), T, 0, st>>>(P, ix.npair, ix.pair_a, ix.pair_b, ix.pair_R, ix.pair_off,
                                                            ix.pair_mirror, ix.mir, ix.mir_count);
@@ -536,6 +557,11 @@ void build_index_device(const SysParams& P, DevIndex& ix, cudaStream_t st) {
     ix.pair_roff = dalloc<int64_t>(ix.npair + 1);
     ix.nrep = exclusive_scan(psize, ix.pair_roff, ix.npair, st);
     if (ix.nrep >= (int64_t(1) << 31)) throw Error(KBG_ERR_DIMENSION, "build_index: repacked density matrix too large");
+    ix.rep = dalloc<RepackItem>(std::max<int64_t>(1, ix.npair));
+    if (ix.npair)
+        k_repack_items<<<grid_of(ix.npair, T), T, 0, st>>>(P, ix.npair, ix.pair_a, ix.pair_b, ix.pair_R, ix.pair_off,
+                                                           ix.pair_roff, ix.pair_mirror, ix.rep, ix.mir_count + 1);
+    KBG_CUDA(cudaGetLastError());
     pool_free(psize);
     int herr = 0;
     KBG_CUDA(cudaMemcpy(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost));
@@ -561,9 +587,9 @@ void build_index_device(const SysParams& P, DevIndex& ix, cudaStream_t st) {
                                    ix.pair_off, ix.pair_roff, ix.npair, ix.bp, d_err);
     KBG_CUDA(cudaGetLastError());
     Stats hs;
-    int hmir = 0;
+    int hmir[2] = {0, 0};
     KBG_CUDA(cudaMemcpyAsync(&hs, d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, st));
-    KBG_CUDA(cudaMemcpyAsync(&hmir, ix.mir_count, sizeof(int), cudaMemcpyDeviceToHost, st));
+    KBG_CUDA(cudaMemcpyAsync(hmir, ix.mir_count, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
     KBG_CUDA(cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
     KBG_CUDA(cudaStreamSynchronize(st));
     pool_free(d_stats);
@@ -571,7 +597,8 @@ void build_index_device(const SysParams& P, DevIndex& ix, cudaStream_t st) {
     if (herr)
         throw Error(KBG_ERR_CONSISTENCY, "build_index: block " + std::to_string(herr - 1) +
                                              " has covers that share points but form no pair");
-    ix.nmir = hmir;
+    ix.nmir = hmir[0];
+    ix.nrep_items = hmir[1];
     ix.sum_m = static_cast<double>(hs.sum_m);
     ix.sum_m2 = static_cast<double>(hs.sum_m2);
     ix.natompt = static_cast<int64_t>(hs.natompt);

@@ -109,6 +109,13 @@ struct MirrorItem {
     int32_t na, nb;    // dst block is na x nb (src nb x na)
 };
 
+struct RepackItem {
+    int64_t src, dst, srq;  // DM block (na x nb), its repacked block, the mirror DM block (nb x na)
+    int32_t p;              // pair index (shard ownership)
+    int32_t na, nb;         // orbitals
+    int32_t fac2;           // 1: x2 (off the (a, a, 0) blocks)
+};
+
 struct DevIndex {
     int64_t nblock = 0, ncover = 0, npair = 0, nnz = 0, nbpair = 0;
     int32_t* blk_ptr = nullptr;
@@ -123,9 +130,11 @@ struct DevIndex {
     int64_t* pair_roff = nullptr;  // [npair+1] repacked-DM offsets (canonical pairs only)
     int64_t nrep = 0;              // repacked DM doubles per spin
     int32_t* pair_mirror = nullptr;
-    // mirror work list (k_mirror): one item per non-canonical pair (filled from its canonical
+    // mirror work list (k_mirror_list): one item per non-canonical pair (filled from its canonical
     // mirror) and per (a, a, 0) pair (re-symmetrised); nmir items, count also at mir_count[0]
     MirrorItem* mir = nullptr;
+    RepackItem* rep = nullptr;  // canonical pairs (k_dm_repack_list), nrep_items of them (count at mir_count[1])
+    int64_t nrep_items = 0;
     int* mir_count = nullptr;
     int64_t nmir = 0;
     int64_t* bp_ptr = nullptr;
