@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <cstdio>
 #include <string>
 #include <vector>
 
@@ -97,6 +98,9 @@ struct kbg_ctx {
     int pending_nspin = 0;  // kbg_hamiltonian_partial_dev done, exchange pending
     uint8_t* d_pown = nullptr;      // per pair: 1 if this rank's blocks touch it (kbg_comm_open)
     std::vector<int64_t> dm_runs;   // [off, len] pairs: DM ranges (per spin) covering the pairs the repack reads
+    int64_t* d_xruns = nullptr;     // the exact [off, len] runs of the needed pair blocks (k_dm_gather)
+    int64_t dm_xruns_n = 0;
+    int64_t dm_read_copy = 0;       // doubles per spin the memcpy runs move (pageable DM)
     int64_t io[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // kbg_shard_io
 };
 
@@ -785,6 +789,17 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
         // smaller one to wait for and rho (npts) the smaller output left after the last kernel. The DM
         // check is read at the end.
         int n = 0;
+        // KBG_PHASE_TIMING=1 (diagnostic): events at the phase boundaries of both streams, printed to stderr
+        static const bool kPhase = std::getenv("KBG_PHASE_TIMING") != nullptr;
+        std::vector<std::pair<const char*, cudaEvent_t>> ph;
+        auto mark = [&](const char* what, cudaStream_t s) {
+            if (!kPhase) return;
+            cudaEvent_t e;
+            KBG_CUDA(cudaEventCreate(&e));
+            KBG_CUDA(cudaEventRecord(e, s));
+            ph.emplace_back(what, e);
+        };
+        mark("start", c->stream2);
         // Legacy H: V from pinned host memory is read in place by the H kernel (mapped_input), so the
         // first DMMAs do not wait for a whole-array copy. Deterministic H needs max|V| before the
         // first contribution: V is copied first, at the full PCIe bandwidth (the DM copy waits for
@@ -797,19 +812,32 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
         // its plane range), and H -- complete on every rank after the fused reduction -- leaves only
         // the rank's slice [io[4], io[5]) of each spin. kbg_shard_io reports the ranges.
         const bool sio = c->comm_ready && c->shard_io;
-        auto rho_half = [&] {
+        // exchange right after the H accumulate (default; KBG_XCHG_FIRST=0: after the density pass)
+        const char* xf_env = std::getenv("KBG_XCHG_FIRST");
+        const bool xfirst = !(xf_env && xf_env[0] == '0');
+        // pinned DM on a shard: its pair blocks are gathered in place (KBG_NO_DM_GATHER: memcpy runs)
+        const char* ng_env = std::getenv("KBG_NO_DM_GATHER");
+        const double* dm_map = sio && c->d_xruns && !(ng_env && ng_env[0] == '1') ? mapped_input(c, dm) : nullptr;
+        const bool dm_gathered = dm_map != nullptr;
+        auto rho_half = [&](bool after_exchange) {
             if (c->det) KBG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_pass, 0));
             // the DM crosses on the copy engine while the H kernel computes; a shard copies only the pair
             // blocks its rho reads (a few dozen copies of their merged contiguous runs)
-            if (sio && !c->dm_runs.empty())
+            mark("s1 start", c->stream);
+            if (dm_gathered) {
+                // the pair blocks were fetched in place by k_dm_gather (launched ahead of the H kernel)
+            } else if (sio && !c->dm_runs.empty())
                 dm_run_copy(c, nspin, dm);
             else
                 KBG_CUDA(cudaMemcpyAsync(c->d_in, dm, ndm * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+            mark("s1 dm copied", c->stream);
             KBG_CUDA(cudaMemsetAsync(c->d_check, 0, 4 * sizeof(unsigned long long), c->stream));
             if (c->nranks > 1 && !rho_map) KBG_CUDA(cudaMemsetAsync(c->d_out, 0, npt * sizeof(double), c->stream));
+            if (after_exchange) KBG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_rho, 0));
             // the DM symmetry check rides along in the repack pass (no separate k_dm_check)
             n += run_density(c, nspin, c->d_in, rho_map ? rho_map : c->d_out, c->stream, c->d_check,
                              sio ? c->d_pown : nullptr);
+            mark("s1 density done", c->stream);
             if (!rho_map) {
                 if (sio) {
                     const int64_t p0 = c->io[2], p1 = c->io[3];
@@ -821,6 +849,7 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
                     KBG_CUDA(cudaMemcpyAsync(rho, c->d_out, npt * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
                 }
             }
+            mark("s1 rho out", c->stream);
         };
         auto h_half = [&] {
             if (!v_map)
@@ -832,13 +861,28 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
                 // mirror over NVLink (kb_comm.cu) -- the full H on every rank. The reduce waits for this
                 // rank's density kernel (ev_rho): the rank spread and the flag round trip hide behind it,
                 // and its spinning CTAs never keep the density kernel off the SMs.
+                if (dm_gathered) n += kbg::launch_dm_gather(c->d_xruns, c->dm_xruns_n, nspin, c->ix.nnz, dm_map, c->d_in,
+                                                            c->stream);
                 n += h_accumulate(c, nspin, dV, vin, c->d_xbuf, c->stream2);
-                rho_half();
-                KBG_CUDA(cudaEventRecord(c->ev_rho, c->stream));
-                KBG_CUDA(cudaStreamWaitEvent(c->stream2, c->ev_rho, 0));
-                c->epoch += 2;
-                c->comm.ls = h_limbs(c);
-                n += kbg::launch_reduce_mirror(c->comm, c->ix, c->P, nspin, c->d_out2, c->epoch - 1, c->stream2);
+                mark("s2 h accumulated", c->stream2);
+                if (xfirst) {
+                    // exchange right after the accumulate, then the density pass (it waits for the
+                    // exchange's CTAs to leave the SMs): the H slice's D2H overlaps the density kernel
+                    c->epoch += 2;
+                    c->comm.ls = h_limbs(c);
+                    n += kbg::launch_reduce_mirror(c->comm, c->ix, c->P, nspin, c->d_out2, c->epoch - 1, c->stream2);
+                    KBG_CUDA(cudaEventRecord(c->ev_rho, c->stream2));
+                    mark("s2 exchanged", c->stream2);
+                    rho_half(true);
+                } else {
+                    rho_half(false);
+                    KBG_CUDA(cudaEventRecord(c->ev_rho, c->stream));
+                    KBG_CUDA(cudaStreamWaitEvent(c->stream2, c->ev_rho, 0));
+                    c->epoch += 2;
+                    c->comm.ls = h_limbs(c);
+                    n += kbg::launch_reduce_mirror(c->comm, c->ix, c->P, nspin, c->d_out2, c->epoch - 1, c->stream2);
+                    mark("s2 exchanged", c->stream2);
+                }
             } else {
                 double* acc = h_acc_buffer(c, nspin, c->d_out2);
                 n += h_accumulate(c, nspin, dV, vin, acc, c->stream2);
@@ -856,13 +900,24 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
             } else {
                 KBG_CUDA(cudaMemcpyAsync(h, c->d_out2, ndm * sizeof(double), cudaMemcpyDeviceToHost, c->stream2));
             }
+            mark("s2 h out", c->stream2);
         };
         h_half();
-        if (!c->comm_ready) rho_half();  // sharded: h_half runs rho_half between accumulate and reduce
+        if (!c->comm_ready) rho_half(false);  // sharded: h_half runs rho_half itself
         unsigned long long chk[4];
         KBG_CUDA(cudaMemcpyAsync(chk, c->d_check, sizeof(chk), cudaMemcpyDeviceToHost, c->stream));
         KBG_CUDA(cudaStreamSynchronize(c->stream2));
         KBG_CUDA(cudaStreamSynchronize(c->stream));
+        if (kPhase && !ph.empty()) {
+            std::string line = "kbg_grid_pass phases (us from start):";
+            for (auto& e : ph) {
+                float ms = 0.f;
+                KBG_CUDA(cudaEventElapsedTime(&ms, ph[0].second, e.second));
+                line += std::string(" [") + e.first + " " + std::to_string(static_cast<int>(ms * 1e3f)) + "]";
+            }
+            for (auto& e : ph) KBG_CUDA(cudaEventDestroy(e.second));
+            std::fprintf(stderr, "%s\n", line.c_str());
+        }
         if (c->comm_ready) comm_check(c);
         check_vbits(c, "grid_pass");
         c->last_launches = n;
@@ -1392,10 +1447,16 @@ int kbg_comm_open(kbg_ctx* c, const void* handles) {
         }
         {
             // pairs this rank's blocks touch: the DM it reads in kbg_grid_pass (shard-local input)
+            // bit 0: the rank's blocks touch pair p (its repack reads it); bit 1: the rank checks p's DM
+            // symmetry -- every pair is checked by exactly one rank, its lowest owner, which alone reads
+            // the mirror block (each mirror crosses PCIe once in total, not once per owner)
             std::vector<uint8_t> mine(std::max<int64_t>(1, c->ix.npair), 0), need(std::max<int64_t>(1, c->ix.npair), 0);
             for (int64_t p = 0; p < c->ix.npair; ++p) {
-                mine[p] = (owners[p] >> c->rank) & 1u;
-                if (mine[p]) need[p] = need[h.pair_mirror[p]] = 1;  // the block and its mirror (symmetry check)
+                const uint32_t o = owners[p];
+                if ((o >> c->rank) & 1u) mine[p] = 1;
+                if (o && __builtin_ctz(o) == c->rank) mine[p] |= 2;
+                if (mine[p]) need[p] = 1;
+                if (mine[p] & 2) need[h.pair_mirror[p]] = 1;
             }
             // contiguous runs of the needed pair blocks, then the smallest gaps merged until at most
             // kMaxDmRuns copies remain (448 atoms on 4 GPUs: 2.5 k runs, 42 % of the DM)
@@ -1410,7 +1471,16 @@ int kbg_comm_open(kbg_ctx* c, const void* handles) {
                     runs.push_back(n);
                 }
             }
-            // a copy costs the host a few us to issue: about one per 4 MB of DM, at most 48 (56 atoms:
+            // exact runs for the in-place gather (k_dm_gather, pinned DM: no bytes beyond the blocks)
+            c->dm_xruns_n = static_cast<int64_t>(runs.size() / 2);
+            if (c->d_xruns) cudaFree(c->d_xruns);
+            c->d_xruns = nullptr;
+            KBG_CUDA(cudaMalloc(&c->d_xruns, std::max<size_t>(1, runs.size()) * sizeof(int64_t)));
+            if (!runs.empty())
+                KBG_CUDA(cudaMemcpy(c->d_xruns, runs.data(), runs.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+            int64_t dm_exact = 0;
+            for (size_t r = 0; r < runs.size() / 2; ++r) dm_exact += runs[2 * r + 1];
+            // memcpy runs (pageable DM): a copy costs the host a few us to issue: about one per 4 MB of DM, at most 48 (56 atoms:
             // a single copy of the whole 3.8 MB DM; 448 atoms: 7; 1512 atoms: 24)
             const size_t kMaxDmRuns = static_cast<size_t>(
                 std::max<int64_t>(1, std::min<int64_t>(48, c->ix.nnz * 8 / (4 << 20))));
@@ -1434,6 +1504,8 @@ int kbg_comm_open(kbg_ctx* c, const void* handles) {
             c->dm_runs = runs;
             int64_t dm_read = 0;
             for (size_t r = 0; r < runs.size() / 2; ++r) dm_read += runs[2 * r + 1];
+            c->dm_read_copy = dm_read;
+            dm_read = dm_exact;  // io[6]: the pinned (gather) path; kbg_shard_io reports the copy path's if pageable
             if (c->d_pown) cudaFree(c->d_pown);
             c->d_pown = nullptr;
             KBG_CUDA(cudaMalloc(&c->d_pown, mine.size()));
@@ -1978,6 +2050,7 @@ void kbg_destroy(kbg_ctx* c) {
     if (c->d_canon) cudaFree(c->d_canon);
     if (c->d_pairtab) cudaFree(c->d_pairtab);
     if (c->d_pown) cudaFree(c->d_pown);
+    if (c->d_xruns) cudaFree(c->d_xruns);
     if (c->comm.tstamp) cudaFree(c->comm.tstamp);
     if (c->d_cpre) cudaFree(c->d_cpre);
     c->veff.release();

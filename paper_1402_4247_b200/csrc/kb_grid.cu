@@ -96,11 +96,12 @@ __global__ void k_dm_repack(SysParams P, int64_t npair, int nspin, int64_t nnz, 
         // touch are read (dm may be mapped host memory); the others are never used by its rho kernel
         if (own && !own[p]) canon = false;
     }
+    const bool chk_p = chk && (!own || (p < npair && (own[p] & 2)));
     if (canon) {
         const double fac = (a == b && R0 == 0 && R1 == 0 && R2 == 0) ? 1.0 : 2.0;
         const int na = P.sp[P.spc[a]].norb, nb = P.sp[P.spc[b]].norb;
         const int stride = 16 * ((nb + 15) >> 4);
-        const int64_t q = chk ? mirror[p] : p;
+        const int64_t q = chk_p ? mirror[p] : p;
         for (int s = 0; s < nspin; ++s) {
             const double* src = dm + s * nnz + poff[p];
             const double* srq = dm + s * nnz + poff[q];  // nb x na
@@ -114,7 +115,7 @@ __global__ void k_dm_repack(SysParams P, int64_t npair, int nspin, int64_t nnz, 
                 const int j = 16 * c + 4 * st + k;
                 const double v = j < nb ? src[i * nb + j] : 0.0;
                 dst[e] = fac * v;
-                if (chk && j < nb) {
+                if (chk_p && j < nb) {
                     const double y = srq[j * na + i];
                     finite &= isfinite(v) && isfinite(y);
                     dmax = fmax(dmax, fabs(v - y));
@@ -170,6 +171,8 @@ __global__ void __launch_bounds__(256) k_dm_repack_list(const RepackItem* __rest
     if (w < *count) {
         const RepackItem it = items[w];
         if (!own || own[it.p]) {
+            // a shard checks only the pairs it is assigned (own bit 1; it alone holds their mirror blocks)
+            const bool chk_p = CHK && (!own || (own[it.p] & 2));
             const double fac = it.fac2 ? 2.0 : 1.0;
             const int na = it.na, nb = it.nb;
             for (int s = 0; s < nspin; ++s) {
@@ -184,13 +187,13 @@ __global__ void __launch_bounds__(256) k_dm_repack_list(const RepackItem* __rest
                     for (int k = 0; k < 8; ++k) {
                         const int i = i0 + 2 * k;
                         v[k] = (i < na && j < nb) ? src[i * nb + j] : 0.0;
-                        y[k] = (CHK && i < na && j < nb) ? srq[j * na + i] : 0.0;
+                        y[k] = (chk_p && i < na && j < nb) ? srq[j * na + i] : 0.0;
                     }
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
                         const int i = i0 + 2 * k;
                         if (i < na) dst[i * 16 + pos] = fac * v[k];
-                        if (CHK && i < na && j < nb) {
+                        if (chk_p && i < na && j < nb) {
                             finite &= isfinite(v[k]) && isfinite(y[k]);
                             dmax = fmax(dmax, fabs(v[k] - y[k]));
                             amax = fmax(amax, fmax(fabs(v[k]), fabs(y[k])));
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(256) k_dm_repack_list(const RepackItem* __rest
                         const int j = 16 * c + 4 * st + k;
                         const double v = j < nb ? src[i * nb + j] : 0.0;
                         dst[e] = fac * v;
-                        if (CHK && j < nb) {
+                        if (chk_p && j < nb) {
                             const double y = srq[j * na + i];
                             finite &= isfinite(v) && isfinite(y);
                             dmax = fmax(dmax, fabs(v - y));
@@ -241,6 +244,35 @@ __global__ void __launch_bounds__(256) k_dm_repack_list(const RepackItem* __rest
         atomicMax(chk + 1, static_cast<unsigned long long>(__double_as_longlong(amax)));
         if (!s_f) atomicMax(chk + 2, 1ull);
     }
+}
+
+// Shard-local DM input (kbg_grid_pass on a sharded context, DM in pinned host memory): the exact
+// [off, len) runs of the pair blocks this rank reads, gathered in place over PCIe into the device
+// copy at the same offsets. One warp per run, 8 coalesced loads per lane in flight. Launched on 2
+// CTAs ahead of the H kernel (which leaves them their SMs): the fetch overlaps the H pass without a
+// copy per run and without the bytes between the runs.
+__global__ void __launch_bounds__(1024) k_dm_gather(const int64_t* __restrict__ runs, int64_t nruns, int nspin,
+                                                    int64_t nnz, const double* src,
+                                                    double* __restrict__ dst) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int s = 0; s < nspin; ++s)
+        for (int64_t r = warp; r < nruns; r += nw) {
+            const int64_t o = s * nnz + runs[2 * r], n = runs[2 * r + 1];
+            for (int64_t e = lane; e < n; e += 32 * 8) {
+                double v[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    v[k] = 0.0;
+                    // plain (coherent) global load: the read-only path does not serve host memory
+                    if (e + 32 * k < n) asm volatile("ld.global.f64 %0, [%1];" : "=d"(v[k]) : "l"(src + o + e + 32 * k));
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (e + 32 * k < n) dst[o + e + 32 * k] = v[k];
+            }
+        }
 }
 
 // ---- mirror: H_ba(-R) = H_ab(R)^T ------------------------------------------------
@@ -534,6 +566,15 @@ int launch_hamiltonian(const GridArgs& g0, int64_t nblk, int nwarps, cudaStream_
     return 1;
 }
 
+int launch_dm_gather(const int64_t* d_runs, int64_t nruns, int nspin, int64_t nnz, const double* src, double* dst,
+                     cudaStream_t st) {
+    if (nruns <= 0) return 0;
+    k_dm_gather<<<2, 1024, 0, st>>>(d_runs, nruns, nspin, nnz, src, dst);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw Error(KBG_ERR_CUDA, std::string("k_dm_gather: ") + cudaGetErrorString(e));
+    return 1;
+}
+
 int launch_mirror(const DevIndex& ix, const SysParams& sys, int nspin, double* h, cudaStream_t st) {
     if (ix.npair == 0) return 0;
     if (ix.mir && ix.nmir > 0) {
@@ -578,7 +619,8 @@ int launch_dm_repack(const DevIndex& ix, const SysParams& sys, int nspin, const 
         else
             k_dm_repack_list<false><<<g, 256, 0, st>>>(ix.rep, ix.mir_count + 1, nspin, ix.nnz, ix.nrep, dm, dmr,
                                                        chk, own);
-        KBG_CUDA(cudaGetLastError());
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) throw Error(KBG_ERR_CUDA, std::string("k_dm_repack_list: ") + cudaGetErrorString(e));
         return 1;
     }
     const unsigned grid = static_cast<unsigned>((ix.npair * 32 + 255) / 256);

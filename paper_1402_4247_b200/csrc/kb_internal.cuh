@@ -363,6 +363,8 @@ bool persist_fits(const GridArgs& g, bool density);
 size_t persist_smem(const GridArgs& g, bool density);
 int launch_density_persist(const GridArgs& g, cudaStream_t st);
 int launch_hamiltonian_persist(const GridArgs& g, cudaStream_t st);
+int launch_dm_gather(const int64_t* d_runs, int64_t nruns, int nspin, int64_t nnz, const double* src, double* dst,
+                     cudaStream_t st);
 int launch_mirror(const DevIndex& ix, const SysParams& sys, int nspin, double* h, cudaStream_t st);
 // Deterministic H (kb_gridcore.cuh h_scatter): max|x| as a bit pattern (atomicMax into *d_out, which the
 // caller zeroes), and H = hi + lo of the two-limb accumulator [nspin][nnz][2] (+ mirror blocks).

@@ -106,6 +106,21 @@ def main(cfg="cubic56_200Ry"):
     dist.all_reduce(rho_t)  # owned points only per rank: the sum is the full density
     ios = [None] * world
     dist.all_gather_object(ios, io)
+    # a DM that violates DM_ba(-R) = DM_ab(R)^T in one pair block: the sharded host API checks every
+    # pair on exactly one rank (its lowest owner), so exactly one rank raises KBG_ERR_CONSISTENCY
+    from paper_1402_4247_b200.errors import ConsistencyError
+
+    canon_p = [p for p in range(len(ix["pair_a"])) if ix["pair_mirror"][p] != p][0]
+    dm_bad = torch.from_numpy(dm.copy()).pin_memory().numpy()
+    dm_bad[0, int(ix["pair_off"][canon_p])] += 1e-3
+    raised = False
+    try:
+        gp.grid_pass(dm_bad, v_p, f.dV)
+    except ConsistencyError:
+        raised = True
+    asym = [None] * world
+    dist.all_gather_object(asym, raised)
+    asym_ranks = int(sum(bool(x) for x in asym))
 
     def local_ms(fn, reps=20):
         for _ in range(3):
@@ -181,9 +196,11 @@ def main(cfg="cubic56_200Ry"):
                           "h_ms_accumulate_only": round(t_acc, 4), "accumulate_ms_per_rank": acc_ranks,
                           "grid_pass_h_vs_p2p": d_gp, "grid_pass_rho_sum_vs_single_gpu": d_rho,
                           "exchange_phases_us_per_rank": phases, "shard_io": ios,
+                          "dm_asymmetry_detected_ranks": asym_ranks,
                           "note": "deterministic H (KBG_OPT_DETERMINISTIC): the sharded H must equal the "
                                   "single-GPU H bit for bit and repeat bitwise",
                           "ok": bool(same_bits and det and split_same and d_nccl <= 1e-14 and d_gp == 0.0 and d_rho == 0.0
+                                     and asym_ranks == 1
                                      and h_norm <= 1e-10 and h_elem <= 1e-10 and r_norm <= 1e-10
                                      and r_elem <= 1e-10 and h_small <= 1e-8 and r_small <= 1e-8)}), flush=True)
     dist.destroy_process_group()
