@@ -335,6 +335,8 @@ kbg::GridArgs grid_args(kbg_ctx* c, int nspin, double dV, const double* in, doub
     g.out = out;
     if (!density) {
         g.scatter |= c->sparse_thr << 8;  // A5 switch: tasks below this point density (1/255) run DFMA
+        if (KBG_EXPERIMENTS && std::getenv("KBG_DFMA_WARPS"))  // timing experiment: DFMA-only warps
+            g.scatter |= (std::atoi(std::getenv("KBG_DFMA_WARPS")) << 16) | (1 << 8);
         g.vbits = c->d_vbits;  // deterministic: max|V| (k_absmax); legacy: non-finite flag of the kernels
         if (c->det) {
             g.scatter |= 16;  // deterministic two-limb scatter (kb_gridcore.cuh h_scatter)

@@ -21,11 +21,6 @@
 
 #include "kb_device.cuh"
 
-// Timing-experiment paths (KBG_OPT_SCATTER_STORE bits, KBG_OPT_DEBUG_COUNTERS) exist only in builds
-// with -DKBG_EXPERIMENTS=1 (tools/build_variants.sh): the product kernels carry no runtime checks for them.
-#ifndef KBG_EXPERIMENTS
-#define KBG_EXPERIMENTS 0
-#endif
 
 // L2 policy of the persistent kernels: 1 streams the geometry cache with
 // evict_first; 2 also loads the repacked DM with evict_last.
@@ -637,8 +632,8 @@ __device__ __forceinline__ void h_task_dfma(const Smem& sm, const double* __rest
 
 template <bool DET, bool SPARSE = false>
 __device__ __forceinline__ void h_task(const Smem& sm, const double* w, int ncov, const Task& t, double* H,
-                                       int scatter, int lane) {
-    if (SPARSE && t.pad2_ < (scatter >> 8)) {
+                                       int scatter, int lane, bool dfma_warp = false) {
+    if (SPARSE && (dfma_warp || t.pad2_ < ((scatter >> 8) & 0xFF))) {
         h_task_dfma<DET>(sm, w, ncov, t, H, lane);
         return;
     }

@@ -30,6 +30,12 @@ __host__ __device__ __forceinline__ int64_t det_lo(int s, int64_t e, int64_t nnz
 }
 constexpr int kGroupRows = 16;  // covers are packed into row groups of <= 16 orbitals (2 DMMA row tiles)
 constexpr int kMaxTaskWarps = 32;  // task lists are LPT-balanced over <= 24 consumer warps
+// Timing-experiment paths (KBG_OPT_SCATTER_STORE bits, KBG_OPT_DEBUG_COUNTERS, KBG_DFMA_WARPS) exist only
+// in builds with -DKBG_EXPERIMENTS=1 (tools/build_variants.sh): the product kernels carry no runtime checks.
+#ifndef KBG_EXPERIMENTS
+#define KBG_EXPERIMENTS 0
+#endif
+
 constexpr int kMaxCoverPerBlock = 64;
 constexpr int kRhoOct = 4;  // octets per rho task (4: halves of the block, 2: quarters; halves measured faster)
 

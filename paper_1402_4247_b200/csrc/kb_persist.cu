@@ -314,8 +314,11 @@ __device__ void consumer(const GridArgs& g, const Buffers<DENSITY>& B, int cw, i
                     __syncwarp();
                     rho_task(sm, ncov, t, g.dmr + spin * g.nrep, res - 32 * t.half, lane);
                 } else {
+                    // timing experiment (KBG_EXPERIMENTS builds, KBG_DFMA_WARPS): the last consumer warps
+                    // run every task they pull on the FP64 FMA pipe, next to the DMMA warps
+                    const bool dfma_warp = KBG_EXPERIMENTS && SPARSE && cw >= NC - ((g.scatter >> 16) & 0xFF);
                     h_task<DET, SPARSE>(sm, sm.acc() + spin * 64, ncov, t, g.out + spin * g.nnz * (DET ? 2 : 1), g.scatter,
-                                        lane);
+                                        lane, dfma_warp);
                 }
             }
         } else

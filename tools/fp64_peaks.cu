@@ -54,6 +54,36 @@ __global__ void k_dmma(double* out, double s) {
     if (r == 12345.678) out[0] = r;
 }
 
+// DMMA and DFMA at once: even warps run DMMA chains, odd warps DFMA chains (or every warp interleaves
+// both when `both`), to see whether the two FP64 paths share one pipe.
+__global__ void k_mixed(double* out, double s, int both) {
+    const int warp = threadIdx.x >> 5;
+    double c[8][2], a[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        c[i][0] = c[i][1] = 0.0;
+        a[i] = threadIdx.x * 1e-3 + i;
+    }
+    const double x = threadIdx.x * 1e-3;
+    const bool do_mma = both || !(warp & 1), do_fma = both || (warp & 1);
+    for (int it = 0; it < kIters / 4; ++it) {
+        if (do_mma) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) dmma(c[i], x, s);
+        }
+        if (do_fma) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) a[i] = fma(a[i], s, 1e-7);
+        }
+    }
+    double r = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r += c[i][0] + c[i][1] + a[i];
+    if (r == 12345.678) out[0] = r;
+}
+
 // RED.ADD.F64 into an L2-resident array of n doubles; each warp adds 32
 // consecutive doubles (coalesced) or scattered lanes.
 __global__ void k_red(double* arr, long long n, int per_thread, int scattered) {
@@ -118,6 +148,19 @@ int main() {
     }, &cfg, 5);
     const double f_dmma4 = 512.0 * 2 * (kIters / 4) * (double)cfg.blocks * (cfg.threads / 32);
 
+    float t_mix = time_ms([](void* p) {
+        Cfg* c = (Cfg*)p;
+        k_mixed<<<c->blocks, c->threads>>>(c->out, 0.999999, 0);
+    }, &cfg, 5);
+    // half the warps: 8 DMMAs (512 FMA each) per iteration; the other half: 32 DFMAs per lane
+    const double f_mix = (double)cfg.blocks * (cfg.threads / 64) * (kIters / 4) *
+                         (8 * 512.0 * 2 + 32 * 32 * 2.0);
+    float t_both = time_ms([](void* p) {
+        Cfg* c = (Cfg*)p;
+        k_mixed<<<c->blocks, c->threads>>>(c->out, 0.999999, 1);
+    }, &cfg, 5);
+    const double f_both = (double)cfg.blocks * (cfg.threads / 32) * (kIters / 4) * (8 * 512.0 * 2 + 32 * 32 * 2.0);
+
     Cfg rc{out, sms * 16, 256, (4ll << 20) / 8, 64, 0};
     float t_red = time_ms([](void* p) {
         Cfg* c = (Cfg*)p;
@@ -132,8 +175,9 @@ int main() {
 
     std::printf(
         "{\"sms\": %d, \"dfma_tflops\": %.3f, \"dmma_tflops\": %.3f, \"dmma_2chain_tflops\": %.3f, "
-        "\"red_f64_coalesced_gops\": %.2f, \"red_f64_scattered_gops\": %.2f}\n",
+        "\"red_f64_coalesced_gops\": %.2f, \"red_f64_scattered_gops\": %.2f, "
+        "\"dmma_dfma_split_warps_tflops\": %.3f, \"dmma_dfma_same_warp_tflops\": %.3f}\n",
         sms, f_dfma / t_dfma * 1e-9, f_dmma / t_dmma * 1e-9, f_dmma4 / t_dmma4 * 1e-9, n_red / t_red * 1e-6,
-        n_red / t_red_s * 1e-6);
+        n_red / t_red_s * 1e-6, f_mix / t_mix * 1e-9, f_both / t_both * 1e-9);
     return 0;
 }
