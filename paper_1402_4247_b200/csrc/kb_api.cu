@@ -99,6 +99,7 @@ struct kbg_ctx {
     uint8_t* d_pown = nullptr;      // per pair: 1 if this rank's blocks touch it (kbg_comm_open)
     std::vector<int64_t> dm_runs;   // [off, len] pairs: DM ranges (per spin) covering the pairs the repack reads
     int64_t* d_xruns = nullptr;     // the exact [off, len] runs of the needed pair blocks (k_dm_gather)
+    unsigned long long* h_flags = nullptr;  // pinned: kbg_grid_pass's DM check words and V flag
     int64_t dm_xruns_n = 0;
     int64_t dm_read_copy = 0;       // doubles per spin the memcpy runs move (pageable DM)
     int64_t io[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // kbg_shard_io
@@ -892,6 +893,10 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
                     n += kbg::launch_finalize(c->ix, c->P, nspin, acc, c->d_out2, true, c->stream2, h_limbs(c));
                 else
                     n += kbg::launch_mirror(c->ix, c->P, nspin, c->d_out2, c->stream2);
+                // the density kernel starts after the mirror: otherwise its CTAs take every SM the
+                // moment the H kernel ends, the mirror waits for the whole density pass and the H
+                // D2H trails it (~80 us at 56 atoms); this way the D2H overlaps the density pass
+                KBG_CUDA(cudaEventRecord(c->ev_rho, c->stream2));
             }
             if (sio) {
                 const int64_t h0 = c->io[4], h1 = c->io[5];
@@ -905,9 +910,12 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
             mark("s2 h out", c->stream2);
         };
         h_half();
-        if (!c->comm_ready) rho_half(false);  // sharded: h_half runs rho_half itself
-        unsigned long long chk[4];
-        KBG_CUDA(cudaMemcpyAsync(chk, c->d_check, sizeof(chk), cudaMemcpyDeviceToHost, c->stream));
+        if (!c->comm_ready) rho_half(true);  // sharded: h_half runs rho_half itself
+        // the DM check words and the non-finite-V flag land in pinned scratch: one wait per stream
+        if (!c->h_flags) KBG_CUDA(cudaMallocHost(&c->h_flags, 8 * sizeof(unsigned long long)));
+        unsigned long long* chk = c->h_flags;
+        KBG_CUDA(cudaMemcpyAsync(chk, c->d_check, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+        KBG_CUDA(cudaMemcpyAsync(chk + 4, c->d_vbits, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream2));
         KBG_CUDA(cudaStreamSynchronize(c->stream2));
         KBG_CUDA(cudaStreamSynchronize(c->stream));
         if (kPhase && !ph.empty()) {
@@ -921,7 +929,8 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
             std::fprintf(stderr, "%s\n", line.c_str());
         }
         if (c->comm_ready) comm_check(c);
-        check_vbits(c, "grid_pass");
+        if (chk[4] >= 0x7ff0000000000000ull)
+            throw Error(KBG_ERR_NONFINITE, "grid_pass: non-finite V_eff (outputs invalid)");
         c->last_launches = n;
         double dmax, amax;
         std::memcpy(&dmax, &chk[0], 8);
@@ -2053,6 +2062,7 @@ void kbg_destroy(kbg_ctx* c) {
     if (c->d_pairtab) cudaFree(c->d_pairtab);
     if (c->d_pown) cudaFree(c->d_pown);
     if (c->d_xruns) cudaFree(c->d_xruns);
+    if (c->h_flags) cudaFreeHost(c->h_flags);
     if (c->comm.tstamp) cudaFree(c->comm.tstamp);
     if (c->d_cpre) cudaFree(c->d_cpre);
     c->veff.release();
