@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--warps", type=int, default=8)
     p.add_argument("--profile", action="store_true", help="one warm pass only (for ncu)")
+    p.add_argument("--xsms", type=int, default=8,
+                   help="N > 1: SMs the H exchange runs on next to the density pass (KBG_OPT_EXCHANGE_SMS; 0: after it)")
     p.add_argument("--collective", default="p2p", choices=["p2p", "nccl"],
                    help="N > 1: H reduction+mirror over peer memory (kb_comm.cu) or NCCL all_reduce")
     return p.parse_args()
@@ -259,6 +261,10 @@ def main():
     sysm = f.system
     gp = GridPass(sysm, device=local, rank=rank, nranks=world)
     gp.set_option(1, args.warps)
+    if world > 1:
+        from paper_1402_4247_b200 import _abi
+
+        gp.set_option(_abi.KBG_OPT_EXCHANGE_SMS, args.xsms)
     t_idx = time.perf_counter()
     ix = gp.build_index()  # index + task lists + geometry cache (Phi), once per geometry
     t_idx = time.perf_counter() - t_idx
@@ -279,6 +285,8 @@ def main():
     d_h = torch.empty((nspin, nnz), dtype=torch.float64, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     p2p = world > 1 and args.collective == "p2p"
+    stream2 = torch.cuda.Stream(device=dev)
+    ev_part, ev_x = torch.cuda.Event(), torch.cuda.Event()
     if p2p:  # exchange-buffer handles (CUDA IPC) all-gathered once
         handles = [None] * world
         dist.all_gather_object(handles, gp.comm_handle())
@@ -290,17 +298,27 @@ def main():
             ev[0].record(stream)
         if p2p and collective:
             # H partial -> density -> fused reduce/mirror over NVLink (full H on every rank): the exchange
-            # runs after the density pass, so the ranks' spread and the flag round trip hide behind it
+            # runs after the density pass, so the ranks' spread and the flag round trip hide behind it;
+            # with --xsms K it runs on K SMs of its own next to the density kernel (second stream)
             gp.hamiltonian_partial_dev(d_veff, f.dV, stream)
             n += gp.last_launches
             if ev:
                 ev[1].record(stream)
+            if args.xsms:
+                ev_part.record(stream)
+                stream2.wait_event(ev_part)
+                gp.hamiltonian_exchange_dev(d_h, stream2)
+                n += gp.last_launches
             gp.density_dev(d_dm, d_rho, stream)
             n += gp.last_launches
             if ev:
                 ev[2].record(stream)
-            gp.hamiltonian_exchange_dev(d_h, stream)
-            n += gp.last_launches
+            if args.xsms:
+                ev_x.record(stream2)
+                stream.wait_event(ev_x)
+            else:
+                gp.hamiltonian_exchange_dev(d_h, stream)
+                n += gp.last_launches
             if ev:
                 ev[3].record(stream)
                 ev[4].record(stream)

@@ -233,6 +233,12 @@ int kbg_last_tally(const kbg_ctx* ctx, kbg_tally* out);
  * DMMA path executes, x 255) is below this threshold run point-exact FP64 FMAs instead of DMMA over whole
  * quads. 0 (default): every task on the FP64 tensor path (measured faster at every cutoff). */
 #define KBG_OPT_SPARSE_DFMA 11
+/* Sharded contexts: SMs the peer-memory H exchange runs on while the density pass runs on the others
+ * (0..32). k > 0 (default 8): the exchange runs as k whole-SM CTAs concurrently with the density kernel,
+ * which leaves those k SMs free -- in kbg_grid_pass, and for a caller that runs
+ * kbg_hamiltonian_exchange_dev on a second stream next to kbg_density_dev. 0: the exchange takes the
+ * whole GPU before (kbg_grid_pass) or after (the split device API on one stream) the density pass. */
+#define KBG_OPT_EXCHANGE_SMS 12
 int kbg_set_option(kbg_ctx* ctx, int option, int64_t value);
 
 const char* kbg_last_error(const kbg_ctx* ctx);

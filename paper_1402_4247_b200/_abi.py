@@ -35,6 +35,7 @@ KBG_OPT_XC = 8
 KBG_OPT_DETERMINISTIC = 9
 KBG_OPT_SHARD_IO = 10
 KBG_OPT_SPARSE_DFMA = 11
+KBG_OPT_EXCHANGE_SMS = 12
 KBG_COMM_HANDLE_BYTES = 96
 KBG_CELL_PRIMITIVE = 0
 KBG_CELL_CUBIC = 1

@@ -95,6 +95,7 @@ struct kbg_ctx {
     // shard-local host transfers of kbg_grid_pass on a sharded context (KBG_OPT_SHARD_IO)
     int shard_io = 1;
     int sparse_thr = 0;  // KBG_OPT_SPARSE_DFMA (0: every task on DMMA)
+    int xsms = 8;        // KBG_OPT_EXCHANGE_SMS (0: exchange on the whole GPU, not overlapped)
     int pending_nspin = 0;  // kbg_hamiltonian_partial_dev done, exchange pending
     uint8_t* d_pown = nullptr;      // per pair: 1 if this rank's blocks touch it (kbg_comm_open)
     std::vector<int64_t> dm_runs;   // [off, len] pairs: DM ranges (per spin) covering the pairs the repack reads
@@ -315,6 +316,8 @@ kbg::GridArgs grid_args(kbg_ctx* c, int nspin, double dV, const double* in, doub
     g.order = c->ix.order;
     g.norder = c->ix.norder;
     g.counter = c->d_counter + (density ? 0 : 1);
+    // the density kernel of a sharded context leaves the exchange's SMs free (KBG_OPT_EXCHANGE_SMS)
+    g.reserve_sms = density && c->comm_ready ? c->xsms : 0;
     g.nrep = c->ix.nrep;
     g.t_ptr = density ? c->ix.rt_ptr : c->ix.ht_ptr;
     g.tasks = density ? c->ix.rt : c->ix.ht;
@@ -873,16 +876,18 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
                     // exchange's CTAs to leave the SMs): the H slice's D2H overlaps the density kernel
                     c->epoch += 2;
                     c->comm.ls = h_limbs(c);
+                    c->comm.sms = c->xsms;  // > 0: on its own SMs, next to the density kernel
                     n += kbg::launch_reduce_mirror(c->comm, c->ix, c->P, nspin, c->d_out2, c->epoch - 1, c->stream2);
                     KBG_CUDA(cudaEventRecord(c->ev_rho, c->stream2));
                     mark("s2 exchanged", c->stream2);
-                    rho_half(true);
+                    rho_half(c->xsms == 0);
                 } else {
                     rho_half(false);
                     KBG_CUDA(cudaEventRecord(c->ev_rho, c->stream));
                     KBG_CUDA(cudaStreamWaitEvent(c->stream2, c->ev_rho, 0));
                     c->epoch += 2;
                     c->comm.ls = h_limbs(c);
+                    c->comm.sms = 0;
                     n += kbg::launch_reduce_mirror(c->comm, c->ix, c->P, nspin, c->d_out2, c->epoch - 1, c->stream2);
                     mark("s2 exchanged", c->stream2);
                 }
@@ -1637,6 +1642,7 @@ int kbg_hamiltonian_allreduce_dev(kbg_ctx* c, int nspin, const double* d_veff, d
         int n = h_accumulate(c, nspin, dV, d_veff, c->d_xbuf, st);
         c->epoch += 2;
         c->comm.ls = h_limbs(c);
+        c->comm.sms = 0;  // nothing runs next to it here: the whole GPU
         n += kbg::launch_reduce_mirror(c->comm, c->ix, c->P, nspin, d_h, c->epoch - 1, st);
         c->last_launches = n;
         c->tally.flops = nspin * 2.0 * c->ix.sum_m2 / c->nranks;
@@ -1673,6 +1679,7 @@ int kbg_hamiltonian_exchange_dev(kbg_ctx* c, int nspin, double* d_h, void* strea
         c->pending_nspin = 0;
         c->epoch += 2;
         c->comm.ls = h_limbs(c);
+        c->comm.sms = c->xsms;
         c->last_launches = kbg::launch_reduce_mirror(c->comm, c->ix, c->P, nspin, d_h, c->epoch - 1,
                                                      static_cast<cudaStream_t>(stream));
     });
@@ -2019,6 +2026,13 @@ int kbg_set_option(kbg_ctx* c, int option, int64_t value) {
             return KBG_OK;
         case KBG_OPT_SHARD_IO:
             c->shard_io = value ? 1 : 0;
+            return KBG_OK;
+        case KBG_OPT_EXCHANGE_SMS:
+            if (value < 0 || value > 32) {
+                c->err = "set_option: exchange SMs must be 0..32";
+                return KBG_ERR_CONFIG;
+            }
+            c->xsms = static_cast<int>(value);
             return KBG_OK;
         case KBG_OPT_SPARSE_DFMA:
             if (value < 0 || value > 255) {

@@ -112,7 +112,7 @@ __device__ __forceinline__ void copy_mirror(const CommArgs& c, int64_t npair, in
 // entry -- or the transposed entry of an (a,a,0) block, flagged by bit 31 --
 // or el0 itself on such a block's diagonal): one coalesced index load, then
 // all N partials in flight at once, then the stores.
-__global__ void __launch_bounds__(256, 4) k_reduce_mirror(CommArgs c, int nspin, int64_t nnz, int64_t ne,
+__global__ void __launch_bounds__(1024, 1) k_reduce_mirror(CommArgs c, int nspin, int64_t nnz, int64_t ne,
                                                        const int32_t* __restrict__ el0,
                                                        const int32_t* __restrict__ el1, unsigned long long epoch,
                                                        int64_t npair, const int64_t* __restrict__ poff,
@@ -235,10 +235,18 @@ int launch_reduce_mirror(const CommArgs& c, const DevIndex& ix, const SysParams&
     // 4 % slower at 448 atoms on 4 GPUs).
     int per_sm = 0;
     KBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_reduce_mirror, 256, 0));
-    const unsigned grid = static_cast<unsigned>(sms) * static_cast<unsigned>(std::max(1, std::min(4, per_sm)));
+    unsigned grid = static_cast<unsigned>(sms) * static_cast<unsigned>(std::max(1, std::min(4, per_sm)));
+    unsigned threads = 256;
+    if (c.sms > 0 && c.pair_na) {
+        // next to the density kernel (KBG_OPT_EXCHANGE_SMS): one 1024-thread CTA per SM (<= 64 registers,
+        // __launch_bounds__), so each CTA holds a whole SM and the density kernel's CTAs, which leave
+        // that many SMs free, cannot take the SMs the exchange needs resident
+        grid = static_cast<unsigned>(std::min(c.sms, sms));
+        threads = 1024;
+    }
     if (c.pair_na) {  // reduce, then (same kernel) copy-out + mirror once every slice has landed
-        k_reduce_mirror<<<grid, 256, 0, st>>>(c, nspin, ix.nnz, c.ne, c.el0, c.el1, epoch, ix.npair, ix.pair_off,
-                                              ix.pair_mirror, d_out);
+        k_reduce_mirror<<<grid, threads, 0, st>>>(c, nspin, ix.nnz, c.ne, c.el0, c.el1, epoch, ix.npair, ix.pair_off,
+                                                  ix.pair_mirror, d_out);
         KBG_CUDA(cudaGetLastError());
         return 1;
     }

@@ -228,6 +228,7 @@ struct GridArgs {
     // parameters, so the compiler reloads them from the constant bank instead
     // of recomputing the layout arithmetic under register pressure.
     uint32_t lay[13];
+    int reserve_sms;    // persistent kernels: SMs left free (a concurrent exchange, KBG_OPT_EXCHANGE_SMS)
 };
 
 // Allocations of the once-per-geometry build (index, task lists, geometry cache,
@@ -308,6 +309,7 @@ struct CommArgs {
     const uint8_t* pair_canon = nullptr;
     unsigned long long* tstamp = nullptr;  // KBG_COMM_TIMING: globaltimer stamps of the exchange phases [8]
     int ls = 1;  // doubles per entry of the partials: 2 = two-limb deterministic accumulators, 1 = FP64
+    int sms = 0;  // > 0: run as this many whole-SM CTAs (concurrent with the density pass), else the GPU
 };
 // Per pair, the ranks (bit k) whose block range [bounds[k], bounds[k + 1]) holds
 // a canonical (block, cover pair) work item of that pair.

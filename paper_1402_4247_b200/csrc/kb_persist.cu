@@ -443,7 +443,7 @@ int launch_persist(const GridArgs& g0, bool density, cudaStream_t st) {
     int dev = 0, sms = 0;
     KBG_CUDA(cudaGetDevice(&dev));
     KBG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(sms, g.norder));
+    const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(sms - g.reserve_sms, g.norder)));
     const size_t smem = persist_bytes(g, density);
     set_layout(g, persist_acc(g, density));
     KBG_CUDA(cudaMemsetAsync(g.counter, 0, sizeof(int), st));

@@ -34,6 +34,8 @@ def main(cfg="cubic56_200Ry"):
     f = Fe3O4.config(cfg)
     gp = GridPass(f.system, device=local, rank=rank, nranks=world)
     gp.set_option(_abi.KBG_OPT_DETERMINISTIC, mode)
+    xsms = int(os.environ.get("P2P_XSMS", "0"))  # KBG_OPT_EXCHANGE_SMS: exchange next to the density pass
+    gp.set_option(_abi.KBG_OPT_EXCHANGE_SMS, xsms)
     ix = gp.build_index()
     handles = [None] * world
     dist.all_gather_object(handles, gp.comm_handle())
@@ -185,7 +187,7 @@ def main(cfg="cubic56_200Ry"):
         h_norm, h_elem, h_small = errs(h_np, h_or)
         r_norm, r_elem, r_small = errs(rho_sum, rho_or)
         det = bool(repeat and bitwise_single)
-        print(json.dumps({"config": cfg, "world": world, "same_bits_all_ranks": same_bits, "repeatable": repeat,
+        print(json.dumps({"config": cfg, "world": world, "exchange_sms": xsms, "same_bits_all_ranks": same_bits, "repeatable": repeat,
                           "bitwise_equal_single_gpu": bitwise_single, "split_api_same_bits": split_same,
                           "rel_diff_vs_nccl": d_nccl, "rel_diff_vs_single_gpu": d_full,
                           "oracle_h_normwise": h_norm, "oracle_h_elementwise": h_elem,
