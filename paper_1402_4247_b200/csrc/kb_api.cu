@@ -790,6 +790,7 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
         ensure(c->d_out, c->cap_out, npt);
         ensure(c->d_in2, c->cap_in2, npt);
         ensure(c->d_out2, c->cap_out2, ndm);
+        if (!c->h_flags) KBG_CUDA(cudaMallocHost(&c->h_flags, 8 * sizeof(unsigned long long)));
         // stream 2: V in -> H -> mirror -> H out; stream 1: DM in -> symmetry check -> rho -> rho out.
         // The copies of one half overlap the kernels of the other. H goes first: its input (npts) is the
         // smaller one to wait for and rho (npts) the smaller output left after the last kernel. The DM
@@ -916,8 +917,8 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
         };
         h_half();
         if (!c->comm_ready) rho_half(true);  // sharded: h_half runs rho_half itself
-        // the DM check words and the non-finite-V flag land in pinned scratch: one wait per stream
-        if (!c->h_flags) KBG_CUDA(cudaMallocHost(&c->h_flags, 8 * sizeof(unsigned long long)));
+        // the DM check words and the non-finite-V flag land in pinned scratch (allocated before the
+        // first launch: an allocation may synchronize, and a sharded pass must not wait on itself)
         unsigned long long* chk = c->h_flags;
         KBG_CUDA(cudaMemcpyAsync(chk, c->d_check, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
         KBG_CUDA(cudaMemcpyAsync(chk + 4, c->d_vbits, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream2));
@@ -1596,6 +1597,22 @@ int kbg_comm_open(kbg_ctx* c, const void* handles) {
         cm.el1 = c->d_canon + e0.size();
         cm.elm = reinterpret_cast<const uint8_t*>(c->d_canon + 2 * e0.size());
         cm.ne = static_cast<int64_t>(e0.size());
+        // Everything kbg_grid_pass allocates, for up to kMaxSpin spins, now: an allocation (or the free
+        // of a growing buffer) inside a sharded pass may synchronize the device while a peer's exchange
+        // waits for this rank's -- a deadlock until the 10 s timeout when the ranks share a process.
+        {
+            const size_t ndm = static_cast<size_t>(kbg::kMaxSpin) * std::max<int64_t>(1, c->ix.nnz);
+            const size_t npt = static_cast<size_t>(kbg::kMaxSpin) * std::max<int64_t>(1, c->npts);
+            ensure(c->d_in, c->cap_in, ndm);
+            ensure(c->d_out, c->cap_out, npt);
+            ensure(c->d_in2, c->cap_in2, npt);
+            ensure(c->d_out2, c->cap_out2, ndm);
+            ensure(c->d_dmr, c->cap_dmr, static_cast<size_t>(kbg::kMaxSpin) * std::max<int64_t>(1, c->ix.nrep));
+            if (!c->stream2) KBG_CUDA(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+            if (!c->ev_pass) KBG_CUDA(cudaEventCreateWithFlags(&c->ev_pass, cudaEventDisableTiming));
+            if (!c->ev_rho) KBG_CUDA(cudaEventCreateWithFlags(&c->ev_rho, cudaEventDisableTiming));
+            if (!c->h_flags) KBG_CUDA(cudaMallocHost(&c->h_flags, 8 * sizeof(unsigned long long)));
+        }
         c->comm_ready = true;
     });
 }

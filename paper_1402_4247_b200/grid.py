@@ -136,15 +136,26 @@ class GridPass:
                     "kbg_hamiltonian")
         return h
 
-    def grid_pass(self, dm: np.ndarray, veff: np.ndarray, dV: float) -> tuple[np.ndarray, np.ndarray]:
-        """rho and H of one SCF iteration in one call (overlapped transfers): returns (rho, h)."""
+    def grid_pass(self, dm: np.ndarray, veff: np.ndarray, dV: float,
+                  out: tuple[np.ndarray, np.ndarray] | None = None) -> tuple[np.ndarray, np.ndarray]:
+        """rho and H of one SCF iteration in one call (overlapped transfers): returns (rho, h).
+        `out` = (rho, h): caller-owned C-contiguous float64 outputs (e.g. pinned, which the kernels write
+        in place); a sharded context writes only its share of them (KBG_OPT_SHARD_IO)."""
         dm = self._spin_array(dm, self._nnz(), "grid_pass: dm")
         veff = self._spin_array(veff, self.system.npts, "grid_pass: veff")
         if dm.shape[0] != veff.shape[0]:
             raise_for_status(_abi.KBG_ERR_DIMENSION, "grid_pass", "dm and veff spin counts differ")
-        # sharded contexts write only their share of rho and H (KBG_OPT_SHARD_IO): zeros elsewhere
-        rho = np.zeros((dm.shape[0], self.system.npts))
-        h = np.zeros((dm.shape[0], self._nnz()))
+        if out is not None:
+            rho, h = out
+            for a, n, what in ((rho, self.system.npts, "rho"), (h, self._nnz(), "h")):
+                if (not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags.c_contiguous
+                        or a.shape != (dm.shape[0], n)):
+                    raise_for_status(_abi.KBG_ERR_DIMENSION, "grid_pass", f"out {what}: C-contiguous float64 "
+                                     f"({dm.shape[0]}, {n}) required")
+        else:
+            # sharded contexts write only their share of rho and H (KBG_OPT_SHARD_IO): zeros elsewhere
+            rho = np.zeros((dm.shape[0], self.system.npts))
+            h = np.zeros((dm.shape[0], self._nnz()))
         self._check(self._lib.kbg_grid_pass(self._h, dm.shape[0], _abi.dptr(dm), _abi.dptr(veff), dV, _abi.dptr(rho),
                                             _abi.dptr(h)), "kbg_grid_pass")
         return rho, h

@@ -58,3 +58,61 @@ def test_p2p_missing_peer_fails_loudly(built):
     torch.cuda.synchronize()
     with pytest.raises(CollectiveError):
         gps[0].comm_check()
+
+
+def _two_rank_contexts(name, det=1):
+    from paper_1402_4247_b200 import _abi
+    from paper_1402_4247_b200.grid import GridPass
+    from paper_1402_4247_b200.system import Fe3O4
+
+    f = Fe3O4.config(name)
+    gps = [GridPass(f.system, device=0, rank=r, nranks=2) for r in range(2)]
+    for gp in gps:
+        gp.set_option(_abi.KBG_OPT_DETERMINISTIC, det)
+        gp.set_option(_abi.KBG_OPT_EXCHANGE_SMS, 8)  # both ranks' exchange CTAs fit on one GPU
+        gp.build_index()
+    handles = [gp.comm_handle() for gp in gps]
+    for gp in gps:
+        gp.comm_open(handles)
+    return f, gps
+
+
+@pytest.mark.gpu
+def test_two_ranks_on_one_gpu_exchange_matches_single_gpu(built):
+    """The sharded H path (kb_comm.cu) on the driver's 1-GPU tier: two ranks' contexts on one GPU with
+    direct-pointer peers, each exchange on 8 SMs of its own (KBG_OPT_EXCHANGE_SMS), so both are resident
+    at once. With the deterministic accumulation the exchanged H equals the single-GPU H bit for bit on
+    both ranks, and the ranks' rho points sum to the single-GPU rho exactly."""
+    import numpy as np
+    import torch
+
+    from paper_1402_4247_b200 import _abi
+    from paper_1402_4247_b200.grid import GridPass
+
+    f, gps = _two_rank_contexts("cubic56_200Ry")
+    ix = gps[0].build_index()
+    dev = torch.device("cuda", 0)
+    v = torch.from_numpy(f.veff()).to(dev)
+    dm = torch.from_numpy(f.dm(ix)).to(dev)
+    hs = [torch.empty((1, ix["nnz"]), dtype=torch.float64, device=dev) for _ in gps]
+    rhos = [torch.zeros((1, f.system.npts), dtype=torch.float64, device=dev) for _ in gps]
+    streams = [torch.cuda.Stream(device=dev) for _ in gps]
+    for rep in range(2):
+        for gp, st in zip(gps, streams):
+            gp.hamiltonian_partial_dev(v, f.dV, st)
+        for gp, h, st in zip(gps, hs, streams):
+            gp.hamiltonian_exchange_dev(h, st)
+        for gp, rho, st in zip(gps, rhos, streams):
+            gp.density_dev(dm, rho, st)
+        torch.cuda.synchronize()
+        for gp in gps:
+            gp.comm_check()
+    single = GridPass(f.system, device=0)
+    single.set_option(_abi.KBG_OPT_DETERMINISTIC, 1)
+    single.build_index()
+    h_ref = single.hamiltonian(f.veff(), f.dV)
+    rho_ref = single.density(f.dm(ix))
+    for h in hs:
+        assert np.array_equal(h.cpu().numpy(), h_ref)
+    # each rank writes rho at its own points only (the rest stays as initialised: zeros)
+    assert np.array_equal((rhos[0] + rhos[1]).cpu().numpy(), rho_ref)

@@ -1,4 +1,3 @@
-for x in 0 1; do for g in "" 1; do
-echo "== xfirst=$x no_gather=$g"
-KBG_NO_DM_GATHER=${g:-} KBG_XCHG_FIRST=$x timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29544 tools/e2e_probe.py ${1:-cubic56_200Ry} 2>&1 | grep -E "^\{|illegal|rror" | head -1 | cut -c1-300
-done; done
+for v in "XSMS=8" "XSMS=8 KBG_NO_DM_GATHER=1" "XSMS=8 KBG_NO_ZERO_COPY=1 KBG_NO_ZERO_COPY_OUT=1" "XSMS=8 KBG_NO_DM_GATHER=1 KBG_NO_ZERO_COPY=1 KBG_NO_ZERO_COPY_OUT=1" "XSMS=8 PIN=0" "XSMS=16" "XSMS=8 KBG_XCHG_FIRST=0"; do
+  env $v KBG_PHASE_TIMING=1 timeout 120 python tools/two_rank_probe.py 2>&1 | grep -E "errors|phases" | cut -c1-330
+done
