@@ -321,7 +321,6 @@ def main():
                 n += gp.last_launches
             if ev:
                 ev[3].record(stream)
-                ev[4].record(stream)
             return n
         gp.density_dev(d_dm, d_rho, stream)
         n += gp.last_launches
@@ -337,8 +336,8 @@ def main():
             ev[3].record(stream)
         if world > 1 and collective:
             dist.all_reduce(d_h)
-        if ev:
-            ev[4].record(stream)
+            if ev:
+                ev[4].record(stream)
         return n
 
     if args.profile:
@@ -354,6 +353,7 @@ def main():
 
     launches = 0
     seg = np.zeros(4)
+    nccl_seg = world > 1 and not p2p
     tot = []
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
     if world > 1:
@@ -378,7 +378,8 @@ def main():
     if world > 1:
         dist.barrier()
     for e in evs:
-        t = [e[i].elapsed_time(e[i + 1]) for i in range(4)]
+        # the all-reduce segment exists only with the NCCL collective (no empty event pair otherwise)
+        t = [e[i].elapsed_time(e[i + 1]) for i in range(3)] + [e[3].elapsed_time(e[4]) if nccl_seg else 0.0]
         seg += np.array(t)
         tot.append(sum(t))
         if os.environ.get("BENCH_STEP_LOG"):
