@@ -2,6 +2,7 @@
 // entry points. Errors follow the kband taxonomy (common.hpp:21-38) as status
 // codes with a message naming the failing field (kbg_last_error).
 #include <algorithm>
+#include <chrono>
 #include <array>
 #include <cmath>
 #include <cstdlib>
@@ -798,6 +799,7 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
         int n = 0;
         // KBG_PHASE_TIMING=1 (diagnostic): events at the phase boundaries of both streams, printed to stderr
         static const bool kPhase = std::getenv("KBG_PHASE_TIMING") != nullptr;
+        const auto t_entry = std::chrono::steady_clock::now();
         std::vector<std::pair<const char*, cudaEvent_t>> ph;
         auto mark = [&](const char* what, cudaStream_t s) {
             if (!kPhase) return;
@@ -922,10 +924,15 @@ int kbg_grid_pass(kbg_ctx* c, int nspin, const double* dm, const double* veff, d
         unsigned long long* chk = c->h_flags;
         KBG_CUDA(cudaMemcpyAsync(chk, c->d_check, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
         KBG_CUDA(cudaMemcpyAsync(chk + 4, c->d_vbits, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream2));
+        const auto t_issued = std::chrono::steady_clock::now();
         KBG_CUDA(cudaStreamSynchronize(c->stream2));
         KBG_CUDA(cudaStreamSynchronize(c->stream));
+        const auto t_synced = std::chrono::steady_clock::now();
         if (kPhase && !ph.empty()) {
-            std::string line = "kbg_grid_pass phases (us from start):";
+            auto us = [&](auto t) { return std::to_string(static_cast<long>(
+                std::chrono::duration_cast<std::chrono::microseconds>(t - t_entry).count())); };
+            std::string line = "kbg_grid_pass host (us from entry): issued " + us(t_issued) + ", synced " +
+                               us(t_synced) + "; phases (us from start):";
             for (auto& e : ph) {
                 float ms = 0.f;
                 KBG_CUDA(cudaEventElapsedTime(&ms, ph[0].second, e.second));
