@@ -70,3 +70,21 @@ def test_null_arguments_are_config_errors(built):
     assert lib.kbg_create(None, 0, C.byref(h)) == _abi.KBG_ERR_CONFIG
     assert lib.kbg_build_index(None) == _abi.KBG_ERR_CONFIG
     assert lib.kbg_density(None, 1, None, None) == _abi.KBG_ERR_CONFIG
+
+
+def test_header_constants_match_python_mirror():
+    """Every #define KBG_* integer constant of include/kbgrid.h has the same value in _abi.py (options,
+    status codes): the Python mirror cannot drift from the C-ABI."""
+    import os
+    import re
+
+    from paper_1402_4247_b200 import _abi
+
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "kbgrid.h")).read()
+    consts = dict(re.findall(r"^#define (KBG_[A-Z0-9_]+) (-?\d+)\b", hdr, flags=re.M))
+    assert "KBG_OPT_EXCHANGE_SMS" in consts
+    missing = [k for k in consts if not hasattr(_abi, k)]
+    wrong = [k for k, v in consts.items() if hasattr(_abi, k) and getattr(_abi, k) != int(v)]
+    assert not wrong, wrong
+    # options must all be mirrored; other constants (sizes, status codes) where the mirror has them
+    assert not [k for k in missing if k.startswith("KBG_OPT_")], missing
