@@ -178,6 +178,13 @@ int kbg_hamiltonian_accumulate_dev(kbg_ctx* ctx, int nspin, const double* d_veff
                                    double* d_h, void* stream);
 int kbg_hamiltonian_mirror_dev(kbg_ctx* ctx, int nspin, double* d_h, void* stream);
 
+/* (new) One SCF grid pass on device buffers: rho and the mirrored H, on a single-rank context: density
+ * then Hamiltonian, or with KBG_OPT_FUSED_PASS = 1 (FP64-atomic H, persistent kernels) ONE fused
+ * persistent kernel -- each block's Phi staged once, its rho and H tasks interleaved on the same SM
+ * (56 atoms 1.4 % faster, 448 atoms 13 % slower: DESIGN.md). No host synchronisation. */
+int kbg_grid_pass_dev(kbg_ctx* ctx, int nspin, const double* d_dm, const double* d_veff, double dV, double* d_rho,
+                      double* d_h, void* stream);
+
 /* Orbital values phi on all grid points of one block, [ncover_blk][64] rows
  * in cover order (testing surface for G2). out must hold M*64 doubles where
  * M = total orbitals of the block's covers; *m_out receives M. */
@@ -239,6 +246,8 @@ int kbg_last_tally(const kbg_ctx* ctx, kbg_tally* out);
  * kbg_hamiltonian_exchange_dev on a second stream next to kbg_density_dev. 0: the exchange takes the
  * whole GPU before (kbg_grid_pass) or after (the split device API on one stream) the density pass. */
 #define KBG_OPT_EXCHANGE_SMS 12
+/* kbg_grid_pass_dev: 1 = one fused rho + H persistent kernel (see there), 0 (default) = separate kernels. */
+#define KBG_OPT_FUSED_PASS 13
 int kbg_set_option(kbg_ctx* ctx, int option, int64_t value);
 
 const char* kbg_last_error(const kbg_ctx* ctx);

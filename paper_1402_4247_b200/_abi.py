@@ -36,6 +36,7 @@ KBG_OPT_DETERMINISTIC = 9
 KBG_OPT_SHARD_IO = 10
 KBG_OPT_SPARSE_DFMA = 11
 KBG_OPT_EXCHANGE_SMS = 12
+KBG_OPT_FUSED_PASS = 13
 KBG_COMM_HANDLE_BYTES = 96
 KBG_CELL_PRIMITIVE = 0
 KBG_CELL_CUBIC = 1
@@ -112,6 +113,7 @@ KBGRID_SYMBOLS = [
     ("kbg_hamiltonian_dev", _I, [_P, _I, _P, _D, _P, _P]),
     ("kbg_hamiltonian_accumulate_dev", _I, [_P, _I, _P, _D, _P, _P]),
     ("kbg_hamiltonian_mirror_dev", _I, [_P, _I, _P, _P]),
+    ("kbg_grid_pass_dev", _I, [_P, _I, _P, _P, C.c_double, _P, _P, _P]),
     ("kbg_block_orbitals", _I, [_P, _I64, _DP, _I64, C.POINTER(_I)]),
     ("kbg_last_launches", _I, [_P]),
     ("kbg_last_tally", _I, [_P, C.POINTER(kbg_tally)]),

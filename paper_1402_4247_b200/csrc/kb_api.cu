@@ -97,6 +97,7 @@ struct kbg_ctx {
     int shard_io = 1;
     int sparse_thr = 0;  // KBG_OPT_SPARSE_DFMA (0: every task on DMMA)
     int xsms = 8;        // KBG_OPT_EXCHANGE_SMS (0: exchange on the whole GPU, not overlapped)
+    int fused = 0;       // KBG_OPT_FUSED_PASS
     int pending_nspin = 0;  // kbg_hamiltonian_partial_dev done, exchange pending
     uint8_t* d_pown = nullptr;      // per pair: 1 if this rank's blocks touch it (kbg_comm_open)
     std::vector<int64_t> dm_runs;   // [off, len] pairs: DM ranges (per spin) covering the pairs the repack reads
@@ -664,6 +665,44 @@ int kbg_hamiltonian_accumulate_dev(kbg_ctx* c, int nspin, const double* d_veff, 
         if (c->det) c->last_launches += kbg::launch_finalize(c->ix, c->P, nspin, acc, d_h, false, st, h_limbs(c));
         c->tally.flops = nspin * 2.0 * c->ix.sum_m2;
         c->tally.bytes = 8.0 * nspin * (c->ix.nnz + c->npts);
+    });
+}
+
+int kbg_grid_pass_dev(kbg_ctx* c, int nspin, const double* d_dm, const double* d_veff, double dV, double* d_rho,
+                      double* d_h, void* stream) {
+    if (!c || !d_dm || !d_veff || !d_rho || !d_h) return KBG_ERR_CONFIG;
+    return guard(c, [&] {
+        check_nspin(nspin);
+        require_index(c);
+        KBG_CUDA(cudaSetDevice(c->device));
+        if (c->nranks > 1) throw Error(KBG_ERR_CONFIG, "grid_pass_dev: single-rank contexts only");
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        int n = 0;
+        const bool fused_ok = c->fused && c->persist_ok && c->persist && c->ix.phis && !c->det &&
+                              c->sparse_thr == 0 && c->scatter == 0;
+        kbg::GridArgs gh = grid_args(c, nspin, dV, d_veff, d_h, false);
+        kbg::GridArgs gr = grid_args(c, nspin, 0.0, d_dm, d_rho, true);
+        if (fused_ok && kbg::fused_fits(gh, gr)) {
+            ensure(c->d_dmr, c->cap_dmr, static_cast<size_t>(nspin) * std::max<int64_t>(1, c->ix.nrep));
+            gr.dmr = c->d_dmr;
+            n += kbg::launch_dm_repack(c->ix, c->P, nspin, d_dm, c->d_dmr, st);
+            KBG_CUDA(cudaMemsetAsync(d_h, 0, static_cast<size_t>(nspin) * c->ix.nnz * sizeof(double), st));
+            KBG_CUDA(cudaMemsetAsync(c->d_vbits, 0, sizeof(unsigned long long), st));
+            n += kbg::launch_fused(gh, gr, st);
+        } else {
+            n += run_density(c, nspin, d_dm, d_rho, st);
+            double* acc = h_acc_buffer(c, nspin, d_h);
+            n += h_accumulate(c, nspin, dV, d_veff, acc, st);
+            if (c->det) {
+                n += kbg::launch_finalize(c->ix, c->P, nspin, acc, d_h, true, st, h_limbs(c));
+                c->last_launches = n;
+                return;
+            }
+        }
+        n += kbg::launch_mirror(c->ix, c->P, nspin, d_h, st);
+        c->last_launches = n;
+        c->tally.flops = nspin * (4.0 * c->ix.sum_m2 + 2.0 * c->ix.sum_m);
+        c->tally.bytes = 16.0 * nspin * (c->ix.nnz + c->npts);
     });
 }
 
@@ -2050,6 +2089,9 @@ int kbg_set_option(kbg_ctx* c, int option, int64_t value) {
             return KBG_OK;
         case KBG_OPT_SHARD_IO:
             c->shard_io = value ? 1 : 0;
+            return KBG_OK;
+        case KBG_OPT_FUSED_PASS:
+            c->fused = value ? 1 : 0;
             return KBG_OK;
         case KBG_OPT_EXCHANGE_SMS:
             if (value < 0 || value > 32) {

@@ -229,6 +229,9 @@ struct GridArgs {
     // of recomputing the layout arithmetic under register pressure.
     uint32_t lay[13];
     int reserve_sms;    // persistent kernels: SMs left free (a concurrent exchange, KBG_OPT_EXCHANGE_SMS)
+    // fused rho + H pass (k_fused): the rho table images and the rho output next to H's
+    const unsigned char* tabs2;
+    double* out2;
 };
 
 // Allocations of the once-per-geometry build (index, task lists, geometry cache,
@@ -370,6 +373,11 @@ void free_cache(DevIndex& ix);
 bool persist_fits(const GridArgs& g, bool density);
 size_t persist_smem(const GridArgs& g, bool density);
 int launch_density_persist(const GridArgs& g, cudaStream_t st);
+// Fused rho + H pass (one persistent kernel, a block's Phi staged once, both task queues interleaved):
+// gh = the H launch's args (in = V, out = H accumulator), gr = the rho launch's (dmr, out = rho).
+// Returns 0 (nothing launched) when the fused buffers do not fit shared memory.
+bool fused_fits(const GridArgs& gh, const GridArgs& gr);
+int launch_fused(const GridArgs& gh, const GridArgs& gr, cudaStream_t st);
 int launch_hamiltonian_persist(const GridArgs& g, cudaStream_t st);
 int launch_dm_gather(const int64_t* d_runs, int64_t nruns, int nspin, int64_t nnz, const double* src, double* dst,
                      cudaStream_t st);

@@ -273,6 +273,49 @@ __device__ void producer(const GridArgs& g, const Buffers<DENSITY>& B, int lane)
     }
 }
 
+// The block's rho from the per-task partial sums of the rho queue (task order: deterministic). Lane l
+// owns slots l (half 0) and 32 + l (half 1); the slots go through the (now idle) Phi rows so each group
+// of 4 lanes stores 4 consecutive k in C order -- 32-byte segments instead of the octet layout's 16 (HBM
+// sectors; PCIe writes when rho is mapped host memory). The next block's bulk copy rewrites those rows.
+__device__ void rho_block_store(const GridArgs& g, const Smem& sm, int ntask, int bi, int bj, int bk, double* out,
+                                int lane) {
+    double r[kMaxSpin][2];
+#pragma unroll
+    for (int spin = 0; spin < kMaxSpin; ++spin) {
+        r[spin][0] = r[spin][1] = 0.0;
+        if (spin >= g.nspin) continue;
+        const double* res = sm.acc() + static_cast<size_t>(spin) * ntask * 32;
+        for (int e = 0; e < ntask; ++e) {
+            const double v = res[e * 32 + lane];
+            if (sm.task()[e].half)
+                r[spin][1] += v;
+            else
+                r[spin][0] += v;
+        }
+    }
+    double* tmp = sm.phi();
+    __syncwarp();
+#pragma unroll
+    for (int spin = 0; spin < kMaxSpin; ++spin) {
+        tmp[spin * 64 + lane] = r[spin][0];
+        tmp[spin * 64 + 32 + lane] = r[spin][1];
+    }
+    __syncwarp();
+    const int lj = (lane >> 2) & 3, lk = lane & 3;
+    const int j = bj * 4 + lj, kk = bk * 4 + lk;
+    for (int hh = 0; hh < 2; ++hh) {
+        const int li = 2 * hh + (lane >> 4);
+        const int slot = ((((li >> 1) << 2) | ((lj >> 1) << 1) | (lk >> 1)) << 3) | ((li & 1) << 2) |
+                         ((lj & 1) << 1) | (lk & 1);
+        const int i = bi * 4 + li;
+        if (i < g.sys.N[0] && j < g.sys.N[1] && kk < g.sys.N[2]) {
+            const int64_t pt = (static_cast<int64_t>(i) * g.sys.N[1] + j) * g.sys.N[2] + kk;
+            for (int spin = 0; spin < g.nspin; ++spin) out[spin * g.npts + pt] = tmp[spin * 64 + slot];
+        }
+    }
+    __syncwarp();
+}
+
 template <bool DENSITY, bool DET, bool SPARSE>
 __device__ void consumer(const GridArgs& g, const Buffers<DENSITY>& B, int cw, int lane) {
     constexpr int NC = Cfg<DENSITY>::NC;
@@ -352,46 +395,7 @@ __device__ void consumer(const GridArgs& g, const Buffers<DENSITY>& B, int cw, i
                 int bi, bj, bk;
                 block_decode(g.sys, b, bi, bj, bk);
                 if (g.task_warps == 1) {
-                    // per-task sums in task order: lane l owns slots l (half 0) and 32 + l (half 1)
-                    double r[kMaxSpin][2];
-#pragma unroll
-                    for (int spin = 0; spin < kMaxSpin; ++spin) {
-                        r[spin][0] = r[spin][1] = 0.0;
-                        if (spin >= g.nspin) continue;
-                        const double* res = sm.acc() + static_cast<size_t>(spin) * ntask * 32;
-                        for (int e = 0; e < ntask; ++e) {
-                            const double v = res[e * 32 + lane];
-                            if (sm.task()[e].half)
-                                r[spin][1] += v;
-                            else
-                                r[spin][0] += v;
-                        }
-                    }
-                    // Store in C order: the slots go through the (now idle) Phi rows so each
-                    // group of 4 lanes writes 4 consecutive k -- 32-byte segments instead of
-                    // the octet layout's 16 (HBM sectors; PCIe writes when rho is mapped host
-                    // memory). The next block's bulk copy rewrites these rows.
-                    double* tmp = sm.phi();
-                    __syncwarp();
-#pragma unroll
-                    for (int spin = 0; spin < kMaxSpin; ++spin) {
-                        tmp[spin * 64 + lane] = r[spin][0];
-                        tmp[spin * 64 + 32 + lane] = r[spin][1];
-                    }
-                    __syncwarp();
-                    const int lj = (lane >> 2) & 3, lk = lane & 3;
-                    const int j = bj * 4 + lj, kk = bk * 4 + lk;
-                    for (int hh = 0; hh < 2; ++hh) {
-                        const int li = 2 * hh + (lane >> 4);
-                        const int slot = ((((li >> 1) << 2) | ((lj >> 1) << 1) | (lk >> 1)) << 3) |
-                                         ((li & 1) << 2) | ((lj & 1) << 1) | (lk & 1);
-                        const int i = bi * 4 + li;
-                        if (i < g.sys.N[0] && j < g.sys.N[1] && kk < g.sys.N[2]) {
-                            const int64_t pt = (static_cast<int64_t>(i) * g.sys.N[1] + j) * g.sys.N[2] + kk;
-                            for (int spin = 0; spin < g.nspin; ++spin) g.out[spin * g.npts + pt] = tmp[spin * 64 + slot];
-                        }
-                    }
-                    __syncwarp();
+                    rho_block_store(g, sm, ntask, bi, bj, bk, g.out, lane);
                 } else
                 for (int i = lane; i < g.nspin * 64; i += 32) {
                     const int spin = i >> 6, p = i & 63;
@@ -432,6 +436,244 @@ __global__ void __launch_bounds__(Cfg<DENSITY>::NT, 1) k_persist(GridArgs g) {
     }
 }
 
+// ---- fused rho + H pass ----------------------------------------------------------------
+// One persistent kernel for both contractions: a block's Phi is staged once, with the H and the rho
+// table images side by side, and the block's rho and H tasks come from one queue, interleaved, so
+// the warps of an SM run latency-bound rho tasks and pipe-bound H tasks at the same time. Buffer:
+// [H tables | rho tables | w (V dV) | rho per-task sums | Phi], two buffers. Non-deterministic
+// FP64-atomic H only; 20 consumer warps at the rho kernel's 96 registers.
+struct FusedCfg {
+    static constexpr int NC = kPersistConsumersR;
+    static constexpr int NT = (kPersistProducers + NC) * 32;
+};
+
+struct FusedBuffers {
+    Smem sm0;       // H view of buffer 0
+    uint32_t T;     // table image bytes: the rho image sits at T
+    uint32_t bsz;   // buffer stride
+    uint32_t wb;    // bytes of w
+    uint64_t* full;
+    uint64_t* empty;
+    __device__ __forceinline__ Smem h(int s) const {
+        Smem x = sm0;
+        x.base = static_cast<uint32_t>(s) * bsz;
+        return x;
+    }
+    __device__ __forceinline__ Smem r(int s) const {  // rho view: tables at T, per-task sums after w
+        Smem x = sm0;
+        x.base = static_cast<uint32_t>(s) * bsz + T;
+        x.o_acc = sm0.o_acc - T + wb;
+        x.o_phi = sm0.o_phi - T;
+        return x;
+    }
+};
+
+// Host: the fused buffer layout into g.lay (table offsets as one image; acc at 2T; Phi after acc).
+__host__ __device__ inline size_t fused_layout(GridArgs& g) {
+    size_t off[12];
+    const size_t T = tables_layout(g, off);
+    const size_t acc = static_cast<size_t>(g.nspin) * 64 + static_cast<size_t>(g.nspin) * g.max_rtasks * 32;
+    off[10] = 2 * T;
+    off[11] = off[10] + align16(acc * sizeof(double));
+    const size_t bytes = off[11] + align16(static_cast<size_t>(g.max_rows) * 64 * sizeof(double));
+    for (int i = 0; i < 12; ++i) g.lay[i] = static_cast<uint32_t>(off[i]);
+    g.lay[12] = static_cast<uint32_t>(bytes);
+    return 2 * align16(bytes) + 64;
+}
+
+__device__ __forceinline__ FusedBuffers carve_fused(const GridArgs& g) {
+    FusedBuffers B;
+    B.sm0 = carve(0u, g);
+    B.T = static_cast<uint32_t>(g.tab_bytes);
+    B.bsz = (g.lay[12] + 15u) & ~15u;
+    B.wb = static_cast<uint32_t>(g.nspin) * 64u * 8u;
+    B.full = reinterpret_cast<uint64_t*>(kbg_smem + 2 * B.bsz);
+    B.empty = B.full + 2;
+    return B;
+}
+
+// Next non-empty owned block (-1: none); empty blocks get rho = 0 on the way.
+__device__ int64_t next_block_fused(const GridArgs& g, int lane) {
+    for (;;) {
+        int idx = 0;
+        if (lane == 0) idx = atomicAdd(g.counter, 1);
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if (idx >= g.norder) return -1;
+        const int64_t b = g.order[idx];
+        if (g.blk_ptr[b + 1] > g.blk_ptr[b]) return b;
+        int bi, bj, bk;
+        block_decode(g.sys, b, bi, bj, bk);
+        for (int p = lane; p < 64; p += 32) {
+            bool valid;
+            const int64_t pt = slot_point(g.sys, bi, bj, bk, p, valid);
+            if (valid)
+                for (int spin = 0; spin < g.nspin; ++spin) g.out2[spin * g.npts + pt] = 0.0;
+        }
+    }
+}
+
+__device__ void producer_fused(const GridArgs& g, const FusedBuffers& B, int lane) {
+    uint64_t pol = 0;
+#if KBG_L2_HINT
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#endif
+    const uint32_t T = B.T;
+    auto phi_of = [&](int64_t b, const double*& phi, uint32_t& pb) {
+        const int64_t i = b - g.blk_begin;
+        phi = g.phis + g.phi_off[i];
+        pb = static_cast<uint32_t>((g.phi_off[i + 1] - g.phi_off[i]) * sizeof(double));
+    };
+    double w_cur[2 * kMaxSpin], w_next[2 * kMaxSpin];
+    auto load_w = [&](int64_t b, double (&w)[2 * kMaxSpin]) {
+        if (b < 0) return;
+        int bi, bj, bk;
+        block_decode(g.sys, b, bi, bj, bk);
+#pragma unroll
+        for (int j = 0; j < 2 * kMaxSpin; ++j) {
+            const int i = lane + 32 * j;
+            bool valid = false;
+            const int64_t pt = slot_point(g.sys, bi, bj, bk, i & 63, valid);
+            w[j] = (valid && i < g.nspin * 64) ? g.in[(i >> 6) * g.npts + pt] : 0.0;
+        }
+    };
+    int64_t b_next = next_block_fused(g, lane);
+    load_w(b_next, w_next);
+    for (int k = 0;; ++k) {
+        const int s = k & 1;
+        const int64_t b = b_next;
+#pragma unroll
+        for (int j = 0; j < 2 * kMaxSpin; ++j) w_cur[j] = w_next[j];
+        if (b >= 0) {
+            b_next = next_block_fused(g, lane);
+            load_w(b_next, w_next);
+            if (b_next >= 0 && lane == 0) {
+                const int64_t i = b_next - g.blk_begin;
+                const double* phi;
+                uint32_t pb;
+                phi_of(b_next, phi, pb);
+                prefetch_l2(g.tabs + i * T, T, pol);
+                prefetch_l2(g.tabs2 + i * T, T, pol);
+                prefetch_l2(phi, pb, pol);
+            }
+        }
+        if (k >= 2) mbar_wait(&B.empty[s], ((k >> 1) - 1) & 1, 256);
+        const Smem sh = B.h(s);
+        if (b < 0) {
+            if (lane == 0) {
+                sh.meta()->block = -1;
+                mbar_arrive(&B.full[s]);
+            }
+            return;
+        }
+        bool fin = true;
+#pragma unroll
+        for (int j = 0; j < 2 * kMaxSpin; ++j) {
+            const int i = lane + 32 * j;
+            if (i < g.nspin * 64) sh.acc()[i] = w_cur[j] * (g.dV * g.sign);
+            fin = fin && isfinite(w_cur[j]);
+        }
+        if (!__all_sync(0xffffffffu, fin) && lane == 0 && g.vbits)
+            atomicMax(const_cast<unsigned long long*>(g.vbits), 0x7ff8000000000000ull);
+        __syncwarp();
+        if (lane == 0) {
+            const int64_t i = b - g.blk_begin;
+            const double* phi;
+            uint32_t pb;
+            phi_of(b, phi, pb);
+            mbar_arrive_tx(&B.full[s], 2 * T + pb);
+            bulk_g2s_hint(sh.meta(), g.tabs + i * T, T, &B.full[s], pol);
+            bulk_g2s_hint(kbg_smem + sh.base + T, g.tabs2 + i * T, T, &B.full[s], pol);
+            bulk_g2s_hint(sh.phi(), phi, pb, &B.full[s], pol);
+        }
+        __syncwarp();
+    }
+}
+
+__device__ void consumer_fused(const GridArgs& g, const FusedBuffers& B, int lane) {
+    constexpr int NC = FusedCfg::NC;
+    for (int k = 0;; ++k) {
+        const int s = k & 1;
+        mbar_wait(&B.full[s], (k >> 1) & 1);
+        const Smem sh = B.h(s), sr = B.r(s);
+        const int64_t b = sh.meta()->block;
+        if (b < 0) return;
+        const int ncov = sh.meta()->ncov;
+        const int nh = sh.wptr()[1], nr = sr.wptr()[1];
+        const int nht = g.nspin * nh, nrt = g.nspin * nr, m = min(nht, nrt), tot = nht + nrt;
+        for (;;) {
+            int q = 0;
+            if (lane == 0) q = atomicAdd(&sh.meta()->next, 1);
+            q = __shfl_sync(0xffffffffu, q, 0);
+            if (q >= tot) break;
+            // interleaved: rho, H, rho, H, ... while both last, then the longer list's rest
+            bool is_rho;
+            int e;
+            if (q < 2 * m) {
+                is_rho = !(q & 1);
+                e = q >> 1;
+            } else {
+                e = q - m;
+                is_rho = nrt > nht;
+            }
+            if (is_rho) {
+                const int spin = e >= nr;
+                const Task t = sr.task()[e - spin * nr];
+                double* res = sr.acc() + static_cast<size_t>(e) * 32;
+                res[lane] = 0.0;
+                __syncwarp();
+                rho_task(sr, ncov, t, g.dmr + spin * g.nrep, res - 32 * t.half, lane);
+            } else {
+                const int spin = e >= nh;
+                const Task t = sh.task()[e - spin * nh];
+                h_task<false, false>(sh, sh.acc() + spin * 64, ncov, t, g.out + spin * g.nnz, g.scatter, lane);
+            }
+        }
+        __syncwarp();
+        int last = 0;
+        if (lane == 0) {
+            __threadfence_block();
+            last = atomicAdd(&sh.meta()->done, 1) == NC - 1;
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {
+            __threadfence_block();
+            int bi, bj, bk;
+            block_decode(g.sys, b, bi, bj, bk);
+            rho_block_store(g, sr, nr, bi, bj, bk, g.out2, lane);
+            if (lane == 0) mbar_arrive(&B.empty[s]);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(FusedCfg::NT, 1) k_fused(GridArgs g) {
+    const FusedBuffers B = carve_fused(g);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&B.full[s], 1);
+            mbar_init(&B.empty[s], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp < kPersistProducers) {
+        if (warp == 0) producer_fused(g, B, lane);
+    } else {
+        consumer_fused(g, B, lane);
+    }
+}
+
+GridArgs fused_args(const GridArgs& gh, const GridArgs& gr) {
+    GridArgs g = gh;
+    g.tabs2 = gr.tabs;
+    g.out2 = gr.out;
+    g.dmr = gr.dmr;
+    g.nrep = gr.nrep;
+    g.max_rtasks = gr.max_rtasks;
+    g.max_tasks = std::max(gh.max_tasks, gr.max_tasks);
+    return g;
+}
+
 template <class K>
 void set_smem(K kernel, size_t bytes) {
     KBG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
@@ -468,6 +710,28 @@ int launch_persist(const GridArgs& g0, bool density, cudaStream_t st) {
 }
 
 }  // namespace
+
+bool fused_fits(const GridArgs& gh, const GridArgs& gr) {
+    if (gh.task_warps != 1 || gr.task_warps != 1 || gh.scatter != 0) return false;
+    GridArgs g = fused_args(gh, gr);
+    return fused_layout(g) <= 227 * 1024;
+}
+
+int launch_fused(const GridArgs& gh, const GridArgs& gr, cudaStream_t st) {
+    GridArgs g = fused_args(gh, gr);
+    if (g.norder <= 0) return 0;
+    const size_t smem = fused_layout(g);
+    if (smem > 227 * 1024) return 0;
+    int dev = 0, sms = 0;
+    KBG_CUDA(cudaGetDevice(&dev));
+    KBG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(sms, g.norder)));
+    KBG_CUDA(cudaMemsetAsync(g.counter, 0, sizeof(int), st));
+    set_smem(k_fused, smem);
+    k_fused<<<grid, FusedCfg::NT, smem, st>>>(g);
+    KBG_CUDA(cudaGetLastError());
+    return 1;
+}
 
 bool persist_fits(const GridArgs& g, bool density) { return persist_bytes(g, density) <= 227 * 1024; }
 size_t persist_smem(const GridArgs& g, bool density) { return persist_bytes(g, density); }

@@ -193,6 +193,16 @@ class GridPass:
                                                              h.data_ptr(), self._stream_ptr(stream)),
                     "kbg_hamiltonian_accumulate_dev")
 
+    def grid_pass_dev(self, dm, veff, dV: float, rho, h, stream=None) -> None:
+        """rho and the mirrored H of one pass on device tensors (kbg_grid_pass_dev: one fused persistent
+        kernel when possible)."""
+        ns = self._spin_tensor(dm, self._nnz(), "grid_pass_dev: dm")
+        for t, n, what in ((veff, self.system.npts, "veff"), (rho, self.system.npts, "rho"), (h, self._nnz(), "h")):
+            if self._spin_tensor(t, n, "grid_pass_dev: " + what) != ns:
+                raise_for_status(_abi.KBG_ERR_DIMENSION, "grid_pass_dev", f"{what} spin count differs from dm's")
+        self._check(self._lib.kbg_grid_pass_dev(self._h, ns, dm.data_ptr(), veff.data_ptr(), dV, rho.data_ptr(),
+                                                h.data_ptr(), self._stream_ptr(stream)), "kbg_grid_pass_dev")
+
     def hamiltonian_mirror_dev(self, h, stream=None) -> None:
         self._spin_tensor(h, self._nnz(), "hamiltonian_mirror_dev: h")
         self._check(self._lib.kbg_hamiltonian_mirror_dev(self._h, h.shape[0], h.data_ptr(),
