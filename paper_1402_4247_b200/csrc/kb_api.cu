@@ -32,7 +32,7 @@ struct kbg_ctx {
     bool persist_ok = false;   // two staging buffers fit: persistent kernels
     int persist = 1;           // option: use the persistent kernels when they fit
     int schedule = 3;          // KBG_OPT_SCHEDULE
-    int block_order = 0;       // KBG_OPT_BLOCK_ORDER
+    int block_order = 2;       // KBG_OPT_BLOCK_ORDER (2: by blocks per SM)
     int xc = 0;                // KBG_OPT_XC
     int plan_schedule = -1;    // schedule / rho split the task lists were built with (kbg_plan_info)
     int plan_split = 0;
@@ -579,7 +579,13 @@ int kbg_build_index(kbg_ctx* c) {
         kbg::pool_free(c->ix.order);
         c->ix.order = nullptr;
         c->ix.norder = c->blk_end - c->blk_begin;
-        kbg::block_order_device(c->ix, c->blk_begin, c->blk_end, c->block_order == 0, c->stream);
+        bool heavy_first = c->block_order == 0;
+        if (c->block_order == 2) {
+            int sms = 148;
+            KBG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+            heavy_first = c->blk_end - c->blk_begin <= static_cast<int64_t>(500) * sms;
+        }
+        kbg::block_order_device(c->ix, c->blk_begin, c->blk_end, heavy_first, c->stream);
         if (!c->d_counter) KBG_CUDA(cudaMalloc(&c->d_counter, 2 * sizeof(int)));
         if (c->persist_ok) {
             kbg::build_cache_device(grid_args(c, 1, 0.0, nullptr, nullptr, false),
@@ -2071,8 +2077,8 @@ int kbg_set_option(kbg_ctx* c, int option, int64_t value) {
             c->xc = static_cast<int>(value);
             return KBG_OK;
         case KBG_OPT_BLOCK_ORDER:
-            if (value < 0 || value > 1) {
-                c->err = "set_option: block order must be 0 or 1";
+            if (value < 0 || value > 2) {
+                c->err = "set_option: block order must be 0, 1 or 2";
                 return KBG_ERR_CONFIG;
             }
             c->block_order = static_cast<int>(value);

@@ -27,7 +27,7 @@ def main():
     ap.add_argument("--nspin", type=int, default=1)
     ap.add_argument("--schedules", default="3,0,1,2", help="KBG_OPT_SCHEDULE values (persistent kernels)")
     ap.add_argument("--fallback", type=int, default=1, help="also time the one-CTA-per-block kernels")
-    ap.add_argument("--orders", default="0", help="KBG_OPT_BLOCK_ORDER values (persistent kernels)")
+    ap.add_argument("--orders", default="2", help="KBG_OPT_BLOCK_ORDER values (persistent kernels)")
     ap.add_argument("--scatter", type=int, default=0, help="KBG_OPT_SCATTER_STORE timing experiment bits")
     ap.add_argument("--det", type=int, default=0, help="KBG_OPT_DETERMINISTIC (1: two-limb exact scatter)")
     ap.add_argument("--kernels", default="density,h_accumulate")
