@@ -78,7 +78,8 @@ def _two_rank_contexts(name, det=1):
 
 
 @pytest.mark.gpu
-def test_two_ranks_on_one_gpu_exchange_matches_single_gpu(built):
+@pytest.mark.parametrize("nspin", [1, 2])
+def test_two_ranks_on_one_gpu_exchange_matches_single_gpu(built, nspin):
     """The sharded H path (kb_comm.cu) on the driver's 1-GPU tier: two ranks' contexts on one GPU with
     direct-pointer peers, each exchange on 8 SMs of its own (KBG_OPT_EXCHANGE_SMS), so both are resident
     at once. With the deterministic accumulation the exchanged H equals the single-GPU H bit for bit on
@@ -92,10 +93,10 @@ def test_two_ranks_on_one_gpu_exchange_matches_single_gpu(built):
     f, gps = _two_rank_contexts("cubic56_200Ry")
     ix = gps[0].build_index()
     dev = torch.device("cuda", 0)
-    v = torch.from_numpy(f.veff()).to(dev)
-    dm = torch.from_numpy(f.dm(ix)).to(dev)
-    hs = [torch.empty((1, ix["nnz"]), dtype=torch.float64, device=dev) for _ in gps]
-    rhos = [torch.zeros((1, f.system.npts), dtype=torch.float64, device=dev) for _ in gps]
+    v = torch.from_numpy(f.veff(nspin=nspin)).to(dev)
+    dm = torch.from_numpy(f.dm(ix, nspin=nspin)).to(dev)
+    hs = [torch.empty((nspin, ix["nnz"]), dtype=torch.float64, device=dev) for _ in gps]
+    rhos = [torch.zeros((nspin, f.system.npts), dtype=torch.float64, device=dev) for _ in gps]
     streams = [torch.cuda.Stream(device=dev) for _ in gps]
     for rep in range(2):
         for gp, st in zip(gps, streams):
@@ -110,8 +111,8 @@ def test_two_ranks_on_one_gpu_exchange_matches_single_gpu(built):
     single = GridPass(f.system, device=0)
     single.set_option(_abi.KBG_OPT_DETERMINISTIC, 1)
     single.build_index()
-    h_ref = single.hamiltonian(f.veff(), f.dV)
-    rho_ref = single.density(f.dm(ix))
+    h_ref = single.hamiltonian(f.veff(nspin=nspin), f.dV)
+    rho_ref = single.density(f.dm(ix, nspin=nspin))
     for h in hs:
         assert np.array_equal(h.cpu().numpy(), h_ref)
     # each rank writes rho at its own points only (the rest stays as initialised: zeros)

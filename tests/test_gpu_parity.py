@@ -379,19 +379,19 @@ def test_sparse_dfma_switch_parity(name, thr):
     assert_parity(h, c.o.hamiltonian(c.veff, c.f.dV))
 
 
-@pytest.mark.parametrize("fused", [0, 1])
-def test_grid_pass_dev_matches_separate_kernels(fused):
+@pytest.mark.parametrize("fused,nspin", [(0, 1), (1, 1), (1, 2)])
+def test_grid_pass_dev_matches_separate_kernels(fused, nspin):
     """kbg_grid_pass_dev (separate kernels, or the fused rho + H persistent kernel with
     KBG_OPT_FUSED_PASS): rho bitwise equal to kbg_density_dev, H equal to the mirrored H within the
     FP64-atomic order difference."""
     import torch
 
-    c = case("cubic56_200Ry")
+    c = case("cubic56_200Ry", nspin)
     dev = torch.device("cuda", 0)
     dm = torch.from_numpy(c.dm).to(dev)
     v = torch.from_numpy(c.veff).to(dev)
-    rho0 = torch.zeros((1, c.f.system.npts), dtype=torch.float64, device=dev)
-    h0 = torch.zeros((1, c.gix["nnz"]), dtype=torch.float64, device=dev)
+    rho0 = torch.zeros((nspin, c.f.system.npts), dtype=torch.float64, device=dev)
+    h0 = torch.zeros((nspin, c.gix["nnz"]), dtype=torch.float64, device=dev)
     c.gp.density_dev(dm, rho0)
     c.gp.hamiltonian_dev(v, c.f.dV, h0)
     rho1, h1 = torch.zeros_like(rho0), torch.zeros_like(h0)
