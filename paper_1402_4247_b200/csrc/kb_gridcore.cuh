@@ -36,6 +36,12 @@
 #endif
 // rho D' gather: 1 = predicated loads (no per-lane branch around rows without a pair to the partner;
 // the density pass 0.352 -> 0.343 ms at 56 atoms and no register spills), 0 = branch + zero fill.
+// H pair tiles (h_tile2): 1 = quad addresses as byte offsets, one XOR + one add per operand (56 atoms H
+// 0.3185 -> 0.3164 ms, 448 atoms 2.376 -> 2.353 ms; the same in the single-partner h_tile adds spills
+// and measured slower); 0 = element indices scaled per access
+#ifndef KBG_H_BYTEADDR
+#define KBG_H_BYTEADDR 1
+#endif
 #ifndef KBG_RHO_PGATHER
 #define KBG_RHO_PGATHER 1
 #endif
@@ -525,21 +531,43 @@ __device__ __forceinline__ void h_tile2(const Smem& sm, const double* __restrict
     // Three loops -- quads of both partners, of cj1 only, of cj2 only -- so every DMMA is
     // unconditional: a DMMA under a per-quad predicate the compiler cannot prove warp-uniform
     // costs a WARPSYNC + NOP pair each (SASS of the single merged loop, profiles/ncu_h_r2.txt).
+#if KBG_H_BYTEADDR
+    // byte offsets: the swizzled quad offset is one XOR of the quad's byte offset with the row's swizzle
+    // bytes, added to a per-lane byte pointer (two instructions per operand address)
+    const char* ca = reinterpret_cast<const char*>(pa);
+    const char* cb1 = reinterpret_cast<const char*>(pb1);
+    const char* cb2 = reinterpret_cast<const char*>(pb2);
+    const char* cw = reinterpret_cast<const char*>(pw);
+    const uint32_t sa8 = 8u * sa, sb18 = 8u * sb1, sb28 = 8u * sb2;
+#endif
     auto run = [&](uint32_t qm, auto with1, auto with2) {
         constexpr bool W1 = decltype(with1)::value, W2 = decltype(with2)::value;
         while (qm) {
             const int q = __ffs(qm) - 1;
             qm &= qm - 1;
             const int col = 4 * q;
+#if KBG_H_BYTEADDR
+            const uint32_t qo = static_cast<uint32_t>(q) << 5;
+            const double wv = *reinterpret_cast<const double*>(cw + qo);
+            double a[TM];
+#pragma unroll
+            for (int i = 0; i < TM; ++i) a[i] = *reinterpret_cast<const double*>(ca + i * 4096 + (qo ^ sa8)) * wv;
+#else
             const double wv = pw[col];
             double a[TM];
 #pragma unroll
             for (int i = 0; i < TM; ++i)
                 a[i] = pa[i * 512 + (col ^ sa)] * wv;
+#endif
             if (W1) {
                 double bb[TN1];
 #pragma unroll
-                for (int j = 0; j < TN1; ++j) bb[j] = pb1[j * 512 + (col ^ sb1)];
+                for (int j = 0; j < TN1; ++j)
+#if KBG_H_BYTEADDR
+                    bb[j] = *reinterpret_cast<const double*>(cb1 + j * 4096 + (qo ^ sb18));
+#else
+                    bb[j] = pb1[j * 512 + (col ^ sb1)];
+#endif
 #pragma unroll
                 for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -548,7 +576,12 @@ __device__ __forceinline__ void h_tile2(const Smem& sm, const double* __restrict
             if (W2) {
                 double bb[TN2];
 #pragma unroll
-                for (int j = 0; j < TN2; ++j) bb[j] = pb2[j * 512 + (col ^ sb2)];
+                for (int j = 0; j < TN2; ++j)
+#if KBG_H_BYTEADDR
+                    bb[j] = *reinterpret_cast<const double*>(cb2 + j * 4096 + (qo ^ sb28));
+#else
+                    bb[j] = pb2[j * 512 + (col ^ sb2)];
+#endif
 #pragma unroll
                 for (int i = 0; i < TM; ++i)
 #pragma unroll
