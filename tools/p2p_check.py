@@ -41,8 +41,9 @@ def main(cfg="cubic56_200Ry"):
     dist.all_gather_object(handles, gp.comm_handle())
     gp.comm_open(handles)
     st = torch.cuda.current_stream()
-    v = torch.from_numpy(f.veff()).to(dev)
-    h_p2p = torch.empty((1, ix["nnz"]), dtype=torch.float64, device=dev)
+    ns = int(os.environ.get("P2P_NSPIN", "1"))  # spin channels of the whole check
+    v = torch.from_numpy(f.veff(nspin=ns)).to(dev)
+    h_p2p = torch.empty((ns, ix["nnz"]), dtype=torch.float64, device=dev)
     h_nccl = torch.empty_like(h_p2p)
 
     def p2p():
@@ -91,9 +92,9 @@ def main(cfg="cubic56_200Ry"):
         return float(t.item())
 
     # host API on the sharded context: kbg_grid_pass returns the full H (fused reduction) on every rank
-    dm = f.dm(ix)
+    dm = f.dm(ix, nspin=ns)
     dm_p = torch.from_numpy(dm).pin_memory().numpy()
-    v_p = torch.from_numpy(f.veff()).pin_memory().numpy()
+    v_p = torch.from_numpy(f.veff(nspin=ns)).pin_memory().numpy()
     rho_g, h_g = gp.grid_pass(dm_p, v_p, f.dV)
     # shard-local host I/O (KBG_OPT_SHARD_IO): each rank returns its slice of H and its points of rho
     # (zeros elsewhere), so the sums over ranks are the full H and rho
@@ -161,19 +162,19 @@ def main(cfg="cubic56_200Ry"):
         full = GridPass(f.system, device=local)
         full.set_option(_abi.KBG_OPT_DETERMINISTIC, mode)
         full.build_index()
-        ref = full.hamiltonian(f.veff(), f.dV)[0]
-        h_np = h_p2p.cpu().numpy()[0]
+        ref = full.hamiltonian(f.veff(nspin=ns), f.dV)
+        h_np = h_p2p.cpu().numpy()
         d_full = float(np.abs(h_np - ref).max() / np.abs(ref).max())
         bitwise_single = bool(np.array_equal(h_np, ref))
-        rho_ref = full.density(dm)[0]
-        rho_sum = rho_t.cpu().numpy()[0]
+        rho_ref = full.density(dm)
+        rho_sum = rho_t.cpu().numpy()
         d_rho = float(np.abs(rho_sum - rho_ref).max() / np.abs(rho_ref).max())
         # the CPU oracle on the same inputs: the sharded H and the assembled rho (parity bar of
         # tests/test_gpu_parity.py: normwise 1e-10, per element 1e-10 where |ref| > 1e-8 max|ref|)
         o = Oracle(f.system)
         o.build_index()
-        h_or = o.hamiltonian(f.veff(), f.dV)[0]
-        rho_or = o.density(dm)[0]
+        h_or = o.hamiltonian(f.veff(nspin=ns), f.dV)
+        rho_or = o.density(dm)
 
         def errs(x, r):
             # the parity bar of tests/test_gpu_parity.py: normwise; per element above 1e-4 max|ref|;
@@ -187,7 +188,7 @@ def main(cfg="cubic56_200Ry"):
         h_norm, h_elem, h_small = errs(h_np, h_or)
         r_norm, r_elem, r_small = errs(rho_sum, rho_or)
         det = bool(repeat and bitwise_single)
-        print(json.dumps({"config": cfg, "world": world, "exchange_sms": xsms, "same_bits_all_ranks": same_bits, "repeatable": repeat,
+        print(json.dumps({"config": cfg, "world": world, "nspin": ns, "exchange_sms": xsms, "same_bits_all_ranks": same_bits, "repeatable": repeat,
                           "bitwise_equal_single_gpu": bitwise_single, "split_api_same_bits": split_same,
                           "rel_diff_vs_nccl": d_nccl, "rel_diff_vs_single_gpu": d_full,
                           "oracle_h_normwise": h_norm, "oracle_h_elementwise": h_elem,
