@@ -22,10 +22,12 @@ def _ngpus():
 
 @pytest.mark.gpu
 @pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
-def test_p2p_reduce_mirror_two_ranks(built):
+@pytest.mark.parametrize("nspin,xsms", [(1, 0), (2, 8)])
+def test_p2p_reduce_mirror_two_ranks(built, nspin, xsms):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", "29531", os.path.join(ROOT, "tools", "p2p_check.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+           "--master-addr", "127.0.0.1", "--master-port", str(29531 + nspin), os.path.join(ROOT, "tools", "p2p_check.py")]
+    env = dict(os.environ, P2P_NSPIN=str(nspin), P2P_XSMS=str(xsms))
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
     rec = json.loads(line)
