@@ -545,7 +545,6 @@ __device__ __forceinline__ void h_tile2(const Smem& sm, const double* __restrict
         while (qm) {
             const int q = __ffs(qm) - 1;
             qm &= qm - 1;
-            const int col = 4 * q;
 #if KBG_H_BYTEADDR
             const uint32_t qo = static_cast<uint32_t>(q) << 5;
             const double wv = *reinterpret_cast<const double*>(cw + qo);
@@ -553,6 +552,7 @@ __device__ __forceinline__ void h_tile2(const Smem& sm, const double* __restrict
 #pragma unroll
             for (int i = 0; i < TM; ++i) a[i] = *reinterpret_cast<const double*>(ca + i * 4096 + (qo ^ sa8)) * wv;
 #else
+            const int col = 4 * q;
             const double wv = pw[col];
             double a[TM];
 #pragma unroll

@@ -365,7 +365,6 @@ __global__ void k_bp_fill(SysParams P, int64_t nblock, const int32_t* __restrict
     for (int ci = c0; ci < c1; ++ci) {
         const uint64_t mi = cov_mask[ci];
         const int ai = cov_atom[ci];
-        const int na = P.sp[P.spc[ai]].norb;
         for (int cj0 = ci; cj0 < c1; cj0 += 32) {
             const int cj = cj0 + lane;
             uint64_t both = 0;
