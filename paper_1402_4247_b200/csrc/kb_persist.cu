@@ -1,11 +1,12 @@
-// Persistent, warp-specialized grid kernels (one CTA per SM, 16 warps).
+// Persistent, warp-specialized grid kernels (one CTA per SM; 1 producer warp +
+// kPersistConsumersR = 19 consumer warps for rho, + kPersistConsumersH = 27 for H).
 //
 // Warp 0 (producer) pulls grid blocks from a global work counter (blocks
-// ordered heaviest first), waits for a free shared-memory buffer (`empty`
+// ordered heaviest first, or in grid order for large grids: KBG_OPT_BLOCK_ORDER), waits for a free shared-memory buffer (`empty`
 // mbarrier) and stages the block with two TMA bulk copies from the geometry
 // cache (kb_cache.cu) -- the block's table image and its Phi rows -- which
 // complete on the buffer's `full` mbarrier (expect_tx). For H it also gathers
-// w = V dV of the block's 64 points. Warps 1..15 (consumers) wait on `full`,
+// w = V dV of the block's 64 points. The other warps (consumers) wait on `full`,
 // run their LPT-assigned tasks (DMMA contractions, kb_gridcore.cuh) and move
 // on to the next buffer without a CTA-wide barrier; the last consumer to
 // finish a block (shared counter) reduces the per-warp rho accumulators in a
