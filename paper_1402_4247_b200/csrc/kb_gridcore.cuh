@@ -769,10 +769,13 @@ __device__ __forceinline__ void gather_a(const Smem& sm, int ncov, const int (&r
 // outside the partner's overlap; 1 k-step-major, branching; 2 k-step-major over
 // all octets of the part (Phi is exactly 0 outside a cover's support, so the
 // extra products add exact zeros); 3 k-step-major with the DMMAs of octets
-// outside the overlap predicated off. With the octet mask made provably
-// warp-uniform (KBG_RHO_UNIFORM: a shuffle from lane 0), order 0 measures
-// 0.359 ms for the 56-atom density pass vs 0.370 (3), 0.372 (3 uniform),
-// 0.373 (0 without the shuffle) and 0.402 (2).
+// outside the overlap predicated off; 4 octet pairs, both-active pairs with
+// their DMMAs interleaved (4 accumulator chains in flight). With the octet mask
+// made provably warp-uniform (KBG_RHO_UNIFORM: a shuffle from lane 0), order 0
+// measures 0.359 ms for the 56-atom density pass vs 0.370 (3), 0.372 (3
+// uniform), 0.373 (0 without the shuffle) and 0.402 (2); on the final tree
+// 0.340 vs 0.379 (1) and 0.340 (4; 448 atoms 2.501 vs 2.510): the accumulator
+// chains are not what limits rho.
 #ifndef KBG_RHO_ORDER
 #define KBG_RHO_ORDER 0
 #endif
@@ -792,6 +795,36 @@ __device__ __forceinline__ void rho_partner(const double* __restrict__ pb, int s
             const double bv = pb[s * 256 + (col ^ swb)];
 #pragma unroll
             for (int t = 0; t < TM; ++t) dmma(y[t][o], a[t][s], bv);
+        }
+    }
+#elif KBG_RHO_ORDER == 4
+    // octet pairs: both active -> their DMMAs interleaved (4 accumulator chains in flight)
+#pragma unroll
+    for (int o = 0; o < kRhoOct; o += 2) {
+        const uint32_t pm = (om4 >> o) & 3u;
+        if (pm == 3u) {
+#pragma unroll
+            for (int s = 0; s < KS; ++s) {
+                const double b0 = pb[s * 256 + ((colbase + 8 * o) ^ swb)];
+                const double b1 = pb[s * 256 + ((colbase + 8 * o + 8) ^ swb)];
+#pragma unroll
+                for (int t = 0; t < TM; ++t) {
+                    dmma(y[t][o], a[t][s], b0);
+                    dmma(y[t][o + 1], a[t][s], b1);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {  // compile-time accumulator index (no local memory)
+                if (pm != (1u << e)) continue;
+                const int col = colbase + 8 * (o + e);
+#pragma unroll
+                for (int s = 0; s < KS; ++s) {
+                    const double bv = pb[s * 256 + (col ^ swb)];
+#pragma unroll
+                    for (int t = 0; t < TM; ++t) dmma(y[t][o + e], a[t][s], bv);
+                }
+            }
         }
     }
 #elif KBG_RHO_ORDER == 3
