@@ -364,8 +364,8 @@ constexpr int kPersistProducers = 1;
 #ifndef KBG_CONSUMERS_H
 #define KBG_CONSUMERS_H 27
 #endif
-constexpr int kPersistConsumersR = KBG_CONSUMERS_R;  // rho: 20 warps (<= 102 registers per thread)
-constexpr int kPersistConsumersH = KBG_CONSUMERS_H;  // H: 28 warps (<= 72 registers per thread)
+constexpr int kPersistConsumersR = KBG_CONSUMERS_R;  // rho: 20 warps with the producer (96 registers)
+constexpr int kPersistConsumersH = KBG_CONSUMERS_H;  // H: 28 warps with the producer (72 registers)
 // Geometry cache (kb_cache.cu): Phi and the per-block tables, built once per
 // geometry after the task lists.
 void build_cache_device(GridArgs gh, GridArgs gr, DevIndex& ix, cudaStream_t st);

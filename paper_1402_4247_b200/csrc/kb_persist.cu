@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(Cfg<DENSITY>::NT, 1) k_persist(GridArgs g) {
 // table images side by side, and the block's rho and H tasks come from one queue, interleaved, so
 // the warps of an SM run latency-bound rho tasks and pipe-bound H tasks at the same time. Buffer:
 // [H tables | rho tables | w (V dV) | rho per-task sums | Phi], two buffers. Non-deterministic
-// FP64-atomic H only; 20 consumer warps at the rho kernel's 96 registers.
+// FP64-atomic H only; the rho kernel's 19 consumer warps at 96 registers.
 struct FusedCfg {
     static constexpr int NC = kPersistConsumersR;
     static constexpr int NT = (kPersistProducers + NC) * 32;
