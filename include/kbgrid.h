@@ -179,9 +179,9 @@ int kbg_hamiltonian_accumulate_dev(kbg_ctx* ctx, int nspin, const double* d_veff
 int kbg_hamiltonian_mirror_dev(kbg_ctx* ctx, int nspin, double* d_h, void* stream);
 
 /* (new) One SCF grid pass on device buffers: rho and the mirrored H, on a single-rank context: density
- * then Hamiltonian, or with KBG_OPT_FUSED_PASS = 1 (FP64-atomic H, persistent kernels) ONE fused
+ * then Hamiltonian, or with KBG_OPT_FUSED_PASS (FP64-atomic H, persistent kernels) ONE fused
  * persistent kernel -- each block's Phi staged once, its rho and H tasks interleaved on the same SM
- * (56 atoms 1.4 % faster, 448 atoms 13 % slower: DESIGN.md). No host synchronisation. */
+ * (56 atoms 1.7 % faster, 448 atoms 13 % slower: DESIGN.md). No host synchronisation. */
 int kbg_grid_pass_dev(kbg_ctx* ctx, int nspin, const double* d_dm, const double* d_veff, double dV, double* d_rho,
                       double* d_h, void* stream);
 
@@ -248,7 +248,8 @@ int kbg_last_tally(const kbg_ctx* ctx, kbg_tally* out);
  * kbg_hamiltonian_exchange_dev on a second stream next to kbg_density_dev. 0: the exchange takes the
  * whole GPU before (kbg_grid_pass) or after (the split device API on one stream) the density pass. */
 #define KBG_OPT_EXCHANGE_SMS 12
-/* kbg_grid_pass_dev: 1 = one fused rho + H persistent kernel (see there), 0 (default) = separate kernels. */
+/* kbg_grid_pass_dev: 1 = one fused rho + H persistent kernel (see there), 0 = separate kernels,
+ * 2 (default) = fused while nspin x (repacked DM + H) <= 24 MB (the two share L2 without contention). */
 #define KBG_OPT_FUSED_PASS 13
 int kbg_set_option(kbg_ctx* ctx, int option, int64_t value);
 

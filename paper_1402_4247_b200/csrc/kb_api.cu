@@ -97,7 +97,7 @@ struct kbg_ctx {
     int shard_io = 1;
     int sparse_thr = 0;  // KBG_OPT_SPARSE_DFMA (0: every task on DMMA)
     int xsms = 8;        // KBG_OPT_EXCHANGE_SMS (0: exchange on the whole GPU, not overlapped)
-    int fused = 0;       // KBG_OPT_FUSED_PASS
+    int fused = 2;       // KBG_OPT_FUSED_PASS: 0 separate, 1 fused, 2 auto (fused while DM' + H fit kFusedAutoBytes)
     int pending_nspin = 0;  // kbg_hamiltonian_partial_dev done, exchange pending
     uint8_t* d_pown = nullptr;      // per pair: 1 if this rank's blocks touch it (kbg_comm_open)
     std::vector<int64_t> dm_runs;   // [off, len] pairs: DM ranges (per spin) covering the pairs the repack reads
@@ -674,6 +674,9 @@ int kbg_hamiltonian_accumulate_dev(kbg_ctx* c, int nspin, const double* d_veff, 
     });
 }
 
+// KBG_OPT_FUSED_PASS = 2 (auto): the fused pass while nspin * (repacked DM + H) stays below this
+constexpr double kFusedAutoBytes = 24.0 * (1 << 20);
+
 int kbg_grid_pass_dev(kbg_ctx* c, int nspin, const double* d_dm, const double* d_veff, double dV, double* d_rho,
                       double* d_h, void* stream) {
     if (!c || !d_dm || !d_veff || !d_rho || !d_h) return KBG_ERR_CONFIG;
@@ -684,7 +687,11 @@ int kbg_grid_pass_dev(kbg_ctx* c, int nspin, const double* d_dm, const double* d
         if (c->nranks > 1) throw Error(KBG_ERR_CONFIG, "grid_pass_dev: single-rank contexts only");
         const cudaStream_t st = static_cast<cudaStream_t>(stream);
         int n = 0;
-        const bool fused_ok = c->fused && c->persist_ok && c->persist && c->ix.phis && !c->det &&
+        // auto: the fused kernel wins while the repacked DM and the H accumulator share L2 without
+        // contention (56 atoms 0.649 vs 0.660 ms) and loses once they do not (448 atoms, 2 x 30 MB: 5.53 vs 4.89)
+        const double fused_bytes = 8.0 * nspin * static_cast<double>(c->ix.nrep + c->ix.nnz);
+        const bool fused_want = c->fused == 1 || (c->fused == 2 && fused_bytes <= kFusedAutoBytes);
+        const bool fused_ok = fused_want && c->persist_ok && c->persist && c->ix.phis && !c->det &&
                               c->sparse_thr == 0 && c->scatter == 0;
         kbg::GridArgs gh = grid_args(c, nspin, dV, d_veff, d_h, false);
         kbg::GridArgs gr = grid_args(c, nspin, 0.0, d_dm, d_rho, true);
@@ -2097,7 +2104,11 @@ int kbg_set_option(kbg_ctx* c, int option, int64_t value) {
             c->shard_io = value ? 1 : 0;
             return KBG_OK;
         case KBG_OPT_FUSED_PASS:
-            c->fused = value ? 1 : 0;
+            if (value < 0 || value > 2) {
+                c->err = "set_option: fused pass must be 0, 1 or 2";
+                return KBG_ERR_CONFIG;
+            }
+            c->fused = static_cast<int>(value);
             return KBG_OK;
         case KBG_OPT_EXCHANGE_SMS:
             if (value < 0 || value > 32) {

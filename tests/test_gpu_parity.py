@@ -379,10 +379,10 @@ def test_sparse_dfma_switch_parity(name, thr):
     assert_parity(h, c.o.hamiltonian(c.veff, c.f.dV))
 
 
-@pytest.mark.parametrize("fused,nspin", [(0, 1), (1, 1), (1, 2)])
+@pytest.mark.parametrize("fused,nspin", [(0, 1), (1, 1), (1, 2), (2, 1), (2, 2)])
 def test_grid_pass_dev_matches_separate_kernels(fused, nspin):
     """kbg_grid_pass_dev (separate kernels, or the fused rho + H persistent kernel with
-    KBG_OPT_FUSED_PASS): rho bitwise equal to kbg_density_dev, H equal to the mirrored H within the
+    KBG_OPT_FUSED_PASS = 1, or 2 = auto by L2 footprint, the default): rho bitwise equal to kbg_density_dev, H equal to the mirrored H within the
     FP64-atomic order difference."""
     import torch
 
@@ -400,7 +400,7 @@ def test_grid_pass_dev_matches_separate_kernels(fused, nspin):
         c.gp.grid_pass_dev(dm, v, c.f.dV, rho1, h1)
         torch.cuda.synchronize()
     finally:
-        c.gp.set_option(_abi.KBG_OPT_FUSED_PASS, 0)
+        c.gp.set_option(_abi.KBG_OPT_FUSED_PASS, 2)
     assert torch.equal(rho0, rho1)
     assert float((h1 - h0).abs().max() / h0.abs().max()) <= 1e-14
     assert_parity(h1.cpu().numpy(), c.o.hamiltonian(c.veff, c.f.dV))

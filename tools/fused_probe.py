@@ -1,5 +1,6 @@
 """Fused rho + H pass (kbg_grid_pass_dev) vs the separate kernels (density_dev, hamiltonian_accumulate_dev,
-hamiltonian_mirror_dev): time per pass (CUDA events, L2 flushed) and agreement.
+hamiltonian_mirror_dev): time per pass (CUDA events, L2 flushed) and agreement; "auto" = the default
+KBG_OPT_FUSED_PASS = 2 (fused below the L2 footprint threshold, separate kernels above).
 python tools/fused_probe.py [config ...]"""
 import json
 import os
@@ -37,10 +38,16 @@ def main(configs):
             gp.grid_pass_dev(dm, v, f.dV, rho[1], h[1], st)
 
         from paper_1402_4247_b200 import _abi
-        gp.set_option(_abi.KBG_OPT_FUSED_PASS, 1)
+
+        def mode(m, fn):
+            def run():
+                gp.set_option(_abi.KBG_OPT_FUSED_PASS, m)
+                fn()
+            return run
 
         res = {"config": cfg}
-        for name, fn in (("separate", separate), ("fused", fused), ("separate2", separate), ("fused2", fused)):
+        for name, fn in (("separate", separate), ("fused", mode(1, fused)), ("auto", mode(2, fused)),
+                         ("separate2", separate), ("fused2", mode(1, fused)), ("auto2", mode(2, fused))):
             for _ in range(3):
                 fn()
             ts = []
