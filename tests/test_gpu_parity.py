@@ -404,3 +404,12 @@ def test_grid_pass_dev_matches_separate_kernels(fused, nspin):
     assert torch.equal(rho0, rho1)
     assert float((h1 - h0).abs().max() / h0.abs().max()) <= 1e-14
     assert_parity(h1.cpu().numpy(), c.o.hamiltonian(c.veff, c.f.dV))
+
+
+@pytest.mark.parametrize("bad", [-1, 3])
+def test_fused_pass_option_range(bad):
+    """KBG_OPT_FUSED_PASS takes 0, 1 or 2 (auto); anything else is a configuration error."""
+    c = case("cubic56_200Ry", 1)
+    with pytest.raises(ConfigError):
+        c.gp.set_option(_abi.KBG_OPT_FUSED_PASS, bad)
+    c.gp.set_option(_abi.KBG_OPT_FUSED_PASS, 2)
